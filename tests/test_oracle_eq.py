@@ -1,0 +1,302 @@
+"""Pins of the oracle's equaliser, CPR, CFO, frame sync, decisions and counters (CPU only).
+
+SURVEY.md §8(c) pins: AWGN BER closed form, LMS identity / Wiener,
+CPR static rotation, stitching construction, CFO closed form, sync construction
+(S:539-541), Q<->BER, PRBS, end-to-end noiseless BER = 0.
+"""
+import math
+
+import numpy as np
+import pytest
+from scipy.linalg import solve_toeplitz, toeplitz
+
+from oracle import brute
+from oracle import rx_oracle as O
+from rxsynth import gen, make_config
+
+
+# ---------------------------------------------------------------- PRBS / Gray / reference
+
+def test_prbs15_three_independent_implementations_agree_and_have_prbs_properties():
+    a = O.prbs15(3 * 32767)
+    b = brute.prbs15_fibonacci(3 * 32767)
+    c = np.tile(gen.prbs_period_bits(), 3)
+    assert np.array_equal(a, b) and np.array_equal(a, c)
+    per = a[:32767]
+    assert np.array_equal(per, a[32767:65534])          # period 2^15 - 1
+    assert int(per.sum()) == 16384                     # 2^14 ones, 2^14 - 1 zeros
+    # run of 15 ones exactly once per period, no run of 15 zeros
+    s = "".join(map(str, np.concatenate([per, per[:20]])))
+    assert s[:32767 + 14].count("1" * 15) == 1 and "0" * 15 not in s
+
+
+def test_gray_adjacent_levels_differ_in_one_bit():
+    for M in (2, 4, 8, 16):
+        g = O.gray(np.arange(M))
+        assert sorted(g.tolist()) == list(range(M))
+        assert all(bin(int(g[i] ^ g[i + 1])).count("1") == 1 for i in range(M - 1))
+        assert np.array_equal(O.gray_decode(g), np.arange(M))
+
+
+def test_reference_matches_generator_transmit_sequence():
+    for fmt, M in (("pam", 4), ("pam", 16), ("qam", 16), ("qam", 64)):
+        _, idx, vals = O.reference(fmt, M)
+        assert np.array_equal(idx, gen.reference_level_indices(fmt, M))
+    _, _, v = O.reference("qam", 64)
+    assert abs(np.mean(np.abs(v) ** 2) - 1) < 2e-3     # ~unit power (PRBS is balanced)
+    assert abs(np.mean(np.abs(np.outer(O.qam_axis(64), 1) + 1j * O.qam_axis(64)[None, :]) ** 2) - 1) < 1e-12
+
+
+# ---------------------------------------------------------------- decisions / BER / Q
+
+@pytest.mark.parametrize("M", [2, 4, 8, 16])
+def test_pam_awgn_ber_matches_exact_q_sum(M):
+    """BER of the slicer on levels + AWGN equals the exact finite Q-sum within 3 sigma
+    binomial; PAM-2 reduces to Q(1/sigma)."""
+    rng = np.random.default_rng(M)
+    lv = O.pam_levels(M)
+    sigma = {2: 0.4, 4: 0.14, 8: 0.065, 16: 0.032}[M]
+    n = 400_000
+    i = rng.integers(0, M, size=n)
+    y = lv[i] + rng.normal(0, sigma, size=n)
+    sl = O._Slicer("pam", M)
+    d = sl.indices(y)
+    k = int(math.log2(M))
+    errs = int(np.sum(O.popcount(O.gray(d) ^ O.gray(i))))
+    ber = errs / (n * k)
+    exact = brute.pam_awgn_ber(lv, O.midpoints(lv), O.gray(np.arange(M)), sigma)
+    if M == 2:
+        assert abs(exact - brute.q_function(1 / sigma)) < 1e-15
+    sd = math.sqrt(exact * (1 - exact) / (n * k))
+    assert errs >= 100 and abs(ber - exact) < 3 * sd + 1e-12
+
+
+def test_threshold_ties_go_up_and_custom_thresholds():
+    sl = O._Slicer("pam", 4, thresholds=np.array([-0.5, 0.1, 0.5]))
+    assert sl.indices(np.array([-0.5, 0.1, 0.0999, 2.0, -9.0])).tolist() == [1, 2, 1, 3, 0]
+
+
+@pytest.mark.parametrize("M", [4, 16, 64])
+def test_qam_awgn_ber_per_axis_closed_form(M):
+    rng = np.random.default_rng(M)
+    L = int(math.sqrt(M))
+    ax = O.qam_axis(M)
+    sigma = {4: 0.35, 16: 0.11, 64: 0.05}[M]
+    n = 200_000
+    ii = rng.integers(0, L, size=(n, 2))
+    z = ax[ii[:, 0]] + 1j * ax[ii[:, 1]] + sigma * (rng.normal(size=n) + 1j * rng.normal(size=n))
+    sl = O._Slicer("qam", M)
+    d = sl.indices(z)
+    b = int(math.log2(L))
+    lab = (O.gray(d[:, 0]) << b) | O.gray(d[:, 1])
+    ref = (O.gray(ii[:, 0]) << b) | O.gray(ii[:, 1])
+    errs = int(np.sum(O.popcount(lab ^ ref)))
+    per_axis = brute.pam_awgn_ber(ax, O.midpoints(ax), O.gray(np.arange(L)), sigma)
+    exact = per_axis                    # both axes identical, bits split evenly
+    k = 2 * b
+    sd = math.sqrt(exact * (1 - exact) / (n * k))
+    assert errs >= 100 and abs(errs / (n * k) - exact) < 3 * sd
+
+
+def test_q_ber_mapping():
+    """Q 8.4 dB <-> 4.27e-3 (6.7% HD-FEC), 5.7 dB <-> 2.70e-2 (20%) via
+    BER = 1/2 erfc(Q / sqrt 2)."""
+    assert abs(O.q_from_ber(4.266e-3) - 8.4) < 2e-3
+    assert abs(O.q_from_ber(2.696e-2) - 5.7) < 2e-3
+    for q_db in (5.0, 8.4, 14.1):
+        ber = float(brute.q_function(10 ** (q_db / 20)))
+        assert abs(O.q_from_ber(ber) - q_db) < 1e-9
+
+
+# ---------------------------------------------------------------- LMS
+
+def test_lms_identity_channel_freezes_taps():
+    """(i) identity channel + centre spike -> e = 0, taps unchanged."""
+    rng = np.random.default_rng(0)
+    lv = O.pam_levels(4)
+    v = lv[rng.integers(0, 4, size=20000)]
+    lp = O.LmsParams(K=15, T_train=8192, mu=1e-2)
+    traj = []
+    w, _ = O.lms_train(v, 1, 0, v[100:100 + 8192], 100, lp, True, trajectory=traj)
+    spike = np.zeros(15); spike[7] = 1
+    assert np.array_equal(w, spike) and all(np.array_equal(t, spike) for t in traj)
+    sl = O._Slicer("pam", 4)
+    res, dv = O.lms_segments(v, 1, 0, v.shape[0], lambda s: spike, sl,
+                             O.LmsParams(K=15, S=4096), True, range(4))
+    assert not dv and all(np.array_equal(r["w"], spike) for r in res)
+
+
+def test_lms_training_converges_to_wiener_solution():
+    """(ii) known short FIR channel + AWGN: time-averaged taps -> w* = R^-1 p with
+    R = Toeplitz(h*h) + s^2 I and p the channel column at the decision delay."""
+    rng = np.random.default_rng(1)
+    h = np.array([0.1, 1.0, -0.3, 0.15])        # channel, cursor at index 1
+    K, n, s2 = 9, 600_000, 0.01
+    a = rng.choice(O.pam_levels(2), size=n)
+    v = np.convolve(a, h)[:n] + rng.normal(0, math.sqrt(s2), size=n)
+    # u_m[k] = v[m + c - k], c = 4; y_m = w.u_m estimates a_m: v_j = sum_i h_i a_{j-i}
+    c = K // 2
+    r = np.correlate(h, h, "full")[len(h) - 1:]
+    rcol = np.zeros(K); rcol[:len(r)] = r
+    R = toeplitz(rcol) + s2 * np.eye(K)
+    p = np.zeros(K)
+    for k in range(K):
+        i = c - k + 0                           # v_{m+c-k} contains a_m via h_{c-k}
+        if 0 <= i < len(h):
+            p[k] = h[i]
+    w_star = np.linalg.solve(R, p)
+    assert np.allclose(solve_toeplitz(rcol, p) if s2 == 0 else w_star, w_star)
+    lp = O.LmsParams(K=K, T_train=n - 1024, mu=2e-4 / 1)
+    traj = []
+    O.lms_train(v, 1, 0, a[16:16 + lp.T_train], 16, lp, True, trajectory=traj)
+    w_bar = np.mean(np.array(traj[len(traj) // 3:]), axis=0)
+    assert np.linalg.norm(w_bar - w_star) / np.linalg.norm(w_star) < 1e-2
+
+
+# ---------------------------------------------------------------- CPR / stitching
+
+def _qam_stream(M, n, rng):
+    L = int(math.sqrt(M))
+    ii = rng.integers(0, L, size=(n, 2))
+    ax = O.qam_axis(M)
+    return ax[ii[:, 0]] + 1j * ax[ii[:, 1]], ii
+
+
+@pytest.mark.parametrize("theta0", [0.0, 0.3, -0.7, 1.2, 2.9])
+def test_vv_cpr_recovers_static_rotation_mod_quarter_turn(theta0):
+    rng = np.random.default_rng(2)
+    s, _ = _qam_stream(4, 32 * 10, rng)
+    y = (s * np.exp(1j * theta0)).reshape(10, 32)
+    lp = O.LmsParams(K=1, cpr="vv")
+    th = O._cpr_estimate(y, np.ones_like(y, bool), O._Slicer("qam", 4), lp)
+    want = math.remainder(theta0, math.pi / 2)
+    assert np.allclose(np.exp(4j * th), np.exp(4j * want), atol=1e-12)
+    assert np.all(np.abs(th - want) < 1e-12) or np.all(np.abs(np.abs(th - want) - math.pi / 2) < 1e-12)
+
+
+@pytest.mark.parametrize("theta0", [0.05, -0.3, 0.61])
+def test_bps_cpr_resolves_within_quantisation(theta0):
+    rng = np.random.default_rng(3)
+    s, _ = _qam_stream(64, 32 * 8, rng)
+    y = (s * np.exp(1j * theta0)).reshape(8, 32)
+    P_t = 32
+    lp = O.LmsParams(K=1, cpr="bps", P_t=P_t)
+    th = O._cpr_estimate(y, np.ones_like(y, bool), O._Slicer("qam", 64), lp)
+    err = np.abs(np.remainder(th - theta0 + math.pi / 4, math.pi / 2) - math.pi / 4)
+    assert np.all(err <= math.pi / (4 * P_t) + 1e-3)
+
+
+def test_stitching_resolves_forced_segment_quadrants():
+    """Noiseless stream, every segment's seed forced into a random quadrant -> after
+    stitching (R_s prefix + R_0 anchor) the final decisions have zero errors."""
+    rng = np.random.default_rng(4)
+    M, n = 16, 40_000
+    _, idx_ref, vals_ref = O.reference("qam", M)
+    o, m0 = 123, 4096
+    m = np.arange(n)
+    sym = vals_ref[(o + m - m0) % O.P_REF]
+    z = np.zeros(2 * n, dtype=np.complex128)
+    z[0::2] = sym * np.exp(1j * 0.2)              # static phase, T/2 grid, h = 0
+    z[1::2] = 0.5 * (sym + np.roll(sym, -1)) * np.exp(1j * 0.2)
+    lp = O.LmsParams(K=4, S=4096, O=256, mu=1e-3, T_train=2048, E=1 << 20, cpr="bps", P_t=16)
+    sl = O._Slicer("qam", M)
+    rot = rng.integers(0, 4, size=64)
+    lm = O.lms_full(z, 2, 0, n, lambda mm: idx_ref[(o + mm - m0) % O.P_REF],
+                    lambda mm: vals_ref[(o + mm - m0) % O.P_REF], sl, lp, False, m0,
+                    seed_rotation=lambda s: rot[s])
+    # seed w j^r rotates y by j^-r, so the stitch must undo exactly r: R_s - r_s constant
+    assert len(set(((lm["R"] - rot[:len(lm["R"])]) % 4).tolist())) == 1
+    good = np.all(lm["idx"][64:] == idx_ref[(o + m[64:] - m0) % O.P_REF], axis=1)
+    assert np.all(good)
+
+
+# ---------------------------------------------------------------- CFO
+
+@pytest.mark.parametrize("df", [0.0, 5e6, -20e6, 20e6, 37.3e6])
+def test_cfo_estimate_closed_form(df):
+    """c-8: noiseless RRC(0.01) QAM at 2 sps with a frequency offset
+    -> |df^ - df| <= 0.1 MHz; the corrected stream has no residual rotation drift."""
+    rng = np.random.default_rng(5)
+    nsym = 1 << 17
+    s, _ = _qam_stream(16, nsym, rng)
+    up = np.zeros(2 * nsym, dtype=np.complex128)
+    up[::2] = s
+    f = np.fft.fftfreq(2 * nsym, d=0.5)
+    z = np.fft.ifft(np.fft.fft(up) * gen.rrc_amp(f, 0.01) ** 2)
+    q = np.arange(2 * nsym)
+    z = 3.0 * z * np.exp(2j * math.pi * df / 2e9 * q)
+    zc, info = O.kk_norm_cfo(z, 2e9, buffer_len=1 << 18)
+    assert np.all(np.abs(info["df"] - df) < 0.1e6)
+    assert abs(np.mean(np.abs(zc[: 1 << 18]) ** 2) - 1) < 1e-12
+    # after removal the 4th-power line sits at DC
+    blk = zc[:1 << 16].reshape(-1, 1024) ** 4
+    S = np.sum(np.abs(np.fft.fft(blk, axis=1)) ** 2, axis=0)
+    assert int(np.argmax(S)) in (0, 1, 1023)
+
+
+# ---------------------------------------------------------------- frame sync
+
+def test_frame_sync_finds_offset_polarity_rotation_and_matches_brute_force():
+    _, _, r = O.reference("pam", 4)
+    o, W = 1337, 2048
+    zeta = r[(o + np.arange(W)) % O.P_REF].astype(np.complex128)
+    res = O.frame_sync([zeta], r.astype(np.complex128))
+    assert res["offset"] == o and res["polarity"] == 0 and res["gamma"] > 0.999
+    res = O.frame_sync([-zeta], r.astype(np.complex128))
+    assert res["offset"] == o and res["polarity"] == 1
+    _, _, rq = O.reference("qam", 16)
+    zq = rq[(o + np.arange(W)) % O.P_REF] * np.exp(1j * 0.7)
+    res = O.frame_sync([np.roll(zq, 1), zq], rq)
+    assert (res["offset"], res["phase"]) == (o, 1) and abs(res["phi0"] - 0.7) < 1e-9
+    # brute force on a tiny reference
+    rng = np.random.default_rng(6)
+    P = 31
+    ref = rng.normal(size=P) + 1j * rng.normal(size=P)
+    z = rng.normal(size=9) + 1j * rng.normal(size=9)
+    g = []
+    for oo in range(P):
+        rr = ref[(oo + np.arange(9)) % P]
+        g.append(abs(np.sum(z * np.conj(rr))) / (np.linalg.norm(z) * np.linalg.norm(rr)))
+    res = O.frame_sync([z], ref, 0.0)
+    assert res["offset"] == int(np.argmax(g)) and abs(res["gamma"] - max(g)) < 1e-12
+
+
+# ---------------------------------------------------------------- end to end
+
+def _params(rec, rx):
+    return O.RxParams(fmt=rec.fmt, M=rec.M, static_taps=rec.static_taps,
+                      dc_offset=rec.dc_offset, **rx)
+
+
+@pytest.mark.parametrize("M", [2, 4, 8, 16])
+def test_end_to_end_noiseless_pam_is_error_free(M):
+    """noiseless, wide-band, offset-free -> BER = 0."""
+    rec = gen.pam_record(M, 1 << 17, seed=10 + M, snr_db=None, channel="b2b")
+    rx = dict(lms_taps=15, train_symbols=4096, warmup_symbols=256)
+    out = O.receive_pam(rec.codes, _params(rec, rx))
+    assert out["sync"]["offset"] == (rec.offset + 4096) % O.P_REF
+    assert out["bit_errors"] == 0 and out["symbols_counted"] > 60_000
+
+
+@pytest.mark.parametrize("M", [4, 16, 64])
+def test_end_to_end_noiseless_kk_is_error_free(M):
+    rec = gen.kk_record(M, 1 << 18, seed=20 + M, cspr_db=14.0, osnr_db=None)
+    # the Kaiser-windowed 203-tap matched filter leaves a ~-27 dB ISI floor that 8 T/2
+    # taps cannot remove for 64-QAM; 16 taps do
+    rx = dict(lms_taps=8 if M < 64 else 16, lms_overlap=256, mu=2e-3, train_symbols=8192,
+              warmup_symbols=512, cpr_test_phases=0 if M == 4 else 32)
+    out = O.receive_kk(rec.codes, _params(rec, rx))
+    assert out["sync"]["offset"] == (rec.offset + 4096) % O.P_REF
+    assert out["bit_errors"] == 0 and out["bits"] > 50_000
+
+
+def test_c1_ber_matches_closed_form():
+    """C1: PAM-2 at SNR_mf 9 dB -> BER = Q(sqrt(7.94)) = 2.41e-3; the adaptive 15-tap
+    equaliser adds a little misadjustment, so allow 3 sigma binomial + 25%."""
+    rec, rx = make_config("C1")
+    out = O.receive_pam(rec.codes, _params(rec, rx))
+    exact = float(brute.q_function(math.sqrt(10 ** 0.9)))
+    assert abs(exact - 2.41e-3) < 1e-5
+    n = out["bits"]
+    sd = math.sqrt(exact * n)
+    assert exact * n - 3 * sd <= out["bit_errors"] <= 1.25 * exact * n + 3 * sd
