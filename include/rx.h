@@ -1,0 +1,179 @@
+/*
+ * rx.h — C ABI of librx: the B200 (sm_100a) block-wise receiver DSP chain of
+ * van der Heide et al., "Field Trial of a Flexible Real-time Software-defined GPU-based
+ * Optical Receiver" (arXiv 2011.13695, JLT 2021).
+ *
+ * Citations: P:n = PAPER.md line n; S:n = SPEC.md line n; SURVEY §8(x) = the build's
+ * hot-path contract, whose step numbers H0..H25 / c-0..c-11 are used below.
+ *
+ * Shape of the API (BASELINE.json north_star): rx_create(format, baud, samples/symbol, taps,
+ * block/overlap sizes) -> rx_process(device sample buffer, stream) -> decided bits, error
+ * counts, EVM.  The paper's contract is the per-buffer hand-over of a filled GPU buffer to
+ * the control program with ordered carries between buffers.
+ *
+ * General rules
+ *  - C99, no C++ or torch types. All calls return rx_status (RX_OK = 0, errors < 0) unless
+ *    stated. Argument/config errors are returned synchronously (RX_EINVAL) and change nothing.
+ *  - Device pointers ("d_") must be device memory of the handle's CUDA device, 16-byte
+ *    aligned. Host pointers ("host_") are plain host memory. `cuda_stream` is a cudaStream_t
+ *    (NULL = legacy default stream).
+ *  - The caller owns every buffer it passes; it must stay valid until the work enqueued on
+ *    `cuda_stream` completes. The library owns all internal state (overlap halos, clock
+ *    history, DDS phase words, normalisation partials, LMS taps and epoch seeds, CPR /
+ *    stitch state, sync result, counters). A handle is not thread-safe; handles are
+ *    independent (one handle = one channel).
+ *  - rx_process / rx_flush are asynchronous and stream-ordered and never synchronise the host.
+ *    Data-dependent errors (domain, divergence, sync failure, label capacity) set sticky
+ *    device flags, reported by rx_get_stats() and returned by the next rx_process().
+ *  - There is no CPU fallback: every step of the chain runs in the library's CUDA kernels.
+ */
+#ifndef RX_H
+#define RX_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RX_OK = 0,
+  RX_EINVAL = -1,     /* bad argument or configuration */
+  RX_ENOMEM = -2,     /* device allocation failed */
+  RX_ECUDA = -3,      /* a CUDA runtime call failed (no device, launch failure, ...) */
+  RX_EDOMAIN = -4,    /* KK: I + dc <= 0 seen (counted, clamped to 1e-12) */
+  RX_ESYNC = -5,      /* frame-sync correlation below sync_min_corr */
+  RX_EDIVERGE = -6,   /* LMS tap norm > 1e3 */
+  RX_ECAPACITY = -7,  /* internal history ring overrun (call larger than configured) */
+  RX_ESTATE = -8      /* call order violated (e.g. rx_process after rx_flush) */
+} rx_status;
+
+typedef enum { RX_PAM = 0, RX_QAM_KK = 1 } rx_family;
+
+/* Status flag bits (rx_stats.status_flags) */
+#define RX_FLAG_DOMAIN   1
+#define RX_FLAG_SYNC     2
+#define RX_FLAG_DIVERGE  4
+#define RX_FLAG_CAPACITY 8
+
+typedef struct {
+  int family;                 /* rx_family. PAM: IMDD PAM-N chain;
+                                 RX_QAM_KK: Kramers-Kronig QAM-N chain */
+  int order;                  /* PAM 2/4/8/16, QAM 4/16/64 */
+  double baud;                /* symbols/s: 2e9 (PAM), 1e9 (KK) */
+  double sample_rate;         /* ADC rate, 4e9. sps = sample_rate/baud must be 2 (PAM)
+                                 or 4 (KK) */
+  int fft_size;               /* 1024; only 1024 is built */
+  int hop;                    /* 512 = fft_size/2: 100% overlap-save */
+  int buffer_blocks;          /* 8192 blocks = 2^22 samples per buffer; unit of the
+                                 normalisation, CFO and LMS epochs */
+  const double *static_taps;  /* host, copied. Zero-phase odd-length FIR, n <= hop+1, placed
+                                 centred. PAM: n real taps (503 in P:150).
+                                 KK: n complex taps interleaved re,im (203 in P:221) */
+  int n_static_taps;
+  double adc_gain;            /* x = (code - 2047.5)/2047.5 * adc_gain */
+  int clock_avg_half;         /* PAM: 52 -> 105-block clock-phase average */
+  const double *thresholds;   /* PAM: M-1 ascending decision thresholds (P:167 'optimized
+                                 offline'), host, copied; NULL = ideal midpoints */
+  double carrier_offset_hz;   /* KK: 0.547e9 */
+  int sideband;               /* KK: -1 = signal below the carrier (paper set-up) */
+  double dc_offset;           /* KK: static DC restoring the AC-coupled intensity, x units */
+  int lms_taps;               /* K: PAM T-spaced real taps (15/31), KK T/2-spaced complex (4..32) */
+  int lms_block;              /* B symbols per tap update: 32 (only 32 is built) */
+  int lms_segment;            /* S symbols per parallel segment: 4096; divides the epoch */
+  int lms_overlap;            /* O warm-up symbols per segment (KK 256, PAM 0); multiple of B */
+  int tap_lag_epochs;         /* D: seeds of epoch e are the mean canonical taps of e-D (8) */
+  int widely_linear;          /* reserved, must be 0 in this build (paper's WL DDLMS: next) */
+  double mu;                  /* block-sum LMS step (1e-3 PAM, 2e-3 KK) */
+  int train_symbols;          /* data-aided training symbols after sync (8192); multiple of B */
+  int cfo_enable;             /* KK: per-buffer 4th-power CFO estimate + removal (1) */
+  int cpr_test_phases;        /* KK: 0 = Viterbi-Viterbi (QAM-4), else BPS test phases (<= 64) */
+  unsigned prbs_order;        /* 15: PRBS x^15+x^14+1 reference (BER tester) */
+  unsigned prbs_seed;         /* 0x7FFF */
+  long long sync_start;       /* m0: first symbol of the sync window (4096); multiple of
+                                 lms_segment is not required */
+  int sync_window;            /* W_s symbols correlated (2048, <= 4096) */
+  double sync_min_corr;       /* Gamma threshold (0.3) */
+  long long warmup_symbols;   /* symbols below this index are not counted in BER/EVM */
+  int history_buffers;        /* device rings keep this many buffers of each intermediate
+                                 (>= 2; probes can read back only what is still held) */
+} rx_config;
+
+typedef struct rx_handle rx_handle;
+
+typedef struct {
+  long long samples_in;              /* samples accepted so far */
+  long long symbols_out;             /* symbols with final labels (absolute m < symbols_out) */
+  long long bit_errors, bits, symbols_counted;
+  long long clipped;                 /* codes equal to 0 or 4095 */
+  long long domain_errors, first_domain_error_index;   /* KK (A7); index -1 if none */
+  double evm_num, evm_den;           /* sum |d - z'|^2, sum |d|^2 (decision-referenced) */
+  int sync_offset, sync_phase, sync_polarity, synced;
+  double sync_gamma, sync_phi0;
+  int status_flags;                  /* RX_FLAG_* */
+  long long launches;                /* kernels this handle has launched so far */
+} rx_stats;
+
+/* Set *cfg to the defaults for (family, order): PAM 2 GBaud 2 sps / KK 1 GBaud 4 sps. */
+void rx_config_default(rx_config *cfg, int family, int order);
+
+/* Validate cfg, allocate all device state on `cuda_device`, precompute the static-EQ spectra,
+ * twiddles and PRBS reference tables. No allocation happens after this call. */
+rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle **out);
+
+/* Enqueue the chain on the next n_samples of the stream (u12 codes right-aligned in uint16,
+ * the ADC format of P:136 / S:602). n_samples must be a multiple of hop and at most
+ * buffer_blocks*hop. Samples are consumed in stream order (the overlap kernels are
+ * chained). Outputs lag the input (held-back tail: 52 blocks of clock look-ahead for PAM,
+ * one stage-2 block for KK, one buffer of normalisation, one LMS segment); everything that
+ * becomes final is processed. The label of absolute symbol m is written to
+ * d_labels[m % labels_capacity] (PAM: Gray label; QAM: Gray(i_I) << (k/2) | Gray(i_Q));
+ * labels_capacity 0 = no labels. */
+rx_status rx_process(rx_handle *h, const unsigned short *d_samples, long long n_samples,
+                     unsigned char *d_labels, long long labels_capacity, void *cuda_stream);
+
+/* End of stream: drain the tail with truncated windows (SURVEY c-3, A14) and finish every
+ * symbol. After rx_flush only rx_get_stats / rx_probe / rx_destroy are valid. */
+rx_status rx_flush(rx_handle *h, unsigned char *d_labels, long long labels_capacity,
+                   void *cuda_stream);
+
+/* Synchronise `cuda_stream`, copy a snapshot of the cumulative counters to host_out. */
+rx_status rx_get_stats(rx_handle *h, rx_stats *host_out, void *cuda_stream);
+
+/* Zero the BER/EVM/clip/domain counters (enqueued on cuda_stream). */
+rx_status rx_reset_stats(rx_handle *h, void *cuda_stream);
+
+/* Trained taps W_train (after sync + training): K values (PAM) or 2K interleaved (KK),
+ * host_out capacity in doubles. Synchronises the handle's last stream. */
+rx_status rx_get_taps(rx_handle *h, double *host_out, int capacity);
+
+/* Intermediate read-back for parity tests and tracing (synchronises `cuda_stream`).
+ * Copies `count` elements starting at absolute index `first` of intermediate `which`
+ * (still held in the device rings) to host_out. Returns RX_EINVAL if not held. */
+typedef enum {
+  RX_PROBE_C = 0,        /* PAM per block: C_b, complex double (re,im)          (H3) */
+  RX_PROBE_TAU = 1,      /* PAM per block: tau_b, double                        (H4) */
+  RX_PROBE_MB = 2,       /* PAM per block: M_b, int64                           (H4) */
+  RX_PROBE_U = 3,        /* PAM per symbol: u_m, float                          (H7) */
+  RX_PROBE_UHAT = 4,     /* PAM per symbol: normalised u_m, float               (H8) */
+  RX_PROBE_E = 5,        /* KK per 4-sps sample: field E_p, complex float       (H15) */
+  RX_PROBE_Z = 6,        /* KK per 2-sps sample: z_q, complex float             (H18) */
+  RX_PROBE_CFO = 7,      /* KK per buffer: {P, df_hz, kstar, inc, origin} 5 doubles (H19-20) */
+  RX_PROBE_Y = 8,        /* per symbol: equaliser output z'_m (after CPR), complex float
+                            (PAM: imag 0)                                       (H9/H21-22) */
+  RX_PROBE_LEVEL = 9,    /* per symbol: final level index (PAM i; QAM i_I | i_Q << 4), u8 */
+  RX_PROBE_SEG = 10,     /* per segment: {R_s, r_s, theta_final, errors, evm_num, evm_den}
+                            6 doubles                                           (H22) */
+  RX_PROBE_DEBUG = 11    /* internal state words (int64), for diagnostics only */
+} rx_probe;
+rx_status rx_probe_read(rx_handle *h, int which, long long first, long long count,
+                        void *host_out, void *cuda_stream);
+
+void rx_destroy(rx_handle *h);
+const char *rx_strerror(int status);
+
+/* Library build identification (e.g. "librx sm_100a <git>") */
+const char *rx_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RX_H */

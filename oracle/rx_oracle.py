@@ -323,10 +323,15 @@ def kk_norm_cfo(z: np.ndarray, fs2: float, buffer_len: int = 1 << 21, cfo_enable
       P = mean|z|^2; z <- z / sqrt(P)
       S[k] = sum over complete non-overlapping 1024-blocks of |DFT_1024(z^4)[k]|^2
       k* = argmax S (lowest on ties); delta = 1/2 (ln S- - ln S+)/(ln S- - 2 ln S0 + ln S+)
-      df = (kappa(k*) + delta) f_s2 / (4 * 1024)
+      df_c = (kappa(k*) + delta) f_s2 / (4 * 1024)                 (coarse)
+      fine stage (reading R-CFO): a_i = sum_{chunk i} (z_q e^{-j 2 pi df_c n/f_s2})^4,
+      n = q - q_lo; rho = sum_i a_{i+1} conj(a_i); df = df_c + arg(rho) f_s2 / (2 pi 4 1024)
       z_q <- z_q e^{-j psi'_q}: 64-bit DDS at df whose phase word is carried across buffers
 
-    A buffer without a complete 1024-block reuses the previous estimate (0 for buffer 0).
+    The log-parabolic interpolation alone is biased by up to ~0.2 bin (~100 kHz), enough
+    to defeat the training pass (no CPR, c-9); the phase-increment refinement removes it.
+    A buffer without a complete 1024-block reuses the previous estimate (0 for buffer 0);
+    with a single complete block the fine stage is skipped.
     """
     n = z.shape[0]
     nbuf = -(-n // buffer_len)
@@ -350,6 +355,12 @@ def kk_norm_cfo(z: np.ndarray, fs2: float, buffer_len: int = 1 << 21, cfo_enable
                 lm, l0, lp = math.log(Sm), math.log(S0), math.log(Sp)
                 delta = 0.5 * (lm - lp) / (lm - 2.0 * l0 + lp)
                 df = (float(kappa(kstar)) + delta) * fs2 / (4.0 * 1024.0)
+                if nch >= 2:
+                    n_ = np.arange(nch * 1024)
+                    zc4 = (zn[:nch * 1024] * np.exp(-2j * math.pi * df / fs2 * n_)) ** 4
+                    a = np.sum(zc4.reshape(nch, 1024), axis=1)
+                    rho = np.sum(a[1:] * np.conj(a[:-1]))
+                    df = df + math.atan2(rho.imag, rho.real) * fs2 / (2.0 * math.pi * 4.0 * 1024.0)
             inc = dds_increment(df, fs2)
             words = dds_words(np.arange(hi - lo), inc, origin)
             zn = zn * np.exp(-1j * dds_phase(words))
@@ -697,7 +708,11 @@ def lms_full(v, stride, off, m_end, ref_idx_fn, ref_val_fn, slicer: _Slicer, lp:
             if real:
                 canon[s] = r["w"]
             else:
-                canon[s] = r["w"] * np.exp(1j * r["theta"]) * (1j) ** (-int(R[s]))
+                # DESIGN.md reading R-SEED: remove the common (carrier) phase before the epoch
+                # average, phi_s = arg(sum_k w_k |w_k|); carrier phase noise decorrelates the
+                # absolute frame across an epoch, and CPR + stitching absorb the common phase.
+                w = r["w"]
+                canon[s] = w * np.exp(-1j * np.angle(np.sum(w * np.abs(w))))
         for e in range(wave, min(n_epoch, wave + lp.D)):
             lo, hi = e * seg_per_epoch, min(n_seg, (e + 1) * seg_per_epoch)
             seeds[e + lp.D] = np.mean(canon[lo:hi], axis=0)

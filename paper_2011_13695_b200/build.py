@@ -1,0 +1,48 @@
+"""Build librx.so in-tree for sm_100a (nvcc; no torch extension machinery needed: the
+boundary is a plain C ABI, include/rx.h)."""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+SO = os.path.join(HERE, "librx.so")
+SOURCES = ["csrc/rx_api.cu"]
+DEPS = ["csrc/rx_api.cu", "csrc/common.cuh", "csrc/fft.cuh", "csrc/rx_dev.cuh", "csrc/k_pam.cuh",
+        "csrc/k_kk.cuh", "csrc/k_lms.cuh", "../include/rx.h"]
+
+
+def _git_rev() -> str:
+    try:
+        return subprocess.check_output(["git", "-C", ROOT, "rev-parse", "--short", "HEAD"],
+                                       stderr=subprocess.DEVNULL, text=True).strip()
+    except Exception:
+        return "nogit"
+
+
+def needs_build() -> bool:
+    if not os.path.exists(SO):
+        return True
+    t = os.path.getmtime(SO)
+    return any(os.path.getmtime(os.path.join(HERE, p)) > t for p in DEPS)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not needs_build():
+        return SO
+    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+           "-shared", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include"),
+           f"-DRX_GIT=\"{_git_rev()}\"", "-o", SO + ".tmp"] + [os.path.join(HERE, s) for s in SOURCES]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True, cwd=HERE)
+    os.replace(SO + ".tmp", SO)
+    return SO
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -1,0 +1,120 @@
+// fft.cuh — shared-memory radix-8 Stockham FFT-512 and the real<->complex packing that
+// turns it into the 1024-point R2C/C2R transforms of the overlap-save stages
+// (P:150 '100% overlap-save 1024-point FFT', P:218 'real-to-complex FFT', P:221 '512-point
+// IFFT'). No cuFFT (north_star). One transform = 64 threads x 8 points, 3 radix-8 passes,
+// natural-order output (Stockham autosort). Unnormalised in both directions.
+#pragma once
+#include "common.cuh"
+
+#define FFT_PAD_N 576   // 512 float2 + one pad per 8 -> conflict-free 64-bit stores
+
+__device__ __forceinline__ int P8(int i) { return i + (i >> 3); }
+
+// Twiddles: tw[k] = e^{-2 pi i k / 1024}, k in [0, 1024), in shared memory.
+// W512^k = tw[2k].
+template <bool INV>
+__device__ __forceinline__ float2 tw1024(const float2 *tw, int k) {
+  float2 w = tw[k & 1023];
+  return INV ? make_float2(w.x, -w.y) : w;
+}
+
+template <bool INV>
+__device__ __forceinline__ void dft8(float2 (&v)[8]) {
+  const float r = 0.70710678118654752f;
+  // stage 1 (span 4): a_{4+r} = (v_r - v_{r+4}) W8^r
+  float2 a0 = cadd(v[0], v[4]), a4 = csub(v[0], v[4]);
+  float2 a1 = cadd(v[1], v[5]), a5 = csub(v[1], v[5]);
+  float2 a2 = cadd(v[2], v[6]), a6 = csub(v[2], v[6]);
+  float2 a3 = cadd(v[3], v[7]), a7 = csub(v[3], v[7]);
+  if (!INV) {
+    a5 = make_float2((a5.x + a5.y) * r, (a5.y - a5.x) * r);      // * (1 - i)/sqrt2
+    a6 = cmul_mi(a6);                                            // * -i
+    a7 = make_float2((a7.y - a7.x) * r, -(a7.x + a7.y) * r);     // * (-1 - i)/sqrt2
+  } else {
+    a5 = make_float2((a5.x - a5.y) * r, (a5.y + a5.x) * r);      // * (1 + i)/sqrt2
+    a6 = cmul_i(a6);
+    a7 = make_float2(-(a7.x + a7.y) * r, (a7.x - a7.y) * r);     // * (-1 + i)/sqrt2
+  }
+  // stage 2 (span 2)
+  float2 b0 = cadd(a0, a2), b2 = csub(a0, a2);
+  float2 b1 = cadd(a1, a3), b3 = csub(a1, a3);
+  float2 b4 = cadd(a4, a6), b6 = csub(a4, a6);
+  float2 b5 = cadd(a5, a7), b7 = csub(a5, a7);
+  if (!INV) { b3 = cmul_mi(b3); b7 = cmul_mi(b7); }
+  else { b3 = cmul_i(b3); b7 = cmul_i(b7); }
+  // stage 3 (span 1), outputs in natural order
+  v[0] = cadd(b0, b1); v[4] = csub(b0, b1);
+  v[2] = cadd(b2, b3); v[6] = csub(b2, b3);
+  v[1] = cadd(b4, b5); v[5] = csub(b4, b5);
+  v[3] = cadd(b6, b7); v[7] = csub(b6, b7);
+}
+
+// In-place FFT-512 of buf (padded, FFT_PAD_N float2) by the 64 threads j = 0..63 of a group.
+// All threads of the CTA must call it (it uses __syncthreads()).
+// On return thread j holds X[j + 64 r] in v[r] AND buf holds the result (if store).
+template <bool INV>
+__device__ __forceinline__ void fft512(float2 *buf, int j, const float2 *tw, float2 (&v)[8]) {
+  // pass 1: Ns = 1 (no twiddles)
+#pragma unroll
+  for (int r = 0; r < 8; ++r) v[r] = buf[P8(j + 64 * r)];
+  dft8<INV>(v);
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 8; ++r) buf[P8(8 * j + r)] = v[r];
+  __syncthreads();
+  // pass 2: Ns = 8, twiddle W512^(r k), k = j % 8
+  {
+    const int k = j & 7;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = buf[P8(j + 64 * r)];
+#pragma unroll
+    for (int r = 1; r < 8; ++r) v[r] = cmul(v[r], tw1024<INV>(tw, 16 * r * k));
+    dft8<INV>(v);
+    __syncthreads();
+    const int base = (j >> 3) * 64 + k;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) buf[P8(base + 8 * r)] = v[r];
+    __syncthreads();
+  }
+  // pass 3: Ns = 64, twiddle W512^(r j)
+#pragma unroll
+  for (int r = 0; r < 8; ++r) v[r] = buf[P8(j + 64 * r)];
+#pragma unroll
+  for (int r = 1; r < 8; ++r) v[r] = cmul(v[r], tw1024<INV>(tw, 2 * r * j));
+  dft8<INV>(v);
+  // result: v[r] = X[j + 64 r]
+}
+
+// Store the pass-3 result back (natural order) — only needed when other threads read it.
+__device__ __forceinline__ void fft512_store(float2 *buf, int j, const float2 (&v)[8]) {
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 8; ++r) buf[P8(j + 64 * r)] = v[r];
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------------------
+// Real 1024-point transforms through the packed 512-point complex FFT.
+// Forward: z[n] = x[2n] + i x[2n+1]; Z = FFT512(z);
+//   X[k] = Xe + W^k Xo, Xe = (Z[k] + conj Z[512-k])/2, Xo = -i (Z[k] - conj Z[512-k])/2,
+//   X[512-k] = conj(Xe - W^k Xo)   (W = e^{-2 pi i/1024}).
+// Thread j of a group owns the bin pairs (k, 512-k) for k = j + 64 r, r = 0..3; thread 0
+// additionally owns k = 256 (X[256] = conj Z[256]); k = 0 pairs with 512.
+__device__ __forceinline__ void r2c_pair(float2 Zk, float2 Zn, float2 w, float2 &Xk, float2 &Xn) {
+  float2 Xe = cscale(cadd(Zk, cconj(Zn)), 0.5f);
+  float2 Xo = cscale(cmul_mi(csub(Zk, cconj(Zn))), 0.5f);
+  float2 t = cmul(w, Xo);
+  Xk = cadd(Xe, t);
+  Xn = cconj(csub(Xe, t));
+}
+// Inverse packing: given Hermitian half-spectrum pair (Y[k], Y[512-k]) produce Z[k], Z[512-k]
+// such that IFFT512(Z)[n] = (y[2n] + i y[2n+1]) * 512 / 1024 * 2 ... i.e. y = IFFT1024(Y)
+// satisfies y[2n] + i y[2n+1] = IFFT512(Z)[n] / 512 (unnormalised IFFT512 used).
+//   Xe = (Y[k] + conj Y[512-k])/2, Xo = (Y[k] - conj Y[512-k])/2 * conj(W^k)
+//   Z[k] = Xe + i Xo, Z[512-k] = conj(Xe) + i conj(Xo)
+__device__ __forceinline__ void c2r_pair(float2 Yk, float2 Yn, float2 w, float2 &Zk, float2 &Zn) {
+  float2 Xe = cscale(cadd(Yk, cconj(Yn)), 0.5f);
+  float2 Xo = cscale(cmulc(csub(Yk, cconj(Yn)), w), 0.5f);
+  Zk = cadd(Xe, cmul_i(Xo));
+  Zn = cadd(cconj(Xe), cmul_i(cconj(Xo)));
+}

@@ -1,0 +1,630 @@
+// k_lms.cuh — frame sync, segmented block-LMS equaliser with in-loop CPR, quadrant
+// stitching, decisions, Gray labels and BER/EVM counters (c-9..c-11).
+//
+// The paper's KK equaliser is a serial 4-tap widely-linear DDLMS using warp shuffles
+// and its PAM decision uses offline thresholds. The build's equaliser is
+// the segment-parallel block-LMS of SURVEY c-9: one warp owns one segment of S symbols,
+// lane i owns symbol i of each B = 32 block, lane k owns tap k; CPR and decisions are fused.
+#pragma once
+#include "k_kk.cuh"
+
+#define LMS_WMAX 128   // window: stride*(B-1) + K <= 2*31 + 32 = 94
+
+template <bool CPLX>
+__device__ __forceinline__ float2 lms_in(const RxDev &d, long long i, long long vend) {
+  if (CPLX) return kk_zprime(d, i, vend);
+  if (i < 0 || i >= vend) return make_float2(0.f, 0.f);
+  return make_float2(d.uhat[rmod(i, d.sym_cap)], 0.f);
+}
+
+// level index per axis: #{thresholds <= v} (c-11; ties go up)
+__device__ __forceinline__ int slice_pam(const RxDev &d, float v) {
+  int i = 0;
+  for (int t = 0; t < d.M - 1; ++t) i += (__ldg(d.thr + t) <= v);
+  return i;
+}
+__device__ __forceinline__ int slice_axis(float v, float inv2s, int L) {
+  int i = (int)floorf(fmaf(v, inv2s, 0.5f * (float)L));
+  return i < 0 ? 0 : (i > L - 1 ? L - 1 : i);
+}
+
+// rotate a QAM level pair by j^r: j (aI + j aQ) = -aQ + j aI -> (L-1-iQ, iI)
+__device__ __forceinline__ int qam_rot(int code, int r, int L) {
+  int iI = code & 15, iQ = code >> 4;
+  for (int t = 0; t < (r & 3); ++t) { int nI = L - 1 - iQ; iQ = iI; iI = nI; }
+  return iI | (iQ << 4);
+}
+__device__ __forceinline__ int gray(int i) { return i ^ (i >> 1); }
+
+__device__ __forceinline__ long long seg_end_of(const RxDev &d, long long s) {
+  long long hi = (s + 1) * (long long)d.S;
+  const long long me = d.st->m_end;
+  if (me >= 0 && hi > me) hi = me;
+  return hi;
+}
+
+// ------------------------------------------------------------------ H24 frame sync
+// Gamma(o,h) = |sum_i zeta_{m0+i,h} conj(r_{(o+i) mod P})| / (||zeta_h|| ||r_window||) (c-10)
+template <bool CPLX>
+__device__ __forceinline__ bool sync_ready(const RxDev &d) {
+  const long long need = CPLX ? 2 * (d.m0 + d.W_sync) + 2 : d.m0 + d.W_sync;
+  return d.st->v_front >= need;
+}
+
+template <bool CPLX>
+__global__ void __launch_bounds__(256) k_sync_corr(RxDev d) {
+  extern __shared__ float2 zeta[];   // [nh][W]
+  if (d.st->synced || !sync_ready<CPLX>(d)) return;
+  const int nh = CPLX ? 2 : 1, W = d.W_sync;
+  const long long vend = d.st->v_front;
+  for (int i = threadIdx.x; i < nh * W; i += blockDim.x) {
+    const int h = i / W, k = i % W;
+    zeta[i] = CPLX ? lms_in<true>(d, 2 * (d.m0 + k) + h, vend) : lms_in<false>(d, d.m0 + k, vend);
+  }
+  __syncthreads();
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= nh * RX_PREF) return;
+  const int h = gid / RX_PREF, o = gid % RX_PREF;
+  float ar = 0.f, ai = 0.f, rn = 0.f;
+  int idx = o;
+  for (int i = 0; i < W; ++i) {
+    const float2 r = __ldg(d.ref_val + idx);
+    const float2 zz = zeta[h * W + i];
+    ar = fmaf(zz.x, r.x, fmaf(zz.y, r.y, ar));
+    ai = fmaf(zz.y, r.x, fmaf(-zz.x, r.y, ai));
+    rn = fmaf(r.x, r.x, fmaf(r.y, r.y, rn));
+    if (++idx == RX_PREF) idx = 0;
+  }
+  d.sync_c[gid] = make_float2(ar, ai);
+  d.sync_g[gid] = sqrtf(ar * ar + ai * ai) * rsqrtf(fmaxf(rn, 1e-30f));
+}
+
+template <bool CPLX>
+__global__ void __launch_bounds__(1024) k_sync_pick(RxDev d, int flush) {
+  __shared__ double zn[2];
+  __shared__ float bv[32];
+  __shared__ int bi[32];
+  DevState *st = d.st;
+  if (st->synced) return;
+  if (!sync_ready<CPLX>(d)) {
+    if (flush && threadIdx.x == 0) set_flag(st, RX_FLAG_SYNC_DEV);
+    return;
+  }
+  const int nh = CPLX ? 2 : 1, W = d.W_sync;
+  const long long vend = st->v_front;
+  for (int h = 0; h < nh; ++h) {
+    double s = 0.0;
+    for (int k = threadIdx.x; k < W; k += blockDim.x) {
+      const float2 zz = CPLX ? lms_in<true>(d, 2 * (d.m0 + k) + h, vend) : lms_in<false>(d, d.m0 + k, vend);
+      s += (double)cabs2(zz);
+    }
+    s = warp_sum_d(s);
+    __shared__ double wsum[32];
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < 32; ++w) t += wsum[w];
+      zn[h] = sqrt(t);
+    }
+    __syncthreads();
+  }
+  // argmax in (h, o) order, lowest on ties (as the oracle scans h outer, o inner)
+  float best = -1.f;
+  int bidx = 0x7fffffff;
+  for (int gid = threadIdx.x; gid < nh * RX_PREF; gid += blockDim.x) {
+    const int h = gid / RX_PREF;
+    const float g = d.sync_g[gid] / (float)fmax(zn[h], 1e-30);
+    if (g > best || (g == best && gid < bidx)) { best = g; bidx = gid; }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+    if (ob > best || (ob == best && oi < bidx)) { best = ob; bidx = oi; }
+  }
+  if ((threadIdx.x & 31) == 0) { bv[threadIdx.x >> 5] = best; bi[threadIdx.x >> 5] = bidx; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 32; ++w)
+      if (bv[w] > bv[0] || (bv[w] == bv[0] && bi[w] < bi[0])) { bv[0] = bv[w]; bi[0] = bi[w]; }
+    const int gid = bi[0];
+    const float2 c = d.sync_c[gid];
+    st->sync_offset = gid % RX_PREF;
+    st->sync_phase = gid / RX_PREF;
+    st->sync_gamma = bv[0];
+    st->sync_phi0 = atan2((double)c.y, (double)c.x);
+    st->sync_polarity = c.x < 0.f;
+    if (bv[0] < d.sync_min) set_flag(st, RX_FLAG_SYNC_DEV);
+    __threadfence();
+    st->synced = 1;
+    d.hm->synced = 1;
+  }
+}
+
+// ------------------------------------------------------------------ H9/H21 LMS core
+// One warp runs block-LMS over symbols [t_begin, t_end) starting from tap wk (lane k).
+// MODE 0: training (e = r - y, no CPR), MODE 1: decision directed with CPR `CPR`
+// (0 none, 1 VV, 2 BPS). Outputs for m >= out_lo go to the level / yout rings,
+// warm-up decisions (m < out_lo) to warm[]. Returns final theta; accumulates EVM.
+struct LmsSmem {
+  float2 win[2][LMS_WMAX];
+  float2 w[RX_MAX_K];
+  float2 e[32];
+  float dist[RX_MAX_PT][33];
+};
+
+template <bool CPLX, int CPR, int MODE>
+__device__ float lms_run(const RxDev &d, LmsSmem &sm, long long t_begin, long long t_end,
+                         long long out_lo, float2 &wk, unsigned char *warm, double &evn,
+                         double &evd, long long vend) {
+  const int lane = threadIdx.x & 31;
+  const int K = d.K, c = K >> 1;
+  const int stride = CPLX ? 2 : 1;
+  const int off = CPLX ? d.st->sync_phase : 0;
+  const int WL = stride * 31 + K;
+  const float mu = d.mu;
+  const float sc = CPLX ? 0.5f * (__ldg(d.lvl + 1) - __ldg(d.lvl + 0)) : 0.f;   // half spacing
+  const float inv2sc = CPLX ? 1.0f / (2.0f * sc) : 0.f;
+  const long long o_ref = d.st->sync_offset;
+  float theta = 0.f;
+  if (lane < K) sm.w[lane] = wk;
+  // initial window
+  long long wb = (long long)stride * t_begin + off + c - (K - 1);
+  for (int x = lane; x < WL; x += 32) sm.win[0][x] = lms_in<CPLX>(d, wb + x, vend);
+  __syncwarp();
+  int buf = 0;
+  bool first = true;
+  for (long long t = t_begin; t < t_end; t += 32) {
+    // prefetch the next window into registers
+    float2 pre[3];
+    const long long wbn = wb + (long long)stride * 32;
+    const bool more = t + 32 < t_end;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int x = lane + 32 * q;
+      pre[q] = (more && x < WL) ? lms_in<CPLX>(d, wbn + x, vend) : make_float2(0.f, 0.f);
+    }
+    const float2 *cur = sm.win[buf];
+    // y_i = w^H u_i, u_i[k] = win[stride i + K-1-k]
+    float2 y = make_float2(0.f, 0.f);
+    for (int k = 0; k < K; ++k) {
+      const float2 u = cur[stride * lane + K - 1 - k];
+      const float2 w = sm.w[k];
+      // conj(w) u
+      y.x = fmaf(w.x, u.x, fmaf(w.y, u.y, y.x));
+      if (CPLX) y.y = fmaf(w.x, u.y, fmaf(-w.y, u.x, y.y));
+    }
+    const long long m = t + lane;
+    const bool valid = m < t_end;
+    float2 e, zp = y;
+    int code = 0;
+    if (MODE == 0) {
+      const long long ri = ((o_ref + m - d.m0) % RX_PREF + RX_PREF) % RX_PREF;
+      const float2 r = __ldg(d.ref_val + ri);
+      e = CPLX ? csub(r, y) : make_float2(r.x - y.x, 0.f);
+    } else {
+      float cth = 1.f, sth = 0.f;
+      if (CPLX && CPR != 0) {
+        float th_hat;
+        if (CPR == 1) {   // Viterbi-Viterbi: 1/4 arg(-sum y^4)
+          float2 y2 = cmul(y, y), y4 = cmul(y2, y2);
+          if (!valid) y4 = make_float2(0.f, 0.f);
+          const float sx = warp_sum(y4.x), sy = warp_sum(y4.y);
+          th_hat = 0.25f * atan2f(-sy, -sx);
+        } else {           // blind phase search over Pt test phases
+          const int Pt = d.Pt;
+          for (int p = 0; p < Pt; ++p) {
+            const float2 zr = cmul(y, __ldg(d.bps_rot + p));
+            const int iI = slice_axis(zr.x, inv2sc, d.L), iQ = slice_axis(zr.y, inv2sc, d.L);
+            const float dx = zr.x - __ldg(d.lvl + iI), dy = zr.y - __ldg(d.lvl + iQ);
+            sm.dist[p][lane] = valid ? fmaf(dx, dx, dy * dy) : 0.f;
+          }
+          __syncwarp();
+          float bd = 3.4e38f;
+          int bp = 0x7fffffff;
+          for (int p = lane; p < Pt; p += 32) {
+            float s = 0.f;
+            for (int i = 0; i < 32; ++i) s += sm.dist[p][i];
+            if (s < bd) { bd = s; bp = p; }
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const float ob = __shfl_xor_sync(0xffffffffu, bd, o);
+            const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+            if (ob < bd || (ob == bd && op < bp)) { bd = ob; bp = op; }
+          }
+          th_hat = -0.78539816339744831f + ((float)bp + 0.5f) * (1.5707963267948966f / (float)Pt);
+          __syncwarp();
+        }
+        if (first) theta = th_hat;
+        else theta = th_hat + 1.5707963267948966f * rintf((theta - th_hat) * 0.63661977236758134f);
+        sincosf(theta, &sth, &cth);
+        zp = cmul(y, make_float2(cth, -sth));
+      }
+      float2 dv;
+      if (CPLX) {
+        const int iI = slice_axis(zp.x, inv2sc, d.L), iQ = slice_axis(zp.y, inv2sc, d.L);
+        code = iI | (iQ << 4);
+        dv = make_float2(__ldg(d.lvl + iI), __ldg(d.lvl + iQ));
+        e = cmul(csub(dv, zp), make_float2(cth, sth));
+      } else {
+        const int i = slice_pam(d, zp.x);
+        code = i;
+        dv = make_float2(__ldg(d.lvl + i), 0.f);
+        e = make_float2(dv.x - zp.x, 0.f);
+      }
+      if (valid && m >= out_lo) {
+        d.level[rmod(m, d.sym_cap)] = (unsigned char)code;
+        d.yout[rmod(m, d.sym_cap)] = zp;
+        if (m >= d.warmup) {
+          const float ex = dv.x - zp.x, ey = dv.y - zp.y;
+          evn += (double)fmaf(ex, ex, ey * ey);
+          evd += (double)fmaf(dv.x, dv.x, dv.y * dv.y);
+        }
+      } else if (valid && warm) {
+        warm[m - (out_lo - d.O)] = (unsigned char)code;
+      }
+    }
+    sm.e[lane] = valid ? e : make_float2(0.f, 0.f);
+    __syncwarp();
+    // gradient: lane k: g_k = sum_i u_i[k] conj(e_i); w <- w + mu g  (c-9 step 7)
+    if (lane < K) {
+      float gx = 0.f, gy = 0.f;
+      for (int i = 0; i < 32; ++i) {
+        const float2 u = cur[stride * i + K - 1 - lane];
+        const float2 ee = sm.e[i];
+        gx = fmaf(u.x, ee.x, fmaf(u.y, ee.y, gx));
+        if (CPLX) gy = fmaf(u.y, ee.x, fmaf(-u.x, ee.y, gy));
+      }
+      wk.x = fmaf(mu, gx, wk.x);
+      if (CPLX) wk.y = fmaf(mu, gy, wk.y);
+    }
+    // divergence check
+    const float nrm = warp_sum(lane < K ? cabs2(wk) : 0.f);
+    if (lane == 0 && nrm > 1e6f) set_flag(d.st, RX_FLAG_DIVERGE);
+    __syncwarp();
+    if (lane < K) sm.w[lane] = wk;
+    float2 *nxt = sm.win[buf ^ 1];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int x = lane + 32 * q;
+      if (x < WL) nxt[x] = pre[q];
+    }
+    __syncwarp();
+    buf ^= 1;
+    wb = wbn;
+    first = false;
+  }
+  return theta;
+}
+
+// ------------------------------------------------------------------ training (1 warp)
+template <bool CPLX>
+__global__ void __launch_bounds__(32) k_lms_train(RxDev d, int flush) {
+  __shared__ LmsSmem sm;
+  DevState *st = d.st;
+  if (!st->synced || st->trained) return;
+  const int lane = threadIdx.x;
+  const int K = d.K, c = K >> 1, stride = CPLX ? 2 : 1;
+  const long long vend = st->v_front;
+  const long long last = (long long)stride * (d.m0 + d.T_train - 1) + (CPLX ? st->sync_phase : 0) + c;
+  if (last >= vend && !flush) return;
+  float2 wk = make_float2(lane == c ? 1.f : 0.f, 0.f);    // centre spike
+  double en = 0.0, ed = 0.0;
+  lms_run<CPLX, 0, 0>(d, sm, d.m0, d.m0 + d.T_train, 0, wk, nullptr, en, ed, vend);
+  if (lane < K) d.w_train[lane] = wk;
+  __threadfence();
+  if (lane == 0) { st->trained = 1; d.hm->trained = 1; }
+}
+
+// ------------------------------------------------------------------ segments (1 warp each)
+// Segment s outputs [sS, min((s+1)S, m_end)), recursion starts O symbols early (c-9).
+template <bool CPLX, int CPR>
+__global__ void __launch_bounds__(128) k_lms_seg(RxDev d, int flush, int nseg) {
+  __shared__ LmsSmem sm[4];
+  DevState *st = d.st;
+  if (!st->trained) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long s = st->seg_next + (long long)blockIdx.x * 4 + warp;
+  if (blockIdx.x * 4 + warp >= nseg) return;
+  if (d.seg_done[rmod(s, d.seg_cap)] == s + 1) return;
+  const long long S = d.S;
+  const long long lo = s * S;
+  const long long me = st->m_end;
+  if (me >= 0 && lo >= me) return;
+  const long long hi = seg_end_of(d, s);
+  const int K = d.K, c = K >> 1, stride = CPLX ? 2 : 1;
+  const long long vend = st->v_front;
+  if (me < 0) {   // streaming: all taps of the last symbol must be available
+    const long long lastidx = (long long)stride * (hi - 1) + (CPLX ? st->sync_phase : 0) + c;
+    if (lastidx >= vend) return;
+  }
+  // seed: W_train for e < D, else the mean canonical taps of epoch e - D (c-9 'Seed')
+  const long long e = lo / d.E_sym;
+  float2 wk = make_float2(0.f, 0.f);
+  if (e < d.D) {
+    if (lane < K) wk = d.w_train[lane];
+  } else {
+    if (d.seed_ready[rmod(e, d.seed_cap)] != e + 1) return;
+    if (lane < K) wk = d.seed[rmod(e, d.seed_cap) * RX_MAX_K + lane];
+  }
+  long long t0 = lo - d.O;
+  if (t0 < 0) t0 = 0;
+  double en = 0.0, ed = 0.0;
+  unsigned char *warm = d.O > 0 ? d.seg_warm + rmod(s, d.seg_cap) * d.O : nullptr;
+  const float th = lms_run<CPLX, CPR, 1>(d, sm[warp], t0, hi, lo, wk, warm, en, ed, vend);
+  en = warp_sum_d(en);
+  ed = warp_sum_d(ed);
+  const long long si = rmod(s, d.seg_cap);
+  if (lane < K) d.seg_w[si * RX_MAX_K + lane] = wk;
+  if (lane == 0) {
+    d.seg_theta[si] = th;
+    d.seg_evm[2 * si] = en;
+    d.seg_evm[2 * si + 1] = ed;
+    __threadfence();
+    d.seg_done[si] = (int)(s + 1);
+  }
+}
+
+// ------------------------------------------------------------------ H22 stitching
+// r_s = argmax_r #{m in warm-up overlap : d^(s) j^r = d^(s-1)}, lowest r on ties (c-9)
+__global__ void __launch_bounds__(256) k_lms_stitch(RxDev d, int nseg) {
+  __shared__ int cnt[4];
+  const long long s = d.st->seg_next + blockIdx.x;
+  if (blockIdx.x >= nseg) return;
+  const long long si = rmod(s, d.seg_cap);
+  if (d.seg_done[si] != s + 1 || d.seg_stitched[si] == s + 1) return;
+  if (s > 0 && d.seg_done[rmod(s - 1, d.seg_cap)] != s) return;
+  if (threadIdx.x < 4) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const bool doit = (d.family == 1) && d.O > 0 && s > 0;
+  if (doit) {
+    int c4[4] = {0, 0, 0, 0};
+    const long long base = s * (long long)d.S - d.O;
+    for (int x = threadIdx.x; x < d.O; x += blockDim.x) {
+      const int cur = d.seg_warm[si * d.O + x];
+      const int prev = d.level[rmod(base + x, d.sym_cap)];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) c4[r] += (qam_rot(cur, r, d.L) == prev);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int v = __reduce_add_sync(0xffffffffu, c4[r]);
+      if ((threadIdx.x & 31) == 0) atomicAdd(&cnt[r], v);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int best = 0;
+    for (int r = 1; r < 4; ++r) if (cnt[r] > cnt[best]) best = r;
+    d.seg_r[si] = doit ? best : 0;
+    __threadfence();
+    d.seg_stitched[si] = (int)(s + 1);
+  }
+}
+
+// ------------------------------------------------------------------ R_s prefix + anchor
+// R_s = (A + sum_{i<=s} r_i) mod 4 with A fixed by anchoring the segment containing m0 to
+// the known reference over [m0, m0 + 256) (c-9 'Stitching').
+__global__ void __launch_bounds__(1024) k_lms_prefix(RxDev d, int flush, int maxn) {
+  __shared__ int firstbad;
+  __shared__ int pre[1024];
+  __shared__ int acnt[4];
+  DevState *st = d.st;
+  const long long base = st->seg_next;
+  const int t = threadIdx.x;
+  if (t == 0) firstbad = maxn;
+  if (t < 4) acnt[t] = 0;
+  __syncthreads();
+  for (int i = t; i < maxn; i += blockDim.x) {
+    const long long s = base + i;
+    if (d.seg_stitched[rmod(s, d.seg_cap)] != s + 1) atomicMin(&firstbad, i);
+  }
+  __syncthreads();
+  int n = firstbad;
+  // anchor
+  const long long s0 = d.m0 / d.S;
+  __shared__ int A_sh, known_sh;
+  if (t == 0) { A_sh = st->anchor_A; known_sh = st->anchor_known; }
+  __syncthreads();
+  if (!known_sh) {
+    const long long me = st->m_end;
+    const bool s0_exists = !(me >= 0 && s0 * (long long)d.S >= me);
+    if (d.family == 0) {
+      if (t == 0) { A_sh = 0; known_sh = 1; }
+    } else if (!s0_exists) {
+      if (t == 0) { A_sh = 0; known_sh = 1; }
+    } else if (s0 < base + n) {
+      const long long hi0 = seg_end_of(d, s0);
+      long long mend = d.m0 + 256;
+      if (mend > hi0) mend = hi0;
+      int c4[4] = {0, 0, 0, 0};
+      for (long long m = d.m0 + t; m < mend; m += blockDim.x) {
+        const int cur = d.level[rmod(m, d.sym_cap)];
+        const long long ri = ((st->sync_offset + m - d.m0) % RX_PREF + RX_PREF) % RX_PREF;
+        const int ref = d.ref_idx[ri];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) c4[r] += (qam_rot(cur, r, d.L) == ref);
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int v = __reduce_add_sync(0xffffffffu, c4[r]);
+        if ((t & 31) == 0) atomicAdd(&acnt[r], v);
+      }
+      __syncthreads();
+      if (t == 0) {
+        int best = 0;
+        for (int r = 1; r < 4; ++r) if (acnt[r] > acnt[best]) best = r;
+        // P_{s0} = r_prefix + sum_{i=base}^{s0} r_i
+        int p = (int)(st->r_prefix & 3);
+        for (long long s = base; s <= s0; ++s) p += (s == 0) ? 0 : d.seg_r[rmod(s, d.seg_cap)];
+        A_sh = ((best - p) % 4 + 4) % 4;
+        known_sh = 1;
+      }
+    }
+  }
+  __syncthreads();
+  if (!known_sh) n = 0;
+  // prefix of r over [base, base + n) in chunks of 1024
+  int carry = (int)(st->r_prefix & 3);
+  for (int c0 = 0; c0 < n; c0 += 1024) {
+    const long long s = base + c0 + t;
+    int r = 0;
+    if (c0 + t < n && s > 0) r = d.seg_r[rmod(s, d.seg_cap)];
+    pre[t] = r;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+      const int o = (t >= off) ? pre[t - off] : 0;
+      __syncthreads();
+      pre[t] += o;
+      __syncthreads();
+    }
+    if (c0 + t < n) d.seg_R[rmod(s, d.seg_cap)] = (A_sh + carry + pre[t]) & 3;
+    const int tot = pre[1023];
+    __syncthreads();
+    carry = (carry + tot) & 3;
+  }
+  if (t == 0) {
+    st->anchor_known = known_sh;
+    st->anchor_A = A_sh;
+    st->fin_lo = base;
+    st->fin_hi = base + n;
+    st->seg_next = base + n;
+    st->r_prefix = carry;
+    d.hm->seg_next = base + n;
+  }
+}
+
+// ------------------------------------------------------------------ H10/H23/H25 finalise
+// Final labels (rotated by j^{R_s}), reference comparison, per-segment error counts,
+// canonical absolute-frame taps w~_s = w e^{j theta} j^{-R_s} (c-9 'Seed').
+__global__ void __launch_bounds__(256) k_lms_final(RxDev d, unsigned char *labels, long long lab_cap,
+                                                   int nseg) {
+  __shared__ long long red[8];
+  DevState *st = d.st;
+  const long long s = st->fin_lo + blockIdx.x;
+  if (blockIdx.x >= nseg || s >= st->fin_hi) return;
+  const long long si = rmod(s, d.seg_cap);
+  const int R = d.family == 1 ? d.seg_R[si] : 0;
+  const long long lo = s * (long long)d.S, hi = seg_end_of(d, s);
+  const int b = d.kbits >> 1;
+  long long err = 0, cntd = 0;
+  for (long long m = lo + threadIdx.x; m < hi; m += blockDim.x) {
+    int code = d.level[rmod(m, d.sym_cap)];
+    int lab;
+    if (d.family == 1) {
+      code = qam_rot(code, R, d.L);       // level ring stays in the segment frame (stitching)
+      lab = (gray(code & 15) << b) | gray(code >> 4);
+    } else {
+      lab = gray(code);
+    }
+    d.level_fin[rmod(m, d.sym_cap)] = (unsigned char)code;
+    if (labels) labels[m % lab_cap] = (unsigned char)lab;
+    if (m >= d.warmup) {
+      const long long ri = ((st->sync_offset + m - d.m0) % RX_PREF + RX_PREF) % RX_PREF;
+      err += __popc(lab ^ (int)d.ref_lab[ri]);
+      ++cntd;
+    }
+  }
+  err = __reduce_add_sync(0xffffffffu, (unsigned)err);
+  cntd = __reduce_add_sync(0xffffffffu, (unsigned)cntd);
+  if ((threadIdx.x & 31) == 0) { red[threadIdx.x >> 5] = err; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long e2 = 0;
+    for (int w = 0; w < 8; ++w) e2 += red[w];
+    d.seg_err[2 * si] = e2;
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cntd;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long c2 = 0;
+    for (int w = 0; w < 8; ++w) c2 += red[w];
+    d.seg_err[2 * si + 1] = c2;
+  }
+  // canonical taps for the lag-D seeds (reading R-SEED): QAM taps are rotated so
+  // that arg(sum_k w_k |w_k|) = 0 — the common carrier phase is removed before averaging.
+  if (threadIdx.x < 32) {
+    const int k = threadIdx.x;
+    float2 w = k < d.K ? d.seg_w[si * RX_MAX_K + k] : make_float2(0.f, 0.f);
+    if (d.family == 1) {
+      const float a = sqrtf(cabs2(w));
+      const float px = warp_sum(w.x * a), py = warp_sum(w.y * a);
+      const float inv = rsqrtf(fmaxf(px * px + py * py, 1e-30f));
+      w = cmulc(w, make_float2(px * inv, py * inv));
+    }
+    if (k < d.K) d.seg_w[si * RX_MAX_K + k] = w;
+  }
+}
+
+// Counters in fixed order + epoch seeds (mean canonical taps) for epochs fully finalised.
+__global__ void __launch_bounds__(1024) k_lms_epoch(RxDev d, int flush) {
+  __shared__ double sh[32];
+  __shared__ long long shl[32];
+  DevState *st = d.st;
+  const long long lo = st->fin_lo, hi = st->fin_hi;
+  const int t = threadIdx.x;
+  double en = 0.0, ed = 0.0;
+  long long er = 0, ct = 0;
+  for (long long s = lo + t; s < hi; s += blockDim.x) {
+    const long long si = rmod(s, d.seg_cap);
+    en += d.seg_evm[2 * si];
+    ed += d.seg_evm[2 * si + 1];
+    er += d.seg_err[2 * si];
+    ct += d.seg_err[2 * si + 1];
+  }
+  en = warp_sum_d(en);
+  ed = warp_sum_d(ed);
+  for (int o = 16; o > 0; o >>= 1) {
+    er += __shfl_xor_sync(0xffffffffu, er, o);
+    ct += __shfl_xor_sync(0xffffffffu, ct, o);
+  }
+  __shared__ double sh2[32];
+  __shared__ long long shl2[32];
+  if ((t & 31) == 0) { sh[t >> 5] = en; sh2[t >> 5] = ed; shl[t >> 5] = er; shl2[t >> 5] = ct; }
+  __syncthreads();
+  if (t == 0) {
+    double a = 0.0, b = 0.0;
+    long long x = 0, y = 0;
+    for (int w = 0; w < 32; ++w) { a += sh[w]; b += sh2[w]; x += shl[w]; y += shl2[w]; }
+    st->evm_num += a;
+    st->evm_den += b;
+    st->bit_errors += x;
+    st->symbols_counted += y;
+    st->bits += y * d.kbits;
+    long long so = hi * (long long)d.S;
+    if (st->m_end >= 0 && so > st->m_end) so = st->m_end;
+    if (hi > lo) st->symbols_out = so;
+  }
+  __syncthreads();
+  // epoch seeds: epochs e with all segments < hi finalised
+  const long long spe = d.E_sym / d.S;
+  const long long e_lo = lo / spe;
+  long long e_hi = hi / spe;   // epochs [e_lo, e_hi) complete
+  if (flush && st->m_end >= 0 && hi * (long long)d.S >= st->m_end) e_hi = (hi + spe - 1) / spe;
+  for (long long e = e_lo; e < e_hi; ++e) {
+    const long long tgt = e + d.D;
+    if (d.seed_ready[rmod(tgt, d.seed_cap)] == tgt + 1) continue;
+    const long long s_lo = e * spe;
+    long long s_hi = s_lo + spe;
+    if (s_hi > hi) s_hi = hi;
+    // thread layout: k = t >> 5 (tap), lane sums segments lane, lane+32, ... in fixed order
+    const int k = t >> 5, lane = t & 31;
+    float sx = 0.f, sy = 0.f;
+    if (k < d.K)
+      for (long long s = s_lo + lane; s < s_hi; s += 32) {
+        const float2 w = d.seg_w[rmod(s, d.seg_cap) * RX_MAX_K + k];
+        sx += w.x; sy += w.y;
+      }
+    sx = warp_sum(sx);
+    sy = warp_sum(sy);
+    if (k < d.K && lane == 0) {
+      const float inv = 1.0f / (float)(s_hi - s_lo);
+      d.seed[rmod(tgt, d.seed_cap) * RX_MAX_K + k] = make_float2(sx * inv, sy * inv);
+    }
+    __syncthreads();
+    if (t == 0) { __threadfence(); d.seed_ready[rmod(tgt, d.seed_cap)] = (int)(tgt + 1); }
+    __syncthreads();
+  }
+}

@@ -1,0 +1,713 @@
+// rx_api.cu — librx host side: the C ABI of include/rx.h, handle lifetime, constant tables,
+// and the stream-ordered per-call orchestration of the kernels (no host synchronisation
+// inside rx_process / rx_flush).
+//
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -shared -Xcompiler -fPIC
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <vector>
+
+#include "rx.h"
+#define RX_FLAG_SYNC_DEV RX_FLAG_SYNC
+#include "k_pam.cuh"
+#include "k_kk.cuh"
+#include "k_lms.cuh"
+
+#ifndef RX_GIT
+#define RX_GIT "dev"
+#endif
+
+// ------------------------------------------------------------------ small kernels
+__global__ void k_hist_copy(InView in, uint16_t *hist, long long hist_cap, long long p0, long long p1) {
+  for (long long p = p0 + (long long)blockIdx.x * blockDim.x + threadIdx.x; p < p1;
+       p += (long long)gridDim.x * blockDim.x)
+    hist[p & (hist_cap - 1)] = in.cur[p - in.call_start];
+}
+__global__ void k_pam_mend(RxDev d, long long be_done) {
+  long long f = d.Mb[rmod(be_done, d.blk_cap)];
+  if (f < 0) f = 0;
+  d.st->v_front = f;
+  d.st->m_end = f;
+}
+__global__ void k_kk_mend(RxDev d, long long q_end) {
+  d.st->v_front = q_end;
+  if (d.st->synced) {
+    const long long h = d.st->sync_phase;
+    long long me = (q_end - h + 1) / 2;
+    d.st->m_end = me > 0 ? me : 0;
+  } else {
+    d.st->m_end = 0;
+    set_flag(d.st, RX_FLAG_SYNC);
+  }
+}
+__global__ void k_reset_counters(DevState *st) {
+  st->bit_errors = st->bits = st->symbols_counted = st->clipped = st->domain_errors = 0;
+  st->first_domain = 0x7fffffffffffffffLL;
+  st->evm_num = st->evm_den = 0.0;
+  st->flags = 0;
+}
+
+// ------------------------------------------------------------------ handle
+struct rx_handle {
+  rx_config cfg;
+  int device;
+  RxDev d;
+  DevState *st_dev;
+  HostMirror *hm_host;
+  std::vector<void *> allocs;
+  // host-known progress (absolute units)
+  long long n_in, fe_done, clk_done, be_done, norm_done, s2_done, cfo_done;
+  bool flushed;
+  long long launches;
+  int sps;
+  long long Q;   // 2-sps samples per buffer (KK)
+  long long hist_cap;
+};
+
+static long long next_pow2(long long x) {
+  long long p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+#define CK(x)                                      \
+  do {                                             \
+    cudaError_t e_ = (x);                          \
+    if (e_ != cudaSuccess) {                       \
+      fprintf(stderr, "librx: %s: %s\n", #x, cudaGetErrorString(e_)); \
+      return RX_ECUDA;                             \
+    }                                              \
+  } while (0)
+
+template <typename T>
+static rx_status dalloc(rx_handle *h, T **p, long long n) {
+  void *q = nullptr;
+  size_t bytes = (size_t)(n > 0 ? n : 1) * sizeof(T);
+  if (cudaMalloc(&q, bytes) != cudaSuccess) return RX_ENOMEM;
+  if (cudaMemset(q, 0, bytes) != cudaSuccess) return RX_ECUDA;
+  h->allocs.push_back(q);
+  *p = (T *)q;
+  return RX_OK;
+}
+template <typename T>
+static rx_status dupload(rx_handle *h, const T **p, const std::vector<T> &v) {
+  T *q;
+  rx_status s = dalloc(h, &q, (long long)v.size());
+  if (s) return s;
+  if (cudaMemcpy(q, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess) return RX_ECUDA;
+  *p = q;
+  return RX_OK;
+}
+
+extern "C" void rx_config_default(rx_config *c, int family, int order) {
+  memset(c, 0, sizeof(*c));
+  c->family = family;
+  c->order = order;
+  c->baud = family == RX_PAM ? 2e9 : 1e9;
+  c->sample_rate = 4e9;
+  c->fft_size = 1024;
+  c->hop = 512;
+  c->buffer_blocks = 8192;
+  c->adc_gain = 1.0;
+  c->clock_avg_half = 52;
+  c->carrier_offset_hz = 0.547e9;
+  c->sideband = -1;
+  c->lms_taps = family == RX_PAM ? 15 : 4;
+  c->lms_block = 32;
+  c->lms_segment = 4096;
+  c->lms_overlap = family == RX_PAM ? 0 : 256;
+  c->tap_lag_epochs = 8;
+  c->mu = family == RX_PAM ? 1e-3 : 2e-3;
+  c->train_symbols = 8192;
+  c->cfo_enable = 1;
+  c->cpr_test_phases = order == 4 ? 0 : 32;
+  c->prbs_order = 15;
+  c->prbs_seed = 0x7FFF;
+  c->sync_start = 4096;
+  c->sync_window = 2048;
+  c->sync_min_corr = 0.3;
+  c->history_buffers = 3;
+}
+
+extern "C" const char *rx_strerror(int s) {
+  switch (s) {
+    case RX_OK: return "ok";
+    case RX_EINVAL: return "invalid argument or configuration";
+    case RX_ENOMEM: return "device allocation failed";
+    case RX_ECUDA: return "CUDA error";
+    case RX_EDOMAIN: return "KK domain error (I + dc <= 0 seen)";
+    case RX_ESYNC: return "frame synchronisation failed";
+    case RX_EDIVERGE: return "equaliser diverged";
+    case RX_ECAPACITY: return "capacity exceeded";
+    case RX_ESTATE: return "call order violated";
+    default: return "unknown status";
+  }
+}
+
+extern "C" const char *rx_version(void) { return "librx sm_100a " RX_GIT; }
+
+static bool is_pow2(long long x) { return x > 0 && (x & (x - 1)) == 0; }
+
+static rx_status validate(const rx_config *c) {
+  if (!c) return RX_EINVAL;
+  if (c->family != RX_PAM && c->family != RX_QAM_KK) return RX_EINVAL;
+  if (c->family == RX_PAM && !(c->order == 2 || c->order == 4 || c->order == 8 || c->order == 16)) return RX_EINVAL;
+  if (c->family == RX_QAM_KK && !(c->order == 4 || c->order == 16 || c->order == 64)) return RX_EINVAL;
+  if (!(c->baud > 0) || !(c->sample_rate > 0)) return RX_EINVAL;
+  const double sps = c->sample_rate / c->baud;
+  if (fabs(sps - (c->family == RX_PAM ? 2.0 : 4.0)) > 1e-9) return RX_EINVAL;
+  if (c->fft_size != 1024 || c->hop != 512) return RX_EINVAL;
+  if (c->buffer_blocks < 16 || !is_pow2(c->buffer_blocks)) return RX_EINVAL;
+  if (!c->static_taps || c->n_static_taps < 1 || c->n_static_taps % 2 == 0 || c->n_static_taps > c->hop + 1)
+    return RX_EINVAL;
+  if (c->lms_taps < 1 || c->lms_taps > RX_MAX_K) return RX_EINVAL;
+  if (c->lms_block != 32) return RX_EINVAL;
+  if (c->lms_segment < 64 || c->lms_segment % 32 || !is_pow2(c->lms_segment)) return RX_EINVAL;
+  const long long E = (long long)c->buffer_blocks * (c->family == RX_PAM ? 256 : 128);
+  if (E % c->lms_segment) return RX_EINVAL;
+  if (c->lms_overlap < 0 || c->lms_overlap % 32 || c->lms_overlap > RX_MAX_O || c->lms_overlap > c->lms_segment) return RX_EINVAL;
+  if (c->family == RX_PAM && c->lms_overlap != 0) return RX_EINVAL;
+  if (c->tap_lag_epochs < 1 || c->tap_lag_epochs > 32) return RX_EINVAL;
+  if (c->widely_linear != 0) return RX_EINVAL;
+  if (!(c->mu > 0) || c->mu > 1.0) return RX_EINVAL;
+  if (c->train_symbols < 32 || c->train_symbols % 32) return RX_EINVAL;
+  if (c->cpr_test_phases < 0 || c->cpr_test_phases > RX_MAX_PT) return RX_EINVAL;
+  if (c->family == RX_QAM_KK && c->order > 4 && c->cpr_test_phases == 0) return RX_EINVAL;
+  if (c->prbs_order != 15 || (c->prbs_seed & 0x7FFF) == 0) return RX_EINVAL;
+  if (c->sync_start < 0 || c->sync_window < 64 || c->sync_window > 4096) return RX_EINVAL;
+  if (c->clock_avg_half < 0 || c->clock_avg_half > 1024) return RX_EINVAL;
+  if (c->history_buffers < 3 || c->history_buffers > 64) return RX_EINVAL;
+  if (c->family == RX_QAM_KK && !(c->sideband == 1 || c->sideband == -1)) return RX_EINVAL;
+  if (c->family == RX_PAM && c->thresholds) {
+    for (int i = 1; i < c->order - 1; ++i)
+      if (!(c->thresholds[i] > c->thresholds[i - 1])) return RX_EINVAL;
+  }
+  return RX_OK;
+}
+
+// PRBS-15 (x^15 + x^14 + 1), library-side implementation: Galois-free Fibonacci register.
+static void prbs_bits(unsigned seed, std::vector<int> &bits) {
+  bits.resize(RX_PREF);
+  unsigned s = seed & 0x7FFF;
+  for (int i = 0; i < RX_PREF; ++i) {
+    const unsigned b = ((s >> 14) ^ (s >> 13)) & 1u;
+    s = ((s << 1) | b) & 0x7FFFu;
+    bits[i] = (int)b;
+  }
+}
+static int gray_dec(int g) {
+  int i = 0;
+  for (; g; g >>= 1) i ^= g;
+  return i;
+}
+
+extern "C" void rx_destroy(rx_handle *h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  for (void *p : h->allocs) cudaFree(p);
+  if (h->hm_host) cudaFreeHost(h->hm_host);
+  delete h;
+}
+
+extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle **out) {
+  if (!out) return RX_EINVAL;
+  *out = nullptr;
+  rx_status vs = validate(cfg);
+  if (vs) return vs;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || cuda_device < 0 || cuda_device >= ndev) return RX_ECUDA;
+  CK(cudaSetDevice(cuda_device));
+  rx_handle *h = new rx_handle();
+  h->cfg = *cfg;
+  h->cfg.static_taps = nullptr;
+  h->cfg.thresholds = nullptr;
+  h->device = cuda_device;
+  const rx_config &c = *cfg;
+  RxDev &d = h->d;
+  memset(&d, 0, sizeof(d));
+  const bool kk = c.family == RX_QAM_KK;
+  d.family = c.family;
+  d.M = c.order;
+  d.L = kk ? (int)lround(sqrt((double)c.order)) : c.order;
+  d.kbits = (int)lround(log2((double)c.order));
+  d.scale = (float)(c.adc_gain / 2047.5);
+  d.dc = (float)c.dc_offset;
+  d.sideband = c.sideband;
+  d.carrier_inc = (unsigned long long)llrint(ldexp((double)c.sideband * c.carrier_offset_hz / c.sample_rate, 64));
+  d.fs2 = c.sample_rate / 2.0;
+  d.clock_half = c.clock_avg_half;
+  d.buffer_blocks = c.buffer_blocks;
+  d.E_sym = (long long)c.buffer_blocks * (kk ? 128 : 256);
+  d.K = c.lms_taps; d.B = c.lms_block; d.S = c.lms_segment; d.O = c.lms_overlap;
+  d.D = c.tap_lag_epochs;
+  d.cpr = kk ? (c.cpr_test_phases == 0 ? 1 : 2) : 0;
+  d.Pt = c.cpr_test_phases;
+  d.mu = (float)c.mu;
+  d.T_train = c.train_symbols;
+  d.m0 = c.sync_start;
+  d.W_sync = c.sync_window;
+  d.sync_min = (float)c.sync_min_corr;
+  d.warmup = c.warmup_symbols;
+  d.cfo_enable = kk ? c.cfo_enable : 0;
+  h->sps = kk ? 4 : 2;
+  h->Q = (long long)c.buffer_blocks * 256;
+  rx_status s = RX_OK;
+#define TRY(x) do { s = (x); if (s) { rx_destroy(h); return s; } } while (0)
+  // ---- constant tables
+  std::vector<float2> tw(1024);
+  for (int k = 0; k < 1024; ++k) {
+    const double a = -2.0 * M_PI * k / 1024.0;
+    tw[k] = make_float2((float)cos(a), (float)sin(a));
+  }
+  TRY(dupload(h, &d.tw, tw));
+  // static EQ spectrum H = DFT_1024(h_c), h_c[n mod N] = taps[(L-1)/2 + n] (SURVEY c-0, A3)
+  {
+    std::vector<float2> H(1024);
+    const int L = c.n_static_taps, half = (L - 1) / 2;
+    for (int k = 0; k < 1024; ++k) {
+      double re = 0.0, im = 0.0;
+      for (int n = -half; n <= half; ++n) {
+        const double tr = kk ? cfg->static_taps[2 * (half + n)] : cfg->static_taps[half + n];
+        const double ti = kk ? cfg->static_taps[2 * (half + n) + 1] : 0.0;
+        const double a = -2.0 * M_PI * (double)k * (double)n / 1024.0;
+        const double cs = cos(a), sn = sin(a);
+        re += tr * cs - ti * sn;
+        im += tr * sn + ti * cs;
+      }
+      H[k] = make_float2((float)re, (float)im);
+    }
+    TRY(dupload(h, &d.H, H));
+  }
+  // decision levels / thresholds (c-11)
+  {
+    std::vector<float> lv(d.L), th(d.M > 1 ? d.M - 1 : 1);
+    if (!kk) {
+      for (int i = 0; i < d.M; ++i) lv[i] = (float)((2.0 * i - d.M + 1) / (double)(d.M - 1));
+      for (int i = 0; i < d.M - 1; ++i) {
+        const double a = (2.0 * i - d.M + 1) / (double)(d.M - 1), b = (2.0 * (i + 1) - d.M + 1) / (double)(d.M - 1);
+        th[i] = cfg->thresholds ? (float)cfg->thresholds[i] : (float)(0.5 * (a + b));
+      }
+    } else {
+      const double sc = sqrt(3.0 / (2.0 * (d.M - 1)));
+      for (int i = 0; i < d.L; ++i) lv[i] = (float)((2.0 * i - d.L + 1) * sc);
+    }
+    TRY(dupload(h, &d.lvl, lv));
+    TRY(dupload(h, &d.thr, th));
+  }
+  // PRBS reference (c-10): symbol i = bits [k i, k i + k) mod P, MSB first, Gray label
+  {
+    std::vector<int> bits;
+    prbs_bits(c.prbs_seed, bits);
+    std::vector<float2> rv(RX_PREF);
+    std::vector<unsigned char> rl(RX_PREF), ri(RX_PREF);
+    const int k = d.kbits;
+    std::vector<float> lvh(d.L);
+    const double sc = kk ? sqrt(3.0 / (2.0 * (d.M - 1))) : 0.0;
+    for (int i = 0; i < d.L; ++i) lvh[i] = kk ? (float)((2.0 * i - d.L + 1) * sc) : (float)((2.0 * i - d.M + 1) / (double)(d.M - 1));
+    for (int i = 0; i < RX_PREF; ++i) {
+      int lab = 0;
+      for (int t = 0; t < k; ++t) lab = (lab << 1) | bits[((long long)i * k + t) % RX_PREF];
+      rl[i] = (unsigned char)lab;
+      if (!kk) {
+        const int li = gray_dec(lab);
+        ri[i] = (unsigned char)li;
+        rv[i] = make_float2(lvh[li], 0.f);
+      } else {
+        const int b = k / 2;
+        const int iI = gray_dec(lab >> b), iQ = gray_dec(lab & ((1 << b) - 1));
+        ri[i] = (unsigned char)(iI | (iQ << 4));
+        rv[i] = make_float2(lvh[iI], lvh[iQ]);
+      }
+    }
+    TRY(dupload(h, &d.ref_val, rv));
+    TRY(dupload(h, &d.ref_lab, rl));
+    TRY(dupload(h, &d.ref_idx, ri));
+    std::vector<float2> rot(RX_MAX_PT);
+    for (int p = 0; p < RX_MAX_PT; ++p) {
+      const int Pt = c.cpr_test_phases > 0 ? c.cpr_test_phases : 1;
+      const double ph = -M_PI / 4 + (p + 0.5) * (M_PI / 2) / Pt;
+      rot[p] = make_float2((float)cos(ph), (float)-sin(ph));
+    }
+    TRY(dupload(h, &d.bps_rot, rot));
+  }
+  // ---- rings
+  const int HB = c.history_buffers;
+  h->hist_cap = 1 << 16;
+  d.hist_cap = h->hist_cap;
+  TRY(dalloc(h, &d.hist, d.hist_cap));
+  d.blk_cap = next_pow2((long long)HB * c.buffer_blocks + 256);
+  d.buf_cap = 64;
+  d.sym_cap = next_pow2((long long)HB * c.buffer_blocks * (kk ? 128 : 260));
+  if (!kk) {
+    TRY(dalloc(h, &d.C, d.blk_cap));
+    TRY(dalloc(h, &d.theta, d.blk_cap));
+    TRY(dalloc(h, &d.tau, d.blk_cap));
+    TRY(dalloc(h, &d.Mb, d.blk_cap));
+    TRY(dalloc(h, &d.blk_sum, d.blk_cap));
+    TRY(dalloc(h, &d.blk_abs, d.blk_cap));
+    TRY(dalloc(h, &d.u, d.sym_cap));
+    TRY(dalloc(h, &d.uhat, d.sym_cap));
+    TRY(dalloc(h, &d.norm_dc, d.buf_cap));
+    TRY(dalloc(h, &d.norm_amp, d.buf_cap));
+    TRY(dalloc(h, &d.norm_cnt, d.buf_cap));
+  } else {
+    d.E_cap = next_pow2((long long)HB * c.buffer_blocks * 512);
+    d.z_cap = next_pow2((long long)HB * c.buffer_blocks * 256);
+    TRY(dalloc(h, &d.E, d.E_cap));
+    TRY(dalloc(h, &d.z, d.z_cap));
+    TRY(dalloc(h, &d.cfo, d.buf_cap));
+    d.cfo_G = 128;
+    TRY(dalloc(h, &d.cfo_part, (long long)d.cfo_G * 1024));
+    TRY(dalloc(h, &d.cfo_pow, d.cfo_G));
+    TRY(dalloc(h, &d.cfo_a, h->Q / 1024 + 1));
+  }
+  TRY(dalloc(h, &d.sync_g, 2 * RX_PREF));
+  TRY(dalloc(h, &d.sync_c, 2 * RX_PREF));
+  TRY(dalloc(h, &d.w_train, RX_MAX_K));
+  d.seed_cap = 64;
+  TRY(dalloc(h, &d.seed, d.seed_cap * RX_MAX_K));
+  TRY(dalloc(h, &d.seed_ready, d.seed_cap));
+  d.seg_cap = next_pow2(d.sym_cap / c.lms_segment + 8);
+  TRY(dalloc(h, &d.seg_w, d.seg_cap * RX_MAX_K));
+  TRY(dalloc(h, &d.seg_theta, d.seg_cap));
+  TRY(dalloc(h, &d.seg_done, d.seg_cap));
+  TRY(dalloc(h, &d.seg_stitched, d.seg_cap));
+  TRY(dalloc(h, &d.seg_r, d.seg_cap));
+  TRY(dalloc(h, &d.seg_R, d.seg_cap));
+  TRY(dalloc(h, &d.seg_evm, 2 * d.seg_cap));
+  TRY(dalloc(h, &d.seg_err, 2 * d.seg_cap));
+  if (c.lms_overlap > 0) TRY(dalloc(h, &d.seg_warm, d.seg_cap * c.lms_overlap));
+  TRY(dalloc(h, &d.level, d.sym_cap));
+  TRY(dalloc(h, &d.level_fin, d.sym_cap));
+  TRY(dalloc(h, &d.yout, d.sym_cap));
+  // ---- state
+  TRY(dalloc(h, &h->st_dev, 1));
+  {
+    DevState st;
+    memset(&st, 0, sizeof(st));
+    st.m_end = -1;
+    st.first_domain = 0x7fffffffffffffffLL;
+    if (cudaMemcpy(h->st_dev, &st, sizeof(st), cudaMemcpyHostToDevice) != cudaSuccess) { rx_destroy(h); return RX_ECUDA; }
+  }
+  d.st = h->st_dev;
+  if (cudaHostAlloc((void **)&h->hm_host, sizeof(HostMirror), cudaHostAllocMapped) != cudaSuccess) { rx_destroy(h); return RX_ENOMEM; }
+  memset((void *)h->hm_host, 0, sizeof(HostMirror));
+  if (cudaHostGetDevicePointer((void **)&d.hm, (void *)h->hm_host, 0) != cudaSuccess) { rx_destroy(h); return RX_ECUDA; }
+  // kernels needing > 48 KB dynamic shared memory
+  const size_t s2_smem = (1024 + 8 * FFT_PAD_N) * sizeof(float2);
+  const size_t cfo_smem = (1024 + 8 * FFT_PAD_N) * sizeof(float2) + 1024 * sizeof(float);
+  if (cudaFuncSetAttribute(k_kk_s2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2_smem) != cudaSuccess ||
+      cudaFuncSetAttribute(k_cfo_partial, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfo_smem) != cudaSuccess ||
+      cudaFuncSetAttribute(k_sync_corr<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536) != cudaSuccess ||
+      cudaFuncSetAttribute(k_sync_corr<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536) != cudaSuccess) {
+    rx_destroy(h);
+    return RX_ECUDA;
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) { rx_destroy(h); return RX_ECUDA; }
+#undef TRY
+  *out = h;
+  return RX_OK;
+}
+
+// ------------------------------------------------------------------ orchestration
+#define LAUNCH(h, ...)                   \
+  do {                                   \
+    __VA_ARGS__;                         \
+    (h)->launches++;                     \
+  } while (0)
+
+static rx_status check_launch() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    fprintf(stderr, "librx: launch failed: %s\n", cudaGetErrorString(e));
+    return RX_ECUDA;
+  }
+  return RX_OK;
+}
+
+static unsigned gridc(long long n, int per) { return (unsigned)((n + per - 1) / per); }
+
+template <bool CPLX>
+static void launch_sync_train(rx_handle *h, cudaStream_t s, int flush) {
+  RxDev &d = h->d;
+  if (h->hm_host->trained) return;
+  const int nh = CPLX ? 2 : 1;
+  const size_t smem = (size_t)nh * d.W_sync * sizeof(float2);
+  if (!h->hm_host->synced) {
+    LAUNCH(h, (k_sync_corr<CPLX><<<gridc((long long)nh * RX_PREF, 256), 256, smem, s>>>(d)));
+    LAUNCH(h, (k_sync_pick<CPLX><<<1, 1024, 0, s>>>(d, flush)));
+  }
+  LAUNCH(h, (k_lms_train<CPLX><<<1, 32, 0, s>>>(d, flush)));
+}
+
+static void launch_lms_rounds(rx_handle *h, cudaStream_t s, unsigned char *labels, long long lab_cap,
+                              int flush, long long sym_ub) {
+  RxDev &d = h->d;
+  const long long S = d.S;
+  long long seg_lb = h->hm_host->seg_next;   // stale => lower bound
+  long long seg_ub = sym_ub / S + 1;
+  long long nseg = seg_ub - seg_lb + 1;
+  if (nseg < 1) nseg = 1;
+  if (nseg > d.seg_cap / 2) nseg = d.seg_cap / 2;
+  const long long e_lo = seg_lb * S / d.E_sym, e_hi = seg_ub * S / d.E_sym;
+  const long long rounds = (e_hi - e_lo + 1 + d.D - 1) / d.D + 1;
+  for (long long r = 0; r < rounds; ++r) {
+    if (d.family == RX_PAM) {
+      LAUNCH(h, (k_lms_seg<false, 0><<<gridc(nseg, 4), 128, 0, s>>>(d, flush, (int)nseg)));
+    } else if (d.cpr == 1) {
+      LAUNCH(h, (k_lms_seg<true, 1><<<gridc(nseg, 4), 128, 0, s>>>(d, flush, (int)nseg)));
+    } else {
+      LAUNCH(h, (k_lms_seg<true, 2><<<gridc(nseg, 4), 128, 0, s>>>(d, flush, (int)nseg)));
+    }
+    LAUNCH(h, (k_lms_stitch<<<(unsigned)nseg, 256, 0, s>>>(d, (int)nseg)));
+    LAUNCH(h, (k_lms_prefix<<<1, 1024, 0, s>>>(d, flush, (int)nseg)));
+    LAUNCH(h, (k_lms_final<<<(unsigned)nseg, 256, 0, s>>>(d, labels, lab_cap, (int)nseg)));
+    LAUNCH(h, (k_lms_epoch<<<1, 1024, 0, s>>>(d, flush)));
+  }
+}
+
+static void run_pam(rx_handle *h, cudaStream_t s, const InView &in, unsigned char *labels,
+                    long long lab_cap, int flush) {
+  RxDev &d = h->d;
+  const long long BB = d.buffer_blocks;
+  const long long fe_target = h->n_in / 512;
+  if (fe_target > h->fe_done) {
+    LAUNCH(h, (k_pam_fe<<<gridc(fe_target - h->fe_done, FE_GROUPS), 256, 0, s>>>(d, in, h->fe_done, fe_target)));
+    h->fe_done = fe_target;
+  }
+  long long clk_target = flush ? h->fe_done : h->fe_done - d.clock_half;
+  if (clk_target > h->clk_done) {
+    LAUNCH(h, (k_pam_theta<<<gridc(clk_target - h->clk_done, 256), 256, 0, s>>>(d, h->clk_done, clk_target, h->fe_done - 1)));
+    LAUNCH(h, (k_pam_unwrap<<<1, 1024, 0, s>>>(d, h->clk_done, clk_target)));
+    h->clk_done = clk_target;
+  }
+  long long be_target = flush ? h->fe_done - 1 : h->clk_done - 1;
+  if (be_target > h->be_done) {
+    LAUNCH(h, (k_pam_be<<<gridc(be_target - h->be_done, FE_GROUPS), 256, 0, s>>>(d, in, h->be_done, be_target)));
+    h->be_done = be_target;
+  }
+  while ((h->norm_done + 1) * BB <= h->be_done || (flush && h->norm_done * BB < h->be_done)) {
+    const long long blo = h->norm_done * BB;
+    long long bhi = blo + BB;
+    if (bhi > h->be_done) bhi = h->be_done;
+    const long long beta = h->norm_done;
+    LAUNCH(h, (k_norm_dc<<<1, 1024, 0, s>>>(d, beta, blo, bhi)));
+    LAUNCH(h, (k_norm_abs<<<(unsigned)(bhi - blo), 256, 0, s>>>(d, beta, blo, bhi)));
+    LAUNCH(h, (k_norm_amp<<<1, 1024, 0, s>>>(d, beta, blo, bhi)));
+    LAUNCH(h, (k_norm_apply<<<(unsigned)(bhi - blo), 256, 0, s>>>(d, beta, blo, bhi, 0)));
+    h->norm_done++;
+  }
+  if (flush) LAUNCH(h, (k_pam_mend<<<1, 1, 0, s>>>(d, h->be_done > 0 ? h->be_done : 0)));
+  launch_sync_train<false>(h, s, flush);
+  launch_lms_rounds(h, s, labels, lab_cap, flush, 260 * h->be_done + 1024);
+}
+
+static void run_kk(rx_handle *h, cudaStream_t s, const InView &in, unsigned char *labels,
+                   long long lab_cap, int flush) {
+  RxDev &d = h->d;
+  const long long s1_target = h->n_in / 512;
+  if (s1_target > h->fe_done) {
+    LAUNCH(h, (k_kk_s1<<<gridc(s1_target - h->fe_done, FE_GROUPS), 256, 0, s>>>(d, in, h->fe_done, s1_target)));
+    h->fe_done = s1_target;
+  }
+  const long long s2_target = h->fe_done - 1;
+  if (s2_target > h->s2_done) {
+    const size_t smem = (1024 + 8 * FFT_PAD_N) * sizeof(float2);
+    LAUNCH(h, (k_kk_s2<<<gridc(s2_target - h->s2_done, 4), 256, smem, s>>>(d, h->s2_done, s2_target)));
+    h->s2_done = s2_target;
+  }
+  const long long q_front = h->s2_done > 0 ? 256 * h->s2_done - 128 : 0;
+  const long long Q = h->Q;
+  while ((h->cfo_done + 1) * Q <= q_front || (flush && h->cfo_done * Q < q_front)) {
+    const long long qlo = h->cfo_done * Q;
+    long long qhi = qlo + Q;
+    if (qhi > q_front) qhi = q_front;
+    const size_t smem = (1024 + 8 * FFT_PAD_N) * sizeof(float2) + 1024 * sizeof(float);
+    LAUNCH(h, (k_cfo_partial<<<(unsigned)d.cfo_G, 256, smem, s>>>(d, qlo, qhi)));
+    LAUNCH(h, (k_cfo_final<<<1, 1024, 0, s>>>(d, h->cfo_done, qlo, qhi)));
+    if (d.cfo_enable) LAUNCH(h, (k_cfo_fine<<<296, 256, 0, s>>>(d, h->cfo_done, qlo, qhi)));
+    LAUNCH(h, (k_cfo_fine_final<<<1, 1024, 0, s>>>(d, h->cfo_done, qlo, qhi)));
+    h->cfo_done++;
+  }
+  launch_sync_train<true>(h, s, flush);
+  if (flush) LAUNCH(h, (k_kk_mend<<<1, 1, 0, s>>>(d, q_front)));
+  launch_lms_rounds(h, s, labels, lab_cap, flush, q_front / 2 + 1);
+}
+
+extern "C" rx_status rx_process(rx_handle *h, const unsigned short *d_samples, long long n,
+                                unsigned char *d_labels, long long labels_capacity, void *stream) {
+  if (!h || n < 0 || (n > 0 && !d_samples) || n % 512 || labels_capacity < 0) return RX_EINVAL;
+  if (n > (long long)h->d.buffer_blocks * 512) return RX_EINVAL;
+  if (labels_capacity > 0 && !d_labels) return RX_EINVAL;
+  if (((uintptr_t)d_samples) & 15) return RX_EINVAL;
+  if (h->flushed) return RX_ESTATE;
+  CK(cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  InView in;
+  in.cur = d_samples;
+  in.call_start = h->n_in;
+  in.call_end = h->n_in + n;
+  in.hist = h->d.hist;
+  in.hist_cap = h->hist_cap;
+  h->n_in += n;
+  if (h->d.family == RX_PAM) run_pam(h, s, in, labels_capacity ? d_labels : nullptr, labels_capacity ? labels_capacity : 1, 0);
+  else run_kk(h, s, in, labels_capacity ? d_labels : nullptr, labels_capacity ? labels_capacity : 1, 0);
+  if (n > 0) {
+    long long p0 = in.call_end - h->hist_cap;
+    if (p0 < in.call_start) p0 = in.call_start;
+    LAUNCH(h, (k_hist_copy<<<gridc(in.call_end - p0, 256) < 512 ? gridc(in.call_end - p0, 256) : 512, 256, 0, s>>>(
+                   in, h->d.hist, h->hist_cap, p0, in.call_end)));
+  }
+  return check_launch();
+}
+
+extern "C" rx_status rx_flush(rx_handle *h, unsigned char *d_labels, long long labels_capacity, void *stream) {
+  if (!h || labels_capacity < 0 || (labels_capacity > 0 && !d_labels)) return RX_EINVAL;
+  if (h->flushed) return RX_ESTATE;
+  CK(cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  InView in;
+  in.cur = nullptr;
+  in.call_start = h->n_in;
+  in.call_end = h->n_in;
+  in.hist = h->d.hist;
+  in.hist_cap = h->hist_cap;
+  if (h->d.family == RX_PAM) run_pam(h, s, in, labels_capacity ? d_labels : nullptr, labels_capacity ? labels_capacity : 1, 1);
+  else run_kk(h, s, in, labels_capacity ? d_labels : nullptr, labels_capacity ? labels_capacity : 1, 1);
+  h->flushed = true;
+  return check_launch();
+}
+
+extern "C" rx_status rx_get_stats(rx_handle *h, rx_stats *o, void *stream) {
+  if (!h || !o) return RX_EINVAL;
+  CK(cudaSetDevice(h->device));
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  DevState st;
+  CK(cudaMemcpy(&st, h->st_dev, sizeof(st), cudaMemcpyDeviceToHost));
+  memset(o, 0, sizeof(*o));
+  o->samples_in = h->n_in;
+  o->symbols_out = st.symbols_out;
+  o->bit_errors = st.bit_errors;
+  o->bits = st.bits;
+  o->symbols_counted = st.symbols_counted;
+  o->clipped = st.clipped;
+  o->domain_errors = st.domain_errors;
+  o->first_domain_error_index = st.domain_errors ? st.first_domain : -1;
+  o->evm_num = st.evm_num;
+  o->evm_den = st.evm_den;
+  o->sync_offset = st.sync_offset;
+  o->sync_phase = st.sync_phase;
+  o->sync_polarity = st.sync_polarity;
+  o->synced = st.synced;
+  o->sync_gamma = st.sync_gamma;
+  o->sync_phi0 = st.sync_phi0;
+  o->status_flags = st.flags | (st.domain_errors ? RX_FLAG_DOMAIN : 0);
+  o->launches = h->launches;
+  return RX_OK;
+}
+
+extern "C" rx_status rx_reset_stats(rx_handle *h, void *stream) {
+  if (!h) return RX_EINVAL;
+  CK(cudaSetDevice(h->device));
+  LAUNCH(h, (k_reset_counters<<<1, 1, 0, (cudaStream_t)stream>>>(h->st_dev)));
+  return check_launch();
+}
+
+extern "C" rx_status rx_get_taps(rx_handle *h, double *out, int capacity) {
+  if (!h || !out) return RX_EINVAL;
+  const bool kk = h->d.family == RX_QAM_KK;
+  const int need = kk ? 2 * h->d.K : h->d.K;
+  if (capacity < need) return RX_EINVAL;
+  CK(cudaSetDevice(h->device));
+  CK(cudaDeviceSynchronize());
+  float2 w[RX_MAX_K];
+  CK(cudaMemcpy(w, h->d.w_train, sizeof(float2) * h->d.K, cudaMemcpyDeviceToHost));
+  for (int k = 0; k < h->d.K; ++k) {
+    if (kk) { out[2 * k] = w[k].x; out[2 * k + 1] = w[k].y; }
+    else out[k] = w[k].x;
+  }
+  return RX_OK;
+}
+
+// copy [first, first+count) of a ring with capacity cap (elements of size es) to host
+static rx_status ring_read(const void *ring, long long cap, size_t es, long long first, long long count, void *out) {
+  if (first < 0 || count < 0 || count > cap) return RX_EINVAL;
+  const char *r = (const char *)ring;
+  char *o = (char *)out;
+  long long done = 0;
+  while (done < count) {
+    const long long i = (first + done) & (cap - 1);
+    long long chunk = cap - i;
+    if (chunk > count - done) chunk = count - done;
+    if (cudaMemcpy(o + done * es, r + i * es, (size_t)chunk * es, cudaMemcpyDeviceToHost) != cudaSuccess) return RX_ECUDA;
+    done += chunk;
+  }
+  return RX_OK;
+}
+
+extern "C" rx_status rx_probe_read(rx_handle *h, int which, long long first, long long count, void *out,
+                                   void *stream) {
+  if (!h || !out) return RX_EINVAL;
+  CK(cudaSetDevice(h->device));
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  RxDev &d = h->d;
+  const bool kk = d.family == RX_QAM_KK;
+  switch (which) {
+    case RX_PROBE_C: if (kk) return RX_EINVAL; return ring_read(d.C, d.blk_cap, sizeof(double2), first, count, out);
+    case RX_PROBE_TAU: if (kk) return RX_EINVAL; return ring_read(d.tau, d.blk_cap, sizeof(double), first, count, out);
+    case RX_PROBE_MB: if (kk) return RX_EINVAL; return ring_read(d.Mb, d.blk_cap, sizeof(long long), first, count, out);
+    case RX_PROBE_U: if (kk) return RX_EINVAL; return ring_read(d.u, d.sym_cap, sizeof(float), first, count, out);
+    case RX_PROBE_UHAT: if (kk) return RX_EINVAL; return ring_read(d.uhat, d.sym_cap, sizeof(float), first, count, out);
+    case RX_PROBE_E: if (!kk) return RX_EINVAL; return ring_read(d.E, d.E_cap, sizeof(float2), first, count, out);
+    case RX_PROBE_Z: if (!kk) return RX_EINVAL; return ring_read(d.z, d.z_cap, sizeof(float2), first, count, out);
+    case RX_PROBE_CFO: {
+      if (!kk) return RX_EINVAL;
+      std::vector<CfoParam> cp((size_t)count);
+      rx_status st = ring_read(d.cfo, d.buf_cap, sizeof(CfoParam), first, count, cp.data());
+      if (st) return st;
+      double *o = (double *)out;
+      for (long long i = 0; i < count; ++i) {
+        o[5 * i] = cp[i].P; o[5 * i + 1] = cp[i].df; o[5 * i + 2] = cp[i].kstar;
+        o[5 * i + 3] = (double)cp[i].inc; o[5 * i + 4] = (double)cp[i].origin;
+      }
+      return RX_OK;
+    }
+    case RX_PROBE_Y: return ring_read(d.yout, d.sym_cap, sizeof(float2), first, count, out);
+    case RX_PROBE_LEVEL: return ring_read(d.level_fin, d.sym_cap, 1, first, count, out);
+    case RX_PROBE_SEG: {
+      std::vector<int> R(count), r(count);
+      std::vector<float> th(count);
+      std::vector<double> evm(2 * count);
+      std::vector<long long> err(2 * count);
+      for (long long i = 0; i < count; ++i) {
+        const long long si = (first + i) & (d.seg_cap - 1);
+        CK(cudaMemcpy(&R[i], d.seg_R + si, sizeof(int), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&r[i], d.seg_r + si, sizeof(int), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&th[i], d.seg_theta + si, sizeof(float), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&evm[2 * i], d.seg_evm + 2 * si, 2 * sizeof(double), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&err[2 * i], d.seg_err + 2 * si, 2 * sizeof(long long), cudaMemcpyDeviceToHost));
+      }
+      double *o = (double *)out;
+      for (long long i = 0; i < count; ++i) {
+        o[6 * i] = R[i]; o[6 * i + 1] = r[i]; o[6 * i + 2] = th[i];
+        o[6 * i + 3] = (double)err[2 * i]; o[6 * i + 4] = evm[2 * i]; o[6 * i + 5] = evm[2 * i + 1];
+      }
+      return RX_OK;
+    }
+    case RX_PROBE_DEBUG: {
+      DevState st;
+      CK(cudaMemcpy(&st, h->st_dev, sizeof(st), cudaMemcpyDeviceToHost));
+      long long v[16] = {h->n_in, h->fe_done, h->clk_done, h->be_done, h->norm_done, h->s2_done, h->cfo_done,
+                         st.v_front, st.m_end, st.seg_next, st.fin_lo, st.fin_hi, st.synced, st.trained,
+                         st.anchor_known, st.anchor_A};
+      long long n = count < 16 ? count : 16;
+      memcpy(out, v, (size_t)n * sizeof(long long));
+      return RX_OK;
+    }
+    default: return RX_EINVAL;
+  }
+}

@@ -1,0 +1,101 @@
+// rx_dev.cuh — device-resident state of one librx handle.
+// Every ring is indexed by ABSOLUTE index (block b, sample p, 2-sps sample q, symbol m,
+// segment s, buffer beta) modulo its power-of-two capacity, so results do not depend on how
+// the caller chunks rx_process() calls (SURVEY §8(b) 'Ordering', §4 'Determinism').
+#pragma once
+#include "common.cuh"
+
+#define RX_MAX_K 32
+#define RX_MAX_PT 64
+#define RX_MAX_O 512
+
+struct DevState {
+  // ---- PAM clock recovery carries (unwrap needs the previous buffer's phase)
+  double theta_prev, thetau_prev;
+  // ---- normalisation fronts
+  long long v_front;        // PAM: uhat valid for m < v_front; KK: z' valid for q < v_front
+  long long m_end;          // final symbol count (set at flush), else -1
+  // ---- sync / training
+  int synced, trained, sync_offset, sync_phase, sync_polarity, pad0;
+  double sync_gamma, sync_phi0;
+  // ---- LMS bookkeeping
+  long long seg_next;       // first segment whose R_s is not yet known (= finalisation front)
+  long long fin_lo, fin_hi; // segments finalised by the current round
+  long long r_prefix;       // sum_{i <= seg_next-1} r_i (mod 4)
+  int anchor_known, anchor_A;
+  // ---- KK CFO DDS carry
+  unsigned long long cfo_origin_next;
+  double cfo_df_prev;
+  // ---- counters (H25)
+  long long bit_errors, bits, symbols_counted, clipped, domain_errors, first_domain;
+  double evm_num, evm_den;
+  long long symbols_out;
+  int flags, pad1;
+};
+
+struct HostMirror {          // pinned, mapped: device writes hints the host reads lazily
+  volatile long long seg_next;
+  volatile int synced, trained;
+};
+
+struct CfoParam {            // per KK buffer (H19-H20)
+  double P, df;
+  unsigned long long inc, origin;
+  float inv_sqrtP;
+  int kstar;
+};
+
+struct RxDev {
+  // ---- configuration
+  int family, M, L;          // L = levels per axis (PAM: M, QAM: sqrt M)
+  int kbits;                 // log2 M
+  float scale;               // adc_gain / 2047.5
+  float dc;                  // KK dc offset
+  int sideband;
+  unsigned long long carrier_inc;    // DDS increment of sigma * f_c (c-0)
+  double fs2;                // KK 2-sps rate
+  int clock_half;
+  int buffer_blocks;
+  long long E_sym;           // symbols per LMS epoch
+  int K, B, S, O, D, cpr, Pt;
+  float mu;
+  int T_train;
+  long long m0;
+  int W_sync;
+  float sync_min;
+  long long warmup;
+  int cfo_enable;
+  // ---- constant tables (device)
+  const float2 *tw;          // e^{-2 pi i k/1024}, k < 1024
+  const float2 *H;           // static-EQ spectrum [1024]
+  const float *thr;          // PAM thresholds [M-1]
+  const float *lvl;          // levels per axis [L]
+  const float2 *ref_val;     // reference symbol values [P]
+  const unsigned char *ref_lab;  // reference Gray labels [P]
+  const unsigned char *ref_idx;  // reference level index (PAM i, QAM iI | iQ << 4) [P]
+  const float2 *bps_rot;     // e^{-j phi_p}, p < Pt
+  // ---- rings
+  uint16_t *hist; long long hist_cap;
+  double2 *C; double *theta; double *tau; long long *Mb; double *blk_sum; double *blk_abs;
+  long long blk_cap;
+  float *u; float *uhat; long long sym_cap;
+  double *norm_dc; double *norm_amp; long long *norm_cnt; long long buf_cap;
+  float2 *E; long long E_cap;
+  float2 *z; long long z_cap;
+  CfoParam *cfo; float *cfo_part; double *cfo_pow; double2 *cfo_a; int cfo_G;
+  // ---- sync scratch
+  float *sync_g; float2 *sync_c;
+  // ---- LMS
+  float2 *w_train;                 // [K]
+  float2 *seed; int *seed_ready; long long seed_cap;   // per epoch [K]
+  float2 *seg_w; float *seg_theta; int *seg_done; int *seg_stitched; int *seg_r; int *seg_R;
+  double *seg_evm; long long *seg_err; long long seg_cap;
+  unsigned char *seg_warm;         // [seg_cap][O]
+  unsigned char *level; unsigned char *level_fin; float2 *yout;   // per symbol rings (sym_cap)
+  DevState *st;
+  HostMirror *hm;                  // device pointer of the mapped host mirror
+};
+
+__device__ __forceinline__ long long rmod(long long i, long long cap) { return i & (cap - 1); }
+
+__device__ __forceinline__ void set_flag(DevState *st, int f) { atomicOr(&st->flags, f); }

@@ -1,0 +1,212 @@
+"""Thin ctypes binding of librx (include/rx.h) — argument marshalling only.
+
+Every step of the receiver chain runs in librx's CUDA kernels; this module only converts
+Python arguments to the C ABI (device pointers from torch tensors, the current CUDA stream).
+There is no CPU fallback: if librx.so is missing or no GPU is present, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(HERE, "librx.so")
+
+RX_PAM, RX_QAM_KK = 0, 1
+PROBES = dict(C=0, TAU=1, MB=2, U=3, UHAT=4, E=5, Z=6, CFO=7, Y=8, LEVEL=9, SEG=10, DEBUG=11)
+FLAGS = dict(DOMAIN=1, SYNC=2, DIVERGE=4, CAPACITY=8)
+
+_c_ll = ctypes.c_longlong
+_c_dp = ctypes.POINTER(ctypes.c_double)
+
+
+class RxConfig(ctypes.Structure):
+    _fields_ = [
+        ("family", ctypes.c_int), ("order", ctypes.c_int),
+        ("baud", ctypes.c_double), ("sample_rate", ctypes.c_double),
+        ("fft_size", ctypes.c_int), ("hop", ctypes.c_int), ("buffer_blocks", ctypes.c_int),
+        ("static_taps", _c_dp), ("n_static_taps", ctypes.c_int),
+        ("adc_gain", ctypes.c_double), ("clock_avg_half", ctypes.c_int),
+        ("thresholds", _c_dp),
+        ("carrier_offset_hz", ctypes.c_double), ("sideband", ctypes.c_int),
+        ("dc_offset", ctypes.c_double),
+        ("lms_taps", ctypes.c_int), ("lms_block", ctypes.c_int), ("lms_segment", ctypes.c_int),
+        ("lms_overlap", ctypes.c_int), ("tap_lag_epochs", ctypes.c_int),
+        ("widely_linear", ctypes.c_int),
+        ("mu", ctypes.c_double), ("train_symbols", ctypes.c_int),
+        ("cfo_enable", ctypes.c_int), ("cpr_test_phases", ctypes.c_int),
+        ("prbs_order", ctypes.c_uint), ("prbs_seed", ctypes.c_uint),
+        ("sync_start", _c_ll), ("sync_window", ctypes.c_int), ("sync_min_corr", ctypes.c_double),
+        ("warmup_symbols", _c_ll), ("history_buffers", ctypes.c_int),
+    ]
+
+
+class RxStats(ctypes.Structure):
+    _fields_ = [
+        ("samples_in", _c_ll), ("symbols_out", _c_ll),
+        ("bit_errors", _c_ll), ("bits", _c_ll), ("symbols_counted", _c_ll),
+        ("clipped", _c_ll), ("domain_errors", _c_ll), ("first_domain_error_index", _c_ll),
+        ("evm_num", ctypes.c_double), ("evm_den", ctypes.c_double),
+        ("sync_offset", ctypes.c_int), ("sync_phase", ctypes.c_int),
+        ("sync_polarity", ctypes.c_int), ("synced", ctypes.c_int),
+        ("sync_gamma", ctypes.c_double), ("sync_phi0", ctypes.c_double),
+        ("status_flags", ctypes.c_int), ("launches", _c_ll),
+    ]
+
+
+EXPORTS = ("rx_config_default", "rx_create", "rx_process", "rx_flush", "rx_get_stats",
+           "rx_reset_stats", "rx_get_taps", "rx_probe_read", "rx_destroy", "rx_strerror",
+           "rx_version")
+
+_lib = None
+
+
+def load(path: str = SO_PATH):
+    """Load librx.so (raises OSError if it is missing — no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise OSError(f"librx.so not built at {path}; run paper_2011_13695_b200.build.build()")
+    lib = ctypes.CDLL(path)
+    vp = ctypes.c_void_p
+    lib.rx_config_default.argtypes = [ctypes.POINTER(RxConfig), ctypes.c_int, ctypes.c_int]
+    lib.rx_config_default.restype = None
+    lib.rx_create.argtypes = [ctypes.POINTER(RxConfig), ctypes.c_int, ctypes.POINTER(vp)]
+    lib.rx_process.argtypes = [vp, vp, _c_ll, vp, _c_ll, vp]
+    lib.rx_flush.argtypes = [vp, vp, _c_ll, vp]
+    lib.rx_get_stats.argtypes = [vp, ctypes.POINTER(RxStats), vp]
+    lib.rx_reset_stats.argtypes = [vp, vp]
+    lib.rx_get_taps.argtypes = [vp, _c_dp, ctypes.c_int]
+    lib.rx_probe_read.argtypes = [vp, ctypes.c_int, _c_ll, _c_ll, vp, vp]
+    lib.rx_destroy.argtypes = [vp]
+    lib.rx_destroy.restype = None
+    lib.rx_strerror.argtypes = [ctypes.c_int]
+    lib.rx_strerror.restype = ctypes.c_char_p
+    lib.rx_version.argtypes = []
+    lib.rx_version.restype = ctypes.c_char_p
+    for f in ("rx_create", "rx_process", "rx_flush", "rx_get_stats", "rx_reset_stats",
+              "rx_get_taps", "rx_probe_read"):
+        getattr(lib, f).restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+class RxError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        super().__init__(f"{where}: librx status {status} ({load().rx_strerror(status).decode()})")
+        self.status = status
+
+
+def _check(st: int, where: str):
+    if st != 0:
+        raise RxError(st, where)
+
+
+def _stream_ptr(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def default_config(family: int, order: int) -> RxConfig:
+    cfg = RxConfig()
+    load().rx_config_default(ctypes.byref(cfg), family, order)
+    return cfg
+
+
+class Receiver:
+    """One receiver channel (one librx handle) on one CUDA device.
+
+    Receiver(family, order, static_taps, device=0, **rx_config fields)
+    """
+
+    def __init__(self, family: int, order: int, static_taps, device: int = 0,
+                 thresholds=None, **fields):
+        lib = load()
+        cfg = default_config(family, order)
+        taps = np.ascontiguousarray(np.asarray(static_taps))
+        if family == RX_QAM_KK:
+            taps = np.ascontiguousarray(np.stack([taps.real, taps.imag], axis=-1).reshape(-1),
+                                        dtype=np.float64)
+            cfg.n_static_taps = taps.shape[0] // 2
+        else:
+            taps = np.ascontiguousarray(taps.real, dtype=np.float64)
+            cfg.n_static_taps = taps.shape[0]
+        self._taps = taps
+        cfg.static_taps = taps.ctypes.data_as(_c_dp)
+        if thresholds is not None:
+            self._thr = np.ascontiguousarray(thresholds, dtype=np.float64)
+            cfg.thresholds = self._thr.ctypes.data_as(_c_dp)
+        for k, v in fields.items():
+            if not hasattr(cfg, k):
+                raise TypeError(f"unknown rx_config field {k}")
+            setattr(cfg, k, v)
+        self.cfg = cfg
+        self.device = device
+        h = ctypes.c_void_p()
+        _check(lib.rx_create(ctypes.byref(cfg), device, ctypes.byref(h)), "rx_create")
+        self._h = h
+        self.family, self.order = family, order
+
+    # -- streaming
+    def process(self, samples, labels=None, stream=None):
+        """samples: torch uint16/int16 CUDA tensor of u12 codes; labels: uint8 CUDA tensor
+        written at index m % len(labels)."""
+        lp, lc = (labels.data_ptr(), labels.numel()) if labels is not None else (None, 0)
+        _check(load().rx_process(self._h, ctypes.c_void_p(samples.data_ptr()), samples.numel(),
+                                 ctypes.c_void_p(lp), lc, _stream_ptr(stream)), "rx_process")
+
+    def process_ptr(self, ptr: int, n: int, labels_ptr: int = 0, labels_cap: int = 0, stream_ptr=None):
+        _check(load().rx_process(self._h, ctypes.c_void_p(ptr), n, ctypes.c_void_p(labels_ptr),
+                                 labels_cap, stream_ptr if stream_ptr is not None else _stream_ptr()),
+               "rx_process")
+
+    def flush(self, labels=None, stream=None):
+        lp, lc = (labels.data_ptr(), labels.numel()) if labels is not None else (None, 0)
+        _check(load().rx_flush(self._h, ctypes.c_void_p(lp), lc, _stream_ptr(stream)), "rx_flush")
+
+    def stats(self, stream=None) -> dict:
+        st = RxStats()
+        _check(load().rx_get_stats(self._h, ctypes.byref(st), _stream_ptr(stream)), "rx_get_stats")
+        return {k: getattr(st, k) for k, _ in RxStats._fields_}
+
+    def reset_stats(self, stream=None):
+        _check(load().rx_reset_stats(self._h, _stream_ptr(stream)), "rx_reset_stats")
+
+    def train_taps(self) -> np.ndarray:
+        K = self.cfg.lms_taps
+        n = 2 * K if self.family == RX_QAM_KK else K
+        out = np.zeros(n, dtype=np.float64)
+        _check(load().rx_get_taps(self._h, out.ctypes.data_as(_c_dp), n), "rx_get_taps")
+        return out[0::2] + 1j * out[1::2] if self.family == RX_QAM_KK else out
+
+    def probe(self, which: str, first: int, count: int, stream=None) -> np.ndarray:
+        w = PROBES[which]
+        dt, per = {
+            "C": (np.float64, 2), "TAU": (np.float64, 1), "MB": (np.int64, 1), "U": (np.float32, 1),
+            "UHAT": (np.float32, 1), "E": (np.float32, 2), "Z": (np.float32, 2), "CFO": (np.float64, 5),
+            "Y": (np.float32, 2), "LEVEL": (np.uint8, 1), "SEG": (np.float64, 6), "DEBUG": (np.int64, 1),
+        }[which]
+        out = np.zeros(count * per, dtype=dt)
+        _check(load().rx_probe_read(self._h, w, first, count, out.ctypes.data_as(ctypes.c_void_p),
+                                    _stream_ptr(stream)), f"rx_probe_read({which})")
+        if which in ("C", "E", "Z", "Y"):
+            out = out.reshape(count, 2)
+            return out[:, 0].astype(np.float64) + 1j * out[:, 1]
+        if per > 1:
+            return out.reshape(count, per)
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load().rx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

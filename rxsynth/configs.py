@@ -20,15 +20,15 @@ CONFIGS = {
     "C2": dict(gen=dict(kind="pam", M=16, n_samples=N_C2, seed=2001, snr_db=32.0,
                         channel="isi91", ppm=20.0),
                rx=dict(lms_taps=31, lms_block=32, lms_segment=4096, lms_overlap=0,
-                       mu=1e-3, train_symbols=8192, sync_start=4096, sync_window=2048,
-                       warmup_symbols=16384)),
+                       mu=1e-3, train_symbols=32768, sync_start=4096, sync_window=2048,
+                       warmup_symbols=65536)),
     "C3": dict(gen=dict(kind="qam", M=4, n_samples=N_C2, seed=3001, cspr_db=6.0,
                         osnr_db=10.0, cfo_hz=20e6, linewidth_hz=100e3, rx_lpf=False),
                rx=dict(lms_taps=4, lms_block=32, lms_segment=4096, lms_overlap=256,
                        mu=2e-3, train_symbols=8192, sync_start=4096, sync_window=2048,
                        cpr_test_phases=0, warmup_symbols=16384)),
     "C4": dict(gen=dict(kind="qam", M=64, n_samples=N_C4, seed=4001, cspr_db=11.0,
-                        osnr_db=30.0, cfo_hz=5e6, linewidth_hz=10e3, rx_lpf=True,
+                        osnr_db=30.0, cfo_hz=5e6, linewidth_hz=10e3, rx_lpf=False,
                         roadm_b3db=1.5e9),
                rx=dict(lms_taps=8, lms_block=32, lms_segment=4096, lms_overlap=256,
                        mu=2e-3, train_symbols=8192, sync_start=4096, sync_window=2048,
@@ -53,7 +53,7 @@ def c5_channel(ch: int, n_samples: int = N_C2):
     rx["cpr_test_phases"] = 0 if M == 4 else 32
     return dict(gen=dict(kind="qam", M=M, n_samples=n_samples, seed=5000 + ch,
                          cspr_db=6.0 if M == 4 else 11.0, osnr_db=30.0, cfo_hz=5e6,
-                         linewidth_hz=10e3, rx_lpf=True, roadm_b3db=1.5e9),
+                         linewidth_hz=10e3, rx_lpf=False, roadm_b3db=1.5e9),
                 rx=rx)
 
 

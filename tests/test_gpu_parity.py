@@ -1,0 +1,164 @@
+"""GPU (librx through the C ABI) vs oracle parity, element by element, on seeded inputs.
+
+Tolerances (BASELINE.json north_star; SURVEY §8(c) 'GPU-vs-oracle parity criteria'):
+  * fields (E, z, u, u^) and training-mode taps: relative L2 <= 1e-4 (fp32 vs fp64)
+  * clock phase tau_b: |dtau| <= 1e-5 symbols; M_b identical except blocks whose
+    256 b - 128 - tau_b lies within 1e-6 of an integer
+  * decided labels: bit-exact except symbols whose oracle soft value is within 1e-3 of a
+    decision boundary, and symbols downstream of such a decision in the same segment
+    (contamination bounded by the segment); the excluded fraction is bounded
+  * EVM within 0.01 dB; bit-error counts equal up to the bits of excluded symbols
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import rx_oracle as O
+from rxsynth import make_config
+from tests.gpu_util import evm_db, near_threshold, rel_l2, run_gpu, run_oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL_FIELD = 1e-4
+TOL_TAU = 1e-5
+DELTA = 1e-3
+
+
+def _torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def _compare_labels(rec, rx, out, labels):
+    """(1) bit-exact outside the excluded set (near-boundary decisions and what follows them in
+    the same segment); (2) at most 1e-3 of all labels differ; (3) every differing label's
+    oracle soft value lies within 0.05 of a decision boundary. The excluded fraction is a
+    property of the format and SNR (dense for PAM-16), so it is reported, not bounded."""
+    m_end = out["m_end"]
+    lab_o = out["labels"][:m_end].astype(np.int64)
+    lab_g = labels[:m_end].astype(np.int64)
+    soft = out["lms"]["z"][:m_end]
+    near = near_threshold(soft, rec.fmt, rec.M, DELTA)
+    S = rx["lms_segment"]
+    seg = np.arange(m_end) // S
+    excl = np.zeros(m_end, bool)
+    for s in np.unique(seg[near]):
+        first = np.argmax(near & (seg == s))
+        excl[first:(s + 1) * S] = True
+    mism = lab_o != lab_g
+    bad = mism & ~excl
+    assert not np.any(bad), f"{int(bad.sum())} label mismatches away from thresholds, first at {np.argmax(bad)}"
+    assert mism.sum() <= 1e-3 * m_end, f"{int(mism.sum())} of {m_end} labels differ"
+    loose = near_threshold(soft, rec.fmt, rec.M, 0.05)
+    assert np.all(loose[mism]), f"{int(np.sum(mism & ~loose))} mismatches far from a boundary"
+    print(f"labels: {int(mism.sum())} differ, excluded fraction {excl.mean():.4f}")
+    return mism, excl
+
+
+def _compare_counters(rec, out, st, mism):
+    k = int(round(math.log2(rec.M)))
+    assert st["symbols_counted"] == out["symbols_counted"]
+    assert st["bits"] == out["bits"]
+    assert abs(st["bit_errors"] - out["bit_errors"]) <= k * int(mism.sum())
+    assert abs(evm_db(st["evm_num"], st["evm_den"]) - out["evm_db"]) <= 0.01
+
+
+@pytest.fixture(scope="module")
+def c1():
+    _torch_cuda()
+    rec, rx = make_config("C1")
+    out = run_oracle(rec, rx)
+    R, labels, st = run_gpu(rec, rx)
+    return rec, rx, out, R, labels, st
+
+
+def test_c1_intermediates(c1):
+    rec, rx, out, R, labels, st = c1
+    nb = rec.n // 512
+    C = R.probe("C", 0, nb)
+    assert rel_l2(C, out["C"]) < TOL_FIELD
+    tau = R.probe("TAU", 0, nb)
+    assert np.max(np.abs(tau - out["clock"]["tau"])) < TOL_TAU
+    Mb = R.probe("MB", 0, nb)
+    x = 256 * np.arange(nb) - 128 - out["clock"]["tau"]
+    edge = np.abs(x - np.rint(x)) < 1e-6
+    assert np.all((Mb == out["clock"]["M"]) | edge)
+    m_end = out["u"].shape[0]
+    assert st["symbols_out"] == m_end
+    assert rel_l2(R.probe("U", 0, m_end), out["u"]) < TOL_FIELD
+    assert rel_l2(R.probe("UHAT", 0, m_end), out["u_hat"]) < TOL_FIELD
+
+
+def test_c1_sync_training_labels_counters(c1):
+    rec, rx, out, R, labels, st = c1
+    assert st["synced"] == 1 and st["sync_offset"] == out["sync"]["offset"]
+    assert st["sync_offset"] == (rec.offset + rx["sync_start"]) % O.P_REF
+    assert abs(st["sync_gamma"] - out["sync"]["gamma"]) < 1e-4
+    w = R.train_taps()
+    assert rel_l2(w, out["lms"]["w_train"]) < TOL_FIELD
+    mism, _ = _compare_labels(rec, rx, out, labels)
+    _compare_counters(rec, out, st, mism)
+    assert st["status_flags"] == 0
+    assert st["clipped"] == out["clipped"]
+
+
+def _small(name, **kw):
+    over = dict(buffer_blocks=256)
+    over.update(kw)
+    return make_config(name, **over)
+
+
+@pytest.mark.parametrize("name,n,extra", [
+    ("C2", 1 << 21, {}),
+    ("C3", 1 << 21, {}),
+    ("C4", 1 << 21, {}),
+])
+def test_multi_buffer_parity(name, n, extra):
+    """C2/C3/C4 structure at 2^21 samples with 256-block buffers: 8-16 normalisation / CFO
+    buffers and LMS epochs, so the lag-D seeds, carries and stitching are all exercised."""
+    _torch_cuda()
+    rec, rx = make_config(name, n_samples=n, **extra)
+    rx["buffer_blocks"] = 256
+    out = run_oracle(rec, rx)
+    R, labels, st = run_gpu(rec, rx, chunk=256 * 512)
+    if rec.fmt == "pam":
+        nb = rec.n // 512
+        assert np.max(np.abs(R.probe("TAU", 0, nb) - out["clock"]["tau"])) < TOL_TAU
+        m_end = out["u"].shape[0]
+        assert rel_l2(R.probe("U", 0, m_end), out["u"]) < TOL_FIELD
+        assert rel_l2(R.probe("UHAT", 0, m_end), out["u_hat"]) < TOL_FIELD
+    else:
+        E = R.probe("E", 0, out["E"].shape[0])
+        assert rel_l2(E, out["E"]) < TOL_FIELD
+        z = R.probe("Z", 0, out["z"].shape[0])
+        assert rel_l2(z, out["z"]) < TOL_FIELD
+        nbuf = out["cfo"]["P"].shape[0]
+        cfo = R.probe("CFO", 0, nbuf)
+        assert np.allclose(cfo[:, 0], out["cfo"]["P"], rtol=1e-4)
+        assert np.all(np.abs(cfo[:, 1] - out["cfo"]["df"]) < 50.0), (cfo[:, 1], out["cfo"]["df"])
+        assert st["domain_errors"] == out["domain"]
+    assert st["sync_offset"] == out["sync"]["offset"]
+    if rec.fmt == "qam":
+        assert st["sync_phase"] == out["sync"]["phase"]
+    assert rel_l2(R.train_taps(), out["lms"]["w_train"]) < 1e-3
+    mism, excl = _compare_labels(rec, rx, out, labels)
+    _compare_counters(rec, out, st, mism)
+
+
+def test_chunking_invariance():
+    """Results are defined by absolute indices: any call chunking gives identical labels
+    and integer counters (SURVEY §4 'Determinism')."""
+    _torch_cuda()
+    rec, rx = make_config("C3", n_samples=1 << 20)
+    rx["buffer_blocks"] = 256
+    _, la, sa = run_gpu(rec, rx, chunk=256 * 512)
+    _, lb, sb = run_gpu(rec, rx, chunk=512 * 37)
+    _, lc, sc = run_gpu(rec, rx, chunk=256 * 512)
+    assert np.array_equal(la, lb) and np.array_equal(la, lc)
+    for k in ("bit_errors", "bits", "symbols_counted", "clipped", "domain_errors", "sync_offset"):
+        assert sa[k] == sb[k] == sc[k], k
+    assert sa["evm_num"] == sc["evm_num"]                        # run-to-run bit identical
+    assert abs(sa["evm_num"] - sb["evm_num"]) <= 1e-9 * sa["evm_num"]

@@ -215,7 +215,8 @@ def test_stitching_resolves_forced_segment_quadrants():
 @pytest.mark.parametrize("df", [0.0, 5e6, -20e6, 20e6, 37.3e6])
 def test_cfo_estimate_closed_form(df):
     """c-8: noiseless RRC(0.01) QAM at 2 sps with a frequency offset
-    -> |df^ - df| <= 0.1 MHz; the corrected stream has no residual rotation drift."""
+    -> |df^ - df| <= 2 kHz (coarse periodogram + fine phase-increment stage); the corrected
+    stream has no residual rotation drift."""
     rng = np.random.default_rng(5)
     nsym = 1 << 17
     s, _ = _qam_stream(16, nsym, rng)
@@ -226,7 +227,7 @@ def test_cfo_estimate_closed_form(df):
     q = np.arange(2 * nsym)
     z = 3.0 * z * np.exp(2j * math.pi * df / 2e9 * q)
     zc, info = O.kk_norm_cfo(z, 2e9, buffer_len=1 << 18)
-    assert np.all(np.abs(info["df"] - df) < 0.1e6)
+    assert np.all(np.abs(info["df"] - df) < 2e3), info["df"] - df
     assert abs(np.mean(np.abs(zc[: 1 << 18]) ** 2) - 1) < 1e-12
     # after removal the 4th-power line sits at DC
     blk = zc[:1 << 16].reshape(-1, 1024) ** 4
@@ -300,3 +301,23 @@ def test_c1_ber_matches_closed_form():
     n = out["bits"]
     sd = math.sqrt(exact * n)
     assert exact * n - 3 * sd <= out["bit_errors"] <= 1.25 * exact * n + 3 * sd
+
+
+def test_lag_d_seeded_epochs_survive_carrier_phase_noise():
+    """Epochs >= D start from the mean canonical taps of epoch e-D. With carrier phase
+    noise the absolute frame drifts across an epoch, so the canonical taps are phase-
+    normalised before averaging (DESIGN.md R-SEED): seeded epochs must decode as well as the
+    W_train-seeded ones."""
+    rec = gen.kk_record(16, 1 << 19, seed=77, cspr_db=12.0, osnr_db=26.0, cfo_hz=3e6,
+                        linewidth_hz=50e3)
+    rx = dict(lms_taps=8, lms_overlap=256, mu=2e-3, train_symbols=8192, warmup_symbols=0,
+              cpr_test_phases=32, buffer_blocks=64, tap_lag_epochs=4)
+    out = O.receive_kk(rec.codes, _params(rec, rx))
+    lm = out["lms"]
+    _, idx_ref, _ = O.reference("qam", 16)
+    m = np.arange(out["m_end"])
+    ok = np.all(lm["idx"] == idx_ref[(out["sync"]["offset"] + m - 4096) % O.P_REF], axis=1)
+    E = 64 * 128
+    early = 1 - ok[E:4 * E].mean()                      # W_train-seeded epochs 1..3
+    late = 1 - ok[4 * E:(out["m_end"] // E) * E].mean()  # lag-D seeded epochs
+    assert early < 0.01 and late < 2 * early + 2e-3, (early, late)
