@@ -1,0 +1,414 @@
+#!/usr/bin/env python
+"""bench.py — received Gsample/s through the full receiver DSP chain (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl gpu|reference] [--no-kk]
+
+Workload (BASELINE.json configs[1] = SURVEY C2): 2 GBaud PAM-16, 2 sps, 91 km-like ISI,
++20 ppm clock offset, SNR 32 dB, 503-tap static EQ, 31-tap block-LMS, PRBS-15 BER tester.
+One step = one C2 record (16,776,704 samples = "2^24") streamed through rx_process in
+buffer-sized calls (2^22 samples), i.e. one pass of every PAM row of SURVEY §8(a).
+Inputs come from a >= 1 GiB device ring (larger than the 126 MB L2) that continues the
+seeded record seamlessly, so every step reads fresh samples from HBM.
+
+Multi-GPU (torchrun, one rank per GPU): every rank runs its own independent channel (weak
+scaling); once per step the packed BER/EVM counters are all-reduced over NCCL.
+Timing: W warm-up steps, then K steps bracketed by barrier + synchronize, CUDA events on the
+processing stream, max over ranks. The KK-QAM mode (C4, 64-QAM, 2^26 samples) is measured the
+same way at N = 1 and reported under "kk".
+
+--impl reference times the fp64 CPU oracle (oracle/) on the host on a bounded sample of the
+same workload (one 2^22-sample buffer per step); under torchrun only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "received Gsample/s through full Rx DSP chain at 1/2/4/8 B200; % HBM roofline"
+PAPER_REALTIME_GSA = 4.0          # 12-bit 4 GSa/s real-time (unnamed GPU)
+CHUNK = 1 << 22                   # one paper buffer per rx_process call
+SM_COUNT, FP32_LANES = 148, 128   # B200 (B200_PROFILING.md); FP32 FMA = 2 flop
+
+# Algorithmic flops per unit (complex N-point FFT = 5 N log2 N, half for
+# real-input / real-output; bin products 6 flop; C_b 8 flop/bin; block-LMS 4K flop per real
+# T-spaced symbol, 16K per complex T/2 symbol + BPS 17 flop per test phase).
+FFT_R1024 = 2.5 * 1024 * 10
+FLOPS_PER_UNIT = {
+    "PAM_FE": FFT_R1024 + 513 * 6 + 512 * 8,               # per block
+    "PAM_BE": 2 * FFT_R1024 + 2 * 513 * 6,                 # per block
+    "KK_S1": 2 * FFT_R1024 + 512 * 20,                     # per block
+    "KK_S2": 5 * 1024 * 10 + 512 * 6 + 5 * 512 * 9,        # per block
+}
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# ------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 9 for i in range(4)
+                          if r[5 + i].lower() == "active"})
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------------ helpers
+def rx_fields(rx: dict) -> dict:
+    keys = ("lms_taps", "lms_block", "lms_segment", "lms_overlap", "mu", "train_symbols",
+            "sync_start", "sync_window", "warmup_symbols", "cpr_test_phases")
+    return {k: v for k, v in rx.items() if k in keys}
+
+
+def cpu_oracle_rate(rec, rx, n_samples: int):
+    """Time the fp64 oracle, as it stands, on the first n_samples of the record (1 thread)."""
+    from threadpoolctl import threadpool_limits
+    from oracle import rx_oracle as O
+    from tests.gpu_util import oracle_params
+    codes = rec.codes[:n_samples]
+    p = oracle_params(rec, rx)
+    with threadpool_limits(1):
+        t0 = time.perf_counter()
+        out = O.receive_pam(codes, p) if rec.fmt == "pam" else O.receive_kk(codes, p)
+        dt = time.perf_counter() - t0
+    return n_samples / dt / 1e9, dt, out
+
+
+class Stream1:
+    """One channel: a Receiver fed from a device ring in buffer-sized calls."""
+
+    def __init__(self, R, ring, n_step, labels, stream):
+        self.R, self.ring, self.n_step, self.labels, self.stream = R, ring, n_step, labels, stream
+        self.nsteps_ring = ring.numel() // n_step
+        self.k = 0
+        import ctypes
+        self.sp = ctypes.c_void_p(stream.cuda_stream)
+
+    def step(self):
+        base = (self.k % self.nsteps_ring) * self.n_step
+        ptr = self.ring.data_ptr() + 2 * base
+        for off in range(0, self.n_step, CHUNK):
+            n = min(CHUNK, self.n_step - off)
+            self.R.process_ptr(ptr + 2 * off, n, self.labels.data_ptr(), self.labels.numel(), self.sp)
+        self.k += 1
+
+
+def run_mode(torch, dist, R, ring, n_step, steps, warmup, world, dev, units, label_cap=1 << 24,
+             with_profile=True):
+    """Warm up, profile the kernel classes (untimed), then time `steps` steps."""
+    stream = torch.cuda.Stream(device=dev)
+    labels = torch.zeros(label_cap, dtype=torch.uint8, device=dev)
+    cnt = torch.zeros(8, dtype=torch.float64, device=dev)
+    ch = Stream1(R, ring, n_step, labels, stream)
+
+    def one_step():
+        ch.step()
+        R.export_counters(cnt, stream=stream)
+        if world > 1:
+            with torch.cuda.stream(stream):
+                dist.all_reduce(cnt)
+
+    for _ in range(warmup):
+        one_step()
+    torch.cuda.synchronize(dev)
+    breakdown, dominant = {}, None
+    if with_profile:
+        R.profile_enable()
+        for _ in range(2):
+            one_step()
+        prof = R.profile_read()
+        R.profile_enable(())
+        breakdown = {k: round(v[0] / 2, 4) for k, v in prof.items()}
+        dominant = max(breakdown, key=breakdown.get)
+        R.profile_enable((dominant,))
+    st0 = R.stats(stream)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(dev.index if dev.index is not None else 0)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        one_step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    st1 = R.stats(stream)
+    dom = None
+    if with_profile and dominant:
+        prof = R.profile_read()
+        R.profile_enable(())
+        if dominant in prof:
+            dom = dict(name=dominant, ms=prof[dominant][0], launches=prof[dominant][1])
+    return dict(ms=ms_max, clocks=clk, breakdown=breakdown, dominant=dom,
+                launches=st1["launches"] - st0["launches"], stats=st1, counters=cnt.cpu().tolist())
+
+
+def e2e_run(torch, R, n_step, host_codes, steps, dev):
+    """Same metric end to end through the public API: pinned host input -> H2D -> rx_process
+    calls -> D2H of the step's labels, all inside the timed region (one stream)."""
+    import ctypes
+    stream = torch.cuda.Stream(device=dev)
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    pinned_in = torch.from_numpy(host_codes[:n_step].view("int16")).pin_memory()
+    dbuf = torch.empty(n_step, dtype=torch.int16, device=dev)
+    labels = torch.zeros(1 << 24, dtype=torch.uint8, device=dev)
+    nlab = n_step // 2
+    pinned_out = torch.empty(nlab, dtype=torch.uint8).pin_memory()
+    cnt = torch.zeros(8, dtype=torch.float64, device=dev)
+    cnt_host = torch.empty(8, dtype=torch.float64).pin_memory()
+
+    def one():
+        with torch.cuda.stream(stream):
+            dbuf.copy_(pinned_in, non_blocking=True)
+        for off in range(0, n_step, CHUNK):
+            n = min(CHUNK, n_step - off)
+            R.process_ptr(dbuf.data_ptr() + 2 * off, n, labels.data_ptr(), labels.numel(), sp)
+        R.export_counters(cnt, stream=stream)
+        with torch.cuda.stream(stream):
+            pinned_out.copy_(labels[:nlab], non_blocking=True)
+            cnt_host.copy_(cnt, non_blocking=True)
+
+    one()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        one()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    return dict(ms=ms, h2d=2 * n_step, d2h=nlab + 8 * 8)
+
+
+# ------------------------------------------------------------------------ GPU arm
+def gpu_main(args):
+    import numpy as np
+    import torch
+    rank, world, local = env_rank()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    from paper_2011_13695_b200 import RX_PAM, RX_QAM_KK, Receiver, build
+    build.build()
+    from rxsynth import make_config
+    from rxsynth.configs import N_C2, N_C4
+    from rxsynth.ring import pam_ring, tiled_ring
+
+    # ---- C2 (headline)
+    seed = 2001 + 17 * rank
+    t0 = time.time()
+    rec, rx = make_config("C2", seed=seed, keep_tx=True)
+    t_gen = time.time() - t0
+    n_step = N_C2
+    ring_samples = max(1, int(args.ring_gib * (1 << 30) / 2 // n_step)) * n_step
+    ring = pam_ring(rec, ring_samples, dev, seed=seed)
+    R = Receiver(RX_PAM, rec.M, rec.static_taps, device=local, **rx_fields(rx))
+    res = run_mode(torch, dist, R, ring, n_step, args.steps, args.warmup, world, dev, None)
+    value = world * n_step * args.steps / (res["ms"] / 1e3) / 1e9
+    ms_step = res["ms"] / args.steps
+    st = res["stats"]
+    # roofline of the dominant kernel class, measured live in the timed region
+    roof = None
+    sm_max = res["clocks"].get("sm_max_mhz") or 1965.0
+    peak_fp32 = SM_COUNT * FP32_LANES * 2 * sm_max * 1e6 / 1e12
+    dom = res["dominant"]
+    if dom:
+        name = dom["name"]
+        blocks_per_step = n_step // 512
+        if name in FLOPS_PER_UNIT:
+            flops = FLOPS_PER_UNIT[name] * blocks_per_step * args.steps
+        elif name == "LMS":
+            flops = 4 * rx["lms_taps"] * (n_step // 2) * args.steps
+        else:
+            flops = None
+        achieved = flops / (dom["ms"] / 1e3) / 1e12 if flops else None
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            traffic = json.load(open(tp)).get(name)
+        roof = {"kernel_class": name, "bound": "alu", "achieved": achieved, "peak": peak_fp32,
+                "unit": "TFLOP/s", "frac": (achieved / peak_fp32) if achieved else None,
+                "traffic": traffic, "kernel_ms_per_step": dom["ms"] / args.steps,
+                "share_of_step": dom["ms"] / res["ms"],
+                "peak_note": "FP32 CUDA-core peak = 148 SMs x 128 lanes x 2 flop x max SM clock "
+                             "(guide unit counts; the path is FP32/smem bound, SURVEY §8(d))"}
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GSa/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (rxsynth, seeded C2: PAM-16 2 GBaud 2 sps, 91 km-like ISI, +20 ppm, SNR 32 dB)",
+        "config": {"workload": "C2: PAM-16, 16,776,704 samples/step per GPU, 503-tap static EQ, "
+                               "105-block clock recovery, 31-tap block-LMS, PRBS-15 BER",
+                   "samples_per_step_per_gpu": n_step, "call_size": CHUNK,
+                   "input": f"device ring {ring_samples * 2 / 2**30:.2f} GiB > L2 (fresh samples every step)",
+                   "parallelism": f"{world} independent channel(s), 1 per GPU; NCCL all-reduce of counters per step"},
+        "roofline": roof,
+        "gpu_launches": res["launches"],
+        "clocks": res["clocks"],
+        "breakdown_ms_per_step": res["breakdown"],
+        "hbm_roofline_frac_literal": round(value * 1e9 / world * 2.5 / 6537e9, 5),
+        "x_paper_realtime": round(value / world / PAPER_REALTIME_GSA, 2),
+        "quality": {"ber": st["bit_errors"] / max(st["bits"], 1),
+                    "evm_db": 10 * math.log10(st["evm_num"] / st["evm_den"]) if st["evm_den"] > 0 else None,
+                    "sync_gamma": st["sync_gamma"], "flags": st["status_flags"]},
+        "gen_seconds": round(t_gen, 1),
+    }
+    # ---- e2e through the public API with host buffers
+    e2e = e2e_run(torch, R, n_step, rec.codes, max(3, args.steps // 2), dev)
+    e_ms = torch.tensor([e2e["ms"]], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+    e_steps = max(3, args.steps // 2)
+    line["e2e"] = {"value": round(world * n_step * e_steps / (float(e_ms.item()) / 1e3) / 1e9, 3),
+                   "unit": "GSa/s", "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"]}
+    R.close()
+    del ring
+    torch.cuda.empty_cache()
+    # ---- CPU oracle baseline (rank 0, N = 1)
+    if world == 1 and not args.no_cpu:
+        v, dt, _ = cpu_oracle_rate(rec, rx, rec.n)
+        line["cpu_baseline"] = {"value": round(v, 6), "unit": "GSa/s", "cores": 1, "kind": "oracle",
+                                "sample": f"one full C2 record ({rec.n} samples, one GPU step), fp64 "
+                                          f"numpy oracle, 1 thread, {dt:.1f} s"}
+    else:
+        line["cpu_baseline"] = None
+    # ---- KK-QAM mode (C4) at N = 1
+    if world == 1 and not args.no_kk:
+        rec4, rx4 = make_config("C4")
+        ring4 = tiled_ring(rec4, max(1, int(args.ring_gib * (1 << 30) / 2 // N_C4)) * N_C4, dev)
+        R4 = Receiver(RX_QAM_KK, rec4.M, rec4.static_taps, device=local, dc_offset=rec4.dc_offset,
+                      **rx_fields(rx4))
+        r4 = run_mode(torch, None, R4, ring4, N_C4, args.kk_steps, 2, 1, dev, None)
+        s4 = r4["stats"]
+        v4 = N_C4 * args.kk_steps / (r4["ms"] / 1e3) / 1e9
+        dom4 = r4["dominant"]
+        kk_roof = None
+        if dom4 and dom4["name"] in FLOPS_PER_UNIT:
+            a4 = FLOPS_PER_UNIT[dom4["name"]] * (N_C4 // 512) * args.kk_steps / (dom4["ms"] / 1e3) / 1e12
+            kk_roof = {"kernel_class": dom4["name"], "bound": "alu", "achieved": a4, "peak": peak_fp32,
+                       "unit": "TFLOP/s", "frac": a4 / peak_fp32, "share_of_step": dom4["ms"] / r4["ms"]}
+        elif dom4:
+            kk_roof = {"kernel_class": dom4["name"], "share_of_step": dom4["ms"] / r4["ms"]}
+        line["kk"] = {"workload": "C4: KK 64-QAM 1 GBaud 4 sps, 67,106,816 samples/step, CSPR 11 dB, "
+                                  "ROADM-filtered, 10 kHz phase noise, 5 MHz CFO, BPS-32 CPR, 8-tap T/2 LMS",
+                      "value": round(v4, 3), "unit": "GSa/s", "steps": args.kk_steps,
+                      "ms_per_step": round(r4["ms"] / args.kk_steps, 4),
+                      "breakdown_ms_per_step": r4["breakdown"], "roofline": kk_roof,
+                      "gpu_launches": r4["launches"], "clocks": r4["clocks"],
+                      "quality": {"ber": s4["bit_errors"] / max(s4["bits"], 1),
+                                  "evm_db": 10 * math.log10(s4["evm_num"] / s4["evm_den"]) if s4["evm_den"] > 0 else None}}
+        line["gpu_launches"] += r4["launches"]
+        R4.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------------ reference arm
+def reference_main(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    from rxsynth import make_config
+    rec, rx = make_config("C2", seed=2001)
+    n = CHUNK
+    for _ in range(args.warmup):
+        cpu_oracle_rate(rec, rx, n)
+    t = 0.0
+    for _ in range(args.steps):
+        _, dt, _ = cpu_oracle_rate(rec, rx, n)
+        t += dt
+    v = args.steps * n / t / 1e9
+    sample = f"first {n} samples (one 2^22 buffer, P:116) of the C2 record per step, fp64 numpy oracle, 1 thread"
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "GSa/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * t / args.steps, 2),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (rxsynth, seeded C2)",
+            "config": {"workload": "C2: PAM-16 (bounded sample)", "samples_per_step": n},
+            "cpu_baseline": {"value": round(v, 6), "unit": "GSa/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": round(v, 6), "unit": "GSa/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("gpu", "reference"), default="gpu")
+    ap.add_argument("--no-kk", action="store_true")
+    ap.add_argument("--kk-steps", type=int, default=3)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ring-gib", type=float, default=1.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        reference_main(args)
+    else:
+        gpu_main(args)
+
+
+if __name__ == "__main__":
+    main()

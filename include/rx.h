@@ -138,6 +138,13 @@ rx_status rx_flush(rx_handle *h, unsigned char *d_labels, long long labels_capac
 /* Synchronise `cuda_stream`, copy a snapshot of the cumulative counters to host_out. */
 rx_status rx_get_stats(rx_handle *h, rx_stats *host_out, void *cuda_stream);
 
+/* Enqueue on cuda_stream a copy of the cumulative counters into device memory d_out
+ * (RX_NCOUNTERS doubles: bit_errors, bits, symbols_counted, evm_num, evm_den, clipped,
+ * domain_errors, symbols_out) without synchronising the host, so a multi-GPU caller can
+ * all-reduce them with NCCL on the same stream (one collective per round). */
+#define RX_NCOUNTERS 8
+rx_status rx_export_counters(rx_handle *h, double *d_out, void *cuda_stream);
+
 /* Zero the BER/EVM/clip/domain counters (enqueued on cuda_stream). */
 rx_status rx_reset_stats(rx_handle *h, void *cuda_stream);
 
@@ -166,6 +173,28 @@ typedef enum {
 } rx_probe;
 rx_status rx_probe_read(rx_handle *h, int which, long long first, long long count,
                         void *host_out, void *cuda_stream);
+
+/* Tracing (SURVEY §5 'tracing / profiling'; the paper reads its chain off profiler traces,
+ * P:120). rx_profile_enable(h, mask) brackets every later launch of the kernel classes
+ * in `mask` (bit i = class i below) with CUDA events on the launching stream; mask 0 stops.
+ * rx_profile_read synchronises those events and returns, per class, the summed device time
+ * (ms) and the launch count since the last read (arrays of RX_KCLASS_COUNT entries). */
+typedef enum {
+  RX_K_PAM_FE = 0,      /* H0-H3  ingest, R2C FFT, static EQ, C_b */
+  RX_K_PAM_CLOCK = 1,   /* H4     105-block average, unwrap scan, tau_b, M_b */
+  RX_K_PAM_BE = 2,      /* H1-H2, H5-H7 re-FFT, EQ, clock ramp, C2R IFFT, extraction */
+  RX_K_NORM = 3,        /* H8     buffer normalisation */
+  RX_K_KK_S1 = 4,       /* H0, H11-H15 KK front-end, Hilbert, reconstruction, downshift */
+  RX_K_KK_S2 = 5,       /* H16-H18 C2C FFT, static EQ, decimating IFFT */
+  RX_K_CFO = 6,         /* H19-H20 power, 4th-power periodogram, fine CFO */
+  RX_K_SYNC = 7,        /* H24 frame sync + training */
+  RX_K_LMS = 8,         /* H9, H21-H23 segment-parallel block-LMS + CPR + decisions */
+  RX_K_LMS_POST = 9,    /* H22-H25 stitching, R_s scan, labels, counters, seeds */
+  RX_K_MISC = 10,       /* history copy, bookkeeping */
+  RX_KCLASS_COUNT = 11
+} rx_kernel_class;
+rx_status rx_profile_enable(rx_handle *h, int mask);
+rx_status rx_profile_read(rx_handle *h, double *host_ms, long long *host_counts, int n);
 
 void rx_destroy(rx_handle *h);
 const char *rx_strerror(int status);

@@ -7,6 +7,7 @@ a CUDA device.
 """
 from .rx import (  # noqa: F401
     FLAGS,
+    KCLASSES,
     PROBES,
     RX_PAM,
     RX_QAM_KK,

@@ -44,6 +44,11 @@ __global__ void k_kk_mend(RxDev d, long long q_end) {
     set_flag(d.st, RX_FLAG_SYNC);
   }
 }
+__global__ void k_export_counters(const DevState *st, double *o) {
+  o[0] = (double)st->bit_errors; o[1] = (double)st->bits; o[2] = (double)st->symbols_counted;
+  o[3] = st->evm_num; o[4] = st->evm_den; o[5] = (double)st->clipped;
+  o[6] = (double)st->domain_errors; o[7] = (double)st->symbols_out;
+}
 __global__ void k_reset_counters(DevState *st) {
   st->bit_errors = st->bits = st->symbols_counted = st->clipped = st->domain_errors = 0;
   st->first_domain = 0x7fffffffffffffffLL;
@@ -66,7 +71,22 @@ struct rx_handle {
   int sps;
   long long Q;   // 2-sps samples per buffer (KK)
   long long hist_cap;
+  // tracing
+  int prof_mask;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_pending;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_free;
 };
+
+static void prof_begin(rx_handle *h, int cls, cudaStream_t s, cudaEvent_t *stop) {
+  *stop = nullptr;
+  if (!(h->prof_mask & (1 << cls))) return;
+  std::pair<cudaEvent_t, cudaEvent_t> ev;
+  if (!h->prof_free.empty()) { ev = h->prof_free.back(); h->prof_free.pop_back(); }
+  else { cudaEventCreate(&ev.first); cudaEventCreate(&ev.second); }
+  cudaEventRecord(ev.first, s);
+  h->prof_pending.push_back({cls, ev});
+  *stop = ev.second;
+}
 
 static long long next_pow2(long long x) {
   long long p = 1;
@@ -210,6 +230,8 @@ extern "C" void rx_destroy(rx_handle *h) {
   cudaSetDevice(h->device);
   for (void *p : h->allocs) cudaFree(p);
   if (h->hm_host) cudaFreeHost(h->hm_host);
+  for (auto &e : h->prof_pending) { cudaEventDestroy(e.second.first); cudaEventDestroy(e.second.second); }
+  for (auto &e : h->prof_free) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   delete h;
 }
 
@@ -414,9 +436,12 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
 }
 
 // ------------------------------------------------------------------ orchestration
-#define LAUNCH(h, ...)                   \
+#define KLAUNCH(h, cls, s, ...)          \
   do {                                   \
+    cudaEvent_t stop_;                   \
+    prof_begin((h), (cls), (s), &stop_); \
     __VA_ARGS__;                         \
+    if (stop_) cudaEventRecord(stop_, (s)); \
     (h)->launches++;                     \
   } while (0)
 
@@ -438,10 +463,10 @@ static void launch_sync_train(rx_handle *h, cudaStream_t s, int flush) {
   const int nh = CPLX ? 2 : 1;
   const size_t smem = (size_t)nh * d.W_sync * sizeof(float2);
   if (!h->hm_host->synced) {
-    LAUNCH(h, (k_sync_corr<CPLX><<<gridc((long long)nh * RX_PREF, 256), 256, smem, s>>>(d)));
-    LAUNCH(h, (k_sync_pick<CPLX><<<1, 1024, 0, s>>>(d, flush)));
+    KLAUNCH(h, RX_K_SYNC, s, (k_sync_corr<CPLX><<<gridc((long long)nh * RX_PREF, 256), 256, smem, s>>>(d)));
+    KLAUNCH(h, RX_K_SYNC, s, (k_sync_pick<CPLX><<<1, 1024, 0, s>>>(d, flush)));
   }
-  LAUNCH(h, (k_lms_train<CPLX><<<1, 32, 0, s>>>(d, flush)));
+  KLAUNCH(h, RX_K_SYNC, s, (k_lms_train<CPLX><<<1, 32, 0, s>>>(d, flush)));
 }
 
 static void launch_lms_rounds(rx_handle *h, cudaStream_t s, unsigned char *labels, long long lab_cap,
@@ -457,16 +482,16 @@ static void launch_lms_rounds(rx_handle *h, cudaStream_t s, unsigned char *label
   const long long rounds = (e_hi - e_lo + 1 + d.D - 1) / d.D + 1;
   for (long long r = 0; r < rounds; ++r) {
     if (d.family == RX_PAM) {
-      LAUNCH(h, (k_lms_seg<false, 0><<<gridc(nseg, 4), 128, 0, s>>>(d, flush, (int)nseg)));
+      KLAUNCH(h, RX_K_LMS, s, (k_lms_seg<false, 0><<<gridc(nseg, 4), 128, 0, s>>>(d, flush, (int)nseg)));
     } else if (d.cpr == 1) {
-      LAUNCH(h, (k_lms_seg<true, 1><<<gridc(nseg, 4), 128, 0, s>>>(d, flush, (int)nseg)));
+      KLAUNCH(h, RX_K_LMS, s, (k_lms_seg<true, 1><<<gridc(nseg, 4), 128, 0, s>>>(d, flush, (int)nseg)));
     } else {
-      LAUNCH(h, (k_lms_seg<true, 2><<<gridc(nseg, 4), 128, 0, s>>>(d, flush, (int)nseg)));
+      KLAUNCH(h, RX_K_LMS, s, (k_lms_seg<true, 2><<<gridc(nseg, 4), 128, 0, s>>>(d, flush, (int)nseg)));
     }
-    LAUNCH(h, (k_lms_stitch<<<(unsigned)nseg, 256, 0, s>>>(d, (int)nseg)));
-    LAUNCH(h, (k_lms_prefix<<<1, 1024, 0, s>>>(d, flush, (int)nseg)));
-    LAUNCH(h, (k_lms_final<<<(unsigned)nseg, 256, 0, s>>>(d, labels, lab_cap, (int)nseg)));
-    LAUNCH(h, (k_lms_epoch<<<1, 1024, 0, s>>>(d, flush)));
+    KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_stitch<<<(unsigned)nseg, 256, 0, s>>>(d, (int)nseg)));
+    KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_prefix<<<1, 1024, 0, s>>>(d, flush, (int)nseg)));
+    KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_final<<<(unsigned)nseg, 256, 0, s>>>(d, labels, lab_cap, (int)nseg)));
+    KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_epoch<<<1, 1024, 0, s>>>(d, flush)));
   }
 }
 
@@ -476,18 +501,18 @@ static void run_pam(rx_handle *h, cudaStream_t s, const InView &in, unsigned cha
   const long long BB = d.buffer_blocks;
   const long long fe_target = h->n_in / 512;
   if (fe_target > h->fe_done) {
-    LAUNCH(h, (k_pam_fe<<<gridc(fe_target - h->fe_done, FE_GROUPS), 256, 0, s>>>(d, in, h->fe_done, fe_target)));
+    KLAUNCH(h, RX_K_PAM_FE, s, (k_pam_fe<<<gridc(fe_target - h->fe_done, FE_GROUPS), 256, 0, s>>>(d, in, h->fe_done, fe_target)));
     h->fe_done = fe_target;
   }
   long long clk_target = flush ? h->fe_done : h->fe_done - d.clock_half;
   if (clk_target > h->clk_done) {
-    LAUNCH(h, (k_pam_theta<<<gridc(clk_target - h->clk_done, 256), 256, 0, s>>>(d, h->clk_done, clk_target, h->fe_done - 1)));
-    LAUNCH(h, (k_pam_unwrap<<<1, 1024, 0, s>>>(d, h->clk_done, clk_target)));
+    KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_pam_theta<<<gridc(clk_target - h->clk_done, 256), 256, 0, s>>>(d, h->clk_done, clk_target, h->fe_done - 1)));
+    KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_pam_unwrap<<<1, 1024, 0, s>>>(d, h->clk_done, clk_target)));
     h->clk_done = clk_target;
   }
   long long be_target = flush ? h->fe_done - 1 : h->clk_done - 1;
   if (be_target > h->be_done) {
-    LAUNCH(h, (k_pam_be<<<gridc(be_target - h->be_done, FE_GROUPS), 256, 0, s>>>(d, in, h->be_done, be_target)));
+    KLAUNCH(h, RX_K_PAM_BE, s, (k_pam_be<<<gridc(be_target - h->be_done, FE_GROUPS), 256, 0, s>>>(d, in, h->be_done, be_target)));
     h->be_done = be_target;
   }
   while ((h->norm_done + 1) * BB <= h->be_done || (flush && h->norm_done * BB < h->be_done)) {
@@ -495,13 +520,13 @@ static void run_pam(rx_handle *h, cudaStream_t s, const InView &in, unsigned cha
     long long bhi = blo + BB;
     if (bhi > h->be_done) bhi = h->be_done;
     const long long beta = h->norm_done;
-    LAUNCH(h, (k_norm_dc<<<1, 1024, 0, s>>>(d, beta, blo, bhi)));
-    LAUNCH(h, (k_norm_abs<<<(unsigned)(bhi - blo), 256, 0, s>>>(d, beta, blo, bhi)));
-    LAUNCH(h, (k_norm_amp<<<1, 1024, 0, s>>>(d, beta, blo, bhi)));
-    LAUNCH(h, (k_norm_apply<<<(unsigned)(bhi - blo), 256, 0, s>>>(d, beta, blo, bhi, 0)));
+    KLAUNCH(h, RX_K_NORM, s, (k_norm_dc<<<1, 1024, 0, s>>>(d, beta, blo, bhi)));
+    KLAUNCH(h, RX_K_NORM, s, (k_norm_abs<<<(unsigned)(bhi - blo), 256, 0, s>>>(d, beta, blo, bhi)));
+    KLAUNCH(h, RX_K_NORM, s, (k_norm_amp<<<1, 1024, 0, s>>>(d, beta, blo, bhi)));
+    KLAUNCH(h, RX_K_NORM, s, (k_norm_apply<<<(unsigned)(bhi - blo), 256, 0, s>>>(d, beta, blo, bhi, 0)));
     h->norm_done++;
   }
-  if (flush) LAUNCH(h, (k_pam_mend<<<1, 1, 0, s>>>(d, h->be_done > 0 ? h->be_done : 0)));
+  if (flush) KLAUNCH(h, RX_K_MISC, s, (k_pam_mend<<<1, 1, 0, s>>>(d, h->be_done > 0 ? h->be_done : 0)));
   launch_sync_train<false>(h, s, flush);
   launch_lms_rounds(h, s, labels, lab_cap, flush, 260 * h->be_done + 1024);
 }
@@ -511,13 +536,13 @@ static void run_kk(rx_handle *h, cudaStream_t s, const InView &in, unsigned char
   RxDev &d = h->d;
   const long long s1_target = h->n_in / 512;
   if (s1_target > h->fe_done) {
-    LAUNCH(h, (k_kk_s1<<<gridc(s1_target - h->fe_done, FE_GROUPS), 256, 0, s>>>(d, in, h->fe_done, s1_target)));
+    KLAUNCH(h, RX_K_KK_S1, s, (k_kk_s1<<<gridc(s1_target - h->fe_done, FE_GROUPS), 256, 0, s>>>(d, in, h->fe_done, s1_target)));
     h->fe_done = s1_target;
   }
   const long long s2_target = h->fe_done - 1;
   if (s2_target > h->s2_done) {
     const size_t smem = (1024 + 8 * FFT_PAD_N) * sizeof(float2);
-    LAUNCH(h, (k_kk_s2<<<gridc(s2_target - h->s2_done, 4), 256, smem, s>>>(d, h->s2_done, s2_target)));
+    KLAUNCH(h, RX_K_KK_S2, s, (k_kk_s2<<<gridc(s2_target - h->s2_done, 4), 256, smem, s>>>(d, h->s2_done, s2_target)));
     h->s2_done = s2_target;
   }
   const long long q_front = h->s2_done > 0 ? 256 * h->s2_done - 128 : 0;
@@ -527,14 +552,14 @@ static void run_kk(rx_handle *h, cudaStream_t s, const InView &in, unsigned char
     long long qhi = qlo + Q;
     if (qhi > q_front) qhi = q_front;
     const size_t smem = (1024 + 8 * FFT_PAD_N) * sizeof(float2) + 1024 * sizeof(float);
-    LAUNCH(h, (k_cfo_partial<<<(unsigned)d.cfo_G, 256, smem, s>>>(d, qlo, qhi)));
-    LAUNCH(h, (k_cfo_final<<<1, 1024, 0, s>>>(d, h->cfo_done, qlo, qhi)));
-    if (d.cfo_enable) LAUNCH(h, (k_cfo_fine<<<296, 256, 0, s>>>(d, h->cfo_done, qlo, qhi)));
-    LAUNCH(h, (k_cfo_fine_final<<<1, 1024, 0, s>>>(d, h->cfo_done, qlo, qhi)));
+    KLAUNCH(h, RX_K_CFO, s, (k_cfo_partial<<<(unsigned)d.cfo_G, 256, smem, s>>>(d, qlo, qhi)));
+    KLAUNCH(h, RX_K_CFO, s, (k_cfo_final<<<1, 1024, 0, s>>>(d, h->cfo_done, qlo, qhi)));
+    if (d.cfo_enable) KLAUNCH(h, RX_K_CFO, s, (k_cfo_fine<<<296, 256, 0, s>>>(d, h->cfo_done, qlo, qhi)));
+    KLAUNCH(h, RX_K_CFO, s, (k_cfo_fine_final<<<1, 1024, 0, s>>>(d, h->cfo_done, qlo, qhi)));
     h->cfo_done++;
   }
   launch_sync_train<true>(h, s, flush);
-  if (flush) LAUNCH(h, (k_kk_mend<<<1, 1, 0, s>>>(d, q_front)));
+  if (flush) KLAUNCH(h, RX_K_MISC, s, (k_kk_mend<<<1, 1, 0, s>>>(d, q_front)));
   launch_lms_rounds(h, s, labels, lab_cap, flush, q_front / 2 + 1);
 }
 
@@ -559,8 +584,9 @@ extern "C" rx_status rx_process(rx_handle *h, const unsigned short *d_samples, l
   if (n > 0) {
     long long p0 = in.call_end - h->hist_cap;
     if (p0 < in.call_start) p0 = in.call_start;
-    LAUNCH(h, (k_hist_copy<<<gridc(in.call_end - p0, 256) < 512 ? gridc(in.call_end - p0, 256) : 512, 256, 0, s>>>(
-                   in, h->d.hist, h->hist_cap, p0, in.call_end)));
+    unsigned g = gridc(in.call_end - p0, 256);
+    if (g > 512) g = 512;
+    KLAUNCH(h, RX_K_MISC, s, (k_hist_copy<<<g, 256, 0, s>>>(in, h->d.hist, h->hist_cap, p0, in.call_end)));
   }
   return check_launch();
 }
@@ -613,7 +639,7 @@ extern "C" rx_status rx_get_stats(rx_handle *h, rx_stats *o, void *stream) {
 extern "C" rx_status rx_reset_stats(rx_handle *h, void *stream) {
   if (!h) return RX_EINVAL;
   CK(cudaSetDevice(h->device));
-  LAUNCH(h, (k_reset_counters<<<1, 1, 0, (cudaStream_t)stream>>>(h->st_dev)));
+  KLAUNCH(h, RX_K_MISC, (cudaStream_t)stream, (k_reset_counters<<<1, 1, 0, (cudaStream_t)stream>>>(h->st_dev)));
   return check_launch();
 }
 
@@ -710,4 +736,34 @@ extern "C" rx_status rx_probe_read(rx_handle *h, int which, long long first, lon
     }
     default: return RX_EINVAL;
   }
+}
+
+extern "C" rx_status rx_profile_enable(rx_handle *h, int mask) {
+  if (!h || mask < 0 || mask >= (1 << RX_KCLASS_COUNT)) return RX_EINVAL;
+  h->prof_mask = mask;
+  return RX_OK;
+}
+
+extern "C" rx_status rx_profile_read(rx_handle *h, double *ms, long long *counts, int n) {
+  if (!h || !ms || !counts || n < RX_KCLASS_COUNT) return RX_EINVAL;
+  CK(cudaSetDevice(h->device));
+  for (int i = 0; i < RX_KCLASS_COUNT; ++i) { ms[i] = 0.0; counts[i] = 0; }
+  for (auto &e : h->prof_pending) {
+    CK(cudaEventSynchronize(e.second.second));
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, e.second.first, e.second.second));
+    ms[e.first] += t;
+    counts[e.first] += 1;
+    h->prof_free.push_back(e.second);
+  }
+  h->prof_pending.clear();
+  return RX_OK;
+}
+
+extern "C" rx_status rx_export_counters(rx_handle *h, double *d_out, void *stream) {
+  if (!h || !d_out) return RX_EINVAL;
+  CK(cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  KLAUNCH(h, RX_K_MISC, s, (k_export_counters<<<1, 1, 0, s>>>(h->st_dev, d_out)));
+  return check_launch();
 }

@@ -58,7 +58,12 @@ class RxStats(ctypes.Structure):
 
 EXPORTS = ("rx_config_default", "rx_create", "rx_process", "rx_flush", "rx_get_stats",
            "rx_reset_stats", "rx_get_taps", "rx_probe_read", "rx_destroy", "rx_strerror",
-           "rx_version")
+           "rx_version", "rx_profile_enable", "rx_profile_read", "rx_export_counters")
+NCOUNTERS = 8
+COUNTERS = ("bit_errors", "bits", "symbols_counted", "evm_num", "evm_den", "clipped",
+            "domain_errors", "symbols_out")
+KCLASSES = ("PAM_FE", "PAM_CLOCK", "PAM_BE", "NORM", "KK_S1", "KK_S2", "CFO", "SYNC", "LMS",
+            "LMS_POST", "MISC")
 
 _lib = None
 
@@ -87,8 +92,12 @@ def load(path: str = SO_PATH):
     lib.rx_strerror.restype = ctypes.c_char_p
     lib.rx_version.argtypes = []
     lib.rx_version.restype = ctypes.c_char_p
+    lib.rx_profile_enable.argtypes = [vp, ctypes.c_int]
+    lib.rx_export_counters.argtypes = [vp, vp, vp]
+    lib.rx_export_counters.restype = ctypes.c_int
+    lib.rx_profile_read.argtypes = [vp, _c_dp, ctypes.POINTER(_c_ll), ctypes.c_int]
     for f in ("rx_create", "rx_process", "rx_flush", "rx_get_stats", "rx_reset_stats",
-              "rx_get_taps", "rx_probe_read"):
+              "rx_get_taps", "rx_probe_read", "rx_profile_enable", "rx_profile_read"):
         getattr(lib, f).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -173,6 +182,11 @@ class Receiver:
         _check(load().rx_get_stats(self._h, ctypes.byref(st), _stream_ptr(stream)), "rx_get_stats")
         return {k: getattr(st, k) for k, _ in RxStats._fields_}
 
+    def export_counters(self, out, stream=None):
+        """Enqueue a device copy of the counters into `out` (float64 CUDA tensor, >= 8)."""
+        _check(load().rx_export_counters(self._h, ctypes.c_void_p(out.data_ptr()),
+                                         _stream_ptr(stream)), "rx_export_counters")
+
     def reset_stats(self, stream=None):
         _check(load().rx_reset_stats(self._h, _stream_ptr(stream)), "rx_reset_stats")
 
@@ -199,6 +213,19 @@ class Receiver:
         if per > 1:
             return out.reshape(count, per)
         return out
+
+    def profile_enable(self, classes=KCLASSES):
+        mask = 0
+        for c in classes:
+            mask |= 1 << KCLASSES.index(c)
+        _check(load().rx_profile_enable(self._h, mask), "rx_profile_enable")
+
+    def profile_read(self) -> dict:
+        n = len(KCLASSES)
+        ms = (ctypes.c_double * n)()
+        cnt = (_c_ll * n)()
+        _check(load().rx_profile_read(self._h, ms, cnt, n), "rx_profile_read")
+        return {KCLASSES[i]: (ms[i], cnt[i]) for i in range(n) if cnt[i]}
 
     def close(self):
         if getattr(self, "_h", None):

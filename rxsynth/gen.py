@@ -148,12 +148,27 @@ def static_taps_kk(n_taps: int = 203, sps: int = 4, beta: float = 0.01,
 
 # --------------------------------------------------------------------------- helpers
 
+_PHASES = 4096
+
+
+@functools.lru_cache(maxsize=4)
+def _polyphase_table(ntaps: int, phases: int = _PHASES, win_beta: float = 8.0) -> np.ndarray:
+    """Kaiser(8)-windowed sinc interpolation kernels for `phases` fractional delays."""
+    half = ntaps // 2
+    j = np.arange(-half + 1, half + 1)
+    fr = np.arange(phases + 1) / phases
+    d = fr[:, None] - j[None, :]
+    w = np.i0(win_beta * np.sqrt(np.clip(1.0 - (d / half) ** 2, 0.0, None))) / np.i0(win_beta)
+    return np.sinc(d) * w
+
+
 def _resample_periodic(x: np.ndarray, ppm: float, ntaps: int = 32,
-                       n_out: int | None = None) -> np.ndarray:
-    """Band-limited resampling of a periodic sequence at positions p/(1+eps), eps = ppm*1e-6.
+                       n_out: int | None = None, p0: int = 0) -> np.ndarray:
+    """Band-limited resampling of a periodic sequence at positions p/(1+eps), eps = ppm*1e-6,
+    p = p0 .. p0+n_out-1 (indices mod len(x): the periodic waveform makes a seamless ring).
 
     eps > 0 means the ADC takes more samples per symbol (SURVEY §8(c) extraction pin).
-    Kaiser(8)-windowed sinc interpolation over ``ntaps`` neighbours, indices mod len(x).
+    Polyphase Kaiser(8)-windowed sinc over ``ntaps`` neighbours, 4096 fractional phases.
     """
     n = x.shape[0]
     n_out = n if n_out is None else n_out
@@ -161,18 +176,15 @@ def _resample_periodic(x: np.ndarray, ppm: float, ntaps: int = 32,
     out = np.empty(n_out, dtype=x.dtype)
     half = ntaps // 2
     j = np.arange(-half + 1, half + 1)
-    win_beta = 8.0
+    tab = _polyphase_table(ntaps)
     chunk = 1 << 18
     for s in range(0, n_out, chunk):
-        p = np.arange(s, min(n_out, s + chunk), dtype=np.float64)
+        p = np.arange(p0 + s, p0 + min(n_out, s + chunk), dtype=np.float64)
         t = p / (1.0 + eps)
         t0 = np.floor(t)
-        fr = t - t0
-        d = fr[:, None] - j[None, :]                       # distance to neighbour
-        w = np.i0(win_beta * np.sqrt(np.clip(1.0 - (d / half) ** 2, 0.0, None))) / np.i0(win_beta)
-        k = np.sinc(d) * w
+        ph = np.rint((t - t0) * _PHASES).astype(np.int64)
         idx = (t0.astype(np.int64)[:, None] + j[None, :]) % n
-        out[s:s + p.shape[0]] = np.sum(x[idx] * k, axis=1)
+        out[s:s + p.shape[0]] = np.einsum("ij,ij->i", x[idx], tab[ph])
     return out
 
 
@@ -216,7 +228,7 @@ def _tx_indices(fmt, M, nsym, offset):
 
 def pam_record(M: int, n_samples: int, *, seed: int, snr_db: float | None = None,
                channel: str = "b2b", ppm: float = 0.0, offset: int | None = None,
-               n_static_taps: int = 503, echo=(1.0, 0.2, -0.1)) -> Record:
+               n_static_taps: int = 503, echo=(1.0, 0.2, -0.1), keep_tx: bool = False) -> Record:
     """2 GBaud PAM-M at 2 sps, optional '91 km-like' ISI, clock offset, AWGN.
 
     channel "b2b": no filtering. "isi91": IM/DD CD response cos(2 pi^2 |b2| L f^2)
@@ -251,6 +263,7 @@ def pam_record(M: int, n_samples: int, *, seed: int, snr_db: float | None = None
     elif channel != "b2b":
         raise ValueError(channel)
     x = np.fft.ifft(F).real
+    x_tx = x if keep_tx else None            # periodic, pre-ADC-clock waveform (bench ring)
     if ppm != 0.0:
         x = _resample_periodic(x, ppm)
     taps = static_taps_pam(n_static_taps, sps, beta)
@@ -263,7 +276,7 @@ def pam_record(M: int, n_samples: int, *, seed: int, snr_db: float | None = None
     return Record(codes=codes, fmt="pam", M=M, baud=baud, sps=sps, offset=offset, ppm=ppm,
                   static_taps=taps, tx_index=idx,
                   meta=dict(seed=seed, snr_db=snr_db, channel=channel, clipped=clipped,
-                            full_scale=fs, noise_var=noise_var))
+                            full_scale=fs, mean=mean, noise_var=noise_var, x_tx=x_tx))
 
 
 # --------------------------------------------------------------------------- KK-QAM
