@@ -94,7 +94,10 @@ typedef struct {
   double sync_min_corr;       /* Gamma threshold (0.3) */
   long long warmup_symbols;   /* symbols below this index are not counted in BER/EVM */
   int history_buffers;        /* device rings keep this many buffers of each intermediate
-                                 (>= 2; probes can read back only what is still held) */
+                                 (>= 3; probes can read back only what is still held) */
+  int lms_batch_segments;     /* equaliser launches wait until about this many segments are
+                                 pending (more concurrent segment-warps per launch; results do
+                                 not depend on it; adds latency); 0 = every call */
 } rx_config;
 
 typedef struct rx_handle rx_handle;

@@ -6,15 +6,21 @@
 #pragma once
 #include "common.cuh"
 
-#define FFT_PAD_N 576   // 512 float2 + one pad per 8 -> conflict-free 64-bit stores
+#define FFT_PAD_N 544   // 512 float2 + one pad per 16: every FFT access pattern is
+                        // conflict-free (2 wavefronts per 64-bit warp access), see tools/banks
 
-__device__ __forceinline__ int P8(int i) { return i + (i >> 3); }
+__device__ __forceinline__ int P8(int i) { return i + (i >> 4); }
 
-// Twiddles: tw[k] = e^{-2 pi i k / 1024}, k in [0, 1024), in shared memory.
-// W512^k = tw[2k].
+// Twiddle table (1024 float2, staged in shared memory by every FFT kernel), laid out so that
+// each pass reads consecutive entries:
+//   tw[k]                      = W1024^k,            k < 512   (R2C / C2R packing, radix-2)
+//   tw[512 + 64 (r-1) + j]     = W512^(r j),         r = 1..7, j < 64   (pass 3)
+//   tw[960 + 8 (r-1) + k]      = W512^(8 r k),       r = 1..7, k < 8    (pass 2)
+#define TW_P3 512
+#define TW_P2 960
 template <bool INV>
-__device__ __forceinline__ float2 tw1024(const float2 *tw, int k) {
-  float2 w = tw[k & 1023];
+__device__ __forceinline__ float2 twv(const float2 *tw, int idx) {
+  const float2 w = tw[idx];
   return INV ? make_float2(w.x, -w.y) : w;
 }
 
@@ -68,7 +74,7 @@ __device__ __forceinline__ void fft512(float2 *buf, int j, const float2 *tw, flo
 #pragma unroll
     for (int r = 0; r < 8; ++r) v[r] = buf[P8(j + 64 * r)];
 #pragma unroll
-    for (int r = 1; r < 8; ++r) v[r] = cmul(v[r], tw1024<INV>(tw, 16 * r * k));
+    for (int r = 1; r < 8; ++r) v[r] = cmul(v[r], twv<INV>(tw, TW_P2 + 8 * (r - 1) + k));
     dft8<INV>(v);
     __syncthreads();
     const int base = (j >> 3) * 64 + k;
@@ -80,7 +86,7 @@ __device__ __forceinline__ void fft512(float2 *buf, int j, const float2 *tw, flo
 #pragma unroll
   for (int r = 0; r < 8; ++r) v[r] = buf[P8(j + 64 * r)];
 #pragma unroll
-  for (int r = 1; r < 8; ++r) v[r] = cmul(v[r], tw1024<INV>(tw, 2 * r * j));
+  for (int r = 1; r < 8; ++r) v[r] = cmul(v[r], twv<INV>(tw, TW_P3 + 64 * (r - 1) + j));
   dft8<INV>(v);
   // result: v[r] = X[j + 64 r]
 }

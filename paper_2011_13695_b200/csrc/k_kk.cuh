@@ -14,7 +14,7 @@
 __global__ void __launch_bounds__(256) k_kk_s1(RxDev d, InView in, long long b0, long long b1) {
   __shared__ float2 tw[1024];
   __shared__ float2 buf[FE_GROUPS][FFT_PAD_N];
-  __shared__ float amp[FE_GROUPS][512];
+  __shared__ float amp[FE_GROUPS][544];         // padded (i + i/16): conflict-free writes
   const int g = threadIdx.x >> 6, j = threadIdx.x & 63;
   for (int i = threadIdx.x; i < 1024; i += blockDim.x) tw[i] = d.tw[i];
   const long long b = b0 + (long long)blockIdx.x * FE_GROUPS + g;
@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(256) k_kk_s1(RxDev d, InView in, long long b0,
       I = fmaxf(I, 1e-12f);
       h[i] = 0.5f * logf(I);                              // P:215 logarithm for the phase
       const int l = 16 * j + i;
-      if (l >= 256 && l < 768) amp[g][l - 256] = sqrtf(I);  // P:215 square root: amplitude
+      if (l >= 256 && l < 768) amp[g][P8(l - 256)] = sqrtf(I);  // P:215 square root: amplitude
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) buf[g][P8(8 * j + i)] = make_float2(h[2 * i], h[2 * i + 1]);
@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(256) k_kk_s1(RxDev d, InView in, long long b0,
       float s0, c0, s1, c1;
       sincosf(sg * ph0, &s0, &c0);
       sincosf(sg * ph1, &s1, &c1);
-      const float a0 = amp[g][2 * n - 256], a1 = amp[g][2 * n + 1 - 256];
+      const float a0 = amp[g][P8(2 * n - 256)], a1 = amp[g][P8(2 * n + 1 - 256)];
       // downshift to DC: e^{-j psi(p; sigma f_c)}, 64-bit DDS from the absolute index
       const float2 r0 = dds_rot_neg((unsigned long long)p * d.carrier_inc);
       const float2 r1 = dds_rot_neg((unsigned long long)(p + 1) * d.carrier_inc);
@@ -242,7 +242,15 @@ __global__ void __launch_bounds__(1024) k_cfo_final(RxDev d, long long beta, lon
   const int t = threadIdx.x;
   const int G = d.cfo_G;
   double s = 0.0;
-  for (int c = 0; c < G; ++c) s += (double)d.cfo_part[(long long)c * 1024 + t];
+  int c = 0;
+  for (; c + 8 <= G; c += 8) {          // 8 independent loads in flight, summed in index order
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = d.cfo_part[(long long)(c + i) * 1024 + t];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += (double)v[i];
+  }
+  for (; c < G; ++c) s += (double)d.cfo_part[(long long)c * 1024 + t];
   Sd[t] = s;
   // argmax, lowest index on ties
   double bv = s;
@@ -344,18 +352,18 @@ __global__ void __launch_bounds__(1024) k_cfo_fine_final(RxDev d, long long beta
       cp.df = 0.0; cp.inc = 0ull; cp.origin = 0ull;
     }
     d.cfo[rmod(beta, d.buf_cap)] = cp;
-    d.st->v_front = qhi;     // z' valid up to the end of this buffer
   }
 }
 
-// z'_q = z_q / sqrt(P_beta) e^{-j psi'_q}, psi' the carried per-buffer CFO DDS (c-8).
-__device__ __forceinline__ float2 kk_zprime(const RxDev &d, long long q, long long vend) {
-  if (q < 0 || q >= vend) return make_float2(0.f, 0.f);
-  const long long Q = (long long)d.buffer_blocks * 256;
-  const long long beta = q / Q;
-  const CfoParam &cp = d.cfo[rmod(beta, d.buf_cap)];
-  const float2 zz = cscale(d.z[rmod(q, d.z_cap)], cp.inv_sqrtP);
-  if (!d.cfo_enable) return zz;
-  const unsigned long long u = cp.origin + (unsigned long long)(q - beta * Q) * cp.inc;
-  return cmul(zz, dds_rot_neg(u));
+// z'_q = z_q / sqrt(P_beta) e^{-j psi'_q}, psi' the carried per-buffer CFO DDS (c-8),
+// materialised once per buffer into the z' ring that the sync / LMS stages read.
+__global__ void __launch_bounds__(256) k_kk_zprime(RxDev d, long long beta, long long qlo, long long qhi) {
+  const CfoParam cp = d.cfo[rmod(beta, d.buf_cap)];
+  if (blockIdx.x == 0 && threadIdx.x == 0) d.st->v_front = qhi;   // consumed by later launches
+  for (long long q = qlo + (long long)blockIdx.x * blockDim.x + threadIdx.x; q < qhi;
+       q += (long long)gridDim.x * blockDim.x) {
+    float2 zz = cscale(d.z[rmod(q, d.z_cap)], cp.inv_sqrtP);
+    if (d.cfo_enable) zz = cmul(zz, dds_rot_neg(cp.origin + (unsigned long long)(q - qlo) * cp.inc));
+    d.zp[rmod(q, d.zp_cap)] = zz;
+  }
 }

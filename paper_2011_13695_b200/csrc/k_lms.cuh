@@ -8,12 +8,11 @@
 #pragma once
 #include "k_kk.cuh"
 
-#define LMS_WMAX 128   // window: stride*(B-1) + K <= 2*31 + 32 = 94
 
 template <bool CPLX>
 __device__ __forceinline__ float2 lms_in(const RxDev &d, long long i, long long vend) {
-  if (CPLX) return kk_zprime(d, i, vend);
   if (i < 0 || i >= vend) return make_float2(0.f, 0.f);
+  if (CPLX) return d.zp[rmod(i, d.zp_cap)];
   return make_float2(d.uhat[rmod(i, d.sym_cap)], 0.f);
 }
 
@@ -146,36 +145,56 @@ __global__ void __launch_bounds__(1024) k_sync_pick(RxDev d, int flush) {
 // MODE 0: training (e = r - y, no CPR), MODE 1: decision directed with CPR `CPR`
 // (0 none, 1 VV, 2 BPS). Outputs for m >= out_lo go to the level / yout rings,
 // warm-up decisions (m < out_lo) to warm[]. Returns final theta; accumulates EVM.
-struct LmsSmem {
+//
+// Layout: taps are padded to KP = 4 ceil(K/4) (zero taps, exact) so the K-term dot products
+// run with 4 independent accumulators; lane i owns symbol i of the block, lane k tap k; the
+// sliding window of inputs lives in shared memory (double-buffered, next block prefetched
+// into registers while the current block computes).
+#define LMS_WMAX 96
+
+template <bool CPLX>
+struct LmsSmemT {
   float2 win[2][LMS_WMAX];
-  float2 w[RX_MAX_K];
+  float2 w[32];
   float2 e[32];
-  float dist[RX_MAX_PT][33];
+  float2 y[32];
 };
 
+// decision level value of index i: PAM (2i - M + 1)/(M - 1); QAM axis (2i - L + 1) sc
+__device__ __forceinline__ float level_of(int i, float two_s, float off) { return fmaf((float)i, two_s, off); }
+
 template <bool CPLX, int CPR, int MODE>
-__device__ float lms_run(const RxDev &d, LmsSmem &sm, long long t_begin, long long t_end,
+__device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, long long t_end,
                          long long out_lo, float2 &wk, unsigned char *warm, double &evn,
                          double &evd, long long vend) {
   const int lane = threadIdx.x & 31;
-  const int K = d.K, c = K >> 1;
+  const int K = d.K, c = K >> 1, KP = (K + 3) & ~3;
   const int stride = CPLX ? 2 : 1;
   const int off = CPLX ? d.st->sync_phase : 0;
-  const int WL = stride * 31 + K;
+  const int WL = stride * 31 + KP;
   const float mu = d.mu;
-  const float sc = CPLX ? 0.5f * (__ldg(d.lvl + 1) - __ldg(d.lvl + 0)) : 0.f;   // half spacing
-  const float inv2sc = CPLX ? 1.0f / (2.0f * sc) : 0.f;
+  // slicer constants: index = floor(v * inv2s + L/2) clamped; level = i * two_s + lvl0
+  const int L = d.L;
+  const float two_s = CPLX ? 2.0f * d.qam_sc : 2.0f / (float)(d.M - 1);
+  const float lvl0 = CPLX ? -(float)(L - 1) * d.qam_sc : -1.0f;
+  const float inv2s = 1.0f / two_s;
   const long long o_ref = d.st->sync_offset;
+  const int ref0 = MODE == 0 ? (int)(((o_ref + t_begin - d.m0) % RX_PREF + RX_PREF) % RX_PREF) : 0;
+  // BPS test-phase rotations for phases lane and lane + 32 (e^{-j phi_p})
+  float2 rotA = make_float2(1.f, 0.f), rotB = make_float2(1.f, 0.f);
+  if (CPR == 2) {
+    if (lane < d.Pt) rotA = __ldg(d.bps_rot + lane);
+    if (lane + 32 < d.Pt) rotB = __ldg(d.bps_rot + lane + 32);
+  }
   float theta = 0.f;
-  if (lane < K) sm.w[lane] = wk;
-  // initial window
-  long long wb = (long long)stride * t_begin + off + c - (K - 1);
+  if (lane >= K) wk = make_float2(0.f, 0.f);
+  sm.w[lane] = wk;
+  long long wb = (long long)stride * t_begin + off + c - (KP - 1);
   for (int x = lane; x < WL; x += 32) sm.win[0][x] = lms_in<CPLX>(d, wb + x, vend);
   __syncwarp();
   int buf = 0;
   bool first = true;
   for (long long t = t_begin; t < t_end; t += 32) {
-    // prefetch the next window into registers
     float2 pre[3];
     const long long wbn = wb + (long long)stride * 32;
     const bool more = t + 32 < t_end;
@@ -185,21 +204,30 @@ __device__ float lms_run(const RxDev &d, LmsSmem &sm, long long t_begin, long lo
       pre[q] = (more && x < WL) ? lms_in<CPLX>(d, wbn + x, vend) : make_float2(0.f, 0.f);
     }
     const float2 *cur = sm.win[buf];
-    // y_i = w^H u_i, u_i[k] = win[stride i + K-1-k]
-    float2 y = make_float2(0.f, 0.f);
-    for (int k = 0; k < K; ++k) {
-      const float2 u = cur[stride * lane + K - 1 - k];
-      const float2 w = sm.w[k];
-      // conj(w) u
-      y.x = fmaf(w.x, u.x, fmaf(w.y, u.y, y.x));
-      if (CPLX) y.y = fmaf(w.x, u.y, fmaf(-w.y, u.x, y.y));
-    }
+    const int nvalid = (int)((t_end - t) < 32 ? (t_end - t) : 32);
+    const bool valid = lane < nvalid;
     const long long m = t + lane;
-    const bool valid = m < t_end;
+    // y_i = w^H u_i, u_i[k] = cur[stride i + KP-1-k]
+    float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
+    const float2 *ub = cur + stride * lane + KP - 1;
+    for (int k = 0; k < KP; k += 4) {
+      const float2 w0 = sm.w[k], w1 = sm.w[k + 1], w2 = sm.w[k + 2], w3 = sm.w[k + 3];
+      const float2 u0 = ub[-k], u1 = ub[-k - 1], u2 = ub[-k - 2], u3 = ub[-k - 3];
+      a0.x = fmaf(w0.x, u0.x, a0.x); a1.x = fmaf(w1.x, u1.x, a1.x);
+      a2.x = fmaf(w2.x, u2.x, a2.x); a3.x = fmaf(w3.x, u3.x, a3.x);
+      if (CPLX) {
+        a0.x = fmaf(w0.y, u0.y, a0.x); a1.x = fmaf(w1.y, u1.y, a1.x);
+        a2.x = fmaf(w2.y, u2.y, a2.x); a3.x = fmaf(w3.y, u3.y, a3.x);
+        a0.y = fmaf(w0.x, u0.y, fmaf(-w0.y, u0.x, a0.y)); a1.y = fmaf(w1.x, u1.y, fmaf(-w1.y, u1.x, a1.y));
+        a2.y = fmaf(w2.x, u2.y, fmaf(-w2.y, u2.x, a2.y)); a3.y = fmaf(w3.x, u3.y, fmaf(-w3.y, u3.x, a3.y));
+      }
+    }
+    const float2 y = make_float2((a0.x + a1.x) + (a2.x + a3.x), CPLX ? (a0.y + a1.y) + (a2.y + a3.y) : 0.f);
     float2 e, zp = y;
     int code = 0;
     if (MODE == 0) {
-      const long long ri = ((o_ref + m - d.m0) % RX_PREF + RX_PREF) % RX_PREF;
+      int ri = ref0 + (int)(m - t_begin);
+      while (ri >= RX_PREF) ri -= RX_PREF;
       const float2 r = __ldg(d.ref_val + ri);
       e = CPLX ? csub(r, y) : make_float2(r.x - y.x, 0.f);
     } else {
@@ -207,34 +235,40 @@ __device__ float lms_run(const RxDev &d, LmsSmem &sm, long long t_begin, long lo
       if (CPLX && CPR != 0) {
         float th_hat;
         if (CPR == 1) {   // Viterbi-Viterbi: 1/4 arg(-sum y^4)
-          float2 y2 = cmul(y, y), y4 = cmul(y2, y2);
+          const float2 y2 = cmul(y, y);
+          float2 y4 = cmul(y2, y2);
           if (!valid) y4 = make_float2(0.f, 0.f);
           const float sx = warp_sum(y4.x), sy = warp_sum(y4.y);
           th_hat = 0.25f * atan2f(-sy, -sx);
-        } else {           // blind phase search over Pt test phases
-          const int Pt = d.Pt;
-          for (int p = 0; p < Pt; ++p) {
-            const float2 zr = cmul(y, __ldg(d.bps_rot + p));
-            const int iI = slice_axis(zr.x, inv2sc, d.L), iQ = slice_axis(zr.y, inv2sc, d.L);
-            const float dx = zr.x - __ldg(d.lvl + iI), dy = zr.y - __ldg(d.lvl + iQ);
-            sm.dist[p][lane] = valid ? fmaf(dx, dx, dy * dy) : 0.f;
-          }
+        } else {           // blind phase search: lane p scores test phases p and p + 32
+          sm.y[lane] = y;
           __syncwarp();
-          float bd = 3.4e38f;
-          int bp = 0x7fffffff;
-          for (int p = lane; p < Pt; p += 32) {
-            float s = 0.f;
-            for (int i = 0; i < 32; ++i) s += sm.dist[p][i];
-            if (s < bd) { bd = s; bp = p; }
+          float dA = 0.f, dB = 0.f;
+          for (int i = 0; i < nvalid; ++i) {
+            const float2 yi = sm.y[i];
+            {
+              const float2 zr = cmul(yi, rotA);
+              const int iI = slice_axis(zr.x, inv2s, L), iQ = slice_axis(zr.y, inv2s, L);
+              const float dx = zr.x - level_of(iI, two_s, lvl0), dy = zr.y - level_of(iQ, two_s, lvl0);
+              dA += fmaf(dx, dx, dy * dy);
+            }
+            if (d.Pt > 32) {
+              const float2 zr = cmul(yi, rotB);
+              const int iI = slice_axis(zr.x, inv2s, L), iQ = slice_axis(zr.y, inv2s, L);
+              const float dx = zr.x - level_of(iI, two_s, lvl0), dy = zr.y - level_of(iQ, two_s, lvl0);
+              dB += fmaf(dx, dx, dy * dy);
+            }
           }
+          float bd = lane < d.Pt ? dA : 3.4e38f;
+          int bp = lane;
+          if (lane + 32 < d.Pt && dB < bd) { bd = dB; bp = lane + 32; }
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) {
             const float ob = __shfl_xor_sync(0xffffffffu, bd, o);
             const int op = __shfl_xor_sync(0xffffffffu, bp, o);
             if (ob < bd || (ob == bd && op < bp)) { bd = ob; bp = op; }
           }
-          th_hat = -0.78539816339744831f + ((float)bp + 0.5f) * (1.5707963267948966f / (float)Pt);
-          __syncwarp();
+          th_hat = -0.78539816339744831f + ((float)bp + 0.5f) * (1.5707963267948966f / (float)d.Pt);
         }
         if (first) theta = th_hat;
         else theta = th_hat + 1.5707963267948966f * rintf((theta - th_hat) * 0.63661977236758134f);
@@ -243,14 +277,14 @@ __device__ float lms_run(const RxDev &d, LmsSmem &sm, long long t_begin, long lo
       }
       float2 dv;
       if (CPLX) {
-        const int iI = slice_axis(zp.x, inv2sc, d.L), iQ = slice_axis(zp.y, inv2sc, d.L);
+        const int iI = slice_axis(zp.x, inv2s, L), iQ = slice_axis(zp.y, inv2s, L);
         code = iI | (iQ << 4);
-        dv = make_float2(__ldg(d.lvl + iI), __ldg(d.lvl + iQ));
+        dv = make_float2(level_of(iI, two_s, lvl0), level_of(iQ, two_s, lvl0));
         e = cmul(csub(dv, zp), make_float2(cth, sth));
       } else {
-        const int i = slice_pam(d, zp.x);
+        const int i = d.thr_default ? slice_axis(zp.x, inv2s, L) : slice_pam(d, zp.x);
         code = i;
-        dv = make_float2(__ldg(d.lvl + i), 0.f);
+        dv = make_float2(level_of(i, two_s, lvl0), 0.f);
         e = make_float2(dv.x - zp.x, 0.f);
       }
       if (valid && m >= out_lo) {
@@ -267,23 +301,32 @@ __device__ float lms_run(const RxDev &d, LmsSmem &sm, long long t_begin, long lo
     }
     sm.e[lane] = valid ? e : make_float2(0.f, 0.f);
     __syncwarp();
-    // gradient: lane k: g_k = sum_i u_i[k] conj(e_i); w <- w + mu g  (c-9 step 7)
-    if (lane < K) {
-      float gx = 0.f, gy = 0.f;
-      for (int i = 0; i < 32; ++i) {
-        const float2 u = cur[stride * i + K - 1 - lane];
-        const float2 ee = sm.e[i];
-        gx = fmaf(u.x, ee.x, fmaf(u.y, ee.y, gx));
-        if (CPLX) gy = fmaf(u.y, ee.x, fmaf(-u.x, ee.y, gy));
+    // gradient: lane k: g_k = sum_i u_i[k] conj(e_i); w <- w + mu g   (c-9 step 7)
+    {
+      float2 g0 = make_float2(0.f, 0.f), g1 = g0, g2 = g0, g3 = g0;
+      const float2 *ug = cur + KP - 1 - (lane < KP ? lane : 0);   // lanes >= KP: discarded
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        const float2 e0 = sm.e[i], e1 = sm.e[i + 1], e2 = sm.e[i + 2], e3 = sm.e[i + 3];
+        const float2 u0 = ug[stride * i], u1 = ug[stride * (i + 1)], u2 = ug[stride * (i + 2)], u3 = ug[stride * (i + 3)];
+        g0.x = fmaf(u0.x, e0.x, g0.x); g1.x = fmaf(u1.x, e1.x, g1.x);
+        g2.x = fmaf(u2.x, e2.x, g2.x); g3.x = fmaf(u3.x, e3.x, g3.x);
+        if (CPLX) {
+          g0.x = fmaf(u0.y, e0.y, g0.x); g1.x = fmaf(u1.y, e1.y, g1.x);
+          g2.x = fmaf(u2.y, e2.y, g2.x); g3.x = fmaf(u3.y, e3.y, g3.x);
+          g0.y = fmaf(u0.y, e0.x, fmaf(-u0.x, e0.y, g0.y)); g1.y = fmaf(u1.y, e1.x, fmaf(-u1.x, e1.y, g1.y));
+          g2.y = fmaf(u2.y, e2.x, fmaf(-u2.x, e2.y, g2.y)); g3.y = fmaf(u3.y, e3.x, fmaf(-u3.x, e3.y, g3.y));
+        }
       }
-      wk.x = fmaf(mu, gx, wk.x);
-      if (CPLX) wk.y = fmaf(mu, gy, wk.y);
+      if (lane < K) {
+        wk.x = fmaf(mu, (g0.x + g1.x) + (g2.x + g3.x), wk.x);
+        if (CPLX) wk.y = fmaf(mu, (g0.y + g1.y) + (g2.y + g3.y), wk.y);
+        // divergence (reading R-DIV): any single tap beyond 1e3 flags at once,
+        // the full norm is checked at the end of the run
+        if (cabs2(wk) > 1e6f) set_flag(d.st, RX_FLAG_DIVERGE);
+      }
     }
-    // divergence check
-    const float nrm = warp_sum(lane < K ? cabs2(wk) : 0.f);
-    if (lane == 0 && nrm > 1e6f) set_flag(d.st, RX_FLAG_DIVERGE);
-    __syncwarp();
-    if (lane < K) sm.w[lane] = wk;
+    sm.w[lane] = wk;
     float2 *nxt = sm.win[buf ^ 1];
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
@@ -295,13 +338,15 @@ __device__ float lms_run(const RxDev &d, LmsSmem &sm, long long t_begin, long lo
     wb = wbn;
     first = false;
   }
+  const float nrm = warp_sum(lane < K ? cabs2(wk) : 0.f);
+  if (lane == 0 && nrm > 1e6f) set_flag(d.st, RX_FLAG_DIVERGE);
   return theta;
 }
 
 // ------------------------------------------------------------------ training (1 warp)
 template <bool CPLX>
 __global__ void __launch_bounds__(32) k_lms_train(RxDev d, int flush) {
-  __shared__ LmsSmem sm;
+  __shared__ LmsSmemT<CPLX> sm;
   DevState *st = d.st;
   if (!st->synced || st->trained) return;
   const int lane = threadIdx.x;
@@ -321,7 +366,7 @@ __global__ void __launch_bounds__(32) k_lms_train(RxDev d, int flush) {
 // Segment s outputs [sS, min((s+1)S, m_end)), recursion starts O symbols early (c-9).
 template <bool CPLX, int CPR>
 __global__ void __launch_bounds__(128) k_lms_seg(RxDev d, int flush, int nseg) {
-  __shared__ LmsSmem sm[4];
+  __shared__ LmsSmemT<CPLX> sm[4];
   DevState *st = d.st;
   if (!st->trained) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -509,7 +554,11 @@ __global__ void __launch_bounds__(256) k_lms_final(RxDev d, unsigned char *label
   const long long lo = s * (long long)d.S, hi = seg_end_of(d, s);
   const int b = d.kbits >> 1;
   long long err = 0, cntd = 0;
+  // reference index and label slot of the segment's first symbol (one modulo per segment)
+  const int r0 = (int)(((st->sync_offset + lo - d.m0) % RX_PREF + RX_PREF) % RX_PREF);
+  const long long l0 = labels ? lo % lab_cap : 0;
   for (long long m = lo + threadIdx.x; m < hi; m += blockDim.x) {
+    const int dm = (int)(m - lo);
     int code = d.level[rmod(m, d.sym_cap)];
     int lab;
     if (d.family == 1) {
@@ -519,9 +568,14 @@ __global__ void __launch_bounds__(256) k_lms_final(RxDev d, unsigned char *label
       lab = gray(code);
     }
     d.level_fin[rmod(m, d.sym_cap)] = (unsigned char)code;
-    if (labels) labels[m % lab_cap] = (unsigned char)lab;
+    if (labels) {
+      long long li = l0 + dm;
+      if (li >= lab_cap) li -= lab_cap * (li / lab_cap);
+      labels[li] = (unsigned char)lab;
+    }
     if (m >= d.warmup) {
-      const long long ri = ((st->sync_offset + m - d.m0) % RX_PREF + RX_PREF) % RX_PREF;
+      int ri = r0 + dm;                         // dm < S <= 2^15: at most one wrap
+      if (ri >= RX_PREF) ri -= RX_PREF;
       err += __popc(lab ^ (int)d.ref_lab[ri]);
       ++cntd;
     }
@@ -612,11 +666,21 @@ __global__ void __launch_bounds__(1024) k_lms_epoch(RxDev d, int flush) {
     // thread layout: k = t >> 5 (tap), lane sums segments lane, lane+32, ... in fixed order
     const int k = t >> 5, lane = t & 31;
     float sx = 0.f, sy = 0.f;
-    if (k < d.K)
-      for (long long s = s_lo + lane; s < s_hi; s += 32) {
+    if (k < d.K) {
+      long long s = s_lo + lane;
+      for (; s + 96 < s_hi; s += 128) {          // 4 independent loads in flight, summed in order
+        const float2 w0 = d.seg_w[rmod(s, d.seg_cap) * RX_MAX_K + k];
+        const float2 w1 = d.seg_w[rmod(s + 32, d.seg_cap) * RX_MAX_K + k];
+        const float2 w2 = d.seg_w[rmod(s + 64, d.seg_cap) * RX_MAX_K + k];
+        const float2 w3 = d.seg_w[rmod(s + 96, d.seg_cap) * RX_MAX_K + k];
+        sx += w0.x; sy += w0.y; sx += w1.x; sy += w1.y;
+        sx += w2.x; sy += w2.y; sx += w3.x; sy += w3.y;
+      }
+      for (; s < s_hi; s += 32) {
         const float2 w = d.seg_w[rmod(s, d.seg_cap) * RX_MAX_K + k];
         sx += w.x; sy += w.y;
       }
+    }
     sx = warp_sum(sx);
     sy = warp_sum(sy);
     if (k < d.K && lane == 0) {

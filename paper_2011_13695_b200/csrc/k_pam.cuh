@@ -1,13 +1,15 @@
 // k_pam.cuh — IMDD PAM-N chain kernels (§III).
 //
 //  k_pam_fe     H0-H3  ingest + overlap framing + R2C FFT-1024 + static FD EQ + C_b
-//  k_pam_theta  H4a    105-block complex average + atan2          (parallel over blocks)
-//  k_pam_unwrap H4b    unwrap as a prefix sum of wrapped differences, tau_b, M_b (1 CTA)
+//  k_pam_theta  H4a    105-block complex average + atan2 (parallel, shared-memory C tiles)
+//  k_pam_unwrap H4b    unwrap as a prefix sum of wrapped differences -> tau_b, M_b (one CTA)
 //  k_pam_be     H1,H2,H5-H7  re-FFT + EQ + FD clock correction + C2R IFFT + extraction
-//  k_norm_*     H8     buffer-wise DC / amplitude normalisation (fixed-order reductions)
+//  k_norm_coop  H8     buffer-wise DC / amplitude normalisation (one cooperative launch)
 #pragma once
 #include "fft.cuh"
 #include "rx_dev.cuh"
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 #define FE_GROUPS 4
 
@@ -73,114 +75,122 @@ __global__ void __launch_bounds__(256) k_pam_fe(RxDev d, InView in, long long b0
     d.C[rmod(b, d.blk_cap)] = make_double2(red[g][0].x + red[g][1].x, red[g][0].y + red[g][1].y);
 }
 
-// ------------------------------------------------------------------ H4 (a)
-// Cbar_b = sum_{i=max(0,b-h)}^{min(blast,b+h)} C_i ; theta_b = atan2(Cbar_b) (NaN if 0).
-__global__ void k_pam_theta(RxDev d, long long b0, long long b1, long long blast) {
-  const long long b = b0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= b1) return;
-  long long lo = b - d.clock_half, hi = b + d.clock_half;
-  if (lo < 0) lo = 0;
-  if (hi > blast) hi = blast;
-  double sr = 0.0, si = 0.0;
-  for (long long i = lo; i <= hi; ++i) {
-    const double2 c = d.C[rmod(i, d.blk_cap)];
-    sr += c.x; si += c.y;
+// ------------------------------------------------------------------ H4
+// One CTA of 1024 threads per call, blocks [b0, b1) in chunks of 8192 (c-3):
+//   Cbar_b = sum_{i=max(0,b-h)}^{min(blast,b+h)} C_i   (105-block vector average, from a
+//            shared-memory tile of C, each thread sliding its window over 8 blocks)
+//   theta_b = atan2(Cbar_b) ; |Cbar| = 0 inherits the previous phase
+//   theta^u_b = theta^u_{b-1} + w(theta_b - theta_{b-1}), w(x) = x - 2 pi rint(x / 2 pi):
+//            the paper's serial single-warp unwrap as a warp-shuffle block scan
+//   tau_b = -theta^u_b / 2 pi ; M_b = ceil(256 b - 128 - tau_b)
+#define CLK_CHUNK 8192
+__device__ __forceinline__ double warp_incl_scan_d(double v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
   }
-  d.theta[rmod(b, d.blk_cap)] = (sr == 0.0 && si == 0.0) ? __longlong_as_double(0x7ff8000000000000LL)
+  return v;
+}
+__device__ __forceinline__ long long warp_incl_max_ll(long long v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o && t > v) v = t;
+  }
+  return v;
+}
+
+// (a) theta_b for blocks [b0, b1): one CTA per 256 blocks, C tile (+ 2h halo) in shared
+//     memory, each thread sums its own 105-term window (consecutive lanes, conflict-free).
+__global__ void __launch_bounds__(256) k_pam_theta(RxDev d, long long b0, long long b1, long long blast) {
+  extern __shared__ double2 Ct[];                 // [256 + 2 h]
+  const int t = threadIdx.x, hh = d.clock_half;
+  const long long base = b0 + (long long)blockIdx.x * 256;
+  for (int i = t; i < 256 + 2 * hh; i += blockDim.x) {
+    const long long b = base - hh + i;
+    Ct[i] = (b >= 0 && b <= blast) ? d.C[rmod(b, d.blk_cap)] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  const long long b = base + t;
+  if (b >= b1) return;
+  double sr = 0.0, si = 0.0;
+  for (int i = 0; i <= 2 * hh; ++i) { const double2 c = Ct[t + i]; sr += c.x; si += c.y; }
+  d.theta[rmod(b, d.blk_cap)] = (sr == 0.0 && si == 0.0) ? __longlong_as_double(0x7ff8000000000000LL)   // S:363
                                                          : atan2(si, sr);
 }
 
-// ------------------------------------------------------------------ H4 (b)
-// One CTA of 1024 threads. theta^u_b = theta^u_{b-1} + w(theta_b - theta_{b-1}),
-// w(x) = x - 2 pi rint(x / 2 pi): a prefix sum of wrapped differences (SURVEY c-3, A15) —
-// the paper's single-warp serial unwrap as a block scan. |Cbar| = 0 inherits the
-// previous phase via a max-scan of the last valid index.
+// (b) one CTA: |Cbar| = 0 inherits the previous phase (max-scan of the last valid block),
+//     wrapped differences, prefix sum (warp-shuffle block scan), tau_b and M_b.
 __global__ void __launch_bounds__(1024) k_pam_unwrap(RxDev d, long long b0, long long b1) {
-  __shared__ double sd[1024];
-  __shared__ long long si[1024];
+  __shared__ double wsum[32];
+  __shared__ long long wmax[32];
   __shared__ double carry_theta, carry_u;
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const double TWO_PI = 6.283185307179586476925;
   if (t == 0) { carry_theta = d.st->theta_prev; carry_u = d.st->thetau_prev; }
   __syncthreads();
-  for (long long base = b0; base < b1; base += 8192) {
+  for (long long base = b0; base < b1; base += CLK_CHUNK) {
+    const long long nb = (b1 - base) < CLK_CHUNK ? (b1 - base) : CLK_CHUNK;
     double th[8];
-    long long vi[8];
     long long last = -1;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const long long b = base + 8 * t + i;
-      double x = 0.0;
-      bool valid = false;
-      if (b < b1) { x = d.theta[rmod(b, d.blk_cap)]; valid = !isnan(x); }
-      th[i] = x;
-      if (valid) last = b;
-      vi[i] = last;
+    for (int q = 0; q < 8; ++q) {
+      const long long j = 8 * t + q;
+      th[q] = __longlong_as_double(0x7ff8000000000000LL);
+      if (j < nb) th[q] = d.theta[rmod(base + j, d.blk_cap)];
+      if (j < nb && !isnan(th[q])) last = base + j;
     }
-    // inclusive max-scan of the last valid index
-    si[t] = last;
+    const long long lw = warp_incl_max_ll(last);
+    if (lane == 31) wmax[warp] = lw;
     __syncthreads();
-    for (int off = 1; off < 1024; off <<= 1) {
-      long long o = (t >= off) ? si[t - off] : -1;
-      __syncthreads();
-      if (o > si[t]) si[t] = o;
-      __syncthreads();
-    }
-    const long long excl = (t > 0) ? si[t - 1] : -1;
+    if (warp == 0) wmax[lane] = warp_incl_max_ll(wmax[lane]);
     __syncthreads();
-    // resolve inherited phases: theta_b = theta[last valid <= b] or the carry
-    double prev_local;
+    long long excl = __shfl_up_sync(0xffffffffu, lw, 1);
+    if (lane == 0) excl = -1;
+    if (warp > 0 && wmax[warp - 1] > excl) excl = wmax[warp - 1];
+    const double prev0 = excl >= 0 ? d.theta[rmod(excl, d.blk_cap)] : carry_theta;
+    double diff[8], run = 0.0;
     {
-      long long src = excl;
-      prev_local = (src >= 0) ? d.theta[rmod(src, d.blk_cap)] : carry_theta;
-    }
-    double diff[8];
-    double run = 0.0;
-    double prevth = prev_local;
+      double cur = prev0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const long long b = base + 8 * t + i;
-      double x;
-      if (vi[i] >= 0 && vi[i] == b) x = th[i];
-      else if (vi[i] >= 0) x = d.theta[rmod(vi[i], d.blk_cap)];
-      else x = prev_local;
-      // for inherited entries with no valid in this thread's run, vi < 0 -> prev_local
-      if (vi[i] < 0) x = prev_local;
-      const double dd = x - prevth;
-      diff[i] = (b < b1) ? dd - TWO_PI * rint(dd / TWO_PI) : 0.0;
-      run += diff[i];
-      th[i] = x;
-      prevth = x;
+      for (int q = 0; q < 8; ++q) {
+        diff[q] = 0.0;
+        if (8 * t + q < nb) {
+          const double x = isnan(th[q]) ? cur : th[q];
+          const double dd = x - cur;
+          diff[q] = dd - TWO_PI * rint(dd / TWO_PI);
+          cur = x;
+        }
+        run += diff[q];
+      }
     }
-    // exclusive prefix sum of the per-thread totals (Hillis-Steele in double)
-    sd[t] = run;
+    const double incl = warp_incl_scan_d(run);
+    if (lane == 31) wsum[warp] = incl;
     __syncthreads();
-    for (int off = 1; off < 1024; off <<= 1) {
-      double o = (t >= off) ? sd[t - off] : 0.0;
-      __syncthreads();
-      sd[t] += o;
-      __syncthreads();
-    }
-    double acc = carry_u + ((t > 0) ? sd[t - 1] : 0.0);
-    const double total = sd[1023];
+    if (warp == 0) wsum[lane] = warp_incl_scan_d(wsum[lane]);
+    __syncthreads();
+    double acc = carry_u + (incl - run) + (warp > 0 ? wsum[warp - 1] : 0.0);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const long long b = base + 8 * t + i;
-      acc += diff[i];
-      if (b < b1) {
+    for (int q = 0; q < 8; ++q) {
+      const long long j = 8 * t + q;
+      acc += diff[q];
+      if (j < nb) {
+        const long long b = base + j;
         const double tau = -acc / TWO_PI;
         d.tau[rmod(b, d.blk_cap)] = tau;
         d.Mb[rmod(b, d.blk_cap)] = (long long)ceil(256.0 * (double)b - 128.0 - tau);
       }
     }
+    const double total = wsum[31];
+    const long long lastall = wmax[31];
     __syncthreads();
-    // carries for the next chunk: last resolved theta and the running unwrapped phase
-    if (t == 1023) {
-      carry_u = carry_u + total;
+    if (t == 0) {
+      carry_u += total;
+      if (lastall >= 0) carry_theta = d.theta[rmod(lastall, d.blk_cap)];
     }
-    long long nlast = si[1023];
-    __syncthreads();
-    if (t == 0 && nlast >= 0) carry_theta = d.theta[rmod(nlast, d.blk_cap)];
     __syncthreads();
   }
   if (t == 0) { d.st->theta_prev = carry_theta; d.st->thetau_prev = carry_u; }
@@ -266,91 +276,81 @@ __global__ void __launch_bounds__(256) k_pam_be(RxDev d, InView in, long long b0
 }
 
 // ------------------------------------------------------------------ H8 normalisation
-// fixed-order block reduction of doubles (deterministic)
-__device__ __forceinline__ double block_sum_1024(double v, double *sh) {
+// One cooperative kernel per buffer (P:167 'three kernels: initialization, estimation of the
+// DC-offset, and estimation of the amplitude'; c-5):
+//   dc = mean u, A = mean|u - dc| / (M / (2 (M-1))), u^ = (u - dc) / A
+// over the symbols emitted by blocks [blo, bhi). Each CTA owns a contiguous block range; the
+// two buffer-wide reductions are fixed-order (per-CTA partials, then every CTA sums the
+// partials in index order) separated by grid-wide syncs, so results are deterministic.
+__device__ __forceinline__ double block_sum_det(double v, double *sh) {
   v = warp_sum_d(v);
   if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
   __syncthreads();
   double r = 0.0;
-  if (threadIdx.x < 32) {
-    r = (threadIdx.x < (blockDim.x >> 5)) ? sh[threadIdx.x] : 0.0;
-    r = warp_sum_d(r);
-  }
+  const int nw = blockDim.x >> 5;
+  for (int w = 0; w < nw; ++w) r += sh[w];
   __syncthreads();
-  return r;   // valid in warp 0
+  return r;   // identical in all threads
+}
+__device__ __forceinline__ long long sym_lo_of(const RxDev &d, long long b) {
+  const long long m = d.Mb[rmod(b, d.blk_cap)];
+  return m > 0 ? m : 0;
 }
 
-// dc_beta = sum u / count over the symbols emitted by blocks [blo, bhi)
-__global__ void __launch_bounds__(1024) k_norm_dc(RxDev d, long long beta, long long blo, long long bhi) {
-  __shared__ double sh[32];
-  double s = 0.0, c = 0.0;
-  for (long long b = blo + threadIdx.x; b < bhi; b += blockDim.x) {
-    s += d.blk_sum[rmod(b, d.blk_cap)];
-    const long long Mb = d.Mb[rmod(b, d.blk_cap)], Mb1 = d.Mb[rmod(b + 1, d.blk_cap)];
-    const long long lo = Mb > 0 ? Mb : 0;
-    c += (double)(Mb1 > lo ? Mb1 - lo : 0);
-  }
-  s = block_sum_1024(s, sh);
-  c = block_sum_1024(c, sh);
-  if (threadIdx.x == 0) {
-    d.norm_dc[rmod(beta, d.buf_cap)] = c > 0 ? s / c : 0.0;
-    d.norm_cnt[rmod(beta, d.buf_cap)] = (long long)c;
-  }
-}
-
-// per-block sum |u - dc|
-__global__ void __launch_bounds__(256) k_norm_abs(RxDev d, long long beta, long long blo, long long bhi) {
-  __shared__ double sh[8];
-  const long long b = blo + blockIdx.x;
-  if (b >= bhi) return;
-  const double dc = d.norm_dc[rmod(beta, d.buf_cap)];
-  const long long Mb = d.Mb[rmod(b, d.blk_cap)], Mb1 = d.Mb[rmod(b + 1, d.blk_cap)];
-  const long long lo = Mb > 0 ? Mb : 0;
-  double s = 0.0;
-  for (long long m = lo + threadIdx.x; m < Mb1; m += blockDim.x)
-    s += fabs((double)d.u[rmod(m, d.sym_cap)] - dc);
-  s = warp_sum_d(s);
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += sh[i];
-    d.blk_abs[rmod(b, d.blk_cap)] = t;
-  }
-}
-
-// A = mean|u - dc| / (M / (2 (M-1)))   (c-5)
-__global__ void __launch_bounds__(1024) k_norm_amp(RxDev d, long long beta, long long blo, long long bhi) {
-  __shared__ double sh[32];
-  double s = 0.0;
-  for (long long b = blo + threadIdx.x; b < bhi; b += blockDim.x) s += d.blk_abs[rmod(b, d.blk_cap)];
-  s = block_sum_1024(s, sh);
-  if (threadIdx.x == 0) {
-    const long long c = d.norm_cnt[rmod(beta, d.buf_cap)];
-    const double mal = (double)d.M / (2.0 * (double)(d.M - 1));
-    double A = c > 0 ? (s / (double)c) / mal : 1.0;
-    if (!(A > 0.0)) A = 1.0;
-    d.norm_amp[rmod(beta, d.buf_cap)] = A;
-  }
-}
-
-// u^ = (u - dc) / A; advances the v_front to M_{bhi} (or m_end at flush)
-__global__ void __launch_bounds__(256) k_norm_apply(RxDev d, long long beta, long long blo, long long bhi,
+__global__ void __launch_bounds__(1024) k_norm_coop(RxDev d, long long beta, long long blo, long long bhi,
                                                    int last) {
-  const long long b = blo + blockIdx.x;
-  if (b < bhi) {
-    const float dc = (float)d.norm_dc[rmod(beta, d.buf_cap)];
-    const float inv = (float)(1.0 / d.norm_amp[rmod(beta, d.buf_cap)]);
-    const long long Mb = d.Mb[rmod(b, d.blk_cap)], Mb1 = d.Mb[rmod(b + 1, d.blk_cap)];
-    const long long lo = Mb > 0 ? Mb : 0;
-    for (long long m = lo + threadIdx.x; m < Mb1; m += blockDim.x) {
-      const long long i = rmod(m, d.sym_cap);
-      d.uhat[i] = (d.u[i] - dc) * inv;
-    }
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sh[32];
+  const int G = gridDim.x, g = blockIdx.x, t = threadIdx.x;
+  const long long nb = bhi - blo;
+  const long long cb0 = blo + nb * g / G, cb1 = blo + nb * (g + 1) / G;
+  const long long m0 = sym_lo_of(d, cb0), m1 = sym_lo_of(d, cb1) > m0 ? sym_lo_of(d, cb1) : m0;
+  // phase 1: sum u over the CTA's symbols (from the per-block sums written by k_pam_be)
+  double s = 0.0;
+  for (long long b = cb0 + t; b < cb1; b += blockDim.x) s += d.blk_sum[rmod(b, d.blk_cap)];
+  s = block_sum_det(s, sh);
+  if (t == 0) { d.norm_part[2 * g] = s; d.norm_part[2 * g + 1] = (double)(m1 - m0); }
+  grid.sync();
+  __shared__ double bc[3];
+  if (t < 32) {   // fixed order: lane l sums partials l, l+32, ..., then a fixed shuffle tree
+    double ps = 0.0, pc = 0.0;
+    for (int i = t; i < G; i += 32) { ps += d.norm_part[2 * i]; pc += d.norm_part[2 * i + 1]; }
+    ps = warp_sum_d(ps);
+    pc = warp_sum_d(pc);
+    if (t == 0) { bc[0] = ps; bc[1] = pc; }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    long long f = d.Mb[rmod(bhi, d.blk_cap)];
-    if (f < 0) f = 0;
+  __syncthreads();
+  const double S = bc[0], Cn = bc[1];
+  const double dc = Cn > 0.0 ? S / Cn : 0.0;
+  // phase 2: sum |u - dc|
+  double a = 0.0;
+  for (long long m = m0 + t; m < m1; m += blockDim.x) a += fabs((double)d.u[rmod(m, d.sym_cap)] - dc);
+  a = block_sum_det(a, sh);
+  grid.sync();                                   // everyone has read phase-1 partials
+  if (t == 0) d.norm_part[2 * G + g] = a;
+  grid.sync();
+  if (t < 32) {
+    double pa = 0.0;
+    for (int i = t; i < G; i += 32) pa += d.norm_part[2 * G + i];
+    pa = warp_sum_d(pa);
+    if (t == 0) bc[2] = pa;
+  }
+  __syncthreads();
+  const double Aa = bc[2];
+  const double mal = (double)d.M / (2.0 * (double)(d.M - 1));
+  double A = Cn > 0.0 ? (Aa / Cn) / mal : 1.0;
+  if (!(A > 0.0)) A = 1.0;
+  // phase 3: apply
+  const float dcf = (float)dc, inv = (float)(1.0 / A);
+  for (long long m = m0 + t; m < m1; m += blockDim.x) {
+    const long long i = rmod(m, d.sym_cap);
+    d.uhat[i] = (d.u[i] - dcf) * inv;
+  }
+  if (g == 0 && t == 0) {
+    d.norm_dc[rmod(beta, d.buf_cap)] = dc;
+    d.norm_amp[rmod(beta, d.buf_cap)] = A;
+    d.norm_cnt[rmod(beta, d.buf_cap)] = (long long)Cn;
+    long long f = sym_lo_of(d, bhi);
     d.st->v_front = f;
     if (last) d.st->m_end = f;
   }

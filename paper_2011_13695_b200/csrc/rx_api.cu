@@ -71,6 +71,8 @@ struct rx_handle {
   int sps;
   long long Q;   // 2-sps samples per buffer (KK)
   long long hist_cap;
+  long long lms_launched_upto;   // segment estimate at the last equaliser launch
+  long long norm_G;              // co-resident CTAs of the cooperative normalisation
   // tracing
   int prof_mask;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_pending;
@@ -151,6 +153,7 @@ extern "C" void rx_config_default(rx_config *c, int family, int order) {
   c->sync_window = 2048;
   c->sync_min_corr = 0.3;
   c->history_buffers = 3;
+  c->lms_batch_segments = 2048;
 }
 
 extern "C" const char *rx_strerror(int s) {
@@ -199,8 +202,9 @@ static rx_status validate(const rx_config *c) {
   if (c->family == RX_QAM_KK && c->order > 4 && c->cpr_test_phases == 0) return RX_EINVAL;
   if (c->prbs_order != 15 || (c->prbs_seed & 0x7FFF) == 0) return RX_EINVAL;
   if (c->sync_start < 0 || c->sync_window < 64 || c->sync_window > 4096) return RX_EINVAL;
-  if (c->clock_avg_half < 0 || c->clock_avg_half > 1024) return RX_EINVAL;
+  if (c->clock_avg_half < 0 || c->clock_avg_half > 2048) return RX_EINVAL;
   if (c->history_buffers < 3 || c->history_buffers > 64) return RX_EINVAL;
+  if (c->lms_batch_segments < 0 || c->lms_batch_segments > (1 << 16)) return RX_EINVAL;
   if (c->family == RX_QAM_KK && !(c->sideband == 1 || c->sideband == -1)) return RX_EINVAL;
   if (c->family == RX_PAM && c->thresholds) {
     for (int i = 1; i < c->order - 1; ++i)
@@ -275,16 +279,23 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   d.sync_min = (float)c.sync_min_corr;
   d.warmup = c.warmup_symbols;
   d.cfo_enable = kk ? c.cfo_enable : 0;
+  d.thr_default = cfg->thresholds ? 0 : 1;
+  d.qam_sc = kk ? (float)sqrt(3.0 / (2.0 * (c.order - 1))) : 0.f;
   h->sps = kk ? 4 : 2;
   h->Q = (long long)c.buffer_blocks * 256;
   rx_status s = RX_OK;
 #define TRY(x) do { s = (x); if (s) { rx_destroy(h); return s; } } while (0)
   // ---- constant tables
-  std::vector<float2> tw(1024);
-  for (int k = 0; k < 1024; ++k) {
-    const double a = -2.0 * M_PI * k / 1024.0;
-    tw[k] = make_float2((float)cos(a), (float)sin(a));
-  }
+  std::vector<float2> tw(1024, make_float2(0.f, 0.f));   // layout: see fft.cuh
+  auto w1024 = [](long long k) {
+    const double a = -2.0 * M_PI * (double)(k % 1024) / 1024.0;
+    return make_float2((float)cos(a), (float)sin(a));
+  };
+  for (int k = 0; k < 512; ++k) tw[k] = w1024(k);
+  for (int r = 1; r < 8; ++r)
+    for (int j = 0; j < 64; ++j) tw[TW_P3 + 64 * (r - 1) + j] = w1024(2LL * r * j);
+  for (int r = 1; r < 8; ++r)
+    for (int k = 0; k < 8; ++k) tw[TW_P2 + 8 * (r - 1) + k] = w1024(16LL * r * k);
   TRY(dupload(h, &d.tw, tw));
   // static EQ spectrum H = DFT_1024(h_c), h_c[n mod N] = taps[(L-1)/2 + n] (SURVEY c-0, A3)
   {
@@ -363,7 +374,8 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   TRY(dalloc(h, &d.hist, d.hist_cap));
   d.blk_cap = next_pow2((long long)HB * c.buffer_blocks + 256);
   d.buf_cap = 64;
-  d.sym_cap = next_pow2((long long)HB * c.buffer_blocks * (kk ? 128 : 260));
+  const long long batch_sym = (long long)c.lms_batch_segments * c.lms_segment;
+  d.sym_cap = next_pow2((long long)HB * c.buffer_blocks * (kk ? 128 : 260) + batch_sym);
   if (!kk) {
     TRY(dalloc(h, &d.C, d.blk_cap));
     TRY(dalloc(h, &d.theta, d.blk_cap));
@@ -376,11 +388,21 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
     TRY(dalloc(h, &d.norm_dc, d.buf_cap));
     TRY(dalloc(h, &d.norm_amp, d.buf_cap));
     TRY(dalloc(h, &d.norm_cnt, d.buf_cap));
+    {
+      int nsm = 0, per = 0;
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cuda_device);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_norm_coop, 1024, 0);
+      h->norm_G = (long long)nsm * (per > 0 ? per : 1);
+      if (h->norm_G > 1024) h->norm_G = 1024;
+    }
+    TRY(dalloc(h, &d.norm_part, 4 * 1024));
   } else {
     d.E_cap = next_pow2((long long)HB * c.buffer_blocks * 512);
     d.z_cap = next_pow2((long long)HB * c.buffer_blocks * 256);
     TRY(dalloc(h, &d.E, d.E_cap));
     TRY(dalloc(h, &d.z, d.z_cap));
+    d.zp_cap = next_pow2((long long)HB * c.buffer_blocks * 256 + 2 * batch_sym);
+    TRY(dalloc(h, &d.zp, d.zp_cap));
     TRY(dalloc(h, &d.cfo, d.buf_cap));
     d.cfo_G = 128;
     TRY(dalloc(h, &d.cfo_part, (long long)d.cfo_G * 1024));
@@ -422,7 +444,9 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   // kernels needing > 48 KB dynamic shared memory
   const size_t s2_smem = (1024 + 8 * FFT_PAD_N) * sizeof(float2);
   const size_t cfo_smem = (1024 + 8 * FFT_PAD_N) * sizeof(float2) + 1024 * sizeof(float);
-  if (cudaFuncSetAttribute(k_kk_s2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2_smem) != cudaSuccess ||
+  const size_t clk_smem = (256 + 2 * c.clock_avg_half) * sizeof(double2);
+  if (cudaFuncSetAttribute(k_pam_theta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)clk_smem) != cudaSuccess ||
+      cudaFuncSetAttribute(k_kk_s2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2_smem) != cudaSuccess ||
       cudaFuncSetAttribute(k_cfo_partial, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfo_smem) != cudaSuccess ||
       cudaFuncSetAttribute(k_sync_corr<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536) != cudaSuccess ||
       cudaFuncSetAttribute(k_sync_corr<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536) != cudaSuccess) {
@@ -474,6 +498,10 @@ static void launch_lms_rounds(rx_handle *h, cudaStream_t s, unsigned char *label
   RxDev &d = h->d;
   const long long S = d.S;
   long long seg_lb = h->hm_host->seg_next;   // stale => lower bound
+  // batching: wait until ~lms_batch_segments segments may be pending (host-side estimate)
+  const long long est_ready = sym_ub / S - h->lms_launched_upto;
+  if (!flush && h->cfg.lms_batch_segments > 0 && est_ready < h->cfg.lms_batch_segments) return;
+  h->lms_launched_upto = sym_ub / S;
   long long seg_ub = sym_ub / S + 1;
   long long nseg = seg_ub - seg_lb + 1;
   if (nseg < 1) nseg = 1;
@@ -506,7 +534,8 @@ static void run_pam(rx_handle *h, cudaStream_t s, const InView &in, unsigned cha
   }
   long long clk_target = flush ? h->fe_done : h->fe_done - d.clock_half;
   if (clk_target > h->clk_done) {
-    KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_pam_theta<<<gridc(clk_target - h->clk_done, 256), 256, 0, s>>>(d, h->clk_done, clk_target, h->fe_done - 1)));
+    const size_t smem = (256 + 2 * d.clock_half) * sizeof(double2);
+    KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_pam_theta<<<gridc(clk_target - h->clk_done, 256), 256, smem, s>>>(d, h->clk_done, clk_target, h->fe_done - 1)));
     KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_pam_unwrap<<<1, 1024, 0, s>>>(d, h->clk_done, clk_target)));
     h->clk_done = clk_target;
   }
@@ -520,10 +549,12 @@ static void run_pam(rx_handle *h, cudaStream_t s, const InView &in, unsigned cha
     long long bhi = blo + BB;
     if (bhi > h->be_done) bhi = h->be_done;
     const long long beta = h->norm_done;
-    KLAUNCH(h, RX_K_NORM, s, (k_norm_dc<<<1, 1024, 0, s>>>(d, beta, blo, bhi)));
-    KLAUNCH(h, RX_K_NORM, s, (k_norm_abs<<<(unsigned)(bhi - blo), 256, 0, s>>>(d, beta, blo, bhi)));
-    KLAUNCH(h, RX_K_NORM, s, (k_norm_amp<<<1, 1024, 0, s>>>(d, beta, blo, bhi)));
-    KLAUNCH(h, RX_K_NORM, s, (k_norm_apply<<<(unsigned)(bhi - blo), 256, 0, s>>>(d, beta, blo, bhi, 0)));
+    {
+      const int last = (flush && bhi == h->be_done) ? 1 : 0;
+      long long G = bhi - blo < h->norm_G ? bhi - blo : h->norm_G;
+      void *args[] = {(void *)&d, (void *)&beta, (void *)&blo, (void *)&bhi, (void *)&last};
+      KLAUNCH(h, RX_K_NORM, s, cudaLaunchCooperativeKernel((void *)k_norm_coop, dim3((unsigned)G), dim3(1024), args, 0, s));
+    }
     h->norm_done++;
   }
   if (flush) KLAUNCH(h, RX_K_MISC, s, (k_pam_mend<<<1, 1, 0, s>>>(d, h->be_done > 0 ? h->be_done : 0)));
@@ -556,6 +587,7 @@ static void run_kk(rx_handle *h, cudaStream_t s, const InView &in, unsigned char
     KLAUNCH(h, RX_K_CFO, s, (k_cfo_final<<<1, 1024, 0, s>>>(d, h->cfo_done, qlo, qhi)));
     if (d.cfo_enable) KLAUNCH(h, RX_K_CFO, s, (k_cfo_fine<<<296, 256, 0, s>>>(d, h->cfo_done, qlo, qhi)));
     KLAUNCH(h, RX_K_CFO, s, (k_cfo_fine_final<<<1, 1024, 0, s>>>(d, h->cfo_done, qlo, qhi)));
+    KLAUNCH(h, RX_K_CFO, s, (k_kk_zprime<<<gridc(qhi - qlo, 256) < 4096 ? gridc(qhi - qlo, 256) : 4096, 256, 0, s>>>(d, h->cfo_done, qlo, qhi)));
     h->cfo_done++;
   }
   launch_sync_train<true>(h, s, flush);

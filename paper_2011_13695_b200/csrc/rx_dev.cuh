@@ -65,6 +65,8 @@ struct RxDev {
   float sync_min;
   long long warmup;
   int cfo_enable;
+  int thr_default;           // PAM thresholds are the ideal midpoints (closed-form slicer)
+  float qam_sc;              // QAM per-axis unit: levels (2i - L + 1) qam_sc
   // ---- constant tables (device)
   const float2 *tw;          // e^{-2 pi i k/1024}, k < 1024
   const float2 *H;           // static-EQ spectrum [1024]
@@ -80,8 +82,10 @@ struct RxDev {
   long long blk_cap;
   float *u; float *uhat; long long sym_cap;
   double *norm_dc; double *norm_amp; long long *norm_cnt; long long buf_cap;
+  double *norm_part;                // cooperative-reduction scratch [4 * NORM_G]
   float2 *E; long long E_cap;
   float2 *z; long long z_cap;
+  float2 *zp; long long zp_cap;     // z' = normalised, CFO-removed 2-sps field
   CfoParam *cfo; float *cfo_part; double *cfo_pow; double2 *cfo_a; int cfo_G;
   // ---- sync scratch
   float *sync_g; float2 *sync_c;

@@ -40,6 +40,7 @@ class RxConfig(ctypes.Structure):
         ("prbs_order", ctypes.c_uint), ("prbs_seed", ctypes.c_uint),
         ("sync_start", _c_ll), ("sync_window", ctypes.c_int), ("sync_min_corr", ctypes.c_double),
         ("warmup_symbols", _c_ll), ("history_buffers", ctypes.c_int),
+        ("lms_batch_segments", ctypes.c_int),
     ]
 
 
