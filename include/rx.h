@@ -124,7 +124,8 @@ rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle **out);
 
 /* Enqueue the chain on the next n_samples of the stream (u12 codes right-aligned in uint16,
  * the ADC format of P:136 / S:602). n_samples must be a multiple of hop and at most
- * buffer_blocks*hop. Samples are consumed in stream order (the overlap kernels are
+ * (history_buffers - 2) * buffer_blocks * hop (one paper buffer with the default rings).
+ * Samples are consumed in stream order (the overlap kernels are
  * chained). Outputs lag the input (held-back tail: 52 blocks of clock look-ahead for PAM,
  * one stage-2 block for KK, one buffer of normalisation, one LMS segment); everything that
  * becomes final is processed. The label of absolute symbol m is written to
@@ -134,7 +135,9 @@ rx_status rx_process(rx_handle *h, const unsigned short *d_samples, long long n_
                      unsigned char *d_labels, long long labels_capacity, void *cuda_stream);
 
 /* End of stream: drain the tail with truncated windows (SURVEY c-3, A14) and finish every
- * symbol. After rx_flush only rx_get_stats / rx_probe / rx_destroy are valid. */
+ * symbol (the one call that synchronises cuda_stream, to run as many equaliser rounds as the
+ * lag-D seed dependencies of the remaining segments need). After rx_flush only
+ * rx_get_stats / rx_probe / rx_destroy are valid. */
 rx_status rx_flush(rx_handle *h, unsigned char *d_labels, long long labels_capacity,
                    void *cuda_stream);
 

@@ -54,7 +54,9 @@ struct InView {
   long long call_start;
   long long call_end;
   const uint16_t *hist;
-  long long hist_cap;   // power of two
+  long long hist_cap;   // power of two, > max call size + lookback + keep
+  uint16_t *hist_w;     // front-end kernels append the call's last samples here
+  long long keep_from;  // samples p >= keep_from of this call are kept in the history ring
 };
 __device__ __forceinline__ int in_code(const InView &v, long long p, bool &pad) {
   pad = p < 0;
@@ -71,6 +73,12 @@ __device__ __forceinline__ void load16(const InView &v, long long p, float scale
   if (p >= v.call_start && p + 16 <= v.call_end) {
     const uint4 *src = reinterpret_cast<const uint4 *>(v.cur + (p - v.call_start));
     uint4 a = __ldg(src), b = __ldg(src + 1);
+    // owned (new) samples of the call's tail go to the history ring for later calls
+    if (p >= count_from && p >= v.keep_from) {
+      uint4 *dst = reinterpret_cast<uint4 *>(v.hist_w + (p & (v.hist_cap - 1)));
+      dst[0] = a;
+      dst[1] = b;
+    }
     uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
     for (int i = 0; i < 8; ++i) {

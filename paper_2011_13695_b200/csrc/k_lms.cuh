@@ -6,6 +6,7 @@
 // the segment-parallel block-LMS of SURVEY c-9: one warp owns one segment of S symbols,
 // lane i owns symbol i of each B = 32 block, lane k owns tap k; CPR and decisions are fused.
 #pragma once
+#include <type_traits>
 #include "k_kk.cuh"
 
 
@@ -150,19 +151,65 @@ __global__ void __launch_bounds__(1024) k_sync_pick(RxDev d, int flush) {
 // run with 4 independent accumulators; lane i owns symbol i of the block, lane k tap k; the
 // sliding window of inputs lives in shared memory (double-buffered, next block prefetched
 // into registers while the current block computes).
-#define LMS_WMAX 96
+#define LMS_RING 512        // per-warp input ring (power of two), absolute index & (LMS_RING-1)
+#define LMS_AHEAD 4         // blocks of lookahead staged by cp.async
 
 template <bool CPLX>
 struct LmsSmemT {
-  float2 win[2][LMS_WMAX];
+  typename std::conditional<CPLX, float2, float>::type ring[LMS_RING];
   float2 w[32];
   float2 e[32];
   float2 y[32];
 };
 
+__device__ __forceinline__ void cp_async_elem(float *dst, const float *src, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(src), "r"(valid ? 4 : 0));
+}
+__device__ __forceinline__ void cp_async_elem(float2 *dst, const float2 *src, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(src), "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// stage input samples [i0, i1) (absolute index of u^ (PAM) or z' (KK)) into the ring; zero
+// outside [0, vend) (cp.async zero-fill)
+template <bool CPLX>
+__device__ __forceinline__ void lms_stage(const RxDev &d, LmsSmemT<CPLX> &sm, long long i0, long long i1,
+                                          long long vend) {
+  const int lane = threadIdx.x & 31;
+  for (long long i = i0 + lane; i < i1; i += 32) {
+    const bool ok = i >= 0 && i < vend;
+    if (CPLX) {
+      const float2 *src = ok ? d.zp + rmod(i, d.zp_cap) : d.zp;
+      cp_async_elem(reinterpret_cast<float2 *>(sm.ring) + (i & (LMS_RING - 1)), src, ok);
+    } else {
+      const float *src = ok ? d.uhat + rmod(i, d.sym_cap) : d.uhat;
+      cp_async_elem(reinterpret_cast<float *>(sm.ring) + (i & (LMS_RING - 1)), src, ok);
+    }
+  }
+}
+
+template <bool CPLX>
+__device__ __forceinline__ float2 ring_at(const LmsSmemT<CPLX> &sm, long long i) {
+  if (CPLX) return reinterpret_cast<const float2 *>(sm.ring)[i & (LMS_RING - 1)];
+  return make_float2(reinterpret_cast<const float *>(sm.ring)[i & (LMS_RING - 1)], 0.f);
+}
+
 // decision level value of index i: PAM (2i - M + 1)/(M - 1); QAM axis (2i - L + 1) sc
 __device__ __forceinline__ float level_of(int i, float two_s, float off) { return fmaf((float)i, two_s, off); }
 
+// One warp runs block-LMS over symbols [t_begin, t_end) starting from tap wk (lane k).
+// MODE 0: training (e = r - y, no CPR), MODE 1: decision directed with CPR `CPR`
+// (0 none, 1 VV, 2 BPS). Outputs for m >= out_lo go to the level / yout rings,
+// warm-up decisions (m < out_lo) to warm[]. Returns final theta; accumulates EVM.
+//
+// Layout: taps are padded to KP = 4 ceil(K/4) (zero taps, exact) so the K-term dot products
+// run with 4 independent accumulators; lane i owns symbol i of the block, lane k tap k; the
+// inputs stream through a per-warp shared-memory ring filled LMS_AHEAD blocks ahead with
+// cp.async (the serial block recursion never waits on HBM).
 template <bool CPLX, int CPR, int MODE>
 __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, long long t_end,
                          long long out_lo, float2 &wk, unsigned char *warm, double &evn,
@@ -171,16 +218,15 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
   const int K = d.K, c = K >> 1, KP = (K + 3) & ~3;
   const int stride = CPLX ? 2 : 1;
   const int off = CPLX ? d.st->sync_phase : 0;
-  const int WL = stride * 31 + KP;
+  const int WL = stride * 31 + KP;          // window of one block
+  const int DS = stride * 32;               // window shift per block
   const float mu = d.mu;
-  // slicer constants: index = floor(v * inv2s + L/2) clamped; level = i * two_s + lvl0
   const int L = d.L;
   const float two_s = CPLX ? 2.0f * d.qam_sc : 2.0f / (float)(d.M - 1);
   const float lvl0 = CPLX ? -(float)(L - 1) * d.qam_sc : -1.0f;
   const float inv2s = 1.0f / two_s;
   const long long o_ref = d.st->sync_offset;
   const int ref0 = MODE == 0 ? (int)(((o_ref + t_begin - d.m0) % RX_PREF + RX_PREF) % RX_PREF) : 0;
-  // BPS test-phase rotations for phases lane and lane + 32 (e^{-j phi_p})
   float2 rotA = make_float2(1.f, 0.f), rotB = make_float2(1.f, 0.f);
   if (CPR == 2) {
     if (lane < d.Pt) rotA = __ldg(d.bps_rot + lane);
@@ -189,30 +235,33 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
   float theta = 0.f;
   if (lane >= K) wk = make_float2(0.f, 0.f);
   sm.w[lane] = wk;
-  long long wb = (long long)stride * t_begin + off + c - (KP - 1);
-  for (int x = lane; x < WL; x += 32) sm.win[0][x] = lms_in<CPLX>(d, wb + x, vend);
-  __syncwarp();
-  int buf = 0;
+  const long long wb0 = (long long)stride * t_begin + off + c - (KP - 1);
+  const long long nblk = (t_end - t_begin + 31) / 32;
+  // prologue: block 0's window, then the new samples of blocks 1 .. AHEAD-1 (one group each)
+  lms_stage<CPLX>(d, sm, wb0, wb0 + WL, vend);
+  cp_async_commit();
+#pragma unroll 1
+  for (int g = 1; g < LMS_AHEAD; ++g) {
+    if (g < nblk) lms_stage<CPLX>(d, sm, wb0 + WL + (long long)(g - 1) * DS, wb0 + WL + (long long)g * DS, vend);
+    cp_async_commit();
+  }
   bool first = true;
-  for (long long t = t_begin; t < t_end; t += 32) {
-    float2 pre[3];
-    const long long wbn = wb + (long long)stride * 32;
-    const bool more = t + 32 < t_end;
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      const int x = lane + 32 * q;
-      pre[q] = (more && x < WL) ? lms_in<CPLX>(d, wbn + x, vend) : make_float2(0.f, 0.f);
-    }
-    const float2 *cur = sm.win[buf];
+  long long wb = wb0;
+#pragma unroll 1
+  for (long long jb = 0; jb < nblk; ++jb) {
+    const long long t = t_begin + 32 * jb;
+    cp_async_wait<LMS_AHEAD - 1>();
+    __syncwarp();
     const int nvalid = (int)((t_end - t) < 32 ? (t_end - t) : 32);
     const bool valid = lane < nvalid;
     const long long m = t + lane;
-    // y_i = w^H u_i, u_i[k] = cur[stride i + KP-1-k]
+    // y_i = w^H u_i, u_i[k] = x[wb + stride i + KP-1-k]
     float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
-    const float2 *ub = cur + stride * lane + KP - 1;
+    const long long ub = wb + stride * lane + KP - 1;
     for (int k = 0; k < KP; k += 4) {
       const float2 w0 = sm.w[k], w1 = sm.w[k + 1], w2 = sm.w[k + 2], w3 = sm.w[k + 3];
-      const float2 u0 = ub[-k], u1 = ub[-k - 1], u2 = ub[-k - 2], u3 = ub[-k - 3];
+      const float2 u0 = ring_at<CPLX>(sm, ub - k), u1 = ring_at<CPLX>(sm, ub - k - 1);
+      const float2 u2 = ring_at<CPLX>(sm, ub - k - 2), u3 = ring_at<CPLX>(sm, ub - k - 3);
       a0.x = fmaf(w0.x, u0.x, a0.x); a1.x = fmaf(w1.x, u1.x, a1.x);
       a2.x = fmaf(w2.x, u2.x, a2.x); a3.x = fmaf(w3.x, u3.x, a3.x);
       if (CPLX) {
@@ -244,18 +293,21 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
           sm.y[lane] = y;
           __syncwarp();
           float dA = 0.f, dB = 0.f;
+          const float Lh = 0.5f * (float)L, Lm1 = (float)(L - 1);
           for (int i = 0; i < nvalid; ++i) {
             const float2 yi = sm.y[i];
             {
               const float2 zr = cmul(yi, rotA);
-              const int iI = slice_axis(zr.x, inv2s, L), iQ = slice_axis(zr.y, inv2s, L);
-              const float dx = zr.x - level_of(iI, two_s, lvl0), dy = zr.y - level_of(iQ, two_s, lvl0);
+              const float fi = fminf(fmaxf(floorf(fmaf(zr.x, inv2s, Lh)), 0.f), Lm1);
+              const float fq = fminf(fmaxf(floorf(fmaf(zr.y, inv2s, Lh)), 0.f), Lm1);
+              const float dx = zr.x - fmaf(fi, two_s, lvl0), dy = zr.y - fmaf(fq, two_s, lvl0);
               dA += fmaf(dx, dx, dy * dy);
             }
             if (d.Pt > 32) {
               const float2 zr = cmul(yi, rotB);
-              const int iI = slice_axis(zr.x, inv2s, L), iQ = slice_axis(zr.y, inv2s, L);
-              const float dx = zr.x - level_of(iI, two_s, lvl0), dy = zr.y - level_of(iQ, two_s, lvl0);
+              const float fi = fminf(fmaxf(floorf(fmaf(zr.x, inv2s, Lh)), 0.f), Lm1);
+              const float fq = fminf(fmaxf(floorf(fmaf(zr.y, inv2s, Lh)), 0.f), Lm1);
+              const float dx = zr.x - fmaf(fi, two_s, lvl0), dy = zr.y - fmaf(fq, two_s, lvl0);
               dB += fmaf(dx, dx, dy * dy);
             }
           }
@@ -304,11 +356,12 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
     // gradient: lane k: g_k = sum_i u_i[k] conj(e_i); w <- w + mu g   (c-9 step 7)
     {
       float2 g0 = make_float2(0.f, 0.f), g1 = g0, g2 = g0, g3 = g0;
-      const float2 *ug = cur + KP - 1 - (lane < KP ? lane : 0);   // lanes >= KP: discarded
+      const long long ug = wb + KP - 1 - (lane < KP ? lane : 0);   // lanes >= KP: discarded
 #pragma unroll
       for (int i = 0; i < 32; i += 4) {
         const float2 e0 = sm.e[i], e1 = sm.e[i + 1], e2 = sm.e[i + 2], e3 = sm.e[i + 3];
-        const float2 u0 = ug[stride * i], u1 = ug[stride * (i + 1)], u2 = ug[stride * (i + 2)], u3 = ug[stride * (i + 3)];
+        const float2 u0 = ring_at<CPLX>(sm, ug + stride * i), u1 = ring_at<CPLX>(sm, ug + stride * (i + 1));
+        const float2 u2 = ring_at<CPLX>(sm, ug + stride * (i + 2)), u3 = ring_at<CPLX>(sm, ug + stride * (i + 3));
         g0.x = fmaf(u0.x, e0.x, g0.x); g1.x = fmaf(u1.x, e1.x, g1.x);
         g2.x = fmaf(u2.x, e2.x, g2.x); g3.x = fmaf(u3.x, e3.x, g3.x);
         if (CPLX) {
@@ -327,17 +380,15 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
       }
     }
     sm.w[lane] = wk;
-    float2 *nxt = sm.win[buf ^ 1];
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      const int x = lane + 32 * q;
-      if (x < WL) nxt[x] = pre[q];
-    }
     __syncwarp();
-    buf ^= 1;
-    wb = wbn;
+    // stage the new samples of block jb + AHEAD (the slots of block jb are no longer read)
+    const long long jn = jb + LMS_AHEAD;
+    if (jn < nblk) lms_stage<CPLX>(d, sm, wb0 + WL + (jn - 1) * DS, wb0 + WL + jn * DS, vend);
+    cp_async_commit();
+    wb += DS;
     first = false;
   }
+  cp_async_wait<0>();
   const float nrm = warp_sum(lane < K ? cabs2(wk) : 0.f);
   if (lane == 0 && nrm > 1e6f) set_flag(d.st, RX_FLAG_DIVERGE);
   return theta;
@@ -612,10 +663,10 @@ __global__ void __launch_bounds__(256) k_lms_final(RxDev d, unsigned char *label
   }
 }
 
-// Counters in fixed order + epoch seeds (mean canonical taps) for epochs fully finalised.
-__global__ void __launch_bounds__(1024) k_lms_epoch(RxDev d, int flush) {
-  __shared__ double sh[32];
-  __shared__ long long shl[32];
+// Counters in fixed order (one CTA) ...
+__global__ void __launch_bounds__(1024) k_lms_counters(RxDev d) {
+  __shared__ double sh[32], sh2[32];
+  __shared__ long long shl[32], shl2[32];
   DevState *st = d.st;
   const long long lo = st->fin_lo, hi = st->fin_hi;
   const int t = threadIdx.x;
@@ -634,8 +685,6 @@ __global__ void __launch_bounds__(1024) k_lms_epoch(RxDev d, int flush) {
     er += __shfl_xor_sync(0xffffffffu, er, o);
     ct += __shfl_xor_sync(0xffffffffu, ct, o);
   }
-  __shared__ double sh2[32];
-  __shared__ long long shl2[32];
   if ((t & 31) == 0) { sh[t >> 5] = en; sh2[t >> 5] = ed; shl[t >> 5] = er; shl2[t >> 5] = ct; }
   __syncthreads();
   if (t == 0) {
@@ -651,44 +700,46 @@ __global__ void __launch_bounds__(1024) k_lms_epoch(RxDev d, int flush) {
     if (st->m_end >= 0 && so > st->m_end) so = st->m_end;
     if (hi > lo) st->symbols_out = so;
   }
-  __syncthreads();
-  // epoch seeds: epochs e with all segments < hi finalised
+}
+
+// ... and the lag-D epoch seeds: CTA i owns epoch fin_lo/spe + i; when all its segments are
+// finalised the seed of epoch e + D is the mean of their canonical taps (fixed order).
+__global__ void __launch_bounds__(1024) k_lms_seeds(RxDev d, int flush) {
+  DevState *st = d.st;
+  const long long lo = st->fin_lo, hi = st->fin_hi;
   const long long spe = d.E_sym / d.S;
-  const long long e_lo = lo / spe;
-  long long e_hi = hi / spe;   // epochs [e_lo, e_hi) complete
+  const long long e = lo / spe + blockIdx.x;
+  long long e_hi = hi / spe;                      // epochs [., e_hi) complete
   if (flush && st->m_end >= 0 && hi * (long long)d.S >= st->m_end) e_hi = (hi + spe - 1) / spe;
-  for (long long e = e_lo; e < e_hi; ++e) {
-    const long long tgt = e + d.D;
-    if (d.seed_ready[rmod(tgt, d.seed_cap)] == tgt + 1) continue;
-    const long long s_lo = e * spe;
-    long long s_hi = s_lo + spe;
-    if (s_hi > hi) s_hi = hi;
-    // thread layout: k = t >> 5 (tap), lane sums segments lane, lane+32, ... in fixed order
-    const int k = t >> 5, lane = t & 31;
-    float sx = 0.f, sy = 0.f;
-    if (k < d.K) {
-      long long s = s_lo + lane;
-      for (; s + 96 < s_hi; s += 128) {          // 4 independent loads in flight, summed in order
-        const float2 w0 = d.seg_w[rmod(s, d.seg_cap) * RX_MAX_K + k];
-        const float2 w1 = d.seg_w[rmod(s + 32, d.seg_cap) * RX_MAX_K + k];
-        const float2 w2 = d.seg_w[rmod(s + 64, d.seg_cap) * RX_MAX_K + k];
-        const float2 w3 = d.seg_w[rmod(s + 96, d.seg_cap) * RX_MAX_K + k];
-        sx += w0.x; sy += w0.y; sx += w1.x; sy += w1.y;
-        sx += w2.x; sy += w2.y; sx += w3.x; sy += w3.y;
-      }
-      for (; s < s_hi; s += 32) {
-        const float2 w = d.seg_w[rmod(s, d.seg_cap) * RX_MAX_K + k];
-        sx += w.x; sy += w.y;
-      }
+  if (e >= e_hi || hi <= lo) return;
+  const long long tgt = e + d.D;
+  if (d.seed_ready[rmod(tgt, d.seed_cap)] == tgt + 1) return;
+  const long long s_lo = e * spe;
+  long long s_hi = s_lo + spe;
+  if (s_hi > hi) s_hi = hi;
+  const int t = threadIdx.x, k = t >> 5, lane = t & 31;
+  float sx = 0.f, sy = 0.f;
+  if (k < d.K) {
+    long long s = s_lo + lane;
+    for (; s + 96 < s_hi; s += 128) {          // 4 independent loads in flight, summed in order
+      const float2 w0 = d.seg_w[rmod(s, d.seg_cap) * RX_MAX_K + k];
+      const float2 w1 = d.seg_w[rmod(s + 32, d.seg_cap) * RX_MAX_K + k];
+      const float2 w2 = d.seg_w[rmod(s + 64, d.seg_cap) * RX_MAX_K + k];
+      const float2 w3 = d.seg_w[rmod(s + 96, d.seg_cap) * RX_MAX_K + k];
+      sx += w0.x; sy += w0.y; sx += w1.x; sy += w1.y;
+      sx += w2.x; sy += w2.y; sx += w3.x; sy += w3.y;
     }
-    sx = warp_sum(sx);
-    sy = warp_sum(sy);
-    if (k < d.K && lane == 0) {
-      const float inv = 1.0f / (float)(s_hi - s_lo);
-      d.seed[rmod(tgt, d.seed_cap) * RX_MAX_K + k] = make_float2(sx * inv, sy * inv);
+    for (; s < s_hi; s += 32) {
+      const float2 w = d.seg_w[rmod(s, d.seg_cap) * RX_MAX_K + k];
+      sx += w.x; sy += w.y;
     }
-    __syncthreads();
-    if (t == 0) { __threadfence(); d.seed_ready[rmod(tgt, d.seed_cap)] = (int)(tgt + 1); }
-    __syncthreads();
   }
+  sx = warp_sum(sx);
+  sy = warp_sum(sy);
+  if (k < d.K && lane == 0) {
+    const float inv = 1.0f / (float)(s_hi - s_lo);
+    d.seed[rmod(tgt, d.seed_cap) * RX_MAX_K + k] = make_float2(sx * inv, sy * inv);
+  }
+  __syncthreads();
+  if (t == 0) { __threadfence(); d.seed_ready[rmod(tgt, d.seed_cap)] = (int)(tgt + 1); }
 }

@@ -1,15 +1,13 @@
 // k_pam.cuh — IMDD PAM-N chain kernels (§III).
 //
 //  k_pam_fe     H0-H3  ingest + overlap framing + R2C FFT-1024 + static FD EQ + C_b
-//  k_pam_theta  H4a    105-block complex average + atan2 (parallel, shared-memory C tiles)
-//  k_pam_unwrap H4b    unwrap as a prefix sum of wrapped differences -> tau_b, M_b (one CTA)
+//  k_pam_theta/carry/tau  H4  105-block complex average + atan2 + unwrap as a prefix sum of
+//                      wrapped differences (tile-local scans, one-CTA carry scan) -> tau_b, M_b
 //  k_pam_be     H1,H2,H5-H7  re-FFT + EQ + FD clock correction + C2R IFFT + extraction
-//  k_norm_coop  H8     buffer-wise DC / amplitude normalisation (one cooperative launch)
+//  k_norm_*     H8     buffer-wise DC / amplitude normalisation (stats + apply)
 #pragma once
 #include "fft.cuh"
 #include "rx_dev.cuh"
-#include <cooperative_groups.h>
-namespace cg = cooperative_groups;
 
 #define FE_GROUPS 4
 
@@ -103,97 +101,137 @@ __device__ __forceinline__ long long warp_incl_max_ll(long long v) {
   return v;
 }
 
-// (a) theta_b for blocks [b0, b1): one CTA per 256 blocks, C tile (+ 2h halo) in shared
-//     memory, each thread sums its own 105-term window (consecutive lanes, conflict-free).
-__global__ void __launch_bounds__(256) k_pam_theta(RxDev d, long long b0, long long b1, long long blast) {
-  extern __shared__ double2 Ct[];                 // [256 + 2 h]
-  const int t = threadIdx.x, hh = d.clock_half;
-  const long long base = b0 + (long long)blockIdx.x * 256;
-  for (int i = t; i < 256 + 2 * hh; i += blockDim.x) {
-    const long long b = base - hh + i;
+// Three launches, all but (b) fully parallel:
+// (a) k_pam_theta: one CTA per 256 blocks. Cbar_b from a shared-memory C tile (+2h halo),
+//     theta_b = atan2(Cbar_b) (|Cbar| = 0 inherits the previous phase), the wrapped
+//     differences w(theta_b - theta_{b-1}) and their CTA-local inclusive prefix (double).
+// (b) k_pam_carry: one CTA scans the CTA totals -> per-CTA offsets (+ the call's carry).
+// (c) k_pam_tau: tau_b = -(offset + local prefix) / 2 pi, M_b = ceil(256 b - 128 - tau_b).
+#define CLK_TILE 256
+__device__ __forceinline__ double theta_of(const double2 *Ct, int i, int hh) {   // window at tile i
+  double sr = 0.0, si = 0.0;
+  for (int k = 0; k <= 2 * hh; ++k) { const double2 c = Ct[i + k]; sr += c.x; si += c.y; }
+  return (sr == 0.0 && si == 0.0) ? __longlong_as_double(0x7ff8000000000000LL) : atan2(si, sr);
+}
+
+__global__ void __launch_bounds__(CLK_TILE) k_pam_theta(RxDev d, long long b0, long long b1, long long blast) {
+  extern __shared__ double2 Ct[];                 // [CLK_TILE + 1 + 2 h]: blocks base-1-h ..
+  __shared__ double th_sh[CLK_TILE + 1];
+  __shared__ double wsum[CLK_TILE / 32];
+  __shared__ long long wmax[CLK_TILE / 32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, hh = d.clock_half;
+  const double TWO_PI = 6.283185307179586476925, INV_2PI = 0.15915494309189533577;
+  const long long base = b0 + (long long)blockIdx.x * CLK_TILE;
+  for (int i = t; i < CLK_TILE + 1 + 2 * hh; i += blockDim.x) {
+    const long long b = base - 1 - hh + i;
     Ct[i] = (b >= 0 && b <= blast) ? d.C[rmod(b, d.blk_cap)] : make_double2(0.0, 0.0);
   }
   __syncthreads();
+  // theta of blocks base-1+i, i = 0..CLK_TILE (entry 0 = the previous block, for the difference)
+  th_sh[t + 1] = (base + t < b1) ? theta_of(Ct, t + 1, hh) : __longlong_as_double(0x7ff8000000000000LL);
+  if (t == 0) {
+    double p = __longlong_as_double(0x7ff8000000000000LL);
+    if (base - 1 >= b0) p = theta_of(Ct, 0, hh);
+    th_sh[0] = p;
+  }
+  __syncthreads();
   const long long b = base + t;
-  if (b >= b1) return;
-  double sr = 0.0, si = 0.0;
-  for (int i = 0; i <= 2 * hh; ++i) { const double2 c = Ct[t + i]; sr += c.x; si += c.y; }
-  d.theta[rmod(b, d.blk_cap)] = (sr == 0.0 && si == 0.0) ? __longlong_as_double(0x7ff8000000000000LL)
-                                                         : atan2(si, sr);
+  // resolve inherited phases: last valid theta at or before each entry (max-scan of indices)
+  long long last = isnan(th_sh[t + 1]) ? -1 : t + 1;
+  long long inc = last;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o && v > inc) inc = v;
+  }
+  if (lane == 31) wmax[warp] = inc;
+  __syncthreads();
+  long long pre = -1;
+  for (int w = 0; w < warp; ++w) pre = wmax[w] > pre ? wmax[w] : pre;
+  long long excl = __shfl_up_sync(0xffffffffu, inc, 1);   // all lanes shuffle
+  if (lane == 0) excl = -1;
+  long long src_prev = excl > pre ? excl : pre;          // last valid entry before t+1 in tile
+  long long src_cur = inc > pre ? inc : pre;             // last valid entry at or before t+1
+  // entry 0 (previous block) and anything before the tile: walk back through global theta
+  auto resolve_before = [&](void) -> double {
+    if (!isnan(th_sh[0])) return th_sh[0];
+    for (long long q = base - 2; q >= b0; --q) {         // rare: |Cbar| = 0 runs; recompute
+      double sr = 0.0, si = 0.0;                         // from C (other tiles may not have
+      for (long long k = q - hh; k <= q + hh; ++k)       // written theta yet)
+        if (k >= 0 && k <= blast) { const double2 c = d.C[rmod(k, d.blk_cap)]; sr += c.x; si += c.y; }
+      if (!(sr == 0.0 && si == 0.0)) return atan2(si, sr);
+    }
+    return d.st->theta_prev;                             // resolved phase before this call
+  };
+  const double tprev = src_prev >= 1 ? th_sh[src_prev] : resolve_before();
+  const double tcur = src_cur >= 1 ? th_sh[src_cur] : resolve_before();
+  double diff = 0.0;
+  if (b < b1) {
+    const double dd = tcur - tprev;
+    diff = dd - TWO_PI * rint(dd * INV_2PI);
+    if (b == 0) diff = tcur;                             // theta^u_0 = theta_0 (theta_{-1} = 0)
+  }
+  // CTA-local inclusive prefix of the wrapped differences
+  double incl = diff;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  double off = 0.0;
+  for (int w = 0; w < warp; ++w) off += wsum[w];
+  if (b < b1) d.tau[rmod(b, d.blk_cap)] = off + incl;    // local prefix (finished by k_pam_tau)
+  if (t == CLK_TILE - 1) {
+    double tot = 0.0;
+    for (int w = 0; w < CLK_TILE / 32; ++w) tot += wsum[w];
+    d.clk_part[blockIdx.x] = tot;
+    d.clk_last[blockIdx.x] = tcur;                       // resolved phase of the tile's last block
+  }
+  (void)INV_2PI;
 }
 
-// (b) one CTA: |Cbar| = 0 inherits the previous phase (max-scan of the last valid block),
-//     wrapped differences, prefix sum (warp-shuffle block scan), tau_b and M_b.
-__global__ void __launch_bounds__(1024) k_pam_unwrap(RxDev d, long long b0, long long b1) {
-  __shared__ double wsum[32];
-  __shared__ long long wmax[32];
-  __shared__ double carry_theta, carry_u;
+// (b) offsets of the tiles (exclusive scan of the tile totals, plus the carried unwrapped phase)
+__global__ void __launch_bounds__(1024) k_pam_carry(RxDev d, int ntiles) {
+  __shared__ double ws[32];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const double TWO_PI = 6.283185307179586476925;
-  if (t == 0) { carry_theta = d.st->theta_prev; carry_u = d.st->thetau_prev; }
-  __syncthreads();
-  for (long long base = b0; base < b1; base += CLK_CHUNK) {
-    const long long nb = (b1 - base) < CLK_CHUNK ? (b1 - base) : CLK_CHUNK;
-    double th[8];
-    long long last = -1;
+  double carry = d.st->thetau_prev;
+  for (int c0 = 0; c0 < ntiles; c0 += 1024) {
+    const int i = c0 + t;
+    const double v = i < ntiles ? d.clk_part[i] : 0.0;
+    double incl = v;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const long long j = 8 * t + q;
-      th[q] = __longlong_as_double(0x7ff8000000000000LL);
-      if (j < nb) th[q] = d.theta[rmod(base + j, d.blk_cap)];
-      if (j < nb && !isnan(th[q])) last = base + j;
+    for (int o = 1; o < 32; o <<= 1) {
+      const double u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
     }
-    const long long lw = warp_incl_max_ll(last);
-    if (lane == 31) wmax[warp] = lw;
+    if (lane == 31) ws[warp] = incl;
     __syncthreads();
-    if (warp == 0) wmax[lane] = warp_incl_max_ll(wmax[lane]);
+    double off = 0.0;
+    for (int w = 0; w < warp; ++w) off += ws[w];
+    double tot = 0.0;
+    for (int w = 0; w < 32; ++w) tot += ws[w];
+    if (i < ntiles) d.clk_off[i] = carry + off + incl - v;
     __syncthreads();
-    long long excl = __shfl_up_sync(0xffffffffu, lw, 1);
-    if (lane == 0) excl = -1;
-    if (warp > 0 && wmax[warp - 1] > excl) excl = wmax[warp - 1];
-    const double prev0 = excl >= 0 ? d.theta[rmod(excl, d.blk_cap)] : carry_theta;
-    double diff[8], run = 0.0;
-    {
-      double cur = prev0;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        diff[q] = 0.0;
-        if (8 * t + q < nb) {
-          const double x = isnan(th[q]) ? cur : th[q];
-          const double dd = x - cur;
-          diff[q] = dd - TWO_PI * rint(dd / TWO_PI);
-          cur = x;
-        }
-        run += diff[q];
-      }
-    }
-    const double incl = warp_incl_scan_d(run);
-    if (lane == 31) wsum[warp] = incl;
-    __syncthreads();
-    if (warp == 0) wsum[lane] = warp_incl_scan_d(wsum[lane]);
-    __syncthreads();
-    double acc = carry_u + (incl - run) + (warp > 0 ? wsum[warp - 1] : 0.0);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const long long j = 8 * t + q;
-      acc += diff[q];
-      if (j < nb) {
-        const long long b = base + j;
-        const double tau = -acc / TWO_PI;
-        d.tau[rmod(b, d.blk_cap)] = tau;
-        d.Mb[rmod(b, d.blk_cap)] = (long long)ceil(256.0 * (double)b - 128.0 - tau);
-      }
-    }
-    const double total = wsum[31];
-    const long long lastall = wmax[31];
-    __syncthreads();
-    if (t == 0) {
-      carry_u += total;
-      if (lastall >= 0) carry_theta = d.theta[rmod(lastall, d.blk_cap)];
-    }
-    __syncthreads();
+    carry += tot;
   }
-  if (t == 0) { d.st->theta_prev = carry_theta; d.st->thetau_prev = carry_u; }
+  if (t == 0) {
+    d.st->thetau_prev = carry;
+    d.st->theta_prev = d.clk_last[ntiles - 1];
+  }
+}
+
+// (c) tau_b and M_b
+__global__ void __launch_bounds__(256) k_pam_tau(RxDev d, long long b0, long long b1) {
+  const long long b = b0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= b1) return;
+  const double INV_2PI = 0.15915494309189533577;
+  const int tile = (int)((b - b0) / CLK_TILE);
+  const double tu = d.clk_off[tile] + d.tau[rmod(b, d.blk_cap)];
+  const double tau = -tu * INV_2PI;
+  d.tau[rmod(b, d.blk_cap)] = tau;
+  d.Mb[rmod(b, d.blk_cap)] = (long long)ceil(256.0 * (double)b - 128.0 - tau);
 }
 
 // ------------------------------------------------------------------ H1, H2, H5-H7
@@ -276,12 +314,10 @@ __global__ void __launch_bounds__(256) k_pam_be(RxDev d, InView in, long long b0
 }
 
 // ------------------------------------------------------------------ H8 normalisation
-// One cooperative kernel per buffer (P:167 'three kernels: initialization, estimation of the
-// DC-offset, and estimation of the amplitude'; c-5):
-//   dc = mean u, A = mean|u - dc| / (M / (2 (M-1))), u^ = (u - dc) / A
-// over the symbols emitted by blocks [blo, bhi). Each CTA owns a contiguous block range; the
-// two buffer-wide reductions are fixed-order (per-CTA partials, then every CTA sums the
-// partials in index order) separated by grid-wide syncs, so results are deterministic.
+// Buffer-wise normalisation (P:167 'three kernels: initialization, estimation of the DC-offset,
+// and estimation of the amplitude'; c-5): dc = mean u, A = mean|u - dc| / (M / (2 (M-1))),
+// u^ = (u - dc) / A over the symbols emitted by each buffer's blocks. Reductions are fixed
+// order (deterministic).
 __device__ __forceinline__ double block_sum_det(double v, double *sh) {
   v = warp_sum_d(v);
   if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
@@ -297,61 +333,90 @@ __device__ __forceinline__ long long sym_lo_of(const RxDev &d, long long b) {
   return m > 0 ? m : 0;
 }
 
-__global__ void __launch_bounds__(1024) k_norm_coop(RxDev d, long long beta, long long blo, long long bhi,
-                                                   int last) {
-  cg::grid_group grid = cg::this_grid();
+// (1) k_norm_stats: grid (nbuf x G). CTA (buffer bi, part g): dc from the buffer's per-block
+//     sums (every CTA reduces them in the same fixed order), then the partial sum |u - dc| over
+//     its contiguous symbol range; the last CTA of the buffer (atomic ticket) reduces the
+//     partials in index order -> A. (2) k_norm_apply: u^ = (u - dc)/A, elementwise.
+#define NORM_G 64
+__global__ void __launch_bounds__(1024) k_norm_stats(RxDev d, long long beta0, long long be_done, int flush) {
   __shared__ double sh[32];
-  const int G = gridDim.x, g = blockIdx.x, t = threadIdx.x;
-  const long long nb = bhi - blo;
-  const long long cb0 = blo + nb * g / G, cb1 = blo + nb * (g + 1) / G;
-  const long long m0 = sym_lo_of(d, cb0), m1 = sym_lo_of(d, cb1) > m0 ? sym_lo_of(d, cb1) : m0;
-  // phase 1: sum u over the CTA's symbols (from the per-block sums written by k_pam_be)
+  __shared__ double bc[2];
+  __shared__ int ticket;
+  const int g = blockIdx.x, t = threadIdx.x;
+  const long long beta = beta0 + blockIdx.y;
+  const long long blo = beta * d.buffer_blocks;
+  long long bhi = blo + d.buffer_blocks;
+  if (bhi > be_done) bhi = be_done;
+  // dc over the whole buffer (fixed order: thread-strided, then the fixed block tree)
   double s = 0.0;
-  for (long long b = cb0 + t; b < cb1; b += blockDim.x) s += d.blk_sum[rmod(b, d.blk_cap)];
+  for (long long b = blo + t; b < bhi; b += blockDim.x) s += d.blk_sum[rmod(b, d.blk_cap)];
   s = block_sum_det(s, sh);
-  if (t == 0) { d.norm_part[2 * g] = s; d.norm_part[2 * g + 1] = (double)(m1 - m0); }
-  grid.sync();
-  __shared__ double bc[3];
-  if (t < 32) {   // fixed order: lane l sums partials l, l+32, ..., then a fixed shuffle tree
-    double ps = 0.0, pc = 0.0;
-    for (int i = t; i < G; i += 32) { ps += d.norm_part[2 * i]; pc += d.norm_part[2 * i + 1]; }
-    ps = warp_sum_d(ps);
-    pc = warp_sum_d(pc);
-    if (t == 0) { bc[0] = ps; bc[1] = pc; }
-  }
-  __syncthreads();
-  const double S = bc[0], Cn = bc[1];
-  const double dc = Cn > 0.0 ? S / Cn : 0.0;
-  // phase 2: sum |u - dc|
+  const long long mlo = sym_lo_of(d, blo), mhi0 = sym_lo_of(d, bhi);
+  const long long mhi = mhi0 > mlo ? mhi0 : mlo;
+  const double Cn = (double)(mhi - mlo);
+  const double dc = Cn > 0.0 ? s / Cn : 0.0;
+  // partial |u - dc| over this CTA's share of the symbols
+  const long long n = mhi - mlo;
+  const long long m0 = mlo + n * g / NORM_G, m1 = mlo + n * (g + 1) / NORM_G;
   double a = 0.0;
   for (long long m = m0 + t; m < m1; m += blockDim.x) a += fabs((double)d.u[rmod(m, d.sym_cap)] - dc);
   a = block_sum_det(a, sh);
-  grid.sync();                                   // everyone has read phase-1 partials
-  if (t == 0) d.norm_part[2 * G + g] = a;
-  grid.sync();
-  if (t < 32) {
-    double pa = 0.0;
-    for (int i = t; i < G; i += 32) pa += d.norm_part[2 * G + i];
-    pa = warp_sum_d(pa);
-    if (t == 0) bc[2] = pa;
+  double *part = d.norm_part + (blockIdx.y % 16) * NORM_G;
+  if (t == 0) {
+    part[g] = a;
+    __threadfence();
+    ticket = atomicAdd(&d.norm_tick[blockIdx.y % 16], 1);
   }
   __syncthreads();
-  const double Aa = bc[2];
-  const double mal = (double)d.M / (2.0 * (double)(d.M - 1));
-  double A = Cn > 0.0 ? (Aa / Cn) / mal : 1.0;
-  if (!(A > 0.0)) A = 1.0;
-  // phase 3: apply
-  const float dcf = (float)dc, inv = (float)(1.0 / A);
-  for (long long m = m0 + t; m < m1; m += blockDim.x) {
-    const long long i = rmod(m, d.sym_cap);
-    d.uhat[i] = (d.u[i] - dcf) * inv;
+  if (ticket != NORM_G - 1) return;
+  __threadfence();
+  if (t < 32) {
+    double pa = 0.0;
+    for (int i = t; i < NORM_G; i += 32) pa += ((volatile double *)part)[i];
+    pa = warp_sum_d(pa);
+    if (t == 0) {
+      const double mal = (double)d.M / (2.0 * (double)(d.M - 1));
+      double A = Cn > 0.0 ? (pa / Cn) / mal : 1.0;
+      if (!(A > 0.0)) A = 1.0;
+      d.norm_dc[rmod(beta, d.buf_cap)] = dc;
+      d.norm_amp[rmod(beta, d.buf_cap)] = A;
+      d.norm_cnt[rmod(beta, d.buf_cap)] = (long long)Cn;
+      d.norm_tick[blockIdx.y % 16] = 0;
+    }
   }
-  if (g == 0 && t == 0) {
-    d.norm_dc[rmod(beta, d.buf_cap)] = dc;
-    d.norm_amp[rmod(beta, d.buf_cap)] = A;
-    d.norm_cnt[rmod(beta, d.buf_cap)] = (long long)Cn;
-    long long f = sym_lo_of(d, bhi);
-    d.st->v_front = f;
-    if (last) d.st->m_end = f;
+  (void)flush;
+}
+
+// u^ over the symbols of buffers [beta0, beta0 + nbuf); advances the front (and m_end at flush)
+__global__ void __launch_bounds__(256) k_norm_apply(RxDev d, long long beta0, long long nbuf, long long be_done,
+                                                   int flush) {
+  const long long blo = beta0 * d.buffer_blocks;
+  long long bhi = (beta0 + nbuf) * d.buffer_blocks;
+  if (bhi > be_done) bhi = be_done;
+  const long long mlo = sym_lo_of(d, blo);
+  const long long mhi = sym_lo_of(d, bhi) > mlo ? sym_lo_of(d, bhi) : mlo;
+  // buffer boundaries (symbol index of each buffer's first symbol)
+  __shared__ long long mb[17];
+  __shared__ float dcs[16], invs[16];
+  if (threadIdx.x <= nbuf && threadIdx.x < 17) {
+    long long bb = (beta0 + threadIdx.x) * d.buffer_blocks;
+    if (bb > be_done) bb = be_done;
+    mb[threadIdx.x] = sym_lo_of(d, bb);
+  }
+  if (threadIdx.x < nbuf && threadIdx.x < 16) {
+    dcs[threadIdx.x] = (float)d.norm_dc[rmod(beta0 + threadIdx.x, d.buf_cap)];
+    invs[threadIdx.x] = (float)(1.0 / d.norm_amp[rmod(beta0 + threadIdx.x, d.buf_cap)]);
+  }
+  __syncthreads();
+  for (long long m = mlo + (long long)blockIdx.x * blockDim.x + threadIdx.x; m < mhi;
+       m += (long long)gridDim.x * blockDim.x) {
+    int bi = 0;
+    while (bi + 1 < nbuf && m >= mb[bi + 1]) ++bi;
+    const long long i = rmod(m, d.sym_cap);
+    d.uhat[i] = (d.u[i] - dcs[bi]) * invs[bi];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    d.st->v_front = mhi;
+    if (flush && bhi == be_done) d.st->m_end = mhi;
   }
 }

@@ -72,7 +72,8 @@ struct rx_handle {
   long long Q;   // 2-sps samples per buffer (KK)
   long long hist_cap;
   long long lms_launched_upto;   // segment estimate at the last equaliser launch
-  long long norm_G;              // co-resident CTAs of the cooperative normalisation
+  long long lms_carry;           // grid slack carried to the next streaming round
+  long long max_call;            // samples per rx_process call: (history_buffers - 2) buffers
   // tracing
   int prof_mask;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_pending;
@@ -282,6 +283,7 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   d.thr_default = cfg->thresholds ? 0 : 1;
   d.qam_sc = kk ? (float)sqrt(3.0 / (2.0 * (c.order - 1))) : 0.f;
   h->sps = kk ? 4 : 2;
+  const int HB = c.history_buffers;
   h->Q = (long long)c.buffer_blocks * 256;
   rx_status s = RX_OK;
 #define TRY(x) do { s = (x); if (s) { rx_destroy(h); return s; } } while (0)
@@ -368,8 +370,8 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
     TRY(dupload(h, &d.bps_rot, rot));
   }
   // ---- rings
-  const int HB = c.history_buffers;
-  h->hist_cap = 1 << 16;
+  h->max_call = (long long)(HB - 2) * c.buffer_blocks * 512;
+  h->hist_cap = next_pow2(h->max_call + (1 << 18));   // > max call + clock lookback + kept tail
   d.hist_cap = h->hist_cap;
   TRY(dalloc(h, &d.hist, d.hist_cap));
   d.blk_cap = next_pow2((long long)HB * c.buffer_blocks + 256);
@@ -388,14 +390,12 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
     TRY(dalloc(h, &d.norm_dc, d.buf_cap));
     TRY(dalloc(h, &d.norm_amp, d.buf_cap));
     TRY(dalloc(h, &d.norm_cnt, d.buf_cap));
-    {
-      int nsm = 0, per = 0;
-      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cuda_device);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_norm_coop, 1024, 0);
-      h->norm_G = (long long)nsm * (per > 0 ? per : 1);
-      if (h->norm_G > 1024) h->norm_G = 1024;
-    }
-    TRY(dalloc(h, &d.norm_part, 4 * 1024));
+    TRY(dalloc(h, &d.norm_part, 16 * NORM_G));
+    TRY(dalloc(h, &d.norm_tick, 16));
+    const long long maxtiles = ((long long)(HB - 2) * c.buffer_blocks + CLK_TILE - 1) / CLK_TILE + 2;
+    TRY(dalloc(h, &d.clk_part, maxtiles));
+    TRY(dalloc(h, &d.clk_off, maxtiles));
+    TRY(dalloc(h, &d.clk_last, maxtiles));
   } else {
     d.E_cap = next_pow2((long long)HB * c.buffer_blocks * 512);
     d.z_cap = next_pow2((long long)HB * c.buffer_blocks * 256);
@@ -444,7 +444,7 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   // kernels needing > 48 KB dynamic shared memory
   const size_t s2_smem = (1024 + 8 * FFT_PAD_N) * sizeof(float2);
   const size_t cfo_smem = (1024 + 8 * FFT_PAD_N) * sizeof(float2) + 1024 * sizeof(float);
-  const size_t clk_smem = (256 + 2 * c.clock_avg_half) * sizeof(double2);
+  const size_t clk_smem = (CLK_TILE + 1 + 2 * c.clock_avg_half) * sizeof(double2);
   if (cudaFuncSetAttribute(k_pam_theta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)clk_smem) != cudaSuccess ||
       cudaFuncSetAttribute(k_kk_s2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2_smem) != cudaSuccess ||
       cudaFuncSetAttribute(k_cfo_partial, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfo_smem) != cudaSuccess ||
@@ -467,7 +467,13 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
     __VA_ARGS__;                         \
     if (stop_) cudaEventRecord(stop_, (s)); \
     (h)->launches++;                     \
+    if (g_rx_debug) {                    \
+      fprintf(stderr, "librx: launch %s ...", #__VA_ARGS__); \
+      cudaError_t e__ = cudaStreamSynchronize(s); \
+      fprintf(stderr, " %s\n", cudaGetErrorString(e__)); \
+    }                                    \
   } while (0)
+static int g_rx_debug = getenv("RX_DEBUG_SYNC") ? 1 : 0;
 
 static rx_status check_launch() {
   cudaError_t e = cudaGetLastError();
@@ -493,33 +499,54 @@ static void launch_sync_train(rx_handle *h, cudaStream_t s, int flush) {
   KLAUNCH(h, RX_K_SYNC, s, (k_lms_train<CPLX><<<1, 32, 0, s>>>(d, flush)));
 }
 
+static void launch_lms_round(rx_handle *h, cudaStream_t s, unsigned char *labels, long long lab_cap,
+                             int flush, long long nseg) {
+  RxDev &d = h->d;
+  const long long S = d.S;
+  if (d.family == RX_PAM) {
+    KLAUNCH(h, RX_K_LMS, s, (k_lms_seg<false, 0><<<gridc(nseg, 4), 128, 0, s>>>(d, flush, (int)nseg)));
+  } else if (d.cpr == 1) {
+    KLAUNCH(h, RX_K_LMS, s, (k_lms_seg<true, 1><<<gridc(nseg, 4), 128, 0, s>>>(d, flush, (int)nseg)));
+  } else {
+    KLAUNCH(h, RX_K_LMS, s, (k_lms_seg<true, 2><<<gridc(nseg, 4), 128, 0, s>>>(d, flush, (int)nseg)));
+  }
+  KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_stitch<<<(unsigned)nseg, 256, 0, s>>>(d, (int)nseg)));
+  KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_prefix<<<1, 1024, 0, s>>>(d, flush, (int)nseg)));
+  KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_final<<<(unsigned)nseg, 256, 0, s>>>(d, labels, lab_cap, (int)nseg)));
+  KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_counters<<<1, 1024, 0, s>>>(d)));
+  KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_seeds<<<(unsigned)(nseg * S / d.E_sym + 2), 1024, 0, s>>>(d, flush)));
+}
+
+// Equaliser rounds. Streaming: one round per call once ~lms_batch_segments may be pending
+// (a batch spans fewer than D epochs, so every lag-D seed it needs was finalised by an earlier
+// round). Flush: rounds until every segment is final (each round can unlock the next D epochs;
+// the end of stream is the one place the host synchronises).
 static void launch_lms_rounds(rx_handle *h, cudaStream_t s, unsigned char *labels, long long lab_cap,
                               int flush, long long sym_ub) {
   RxDev &d = h->d;
   const long long S = d.S;
-  long long seg_lb = h->hm_host->seg_next;   // stale => lower bound
-  // batching: wait until ~lms_batch_segments segments may be pending (host-side estimate)
-  const long long est_ready = sym_ub / S - h->lms_launched_upto;
-  if (!flush && h->cfg.lms_batch_segments > 0 && est_ready < h->cfg.lms_batch_segments) return;
-  h->lms_launched_upto = sym_ub / S;
-  long long seg_ub = sym_ub / S + 1;
-  long long nseg = seg_ub - seg_lb + 1;
-  if (nseg < 1) nseg = 1;
-  if (nseg > d.seg_cap / 2) nseg = d.seg_cap / 2;
-  const long long e_lo = seg_lb * S / d.E_sym, e_hi = seg_ub * S / d.E_sym;
-  const long long rounds = (e_hi - e_lo + 1 + d.D - 1) / d.D + 1;
-  for (long long r = 0; r < rounds; ++r) {
-    if (d.family == RX_PAM) {
-      KLAUNCH(h, RX_K_LMS, s, (k_lms_seg<false, 0><<<gridc(nseg, 4), 128, 0, s>>>(d, flush, (int)nseg)));
-    } else if (d.cpr == 1) {
-      KLAUNCH(h, RX_K_LMS, s, (k_lms_seg<true, 1><<<gridc(nseg, 4), 128, 0, s>>>(d, flush, (int)nseg)));
-    } else {
-      KLAUNCH(h, RX_K_LMS, s, (k_lms_seg<true, 2><<<gridc(nseg, 4), 128, 0, s>>>(d, flush, (int)nseg)));
-    }
-    KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_stitch<<<(unsigned)nseg, 256, 0, s>>>(d, (int)nseg)));
-    KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_prefix<<<1, 1024, 0, s>>>(d, flush, (int)nseg)));
-    KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_final<<<(unsigned)nseg, 256, 0, s>>>(d, labels, lab_cap, (int)nseg)));
-    KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_epoch<<<1, 1024, 0, s>>>(d, flush)));
+  const long long seg_ub = sym_ub / S + 1;
+  if (!flush) {
+    const long long est_ready = seg_ub - h->lms_launched_upto;
+    if (h->cfg.lms_batch_segments > 0 && est_ready < h->cfg.lms_batch_segments) return;
+    long long nseg = seg_ub - h->lms_launched_upto + h->lms_carry + 2;
+    if (nseg > d.seg_cap / 2) nseg = d.seg_cap / 2;
+    h->lms_launched_upto = seg_ub;
+    h->lms_carry = nseg;                     // segments not finished now are retried next round
+    launch_lms_round(h, s, labels, lab_cap, flush, nseg);
+    return;
+  }
+  long long prev = -1;
+  for (int it = 0; it < 4096; ++it) {
+    DevState st;
+    if (cudaStreamSynchronize(s) != cudaSuccess) return;
+    if (cudaMemcpy(&st, h->st_dev, sizeof(st), cudaMemcpyDeviceToHost) != cudaSuccess) return;
+    const long long total = st.m_end >= 0 ? (st.m_end + S - 1) / S : seg_ub;
+    if (st.seg_next >= total || st.seg_next == prev) break;
+    prev = st.seg_next;
+    long long nseg = total - st.seg_next + 1;
+    if (nseg > d.seg_cap / 2) nseg = d.seg_cap / 2;
+    launch_lms_round(h, s, labels, lab_cap, flush, nseg);
   }
 }
 
@@ -534,9 +561,11 @@ static void run_pam(rx_handle *h, cudaStream_t s, const InView &in, unsigned cha
   }
   long long clk_target = flush ? h->fe_done : h->fe_done - d.clock_half;
   if (clk_target > h->clk_done) {
-    const size_t smem = (256 + 2 * d.clock_half) * sizeof(double2);
-    KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_pam_theta<<<gridc(clk_target - h->clk_done, 256), 256, smem, s>>>(d, h->clk_done, clk_target, h->fe_done - 1)));
-    KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_pam_unwrap<<<1, 1024, 0, s>>>(d, h->clk_done, clk_target)));
+    const size_t smem = (CLK_TILE + 1 + 2 * d.clock_half) * sizeof(double2);
+    const unsigned ntiles = gridc(clk_target - h->clk_done, CLK_TILE);
+    KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_pam_theta<<<ntiles, CLK_TILE, smem, s>>>(d, h->clk_done, clk_target, h->fe_done - 1)));
+    KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_pam_carry<<<1, 1024, 0, s>>>(d, (int)ntiles)));
+    KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_pam_tau<<<gridc(clk_target - h->clk_done, 256), 256, 0, s>>>(d, h->clk_done, clk_target)));
     h->clk_done = clk_target;
   }
   long long be_target = flush ? h->fe_done - 1 : h->clk_done - 1;
@@ -544,22 +573,23 @@ static void run_pam(rx_handle *h, cudaStream_t s, const InView &in, unsigned cha
     KLAUNCH(h, RX_K_PAM_BE, s, (k_pam_be<<<gridc(be_target - h->be_done, FE_GROUPS), 256, 0, s>>>(d, in, h->be_done, be_target)));
     h->be_done = be_target;
   }
-  while ((h->norm_done + 1) * BB <= h->be_done || (flush && h->norm_done * BB < h->be_done)) {
-    const long long blo = h->norm_done * BB;
-    long long bhi = blo + BB;
-    if (bhi > h->be_done) bhi = h->be_done;
-    const long long beta = h->norm_done;
-    {
-      const int last = (flush && bhi == h->be_done) ? 1 : 0;
-      long long G = bhi - blo < h->norm_G ? bhi - blo : h->norm_G;
-      void *args[] = {(void *)&d, (void *)&beta, (void *)&blo, (void *)&bhi, (void *)&last};
-      KLAUNCH(h, RX_K_NORM, s, cudaLaunchCooperativeKernel((void *)k_norm_coop, dim3((unsigned)G), dim3(1024), args, 0, s));
+  {
+    long long nbuf = 0;
+    while ((h->norm_done + nbuf + 1) * BB <= h->be_done || (flush && (h->norm_done + nbuf) * BB < h->be_done)) ++nbuf;
+    if (nbuf > 0) {
+      const long long beta0 = h->norm_done;
+      const long long bend = h->be_done;
+      for (long long b0 = 0; b0 < nbuf; b0 += 16) {
+        const long long nb = nbuf - b0 < 16 ? nbuf - b0 : 16;
+        KLAUNCH(h, RX_K_NORM, s, (k_norm_stats<<<dim3(NORM_G, (unsigned)nb), 1024, 0, s>>>(d, beta0 + b0, bend, flush)));
+        KLAUNCH(h, RX_K_NORM, s, (k_norm_apply<<<1184, 256, 0, s>>>(d, beta0 + b0, nb, bend, flush)));
+      }
+      h->norm_done += nbuf;
     }
-    h->norm_done++;
   }
   if (flush) KLAUNCH(h, RX_K_MISC, s, (k_pam_mend<<<1, 1, 0, s>>>(d, h->be_done > 0 ? h->be_done : 0)));
   launch_sync_train<false>(h, s, flush);
-  launch_lms_rounds(h, s, labels, lab_cap, flush, 260 * h->be_done + 1024);
+  launch_lms_rounds(h, s, labels, lab_cap, flush, 256 * h->be_done + h->be_done / 4 + 4096);
 }
 
 static void run_kk(rx_handle *h, cudaStream_t s, const InView &in, unsigned char *labels,
@@ -598,7 +628,7 @@ static void run_kk(rx_handle *h, cudaStream_t s, const InView &in, unsigned char
 extern "C" rx_status rx_process(rx_handle *h, const unsigned short *d_samples, long long n,
                                 unsigned char *d_labels, long long labels_capacity, void *stream) {
   if (!h || n < 0 || (n > 0 && !d_samples) || n % 512 || labels_capacity < 0) return RX_EINVAL;
-  if (n > (long long)h->d.buffer_blocks * 512) return RX_EINVAL;
+  if (n > h->max_call) return RX_EINVAL;
   if (labels_capacity > 0 && !d_labels) return RX_EINVAL;
   if (((uintptr_t)d_samples) & 15) return RX_EINVAL;
   if (h->flushed) return RX_ESTATE;
@@ -610,16 +640,11 @@ extern "C" rx_status rx_process(rx_handle *h, const unsigned short *d_samples, l
   in.call_end = h->n_in + n;
   in.hist = h->d.hist;
   in.hist_cap = h->hist_cap;
+  in.hist_w = h->d.hist;
+  in.keep_from = h->n_in + n - (1 << 16);
   h->n_in += n;
   if (h->d.family == RX_PAM) run_pam(h, s, in, labels_capacity ? d_labels : nullptr, labels_capacity ? labels_capacity : 1, 0);
   else run_kk(h, s, in, labels_capacity ? d_labels : nullptr, labels_capacity ? labels_capacity : 1, 0);
-  if (n > 0) {
-    long long p0 = in.call_end - h->hist_cap;
-    if (p0 < in.call_start) p0 = in.call_start;
-    unsigned g = gridc(in.call_end - p0, 256);
-    if (g > 512) g = 512;
-    KLAUNCH(h, RX_K_MISC, s, (k_hist_copy<<<g, 256, 0, s>>>(in, h->d.hist, h->hist_cap, p0, in.call_end)));
-  }
   return check_launch();
 }
 
@@ -634,6 +659,8 @@ extern "C" rx_status rx_flush(rx_handle *h, unsigned char *d_labels, long long l
   in.call_end = h->n_in;
   in.hist = h->d.hist;
   in.hist_cap = h->hist_cap;
+  in.hist_w = h->d.hist;
+  in.keep_from = h->n_in;
   if (h->d.family == RX_PAM) run_pam(h, s, in, labels_capacity ? d_labels : nullptr, labels_capacity ? labels_capacity : 1, 1);
   else run_kk(h, s, in, labels_capacity ? d_labels : nullptr, labels_capacity ? labels_capacity : 1, 1);
   h->flushed = true;

@@ -82,7 +82,8 @@ struct RxDev {
   long long blk_cap;
   float *u; float *uhat; long long sym_cap;
   double *norm_dc; double *norm_amp; long long *norm_cnt; long long buf_cap;
-  double *norm_part;                // cooperative-reduction scratch [4 * NORM_G]
+  double *norm_part; int *norm_tick;   // normalisation partials [16][NORM_G], tickets [16]
+  double *clk_part, *clk_off, *clk_last; // unwrap tile totals / offsets / last phases
   float2 *E; long long E_cap;
   float2 *z; long long z_cap;
   float2 *zp; long long zp_cap;     // z' = normalised, CFO-removed 2-sps field

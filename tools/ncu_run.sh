@@ -12,6 +12,6 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:^
   --log-file gpurun_out/launches_all.csv $BK > gpurun_out/ncu_launch_all.log 2>&1
 fi
 for k in "$@"; do
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 20 -c 1 \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s ${SKIP:-20} -c 1 \
     -o gpurun_out/prof_$k $B > gpurun_out/ncu_full_$k.log 2>&1
 done
