@@ -151,14 +151,20 @@ __global__ void __launch_bounds__(1024) k_sync_pick(RxDev d, int flush) {
 // run with 4 independent accumulators; lane i owns symbol i of the block, lane k tap k; the
 // sliding window of inputs lives in shared memory (double-buffered, next block prefetched
 // into registers while the current block computes).
-#define LMS_RING 512        // per-warp input ring (power of two), absolute index & (LMS_RING-1)
+#define LMS_RING 512        // per-warp input ring (power of two), mirrored: element i lives at
+                            // (i & (RING-1)) and (i & (RING-1)) + RING, so every block window is
+                            // contiguous and read with compile-time offsets
 #define LMS_AHEAD 4         // blocks of lookahead staged by cp.async
+
+template <bool CPLX> struct LmsElem { using T = float; };    // PAM: real
+template <> struct LmsElem<true> { using T = float2; };     // KK: complex
 
 template <bool CPLX>
 struct LmsSmemT {
-  typename std::conditional<CPLX, float2, float>::type ring[LMS_RING];
-  float2 w[32];
-  float2 e[32];
+  using T = typename LmsElem<CPLX>::T;
+  alignas(16) T ring[2 * LMS_RING];
+  alignas(16) T w[32];
+  alignas(16) T e[32];
   float2 y[32];
 };
 
@@ -174,29 +180,29 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-// stage input samples [i0, i1) (absolute index of u^ (PAM) or z' (KK)) into the ring; zero
-// outside [0, vend) (cp.async zero-fill)
+// stage input samples [i0, i1) (absolute index of u^ (PAM) or z' (KK)) into the mirrored ring;
+// zero outside [0, vend) (cp.async zero-fill)
 template <bool CPLX>
 __device__ __forceinline__ void lms_stage(const RxDev &d, LmsSmemT<CPLX> &sm, long long i0, long long i1,
                                           long long vend) {
   const int lane = threadIdx.x & 31;
   for (long long i = i0 + lane; i < i1; i += 32) {
     const bool ok = i >= 0 && i < vend;
-    if (CPLX) {
+    const int slot = (int)(i & (LMS_RING - 1));
+    if constexpr (CPLX) {
       const float2 *src = ok ? d.zp + rmod(i, d.zp_cap) : d.zp;
-      cp_async_elem(reinterpret_cast<float2 *>(sm.ring) + (i & (LMS_RING - 1)), src, ok);
+      cp_async_elem(&sm.ring[slot], src, ok);
+      cp_async_elem(&sm.ring[slot + LMS_RING], src, ok);
     } else {
       const float *src = ok ? d.uhat + rmod(i, d.sym_cap) : d.uhat;
-      cp_async_elem(reinterpret_cast<float *>(sm.ring) + (i & (LMS_RING - 1)), src, ok);
+      cp_async_elem(&sm.ring[slot], src, ok);
+      cp_async_elem(&sm.ring[slot + LMS_RING], src, ok);
     }
   }
 }
 
-template <bool CPLX>
-__device__ __forceinline__ float2 ring_at(const LmsSmemT<CPLX> &sm, long long i) {
-  if (CPLX) return reinterpret_cast<const float2 *>(sm.ring)[i & (LMS_RING - 1)];
-  return make_float2(reinterpret_cast<const float *>(sm.ring)[i & (LMS_RING - 1)], 0.f);
-}
+__device__ __forceinline__ float2 as_c(float v) { return make_float2(v, 0.f); }
+__device__ __forceinline__ float2 as_c(float2 v) { return v; }
 
 // decision level value of index i: PAM (2i - M + 1)/(M - 1); QAM axis (2i - L + 1) sc
 __device__ __forceinline__ float level_of(int i, float two_s, float off) { return fmaf((float)i, two_s, off); }
@@ -206,20 +212,21 @@ __device__ __forceinline__ float level_of(int i, float two_s, float off) { retur
 // (0 none, 1 VV, 2 BPS). Outputs for m >= out_lo go to the level / yout rings,
 // warm-up decisions (m < out_lo) to warm[]. Returns final theta; accumulates EVM.
 //
-// Layout: taps are padded to KP = 4 ceil(K/4) (zero taps, exact) so the K-term dot products
-// run with 4 independent accumulators; lane i owns symbol i of the block, lane k tap k; the
-// inputs stream through a per-warp shared-memory ring filled LMS_AHEAD blocks ahead with
-// cp.async (the serial block recursion never waits on HBM).
-template <bool CPLX, int CPR, int MODE>
+// Layout: taps are padded to KP in {4, 8, 16, 32} (zero taps, exact); lane i owns symbol i of
+// the block, lane k tap k; the inputs stream through a per-warp mirrored shared-memory ring
+// filled LMS_AHEAD blocks ahead with cp.async, so the serial block recursion never waits on
+// HBM and every window access is an immediate offset.
+template <bool CPLX, int CPR, int MODE, int KP>
 __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, long long t_end,
                          long long out_lo, float2 &wk, unsigned char *warm, double &evn,
                          double &evd, long long vend) {
+  using T = typename LmsElem<CPLX>::T;
   const int lane = threadIdx.x & 31;
-  const int K = d.K, c = K >> 1, KP = (K + 3) & ~3;
-  const int stride = CPLX ? 2 : 1;
+  const int K = d.K, c = K >> 1;
+  constexpr int stride = CPLX ? 2 : 1;
   const int off = CPLX ? d.st->sync_phase : 0;
-  const int WL = stride * 31 + KP;          // window of one block
-  const int DS = stride * 32;               // window shift per block
+  constexpr int WL = stride * 31 + KP;      // window of one block
+  constexpr int DS = stride * 32;           // window shift per block
   const float mu = d.mu;
   const int L = d.L;
   const float two_s = CPLX ? 2.0f * d.qam_sc : 2.0f / (float)(d.M - 1);
@@ -234,10 +241,10 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
   }
   float theta = 0.f;
   if (lane >= K) wk = make_float2(0.f, 0.f);
-  sm.w[lane] = wk;
+  if (CPLX) reinterpret_cast<float2 *>(sm.w)[lane] = wk;
+  else reinterpret_cast<float *>(sm.w)[lane] = wk.x;
   const long long wb0 = (long long)stride * t_begin + off + c - (KP - 1);
   const long long nblk = (t_end - t_begin + 31) / 32;
-  // prologue: block 0's window, then the new samples of blocks 1 .. AHEAD-1 (one group each)
   lms_stage<CPLX>(d, sm, wb0, wb0 + WL, vend);
   cp_async_commit();
 #pragma unroll 1
@@ -255,23 +262,38 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
     const int nvalid = (int)((t_end - t) < 32 ? (t_end - t) : 32);
     const bool valid = lane < nvalid;
     const long long m = t + lane;
-    // y_i = w^H u_i, u_i[k] = x[wb + stride i + KP-1-k]
-    float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
-    const long long ub = wb + stride * lane + KP - 1;
-    for (int k = 0; k < KP; k += 4) {
-      const float2 w0 = sm.w[k], w1 = sm.w[k + 1], w2 = sm.w[k + 2], w3 = sm.w[k + 3];
-      const float2 u0 = ring_at<CPLX>(sm, ub - k), u1 = ring_at<CPLX>(sm, ub - k - 1);
-      const float2 u2 = ring_at<CPLX>(sm, ub - k - 2), u3 = ring_at<CPLX>(sm, ub - k - 3);
-      a0.x = fmaf(w0.x, u0.x, a0.x); a1.x = fmaf(w1.x, u1.x, a1.x);
-      a2.x = fmaf(w2.x, u2.x, a2.x); a3.x = fmaf(w3.x, u3.x, a3.x);
+    const T *win = sm.ring + (int)(wb & (LMS_RING - 1));   // contiguous window (mirror)
+    // y_i = w^H u_i, u_i[k] = win[stride i + KP-1-k]
+    float2 y;
+    {
+      const T *ub = win + stride * lane + KP - 1;
+      float2 a[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       if (CPLX) {
-        a0.x = fmaf(w0.y, u0.y, a0.x); a1.x = fmaf(w1.y, u1.y, a1.x);
-        a2.x = fmaf(w2.y, u2.y, a2.x); a3.x = fmaf(w3.y, u3.y, a3.x);
-        a0.y = fmaf(w0.x, u0.y, fmaf(-w0.y, u0.x, a0.y)); a1.y = fmaf(w1.x, u1.y, fmaf(-w1.y, u1.x, a1.y));
-        a2.y = fmaf(w2.x, u2.y, fmaf(-w2.y, u2.x, a2.y)); a3.y = fmaf(w3.x, u3.y, fmaf(-w3.y, u3.x, a3.y));
+        const float4 *w4 = reinterpret_cast<const float4 *>(sm.w);
+#pragma unroll
+        for (int k = 0; k < KP; k += 2) {
+          const float4 ww = w4[k >> 1];                         // taps k, k+1 (broadcast)
+          const float2 u0 = as_c(ub[-k]), u1 = as_c(ub[-k - 1]);
+          float2 &A = a[(k >> 1) & 3];
+          A.x = fmaf(ww.x, u0.x, fmaf(ww.y, u0.y, A.x));
+          A.y = fmaf(ww.x, u0.y, fmaf(-ww.y, u0.x, A.y));
+          A.x = fmaf(ww.z, u1.x, fmaf(ww.w, u1.y, A.x));
+          A.y = fmaf(ww.z, u1.y, fmaf(-ww.w, u1.x, A.y));
+        }
+      } else {
+        const float4 *w4 = reinterpret_cast<const float4 *>(sm.w);
+#pragma unroll
+        for (int k = 0; k < KP; k += 4) {
+          const float4 ww = w4[k >> 2];                         // taps k..k+3 (broadcast)
+          float2 &A = a[(k >> 2) & 3];
+          A.x = fmaf(ww.x, as_c(ub[-k]).x, A.x);
+          A.x = fmaf(ww.y, as_c(ub[-k - 1]).x, A.x);
+          A.x = fmaf(ww.z, as_c(ub[-k - 2]).x, A.x);
+          A.x = fmaf(ww.w, as_c(ub[-k - 3]).x, A.x);
+        }
       }
+      y = make_float2((a[0].x + a[1].x) + (a[2].x + a[3].x), CPLX ? (a[0].y + a[1].y) + (a[2].y + a[3].y) : 0.f);
     }
-    const float2 y = make_float2((a0.x + a1.x) + (a2.x + a3.x), CPLX ? (a0.y + a1.y) + (a2.y + a3.y) : 0.f);
     float2 e, zp = y;
     int code = 0;
     if (MODE == 0) {
@@ -351,35 +373,48 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
         warm[m - (out_lo - d.O)] = (unsigned char)code;
       }
     }
-    sm.e[lane] = valid ? e : make_float2(0.f, 0.f);
+    if (!valid) e = make_float2(0.f, 0.f);
+    if (CPLX) reinterpret_cast<float2 *>(sm.e)[lane] = e;
+    else reinterpret_cast<float *>(sm.e)[lane] = e.x;
     __syncwarp();
     // gradient: lane k: g_k = sum_i u_i[k] conj(e_i); w <- w + mu g   (c-9 step 7)
     {
-      float2 g0 = make_float2(0.f, 0.f), g1 = g0, g2 = g0, g3 = g0;
-      const long long ug = wb + KP - 1 - (lane < KP ? lane : 0);   // lanes >= KP: discarded
+      const T *ug = win + KP - 1 - (lane < KP ? lane : 0);     // lanes >= KP: discarded
+      float2 g[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      if (CPLX) {
+        const float4 *e4 = reinterpret_cast<const float4 *>(sm.e);
 #pragma unroll
-      for (int i = 0; i < 32; i += 4) {
-        const float2 e0 = sm.e[i], e1 = sm.e[i + 1], e2 = sm.e[i + 2], e3 = sm.e[i + 3];
-        const float2 u0 = ring_at<CPLX>(sm, ug + stride * i), u1 = ring_at<CPLX>(sm, ug + stride * (i + 1));
-        const float2 u2 = ring_at<CPLX>(sm, ug + stride * (i + 2)), u3 = ring_at<CPLX>(sm, ug + stride * (i + 3));
-        g0.x = fmaf(u0.x, e0.x, g0.x); g1.x = fmaf(u1.x, e1.x, g1.x);
-        g2.x = fmaf(u2.x, e2.x, g2.x); g3.x = fmaf(u3.x, e3.x, g3.x);
-        if (CPLX) {
-          g0.x = fmaf(u0.y, e0.y, g0.x); g1.x = fmaf(u1.y, e1.y, g1.x);
-          g2.x = fmaf(u2.y, e2.y, g2.x); g3.x = fmaf(u3.y, e3.y, g3.x);
-          g0.y = fmaf(u0.y, e0.x, fmaf(-u0.x, e0.y, g0.y)); g1.y = fmaf(u1.y, e1.x, fmaf(-u1.x, e1.y, g1.y));
-          g2.y = fmaf(u2.y, e2.x, fmaf(-u2.x, e2.y, g2.y)); g3.y = fmaf(u3.y, e3.x, fmaf(-u3.x, e3.y, g3.y));
+        for (int i = 0; i < 32; i += 2) {
+          const float4 ee = e4[i >> 1];                         // e_i, e_{i+1} (broadcast)
+          const float2 u0 = as_c(ug[stride * i]), u1 = as_c(ug[stride * (i + 1)]);
+          float2 &G = g[(i >> 1) & 3];
+          G.x = fmaf(u0.x, ee.x, fmaf(u0.y, ee.y, G.x));
+          G.y = fmaf(u0.y, ee.x, fmaf(-u0.x, ee.y, G.y));
+          G.x = fmaf(u1.x, ee.z, fmaf(u1.y, ee.w, G.x));
+          G.y = fmaf(u1.y, ee.z, fmaf(-u1.x, ee.w, G.y));
+        }
+      } else {
+        const float4 *e4 = reinterpret_cast<const float4 *>(sm.e);
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          const float4 ee = e4[i >> 2];
+          float2 &G = g[(i >> 2) & 3];
+          G.x = fmaf(as_c(ug[i]).x, ee.x, G.x);
+          G.x = fmaf(as_c(ug[i + 1]).x, ee.y, G.x);
+          G.x = fmaf(as_c(ug[i + 2]).x, ee.z, G.x);
+          G.x = fmaf(as_c(ug[i + 3]).x, ee.w, G.x);
         }
       }
       if (lane < K) {
-        wk.x = fmaf(mu, (g0.x + g1.x) + (g2.x + g3.x), wk.x);
-        if (CPLX) wk.y = fmaf(mu, (g0.y + g1.y) + (g2.y + g3.y), wk.y);
+        wk.x = fmaf(mu, (g[0].x + g[1].x) + (g[2].x + g[3].x), wk.x);
+        if (CPLX) wk.y = fmaf(mu, (g[0].y + g[1].y) + (g[2].y + g[3].y), wk.y);
         // divergence (reading R-DIV): any single tap beyond 1e3 flags at once,
         // the full norm is checked at the end of the run
         if (cabs2(wk) > 1e6f) set_flag(d.st, RX_FLAG_DIVERGE);
       }
     }
-    sm.w[lane] = wk;
+    if (CPLX) reinterpret_cast<float2 *>(sm.w)[lane] = wk;
+    else reinterpret_cast<float *>(sm.w)[lane] = wk.x;
     __syncwarp();
     // stage the new samples of block jb + AHEAD (the slots of block jb are no longer read)
     const long long jn = jb + LMS_AHEAD;
@@ -395,7 +430,7 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
 }
 
 // ------------------------------------------------------------------ training (1 warp)
-template <bool CPLX>
+template <bool CPLX, int KP>
 __global__ void __launch_bounds__(32) k_lms_train(RxDev d, int flush) {
   __shared__ LmsSmemT<CPLX> sm;
   DevState *st = d.st;
@@ -407,7 +442,7 @@ __global__ void __launch_bounds__(32) k_lms_train(RxDev d, int flush) {
   if (last >= vend && !flush) return;
   float2 wk = make_float2(lane == c ? 1.f : 0.f, 0.f);    // centre spike
   double en = 0.0, ed = 0.0;
-  lms_run<CPLX, 0, 0>(d, sm, d.m0, d.m0 + d.T_train, 0, wk, nullptr, en, ed, vend);
+  lms_run<CPLX, 0, 0, KP>(d, sm, d.m0, d.m0 + d.T_train, 0, wk, nullptr, en, ed, vend);
   if (lane < K) d.w_train[lane] = wk;
   __threadfence();
   if (lane == 0) { st->trained = 1; d.hm->trained = 1; }
@@ -415,7 +450,7 @@ __global__ void __launch_bounds__(32) k_lms_train(RxDev d, int flush) {
 
 // ------------------------------------------------------------------ segments (1 warp each)
 // Segment s outputs [sS, min((s+1)S, m_end)), recursion starts O symbols early (c-9).
-template <bool CPLX, int CPR>
+template <bool CPLX, int CPR, int KP>
 __global__ void __launch_bounds__(128) k_lms_seg(RxDev d, int flush, int nseg) {
   __shared__ LmsSmemT<CPLX> sm[4];
   DevState *st = d.st;
@@ -448,7 +483,7 @@ __global__ void __launch_bounds__(128) k_lms_seg(RxDev d, int flush, int nseg) {
   if (t0 < 0) t0 = 0;
   double en = 0.0, ed = 0.0;
   unsigned char *warm = d.O > 0 ? d.seg_warm + rmod(s, d.seg_cap) * d.O : nullptr;
-  const float th = lms_run<CPLX, CPR, 1>(d, sm[warp], t0, hi, lo, wk, warm, en, ed, vend);
+  const float th = lms_run<CPLX, CPR, 1, KP>(d, sm[warp], t0, hi, lo, wk, warm, en, ed, vend);
   en = warp_sum_d(en);
   ed = warp_sum_d(ed);
   const long long si = rmod(s, d.seg_cap);

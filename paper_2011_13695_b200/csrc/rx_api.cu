@@ -72,7 +72,6 @@ struct rx_handle {
   long long Q;   // 2-sps samples per buffer (KK)
   long long hist_cap;
   long long lms_launched_upto;   // segment estimate at the last equaliser launch
-  long long lms_carry;           // grid slack carried to the next streaming round
   long long max_call;            // samples per rx_process call: (history_buffers - 2) buffers
   // tracing
   int prof_mask;
@@ -486,6 +485,33 @@ static rx_status check_launch() {
 
 static unsigned gridc(long long n, int per) { return (unsigned)((n + per - 1) / per); }
 
+// tap padding KP in {4, 8, 16, 32} (compile-time) and the CPR flavour select the instance
+typedef void (*lms_seg_fn)(RxDev, int, int);
+typedef void (*lms_train_fn)(RxDev, int);
+static int kp_of(int K) { return K <= 4 ? 4 : (K <= 8 ? 8 : (K <= 16 ? 16 : 32)); }
+template <bool CPLX, int CPR>
+static lms_seg_fn seg_kp(int K) {
+  switch (kp_of(K)) {
+    case 4: return k_lms_seg<CPLX, CPR, 4>;
+    case 8: return k_lms_seg<CPLX, CPR, 8>;
+    case 16: return k_lms_seg<CPLX, CPR, 16>;
+    default: return k_lms_seg<CPLX, CPR, 32>;
+  }
+}
+static lms_seg_fn lms_seg_kernel(const RxDev &d) {
+  if (d.family == RX_PAM) return seg_kp<false, 0>(d.K);
+  return d.cpr == 1 ? seg_kp<true, 1>(d.K) : seg_kp<true, 2>(d.K);
+}
+template <bool CPLX>
+static lms_train_fn lms_train_kernel(int K) {
+  switch (kp_of(K)) {
+    case 4: return k_lms_train<CPLX, 4>;
+    case 8: return k_lms_train<CPLX, 8>;
+    case 16: return k_lms_train<CPLX, 16>;
+    default: return k_lms_train<CPLX, 32>;
+  }
+}
+
 template <bool CPLX>
 static void launch_sync_train(rx_handle *h, cudaStream_t s, int flush) {
   RxDev &d = h->d;
@@ -496,20 +522,14 @@ static void launch_sync_train(rx_handle *h, cudaStream_t s, int flush) {
     KLAUNCH(h, RX_K_SYNC, s, (k_sync_corr<CPLX><<<gridc((long long)nh * RX_PREF, 256), 256, smem, s>>>(d)));
     KLAUNCH(h, RX_K_SYNC, s, (k_sync_pick<CPLX><<<1, 1024, 0, s>>>(d, flush)));
   }
-  KLAUNCH(h, RX_K_SYNC, s, (k_lms_train<CPLX><<<1, 32, 0, s>>>(d, flush)));
+  KLAUNCH(h, RX_K_SYNC, s, (lms_train_kernel<CPLX>(d.K)<<<1, 32, 0, s>>>(d, flush)));
 }
 
 static void launch_lms_round(rx_handle *h, cudaStream_t s, unsigned char *labels, long long lab_cap,
                              int flush, long long nseg) {
   RxDev &d = h->d;
   const long long S = d.S;
-  if (d.family == RX_PAM) {
-    KLAUNCH(h, RX_K_LMS, s, (k_lms_seg<false, 0><<<gridc(nseg, 4), 128, 0, s>>>(d, flush, (int)nseg)));
-  } else if (d.cpr == 1) {
-    KLAUNCH(h, RX_K_LMS, s, (k_lms_seg<true, 1><<<gridc(nseg, 4), 128, 0, s>>>(d, flush, (int)nseg)));
-  } else {
-    KLAUNCH(h, RX_K_LMS, s, (k_lms_seg<true, 2><<<gridc(nseg, 4), 128, 0, s>>>(d, flush, (int)nseg)));
-  }
+  KLAUNCH(h, RX_K_LMS, s, (lms_seg_kernel(d)<<<gridc(nseg, 4), 128, 0, s>>>(d, flush, (int)nseg)));
   KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_stitch<<<(unsigned)nseg, 256, 0, s>>>(d, (int)nseg)));
   KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_prefix<<<1, 1024, 0, s>>>(d, flush, (int)nseg)));
   KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_final<<<(unsigned)nseg, 256, 0, s>>>(d, labels, lab_cap, (int)nseg)));
@@ -529,11 +549,18 @@ static void launch_lms_rounds(rx_handle *h, cudaStream_t s, unsigned char *label
   if (!flush) {
     const long long est_ready = seg_ub - h->lms_launched_upto;
     if (h->cfg.lms_batch_segments > 0 && est_ready < h->cfg.lms_batch_segments) return;
-    long long nseg = seg_ub - h->lms_launched_upto + h->lms_carry + 2;
+    // grid: segments from the device's seg_next; pending ones are bounded by this batch plus
+    // what could not run last time (data not yet normalised: at most one call of symbols)
+    const long long call_segs = (h->max_call / h->sps) / S + 2;
+    long long nseg = seg_ub - h->lms_launched_upto + call_segs + 2;
     if (nseg > d.seg_cap / 2) nseg = d.seg_cap / 2;
     h->lms_launched_upto = seg_ub;
-    h->lms_carry = nseg;                     // segments not finished now are retried next round
-    launch_lms_round(h, s, labels, lab_cap, flush, nseg);
+    // a segment of epoch e needs the seed of epoch e - D: a batch spanning E epochs needs
+    // 1 + floor(E / D) rounds so nothing waits a whole batch (the rings hold one batch)
+    const long long spe = d.E_sym / S;
+    const long long span = (nseg + spe - 1) / spe + 1;
+    const long long rounds = 1 + span / d.D;
+    for (long long r = 0; r < rounds; ++r) launch_lms_round(h, s, labels, lab_cap, flush, nseg);
     return;
   }
   long long prev = -1;

@@ -111,20 +111,29 @@ def _small(name, **kw):
     return make_config(name, **over)
 
 
-@pytest.mark.parametrize("name,n,extra", [
-    ("C2", 1 << 21, {}),
-    ("C3", 1 << 21, {}),
-    ("C4", 1 << 21, {}),
+@pytest.mark.parametrize("name,n,extra,batch,call_bufs", [
+    ("C2", 1 << 21, {}, None, 1),
+    ("C3", 1 << 21, {}, None, 1),
+    ("C4", 1 << 21, {}, None, 1),
+    ("C2", 1 << 21, {}, 100, 2),      # streaming equaliser batches spanning > D epochs
+    ("C4", 1 << 21, {}, 60, 3),
 ])
-def test_multi_buffer_parity(name, n, extra):
+def test_multi_buffer_parity(name, n, extra, batch, call_bufs):
     """C2/C3/C4 structure at 2^21 samples with 256-block buffers: 8-16 normalisation / CFO
-    buffers and LMS epochs, so the lag-D seeds, carries and stitching are all exercised."""
+    buffers and LMS epochs, so the lag-D seeds, carries and stitching are all exercised; the
+    batched variants run the equaliser while streaming (multi-buffer calls, batches spanning
+    more than D epochs) instead of at flush."""
     _torch_cuda()
     rec, rx = make_config(name, n_samples=n, **extra)
     rx["buffer_blocks"] = 256
+    if batch is not None:
+        rx["lms_batch_segments"] = batch
     out = run_oracle(rec, rx)
-    R, labels, st = run_gpu(rec, rx, chunk=256 * 512)
-    if rec.fmt == "pam":
+    R, labels, st = run_gpu(rec, rx, chunk=256 * 512 * call_bufs,
+                            history_buffers=(None if batch is None else call_bufs + 2))
+    if batch is not None:
+        pass                       # streaming rings no longer hold the whole record
+    elif rec.fmt == "pam":
         nb = rec.n // 512
         assert np.max(np.abs(R.probe("TAU", 0, nb) - out["clock"]["tau"])) < TOL_TAU
         m_end = out["u"].shape[0]
