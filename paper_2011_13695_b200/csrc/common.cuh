@@ -80,11 +80,12 @@ __device__ __forceinline__ void load16(const InView &v, long long p, float scale
       dst[1] = b;
     }
     uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    const float off = -2047.5f * scale;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       int c0 = (int)(w[i] & 0xffffu), c1 = (int)(w[i] >> 16);
-      x[2 * i] = ((float)c0 - 2047.5f) * scale;
-      x[2 * i + 1] = ((float)c1 - 2047.5f) * scale;
+      x[2 * i] = fmaf((float)c0, scale, off);
+      x[2 * i + 1] = fmaf((float)c1, scale, off);
       if (p + 2 * i >= count_from) clip += (c0 == 0 || c0 == 4095);
       if (p + 2 * i + 1 >= count_from) clip += (c1 == 0 || c1 == 4095);
     }
@@ -93,7 +94,7 @@ __device__ __forceinline__ void load16(const InView &v, long long p, float scale
     for (int i = 0; i < 16; ++i) {
       bool pad;
       int c = in_code(v, p + i, pad);
-      x[i] = pad ? padval : ((float)c - 2047.5f) * scale;
+      x[i] = pad ? padval : fmaf((float)c, scale, -2047.5f * scale);   // same rounding as fast paths
       if (!pad && p + i >= count_from) clip += (c == 0 || c == 4095);
     }
   }

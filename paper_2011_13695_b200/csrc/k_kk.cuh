@@ -9,67 +9,76 @@
 #pragma once
 #include "fft.cuh"
 #include "rx_dev.cuh"
+#include "k_pam.cuh"
 
 // ------------------------------------------------------------------ H0, H11-H15
 __global__ void __launch_bounds__(256) k_kk_s1(RxDev d, InView in, long long b0, long long b1) {
   __shared__ float2 tw[1024];
   __shared__ float2 buf[FE_GROUPS][FFT_PAD_N];
-  __shared__ float amp[FE_GROUPS][544];         // padded (i + i/16): conflict-free writes
   const int g = threadIdx.x >> 6, j = threadIdx.x & 63;
   for (int i = threadIdx.x; i < 1024; i += blockDim.x) tw[i] = d.tw[i];
   const long long b = b0 + (long long)blockIdx.x * FE_GROUPS + g;
   const bool act = b < b1;
   int clip = 0, dom = 0;
   long long first_dom = 0x7fffffffffffffffLL;
+  float2 v[8];
+  float amp[4][2];                                      // sqrt(I) of the kept samples (r = 2..5)
   if (act) {
-    const long long p = 512 * b - 512 + 16 * j;
-    float x[16];
-    load16(in, p, d.scale, 0.f, x, 512 * b, clip);   // x_p = 0 for p < 0 (c-0) -> I = dc
-    float h[16];
+    clip = load_block_regs(in, b, d.scale, j, v);       // x_p = 0 for p < 0 (c-0) -> I = dc
+    const long long p0 = 512 * b - 512;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      float I = x[i] + d.dc;                              // P:215 static DC offset
-      const long long pi = p + i;
-      if (I <= 0.0f && pi >= 512 * b) {                   // owned samples counted once (A7)
-        ++dom;
-        if (pi < first_dom) first_dom = pi;
+    for (int r = 0; r < 8; ++r) {
+      float hh[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        float I = (e ? v[r].y : v[r].x) + d.dc;         // P:215 static DC offset
+        const long long p = p0 + 2 * (j + 64 * r) + e;
+        if (I <= 0.0f && r >= 4) {                      // owned samples counted once (A7)
+          ++dom;
+          if (p < first_dom) first_dom = p;
+        }
+        I = fmaxf(I, 1e-12f);
+        hh[e] = 0.5f * logf(I);                         // P:215 logarithm for the phase
+        if (r >= 2 && r < 6) amp[r - 2][e] = sqrtf(I);  // P:215 square root: amplitude
       }
-      I = fmaxf(I, 1e-12f);
-      h[i] = 0.5f * logf(I);                              // P:215 logarithm for the phase
-      const int l = 16 * j + i;
-      if (l >= 256 && l < 768) amp[g][P8(l - 256)] = sqrtf(I);  // P:215 square root: amplitude
+      v[r] = make_float2(hh[0], hh[1]);
     }
+  } else {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) buf[g][P8(8 * j + i)] = make_float2(h[2 * i], h[2 * i + 1]);
+    for (int r = 0; r < 8; ++r) v[r] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) amp[r][0] = amp[r][1] = 0.f;
   }
   block_reduce_clip(d.st, clip);
   dom = __reduce_add_sync(0xffffffffu, dom);
   if ((threadIdx.x & 31) == 0 && dom) atomicAdd((unsigned long long *)&d.st->domain_errors, (unsigned long long)dom);
   if (first_dom != 0x7fffffffffffffffLL) atomicMin(&d.st->first_domain, first_dom);
-  __syncthreads();
-  float2 v[8];
-  fft512<false>(buf[g], j, tw, v);
-  fft512_store(buf[g], j, v);
+  fft512_regs<false>(buf[g], j, tw, v);
+  fft512_publish_upper(buf[g], j, v);
   // FD Hilbert (c-6, A8): Phi = -j sgn(kappa) H, Phi[0] = Phi[512] = 0
   float2 Zk[4], Zn[4];
+  const float2 *pm = fft_mirror_base(buf[g], j);
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     const int k = j + 64 * r;
     float2 Xk, Xn;
-    r2c_pair(buf[g][P8(k)], buf[g][P8((512 - k) & 511)], tw[k], Xk, Xn);
+    r2c_pair(v[r], fft_partner(pm, j, r, v), tw[k], Xk, Xn);
     float2 Pk = cmul_mi(Xk), Pn = cmul_mi(Xn);
     if (k == 0) { Pk = make_float2(0.f, 0.f); Pn = make_float2(0.f, 0.f); }
     c2r_pair(Pk, Pn, tw[k], Zk[r], Zn[r]);
   }
-  float2 Z256 = cconj(cmul_mi(cconj(buf[g][P8(256)])));
+  const float2 Z256 = cconj(cmul_mi(cconj(v[4])));
   __syncthreads();
+  {
+    float2 *paw = buf[g] + j + (j >> 4);
+    float2 *pmw = buf[g] + (512 - j) + ((512 - j) >> 4);
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int k = j + 64 * r;
-    buf[g][P8(k)] = Zk[r];
-    if (k != 0) buf[g][P8(512 - k)] = Zn[r];
+    for (int r = 0; r < 4; ++r) {
+      paw[68 * r] = Zk[r];
+      if (!(j == 0 && r == 0)) pmw[-68 * r] = Zn[r];
+    }
+    if (j == 0) buf[g][256 + (256 >> 4)] = Z256;
   }
-  if (j == 0) buf[g][P8(256)] = Z256;
   __syncthreads();
   fft512<true>(buf[g], j, tw, v);
   // v[r] = 512 (phi[2n] + i phi[2n+1]), n = j + 64 r; kept local [256, 768) <=> r = 2..5
@@ -84,7 +93,7 @@ __global__ void __launch_bounds__(256) k_kk_s1(RxDev d, InView in, long long b0,
       float s0, c0, s1, c1;
       sincosf(sg * ph0, &s0, &c0);
       sincosf(sg * ph1, &s1, &c1);
-      const float a0 = amp[g][P8(2 * n - 256)], a1 = amp[g][P8(2 * n + 1 - 256)];
+      const float a0 = amp[r - 2][0], a1 = amp[r - 2][1];
       // downshift to DC: e^{-j psi(p; sigma f_c)}, 64-bit DDS from the absolute index
       const float2 r0 = dds_rot_neg((unsigned long long)p * d.carrier_inc);
       const float2 r1 = dds_rot_neg((unsigned long long)(p + 1) * d.carrier_inc);

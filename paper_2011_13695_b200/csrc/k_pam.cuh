@@ -13,15 +13,81 @@
 
 // Load block b's 1024 samples (input [512b-512, 512b+512)) into buf as packed complex
 // z[n] = x[2n] + i x[2n+1]; returns clipped count of the samples the block owns
-// ([512b, 512b+512), so every sample is counted once).
+// ([512b, 512b+512), so every sample is counted once). Thread j loads samples 16j..16j+15.
+__device__ __forceinline__ float code_lo(uint32_t w) {     // exact float of the low 16 bits
+  return __uint_as_float((w & 0xFFFFu) | 0x4B000000u) - 8388608.0f;
+}
+__device__ __forceinline__ float code_hi(uint32_t w) {
+  return __uint_as_float((w >> 16) | 0x4B000000u) - 8388608.0f;
+}
 __device__ __forceinline__ int load_block_packed(const InView &in, long long b, float scale,
                                                  float2 *buf, int j) {
-  long long p = 512 * b - 512 + 16 * j;
-  float x[16];
+  const long long p = 512 * b - 512 + 16 * j;
+  float2 *dst = buf + 8 * j + (j >> 1);                     // P8(8 j + i) = dst + i
   int clip = 0;
-  load16(in, p, scale, 0.f, x, 512 * b, clip);
+  if (p >= in.call_start && p + 16 <= in.call_end) {
+    const uint4 *src = reinterpret_cast<const uint4 *>(in.cur + (p - in.call_start));
+    const uint4 a = __ldg(src), c = __ldg(src + 1);
+    const bool owned = j >= 32;                               // p >= 512 b
+    if (owned && p >= in.keep_from) {                         // history ring for later calls
+      uint4 *h = reinterpret_cast<uint4 *>(in.hist_w + (p & (in.hist_cap - 1)));
+      h[0] = a;
+      h[1] = c;
+    }
+    const uint32_t w[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
+    const float off = -2047.5f * scale;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) buf[P8(8 * j + i)] = make_float2(x[2 * i], x[2 * i + 1]);
+    for (int i = 0; i < 8; ++i) {
+      dst[i] = make_float2(fmaf(code_lo(w[i]), scale, off), fmaf(code_hi(w[i]), scale, off));
+      if (owned) clip += __popc(__vcmpeq2(w[i], 0u) | __vcmpeq2(w[i], 0x0FFF0FFFu)) >> 4;
+    }
+  } else {
+    float x[16];
+    load16(in, p, scale, 0.f, x, 512 * b, clip);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dst[i] = make_float2(x[2 * i], x[2 * i + 1]);
+  }
+  return clip;
+}
+
+// Thread j of a block's group receives v[r] = (x[2(j + 64 r)], x[2(j + 64 r) + 1]) of block b's
+// frame (input [512b-512, 512b+512)) directly in registers: the FFT's pass-1 operands. The
+// block owns the frame's second half (r >= 4): those samples are counted for clipping and
+// appended to the history ring when they are the call's tail.
+__device__ __forceinline__ int load_block_regs(const InView &in, long long b, float scale, int j,
+                                               float2 (&v)[8]) {
+  const long long p0 = 512 * b - 512;
+  const float off = -2047.5f * scale;
+  int clip = 0;
+  if (p0 >= in.call_start && p0 + 1024 <= in.call_end) {
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(in.cur + (p0 - in.call_start));
+    uint32_t w[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) w[r] = __ldg(src + j + 64 * r);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = make_float2(fmaf(code_lo(w[r]), scale, off), fmaf(code_hi(w[r]), scale, off));
+#pragma unroll
+    for (int r = 4; r < 8; ++r) {
+      clip += __popc(__vcmpeq2(w[r], 0u) | __vcmpeq2(w[r], 0x0FFF0FFFu)) >> 4;
+      const long long p = p0 + 2 * (j + 64 * r);
+      if (p >= in.keep_from)
+        reinterpret_cast<uint32_t *>(in.hist_w)[(p & (in.hist_cap - 1)) >> 1] = w[r];
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      float x[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const long long p = p0 + 2 * (j + 64 * r) + e;
+        bool pad;
+        const int c = in_code(in, p, pad);
+        x[e] = pad ? 0.f : fmaf((float)c, scale, off);
+        if (!pad && r >= 4) clip += (c == 0 || c == 4095);
+      }
+      v[r] = make_float2(x[0], x[1]);
+    }
+  }
   return clip;
 }
 
@@ -31,6 +97,9 @@ __device__ __forceinline__ void block_reduce_clip(DevState *st, int clip) {
 }
 
 // ------------------------------------------------------------------ H0-H3
+// HREAL: the static-EQ spectrum is real (zero-phase symmetric real taps, the PAM case) and is
+// applied as a real scale per bin.
+template <bool HREAL>
 __global__ void __launch_bounds__(256) k_pam_fe(RxDev d, InView in, long long b0, long long b1) {
   __shared__ float2 tw[1024];
   __shared__ float2 buf[FE_GROUPS][FFT_PAD_N];
@@ -40,34 +109,43 @@ __global__ void __launch_bounds__(256) k_pam_fe(RxDev d, InView in, long long b0
   const long long b = b0 + (long long)blockIdx.x * FE_GROUPS + g;
   const bool act = b < b1;
   int clip = 0;
-  if (act) clip = load_block_packed(in, b, d.scale, buf[g], j);
-  block_reduce_clip(d.st, clip);
-  __syncthreads();
   float2 v[8];
-  fft512<false>(buf[g], j, tw, v);
-  fft512_store(buf[g], j, v);
+  if (act) clip = load_block_regs(in, b, d.scale, j, v);
+  else {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = make_float2(0.f, 0.f);
+  }
+  block_reduce_clip(d.st, clip);
+  fft512_regs<false>(buf[g], j, tw, v);
+  fft512_publish_upper(buf[g], j, v);
   // C_b = sum_{k<512} Y[k] conj(Y[k+512]) = Y0 conj(Y512) + Y256^2 + 2 sum_{k=1}^{255} Y[k] Y[512-k]
-  double cr = 0.0, ci = 0.0;
+  // (per-thread fp32 partials of 4-5 terms, fp64 across threads)
+  float cr = 0.f, ci = 0.f;
   if (act) {
+    const float2 *pm = fft_mirror_base(buf[g], j);
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int k = j + 64 * r;
       float2 Xk, Xn;
-      r2c_pair(buf[g][P8(k)], buf[g][P8((512 - k) & 511)], tw[k], Xk, Xn);
-      const float2 Yk = cmul(Xk, __ldg(d.H + k)), Yn = cmul(Xn, __ldg(d.H + 512 - k));
-      const double ar = Yk.x, ai = Yk.y, br = Yn.x, bi = Yn.y;
-      if (k == 0) { cr += ar * br + ai * bi; ci += ai * br - ar * bi; }   // Y0 conj(Y512)
-      else { cr += 2.0 * (ar * br - ai * bi); ci += 2.0 * (ar * bi + ai * br); }
+      r2c_pair(v[r], fft_partner(pm, j, r, v), tw[k], Xk, Xn);
+      float2 Yk, Yn;
+      if (HREAL) { Yk = cscale(Xk, __ldg(d.Hr + k)); Yn = cscale(Xn, __ldg(d.Hr + 512 - k)); }
+      else { Yk = cmul(Xk, __ldg(d.H + k)); Yn = cmul(Xn, __ldg(d.H + 512 - k)); }
+      if (k == 0) { cr = fmaf(Yk.x, Yn.x, fmaf(Yk.y, Yn.y, cr)); ci = fmaf(Yk.y, Yn.x, fmaf(-Yk.x, Yn.y, ci)); }
+      else {
+        cr = fmaf(2.f * Yk.x, Yn.x, fmaf(-2.f * Yk.y, Yn.y, cr));
+        ci = fmaf(2.f * Yk.x, Yn.y, fmaf(2.f * Yk.y, Yn.x, ci));
+      }
     }
     if (j == 0) {
-      const float2 Y = cmul(cconj(buf[g][P8(256)]), __ldg(d.H + 256));
-      cr += (double)Y.x * Y.x - (double)Y.y * Y.y;
-      ci += 2.0 * (double)Y.x * Y.y;
+      const float2 Z = v[4];                                   // X[256] = conj Z[256]
+      const float2 Y = HREAL ? cscale(cconj(Z), __ldg(d.Hr + 256)) : cmul(cconj(Z), __ldg(d.H + 256));
+      cr = fmaf(Y.x, Y.x, fmaf(-Y.y, Y.y, cr));
+      ci = fmaf(2.f * Y.x, Y.y, ci);
     }
   }
-  cr = warp_sum_d(cr);
-  ci = warp_sum_d(ci);
-  if ((threadIdx.x & 31) == 0) red[g][(threadIdx.x >> 5) & 1] = make_double2(cr, ci);
+  const double dr = warp_sum_d((double)cr), di = warp_sum_d((double)ci);
+  if ((threadIdx.x & 31) == 0) red[g][(threadIdx.x >> 5) & 1] = make_double2(dr, di);
   __syncthreads();
   if (act && j == 0)
     d.C[rmod(b, d.blk_cap)] = make_double2(red[g][0].x + red[g][1].x, red[g][0].y + red[g][1].y);
@@ -235,6 +313,7 @@ __global__ void __launch_bounds__(256) k_pam_tau(RxDev d, long long b0, long lon
 }
 
 // ------------------------------------------------------------------ H1, H2, H5-H7
+template <bool HREAL>
 __global__ void __launch_bounds__(256) k_pam_be(RxDev d, InView in, long long b0, long long b1) {
   __shared__ float2 tw[1024];
   __shared__ float2 buf[FE_GROUPS][FFT_PAD_N];
@@ -243,52 +322,59 @@ __global__ void __launch_bounds__(256) k_pam_be(RxDev d, InView in, long long b0
   for (int i = threadIdx.x; i < 1024; i += blockDim.x) tw[i] = d.tw[i];
   const long long b = b0 + (long long)blockIdx.x * FE_GROUPS + g;
   const bool act = b < b1;
-  if (act) load_block_packed(in, b, d.scale, buf[g], j);
-  __syncthreads();
   float2 v[8];
-  fft512<false>(buf[g], j, tw, v);
-  fft512_store(buf[g], j, v);
+  if (act) load_block_regs(in, b, d.scale, j, v);
+  else {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = make_float2(0.f, 0.f);
+  }
+  fft512_regs<false>(buf[g], j, tw, v);
+  fft512_publish_upper(buf[g], j, v);
   // clock phase of this block: s = 2 tau, i_b = rint(s), f_b = s - i_b   (c-4)
-  double tau = act ? d.tau[rmod(b, d.blk_cap)] : 0.0;
-  const double s = 2.0 * tau;
-  const double ibd = rint(s);
-  const float f = (float)(s - ibd);
+  const double tau = act ? d.tau[rmod(b, d.blk_cap)] : 0.0;
+  const double sd = 2.0 * tau;
+  const double ibd = rint(sd);
+  const float f = (float)(sd - ibd);
+  // FD clock correction Y'[k] = Y[k] e^{+j pi kappa(k) f / 512}: rotations for k = j + 64 r from
+  // base e^{j pi j f/512} and step e^{j pi f/8}; the partner 512-k is e^{j pi f} conj(rot(k))
+  float2 rot, step, nyq;
+  sincospif((float)j * f * (1.0f / 512.0f), &rot.y, &rot.x);
+  sincospif(f * 0.125f, &step.y, &step.x);
+  sincospif(f, &nyq.y, &nyq.x);
   float2 Zk[4], Zn[4], Z256;
+  const float2 *pm = fft_mirror_base(buf[g], j);
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     const int k = j + 64 * r;
     float2 Xk, Xn;
-    r2c_pair(buf[g][P8(k)], buf[g][P8((512 - k) & 511)], tw[k], Xk, Xn);
-    float2 Yk = cmul(Xk, __ldg(d.H + k)), Yn = cmul(Xn, __ldg(d.H + 512 - k));
-    // Y'[k] = Y[k] e^{+j 2 pi kappa(k) f / 1024}; kappa(k) = k, kappa(512-k) = 512-k,
-    // Nyquist (k = 0 partner): Re(Y[512] e^{-j pi f})
-    float sk, ck, sn, cn;
-    sincospif((float)k * f * (1.0f / 512.0f), &sk, &ck);
-    Yk = cmul(Yk, make_float2(ck, sk));
-    if (k == 0) {
-      sincospif(f, &sn, &cn);
-      Yn = make_float2(Yn.x * cn + Yn.y * sn, 0.0f);
-    } else {
-      sincospif((float)(512 - k) * f * (1.0f / 512.0f), &sn, &cn);
-      Yn = cmul(Yn, make_float2(cn, sn));
-    }
+    r2c_pair(v[r], fft_partner(pm, j, r, v), tw[k], Xk, Xn);
+    float2 Yk, Yn;
+    if (HREAL) { Yk = cscale(Xk, __ldg(d.Hr + k)); Yn = cscale(Xn, __ldg(d.Hr + 512 - k)); }
+    else { Yk = cmul(Xk, __ldg(d.H + k)); Yn = cmul(Xn, __ldg(d.H + 512 - k)); }
+    Yk = cmul(Yk, rot);
+    if (k == 0) Yn = make_float2(Yn.x * nyq.x + Yn.y * nyq.y, 0.0f);   // Nyquist: Re(Y e^{-j pi f})
+    else Yn = cmul(Yn, cmulc(nyq, rot));
     c2r_pair(Yk, Yn, tw[k], Zk[r], Zn[r]);
+    rot = cmul(rot, step);
   }
   {
-    float2 Y = cmul(cconj(buf[g][P8(256)]), __ldg(d.H + 256));
-    float s2, c2;
-    sincospif(256.0f * f * (1.0f / 512.0f), &s2, &c2);
-    Y = cmul(Y, make_float2(c2, s2));
-    Z256 = cconj(Y);
+    const float2 Z = v[4];
+    float2 Y = HREAL ? cscale(cconj(Z), __ldg(d.Hr + 256)) : cmul(cconj(Z), __ldg(d.H + 256));
+    float2 r256;
+    sincospif(0.5f * f, &r256.y, &r256.x);
+    Z256 = cconj(cmul(Y, r256));
   }
   __syncthreads();
+  {
+    float2 *paw = buf[g] + j + (j >> 4);
+    float2 *pmw = buf[g] + (512 - j) + ((512 - j) >> 4);
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int k = j + 64 * r;
-    buf[g][P8(k)] = Zk[r];
-    if (k != 0) buf[g][P8(512 - k)] = Zn[r];
+    for (int r = 0; r < 4; ++r) {
+      paw[68 * r] = Zk[r];
+      if (!(j == 0 && r == 0)) pmw[-68 * r] = Zn[r];
+    }
+    if (j == 0) buf[g][256 + (256 >> 4)] = Z256;
   }
-  if (j == 0) buf[g][P8(256)] = Z256;
   __syncthreads();
   fft512<true>(buf[g], j, tw, v);
   fft512_store(buf[g], j, v);
@@ -297,15 +383,20 @@ __global__ void __launch_bounds__(256) k_pam_be(RxDev d, InView in, long long b0
   if (act) {
     const long long Mb = d.Mb[rmod(b, d.blk_cap)], Mb1 = d.Mb[rmod(b + 1, d.blk_cap)];
     const long long lo = Mb > 0 ? Mb : 0;
-    const long long ib = (long long)ibd;
-    for (long long m = lo + j; m < Mb1; m += 64) {
-      long long loc = 2 * m + ib - 512 * b + 512;
+    const int base2 = (int)(2 * lo + (long long)ibd - 512 * b + 512);   // local index of m = lo
+    const int cnt = (int)(Mb1 - lo);
+    float ps = 0.f;
+    for (int t = j; t < cnt; t += 64) {
+      const long long m = lo + t;
+      int loc = base2 + 2 * t;                                        // 2m + i_b - 512b + 512
       if (loc < 0 || loc >= 1024) { set_flag(d.st, 8); loc = loc < 0 ? 0 : 1023; }
-      const float2 zz = buf[g][P8((int)(loc >> 1))];
+      const int n = loc >> 1;
+      const float2 zz = buf[g][n + (n >> 4)];
       const float y = ((loc & 1) ? zz.y : zz.x) * (1.0f / 512.0f);
       d.u[rmod(m, d.sym_cap)] = y;
-      part += (double)y;
+      ps += y;
     }
+    part = (double)ps;
   }
   part = warp_sum_d(part);
   if ((threadIdx.x & 31) == 0) red[g][(threadIdx.x >> 5) & 1] = part;
@@ -313,7 +404,6 @@ __global__ void __launch_bounds__(256) k_pam_be(RxDev d, InView in, long long b0
   if (act && j == 0) d.blk_sum[rmod(b, d.blk_cap)] = red[g][0] + red[g][1];
 }
 
-// ------------------------------------------------------------------ H8 normalisation
 // Buffer-wise normalisation (P:167 'three kernels: initialization, estimation of the DC-offset,
 // and estimation of the amplitude'; c-5): dc = mean u, A = mean|u - dc| / (M / (2 (M-1))),
 // u^ = (u - dc) / A over the symbols emitted by each buffer's blocks. Reductions are fixed

@@ -315,6 +315,16 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
       H[k] = make_float2((float)re, (float)im);
     }
     TRY(dupload(h, &d.H, H));
+    std::vector<float> Hr(1024);
+    bool real = true;
+    for (int k = 0; k < 1024; ++k) { Hr[k] = H[k].x; if (H[k].y != 0.0f) real = false; }
+    // symmetric real taps give an exactly real spectrum up to rounding: treat |imag| < 1e-6 max|H|
+    float mx = 0.f;
+    for (int k = 0; k < 1024; ++k) mx = fmaxf(mx, fabsf(H[k].x));
+    real = true;
+    for (int k = 0; k < 1024; ++k) if (fabsf(H[k].y) > 1e-7f * mx) real = false;
+    d.H_real = real ? 1 : 0;
+    TRY(dupload(h, &d.Hr, Hr));
   }
   // decision levels / thresholds (c-11)
   {
@@ -583,7 +593,8 @@ static void run_pam(rx_handle *h, cudaStream_t s, const InView &in, unsigned cha
   const long long BB = d.buffer_blocks;
   const long long fe_target = h->n_in / 512;
   if (fe_target > h->fe_done) {
-    KLAUNCH(h, RX_K_PAM_FE, s, (k_pam_fe<<<gridc(fe_target - h->fe_done, FE_GROUPS), 256, 0, s>>>(d, in, h->fe_done, fe_target)));
+    if (d.H_real) KLAUNCH(h, RX_K_PAM_FE, s, (k_pam_fe<true><<<gridc(fe_target - h->fe_done, FE_GROUPS), 256, 0, s>>>(d, in, h->fe_done, fe_target)));
+    else KLAUNCH(h, RX_K_PAM_FE, s, (k_pam_fe<false><<<gridc(fe_target - h->fe_done, FE_GROUPS), 256, 0, s>>>(d, in, h->fe_done, fe_target)));
     h->fe_done = fe_target;
   }
   long long clk_target = flush ? h->fe_done : h->fe_done - d.clock_half;
@@ -597,7 +608,8 @@ static void run_pam(rx_handle *h, cudaStream_t s, const InView &in, unsigned cha
   }
   long long be_target = flush ? h->fe_done - 1 : h->clk_done - 1;
   if (be_target > h->be_done) {
-    KLAUNCH(h, RX_K_PAM_BE, s, (k_pam_be<<<gridc(be_target - h->be_done, FE_GROUPS), 256, 0, s>>>(d, in, h->be_done, be_target)));
+    if (d.H_real) KLAUNCH(h, RX_K_PAM_BE, s, (k_pam_be<true><<<gridc(be_target - h->be_done, FE_GROUPS), 256, 0, s>>>(d, in, h->be_done, be_target)));
+    else KLAUNCH(h, RX_K_PAM_BE, s, (k_pam_be<false><<<gridc(be_target - h->be_done, FE_GROUPS), 256, 0, s>>>(d, in, h->be_done, be_target)));
     h->be_done = be_target;
   }
   {

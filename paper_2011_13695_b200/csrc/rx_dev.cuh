@@ -70,6 +70,8 @@ struct RxDev {
   // ---- constant tables (device)
   const float2 *tw;          // e^{-2 pi i k/1024}, k < 1024
   const float2 *H;           // static-EQ spectrum [1024]
+  const float *Hr;           // its real part (used when the spectrum is real: H_real = 1)
+  int H_real;
   const float *thr;          // PAM thresholds [M-1]
   const float *lvl;          // levels per axis [L]
   const float2 *ref_val;     // reference symbol values [P]
