@@ -103,6 +103,12 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------ helpers
+def multi_summary(counters):
+    from paper_2011_13695_b200 import multi
+    out = multi.summarize(counters)
+    return {k: (round(v, 6) if isinstance(v, float) else v) for k, v in out.items()}
+
+
 def rx_fields(rx: dict) -> dict:
     keys = ("lms_taps", "lms_block", "lms_segment", "lms_overlap", "mu", "train_symbols",
             "sync_start", "sync_window", "warmup_symbols", "cpr_test_phases")
@@ -150,12 +156,14 @@ def run_mode(torch, dist, R, ring, n_step, steps, warmup, world, dev, units, lab
     cnt = torch.zeros(8, dtype=torch.float64, device=dev)
     ch = Stream1(R, ring, n_step, labels, stream)
 
+    from paper_2011_13695_b200 import multi
+
     def one_step():
         ch.step()
         R.export_counters(cnt, stream=stream)
-        if world > 1:
+        if world > 1:                      # one packed NCCL all-reduce of the counters per round
             with torch.cuda.stream(stream):
-                dist.all_reduce(cnt)
+                multi.allreduce_counters(cnt)
 
     for _ in range(warmup):
         one_step()
@@ -313,6 +321,7 @@ def gpu_main(args):
         "host_enqueue_ms_per_step": round(res["host_ms"], 4),
         "hbm_roofline_frac_literal": round(value * 1e9 / world * 2.5 / 6537e9, 5),
         "x_paper_realtime": round(value / world / PAPER_REALTIME_GSA, 2),
+        "quality_all_ranks": multi_summary(res["counters"]),
         "quality": {"ber": st["bit_errors"] / max(st["bits"], 1),
                     "evm_db": 10 * math.log10(st["evm_num"] / st["evm_den"]) if st["evm_den"] > 0 else None,
                     "sync_gamma": st["sync_gamma"], "flags": st["status_flags"]},

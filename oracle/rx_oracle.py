@@ -631,12 +631,14 @@ def lms_segments(v, stride, off, m_end, seeds_fn, slicer: _Slicer, lp: LmsParams
         W = W + lp.mu * np.einsum("sbk,sb->sk", U, np.conj(e))
         if lp.widely_linear:
             Vw = Vw + lp.mu * np.einsum("sbk,sb->sk", np.conj(U), np.conj(e))
-        if np.any(np.linalg.norm(W, axis=1) > 1e3):
+        if np.any(np.abs(W) > 1e3):        # DESIGN.md R-DIV: any tap beyond 1e3 ...
             diverged = True
         for i in range(ns):
             ok = valid[i]
             if np.any(ok):
                 out_m[i].append(m[i, ok]); out_idx[i].append(idx[i, ok]); out_z[i].append(zp[i, ok])
+    if np.any(np.linalg.norm(W, axis=1) > 1e3):   # ... or the tap norm at the end of the run
+        diverged = True
     res = []
     for i, s in enumerate(segs):
         mm = np.concatenate(out_m[i]) if out_m[i] else np.zeros(0, np.int64)

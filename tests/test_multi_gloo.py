@@ -1,0 +1,83 @@
+"""Multi-process (world size 2, gloo, CPU) tests of the multi-GPU host logic: channel
+sharding and the packed counter all-reduce used once per round."""
+import math
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2011_13695_b200 import multi
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        mine = multi.channel_shard(64, world, rank)
+        # per-channel counters: channel c contributes bit_errors = c, bits = 1000, evm = (c, 10)
+        t = torch.zeros(multi.NCOUNTERS, dtype=torch.float64)
+        for ch in mine:
+            t[multi.IDX["bit_errors"]] += ch
+            t[multi.IDX["bits"]] += 1000
+            t[multi.IDX["symbols_counted"]] += 500
+            t[multi.IDX["evm_num"]] += ch
+            t[multi.IDX["evm_den"]] += 10
+        multi.allreduce_counters(t)
+        allch = [None] * world
+        dist.all_gather_object(allch, mine)
+        q.put((rank, t.tolist(), allch))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_counter_allreduce_and_sharding_world2():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, t, allch in res:
+        flat = sorted(c for part in allch for c in part)
+        assert flat == list(range(64))                       # every channel exactly once
+        assert t[multi.IDX["bit_errors"]] == sum(range(64))  # sum over both ranks
+        assert t[multi.IDX["bits"]] == 64 * 1000
+        assert t[multi.IDX["evm_den"]] == 640
+    assert res[0][1] == res[1][1]                            # identical on every rank
+
+
+def test_channel_shard_properties():
+    for world in (1, 2, 3, 8):
+        got = [c for r in range(world) for c in multi.channel_shard(64, world, r)]
+        assert got == list(range(64))
+    with pytest.raises(ValueError):
+        multi.channel_shard(64, 2, 2)
+
+
+def test_summary_q_from_ber():
+    c = [0.0] * multi.NCOUNTERS
+    c[multi.IDX["bit_errors"]] = 4266
+    c[multi.IDX["bits"]] = 1_000_000
+    c[multi.IDX["evm_num"]] = 1.0
+    c[multi.IDX["evm_den"]] = 100.0
+    s = multi.summarize(c)
+    assert abs(s["q_db"] - 8.4) < 2e-3          # HD-FEC threshold
+    assert abs(s["evm_db"] + 20.0) < 1e-12
+    assert math.isinf(multi.q_db_from_ber(0.0))
