@@ -166,63 +166,70 @@ __global__ void __launch_bounds__(256) k_kk_s2(RxDev d, long long b0, long long 
 }
 
 // ------------------------------------------------------------------ H19-H20
-// Partial sums over the complete 1024-sample chunks of buffer beta:
-//   pow_part[cta] = sum |z|^2 (all samples of [qlo, qhi)),
-//   S_part[cta][k] = sum_chunks |DFT_1024(z^4)[k]|^2
-__global__ void __launch_bounds__(256) k_cfo_partial(RxDev d, long long qlo, long long qhi) {
+// Per-buffer power normalisation and coarse + fine CFO (c-8, reading R-CFO), batched over the
+// buffers that complete in one call (blockIdx.y = buffer of the call):
+//  k_cfo_spec   16 chunks of 1024 per CTA (one per 64-thread group): |DFT_1024(z^4)|^2 summed
+//               over the CTA's chunks in fixed group order -> one partial row; power partials
+//  k_cfo_final  one CTA per buffer: rows -> S[k] (fixed order), P, k* (lowest on ties), delta,
+//               coarse df and its DDS increment
+//  k_cfo_fine   one warp per chunk: a_i = sum (z e^{-j psi_c})^4; the last CTA of a buffer forms
+//               rho = sum a_{i+1} conj(a_i) in index order -> fine df
+//  k_cfo_carry  one thread: DDS increments and phase origins carried across buffers
+//  k_kk_zprime  z' = z / sqrt(P) e^{-j psi'} over the call's buffers
+#define CFO_GROUPS 16
+__device__ __forceinline__ void buf_range(const RxDev &d, long long beta, long long qfront,
+                                          long long &qlo, long long &qhi) {
+  const long long Q = (long long)d.buffer_blocks * 256;
+  qlo = beta * Q;
+  qhi = qlo + Q < qfront ? qlo + Q : qfront;
+}
+
+__global__ void __launch_bounds__(1024) k_cfo_spec(RxDev d, long long beta0, long long qfront) {
   extern __shared__ float2 sm[];
   float2 *tw = sm;
-  float2 *bufs = sm + 1024;                    // [4 groups][2][FFT_PAD_N]
-  float *S = reinterpret_cast<float *>(bufs + 8 * FFT_PAD_N);   // [1024]
-  __shared__ double red[8];
+  float2 *bufs = sm + 1024;                    // [CFO_GROUPS][2][FFT_PAD_N]
+  float *S = reinterpret_cast<float *>(bufs + 2 * CFO_GROUPS * FFT_PAD_N);   // [1024]
+  __shared__ double red[32];
   const int g = threadIdx.x >> 6, j = threadIdx.x & 63;
+  long long qlo, qhi;
+  buf_range(d, beta0 + blockIdx.y, qfront, qlo, qhi);
   for (int i = threadIdx.x; i < 1024; i += blockDim.x) { tw[i] = d.tw[i]; S[i] = 0.f; }
-  const long long n = qhi - qlo;
-  const long long nch = n / 1024;
+  const long long nch = (qhi - qlo) / 1024;
+  // power partial over this CTA's share of all samples (including a tail shorter than a chunk)
   double pw = 0.0;
-  for (long long q = qlo + (long long)blockIdx.x * blockDim.x + threadIdx.x; q < qhi;
-       q += (long long)gridDim.x * blockDim.x)
-    pw += (double)cabs2(d.z[rmod(q, d.z_cap)]);
-  __syncthreads();
+  {
+    const long long n = qhi - qlo;
+    const long long a0 = qlo + n * blockIdx.x / gridDim.x, a1 = qlo + n * (blockIdx.x + 1) / gridDim.x;
+    for (long long q = a0 + threadIdx.x; q < a1; q += blockDim.x) pw += (double)cabs2(d.z[rmod(q, d.z_cap)]);
+  }
+  const long long c = (long long)blockIdx.x * CFO_GROUPS + g;
+  const bool act = c < nch;
+  float2 *be = bufs + (g * 2) * FFT_PAD_N, *bo = bufs + (g * 2 + 1) * FFT_PAD_N;
+  float2 ve[8], vo[8];
+  float4 zz[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    zz[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (act) zz[r] = *reinterpret_cast<const float4 *>(d.z + rmod(qlo + 1024 * c + 2 * (j + 64 * r), d.z_cap));
+  }
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const float2 a = make_float2(zz[r].x, zz[r].y), bq = make_float2(zz[r].z, zz[r].w);
+    const float2 a2 = cmul(a, a), b2 = cmul(bq, bq);
+    ve[r] = cmul(a2, a2);
+    vo[r] = cmul(b2, b2);
+  }
+  fft512_regs<false>(be, j, tw, ve);
+  fft512_regs<false>(bo, j, tw, vo);
   float acc[16];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) acc[i] = 0.f;
-  const long long per = (nch + gridDim.x - 1) / gridDim.x;   // chunks per CTA (contiguous)
-  const long long c0 = (long long)blockIdx.x * per;
-  const long long c1 = c0 + per < nch ? c0 + per : nch;
-  for (long long cb = c0; cb < c1; cb += 4) {
-    const long long c = cb + g;
-    float2 *be = bufs + (g * 2) * FFT_PAD_N, *bo = bufs + (g * 2 + 1) * FFT_PAD_N;
-    const bool act = c < c1;
-    for (int t = j; t < 512; t += 64) {
-      float2 a = make_float2(0.f, 0.f), bq = a;
-      if (act) {
-        const long long q = qlo + 1024 * c + 2 * t;
-        a = d.z[rmod(q, d.z_cap)];
-        bq = d.z[rmod(q + 1, d.z_cap)];
-      }
-      float2 a2 = cmul(a, a), b2 = cmul(bq, bq);
-      be[P8(t)] = cmul(a2, a2);
-      bo[P8(t)] = cmul(b2, b2);
-    }
-    __syncthreads();
-    float2 ve[8], vo[8];
-    fft512<false>(be, j, tw, ve);
-    __syncthreads();
-    fft512<false>(bo, j, tw, vo);
-    if (act) {
-#pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        const int k = j + 64 * r;
-        const float2 od = cmul(vo[r], tw[k]);
-        acc[r] += cabs2(cadd(ve[r], od));        // X[k]
-        acc[8 + r] += cabs2(csub(ve[r], od));    // X[k + 512]
-      }
-    }
-    __syncthreads();
+  for (int r = 0; r < 8; ++r) {
+    const int k = j + 64 * r;
+    const float2 od = cmul(vo[r], tw[k]);
+    acc[r] = act ? cabs2(cadd(ve[r], od)) : 0.f;        // X[k]
+    acc[8 + r] = act ? cabs2(csub(ve[r], od)) : 0.f;    // X[k + 512]
   }
-  // combine the 4 groups' accumulators in fixed order
-  for (int gg = 0; gg < 4; ++gg) {
+  for (int gg = 0; gg < CFO_GROUPS; ++gg) {             // groups in fixed order
     if (g == gg) {
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
@@ -232,36 +239,45 @@ __global__ void __launch_bounds__(256) k_cfo_partial(RxDev d, long long qlo, lon
     }
     __syncthreads();
   }
-  for (int i = threadIdx.x; i < 1024; i += blockDim.x) d.cfo_part[(long long)blockIdx.x * 1024 + i] = S[i];
+  const long long row = (long long)blockIdx.y * gridDim.x + blockIdx.x;
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) d.cfo_part[row * 1024 + i] = S[i];
   pw = warp_sum_d(pw);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = pw;
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
-    for (int i = 0; i < 8; ++i) t += red[i];
-    d.cfo_pow[blockIdx.x] = t;
+    for (int i = 0; i < 32; ++i) t += red[i];
+    d.cfo_pow[row] = t;
   }
 }
 
-// P, k* = argmax S (lowest on ties), delta, df, DDS increment and carried origin (c-8).
-__global__ void __launch_bounds__(1024) k_cfo_final(RxDev d, long long beta, long long qlo, long long qhi) {
+__global__ void __launch_bounds__(1024) k_cfo_final(RxDev d, long long beta0, long long qfront, int nrows) {
   __shared__ double Sd[1024];
   __shared__ double wv[32];
   __shared__ int wi[32];
+  __shared__ double pws[32];
   const int t = threadIdx.x;
-  const int G = d.cfo_G;
+  const long long beta = beta0 + blockIdx.x;
+  long long qlo, qhi;
+  buf_range(d, beta, qfront, qlo, qhi);
+  const long long rb = (long long)blockIdx.x * nrows;
   double s = 0.0;
-  int c = 0;
-  for (; c + 8 <= G; c += 8) {          // 8 independent loads in flight, summed in index order
-    float v[8];
+  {
+    int r = 0;
+    for (; r + 8 <= nrows; r += 8) {          // 8 independent loads in flight, summed in order
+      float v[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = d.cfo_part[(long long)(c + i) * 1024 + t];
+      for (int i = 0; i < 8; ++i) v[i] = d.cfo_part[(rb + r + i) * 1024 + t];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) s += (double)v[i];
+      for (int i = 0; i < 8; ++i) s += (double)v[i];
+    }
+    for (; r < nrows; ++r) s += (double)d.cfo_part[(rb + r) * 1024 + t];
   }
-  for (; c < G; ++c) s += (double)d.cfo_part[(long long)c * 1024 + t];
   Sd[t] = s;
-  // argmax, lowest index on ties
+  double pw = 0.0;
+  for (int r = t; r < nrows; r += blockDim.x) pw += d.cfo_pow[rb + r];
+  pw = warp_sum_d(pw);
+  if ((t & 31) == 0) pws[t >> 5] = pw;
   double bv = s;
   int bi = t;
 #pragma unroll
@@ -274,7 +290,7 @@ __global__ void __launch_bounds__(1024) k_cfo_final(RxDev d, long long beta, lon
   __syncthreads();
   if (t == 0) {
     double P = 0.0;
-    for (int c = 0; c < G; ++c) P += d.cfo_pow[c];
+    for (int w = 0; w < 32; ++w) P += pws[w];
     const long long n = qhi - qlo;
     P = n > 0 ? P / (double)n : 1.0;
     if (!(P > 0.0)) P = 1.0;
@@ -283,8 +299,9 @@ __global__ void __launch_bounds__(1024) k_cfo_final(RxDev d, long long beta, lon
     for (int w = 1; w < 32; ++w)
       if (wv[w] > best || (wv[w] == best && wi[w] < k)) { best = wv[w]; k = wi[w]; }
     const long long nch = n / 1024;
-    double df = d.st->cfo_df_prev;
-    if (nch > 0) {
+    double df = 0.0;
+    const bool have = nch > 0;
+    if (have) {
       const double lm = log(Sd[(k + 1023) & 1023]), l0 = log(Sd[k]), lp = log(Sd[(k + 1) & 1023]);
       const double delta = 0.5 * (lm - lp) / (lm - 2.0 * l0 + lp);
       const double kap = (double)(k < 512 ? k : k - 1024);
@@ -296,61 +313,72 @@ __global__ void __launch_bounds__(1024) k_cfo_final(RxDev d, long long beta, lon
     cp.P = P;
     cp.inv_sqrtP = (float)(1.0 / sqrt(P));
     cp.kstar = k;
-    cp.df = df;                      // coarse; refined by k_cfo_fine_final
+    cp.df = df;                      // coarse (refined by k_cfo_fine; kstar < 0: reuse previous)
     cp.inc = (unsigned long long)llrint(ldexp(df / d.fs2, 64));
     cp.origin = 0ull;
     d.cfo[rmod(beta, d.buf_cap)] = cp;
   }
 }
 
-// Fine stage (reading R-CFO): a_i = sum_{chunk i} (z_q e^{-j 2 pi df_c n / f_s2})^4,
-// n = q - q_lo, the coarse rotation from a 64-bit DDS word n * inc_c.
-__global__ void __launch_bounds__(256) k_cfo_fine(RxDev d, long long beta, long long qlo, long long qhi) {
-  __shared__ double2 red[8];
+__global__ void __launch_bounds__(256) k_cfo_fine(RxDev d, long long beta0, long long qfront, int cta_per_buf) {
+  __shared__ int ticket;
+  const long long beta = beta0 + blockIdx.y;
+  long long qlo, qhi;
+  buf_range(d, beta, qfront, qlo, qhi);
   const long long nch = (qhi - qlo) / 1024;
-  const CfoParam cp = d.cfo[rmod(beta, d.buf_cap)];
-  for (long long i = blockIdx.x; i < nch; i += gridDim.x) {
+  CfoParam *cpp = &d.cfo[rmod(beta, d.buf_cap)];
+  const unsigned long long inc = cpp->inc;
+  const int lane = threadIdx.x & 31;
+  const long long i = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  double2 *abuf = d.cfo_a + (long long)blockIdx.y * (d.buffer_blocks / 4 + 1);
+  if (i < nch) {
+    float2 zz[32];
+#pragma unroll
+    for (int u = 0; u < 32; ++u) zz[u] = d.z[rmod(qlo + 1024 * i + lane + 32 * u, d.z_cap)];
     float ax = 0.f, ay = 0.f;
-    for (int t = threadIdx.x; t < 1024; t += blockDim.x) {
-      const long long n = 1024 * i + t;
-      float2 zz = cmul(d.z[rmod(qlo + n, d.z_cap)], dds_rot_neg((unsigned long long)n * cp.inc));
-      float2 z2 = cmul(zz, zz);
-      float2 z4 = cmul(z2, z2);
-      ax += z4.x; ay += z4.y;
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+      const long long n = 1024 * i + lane + 32 * u;
+      const float2 w = cmul(zz[u], dds_rot_neg((unsigned long long)n * inc));
+      const float2 w2 = cmul(w, w), w4 = cmul(w2, w2);
+      ax += w4.x;
+      ay += w4.y;
     }
-    double sx = warp_sum_d((double)ax), sy = warp_sum_d((double)ay);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = make_double2(sx, sy);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double2 a = make_double2(0.0, 0.0);
-      for (int w = 0; w < 8; ++w) { a.x += red[w].x; a.y += red[w].y; }
-      d.cfo_a[i] = a;
-    }
-    __syncthreads();
+    const double sx = warp_sum_d((double)ax), sy = warp_sum_d((double)ay);
+    if (lane == 0) abuf[i] = make_double2(sx, sy);
   }
-}
-
-// rho = sum_i a_{i+1} conj(a_i); df = df_c + arg(rho) f_s2 / (2 pi 4 1024); DDS increment and
-// carried phase origin (c-8); z' becomes valid up to qhi.
-__global__ void __launch_bounds__(1024) k_cfo_fine_final(RxDev d, long long beta, long long qlo, long long qhi) {
-  __shared__ double2 red[32];
-  const long long nch = (qhi - qlo) / 1024;
+  // last CTA of this buffer: rho in index order -> fine df (stored in the coarse slot)
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) ticket = atomicAdd(&d.cfo_tick[blockIdx.y], 1);
+  __syncthreads();
+  if (ticket != cta_per_buf - 1) return;
+  __threadfence();
   double rx = 0.0, ry = 0.0;
-  for (long long i = threadIdx.x; i + 1 < nch; i += blockDim.x) {
-    const double2 a = d.cfo_a[i], b = d.cfo_a[i + 1];
-    rx += b.x * a.x + b.y * a.y;
-    ry += b.y * a.x - b.x * a.y;
+  for (long long k = threadIdx.x; k + 1 < nch; k += blockDim.x) {
+    volatile const double *vb = reinterpret_cast<volatile const double *>(abuf);
+    const double ax = vb[2 * k], ay = vb[2 * k + 1], bx = vb[2 * k + 2], by = vb[2 * k + 3];
+    rx += bx * ax + by * ay;
+    ry += by * ax - bx * ay;
   }
   rx = warp_sum_d(rx);
   ry = warp_sum_d(ry);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = make_double2(rx, ry);
+  __shared__ double2 red[8];
+  if (lane == 0) red[threadIdx.x >> 5] = make_double2(rx, ry);
   __syncthreads();
   if (threadIdx.x == 0) {
     double sx = 0.0, sy = 0.0;
-    for (int w = 0; w < 32; ++w) { sx += red[w].x; sy += red[w].y; }
-    CfoParam cp = d.cfo[rmod(beta, d.buf_cap)];
-    double df = cp.df;
-    if (nch >= 2) df += atan2(sy, sx) * d.fs2 / (2.0 * 3.141592653589793 * 4.0 * 1024.0);
+    for (int w = 0; w < 8; ++w) { sx += red[w].x; sy += red[w].y; }
+    if (nch >= 2) cpp->df = cpp->df + atan2(sy, sx) * d.fs2 / (2.0 * 3.141592653589793 * 4.0 * 1024.0);
+    d.cfo_tick[blockIdx.y] = 0;
+  }
+}
+
+// DDS increments and phase origins, carried across buffers (sequential, tiny)
+__global__ void k_cfo_carry(RxDev d, long long beta0, int nbuf) {
+  for (int i = 0; i < nbuf; ++i) {
+    CfoParam cp = d.cfo[rmod(beta0 + i, d.buf_cap)];
+    double df = cp.kstar >= 0 ? cp.df : d.st->cfo_df_prev;   // no complete chunk: reuse
     if (d.cfo_enable) {
       cp.df = df;
       cp.inc = (unsigned long long)llrint(ldexp(df / d.fs2, 64));
@@ -360,19 +388,30 @@ __global__ void __launch_bounds__(1024) k_cfo_fine_final(RxDev d, long long beta
     } else {
       cp.df = 0.0; cp.inc = 0ull; cp.origin = 0ull;
     }
-    d.cfo[rmod(beta, d.buf_cap)] = cp;
+    d.cfo[rmod(beta0 + i, d.buf_cap)] = cp;
   }
 }
 
 // z'_q = z_q / sqrt(P_beta) e^{-j psi'_q}, psi' the carried per-buffer CFO DDS (c-8),
-// materialised once per buffer into the z' ring that the sync / LMS stages read.
-__global__ void __launch_bounds__(256) k_kk_zprime(RxDev d, long long beta, long long qlo, long long qhi) {
-  const CfoParam cp = d.cfo[rmod(beta, d.buf_cap)];
-  if (blockIdx.x == 0 && threadIdx.x == 0) d.st->v_front = qhi;   // consumed by later launches
-  for (long long q = qlo + (long long)blockIdx.x * blockDim.x + threadIdx.x; q < qhi;
-       q += (long long)gridDim.x * blockDim.x) {
-    float2 zz = cscale(d.z[rmod(q, d.z_cap)], cp.inv_sqrtP);
-    if (d.cfo_enable) zz = cmul(zz, dds_rot_neg(cp.origin + (unsigned long long)(q - qlo) * cp.inc));
-    d.zp[rmod(q, d.zp_cap)] = zz;
+// materialised once into the z' ring that the sync / LMS stages read.
+__global__ void __launch_bounds__(256) k_kk_zprime(RxDev d, long long beta0, int nbuf, long long qfront) {
+  const long long Q = (long long)d.buffer_blocks * 256;
+  const long long q0 = beta0 * Q;
+  long long q1 = (beta0 + nbuf) * Q;
+  if (q1 > qfront) q1 = qfront;
+  if (blockIdx.x == 0 && threadIdx.x == 0) d.st->v_front = q1;   // consumed by later launches
+  for (long long q = q0 + 2 * ((long long)blockIdx.x * blockDim.x + threadIdx.x); q < q1;
+       q += 2 * (long long)gridDim.x * blockDim.x) {
+    const long long beta = q / Q;
+    const CfoParam &cp = d.cfo[rmod(beta, d.buf_cap)];
+    const float4 zz = *reinterpret_cast<const float4 *>(d.z + rmod(q, d.z_cap));
+    float2 a = cscale(make_float2(zz.x, zz.y), cp.inv_sqrtP), b = cscale(make_float2(zz.z, zz.w), cp.inv_sqrtP);
+    if (d.cfo_enable) {
+      const long long n = q - beta * Q;
+      a = cmul(a, dds_rot_neg(cp.origin + (unsigned long long)n * cp.inc));
+      b = cmul(b, dds_rot_neg(cp.origin + (unsigned long long)(n + 1) * cp.inc));
+    }
+    if (q + 1 < q1) *reinterpret_cast<float4 *>(d.zp + rmod(q, d.zp_cap)) = make_float4(a.x, a.y, b.x, b.y);
+    else d.zp[rmod(q, d.zp_cap)] = a;
   }
 }

@@ -413,10 +413,12 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
     d.zp_cap = next_pow2((long long)HB * c.buffer_blocks * 256 + 2 * batch_sym);
     TRY(dalloc(h, &d.zp, d.zp_cap));
     TRY(dalloc(h, &d.cfo, d.buf_cap));
-    d.cfo_G = 128;
-    TRY(dalloc(h, &d.cfo_part, (long long)d.cfo_G * 1024));
-    TRY(dalloc(h, &d.cfo_pow, d.cfo_G));
-    TRY(dalloc(h, &d.cfo_a, h->Q / 1024 + 1));
+    d.cfo_G = (int)(h->Q / 1024 / CFO_GROUPS + 1);      // spectrum rows per buffer
+    const long long maxbuf = HB;                           // buffers completing in one call
+    TRY(dalloc(h, &d.cfo_part, maxbuf * d.cfo_G * 1024));
+    TRY(dalloc(h, &d.cfo_pow, maxbuf * d.cfo_G));
+    TRY(dalloc(h, &d.cfo_tick, maxbuf));
+    TRY(dalloc(h, &d.cfo_a, maxbuf * (h->Q / 1024 + 1)));
   }
   TRY(dalloc(h, &d.sync_g, 2 * RX_PREF));
   TRY(dalloc(h, &d.sync_c, 2 * RX_PREF));
@@ -452,11 +454,11 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   if (cudaHostGetDevicePointer((void **)&d.hm, (void *)h->hm_host, 0) != cudaSuccess) { rx_destroy(h); return RX_ECUDA; }
   // kernels needing > 48 KB dynamic shared memory
   const size_t s2_smem = (1024 + 8 * FFT_PAD_N) * sizeof(float2);
-  const size_t cfo_smem = (1024 + 8 * FFT_PAD_N) * sizeof(float2) + 1024 * sizeof(float);
+  const size_t cfo_smem = (1024 + 2 * CFO_GROUPS * FFT_PAD_N) * sizeof(float2) + 1024 * sizeof(float);
   const size_t clk_smem = (CLK_TILE + 1 + 2 * c.clock_avg_half) * sizeof(double2);
   if (cudaFuncSetAttribute(k_pam_theta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)clk_smem) != cudaSuccess ||
       cudaFuncSetAttribute(k_kk_s2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2_smem) != cudaSuccess ||
-      cudaFuncSetAttribute(k_cfo_partial, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfo_smem) != cudaSuccess ||
+      cudaFuncSetAttribute(k_cfo_spec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfo_smem) != cudaSuccess ||
       cudaFuncSetAttribute(k_sync_corr<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536) != cudaSuccess ||
       cudaFuncSetAttribute(k_sync_corr<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536) != cudaSuccess) {
     rx_destroy(h);
@@ -647,17 +649,24 @@ static void run_kk(rx_handle *h, cudaStream_t s, const InView &in, unsigned char
   }
   const long long q_front = h->s2_done > 0 ? 256 * h->s2_done - 128 : 0;
   const long long Q = h->Q;
-  while ((h->cfo_done + 1) * Q <= q_front || (flush && h->cfo_done * Q < q_front)) {
-    const long long qlo = h->cfo_done * Q;
-    long long qhi = qlo + Q;
-    if (qhi > q_front) qhi = q_front;
-    const size_t smem = (1024 + 8 * FFT_PAD_N) * sizeof(float2) + 1024 * sizeof(float);
-    KLAUNCH(h, RX_K_CFO, s, (k_cfo_partial<<<(unsigned)d.cfo_G, 256, smem, s>>>(d, qlo, qhi)));
-    KLAUNCH(h, RX_K_CFO, s, (k_cfo_final<<<1, 1024, 0, s>>>(d, h->cfo_done, qlo, qhi)));
-    if (d.cfo_enable) KLAUNCH(h, RX_K_CFO, s, (k_cfo_fine<<<296, 256, 0, s>>>(d, h->cfo_done, qlo, qhi)));
-    KLAUNCH(h, RX_K_CFO, s, (k_cfo_fine_final<<<1, 1024, 0, s>>>(d, h->cfo_done, qlo, qhi)));
-    KLAUNCH(h, RX_K_CFO, s, (k_kk_zprime<<<gridc(qhi - qlo, 256) < 4096 ? gridc(qhi - qlo, 256) : 4096, 256, 0, s>>>(d, h->cfo_done, qlo, qhi)));
-    h->cfo_done++;
+  {
+    long long nbuf = 0;
+    while ((h->cfo_done + nbuf + 1) * Q <= q_front || (flush && (h->cfo_done + nbuf) * Q < q_front)) ++nbuf;
+    if (nbuf > 0) {
+      const long long beta0 = h->cfo_done;
+      const size_t smem = (1024 + 2 * CFO_GROUPS * FFT_PAD_N) * sizeof(float2) + 1024 * sizeof(float);
+      const int nrows = d.cfo_G;
+      const int fine_ctas = (int)((Q / 1024 + 7) / 8);
+      for (long long b0 = 0; b0 < nbuf; b0 += h->cfg.history_buffers) {
+        const long long nb = nbuf - b0 < h->cfg.history_buffers ? nbuf - b0 : h->cfg.history_buffers;
+        KLAUNCH(h, RX_K_CFO, s, (k_cfo_spec<<<dim3((unsigned)nrows, (unsigned)nb), 1024, smem, s>>>(d, beta0 + b0, q_front)));
+        KLAUNCH(h, RX_K_CFO, s, (k_cfo_final<<<(unsigned)nb, 1024, 0, s>>>(d, beta0 + b0, q_front, nrows)));
+        if (d.cfo_enable) KLAUNCH(h, RX_K_CFO, s, (k_cfo_fine<<<dim3((unsigned)fine_ctas, (unsigned)nb), 256, 0, s>>>(d, beta0 + b0, q_front, fine_ctas)));
+        KLAUNCH(h, RX_K_CFO, s, (k_cfo_carry<<<1, 1, 0, s>>>(d, beta0 + b0, (int)nb)));
+        KLAUNCH(h, RX_K_CFO, s, (k_kk_zprime<<<2048, 256, 0, s>>>(d, beta0 + b0, (int)nb, q_front)));
+      }
+      h->cfo_done += nbuf;
+    }
   }
   launch_sync_train<true>(h, s, flush);
   if (flush) KLAUNCH(h, RX_K_MISC, s, (k_kk_mend<<<1, 1, 0, s>>>(d, q_front)));
