@@ -274,7 +274,7 @@ def gpu_main(args):
     ring_samples = max(1, int(args.ring_gib * (1 << 30) / 2 // n_step)) * n_step
     ring = pam_ring(rec, ring_samples, dev, seed=seed)
     R = Receiver(RX_PAM, rec.M, rec.static_taps, device=local, history_buffers=CALL_BUFFERS + 2,
-                 lms_batch_segments=args.lms_batch, **rx_fields(rx))
+                 **({"lms_batch_segments": args.lms_batch} if args.lms_batch else {}), **rx_fields(rx))
     res = run_mode(torch, dist, R, ring, n_step, args.steps, args.warmup, world, dev, None)
     value = world * n_step * args.steps / (res["ms"] / 1e3) / 1e9
     ms_step = res["ms"] / args.steps
@@ -351,8 +351,8 @@ def gpu_main(args):
         rec4, rx4 = make_config("C4")
         ring4 = tiled_ring(rec4, max(1, int(args.ring_gib * (1 << 30) / 2 // N_C4)) * N_C4, dev)
         R4 = Receiver(RX_QAM_KK, rec4.M, rec4.static_taps, device=local, dc_offset=rec4.dc_offset,
-                      history_buffers=CALL_BUFFERS + 2, lms_batch_segments=args.lms_batch,
-                      **rx_fields(rx4))
+                      history_buffers=CALL_BUFFERS + 2,
+                      **({"lms_batch_segments": args.lms_batch} if args.lms_batch else {}), **rx_fields(rx4))
         r4 = run_mode(torch, None, R4, ring4, N_C4, args.kk_steps, 2, 1, dev, None)
         s4 = r4["stats"]
         v4 = N_C4 * args.kk_steps / (r4["ms"] / 1e3) / 1e9
@@ -418,8 +418,9 @@ def main():
     ap.add_argument("--kk-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ring-gib", type=float, default=1.0)
-    ap.add_argument("--lms-batch", type=int, default=4096,
-                    help="segments per equaliser launch (rx_config.lms_batch_segments)")
+    ap.add_argument("--lms-batch", type=int, default=0,
+                    help="segments per equaliser launch (rx_config.lms_batch_segments; 0 = library "
+                         "default: D epochs, i.e. 4096 PAM / 2048 KK)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

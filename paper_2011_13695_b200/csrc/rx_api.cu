@@ -153,7 +153,7 @@ extern "C" void rx_config_default(rx_config *c, int family, int order) {
   c->sync_window = 2048;
   c->sync_min_corr = 0.3;
   c->history_buffers = 3;
-  c->lms_batch_segments = 2048;
+  c->lms_batch_segments = family == RX_PAM ? 4096 : 2048;   // D epochs (one round each)
 }
 
 extern "C" const char *rx_strerror(int s) {
@@ -385,7 +385,11 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   TRY(dalloc(h, &d.hist, d.hist_cap));
   d.blk_cap = next_pow2((long long)HB * c.buffer_blocks + 256);
   d.buf_cap = 64;
-  const long long batch_sym = (long long)c.lms_batch_segments * c.lms_segment;
+  // equaliser batch + the seed-blocked tail that may wait for the next batch (<= D epochs)
+  const long long E_sym = (long long)c.buffer_blocks * (kk ? 128 : 256);
+  const long long tail_sym = (long long)c.tap_lag_epochs * E_sym;
+  const long long bsym = (long long)c.lms_batch_segments * c.lms_segment;
+  const long long batch_sym = bsym + (bsym > tail_sym ? tail_sym : bsym);
   d.sym_cap = next_pow2((long long)HB * c.buffer_blocks * (kk ? 128 : 260) + batch_sym);
   if (!kk) {
     TRY(dalloc(h, &d.C, d.blk_cap));
@@ -561,17 +565,21 @@ static void launch_lms_rounds(rx_handle *h, cudaStream_t s, unsigned char *label
   if (!flush) {
     const long long est_ready = seg_ub - h->lms_launched_upto;
     if (h->cfg.lms_batch_segments > 0 && est_ready < h->cfg.lms_batch_segments) return;
+    const long long prev_upto = h->lms_launched_upto;
     // grid: segments from the device's seg_next; pending ones are bounded by this batch plus
     // what could not run last time (data not yet normalised: at most one call of symbols)
     const long long call_segs = (h->max_call / h->sps) / S + 2;
-    long long nseg = seg_ub - h->lms_launched_upto + call_segs + 2;
+    const long long tail = (long long)d.D * (d.E_sym / S);
+    long long nseg = seg_ub - h->lms_launched_upto + call_segs + tail + 2;
     if (nseg > d.seg_cap / 2) nseg = d.seg_cap / 2;
     h->lms_launched_upto = seg_ub;
-    // a segment of epoch e needs the seed of epoch e - D: a batch spanning E epochs needs
-    // 1 + floor(E / D) rounds so nothing waits a whole batch (the rings hold one batch)
-    const long long spe = d.E_sym / S;
-    const long long span = (nseg + spe - 1) / spe + 1;
-    const long long rounds = 1 + span / d.D;
+    // a round can finish at most D epochs in a row (each segment needs the seed of epoch
+    // e - D): new segments beyond that need further rounds; a seed-blocked tail shorter than
+    // a round rides along with the next batch (the rings hold one batch + D epochs)
+    const long long per_round = (long long)d.D * (d.E_sym / S);
+    const long long fresh = seg_ub - prev_upto;
+    long long rounds = (fresh + per_round - 1) / per_round;
+    if (rounds < 1) rounds = 1;
     for (long long r = 0; r < rounds; ++r) launch_lms_round(h, s, labels, lab_cap, flush, nseg);
     return;
   }
