@@ -184,11 +184,11 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // zero outside [0, vend) (cp.async zero-fill)
 template <bool CPLX>
 __device__ __forceinline__ void lms_stage(const RxDev &d, LmsSmemT<CPLX> &sm, long long i0, long long i1,
-                                          long long vend) {
+                                          long long vend, long long base) {
   const int lane = threadIdx.x & 31;
   for (long long i = i0 + lane; i < i1; i += 32) {
     const bool ok = i >= 0 && i < vend;
-    const int slot = (int)(i & (LMS_RING - 1));
+    const int slot = (int)((i - base) & (LMS_RING - 1));   // block windows start 128 B aligned
     if constexpr (CPLX) {
       const float2 *src = ok ? d.zp + rmod(i, d.zp_cap) : d.zp;
       cp_async_elem(&sm.ring[slot], src, ok);
@@ -199,6 +199,30 @@ __device__ __forceinline__ void lms_stage(const RxDev &d, LmsSmemT<CPLX> &sm, lo
       cp_async_elem(&sm.ring[slot + LMS_RING], src, ok);
     }
   }
+}
+
+// 4 x 8 register tile of a 32 x 32 Toeplitz contraction (TILED path of lms_run): x4 -> 12
+// consecutive window samples X, v4 -> 8 coefficients V; FILTER: acc[a] = sum_b V[b] X[a + 7 - b]
+// (outputs a, taps b), else acc[a] = sum_b V[b] X[b + 3 - a] (taps a, outputs b)
+__device__ __forceinline__ void lms_tile(const float4 *x4, const float4 *v4, float acc[4], bool filter) {
+  const float4 xa = x4[0], xb = x4[1], xc = x4[2], va = v4[0], vb = v4[1];
+  const float X[12] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w, xc.x, xc.y, xc.z, xc.w};
+  const float V[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    float s = 0.f;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) s = fmaf(V[b], filter ? X[a + 7 - b] : X[b + 3 - a], s);
+    acc[a] = s;
+  }
+}
+// reduce-scatter of acc[0..3] over the four lane quarters q: returns sum_q' acc_q'[q]
+__device__ __forceinline__ float lms_tile_reduce(const float acc[4], int q) {
+  const bool h = q & 2, l = q & 1;
+  const float s0 = h ? acc[0] : acc[2], s1 = h ? acc[1] : acc[3];
+  const float k0 = (h ? acc[2] : acc[0]) + __shfl_xor_sync(0xffffffffu, s0, 16);
+  const float k1 = (h ? acc[3] : acc[1]) + __shfl_xor_sync(0xffffffffu, s1, 16);
+  return (l ? k1 : k0) + __shfl_xor_sync(0xffffffffu, l ? k0 : k1, 8);
 }
 
 __device__ __forceinline__ float2 as_c(float v) { return make_float2(v, 0.f); }
@@ -240,16 +264,26 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
     if (lane + 32 < d.Pt) rotB = __ldg(d.bps_rot + lane + 32);
   }
   float theta = 0.f;
+  // TILED (PAM, KP = 32): lane (q, r) = (lane >> 3, lane & 7) owns output / tap io = 4r + q and
+  // computes a 4 x 8 register tile of each contraction from 128-bit shared loads, reduced over q
+  // with two shuffle stages; otherwise lane i owns output i and tap i
+  constexpr bool TILED = !CPLX && KP == 32;
+  const int tq = lane >> 3, tr = lane & 7;
+  const int io = TILED ? 4 * tr + tq : lane;
   if (lane >= K) wk = make_float2(0.f, 0.f);
   if (CPLX) reinterpret_cast<float2 *>(sm.w)[lane] = wk;
   else reinterpret_cast<float *>(sm.w)[lane] = wk.x;
+  if (TILED) {
+    __syncwarp();
+    wk.x = reinterpret_cast<const float *>(sm.w)[io];
+  }
   const long long wb0 = (long long)stride * t_begin + off + c - (KP - 1);
   const long long nblk = (t_end - t_begin + 31) / 32;
-  lms_stage<CPLX>(d, sm, wb0, wb0 + WL, vend);
+  lms_stage<CPLX>(d, sm, wb0, wb0 + WL, vend, wb0);
   cp_async_commit();
 #pragma unroll 1
   for (int g = 1; g < LMS_AHEAD; ++g) {
-    if (g < nblk) lms_stage<CPLX>(d, sm, wb0 + WL + (long long)(g - 1) * DS, wb0 + WL + (long long)g * DS, vend);
+    if (g < nblk) lms_stage<CPLX>(d, sm, wb0 + WL + (long long)(g - 1) * DS, wb0 + WL + (long long)g * DS, vend, wb0);
     cp_async_commit();
   }
   bool first = true;
@@ -260,12 +294,20 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
     cp_async_wait<LMS_AHEAD - 1>();
     __syncwarp();
     const int nvalid = (int)((t_end - t) < 32 ? (t_end - t) : 32);
-    const bool valid = lane < nvalid;
-    const long long m = t + lane;
-    const T *win = sm.ring + (int)(wb & (LMS_RING - 1));   // contiguous window (mirror)
+    const bool valid = io < nvalid;
+    const long long m = t + io;
+    const T *win = sm.ring + (int)((wb - wb0) & (LMS_RING - 1));   // contiguous window (mirror)
     // y_i = w^H u_i, u_i[k] = win[stride i + KP-1-k]
     float2 y;
-    {
+    if constexpr (TILED) {
+      // y_i = sum_k w_k win[i + 31 - k]; lane: i = 4r + a, k = 8q + b -> win[4r + 24 - 8q + (a + 7 - b)]
+      const float *wf = reinterpret_cast<const float *>(win);
+      const float4 *x4 = reinterpret_cast<const float4 *>(wf + 4 * tr + 24 - 8 * tq);
+      const float4 *w4 = reinterpret_cast<const float4 *>(sm.w) + 2 * tq;
+      float acc[4];
+      lms_tile(x4, w4, acc, true);
+      y = make_float2(lms_tile_reduce(acc, tq), 0.f);
+    } else {
       const T *ub = win + stride * lane + KP - 1;
       float2 a[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       if (CPLX) {
@@ -375,10 +417,22 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
     }
     if (!valid) e = make_float2(0.f, 0.f);
     if (CPLX) reinterpret_cast<float2 *>(sm.e)[lane] = e;
-    else reinterpret_cast<float *>(sm.e)[lane] = e.x;
+    else reinterpret_cast<float *>(sm.e)[io] = e.x;
     __syncwarp();
     // gradient: lane k: g_k = sum_i u_i[k] conj(e_i); w <- w + mu g   (c-9 step 7)
-    {
+    if constexpr (TILED) {
+      // g_k = sum_i win[i + 31 - k] e_i; lane: k = 4r + a, i = 8q + b -> win[8q + 28 - 4r + (b + 3 - a)]
+      const float *wf = reinterpret_cast<const float *>(win);
+      const float4 *x4 = reinterpret_cast<const float4 *>(wf + 8 * tq + 28 - 4 * tr);
+      const float4 *e4 = reinterpret_cast<const float4 *>(sm.e) + 2 * tq;
+      float acc[4];
+      lms_tile(x4, e4, acc, false);
+      const float g = lms_tile_reduce(acc, tq);
+      if (io < K) {
+        wk.x = fmaf(mu, g, wk.x);
+        if (fabsf(wk.x) > 1e3f) set_flag(d.st, RX_FLAG_DIVERGE);
+      }
+    } else {
       const T *ug = win + KP - 1 - (lane < KP ? lane : 0);     // lanes >= KP: discarded
       float2 g[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       if (CPLX) {
@@ -414,16 +468,17 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
       }
     }
     if (CPLX) reinterpret_cast<float2 *>(sm.w)[lane] = wk;
-    else reinterpret_cast<float *>(sm.w)[lane] = wk.x;
+    else reinterpret_cast<float *>(sm.w)[io] = wk.x;
     __syncwarp();
     // stage the new samples of block jb + AHEAD (the slots of block jb are no longer read)
     const long long jn = jb + LMS_AHEAD;
-    if (jn < nblk) lms_stage<CPLX>(d, sm, wb0 + WL + (jn - 1) * DS, wb0 + WL + jn * DS, vend);
+    if (jn < nblk) lms_stage<CPLX>(d, sm, wb0 + WL + (jn - 1) * DS, wb0 + WL + jn * DS, vend, wb0);
     cp_async_commit();
     wb += DS;
     first = false;
   }
   cp_async_wait<0>();
+  if (TILED) wk.x = reinterpret_cast<const float *>(sm.w)[lane];   // back to lane = tap order
   const float nrm = warp_sum(lane < K ? cabs2(wk) : 0.f);
   if (lane == 0 && nrm > 1e6f) set_flag(d.st, RX_FLAG_DIVERGE);
   return theta;
