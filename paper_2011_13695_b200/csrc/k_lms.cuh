@@ -225,6 +225,31 @@ __device__ __forceinline__ float lms_tile_reduce(const float acc[4], int q) {
   return (l ? k1 : k0) + __shfl_xor_sync(0xffffffffu, l ? k0 : k1, 8);
 }
 
+// PAM fast staging: 16-byte cp.async of 4 consecutive u^ (needs i0 = 0 mod 4, (i1 - i0) = 0 mod 4;
+// a chunk never straddles index 0 or the ring wrap); zero-fill beyond vend / below 0
+__device__ __forceinline__ void lms_stage_vec(const RxDev &d, LmsSmemT<false> &sm, long long i0, long long i1,
+                                              long long vend, long long base) {
+  const int lane = threadIdx.x & 31;
+  for (long long i = i0 + 4 * lane; i < i1; i += 128) {
+    long long nv = vend - i;
+    nv = i < 0 ? 0 : (nv < 0 ? 0 : (nv > 4 ? 4 : nv));
+    const int slot = (int)((i - base) & (LMS_RING - 1));
+    const float *src = nv ? d.uhat + rmod(i, d.sym_cap) : d.uhat;
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(&sm.ring[slot]);
+    const unsigned sb = (unsigned)__cvta_generic_to_shared(&sm.ring[slot + LMS_RING]);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(src), "r"((int)(4 * nv)));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sb), "l"(src), "r"((int)(4 * nv)));
+  }
+}
+template <bool CPLX>
+__device__ __forceinline__ void lms_stage_any(const RxDev &d, LmsSmemT<CPLX> &sm, long long i0, long long i1,
+                                              long long vend, long long base, bool vec) {
+  if constexpr (!CPLX) {
+    if (vec) { lms_stage_vec(d, sm, i0, i1, vend, base); return; }
+  }
+  lms_stage<CPLX>(d, sm, i0, i1, vend, base);
+}
+
 __device__ __forceinline__ float2 as_c(float v) { return make_float2(v, 0.f); }
 __device__ __forceinline__ float2 as_c(float2 v) { return v; }
 
@@ -279,11 +304,13 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
   }
   const long long wb0 = (long long)stride * t_begin + off + c - (KP - 1);
   const long long nblk = (t_end - t_begin + 31) / 32;
-  lms_stage<CPLX>(d, sm, wb0, wb0 + WL, vend, wb0);
+  constexpr int WLa = (WL + 3) & ~3;        // first stage rounded up: later stages stay 4-aligned
+  const bool vec = !CPLX && (wb0 & 3) == 0;
+  lms_stage_any<CPLX>(d, sm, wb0, wb0 + WLa, vend, wb0, vec);
   cp_async_commit();
 #pragma unroll 1
   for (int g = 1; g < LMS_AHEAD; ++g) {
-    if (g < nblk) lms_stage<CPLX>(d, sm, wb0 + WL + (long long)(g - 1) * DS, wb0 + WL + (long long)g * DS, vend, wb0);
+    if (g < nblk) lms_stage_any<CPLX>(d, sm, wb0 + WLa + (long long)(g - 1) * DS, wb0 + WLa + (long long)g * DS, vend, wb0, vec);
     cp_async_commit();
   }
   bool first = true;
@@ -472,10 +499,11 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
     __syncwarp();
     // stage the new samples of block jb + AHEAD (the slots of block jb are no longer read)
     const long long jn = jb + LMS_AHEAD;
-    if (jn < nblk) lms_stage<CPLX>(d, sm, wb0 + WL + (jn - 1) * DS, wb0 + WL + jn * DS, vend, wb0);
+    if (jn < nblk) lms_stage_any<CPLX>(d, sm, wb0 + WLa + (jn - 1) * DS, wb0 + WLa + jn * DS, vend, wb0, vec);
     cp_async_commit();
     wb += DS;
     first = false;
+
   }
   cp_async_wait<0>();
   if (TILED) wk.x = reinterpret_cast<const float *>(sm.w)[lane];   // back to lane = tap order
@@ -503,10 +531,64 @@ __global__ void __launch_bounds__(32) k_lms_train(RxDev d, int flush) {
   if (lane == 0) { st->trained = 1; d.hm->trained = 1; }
 }
 
+// PAM labels and bit errors of output symbols [lo, hi) from the level ring (written by this warp)
+__device__ __forceinline__ void pam_finalise(const RxDev &d, long long lo, long long hi, unsigned char *labels,
+                                             long long lab_cap, int &err, int &cnt) {
+  const int lane = threadIdx.x & 31;
+  const DevState *st = d.st;
+  const int r0 = (int)(((st->sync_offset + lo - d.m0) % RX_PREF + RX_PREF) % RX_PREF);
+  const bool vec = labels && (((unsigned long long)labels | (unsigned long long)lab_cap | (unsigned long long)lo) & 15) == 0;
+  const long long n = hi - lo;
+  for (long long v = 16LL * lane; v < n; v += 512) {
+    const long long m0v = lo + v;
+    const int nv = n - v < 16 ? (int)(n - v) : 16;
+    unsigned char code[16];
+    if (nv == 16 && (m0v & 15) == 0) {
+      const uint4 q = *reinterpret_cast<const uint4 *>(d.level + rmod(m0v, d.sym_cap));
+      const unsigned w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int j = 0; j < 16; ++j) code[j] = (unsigned char)(w[j >> 2] >> (8 * (j & 3)));
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) code[j] = j < nv ? d.level[rmod(m0v + j, d.sym_cap)] : 0;
+    }
+    unsigned char lab[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) lab[j] = (unsigned char)(code[j] ^ (code[j] >> 1));
+    if (labels) {
+      const long long li0 = m0v % lab_cap;
+      if (vec && nv == 16) {
+        unsigned w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int j = 0; j < 16; ++j) w[j >> 2] |= (unsigned)lab[j] << (8 * (j & 3));
+        *reinterpret_cast<uint4 *>(labels + li0) = make_uint4(w[0], w[1], w[2], w[3]);
+      } else {
+        long long li = li0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          if (j < nv) labels[li] = lab[j];
+          if (++li == lab_cap) li = 0;
+        }
+      }
+    }
+    int ri = r0 + (int)(v % RX_PREF);
+    if (ri >= RX_PREF) ri -= RX_PREF;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (j < nv && m0v + j >= d.warmup) {
+        err += __popc((int)lab[j] ^ (int)__ldg(d.ref_lab + ri));
+        ++cnt;
+      }
+      if (++ri == RX_PREF) ri = 0;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ segments (1 warp each)
 // Segment s outputs [sS, min((s+1)S, m_end)), recursion starts O symbols early (c-9).
 template <bool CPLX, int CPR, int KP>
-__global__ void __launch_bounds__(128) k_lms_seg(RxDev d, int flush, int nseg) {
+__global__ void __launch_bounds__(128) k_lms_seg(RxDev d, int flush, int nseg, unsigned char *labels,
+                                                 long long lab_cap) {
   __shared__ LmsSmemT<CPLX> sm[4];
   DevState *st = d.st;
   if (!st->trained) return;
@@ -543,6 +625,16 @@ __global__ void __launch_bounds__(128) k_lms_seg(RxDev d, int flush, int nseg) {
   ed = warp_sum_d(ed);
   const long long si = rmod(s, d.seg_cap);
   if (lane < K) d.seg_w[si * RX_MAX_K + lane] = wk;
+  if (!CPLX) {
+    // PAM finalises its own symbols (R_s = 0): Gray labels + reference comparison (H10/H25)
+    // over the segment's level codes, 16 per lane-step, off the serial recursion
+    __syncwarp();
+    int er = 0, ct = 0;
+    pam_finalise(d, lo, hi, labels, lab_cap, er, ct);
+    er = __reduce_add_sync(0xffffffffu, (unsigned)er);
+    ct = __reduce_add_sync(0xffffffffu, (unsigned)ct);
+    if (lane == 0) { d.seg_err[2 * si] = er; d.seg_err[2 * si + 1] = ct; }
+  }
   if (lane == 0) {
     d.seg_theta[si] = th;
     d.seg_evm[2 * si] = en;
@@ -589,12 +681,49 @@ __global__ void __launch_bounds__(256) k_lms_stitch(RxDev d, int nseg) {
   }
 }
 
+// Counters in fixed order (one CTA of 1024 threads) over finalised segments [lo, hi)
+__device__ __forceinline__ void lms_add_counters(const RxDev &d, long long lo, long long hi) {
+  __shared__ double sh[32], sh2[32];
+  __shared__ long long shl[32], shl2[32];
+  DevState *st = d.st;
+  const int t = threadIdx.x;
+  double en = 0.0, ed = 0.0;
+  long long er = 0, ct = 0;
+  for (long long s = lo + t; s < hi; s += blockDim.x) {
+    const long long si = rmod(s, d.seg_cap);
+    en += d.seg_evm[2 * si];
+    ed += d.seg_evm[2 * si + 1];
+    er += d.seg_err[2 * si];
+    ct += d.seg_err[2 * si + 1];
+  }
+  en = warp_sum_d(en);
+  ed = warp_sum_d(ed);
+  for (int o = 16; o > 0; o >>= 1) {
+    er += __shfl_xor_sync(0xffffffffu, er, o);
+    ct += __shfl_xor_sync(0xffffffffu, ct, o);
+  }
+  if ((t & 31) == 0) { sh[t >> 5] = en; sh2[t >> 5] = ed; shl[t >> 5] = er; shl2[t >> 5] = ct; }
+  __syncthreads();
+  if (t == 0) {
+    double a = 0.0, b = 0.0;
+    long long x = 0, y = 0;
+    for (int w = 0; w < 32; ++w) { a += sh[w]; b += sh2[w]; x += shl[w]; y += shl2[w]; }
+    st->evm_num += a;
+    st->evm_den += b;
+    st->bit_errors += x;
+    st->symbols_counted += y;
+    st->bits += y * d.kbits;
+    long long so = hi * (long long)d.S;
+    if (st->m_end >= 0 && so > st->m_end) so = st->m_end;
+    if (hi > lo) st->symbols_out = so;
+  }
+}
+
 // ------------------------------------------------------------------ R_s prefix + anchor
 // R_s = (A + sum_{i<=s} r_i) mod 4 with A fixed by anchoring the segment containing m0 to
 // the known reference over [m0, m0 + 256) (c-9 'Stitching').
 __global__ void __launch_bounds__(1024) k_lms_prefix(RxDev d, int flush, int maxn) {
   __shared__ int firstbad;
-  __shared__ int pre[1024];
   __shared__ int acnt[4];
   DevState *st = d.st;
   const long long base = st->seg_next;
@@ -602,9 +731,10 @@ __global__ void __launch_bounds__(1024) k_lms_prefix(RxDev d, int flush, int max
   if (t == 0) firstbad = maxn;
   if (t < 4) acnt[t] = 0;
   __syncthreads();
+  const int *ready = d.family == 1 ? d.seg_stitched : d.seg_done;   // PAM: no stitching (R_s = 0)
   for (int i = t; i < maxn; i += blockDim.x) {
     const long long s = base + i;
-    if (d.seg_stitched[rmod(s, d.seg_cap)] != s + 1) atomicMin(&firstbad, i);
+    if (ready[rmod(s, d.seg_cap)] != s + 1) atomicMin(&firstbad, i);
   }
   __syncthreads();
   int n = firstbad;
@@ -651,24 +781,41 @@ __global__ void __launch_bounds__(1024) k_lms_prefix(RxDev d, int flush, int max
   }
   __syncthreads();
   if (!known_sh) n = 0;
-  // prefix of r over [base, base + n) in chunks of 1024
+  // prefix of r over [base, base + n) in chunks of 1024 (QAM; PAM has R_s = 0): warp shuffle
+  // scans + one scan of the 32 warp totals
   int carry = (int)(st->r_prefix & 3);
-  for (int c0 = 0; c0 < n; c0 += 1024) {
-    const long long s = base + c0 + t;
-    int r = 0;
-    if (c0 + t < n && s > 0) r = d.seg_r[rmod(s, d.seg_cap)];
-    pre[t] = r;
-    __syncthreads();
-    for (int off = 1; off < 1024; off <<= 1) {
-      const int o = (t >= off) ? pre[t - off] : 0;
+  if (d.family == 1) {
+    __shared__ int wsum[32];
+    const int lane = t & 31, warp = t >> 5;
+    for (int c0 = 0; c0 < n; c0 += 1024) {
+      const long long s = base + c0 + t;
+      int x = 0;
+      if (c0 + t < n && s > 0) x = d.seg_r[rmod(s, d.seg_cap)];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) wsum[warp] = x;
       __syncthreads();
-      pre[t] += o;
+      if (warp == 0) {
+        int v = wsum[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, v, o);
+          if (lane >= o) v += y;
+        }
+        wsum[lane] = v;
+      }
       __syncthreads();
+      const int incl = x + (warp > 0 ? wsum[warp - 1] : 0);
+      if (c0 + t < n) d.seg_R[rmod(s, d.seg_cap)] = (A_sh + carry + incl) & 3;
+      const int tot = wsum[31];
+      __syncthreads();
+      carry = (carry + tot) & 3;
     }
-    if (c0 + t < n) d.seg_R[rmod(s, d.seg_cap)] = (A_sh + carry + pre[t]) & 3;
-    const int tot = pre[1023];
-    __syncthreads();
-    carry = (carry + tot) & 3;
+  } else {
+    lms_add_counters(d, base, base + n);   // PAM: the segments counted their own errors
   }
   if (t == 0) {
     st->anchor_known = known_sh;
@@ -753,43 +900,8 @@ __global__ void __launch_bounds__(256) k_lms_final(RxDev d, unsigned char *label
   }
 }
 
-// Counters in fixed order (one CTA) ...
 __global__ void __launch_bounds__(1024) k_lms_counters(RxDev d) {
-  __shared__ double sh[32], sh2[32];
-  __shared__ long long shl[32], shl2[32];
-  DevState *st = d.st;
-  const long long lo = st->fin_lo, hi = st->fin_hi;
-  const int t = threadIdx.x;
-  double en = 0.0, ed = 0.0;
-  long long er = 0, ct = 0;
-  for (long long s = lo + t; s < hi; s += blockDim.x) {
-    const long long si = rmod(s, d.seg_cap);
-    en += d.seg_evm[2 * si];
-    ed += d.seg_evm[2 * si + 1];
-    er += d.seg_err[2 * si];
-    ct += d.seg_err[2 * si + 1];
-  }
-  en = warp_sum_d(en);
-  ed = warp_sum_d(ed);
-  for (int o = 16; o > 0; o >>= 1) {
-    er += __shfl_xor_sync(0xffffffffu, er, o);
-    ct += __shfl_xor_sync(0xffffffffu, ct, o);
-  }
-  if ((t & 31) == 0) { sh[t >> 5] = en; sh2[t >> 5] = ed; shl[t >> 5] = er; shl2[t >> 5] = ct; }
-  __syncthreads();
-  if (t == 0) {
-    double a = 0.0, b = 0.0;
-    long long x = 0, y = 0;
-    for (int w = 0; w < 32; ++w) { a += sh[w]; b += sh2[w]; x += shl[w]; y += shl2[w]; }
-    st->evm_num += a;
-    st->evm_den += b;
-    st->bit_errors += x;
-    st->symbols_counted += y;
-    st->bits += y * d.kbits;
-    long long so = hi * (long long)d.S;
-    if (st->m_end >= 0 && so > st->m_end) so = st->m_end;
-    if (hi > lo) st->symbols_out = so;
-  }
+  lms_add_counters(d, d.st->fin_lo, d.st->fin_hi);
 }
 
 // ... and the lag-D epoch seeds: CTA i owns epoch fin_lo/spe + i; when all its segments are

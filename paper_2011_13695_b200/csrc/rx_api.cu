@@ -72,6 +72,7 @@ struct rx_handle {
   long long Q;   // 2-sps samples per buffer (KK)
   long long hist_cap;
   long long lms_launched_upto;   // segment estimate at the last equaliser launch
+  long long lms_fin_est;         // host estimate of the finalised segment frontier (streaming)
   long long max_call;            // samples per rx_process call: (history_buffers - 2) buffers
   // tracing
   int prof_mask;
@@ -441,7 +442,8 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   TRY(dalloc(h, &d.seg_err, 2 * d.seg_cap));
   if (c.lms_overlap > 0) TRY(dalloc(h, &d.seg_warm, d.seg_cap * c.lms_overlap));
   TRY(dalloc(h, &d.level, d.sym_cap));
-  TRY(dalloc(h, &d.level_fin, d.sym_cap));
+  if (kk) TRY(dalloc(h, &d.level_fin, d.sym_cap));
+  else d.level_fin = d.level;            // PAM: R_s = 0, the segment frame is final
   TRY(dalloc(h, &d.yout, d.sym_cap));
   // ---- state
   TRY(dalloc(h, &h->st_dev, 1));
@@ -502,7 +504,7 @@ static rx_status check_launch() {
 static unsigned gridc(long long n, int per) { return (unsigned)((n + per - 1) / per); }
 
 // tap padding KP in {4, 8, 16, 32} (compile-time) and the CPR flavour select the instance
-typedef void (*lms_seg_fn)(RxDev, int, int);
+typedef void (*lms_seg_fn)(RxDev, int, int, unsigned char *, long long);
 typedef void (*lms_train_fn)(RxDev, int);
 static int kp_of(int K) { return K <= 4 ? 4 : (K <= 8 ? 8 : (K <= 16 ? 16 : 32)); }
 template <bool CPLX, int CPR>
@@ -545,11 +547,16 @@ static void launch_lms_round(rx_handle *h, cudaStream_t s, unsigned char *labels
                              int flush, long long nseg) {
   RxDev &d = h->d;
   const long long S = d.S;
-  KLAUNCH(h, RX_K_LMS, s, (lms_seg_kernel(d)<<<gridc(nseg, 4), 128, 0, s>>>(d, flush, (int)nseg)));
-  KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_stitch<<<(unsigned)nseg, 256, 0, s>>>(d, (int)nseg)));
-  KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_prefix<<<1, 1024, 0, s>>>(d, flush, (int)nseg)));
-  KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_final<<<(unsigned)nseg, 256, 0, s>>>(d, labels, lab_cap, (int)nseg)));
-  KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_counters<<<1, 1024, 0, s>>>(d)));
+  KLAUNCH(h, RX_K_LMS, s, (lms_seg_kernel(d)<<<gridc(nseg, 4), 128, 0, s>>>(d, flush, (int)nseg, labels, lab_cap)));
+  if (d.family == RX_PAM) {
+    // PAM segments wrote their labels and error counts; the prefix also adds the counters
+    KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_prefix<<<1, 1024, 0, s>>>(d, flush, (int)nseg)));
+  } else {
+    KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_stitch<<<(unsigned)nseg, 256, 0, s>>>(d, (int)nseg)));
+    KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_prefix<<<1, 1024, 0, s>>>(d, flush, (int)nseg)));
+    KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_final<<<(unsigned)nseg, 256, 0, s>>>(d, labels, lab_cap, (int)nseg)));
+    KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_counters<<<1, 1024, 0, s>>>(d)));
+  }
   KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_seeds<<<(unsigned)(nseg * S / d.E_sym + 2), 1024, 0, s>>>(d, flush)));
 }
 
@@ -576,11 +583,20 @@ static void launch_lms_rounds(rx_handle *h, cudaStream_t s, unsigned char *label
     // a round can finish at most D epochs in a row (each segment needs the seed of epoch
     // e - D): new segments beyond that need further rounds; a seed-blocked tail shorter than
     // a round rides along with the next batch (the rings hold one batch + D epochs)
+    // Every round costs a full segment recursion however few segments it runs, so a short
+    // remainder (e.g. the first segment of epoch e + D, whose seed this same round produces)
+    // waits for the next batch; the host tracks an estimate of the finalised frontier and runs
+    // a second round only when at least half a round more is pending. The backlog stays below
+    // one batch + D epochs, which the rings hold (rx_create).
+    (void)prev_upto;
     const long long per_round = (long long)d.D * (d.E_sym / S);
-    const long long fresh = seg_ub - prev_upto;
-    long long rounds = (fresh + per_round - 1) / per_round;
+    if (h->lms_fin_est < seg_ub - 2 * per_round - call_segs) h->lms_fin_est = seg_ub - 2 * per_round - call_segs;
+    const long long backlog = seg_ub - h->lms_fin_est;
+    long long rounds = (backlog + per_round / 2) / per_round;
     if (rounds < 1) rounds = 1;
     for (long long r = 0; r < rounds; ++r) launch_lms_round(h, s, labels, lab_cap, flush, nseg);
+    h->lms_fin_est += rounds * per_round;
+    if (h->lms_fin_est > seg_ub) h->lms_fin_est = seg_ub;
     return;
   }
   long long prev = -1;
