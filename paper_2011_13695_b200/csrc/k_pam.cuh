@@ -430,7 +430,6 @@ __device__ __forceinline__ long long sym_lo_of(const RxDev &d, long long b) {
 #define NORM_G 64
 __global__ void __launch_bounds__(1024) k_norm_stats(RxDev d, long long beta0, long long be_done, int flush) {
   __shared__ double sh[32];
-  __shared__ double bc[2];
   __shared__ int ticket;
   const int g = blockIdx.x, t = threadIdx.x;
   const long long beta = beta0 + blockIdx.y;
@@ -449,7 +448,20 @@ __global__ void __launch_bounds__(1024) k_norm_stats(RxDev d, long long beta0, l
   const long long n = mhi - mlo;
   const long long m0 = mlo + n * g / NORM_G, m1 = mlo + n * (g + 1) / NORM_G;
   double a = 0.0;
-  for (long long m = m0 + t; m < m1; m += blockDim.x) a += fabs((double)d.u[rmod(m, d.sym_cap)] - dc);
+  {
+    const long long a0 = (m0 + 3) & ~3LL, a1 = m1 & ~3LL;
+    const long long h1 = a0 < m1 ? a0 : m1;
+    if (m0 + t < h1) a += fabs((double)d.u[rmod(m0 + t, d.sym_cap)] - dc);
+    const long long tl = a1 > h1 ? a1 : h1;
+    if (tl + t < m1) a += fabs((double)d.u[rmod(tl + t, d.sym_cap)] - dc);
+    double a2 = 0.0;
+    for (long long q = a0 / 4 + t; q < a1 / 4; q += blockDim.x) {
+      const float4 x = *reinterpret_cast<const float4 *>(d.u + rmod(4 * q, d.sym_cap));
+      a += fabs((double)x.x - dc) + fabs((double)x.y - dc);
+      a2 += fabs((double)x.z - dc) + fabs((double)x.w - dc);
+    }
+    a += a2;
+  }
   a = block_sum_det(a, sh);
   double *part = d.norm_part + (blockIdx.y % 16) * NORM_G;
   if (t == 0) {
@@ -477,36 +489,40 @@ __global__ void __launch_bounds__(1024) k_norm_stats(RxDev d, long long beta0, l
   (void)flush;
 }
 
-// u^ over the symbols of buffers [beta0, beta0 + nbuf); advances the front (and m_end at flush)
+// u^ over the symbols of buffers [beta0, beta0 + nbuf): grid (NORM_AG, nbuf), CTA (g, y) scales
+// its share of buffer beta0 + y with that buffer's (dc, 1/A), 4 symbols per thread-step (float4
+// where the absolute index is 4-aligned); advances the front (and m_end at flush)
+#define NORM_AG 128
 __global__ void __launch_bounds__(256) k_norm_apply(RxDev d, long long beta0, long long nbuf, long long be_done,
                                                    int flush) {
-  const long long blo = beta0 * d.buffer_blocks;
-  long long bhi = (beta0 + nbuf) * d.buffer_blocks;
+  const long long beta = beta0 + blockIdx.y;
+  const long long blo = beta * d.buffer_blocks;
+  long long bhi = blo + d.buffer_blocks;
   if (bhi > be_done) bhi = be_done;
   const long long mlo = sym_lo_of(d, blo);
   const long long mhi = sym_lo_of(d, bhi) > mlo ? sym_lo_of(d, bhi) : mlo;
-  // buffer boundaries (symbol index of each buffer's first symbol)
-  __shared__ long long mb[17];
-  __shared__ float dcs[16], invs[16];
-  if (threadIdx.x <= nbuf && threadIdx.x < 17) {
-    long long bb = (beta0 + threadIdx.x) * d.buffer_blocks;
-    if (bb > be_done) bb = be_done;
-    mb[threadIdx.x] = sym_lo_of(d, bb);
+  const float dc = (float)d.norm_dc[rmod(beta, d.buf_cap)];
+  const float inv = (float)(1.0 / d.norm_amp[rmod(beta, d.buf_cap)]);
+  const long long a0 = (mlo + 3) & ~3LL, a1 = mhi & ~3LL;
+  const int t = threadIdx.x;
+  if (blockIdx.x == 0) {   // unaligned head / tail
+    const long long h1 = a0 < mhi ? a0 : mhi;
+    if (mlo + t < h1) { const long long i = rmod(mlo + t, d.sym_cap); d.uhat[i] = (d.u[i] - dc) * inv; }
+    const long long tl = a1 > h1 ? a1 : h1;
+    if (tl + t < mhi) { const long long i = rmod(tl + t, d.sym_cap); d.uhat[i] = (d.u[i] - dc) * inv; }
   }
-  if (threadIdx.x < nbuf && threadIdx.x < 16) {
-    dcs[threadIdx.x] = (float)d.norm_dc[rmod(beta0 + threadIdx.x, d.buf_cap)];
-    invs[threadIdx.x] = (float)(1.0 / d.norm_amp[rmod(beta0 + threadIdx.x, d.buf_cap)]);
+  for (long long q = a0 / 4 + (long long)blockIdx.x * blockDim.x + t; q < a1 / 4;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long i = rmod(4 * q, d.sym_cap);
+    const float4 x = *reinterpret_cast<const float4 *>(d.u + i);
+    *reinterpret_cast<float4 *>(d.uhat + i) =
+        make_float4((x.x - dc) * inv, (x.y - dc) * inv, (x.z - dc) * inv, (x.w - dc) * inv);
   }
-  __syncthreads();
-  for (long long m = mlo + (long long)blockIdx.x * blockDim.x + threadIdx.x; m < mhi;
-       m += (long long)gridDim.x * blockDim.x) {
-    int bi = 0;
-    while (bi + 1 < nbuf && m >= mb[bi + 1]) ++bi;
-    const long long i = rmod(m, d.sym_cap);
-    d.uhat[i] = (d.u[i] - dcs[bi]) * invs[bi];
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    d.st->v_front = mhi;
-    if (flush && bhi == be_done) d.st->m_end = mhi;
+  if (blockIdx.x == 0 && blockIdx.y == 0 && t == 0) {
+    long long bend = (beta0 + nbuf) * d.buffer_blocks;
+    if (bend > be_done) bend = be_done;
+    const long long mend = sym_lo_of(d, bend) > mlo ? sym_lo_of(d, bend) : mlo;
+    d.st->v_front = mend;
+    if (flush && bend == be_done) d.st->m_end = mend;
   }
 }

@@ -73,6 +73,7 @@ struct rx_handle {
   long long hist_cap;
   long long lms_launched_upto;   // segment estimate at the last equaliser launch
   long long lms_fin_est;         // host estimate of the finalised segment frontier (streaming)
+  int n_sm;                      // SM count (persistent grids)
   long long max_call;            // samples per rx_process call: (history_buffers - 2) buffers
   // tracing
   int prof_mask;
@@ -253,6 +254,7 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   h->cfg.static_taps = nullptr;
   h->cfg.thresholds = nullptr;
   h->device = cuda_device;
+  cudaDeviceGetAttribute(&h->n_sm, cudaDevAttrMultiProcessorCount, cuda_device);
   const rx_config &c = *cfg;
   RxDev &d = h->d;
   memset(&d, 0, sizeof(d));
@@ -502,6 +504,11 @@ static rx_status check_launch() {
 }
 
 static unsigned gridc(long long n, int per) { return (unsigned)((n + per - 1) / per); }
+// persistent grid: one wave (SMs x resident CTAs), never more CTAs than work groups
+static unsigned pgrid(const rx_handle *h, long long n, int per, int occ) {
+  const long long g = (n + per - 1) / per, cap = (long long)h->n_sm * (occ > 0 ? occ : 1);
+  return (unsigned)(g < cap ? g : cap);
+}
 
 // tap padding KP in {4, 8, 16, 32} (compile-time) and the CPR flavour select the instance
 typedef void (*lms_seg_fn)(RxDev, int, int, unsigned char *, long long);
@@ -647,7 +654,7 @@ static void run_pam(rx_handle *h, cudaStream_t s, const InView &in, unsigned cha
       for (long long b0 = 0; b0 < nbuf; b0 += 16) {
         const long long nb = nbuf - b0 < 16 ? nbuf - b0 : 16;
         KLAUNCH(h, RX_K_NORM, s, (k_norm_stats<<<dim3(NORM_G, (unsigned)nb), 1024, 0, s>>>(d, beta0 + b0, bend, flush)));
-        KLAUNCH(h, RX_K_NORM, s, (k_norm_apply<<<1184, 256, 0, s>>>(d, beta0 + b0, nb, bend, flush)));
+        KLAUNCH(h, RX_K_NORM, s, (k_norm_apply<<<dim3(NORM_AG, (unsigned)nb), 256, 0, s>>>(d, beta0 + b0, nb, bend, flush)));
       }
       h->norm_done += nbuf;
     }
