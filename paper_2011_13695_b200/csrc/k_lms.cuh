@@ -165,7 +165,7 @@ struct LmsSmemT {
   alignas(16) T ring[2 * LMS_RING];
   alignas(16) T w[32];
   alignas(16) T e[32];
-  float2 y[32];
+  alignas(16) float2 y[32];
 };
 
 __device__ __forceinline__ void cp_async_elem(float *dst, const float *src, bool valid) {
@@ -381,27 +381,41 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
           const float sx = warp_sum(y4.x), sy = warp_sum(y4.y);
           th_hat = 0.25f * atan2f(-sy, -sx);
         } else {           // blind phase search: lane p scores test phases p and p + 32
+          // distance in units of the level spacing 2s: u = y e^{-j phi_p} / 2s + (L - 1)/2 puts
+          // the levels on the integers 0..L-1, so |z - slice(z)|^2 = (2s)^2 sum (u - clamp(rint u))^2
+          // (the common factor (2s)^2 does not move the argmin)
           sm.y[lane] = y;
           __syncwarp();
-          float dA = 0.f, dB = 0.f;
-          const float Lh = 0.5f * (float)L, Lm1 = (float)(L - 1);
-          for (int i = 0; i < nvalid; ++i) {
-            const float2 yi = sm.y[i];
-            {
-              const float2 zr = cmul(yi, rotA);
-              const float fi = fminf(fmaxf(floorf(fmaf(zr.x, inv2s, Lh)), 0.f), Lm1);
-              const float fq = fminf(fmaxf(floorf(fmaf(zr.y, inv2s, Lh)), 0.f), Lm1);
-              const float dx = zr.x - fmaf(fi, two_s, lvl0), dy = zr.y - fmaf(fq, two_s, lvl0);
-              dA += fmaf(dx, dx, dy * dy);
-            }
+          const float cst = 0.5f * (float)(L - 1), Lm1 = (float)(L - 1);
+          const float2 rsA = make_float2(rotA.x * inv2s, rotA.y * inv2s);
+          const float2 rsB = make_float2(rotB.x * inv2s, rotB.y * inv2s);
+          float dA = 0.f, dA2 = 0.f, dB = 0.f, dB2 = 0.f;
+          auto bdist = [&](float2 yi, float2 r) -> float {
+            const float ux = fmaf(yi.x, r.x, fmaf(-yi.y, r.y, cst));
+            const float uy = fmaf(yi.x, r.y, fmaf(yi.y, r.x, cst));
+            const float ex = ux - fminf(fmaxf(rintf(ux), 0.f), Lm1);
+            const float ey = uy - fminf(fmaxf(rintf(uy), 0.f), Lm1);
+            return fmaf(ex, ex, ey * ey);
+          };
+          const float4 *y4 = reinterpret_cast<const float4 *>(sm.y);
+          const int n2 = nvalid >> 1;
+#pragma unroll 4
+          for (int i = 0; i < n2; ++i) {
+            const float4 yy = y4[i];
+            dA += bdist(make_float2(yy.x, yy.y), rsA);
+            dA2 += bdist(make_float2(yy.z, yy.w), rsA);
             if (d.Pt > 32) {
-              const float2 zr = cmul(yi, rotB);
-              const float fi = fminf(fmaxf(floorf(fmaf(zr.x, inv2s, Lh)), 0.f), Lm1);
-              const float fq = fminf(fmaxf(floorf(fmaf(zr.y, inv2s, Lh)), 0.f), Lm1);
-              const float dx = zr.x - fmaf(fi, two_s, lvl0), dy = zr.y - fmaf(fq, two_s, lvl0);
-              dB += fmaf(dx, dx, dy * dy);
+              dB += bdist(make_float2(yy.x, yy.y), rsB);
+              dB2 += bdist(make_float2(yy.z, yy.w), rsB);
             }
           }
+          if (nvalid & 1) {
+            const float2 yi = sm.y[nvalid - 1];
+            dA += bdist(yi, rsA);
+            if (d.Pt > 32) dB += bdist(yi, rsB);
+          }
+          dA += dA2;
+          dB += dB2;
           float bd = lane < d.Pt ? dA : 3.4e38f;
           int bp = lane;
           if (lane + 32 < d.Pt && dB < bd) { bd = dB; bp = lane + 32; }
@@ -415,7 +429,9 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
         }
         if (first) theta = th_hat;
         else theta = th_hat + 1.5707963267948966f * rintf((theta - th_hat) * 0.63661977236758134f);
-        sincosf(theta, &sth, &cth);
+        // theta reduced to [-pi, pi] first: the fast sincos is accurate there (no local-memory
+        // range reduction in the serial loop)
+        __sincosf(theta - 6.283185307179586f * rintf(theta * 0.15915494309189535f), &sth, &cth);
         zp = cmul(y, make_float2(cth, -sth));
       }
       float2 dv;

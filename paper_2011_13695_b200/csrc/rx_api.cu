@@ -504,11 +504,6 @@ static rx_status check_launch() {
 }
 
 static unsigned gridc(long long n, int per) { return (unsigned)((n + per - 1) / per); }
-// persistent grid: one wave (SMs x resident CTAs), never more CTAs than work groups
-static unsigned pgrid(const rx_handle *h, long long n, int per, int occ) {
-  const long long g = (n + per - 1) / per, cap = (long long)h->n_sm * (occ > 0 ? occ : 1);
-  return (unsigned)(g < cap ? g : cap);
-}
 
 // tap padding KP in {4, 8, 16, 32} (compile-time) and the CPR flavour select the instance
 typedef void (*lms_seg_fn)(RxDev, int, int, unsigned char *, long long);
