@@ -201,6 +201,45 @@ __device__ __forceinline__ void lms_stage(const RxDev &d, LmsSmemT<CPLX> &sm, lo
   }
 }
 
+// Blind phase search partial sums over symbols [i0, i1) of a block (lane p: test phases p and
+// p + 32). Distances are in units of the level spacing 2s: u = y e^{-j phi_p} / 2s + (L - 1)/2
+// puts the levels on the integers 0..L-1, so |z - slice(z)|^2 = (2s)^2 sum (u - clamp(rint u))^2
+// (the common factor (2s)^2 does not move the argmin). Fixed summation order.
+__device__ __forceinline__ float bps_dist(float2 yi, float2 r, float cst, float Lm1) {
+  const float ux = fmaf(yi.x, r.x, fmaf(-yi.y, r.y, cst));
+  const float uy = fmaf(yi.x, r.y, fmaf(yi.y, r.x, cst));
+  const float ex = ux - fminf(fmaxf(rintf(ux), 0.f), Lm1);
+  const float ey = uy - fminf(fmaxf(rintf(uy), 0.f), Lm1);
+  return fmaf(ex, ex, ey * ey);
+}
+__device__ __forceinline__ void bps_partial(const float2 *ys, int i0, int i1, float2 rsA, float2 rsB, int L,
+                                            bool two, float &dA, float &dB) {
+  const float cst = 0.5f * (float)(L - 1), Lm1 = (float)(L - 1);
+  float a0 = 0.f, a1 = 0.f, b0 = 0.f, b1 = 0.f;
+  const float4 *y4 = reinterpret_cast<const float4 *>(ys);
+  const int n2 = (i1 - i0) >> 1;     // i0 even
+#pragma unroll 4
+  for (int i = 0; i < n2; ++i) {
+    const float4 yy = y4[(i0 >> 1) + i];
+    a0 += bps_dist(make_float2(yy.x, yy.y), rsA, cst, Lm1);
+    a1 += bps_dist(make_float2(yy.z, yy.w), rsA, cst, Lm1);
+    if (two) {
+      b0 += bps_dist(make_float2(yy.x, yy.y), rsB, cst, Lm1);
+      b1 += bps_dist(make_float2(yy.z, yy.w), rsB, cst, Lm1);
+    }
+  }
+  if ((i1 - i0) & 1) {
+    const float2 yi = ys[i1 - 1];
+    a0 += bps_dist(yi, rsA, cst, Lm1);
+    if (two) b0 += bps_dist(yi, rsB, cst, Lm1);
+  }
+  dA += a0 + a1;
+  dB += b0 + b1;
+}
+__device__ __forceinline__ void named_bar(int id) {   // the 64 threads of a segment's warp pair
+  asm volatile("bar.sync %0, 64;\n" ::"r"(id) : "memory");
+}
+
 // 4 x 8 register tile of a 32 x 32 Toeplitz contraction (TILED path of lms_run): x4 -> 12
 // consecutive window samples X, v4 -> 8 coefficients V; FILTER: acc[a] = sum_b V[b] X[a + 7 - b]
 // (outputs a, taps b), else acc[a] = sum_b V[b] X[b + 3 - a] (taps a, outputs b)
@@ -268,7 +307,7 @@ __device__ __forceinline__ float level_of(int i, float two_s, float off) { retur
 template <bool CPLX, int CPR, int MODE, int KP>
 __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, long long t_end,
                          long long out_lo, float2 &wk, unsigned char *warm, double &evn,
-                         double &evd, long long vend) {
+                         double &evd, long long vend, int bps_bar = 0, float2 *bps_part = nullptr) {
   using T = typename LmsElem<CPLX>::T;
   const int lane = threadIdx.x & 31;
   const int K = d.K, c = K >> 1;
@@ -384,38 +423,21 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
           // distance in units of the level spacing 2s: u = y e^{-j phi_p} / 2s + (L - 1)/2 puts
           // the levels on the integers 0..L-1, so |z - slice(z)|^2 = (2s)^2 sum (u - clamp(rint u))^2
           // (the common factor (2s)^2 does not move the argmin)
-          sm.y[lane] = y;
-          __syncwarp();
-          const float cst = 0.5f * (float)(L - 1), Lm1 = (float)(L - 1);
           const float2 rsA = make_float2(rotA.x * inv2s, rotA.y * inv2s);
           const float2 rsB = make_float2(rotB.x * inv2s, rotB.y * inv2s);
-          float dA = 0.f, dA2 = 0.f, dB = 0.f, dB2 = 0.f;
-          auto bdist = [&](float2 yi, float2 r) -> float {
-            const float ux = fmaf(yi.x, r.x, fmaf(-yi.y, r.y, cst));
-            const float uy = fmaf(yi.x, r.y, fmaf(yi.y, r.x, cst));
-            const float ex = ux - fminf(fmaxf(rintf(ux), 0.f), Lm1);
-            const float ey = uy - fminf(fmaxf(rintf(uy), 0.f), Lm1);
-            return fmaf(ex, ex, ey * ey);
-          };
-          const float4 *y4 = reinterpret_cast<const float4 *>(sm.y);
-          const int n2 = nvalid >> 1;
-#pragma unroll 4
-          for (int i = 0; i < n2; ++i) {
-            const float4 yy = y4[i];
-            dA += bdist(make_float2(yy.x, yy.y), rsA);
-            dA2 += bdist(make_float2(yy.z, yy.w), rsA);
-            if (d.Pt > 32) {
-              dB += bdist(make_float2(yy.x, yy.y), rsB);
-              dB2 += bdist(make_float2(yy.z, yy.w), rsB);
-            }
+          float dA = 0.f, dB = 0.f;
+          sm.y[lane] = y;
+          if (bps_bar) {   // helper warp scores symbols 16..31 (bps_helper)
+            named_bar(bps_bar);
+            bps_partial(sm.y, 0, nvalid < 16 ? nvalid : 16, rsA, rsB, L, d.Pt > 32, dA, dB);
+            named_bar(bps_bar);
+            const float2 pb = bps_part[lane];
+            dA += pb.x;
+            dB += pb.y;
+          } else {
+            __syncwarp();
+            bps_partial(sm.y, 0, nvalid, rsA, rsB, L, d.Pt > 32, dA, dB);
           }
-          if (nvalid & 1) {
-            const float2 yi = sm.y[nvalid - 1];
-            dA += bdist(yi, rsA);
-            if (d.Pt > 32) dB += bdist(yi, rsB);
-          }
-          dA += dA2;
-          dB += dB2;
           float bd = lane < d.Pt ? dA : 3.4e38f;
           int bp = lane;
           if (lane + 32 < d.Pt && dB < bd) { bd = dB; bp = lane + 32; }
@@ -600,17 +622,45 @@ __device__ __forceinline__ void pam_finalise(const RxDev &d, long long lo, long 
   }
 }
 
+// BPS helper warp (KK, CPR = BPS): per block, waits for the block's y, scores symbols 16..31
+// for every test phase and hands the partial sums to the segment's LMS warp (c-9 step 2)
+__device__ void bps_helper(const RxDev &d, const float2 *ys, long long t_begin, long long t_end, int bar,
+                           float2 *part) {
+  const int lane = threadIdx.x & 31, L = d.L;
+  const float two_s = 2.0f * d.qam_sc, inv2s = 1.0f / two_s;
+  float2 rotA = make_float2(1.f, 0.f), rotB = make_float2(1.f, 0.f);
+  if (lane < d.Pt) rotA = __ldg(d.bps_rot + lane);
+  if (lane + 32 < d.Pt) rotB = __ldg(d.bps_rot + lane + 32);
+  const float2 rsA = make_float2(rotA.x * inv2s, rotA.y * inv2s);
+  const float2 rsB = make_float2(rotB.x * inv2s, rotB.y * inv2s);
+  const long long nblk = (t_end - t_begin + 31) / 32;
+#pragma unroll 1
+  for (long long jb = 0; jb < nblk; ++jb) {
+    const long long t = t_begin + 32 * jb;
+    const int nvalid = (int)((t_end - t) < 32 ? (t_end - t) : 32);
+    named_bar(bar);
+    float dA = 0.f, dB = 0.f;
+    if (nvalid > 16) bps_partial(ys, 16, nvalid, rsA, rsB, L, d.Pt > 32, dA, dB);
+    part[lane] = make_float2(dA, dB);
+    named_bar(bar);
+  }
+}
+
 // ------------------------------------------------------------------ segments (1 warp each)
 // Segment s outputs [sS, min((s+1)S, m_end)), recursion starts O symbols early (c-9).
 template <bool CPLX, int CPR, int KP>
 __global__ void __launch_bounds__(128) k_lms_seg(RxDev d, int flush, int nseg, unsigned char *labels,
                                                  long long lab_cap) {
-  __shared__ LmsSmemT<CPLX> sm[4];
+  // BPS segments run on a warp pair (LMS warp + BPS helper), others on one warp
+  constexpr int PAIR = 1, SPC = 4 / PAIR;   // PAIR = 2 runs BPS on an extra helper warp
+  __shared__ LmsSmemT<CPLX> sm[SPC];
+  __shared__ float2 bps_part[SPC][32];
   DevState *st = d.st;
   if (!st->trained) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long s = st->seg_next + (long long)blockIdx.x * 4 + warp;
-  if (blockIdx.x * 4 + warp >= nseg) return;
+  const int slot = (threadIdx.x >> 5) / PAIR, role = (threadIdx.x >> 5) % PAIR, lane = threadIdx.x & 31;
+  const int warp = slot;
+  const long long s = st->seg_next + (long long)blockIdx.x * SPC + slot;
+  if (blockIdx.x * SPC + slot >= nseg) return;
   if (d.seg_done[rmod(s, d.seg_cap)] == s + 1) return;
   const long long S = d.S;
   const long long lo = s * S;
@@ -636,7 +686,12 @@ __global__ void __launch_bounds__(128) k_lms_seg(RxDev d, int flush, int nseg, u
   if (t0 < 0) t0 = 0;
   double en = 0.0, ed = 0.0;
   unsigned char *warm = d.O > 0 ? d.seg_warm + rmod(s, d.seg_cap) * d.O : nullptr;
-  const float th = lms_run<CPLX, CPR, 1, KP>(d, sm[warp], t0, hi, lo, wk, warm, en, ed, vend);
+  if (PAIR == 2 && role == 1) {
+    bps_helper(d, sm[warp].y, t0, hi, 1 + slot, bps_part[slot]);
+    return;
+  }
+  const float th = lms_run<CPLX, CPR, 1, KP>(d, sm[warp], t0, hi, lo, wk, warm, en, ed, vend,
+                                             PAIR == 2 ? 1 + slot : 0, bps_part[slot]);
   en = warp_sum_d(en);
   ed = warp_sum_d(ed);
   const long long si = rmod(s, d.seg_cap);
@@ -858,30 +913,63 @@ __global__ void __launch_bounds__(256) k_lms_final(RxDev d, unsigned char *label
   const long long lo = s * (long long)d.S, hi = seg_end_of(d, s);
   const int b = d.kbits >> 1;
   long long err = 0, cntd = 0;
-  // reference index and label slot of the segment's first symbol (one modulo per segment)
+  // reference index of the segment's first symbol (one modulo per segment); 16 symbols per
+  // thread-step: 128-bit level / label accesses where aligned
   const int r0 = (int)(((st->sync_offset + lo - d.m0) % RX_PREF + RX_PREF) % RX_PREF);
-  const long long l0 = labels ? lo % lab_cap : 0;
-  for (long long m = lo + threadIdx.x; m < hi; m += blockDim.x) {
-    const int dm = (int)(m - lo);
-    int code = d.level[rmod(m, d.sym_cap)];
-    int lab;
-    if (d.family == 1) {
-      code = qam_rot(code, R, d.L);       // level ring stays in the segment frame (stitching)
-      lab = (gray(code & 15) << b) | gray(code >> 4);
+  const bool lvec = labels && (((unsigned long long)labels | (unsigned long long)lab_cap) & 15) == 0;
+  for (long long v = 16LL * threadIdx.x; v < hi - lo; v += 16LL * blockDim.x) {
+    const long long m0v = lo + v;
+    const int nv = hi - m0v < 16 ? (int)(hi - m0v) : 16;
+    const bool full = nv == 16 && (m0v & 15) == 0;
+    unsigned char code[16];
+    if (full) {
+      const uint4 q = *reinterpret_cast<const uint4 *>(d.level + rmod(m0v, d.sym_cap));
+      const unsigned w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int j = 0; j < 16; ++j) code[j] = (unsigned char)(w[j >> 2] >> (8 * (j & 3)));
     } else {
-      lab = gray(code);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) code[j] = j < nv ? d.level[rmod(m0v + j, d.sym_cap)] : 0;
     }
-    d.level_fin[rmod(m, d.sym_cap)] = (unsigned char)code;
-    if (labels) {
-      long long li = l0 + dm;
-      if (li >= lab_cap) li -= lab_cap * (li / lab_cap);
-      labels[li] = (unsigned char)lab;
+    unsigned char lab[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      int c = code[j];
+      if (d.family == 1) {
+        c = qam_rot(c, R, d.L);       // level ring stays in the segment frame (stitching)
+        lab[j] = (unsigned char)((gray(c & 15) << b) | gray(c >> 4));
+      } else {
+        lab[j] = (unsigned char)gray(c);
+      }
+      code[j] = (unsigned char)c;
     }
-    if (m >= d.warmup) {
-      int ri = r0 + dm;                         // dm < S <= 2^15: at most one wrap
-      if (ri >= RX_PREF) ri -= RX_PREF;
-      err += __popc(lab ^ (int)d.ref_lab[ri]);
-      ++cntd;
+    if (full) {
+      unsigned w[4] = {0u, 0u, 0u, 0u}, l[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int j = 0; j < 16; ++j) { w[j >> 2] |= (unsigned)code[j] << (8 * (j & 3)); l[j >> 2] |= (unsigned)lab[j] << (8 * (j & 3)); }
+      *reinterpret_cast<uint4 *>(d.level_fin + rmod(m0v, d.sym_cap)) = make_uint4(w[0], w[1], w[2], w[3]);
+      if (lvec) *reinterpret_cast<uint4 *>(labels + m0v % lab_cap) = make_uint4(l[0], l[1], l[2], l[3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) if (j < nv) d.level_fin[rmod(m0v + j, d.sym_cap)] = code[j];
+    }
+    if (labels && !(full && lvec)) {
+      long long li = m0v % lab_cap;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (j < nv) labels[li] = lab[j];
+        if (++li == lab_cap) li = 0;
+      }
+    }
+    int ri = r0 + (int)(v % RX_PREF);
+    if (ri >= RX_PREF) ri -= RX_PREF;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (j < nv && m0v + j >= d.warmup) {
+        err += __popc((int)lab[j] ^ (int)__ldg(d.ref_lab + ri));
+        ++cntd;
+      }
+      if (++ri == RX_PREF) ri = 0;
     }
   }
   err = __reduce_add_sync(0xffffffffu, (unsigned)err);
