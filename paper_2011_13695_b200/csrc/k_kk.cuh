@@ -38,8 +38,8 @@ __global__ void __launch_bounds__(256) k_kk_s1(RxDev d, InView in, long long b0,
           if (p < first_dom) first_dom = p;
         }
         I = fmaxf(I, 1e-12f);
-        hh[e] = 0.5f * logf(I);                         // P:215 logarithm for the phase
-        if (r >= 2 && r < 6) amp[r - 2][e] = sqrtf(I);  // P:215 square root: amplitude
+        hh[e] = 0.5f * __logf(I);                       // P:215 logarithm for the phase (MUFU lg2)
+        if (r >= 2 && r < 6) amp[r - 2][e] = I * rsqrtf(I);   // P:215 square root: amplitude
       }
       v[r] = make_float2(hh[0], hh[1]);
     }
@@ -84,19 +84,27 @@ __global__ void __launch_bounds__(256) k_kk_s1(RxDev d, InView in, long long b0,
   // v[r] = 512 (phi[2n] + i phi[2n+1]), n = j + 64 r; kept local [256, 768) <=> r = 2..5
   if (act) {
     const float sg = (float)d.sideband;
+    // downshift to DC: e^{-j psi(p; sigma f_c)}, 64-bit DDS from the absolute index for
+    // the thread's first sample, then exact-phase-word steps of 1 and 128 samples as rotations
+    // (|error| ~ 1e-7 after the 3 steps)
+    const long long pa = 512 * b - 512 + 2 * (j + 128);
+    float2 rp = dds_rot_neg((unsigned long long)pa * d.carrier_inc);
+    const float2 st1 = dds_rot_neg(d.carrier_inc), st128 = dds_rot_neg(d.carrier_inc * 128ULL);
 #pragma unroll
     for (int r = 2; r < 6; ++r) {
       const int n = j + 64 * r;
       const long long p = 512 * b - 512 + 2 * n;
+      const float2 r0 = rp, r1 = cmul(rp, st1);
+      rp = cmul(rp, st128);
       if (p < 0) continue;
-      const float ph0 = v[r].x * (1.0f / 512.0f), ph1 = v[r].y * (1.0f / 512.0f);
+      // sigma phi in [-pi, pi] first, then the MUFU sin/cos (accurate there)
+      float ph0 = sg * v[r].x * (1.0f / 512.0f), ph1 = sg * v[r].y * (1.0f / 512.0f);
+      ph0 -= 6.283185307179586f * rintf(ph0 * 0.15915494309189535f);
+      ph1 -= 6.283185307179586f * rintf(ph1 * 0.15915494309189535f);
       float s0, c0, s1, c1;
-      sincosf(sg * ph0, &s0, &c0);
-      sincosf(sg * ph1, &s1, &c1);
+      __sincosf(ph0, &s0, &c0);
+      __sincosf(ph1, &s1, &c1);
       const float a0 = amp[r - 2][0], a1 = amp[r - 2][1];
-      // downshift to DC: e^{-j psi(p; sigma f_c)}, 64-bit DDS from the absolute index
-      const float2 r0 = dds_rot_neg((unsigned long long)p * d.carrier_inc);
-      const float2 r1 = dds_rot_neg((unsigned long long)(p + 1) * d.carrier_inc);
       const float2 e0 = cmul(make_float2(a0 * c0, a0 * s0), r0);
       const float2 e1 = cmul(make_float2(a1 * c1, a1 * s1), r1);
       *reinterpret_cast<float4 *>(d.E + rmod(p, d.E_cap)) = make_float4(e0.x, e0.y, e1.x, e1.y);
