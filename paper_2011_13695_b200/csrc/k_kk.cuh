@@ -113,62 +113,47 @@ __global__ void __launch_bounds__(256) k_kk_s1(RxDev d, InView in, long long b0,
 }
 
 // ------------------------------------------------------------------ H16-H18
-// 4 blocks per CTA: pass A runs 8 half-size FFTs (evens / odds of each block) on the 4 groups,
-// pass B the 4 decimating IFFT-512s.
+// One block per 64-thread group, entirely in registers between the FFT passes:
+//   F = DFT_1024(E frame) from the two half-size FFTs of the even / odd samples, whose pass-1
+//   operands (E[p0 + 2n], E[p0 + 2n + 1], n = j + 64 r) are one float4 load each;
+//   G'[k'] = (Ev[k'] + W^k' Od[k']) H2[k'],        k' in [0, 256)   (kappa = k')
+//   G'[k'] = (Ev[k'] - W^k' Od[k']) H2[k' + 512],  k' in [256, 512) (kappa = k' - 512)
+//   — bin k' = j + 64 r is exactly the IFFT's pass-1 operand of thread j, so the band-selected
+//   spectrum feeds the decimating IFFT-512 without a shared-memory round trip.
 __global__ void __launch_bounds__(256) k_kk_s2(RxDev d, long long b0, long long b1) {
-  extern __shared__ float2 sm[];
-  float2 *tw = sm;                               // 1024
-  float2 *bufs = sm + 1024;                      // [4 blocks][2][FFT_PAD_N]
+  __shared__ float2 tw[1024];
+  __shared__ float2 buf[FE_GROUPS][FFT_PAD_N];
   const int g = threadIdx.x >> 6, j = threadIdx.x & 63;
   for (int i = threadIdx.x; i < 1024; i += blockDim.x) tw[i] = d.tw[i];
-  // load E for the 4 blocks: frame p in [512b - 512, 512b + 512), E_p = 0 for p < 0
-  for (int bl = 0; bl < 4; ++bl) {
-    const long long b = b0 + (long long)blockIdx.x * 4 + bl;
-    float2 *be = bufs + (bl * 2) * FFT_PAD_N, *bo = bufs + (bl * 2 + 1) * FFT_PAD_N;
-    for (int n = threadIdx.x; n < 512; n += blockDim.x) {
-      const long long p = 512 * b - 512 + 2 * n;
-      float4 e = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (b < b1 && p >= 0) e = *reinterpret_cast<const float4 *>(d.E + rmod(p, d.E_cap));
-      be[P8(n)] = make_float2(e.x, e.y);
-      bo[P8(n)] = make_float2(e.z, e.w);
-    }
-  }
-  __syncthreads();
-  float2 v[8];
-  // pass A: group g transforms half-buffers 2g and 2g+1 ... (blocks g/2 ... ) -> 8 halves on 4 groups
-  for (int rep = 0; rep < 2; ++rep) {
-    float2 *hb = bufs + (g * 2 + rep) * FFT_PAD_N;
-    fft512<false>(hb, j, tw, v);
-    fft512_store(hb, j, v);
-  }
-  // combine + EQ + band select: for block bl = g:
-  //   G'[k'] = (Ev[k'] + W^k' Od[k']) H2[k'],        k' in [0, 256)   (kappa = k')
-  //   G'[k'] = (Ev[k'] - W^k' Od[k']) H2[k' + 512],  k' in [256, 512) (kappa = k' - 512)
+  const long long b = b0 + (long long)blockIdx.x * FE_GROUPS + g;
+  const bool act = b < b1;
+  float2 ve[8], vo[8];
   {
-    float2 *be = bufs + (g * 2) * FFT_PAD_N, *bo = bufs + (g * 2 + 1) * FFT_PAD_N;
+    float4 e[8];
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int k = j + 64 * r;
-      const float2 ev = be[P8(k)], od = cmul(bo[P8(k)], tw[k]);
-      float2 G;
-      if (k < 256) G = cmul(cadd(ev, od), __ldg(d.H + k));
-      else G = cmul(csub(ev, od), __ldg(d.H + k + 512));
-      be[P8(k)] = G;
+    for (int r = 0; r < 8; ++r) {           // frame p in [512b - 512, 512b + 512), E_p = 0 for p < 0
+      const long long p = 512 * b - 512 + 2 * (j + 64 * r);
+      e[r] = (act && p >= 0) ? *reinterpret_cast<const float4 *>(d.E + rmod(p, d.E_cap))
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-  }
-  __syncthreads();
-  {
-    float2 *be = bufs + (g * 2) * FFT_PAD_N;
-    fft512<true>(be, j, tw, v);
-    // z_local[n] = 1/2 * IDFT512 = v / 1024; keep n in [128, 384) <=> r = 2..5
-    const long long b = b0 + (long long)blockIdx.x * 4 + g;
-    if (b < b1) {
 #pragma unroll
-      for (int r = 2; r < 6; ++r) {
-        const int n = j + 64 * r;
-        const long long q = 256 * b - 256 + n;
-        if (q >= 0) d.z[rmod(q, d.z_cap)] = cscale(v[r], 1.0f / 1024.0f);
-      }
+    for (int r = 0; r < 8; ++r) { ve[r] = make_float2(e[r].x, e[r].y); vo[r] = make_float2(e[r].z, e[r].w); }
+  }
+  fft512_regs<false>(buf[g], j, tw, ve);
+  fft512_regs<false>(buf[g], j, tw, vo);
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int k = j + 64 * r;
+    const float2 od = cmul(vo[r], tw[k]);
+    ve[r] = r < 4 ? cmul(cadd(ve[r], od), __ldg(d.H + k)) : cmul(csub(ve[r], od), __ldg(d.H + k + 512));
+  }
+  fft512_regs<true>(buf[g], j, tw, ve);
+  // z_local[n] = 1/2 * IDFT512 = v / 1024; keep n in [128, 384) <=> r = 2..5
+  if (act) {
+#pragma unroll
+    for (int r = 2; r < 6; ++r) {
+      const long long q = 256 * b - 256 + j + 64 * r;
+      if (q >= 0) d.z[rmod(q, d.z_cap)] = cscale(ve[r], 1.0f / 1024.0f);
     }
   }
 }
@@ -272,12 +257,12 @@ __global__ void __launch_bounds__(1024) k_cfo_final(RxDev d, long long beta0, lo
   double s = 0.0;
   {
     int r = 0;
-    for (; r + 8 <= nrows; r += 8) {          // 8 independent loads in flight, summed in order
-      float v[8];
+    for (; r + 32 <= nrows; r += 32) {        // 32 independent loads in flight, summed in order
+      float v[32];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = d.cfo_part[(rb + r + i) * 1024 + t];
+      for (int i = 0; i < 32; ++i) v[i] = d.cfo_part[(rb + r + i) * 1024 + t];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) s += (double)v[i];
+      for (int i = 0; i < 32; ++i) s += (double)v[i];
     }
     for (; r < nrows; ++r) s += (double)d.cfo_part[(rb + r) * 1024 + t];
   }

@@ -461,11 +461,9 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   memset((void *)h->hm_host, 0, sizeof(HostMirror));
   if (cudaHostGetDevicePointer((void **)&d.hm, (void *)h->hm_host, 0) != cudaSuccess) { rx_destroy(h); return RX_ECUDA; }
   // kernels needing > 48 KB dynamic shared memory
-  const size_t s2_smem = (1024 + 8 * FFT_PAD_N) * sizeof(float2);
   const size_t cfo_smem = (1024 + 2 * CFO_GROUPS * FFT_PAD_N) * sizeof(float2) + 1024 * sizeof(float);
   const size_t clk_smem = (CLK_TILE + 1 + 2 * c.clock_avg_half) * sizeof(double2);
   if (cudaFuncSetAttribute(k_pam_theta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)clk_smem) != cudaSuccess ||
-      cudaFuncSetAttribute(k_kk_s2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2_smem) != cudaSuccess ||
       cudaFuncSetAttribute(k_cfo_spec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfo_smem) != cudaSuccess ||
       cudaFuncSetAttribute(k_sync_corr<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536) != cudaSuccess ||
       cudaFuncSetAttribute(k_sync_corr<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536) != cudaSuccess) {
@@ -670,8 +668,7 @@ static void run_kk(rx_handle *h, cudaStream_t s, const InView &in, unsigned char
   }
   const long long s2_target = h->fe_done - 1;
   if (s2_target > h->s2_done) {
-    const size_t smem = (1024 + 8 * FFT_PAD_N) * sizeof(float2);
-    KLAUNCH(h, RX_K_KK_S2, s, (k_kk_s2<<<gridc(s2_target - h->s2_done, 4), 256, smem, s>>>(d, h->s2_done, s2_target)));
+    KLAUNCH(h, RX_K_KK_S2, s, (k_kk_s2<<<gridc(s2_target - h->s2_done, FE_GROUPS), 256, 0, s>>>(d, h->s2_done, s2_target)));
     h->s2_done = s2_target;
   }
   const long long q_front = h->s2_done > 0 ? 256 * h->s2_done - 128 : 0;
