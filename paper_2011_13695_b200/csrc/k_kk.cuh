@@ -180,30 +180,32 @@ __device__ __forceinline__ void buf_range(const RxDev &d, long long beta, long l
 __global__ void __launch_bounds__(1024) k_cfo_spec(RxDev d, long long beta0, long long qfront) {
   extern __shared__ float2 sm[];
   float2 *tw = sm;
-  float2 *bufs = sm + 1024;                    // [CFO_GROUPS][2][FFT_PAD_N]
-  float *S = reinterpret_cast<float *>(bufs + 2 * CFO_GROUPS * FFT_PAD_N);   // [1024]
+  float2 *bufs = sm + 1024;                    // [CFO_GROUPS][FFT_PAD_N]; later acc[CFO_GROUPS][1024]
   __shared__ double red[32];
   const int g = threadIdx.x >> 6, j = threadIdx.x & 63;
   long long qlo, qhi;
   buf_range(d, beta0 + blockIdx.y, qfront, qlo, qhi);
-  for (int i = threadIdx.x; i < 1024; i += blockDim.x) { tw[i] = d.tw[i]; S[i] = 0.f; }
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) tw[i] = d.tw[i];
   const long long nch = (qhi - qlo) / 1024;
-  // power partial over this CTA's share of all samples (including a tail shorter than a chunk)
-  double pw = 0.0;
-  {
-    const long long n = qhi - qlo;
-    const long long a0 = qlo + n * blockIdx.x / gridDim.x, a1 = qlo + n * (blockIdx.x + 1) / gridDim.x;
-    for (long long q = a0 + threadIdx.x; q < a1; q += blockDim.x) pw += (double)cabs2(d.z[rmod(q, d.z_cap)]);
-  }
   const long long c = (long long)blockIdx.x * CFO_GROUPS + g;
   const bool act = c < nch;
-  float2 *be = bufs + (g * 2) * FFT_PAD_N, *bo = bufs + (g * 2 + 1) * FFT_PAD_N;
+  float2 *bg = bufs + g * FFT_PAD_N;
   float2 ve[8], vo[8];
   float4 zz[8];
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
     zz[r] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (act) zz[r] = *reinterpret_cast<const float4 *>(d.z + rmod(qlo + 1024 * c + 2 * (j + 64 * r), d.z_cap));
+  }
+  // power partial: the chunk samples this thread loaded, plus (last CTA) the tail < one chunk
+  double pw = 0.0;
+  {
+    float p0 = 0.f;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) p0 += zz[r].x * zz[r].x + zz[r].y * zz[r].y + zz[r].z * zz[r].z + zz[r].w * zz[r].w;
+    pw = (double)p0;
+    if (blockIdx.x == gridDim.x - 1)
+      for (long long q = qlo + 1024 * nch + threadIdx.x; q < qhi; q += blockDim.x) pw += (double)cabs2(d.z[rmod(q, d.z_cap)]);
   }
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
@@ -212,28 +214,27 @@ __global__ void __launch_bounds__(1024) k_cfo_spec(RxDev d, long long beta0, lon
     ve[r] = cmul(a2, a2);
     vo[r] = cmul(b2, b2);
   }
-  fft512_regs<false>(be, j, tw, ve);
-  fft512_regs<false>(bo, j, tw, vo);
-  float acc[16];
+  fft512_regs<false>(bg, j, tw, ve);
+  fft512_regs<false>(bg, j, tw, vo);      // same buffer: fft512_regs syncs before its first store
+  __syncthreads();                        // every group done with its FFT buffer
+  float *acc = reinterpret_cast<float *>(bufs);
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
     const int k = j + 64 * r;
     const float2 od = cmul(vo[r], tw[k]);
-    acc[r] = act ? cabs2(cadd(ve[r], od)) : 0.f;        // X[k]
-    acc[8 + r] = act ? cabs2(csub(ve[r], od)) : 0.f;    // X[k + 512]
+    acc[g * 1024 + k] = act ? cabs2(cadd(ve[r], od)) : 0.f;         // X[k]
+    acc[g * 1024 + k + 512] = act ? cabs2(csub(ve[r], od)) : 0.f;   // X[k + 512]
   }
-  for (int gg = 0; gg < CFO_GROUPS; ++gg) {             // groups in fixed order
-    if (g == gg) {
-#pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        S[j + 64 * r] += acc[r];
-        S[j + 64 * r + 512] += acc[8 + r];
-      }
-    }
-    __syncthreads();
-  }
+  __syncthreads();
+  // S[k] = sum over the CTA's chunks in fixed group order
   const long long row = (long long)blockIdx.y * gridDim.x + blockIdx.x;
-  for (int i = threadIdx.x; i < 1024; i += blockDim.x) d.cfo_part[row * 1024 + i] = S[i];
+  {
+    const int k = threadIdx.x;
+    float sk = 0.f;
+#pragma unroll
+    for (int gg = 0; gg < CFO_GROUPS; ++gg) sk += acc[gg * 1024 + k];
+    d.cfo_part[row * 1024 + k] = sk;
+  }
   pw = warp_sum_d(pw);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = pw;
   __syncthreads();
@@ -329,10 +330,15 @@ __global__ void __launch_bounds__(256) k_cfo_fine(RxDev d, long long beta0, long
 #pragma unroll
     for (int u = 0; u < 32; ++u) zz[u] = d.z[rmod(qlo + 1024 * i + lane + 32 * u, d.z_cap)];
     float ax = 0.f, ay = 0.f;
+    // DDS rotation: exact phase word every 8th sample of the lane, 32-sample step rotations
+    // in between (|error| < 1e-6 rad)
+    const float2 st32 = dds_rot_neg(32ULL * inc);
+    float2 rot = make_float2(1.f, 0.f);
 #pragma unroll
     for (int u = 0; u < 32; ++u) {
       const long long n = 1024 * i + lane + 32 * u;
-      const float2 w = cmul(zz[u], dds_rot_neg((unsigned long long)n * inc));
+      rot = (u & 7) == 0 ? dds_rot_neg((unsigned long long)n * inc) : cmul(rot, st32);
+      const float2 w = cmul(zz[u], rot);
       const float2 w2 = cmul(w, w), w4 = cmul(w2, w2);
       ax += w4.x;
       ay += w4.y;
@@ -393,18 +399,37 @@ __global__ void __launch_bounds__(256) k_kk_zprime(RxDev d, long long beta0, int
   long long q1 = (beta0 + nbuf) * Q;
   if (q1 > qfront) q1 = qfront;
   if (blockIdx.x == 0 && threadIdx.x == 0) d.st->v_front = q1;   // consumed by later launches
-  for (long long q = q0 + 2 * ((long long)blockIdx.x * blockDim.x + threadIdx.x); q < q1;
-       q += 2 * (long long)gridDim.x * blockDim.x) {
+  // 8 consecutive samples per thread-step (Q is a multiple of 8: one buffer per step): one exact
+  // DDS phase word, then 1-sample step rotations
+  for (long long q = q0 + 8 * ((long long)blockIdx.x * blockDim.x + threadIdx.x); q < q1;
+       q += 8 * (long long)gridDim.x * blockDim.x) {
     const long long beta = q / Q;
     const CfoParam &cp = d.cfo[rmod(beta, d.buf_cap)];
-    const float4 zz = *reinterpret_cast<const float4 *>(d.z + rmod(q, d.z_cap));
-    float2 a = cscale(make_float2(zz.x, zz.y), cp.inv_sqrtP), b = cscale(make_float2(zz.z, zz.w), cp.inv_sqrtP);
+    const float s = cp.inv_sqrtP;
+    float2 rot = make_float2(1.f, 0.f), st1 = make_float2(1.f, 0.f);
     if (d.cfo_enable) {
-      const long long n = q - beta * Q;
-      a = cmul(a, dds_rot_neg(cp.origin + (unsigned long long)n * cp.inc));
-      b = cmul(b, dds_rot_neg(cp.origin + (unsigned long long)(n + 1) * cp.inc));
+      rot = dds_rot_neg(cp.origin + (unsigned long long)(q - beta * Q) * cp.inc);
+      st1 = dds_rot_neg(cp.inc);
     }
-    if (q + 1 < q1) *reinterpret_cast<float4 *>(d.zp + rmod(q, d.zp_cap)) = make_float4(a.x, a.y, b.x, b.y);
-    else d.zp[rmod(q, d.zp_cap)] = a;
+    if (q + 8 <= q1) {
+      const float4 *src = reinterpret_cast<const float4 *>(d.z + rmod(q, d.z_cap));
+      float4 *dst = reinterpret_cast<float4 *>(d.zp + rmod(q, d.zp_cap));
+      float4 zz[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) zz[u] = src[u];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float2 a = cmul(cscale(make_float2(zz[u].x, zz[u].y), s), rot);
+        rot = cmul(rot, st1);
+        const float2 b = cmul(cscale(make_float2(zz[u].z, zz[u].w), s), rot);
+        rot = cmul(rot, st1);
+        dst[u] = make_float4(a.x, a.y, b.x, b.y);
+      }
+    } else {
+      for (long long e = q; e < q1; ++e) {
+        d.zp[rmod(e, d.zp_cap)] = cmul(cscale(d.z[rmod(e, d.z_cap)], s), rot);
+        rot = cmul(rot, st1);
+      }
+    }
   }
 }

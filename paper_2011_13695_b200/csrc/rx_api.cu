@@ -461,7 +461,7 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   memset((void *)h->hm_host, 0, sizeof(HostMirror));
   if (cudaHostGetDevicePointer((void **)&d.hm, (void *)h->hm_host, 0) != cudaSuccess) { rx_destroy(h); return RX_ECUDA; }
   // kernels needing > 48 KB dynamic shared memory
-  const size_t cfo_smem = (1024 + 2 * CFO_GROUPS * FFT_PAD_N) * sizeof(float2) + 1024 * sizeof(float);
+  const size_t cfo_smem = (1024 + CFO_GROUPS * FFT_PAD_N) * sizeof(float2);
   const size_t clk_smem = (CLK_TILE + 1 + 2 * c.clock_avg_half) * sizeof(double2);
   if (cudaFuncSetAttribute(k_pam_theta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)clk_smem) != cudaSuccess ||
       cudaFuncSetAttribute(k_cfo_spec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfo_smem) != cudaSuccess ||
@@ -678,7 +678,7 @@ static void run_kk(rx_handle *h, cudaStream_t s, const InView &in, unsigned char
     while ((h->cfo_done + nbuf + 1) * Q <= q_front || (flush && (h->cfo_done + nbuf) * Q < q_front)) ++nbuf;
     if (nbuf > 0) {
       const long long beta0 = h->cfo_done;
-      const size_t smem = (1024 + 2 * CFO_GROUPS * FFT_PAD_N) * sizeof(float2) + 1024 * sizeof(float);
+      const size_t smem = (1024 + CFO_GROUPS * FFT_PAD_N) * sizeof(float2);
       const int nrows = d.cfo_G;
       const int fine_ctas = (int)((Q / 1024 + 7) / 8);
       for (long long b0 = 0; b0 < nbuf; b0 += h->cfg.history_buffers) {
