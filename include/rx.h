@@ -98,7 +98,15 @@ typedef struct {
   int lms_batch_segments;     /* equaliser launches wait until about this many segments are
                                  pending (more concurrent segment-warps per launch; results do
                                  not depend on it; adds latency); 0 = every call */
+  int input_format;           /* rx_input_format of every rx_process call of this handle */
 } rx_config;
+
+/* Sample formats accepted by rx_process:
+ *  RX_IN_U12_IN_U16: ADC codes 0..4095 right-aligned in uint16;
+ *                    x = (code - 2047.5) / 2047.5 * adc_gain, codes 0 / 4095 count as clipped
+ *  RX_IN_F32:        x = sample * adc_gain (already in x units; e.g. simulated or
+ *                    pre-processed streams); nothing is counted as clipped */
+typedef enum { RX_IN_U12_IN_U16 = 0, RX_IN_F32 = 1 } rx_input_format;
 
 typedef struct rx_handle rx_handle;
 
@@ -122,8 +130,9 @@ void rx_config_default(rx_config *cfg, int family, int order);
  * twiddles and PRBS reference tables. No allocation happens after this call. */
 rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle **out);
 
-/* Enqueue the chain on the next n_samples of the stream (u12 codes right-aligned in uint16,
- * the ADC format of P:136 / S:602). n_samples must be a multiple of hop and at most
+/* Enqueue the chain on the next n_samples of the stream: uint16 u12 codes (the ADC format of
+ * P:136 / S:602) or float32, as cfg.input_format says; d_samples 16-byte aligned device
+ * memory on the handle's device. n_samples must be a multiple of hop and at most
  * (history_buffers - 2) * buffer_blocks * hop (one paper buffer with the default rings).
  * Samples are consumed in stream order (the overlap kernels are
  * chained). Outputs lag the input (held-back tail: 52 blocks of clock look-ahead for PAM,
@@ -131,7 +140,7 @@ rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle **out);
  * becomes final is processed. The label of absolute symbol m is written to
  * d_labels[m % labels_capacity] (PAM: Gray label; QAM: Gray(i_I) << (k/2) | Gray(i_Q));
  * labels_capacity 0 = no labels. */
-rx_status rx_process(rx_handle *h, const unsigned short *d_samples, long long n_samples,
+rx_status rx_process(rx_handle *h, const void *d_samples, long long n_samples,
                      unsigned char *d_labels, long long labels_capacity, void *cuda_stream);
 
 /* End of stream: drain the tail with truncated windows (SURVEY c-3, A14) and finish every
@@ -157,6 +166,13 @@ rx_status rx_reset_stats(rx_handle *h, void *cuda_stream);
 /* Trained taps W_train (after sync + training): K values (PAM) or 2K interleaved (KK),
  * host_out capacity in doubles. Synchronises the handle's last stream. */
 rx_status rx_get_taps(rx_handle *h, double *host_out, int capacity);
+
+/* Start taps of the training pass, replacing the centre spike of SURVEY c-9 'Training':
+ * a warm start from taps known for the channel (e.g. another handle's rx_get_taps).
+ * host_in: n doubles, n = K (PAM, real) or 2K (KK, interleaved re/im), copied synchronously.
+ * Returns RX_EINVAL on a size mismatch, RX_ESTATE once training has run (synchronises the
+ * device to check). */
+rx_status rx_set_taps(rx_handle *h, const double *host_in, int n);
 
 /* Intermediate read-back for parity tests and tracing (synchronises `cuda_stream`).
  * Copies `count` elements starting at absolute index `first` of intermediate `which`

@@ -650,13 +650,13 @@ def lms_segments(v, stride, off, m_end, seeds_fn, slicer: _Slicer, lp: LmsParams
 
 
 def lms_full(v, stride, off, m_end, ref_idx_fn, ref_val_fn, slicer: _Slicer, lp: LmsParams,
-             real: bool, m0: int, seed_rotation=None):
+             real: bool, m0: int, seed_rotation=None, w_init=None):
     """The whole equaliser of c-9: training -> epoch waves of D epochs -> stitching ->
     canonical lag-D seeds. Returns dict with final level indices per m, z', R_s, taps.
     ``seed_rotation(s)`` (test hook) multiplies segment s's seed by j^r to force it into
-    another quadrant (the stitching pin)."""
+    another quadrant (the stitching pin). ``w_init``: start taps of training (default spike)."""
     m_tr = np.arange(m0, m0 + lp.T_train)
-    w_train, v_train = lms_train(v, stride, off, ref_val_fn(m_tr), m0, lp, real)
+    w_train, v_train = lms_train(v, stride, off, ref_val_fn(m_tr), m0, lp, real, w0=w_init)
     n_seg = -(-m_end // lp.S)
     seg_per_epoch = lp.E // lp.S
     n_epoch = -(-n_seg // seg_per_epoch)
@@ -798,6 +798,7 @@ class RxParams:
     sync_window: int = 2048
     sync_min_corr: float = 0.3
     warmup_symbols: int = 0
+    w_init: np.ndarray | None = None   # start taps of the training pass (rx_set_taps); None = spike
 
 
 def _lms_params(p: RxParams) -> LmsParams:
@@ -824,7 +825,7 @@ def _finish(p: RxParams, v, stride, off, m_end, sync, out):
     slicer = _Slicer(p.fmt, p.M, p.thresholds)
     real = p.fmt == "pam"
     lm = lms_full(v, stride, off, m_end, lambda m: idx_ref[ref_index(m)],
-                  lambda m: vals_ref[ref_index(m)], slicer, lp, real, m0)
+                  lambda m: vals_ref[ref_index(m)], slicer, lp, real, m0, w_init=p.w_init)
     lo = min(max(p.warmup_symbols, 0), m_end)
     lab, errs, bits, nsym = count_errors(p.fmt, p.M, lm["idx"], lm["z"], slicer,
                                          lambda m: labels_ref[ref_index(m)], lo, m_end)

@@ -9,6 +9,8 @@ from .rx import (  # noqa: F401
     FLAGS,
     KCLASSES,
     PROBES,
+    RX_IN_F32,
+    RX_IN_U12_IN_U16,
     RX_PAM,
     RX_QAM_KK,
     Receiver,

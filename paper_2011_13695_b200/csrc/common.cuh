@@ -50,13 +50,18 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 // the history ring (the tail of earlier calls, P:136 'prepending a block … stored
 // elsewhere'), 0 for p < 0 (SURVEY c-0).
 struct InView {
-  const uint16_t *cur;
+  const uint16_t *cur;      // this call's samples (RX_IN_U12_IN_U16) ...
+  const float *curf;        // ... or (RX_IN_F32)
   long long call_start;
   long long call_end;
-  const uint16_t *hist;
-  long long hist_cap;   // power of two, > max call size + lookback + keep
-  uint16_t *hist_w;     // front-end kernels append the call's last samples here
-  long long keep_from;  // samples p >= keep_from of this call are kept in the history ring
+  const uint16_t *hist;     // history ring of earlier calls' samples (u16 codes or floats)
+  const float *histf;
+  long long hist_cap;       // power of two, > max call size + lookback + keep
+  uint16_t *hist_w;         // front-end kernels append the call's last samples here
+  float *histf_w;
+  long long keep_from;      // samples p >= keep_from of this call are kept in the history ring
+  int f32;                  // input format RX_IN_F32
+  float gain;               // adc_gain (f32 input)
 };
 __device__ __forceinline__ int in_code(const InView &v, long long p, bool &pad) {
   pad = p < 0;
@@ -64,38 +69,10 @@ __device__ __forceinline__ int in_code(const InView &v, long long p, bool &pad) 
   if (p >= v.call_start) return __ldg(v.cur + (p - v.call_start));
   return __ldg(v.hist + (p & (v.hist_cap - 1)));
 }
-
-// Load 16 consecutive codes starting at p (p multiple of 16) as floats x = (c-2047.5)*scale;
-// `pad` entries (p < 0) get value `padval`. Also counts clipped codes (0 or 4095) among
-// entries with p >= count_from.
-__device__ __forceinline__ void load16(const InView &v, long long p, float scale, float padval,
-                                       float (&x)[16], long long count_from, int &clip) {
-  if (p >= v.call_start && p + 16 <= v.call_end) {
-    const uint4 *src = reinterpret_cast<const uint4 *>(v.cur + (p - v.call_start));
-    uint4 a = __ldg(src), b = __ldg(src + 1);
-    // owned (new) samples of the call's tail go to the history ring for later calls
-    if (p >= count_from && p >= v.keep_from) {
-      uint4 *dst = reinterpret_cast<uint4 *>(v.hist_w + (p & (v.hist_cap - 1)));
-      dst[0] = a;
-      dst[1] = b;
-    }
-    uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-    const float off = -2047.5f * scale;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      int c0 = (int)(w[i] & 0xffffu), c1 = (int)(w[i] >> 16);
-      x[2 * i] = fmaf((float)c0, scale, off);
-      x[2 * i + 1] = fmaf((float)c1, scale, off);
-      if (p + 2 * i >= count_from) clip += (c0 == 0 || c0 == 4095);
-      if (p + 2 * i + 1 >= count_from) clip += (c1 == 0 || c1 == 4095);
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      bool pad;
-      int c = in_code(v, p + i, pad);
-      x[i] = pad ? padval : fmaf((float)c, scale, -2047.5f * scale);   // same rounding as fast paths
-      if (!pad && p + i >= count_from) clip += (c == 0 || c == 4095);
-    }
-  }
+// x_p of an f32 stream (0 for p < 0)
+__device__ __forceinline__ float in_xf(const InView &v, long long p) {
+  if (p < 0) return 0.f;
+  if (p >= v.call_start) return __ldg(v.curf + (p - v.call_start)) * v.gain;
+  return __ldg(v.histf + (p & (v.hist_cap - 1))) * v.gain;
 }
+

@@ -561,7 +561,8 @@ __global__ void __launch_bounds__(32) k_lms_train(RxDev d, int flush) {
   const long long vend = st->v_front;
   const long long last = (long long)stride * (d.m0 + d.T_train - 1) + (CPLX ? st->sync_phase : 0) + c;
   if (last >= vend && !flush) return;
-  float2 wk = make_float2(lane == c ? 1.f : 0.f, 0.f);    // centre spike
+  float2 wk = make_float2(lane == c ? 1.f : 0.f, 0.f);    // centre spike ...
+  if (d.has_winit) wk = lane < K ? d.w_init[lane] : make_float2(0.f, 0.f);   // ... or rx_set_taps
   double en = 0.0, ed = 0.0;
   lms_run<CPLX, 0, 0, KP>(d, sm, d.m0, d.m0 + d.T_train, 0, wk, nullptr, en, ed, vend);
   if (lane < K) d.w_train[lane] = wk;

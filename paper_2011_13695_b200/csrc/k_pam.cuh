@@ -11,43 +11,11 @@
 
 #define FE_GROUPS 4
 
-// Load block b's 1024 samples (input [512b-512, 512b+512)) into buf as packed complex
-// z[n] = x[2n] + i x[2n+1]; returns clipped count of the samples the block owns
-// ([512b, 512b+512), so every sample is counted once). Thread j loads samples 16j..16j+15.
 __device__ __forceinline__ float code_lo(uint32_t w) {     // exact float of the low 16 bits
   return __uint_as_float((w & 0xFFFFu) | 0x4B000000u) - 8388608.0f;
 }
 __device__ __forceinline__ float code_hi(uint32_t w) {
   return __uint_as_float((w >> 16) | 0x4B000000u) - 8388608.0f;
-}
-__device__ __forceinline__ int load_block_packed(const InView &in, long long b, float scale,
-                                                 float2 *buf, int j) {
-  const long long p = 512 * b - 512 + 16 * j;
-  float2 *dst = buf + 8 * j + (j >> 1);                     // P8(8 j + i) = dst + i
-  int clip = 0;
-  if (p >= in.call_start && p + 16 <= in.call_end) {
-    const uint4 *src = reinterpret_cast<const uint4 *>(in.cur + (p - in.call_start));
-    const uint4 a = __ldg(src), c = __ldg(src + 1);
-    const bool owned = j >= 32;                               // p >= 512 b
-    if (owned && p >= in.keep_from) {                         // history ring for later calls
-      uint4 *h = reinterpret_cast<uint4 *>(in.hist_w + (p & (in.hist_cap - 1)));
-      h[0] = a;
-      h[1] = c;
-    }
-    const uint32_t w[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
-    const float off = -2047.5f * scale;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      dst[i] = make_float2(fmaf(code_lo(w[i]), scale, off), fmaf(code_hi(w[i]), scale, off));
-      if (owned) clip += __popc(__vcmpeq2(w[i], 0u) | __vcmpeq2(w[i], 0x0FFF0FFFu)) >> 4;
-    }
-  } else {
-    float x[16];
-    load16(in, p, scale, 0.f, x, 512 * b, clip);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) dst[i] = make_float2(x[2 * i], x[2 * i + 1]);
-  }
-  return clip;
 }
 
 // Thread j of a block's group receives v[r] = (x[2(j + 64 r)], x[2(j + 64 r) + 1]) of block b's
@@ -59,6 +27,26 @@ __device__ __forceinline__ int load_block_regs(const InView &in, long long b, fl
   const long long p0 = 512 * b - 512;
   const float off = -2047.5f * scale;
   int clip = 0;
+  if (in.f32) {   // RX_IN_F32: x = sample * gain, no clip count; float history ring
+    if (p0 >= in.call_start && p0 + 1024 <= in.call_end) {
+      const float2 *src = reinterpret_cast<const float2 *>(in.curf + (p0 - in.call_start));
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const float2 w = __ldg(src + j + 64 * r);
+        v[r] = make_float2(w.x * in.gain, w.y * in.gain);
+        const long long p = p0 + 2 * (j + 64 * r);
+        if (r >= 4 && p >= in.keep_from)
+          reinterpret_cast<float2 *>(in.histf_w)[(p & (in.hist_cap - 1)) >> 1] = w;
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const long long p = p0 + 2 * (j + 64 * r);
+        v[r] = make_float2(in_xf(in, p), in_xf(in, p + 1));
+      }
+    }
+    return 0;
+  }
   if (p0 >= in.call_start && p0 + 1024 <= in.call_end) {
     const uint32_t *src = reinterpret_cast<const uint32_t *>(in.cur + (p0 - in.call_start));
     uint32_t w[8];

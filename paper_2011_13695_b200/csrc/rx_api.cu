@@ -22,11 +22,6 @@
 #endif
 
 // ------------------------------------------------------------------ small kernels
-__global__ void k_hist_copy(InView in, uint16_t *hist, long long hist_cap, long long p0, long long p1) {
-  for (long long p = p0 + (long long)blockIdx.x * blockDim.x + threadIdx.x; p < p1;
-       p += (long long)gridDim.x * blockDim.x)
-    hist[p & (hist_cap - 1)] = in.cur[p - in.call_start];
-}
 __global__ void k_pam_mend(RxDev d, long long be_done) {
   long long f = d.Mb[rmod(be_done, d.blk_cap)];
   if (f < 0) f = 0;
@@ -137,6 +132,7 @@ extern "C" void rx_config_default(rx_config *c, int family, int order) {
   c->hop = 512;
   c->buffer_blocks = 8192;
   c->adc_gain = 1.0;
+  c->input_format = RX_IN_U12_IN_U16;
   c->clock_avg_half = 52;
   c->carrier_offset_hz = 0.547e9;
   c->sideband = -1;
@@ -206,6 +202,7 @@ static rx_status validate(const rx_config *c) {
   if (c->sync_start < 0 || c->sync_window < 64 || c->sync_window > 4096) return RX_EINVAL;
   if (c->clock_avg_half < 0 || c->clock_avg_half > 2048) return RX_EINVAL;
   if (c->history_buffers < 3 || c->history_buffers > 64) return RX_EINVAL;
+  if (c->input_format != RX_IN_U12_IN_U16 && c->input_format != RX_IN_F32) return RX_EINVAL;
   if (c->lms_batch_segments < 0 || c->lms_batch_segments > (1 << 16)) return RX_EINVAL;
   if (c->family == RX_QAM_KK && !(c->sideband == 1 || c->sideband == -1)) return RX_EINVAL;
   if (c->family == RX_PAM && c->thresholds) {
@@ -385,7 +382,8 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   h->max_call = (long long)(HB - 2) * c.buffer_blocks * 512;
   h->hist_cap = next_pow2(h->max_call + (1 << 18));   // > max call + clock lookback + kept tail
   d.hist_cap = h->hist_cap;
-  TRY(dalloc(h, &d.hist, d.hist_cap));
+  if (c.input_format == RX_IN_F32) TRY(dalloc(h, &d.histf, d.hist_cap));
+  else TRY(dalloc(h, &d.hist, d.hist_cap));
   d.blk_cap = next_pow2((long long)HB * c.buffer_blocks + 256);
   d.buf_cap = 64;
   // equaliser batch + the seed-blocked tail that may wait for the next batch (<= D epochs)
@@ -430,6 +428,7 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   TRY(dalloc(h, &d.sync_g, 2 * RX_PREF));
   TRY(dalloc(h, &d.sync_c, 2 * RX_PREF));
   TRY(dalloc(h, &d.w_train, RX_MAX_K));
+  TRY(dalloc(h, &d.w_init, RX_MAX_K));
   d.seed_cap = 64;
   TRY(dalloc(h, &d.seed, d.seed_cap * RX_MAX_K));
   TRY(dalloc(h, &d.seed_ready, d.seed_cap));
@@ -697,7 +696,25 @@ static void run_kk(rx_handle *h, cudaStream_t s, const InView &in, unsigned char
   launch_lms_rounds(h, s, labels, lab_cap, flush, q_front / 2 + 1);
 }
 
-extern "C" rx_status rx_process(rx_handle *h, const unsigned short *d_samples, long long n,
+static InView make_view(const rx_handle *h, const void *samples, long long n) {
+  InView in;
+  const bool f32 = h->cfg.input_format == RX_IN_F32;
+  in.cur = f32 ? nullptr : (const uint16_t *)samples;
+  in.curf = f32 ? (const float *)samples : nullptr;
+  in.call_start = h->n_in;
+  in.call_end = h->n_in + n;
+  in.hist = h->d.hist;
+  in.histf = h->d.histf;
+  in.hist_cap = h->hist_cap;
+  in.hist_w = h->d.hist;
+  in.histf_w = h->d.histf;
+  in.keep_from = n > 0 ? h->n_in + n - (1 << 16) : h->n_in;
+  in.f32 = f32;
+  in.gain = (float)h->cfg.adc_gain;
+  return in;
+}
+
+extern "C" rx_status rx_process(rx_handle *h, const void *d_samples, long long n,
                                 unsigned char *d_labels, long long labels_capacity, void *stream) {
   if (!h || n < 0 || (n > 0 && !d_samples) || n % 512 || labels_capacity < 0) return RX_EINVAL;
   if (n > h->max_call) return RX_EINVAL;
@@ -706,14 +723,7 @@ extern "C" rx_status rx_process(rx_handle *h, const unsigned short *d_samples, l
   if (h->flushed) return RX_ESTATE;
   CK(cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)stream;
-  InView in;
-  in.cur = d_samples;
-  in.call_start = h->n_in;
-  in.call_end = h->n_in + n;
-  in.hist = h->d.hist;
-  in.hist_cap = h->hist_cap;
-  in.hist_w = h->d.hist;
-  in.keep_from = h->n_in + n - (1 << 16);
+  const InView in = make_view(h, d_samples, n);
   h->n_in += n;
   if (h->d.family == RX_PAM) run_pam(h, s, in, labels_capacity ? d_labels : nullptr, labels_capacity ? labels_capacity : 1, 0);
   else run_kk(h, s, in, labels_capacity ? d_labels : nullptr, labels_capacity ? labels_capacity : 1, 0);
@@ -725,14 +735,7 @@ extern "C" rx_status rx_flush(rx_handle *h, unsigned char *d_labels, long long l
   if (h->flushed) return RX_ESTATE;
   CK(cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)stream;
-  InView in;
-  in.cur = nullptr;
-  in.call_start = h->n_in;
-  in.call_end = h->n_in;
-  in.hist = h->d.hist;
-  in.hist_cap = h->hist_cap;
-  in.hist_w = h->d.hist;
-  in.keep_from = h->n_in;
+  const InView in = make_view(h, nullptr, 0);
   if (h->d.family == RX_PAM) run_pam(h, s, in, labels_capacity ? d_labels : nullptr, labels_capacity ? labels_capacity : 1, 1);
   else run_kk(h, s, in, labels_capacity ? d_labels : nullptr, labels_capacity ? labels_capacity : 1, 1);
   h->flushed = true;
@@ -787,6 +790,22 @@ extern "C" rx_status rx_get_taps(rx_handle *h, double *out, int capacity) {
     if (kk) { out[2 * k] = w[k].x; out[2 * k + 1] = w[k].y; }
     else out[k] = w[k].x;
   }
+  return RX_OK;
+}
+
+extern "C" rx_status rx_set_taps(rx_handle *h, const double *in, int n) {
+  if (!h || !in) return RX_EINVAL;
+  const bool kk = h->d.family == RX_QAM_KK;
+  if (n != (kk ? 2 * h->d.K : h->d.K)) return RX_EINVAL;
+  CK(cudaSetDevice(h->device));
+  CK(cudaDeviceSynchronize());
+  DevState st;
+  CK(cudaMemcpy(&st, h->st_dev, sizeof(st), cudaMemcpyDeviceToHost));
+  if (st.trained) return RX_ESTATE;
+  float2 w[RX_MAX_K];
+  for (int k = 0; k < h->d.K; ++k) w[k] = kk ? make_float2((float)in[2 * k], (float)in[2 * k + 1]) : make_float2((float)in[k], 0.f);
+  CK(cudaMemcpy(h->d.w_init, w, sizeof(float2) * h->d.K, cudaMemcpyHostToDevice));
+  h->d.has_winit = 1;
   return RX_OK;
 }
 

@@ -79,7 +79,7 @@ struct RxDev {
   const unsigned char *ref_idx;  // reference level index (PAM i, QAM iI | iQ << 4) [P]
   const float2 *bps_rot;     // e^{-j phi_p}, p < Pt
   // ---- rings
-  uint16_t *hist; long long hist_cap;
+  uint16_t *hist; float *histf; long long hist_cap;
   double2 *C; double *theta; double *tau; long long *Mb; double *blk_sum; double *blk_abs;
   long long blk_cap;
   float *u; float *uhat; long long sym_cap;
@@ -94,6 +94,8 @@ struct RxDev {
   float *sync_g; float2 *sync_c;
   // ---- LMS
   float2 *w_train;                 // [K]
+  float2 *w_init;                  // [K] start taps of training (rx_set_taps)
+  int has_winit;
   float2 *seed; int *seed_ready; long long seed_cap;   // per epoch [K]
   float2 *seg_w; float *seg_theta; int *seg_done; int *seg_stitched; int *seg_r; int *seg_R;
   double *seg_evm; long long *seg_err; long long seg_cap;

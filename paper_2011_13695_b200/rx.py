@@ -15,6 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.path.join(HERE, "librx.so")
 
 RX_PAM, RX_QAM_KK = 0, 1
+RX_IN_U12_IN_U16, RX_IN_F32 = 0, 1
 PROBES = dict(C=0, TAU=1, MB=2, U=3, UHAT=4, E=5, Z=6, CFO=7, Y=8, LEVEL=9, SEG=10, DEBUG=11)
 FLAGS = dict(DOMAIN=1, SYNC=2, DIVERGE=4, CAPACITY=8)
 
@@ -41,6 +42,7 @@ class RxConfig(ctypes.Structure):
         ("sync_start", _c_ll), ("sync_window", ctypes.c_int), ("sync_min_corr", ctypes.c_double),
         ("warmup_symbols", _c_ll), ("history_buffers", ctypes.c_int),
         ("lms_batch_segments", ctypes.c_int),
+        ("input_format", ctypes.c_int),
     ]
 
 
@@ -59,7 +61,8 @@ class RxStats(ctypes.Structure):
 
 EXPORTS = ("rx_config_default", "rx_create", "rx_process", "rx_flush", "rx_get_stats",
            "rx_reset_stats", "rx_get_taps", "rx_probe_read", "rx_destroy", "rx_strerror",
-           "rx_version", "rx_profile_enable", "rx_profile_read", "rx_export_counters")
+           "rx_version", "rx_profile_enable", "rx_profile_read", "rx_export_counters",
+           "rx_set_taps")
 NCOUNTERS = 8
 COUNTERS = ("bit_errors", "bits", "symbols_counted", "evm_num", "evm_den", "clipped",
             "domain_errors", "symbols_out")
@@ -86,6 +89,7 @@ def load(path: str = SO_PATH):
     lib.rx_get_stats.argtypes = [vp, ctypes.POINTER(RxStats), vp]
     lib.rx_reset_stats.argtypes = [vp, vp]
     lib.rx_get_taps.argtypes = [vp, _c_dp, ctypes.c_int]
+    lib.rx_set_taps.argtypes = [vp, _c_dp, ctypes.c_int]
     lib.rx_probe_read.argtypes = [vp, ctypes.c_int, _c_ll, _c_ll, vp, vp]
     lib.rx_destroy.argtypes = [vp]
     lib.rx_destroy.restype = None
@@ -98,7 +102,7 @@ def load(path: str = SO_PATH):
     lib.rx_export_counters.restype = ctypes.c_int
     lib.rx_profile_read.argtypes = [vp, _c_dp, ctypes.POINTER(_c_ll), ctypes.c_int]
     for f in ("rx_create", "rx_process", "rx_flush", "rx_get_stats", "rx_reset_stats",
-              "rx_get_taps", "rx_probe_read", "rx_profile_enable", "rx_profile_read"):
+              "rx_get_taps", "rx_set_taps", "rx_probe_read", "rx_profile_enable", "rx_profile_read"):
         getattr(lib, f).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -163,8 +167,12 @@ class Receiver:
 
     # -- streaming
     def process(self, samples, labels=None, stream=None):
-        """samples: torch uint16/int16 CUDA tensor of u12 codes; labels: uint8 CUDA tensor
-        written at index m % len(labels)."""
+        """samples: torch uint16/int16 CUDA tensor of u12 codes (RX_IN_U12_IN_U16) or float32
+        (RX_IN_F32), per the handle's input_format; labels: uint8 CUDA tensor written at index
+        m % len(labels)."""
+        want = 4 if self.cfg.input_format == RX_IN_F32 else 2
+        if samples.element_size() != want:
+            raise ValueError(f"input_format {self.cfg.input_format} needs {want}-byte samples")
         lp, lc = (labels.data_ptr(), labels.numel()) if labels is not None else (None, 0)
         _check(load().rx_process(self._h, ctypes.c_void_p(samples.data_ptr()), samples.numel(),
                                  ctypes.c_void_p(lp), lc, _stream_ptr(stream)), "rx_process")
@@ -197,6 +205,16 @@ class Receiver:
         out = np.zeros(n, dtype=np.float64)
         _check(load().rx_get_taps(self._h, out.ctypes.data_as(_c_dp), n), "rx_get_taps")
         return out[0::2] + 1j * out[1::2] if self.family == RX_QAM_KK else out
+
+    def set_taps(self, w) -> None:
+        """Start taps of the training pass (rx_set_taps); K real (PAM) or K complex (KK)."""
+        w = np.asarray(w)
+        if self.family == RX_QAM_KK:
+            buf = np.empty(2 * w.size, dtype=np.float64)
+            buf[0::2], buf[1::2] = w.real, w.imag
+        else:
+            buf = np.ascontiguousarray(w.real, dtype=np.float64)
+        _check(load().rx_set_taps(self._h, buf.ctypes.data_as(_c_dp), int(buf.size)), "rx_set_taps")
 
     def probe(self, which: str, first: int, count: int, stream=None) -> np.ndarray:
         w = PROBES[which]

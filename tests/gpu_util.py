@@ -10,7 +10,8 @@ from oracle import rx_oracle as O
 
 RX_FIELDS = ("lms_taps", "lms_block", "lms_segment", "lms_overlap", "mu", "train_symbols",
              "sync_start", "sync_window", "warmup_symbols", "cpr_test_phases", "tap_lag_epochs",
-             "sync_min_corr", "buffer_blocks", "clock_avg_half", "cfo_enable", "lms_batch_segments")
+             "sync_min_corr", "buffer_blocks", "clock_avg_half", "cfo_enable", "lms_batch_segments",
+             "input_format")
 
 
 def oracle_params(rec, rx) -> O.RxParams:
@@ -24,9 +25,10 @@ def run_oracle(rec, rx):
     return O.receive_pam(rec.codes, p) if rec.fmt == "pam" else O.receive_kk(rec.codes, p)
 
 
-def run_gpu(rec, rx, chunk=1 << 22, history_buffers=None, device=0, keep=True):
+def run_gpu(rec, rx, chunk=1 << 22, history_buffers=None, device=0, keep=True, pre=None):
     """Stream the record through librx in `chunk`-sample calls, flush, return (Receiver,
-    labels numpy, stats)."""
+    labels numpy, stats). rx["input_format"] = 1 streams x = (code - 2047.5)/2047.5 as float32;
+    ``pre(R)`` runs before the first call (e.g. rx_set_taps)."""
     import torch
     from paper_2011_13695_b200 import RX_PAM, RX_QAM_KK, Receiver
     fam = RX_PAM if rec.fmt == "pam" else RX_QAM_KK
@@ -38,7 +40,13 @@ def run_gpu(rec, rx, chunk=1 << 22, history_buffers=None, device=0, keep=True):
     if fam == RX_QAM_KK:
         fields["dc_offset"] = rec.dc_offset
     R = Receiver(fam, rec.M, rec.static_taps, device=device, **fields)
-    codes = torch.from_numpy(rec.codes.view(np.int16)).to(f"cuda:{device}")
+    if fields.get("input_format", 0) == 1:
+        x = ((rec.codes.astype(np.float64) - 2047.5) / 2047.5).astype(np.float32)
+        codes = torch.from_numpy(x).to(f"cuda:{device}")
+    else:
+        codes = torch.from_numpy(rec.codes.view(np.int16)).to(f"cuda:{device}")
+    if pre is not None:
+        pre(R)
     nsym_ub = rec.n // (2 if fam == RX_PAM else 4) + 4096
     labels = torch.full((nsym_ub,), 0xFF, dtype=torch.uint8, device=f"cuda:{device}")
     for off in range(0, rec.n, chunk):

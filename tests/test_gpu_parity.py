@@ -171,3 +171,43 @@ def test_chunking_invariance():
         assert sa[k] == sb[k] == sc[k], k
     assert sa["evm_num"] == sc["evm_num"]                        # run-to-run bit identical
     assert abs(sa["evm_num"] - sb["evm_num"]) <= 1e-9 * sa["evm_num"]
+
+
+def test_f32_input_matches_u16():
+    """RX_IN_F32 (x already in x units) reproduces the u16 path: same labels and counters up to
+    threshold flips, fields within fp32 rounding (SURVEY §8(b) rx_input_format)."""
+    _torch_cuda()
+    rec, rx = make_config("C3", n_samples=1 << 20)
+    rx["buffer_blocks"] = 256
+    out = run_oracle(rec, rx)
+    Ra, la, sa = run_gpu(rec, rx, chunk=256 * 512)
+    rxf = dict(rx, input_format=1)
+    Rb, lb, sb = run_gpu(rec, rxf, chunk=256 * 512)
+    m_end = out["m_end"]
+    assert rel_l2(Rb.probe("E", 0, 4096), out["E"][:4096]) < TOL_FIELD
+    mism, excl = _compare_labels(rec, rx, out, lb)
+    _compare_counters(rec, out, sb, mism)
+    assert sb["clipped"] == 0
+    assert np.mean(la[:m_end] != lb[:m_end]) <= 1e-3
+
+
+def test_set_taps_warm_start():
+    """rx_set_taps replaces the centre spike as the training start (c-9): the trained taps
+    follow the oracle run from the same start; after training the call is refused."""
+    torch = _torch_cuda()
+    from paper_2011_13695_b200 import RxError
+    rec, rx = make_config("C1")
+    K = rx["lms_taps"]
+    w0 = np.zeros(K)
+    w0[K // 2] = 0.8
+    w0[K // 2 - 1] = 0.15
+    w0[K // 2 + 1] = -0.1
+    p = O.RxParams(**{**{k: v for k, v in rx.items() if k in O.RxParams.__dataclass_fields__},
+                      "fmt": rec.fmt, "M": rec.M, "static_taps": rec.static_taps,
+                      "dc_offset": rec.dc_offset, "w_init": w0})
+    out = O.receive_pam(rec.codes, p)
+    R, labels, st = run_gpu(rec, rx, pre=lambda R: R.set_taps(w0))
+    assert rel_l2(R.train_taps(), out["lms"]["w_train"]) < 1e-3
+    mism, excl = _compare_labels(rec, rx, out, labels)
+    with pytest.raises(RxError):
+        R.set_taps(w0)
