@@ -3,7 +3,7 @@
 //  k_pam_fe     H0-H3  ingest + overlap framing + R2C FFT-1024 + static FD EQ + C_b
 //  k_pam_theta/carry/tau  H4  105-block complex average + atan2 + unwrap as a prefix sum of
 //                      wrapped differences (tile-local scans, one-CTA carry scan) -> tau_b, M_b
-//  k_pam_be     H1,H2,H5-H7  re-FFT + EQ + FD clock correction + C2R IFFT + extraction
+//  k_pam_be     H2,H5-H7  stored spectrum + EQ + FD clock correction + C2R IFFT + extraction
 //  k_norm_*     H8     buffer-wise DC / amplitude normalisation (stats + apply)
 #pragma once
 #include "fft.cuh"
@@ -111,11 +111,15 @@ __global__ void __launch_bounds__(256) k_pam_fe(RxDev d, InView in, long long b0
   float cr = 0.f, ci = 0.f;
   if (act) {
     const float2 *pm = fft_mirror_base(buf[g], j);
+    float2 *xs = d.Xspec + rmod(b, d.xs_cap) * 512;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int k = j + 64 * r;
       float2 Xk, Xn;
       r2c_pair(v[r], fft_partner(pm, j, r, v), tw[k], Xk, Xn);
+      // X for k_pam_be (slot 0 packs the real X[0], X[512]; slot k < 512 holds X[k])
+      if (k == 0) xs[0] = make_float2(Xk.x, Xn.x);
+      else { xs[k] = Xk; xs[512 - k] = Xn; }
       float2 Yk, Yn;
       if (HREAL) { Yk = cscale(Xk, __ldg(d.Hr + k)); Yn = cscale(Xn, __ldg(d.Hr + 512 - k)); }
       else { Yk = cmul(Xk, __ldg(d.H + k)); Yn = cmul(Xn, __ldg(d.H + 512 - k)); }
@@ -127,6 +131,7 @@ __global__ void __launch_bounds__(256) k_pam_fe(RxDev d, InView in, long long b0
     }
     if (j == 0) {
       const float2 Z = v[4];                                   // X[256] = conj Z[256]
+      xs[256] = cconj(Z);
       const float2 Y = HREAL ? cscale(cconj(Z), __ldg(d.Hr + 256)) : cmul(cconj(Z), __ldg(d.H + 256));
       cr = fmaf(Y.x, Y.x, fmaf(-Y.y, Y.y, cr));
       ci = fmaf(2.f * Y.x, Y.y, ci);
@@ -302,7 +307,7 @@ __global__ void __launch_bounds__(256) k_pam_tau(RxDev d, long long b0, long lon
 
 // ------------------------------------------------------------------ H1, H2, H5-H7
 template <bool HREAL>
-__global__ void __launch_bounds__(256) k_pam_be(RxDev d, InView in, long long b0, long long b1) {
+__global__ void __launch_bounds__(256) k_pam_be(RxDev d, long long b0, long long b1) {
   __shared__ float2 tw[1024];
   __shared__ float2 buf[FE_GROUPS][FFT_PAD_N];
   __shared__ double red[FE_GROUPS][2];
@@ -310,14 +315,21 @@ __global__ void __launch_bounds__(256) k_pam_be(RxDev d, InView in, long long b0
   for (int i = threadIdx.x; i < 1024; i += blockDim.x) tw[i] = d.tw[i];
   const long long b = b0 + (long long)blockIdx.x * FE_GROUPS + g;
   const bool act = b < b1;
-  float2 v[8];
-  if (act) load_block_regs(in, b, d.scale, j, v);
-  else {
+  // the block's spectrum X stored by k_pam_fe (SURVEY §8(a) 'read back spectra' option):
+  // thread j owns the pairs (k, 512 - k), k = j + 64 r, r < 4, and thread 0 also X[256]
+  float2 Xk_[4], Xn_[4], X256 = make_float2(0.f, 0.f);
+  {
+    const float2 *xs = d.Xspec + rmod(act ? b : b0, d.xs_cap) * 512;
 #pragma unroll
-    for (int r = 0; r < 8; ++r) v[r] = make_float2(0.f, 0.f);
+    for (int r = 0; r < 4; ++r) {
+      const int k = j + 64 * r;
+      const float2 a = act ? xs[k] : make_float2(0.f, 0.f);
+      const float2 c = act ? xs[(512 - k) & 511] : make_float2(0.f, 0.f);
+      if (k == 0) { Xk_[r] = make_float2(a.x, 0.f); Xn_[r] = make_float2(a.y, 0.f); }
+      else { Xk_[r] = a; Xn_[r] = c; }
+    }
+    if (j == 0 && act) X256 = xs[256];
   }
-  fft512_regs<false>(buf[g], j, tw, v);
-  fft512_publish_upper(buf[g], j, v);
   // clock phase of this block: s = 2 tau, i_b = rint(s), f_b = s - i_b   (c-4)
   const double tau = act ? d.tau[rmod(b, d.blk_cap)] : 0.0;
   const double sd = 2.0 * tau;
@@ -330,12 +342,10 @@ __global__ void __launch_bounds__(256) k_pam_be(RxDev d, InView in, long long b0
   sincospif(f * 0.125f, &step.y, &step.x);
   sincospif(f, &nyq.y, &nyq.x);
   float2 Zk[4], Zn[4], Z256;
-  const float2 *pm = fft_mirror_base(buf[g], j);
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     const int k = j + 64 * r;
-    float2 Xk, Xn;
-    r2c_pair(v[r], fft_partner(pm, j, r, v), tw[k], Xk, Xn);
+    const float2 Xk = Xk_[r], Xn = Xn_[r];
     float2 Yk, Yn;
     if (HREAL) { Yk = cscale(Xk, __ldg(d.Hr + k)); Yn = cscale(Xn, __ldg(d.Hr + 512 - k)); }
     else { Yk = cmul(Xk, __ldg(d.H + k)); Yn = cmul(Xn, __ldg(d.H + 512 - k)); }
@@ -346,8 +356,7 @@ __global__ void __launch_bounds__(256) k_pam_be(RxDev d, InView in, long long b0
     rot = cmul(rot, step);
   }
   {
-    const float2 Z = v[4];
-    float2 Y = HREAL ? cscale(cconj(Z), __ldg(d.Hr + 256)) : cmul(cconj(Z), __ldg(d.H + 256));
+    float2 Y = HREAL ? cscale(X256, __ldg(d.Hr + 256)) : cmul(X256, __ldg(d.H + 256));
     float2 r256;
     sincospif(0.5f * f, &r256.y, &r256.x);
     Z256 = cconj(cmul(Y, r256));
@@ -364,6 +373,7 @@ __global__ void __launch_bounds__(256) k_pam_be(RxDev d, InView in, long long b0
     if (j == 0) buf[g][256 + (256 >> 4)] = Z256;
   }
   __syncthreads();
+  float2 v[8];
   fft512<true>(buf[g], j, tw, v);
   fft512_store(buf[g], j, v);
   // variable-rate extraction (c-4): u_m = y[2m + i_b - 512b + 512], m in [max(M_b,0), M_{b+1})

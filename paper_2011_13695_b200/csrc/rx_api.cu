@@ -385,6 +385,10 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   if (c.input_format == RX_IN_F32) TRY(dalloc(h, &d.histf, d.hist_cap));
   else TRY(dalloc(h, &d.hist, d.hist_cap));
   d.blk_cap = next_pow2((long long)HB * c.buffer_blocks + 256);
+  if (!kk) {   // spectra from k_pam_fe to k_pam_be: one call + the clock look-ahead
+    d.xs_cap = next_pow2((long long)(HB - 2) * c.buffer_blocks + 2 * c.clock_avg_half + 64);
+    TRY(dalloc(h, &d.Xspec, d.xs_cap * 512));
+  }
   d.buf_cap = 64;
   // equaliser batch + the seed-blocked tail that may wait for the next batch (<= D epochs)
   const long long E_sym = (long long)c.buffer_blocks * (kk ? 128 : 256);
@@ -634,8 +638,8 @@ static void run_pam(rx_handle *h, cudaStream_t s, const InView &in, unsigned cha
   }
   long long be_target = flush ? h->fe_done - 1 : h->clk_done - 1;
   if (be_target > h->be_done) {
-    if (d.H_real) KLAUNCH(h, RX_K_PAM_BE, s, (k_pam_be<true><<<gridc(be_target - h->be_done, FE_GROUPS), 256, 0, s>>>(d, in, h->be_done, be_target)));
-    else KLAUNCH(h, RX_K_PAM_BE, s, (k_pam_be<false><<<gridc(be_target - h->be_done, FE_GROUPS), 256, 0, s>>>(d, in, h->be_done, be_target)));
+    if (d.H_real) KLAUNCH(h, RX_K_PAM_BE, s, (k_pam_be<true><<<gridc(be_target - h->be_done, FE_GROUPS), 256, 0, s>>>(d, h->be_done, be_target)));
+    else KLAUNCH(h, RX_K_PAM_BE, s, (k_pam_be<false><<<gridc(be_target - h->be_done, FE_GROUPS), 256, 0, s>>>(d, h->be_done, be_target)));
     h->be_done = be_target;
   }
   {

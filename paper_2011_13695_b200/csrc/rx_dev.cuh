@@ -80,6 +80,7 @@ struct RxDev {
   const float2 *bps_rot;     // e^{-j phi_p}, p < Pt
   // ---- rings
   uint16_t *hist; float *histf; long long hist_cap;
+  float2 *Xspec; long long xs_cap;      // PAM: R2C spectra of blocks [be_done, fe_done), 512 float2 each
   double2 *C; double *theta; double *tau; long long *Mb; double *blk_sum; double *blk_abs;
   long long blk_cap;
   float *u; float *uhat; long long sym_cap;
