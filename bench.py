@@ -46,7 +46,7 @@ SM_COUNT, FP32_LANES = 148, 128   # B200 (B200_PROFILING.md); FP32 FMA = 2 flop
 FFT_R1024 = 2.5 * 1024 * 10
 FLOPS_PER_UNIT = {
     "PAM_FE": FFT_R1024 + 513 * 6 + 512 * 8,               # per block
-    "PAM_BE": 2 * FFT_R1024 + 2 * 513 * 6,                 # per block
+    "PAM_BE": FFT_R1024 + 2 * 513 * 6,                     # per block (C2R; R2C counted in PAM_FE)
     "KK_S1": 2 * FFT_R1024 + 512 * 20,                     # per block
     "KK_S2": 5 * 1024 * 10 + 512 * 6 + 5 * 512 * 9,        # per block
 }
@@ -358,8 +358,12 @@ def gpu_main(args):
         v4 = N_C4 * args.kk_steps / (r4["ms"] / 1e3) / 1e9
         dom4 = r4["dominant"]
         kk_roof = None
-        if dom4 and dom4["name"] in FLOPS_PER_UNIT:
-            a4 = FLOPS_PER_UNIT[dom4["name"]] * (N_C4 // 512) * args.kk_steps / (dom4["ms"] / 1e3) / 1e12
+        if dom4 and (dom4["name"] in FLOPS_PER_UNIT or dom4["name"] == "LMS"):
+            if dom4["name"] == "LMS":   # 16K flop per complex T/2 symbol + BPS 17 flop per test phase
+                f4 = (16 * rx4["lms_taps"] + 17 * rx4["cpr_test_phases"]) * (N_C4 // 4)
+            else:
+                f4 = FLOPS_PER_UNIT[dom4["name"]] * (N_C4 // 512)
+            a4 = f4 * args.kk_steps / (dom4["ms"] / 1e3) / 1e12
             kk_roof = {"kernel_class": dom4["name"], "bound": "alu", "achieved": a4, "peak": peak_fp32,
                        "unit": "TFLOP/s", "frac": a4 / peak_fp32, "share_of_step": dom4["ms"] / r4["ms"]}
         elif dom4:
