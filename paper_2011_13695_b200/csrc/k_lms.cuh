@@ -320,6 +320,7 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
   const float two_s = CPLX ? 2.0f * d.qam_sc : 2.0f / (float)(d.M - 1);
   const float lvl0 = CPLX ? -(float)(L - 1) * d.qam_sc : -1.0f;
   const float inv2s = 1.0f / two_s;
+  const float Lh = 0.5f * (float)L, Lm1 = (float)(L - 1);
   const long long o_ref = d.st->sync_offset;
   const int ref0 = MODE == 0 ? (int)(((o_ref + t_begin - d.m0) % RX_PREF + RX_PREF) % RX_PREF) : 0;
   float2 rotA = make_float2(1.f, 0.f), rotB = make_float2(1.f, 0.f);
@@ -345,6 +346,10 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
   const long long nblk = (t_end - t_begin + 31) / 32;
   constexpr int WLa = (WL + 3) & ~3;        // first stage rounded up: later stages stay 4-aligned
   const bool vec = !CPLX && (wb0 & 3) == 0;
+  // PAM fast staging: every staged index of the run lies in [0, vend): 16-byte copies with
+  // 32-bit ring arithmetic, the mirror copy only for the slots a window can wrap onto (< 64)
+  const bool fast = vec && wb0 >= 0 && wb0 + WLa + DS * nblk <= vend;
+  const int gbase = (int)(wb0 & (d.sym_cap - 1)), gmask = (int)(d.sym_cap - 1);
   lms_stage_any<CPLX>(d, sm, wb0, wb0 + WLa, vend, wb0, vec);
   cp_async_commit();
 #pragma unroll 1
@@ -353,16 +358,25 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
     cp_async_commit();
   }
   bool first = true;
-  long long wb = wb0;
+  // 32-bit offsets relative to t_begin inside the loop (a run spans < 2^31 symbols)
+  const int nsym = (int)(t_end - t_begin);
+  auto rel_of = [&](long long a) -> int {
+    const long long r = a - t_begin;
+    return r < -(1 << 30) ? -(1 << 30) : (r > (1 << 30) ? (1 << 30) : (int)r);
+  };
+  const int olo = rel_of(out_lo), wmr = rel_of(d.warmup), wlo = olo - d.O;
+  const int smask = (int)(d.sym_cap - 1), mb0 = (int)(t_begin & (d.sym_cap - 1));
+  float evn_f = 0.f, evd_f = 0.f;
+  const int nblk32 = (int)nblk;
 #pragma unroll 1
-  for (long long jb = 0; jb < nblk; ++jb) {
-    const long long t = t_begin + 32 * jb;
+  for (int jb = 0; jb < nblk32; ++jb) {
+    const int rb = 32 * jb;                  // block start relative to t_begin
     cp_async_wait<LMS_AHEAD - 1>();
     __syncwarp();
-    const int nvalid = (int)((t_end - t) < 32 ? (t_end - t) : 32);
+    const int nvalid = nsym - rb < 32 ? nsym - rb : 32;
     const bool valid = io < nvalid;
-    const long long m = t + io;
-    const T *win = sm.ring + (int)((wb - wb0) & (LMS_RING - 1));   // contiguous window (mirror)
+    const int mr = rb + io;                  // this lane's symbol, relative
+    const T *win = sm.ring + ((DS * jb) & (LMS_RING - 1));   // contiguous window (mirror)
     // y_i = w^H u_i, u_i[k] = win[stride i + KP-1-k]
     float2 y;
     if constexpr (TILED) {
@@ -405,7 +419,7 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
     float2 e, zp = y;
     int code = 0;
     if (MODE == 0) {
-      int ri = ref0 + (int)(m - t_begin);
+      int ri = ref0 + mr;
       while (ri >= RX_PREF) ri -= RX_PREF;
       const float2 r = __ldg(d.ref_val + ri);
       e = CPLX ? csub(r, y) : make_float2(r.x - y.x, 0.f);
@@ -456,28 +470,37 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
         __sincosf(theta - 6.283185307179586f * rintf(theta * 0.15915494309189535f), &sth, &cth);
         zp = cmul(y, make_float2(cth, -sth));
       }
+      // slicing in the float domain (level index = clamp(floor(v / 2s + L/2)), same value as
+      // slice_axis) keeps the integer conversion off the error's dependency chain
       float2 dv;
       if (CPLX) {
-        const int iI = slice_axis(zp.x, inv2s, L), iQ = slice_axis(zp.y, inv2s, L);
-        code = iI | (iQ << 4);
-        dv = make_float2(level_of(iI, two_s, lvl0), level_of(iQ, two_s, lvl0));
+        const float fI = fminf(fmaxf(floorf(fmaf(zp.x, inv2s, Lh)), 0.f), Lm1);
+        const float fQ = fminf(fmaxf(floorf(fmaf(zp.y, inv2s, Lh)), 0.f), Lm1);
+        dv = make_float2(fmaf(fI, two_s, lvl0), fmaf(fQ, two_s, lvl0));
         e = cmul(csub(dv, zp), make_float2(cth, sth));
+        code = (int)fI | ((int)fQ << 4);
+      } else if (d.thr_default) {
+        const float fi = fminf(fmaxf(floorf(fmaf(zp.x, inv2s, Lh)), 0.f), Lm1);
+        dv = make_float2(fmaf(fi, two_s, lvl0), 0.f);
+        e = make_float2(dv.x - zp.x, 0.f);
+        code = (int)fi;
       } else {
-        const int i = d.thr_default ? slice_axis(zp.x, inv2s, L) : slice_pam(d, zp.x);
+        const int i = slice_pam(d, zp.x);
         code = i;
         dv = make_float2(level_of(i, two_s, lvl0), 0.f);
         e = make_float2(dv.x - zp.x, 0.f);
       }
-      if (valid && m >= out_lo) {
-        d.level[rmod(m, d.sym_cap)] = (unsigned char)code;
-        d.yout[rmod(m, d.sym_cap)] = zp;
-        if (m >= d.warmup) {
+      if (valid && mr >= olo) {
+        const int ix = (mb0 + mr) & smask;
+        d.level[ix] = (unsigned char)code;
+        d.yout[ix] = zp;
+        if (mr >= wmr) {
           const float ex = dv.x - zp.x, ey = dv.y - zp.y;
-          evn += (double)fmaf(ex, ex, ey * ey);
-          evd += (double)fmaf(dv.x, dv.x, dv.y * dv.y);
+          evn_f = fmaf(ex, ex, fmaf(ey, ey, evn_f));
+          evd_f = fmaf(dv.x, dv.x, fmaf(dv.y, dv.y, evd_f));
         }
       } else if (valid && warm) {
-        warm[m - (out_lo - d.O)] = (unsigned char)code;
+        warm[mr - wlo] = (unsigned char)code;
       }
     }
     if (!valid) e = make_float2(0.f, 0.f);
@@ -536,14 +559,32 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
     else reinterpret_cast<float *>(sm.w)[io] = wk.x;
     __syncwarp();
     // stage the new samples of block jb + AHEAD (the slots of block jb are no longer read)
-    const long long jn = jb + LMS_AHEAD;
-    if (jn < nblk) lms_stage_any<CPLX>(d, sm, wb0 + WLa + (jn - 1) * DS, wb0 + WLa + jn * DS, vend, wb0, vec);
+    const int jn = jb + LMS_AHEAD;
+    if constexpr (!CPLX) {
+      if (fast) {
+        if (jn < nblk && lane < 8) {
+          const int rel = WLa + (jn - 1) * DS + 4 * lane;
+          const int slot = rel & (LMS_RING - 1);
+          const float *src = d.uhat + ((gbase + rel) & gmask);
+          const unsigned sa = (unsigned)__cvta_generic_to_shared(&sm.ring[slot]);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src));
+          if (slot < 64) {
+            const unsigned sb = (unsigned)__cvta_generic_to_shared(&sm.ring[slot + LMS_RING]);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sb), "l"(src));
+          }
+        }
+      } else if (jn < nblk) {
+        lms_stage_any<CPLX>(d, sm, wb0 + WLa + (long long)(jn - 1) * DS, wb0 + WLa + (long long)jn * DS, vend, wb0, vec);
+      }
+    } else if (jn < nblk) {
+      lms_stage_any<CPLX>(d, sm, wb0 + WLa + (long long)(jn - 1) * DS, wb0 + WLa + (long long)jn * DS, vend, wb0, vec);
+    }
     cp_async_commit();
-    wb += DS;
     first = false;
-
   }
   cp_async_wait<0>();
+  evn += (double)evn_f;
+  evd += (double)evd_f;
   if (TILED) wk.x = reinterpret_cast<const float *>(sm.w)[lane];   // back to lane = tap order
   const float nrm = warp_sum(lane < K ? cabs2(wk) : 0.f);
   if (lane == 0 && nrm > 1e6f) set_flag(d.st, RX_FLAG_DIVERGE);
