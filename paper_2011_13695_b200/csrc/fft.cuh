@@ -56,13 +56,22 @@ __device__ __forceinline__ void dft8(float2 (&v)[8]) {
 }
 
 // In-place FFT-512 of buf (padded, FFT_PAD_N float2) by the 64 threads j = 0..63 of a group.
-// All threads of the CTA must call it (it uses __syncthreads()).
+// All threads of the group (GB = 1) or CTA (GB = 0) must call it.
 // On return thread j holds X[j + 64 r] in v[r]; fft512_store() writes them back.
 // Padded addresses are formed from one per-thread base plus compile-time offsets:
 //   P8(j + 64 r)   = (j + j/16) + 68 r
 //   P8(8 j + r)    = (8 j + j/2) + r                     (r < 8)
 //   P8(B + 8 r)    = (B + B/16) + 8 r + r/2,  B = 64 (j/8) + j%8
-template <bool INV>
+// Barrier of one transform: GB = 0 -> __syncthreads (default); GB = 1 -> only the 64 threads of
+// the group (named barrier 1 + group; measured 3-5% slower on k_pam_fe / k_pam_be than the CTA
+// barrier, kept for experiments; kernels then need a CTA barrier after staging shared tables).
+template <int GB>
+__device__ __forceinline__ void fft_sync() {
+  if constexpr (GB != 0) asm volatile("bar.sync %0, 64;\n" ::"r"(1 + (int)(threadIdx.x >> 6)) : "memory");
+  else __syncthreads();
+}
+
+template <bool INV, int GB = 0>
 __device__ __forceinline__ void fft512_regs(float2 *buf, int j, const float2 *tw, float2 (&v)[8]) {
   // pass-1 input already in registers: v[r] = z[j + 64 r]
   float2 *const pa = buf + j + (j >> 4);
@@ -70,10 +79,10 @@ __device__ __forceinline__ void fft512_regs(float2 *buf, int j, const float2 *tw
   const int B = (j >> 3) * 64 + (j & 7);
   float2 *const pw2 = buf + B + (B >> 4);
   dft8<INV>(v);
-  __syncthreads();
+  fft_sync<GB>();
 #pragma unroll
   for (int r = 0; r < 8; ++r) pw1[r] = v[r];
-  __syncthreads();
+  fft_sync<GB>();
   // pass 2: Ns = 8, twiddle W512^(r k), k = j % 8
   {
     const float2 *t2 = tw + TW_P2 + (j & 7);
@@ -82,10 +91,10 @@ __device__ __forceinline__ void fft512_regs(float2 *buf, int j, const float2 *tw
 #pragma unroll
     for (int r = 1; r < 8; ++r) v[r] = cmul(v[r], twv<INV>(t2, 8 * (r - 1)));
     dft8<INV>(v);
-    __syncthreads();
+    fft_sync<GB>();
 #pragma unroll
     for (int r = 0; r < 8; ++r) pw2[8 * r + (r >> 1)] = v[r];
-    __syncthreads();
+    fft_sync<GB>();
   }
   // pass 3: Ns = 64, twiddle W512^(r j)
   const float2 *t3 = tw + TW_P3 + j;
@@ -97,34 +106,36 @@ __device__ __forceinline__ void fft512_regs(float2 *buf, int j, const float2 *tw
   // result: v[r] = X[j + 64 r]
 }
 
-template <bool INV>
+template <bool INV, int GB = 0>
 __device__ __forceinline__ void fft512(float2 *buf, int j, const float2 *tw, float2 (&v)[8]) {
   const float2 *const pa = buf + j + (j >> 4);
 #pragma unroll
   for (int r = 0; r < 8; ++r) v[r] = pa[68 * r];
-  fft512_regs<INV>(buf, j, tw, v);
+  fft512_regs<INV, GB>(buf, j, tw, v);
 }
 
 // Real-FFT pairing without a full store: bin k = j + 64 r (r < 4) is v[r] of thread j, its
 // partner 512 - k is v[7 - r] of thread (64 - j) % 64, so only v[4..7] are published.
+template <int GB = 0>
 __device__ __forceinline__ void fft512_publish_upper(float2 *buf, int j, const float2 (&v)[8]) {
   float2 *const pa = buf + j + (j >> 4);
-  __syncthreads();
+  fft_sync<GB>();
 #pragma unroll
   for (int q = 4; q < 8; ++q) pa[68 * q] = v[q];
-  __syncthreads();
+  fft_sync<GB>();
 }
 __device__ __forceinline__ float2 fft_partner(const float2 *pm, int j, int r, const float2 (&v)[8]) {
   return (j == 0 && r == 0) ? v[0] : pm[-68 * r];
 }
 
 // Store the pass-3 result back (natural order) — only needed when other threads read it.
+template <int GB = 0>
 __device__ __forceinline__ void fft512_store(float2 *buf, int j, const float2 (&v)[8]) {
   float2 *const pa = buf + j + (j >> 4);
-  __syncthreads();
+  fft_sync<GB>();
 #pragma unroll
   for (int r = 0; r < 8; ++r) pa[68 * r] = v[r];
-  __syncthreads();
+  fft_sync<GB>();
 }
 
 // Mirror addresses used by the real-FFT packing: for k = j + 64 r (r = 0..3) thread j needs

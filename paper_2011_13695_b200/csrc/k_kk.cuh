@@ -17,6 +17,7 @@ __global__ void __launch_bounds__(256) k_kk_s1(RxDev d, InView in, long long b0,
   __shared__ float2 buf[FE_GROUPS][FFT_PAD_N];
   const int g = threadIdx.x >> 6, j = threadIdx.x & 63;
   for (int i = threadIdx.x; i < 1024; i += blockDim.x) tw[i] = d.tw[i];
+  __syncthreads();   // twiddles visible to every group (the FFT barriers are per group)
   const long long b = b0 + (long long)blockIdx.x * FE_GROUPS + g;
   const bool act = b < b1;
   int clip = 0, dom = 0;
@@ -125,6 +126,7 @@ __global__ void __launch_bounds__(256) k_kk_s2(RxDev d, long long b0, long long 
   __shared__ float2 buf[FE_GROUPS][FFT_PAD_N];
   const int g = threadIdx.x >> 6, j = threadIdx.x & 63;
   for (int i = threadIdx.x; i < 1024; i += blockDim.x) tw[i] = d.tw[i];
+  __syncthreads();   // twiddles visible to every group (the FFT barriers are per group)
   const long long b = b0 + (long long)blockIdx.x * FE_GROUPS + g;
   const bool act = b < b1;
   float2 ve[8], vo[8];
@@ -186,6 +188,7 @@ __global__ void __launch_bounds__(1024) k_cfo_spec(RxDev d, long long beta0, lon
   long long qlo, qhi;
   buf_range(d, beta0 + blockIdx.y, qfront, qlo, qhi);
   for (int i = threadIdx.x; i < 1024; i += blockDim.x) tw[i] = d.tw[i];
+  __syncthreads();   // twiddles visible to every group (the FFT barriers are per group)
   const long long nch = (qhi - qlo) / 1024;
   const long long c = (long long)blockIdx.x * CFO_GROUPS + g;
   const bool act = c < nch;
@@ -214,8 +217,8 @@ __global__ void __launch_bounds__(1024) k_cfo_spec(RxDev d, long long beta0, lon
     ve[r] = cmul(a2, a2);
     vo[r] = cmul(b2, b2);
   }
-  fft512_regs<false>(bg, j, tw, ve);
-  fft512_regs<false>(bg, j, tw, vo);      // same buffer: fft512_regs syncs before its first store
+  fft512_regs<false, 0>(bg, j, tw, ve);
+  fft512_regs<false, 0>(bg, j, tw, vo);   // same buffer: fft512_regs syncs before its first store
   __syncthreads();                        // every group done with its FFT buffer
   float *acc = reinterpret_cast<float *>(bufs);
 #pragma unroll

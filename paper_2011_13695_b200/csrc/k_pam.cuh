@@ -94,6 +94,7 @@ __global__ void __launch_bounds__(256) k_pam_fe(RxDev d, InView in, long long b0
   __shared__ double2 red[FE_GROUPS][2];
   const int g = threadIdx.x >> 6, j = threadIdx.x & 63;
   for (int i = threadIdx.x; i < 1024; i += blockDim.x) tw[i] = d.tw[i];
+  __syncthreads();   // twiddles visible to every group (the FFT barriers are per group)
   const long long b = b0 + (long long)blockIdx.x * FE_GROUPS + g;
   const bool act = b < b1;
   int clip = 0;
@@ -313,6 +314,7 @@ __global__ void __launch_bounds__(256) k_pam_be(RxDev d, long long b0, long long
   __shared__ double red[FE_GROUPS][2];
   const int g = threadIdx.x >> 6, j = threadIdx.x & 63;
   for (int i = threadIdx.x; i < 1024; i += blockDim.x) tw[i] = d.tw[i];
+  __syncthreads();   // twiddles visible to every group (the FFT barriers are per group)
   const long long b = b0 + (long long)blockIdx.x * FE_GROUPS + g;
   const bool act = b < b1;
   // the block's spectrum X stored by k_pam_fe (SURVEY §8(a) 'read back spectra' option):
@@ -361,7 +363,6 @@ __global__ void __launch_bounds__(256) k_pam_be(RxDev d, long long b0, long long
     sincospif(0.5f * f, &r256.y, &r256.x);
     Z256 = cconj(cmul(Y, r256));
   }
-  __syncthreads();
   {
     float2 *paw = buf[g] + j + (j >> 4);
     float2 *pmw = buf[g] + (512 - j) + ((512 - j) >> 4);

@@ -22,3 +22,4 @@ done
 timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
   -k "regex:k_lms_seg<.bool.1" -s 4 -c 1 -o gpurun_out/$TAG/prof_kk_k_lms_seg $BK \
   > gpurun_out/$TAG/ncu_full_kk_k_lms_seg.log 2>&1
+python tools/profile_digest.py gpurun_out/$TAG
