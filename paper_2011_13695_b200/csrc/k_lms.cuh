@@ -802,12 +802,18 @@ __device__ __forceinline__ void lms_add_counters(const RxDev &d, long long lo, l
   const int t = threadIdx.x;
   double en = 0.0, ed = 0.0;
   long long er = 0, ct = 0;
-  for (long long s = lo + t; s < hi; s += blockDim.x) {
-    const long long si = rmod(s, d.seg_cap);
-    en += d.seg_evm[2 * si];
-    ed += d.seg_evm[2 * si + 1];
-    er += d.seg_err[2 * si];
-    ct += d.seg_err[2 * si + 1];
+  for (long long s0 = lo + t; s0 < hi; s0 += 4 * (long long)blockDim.x) {   // 4 segments in flight
+    double2 ev[4];
+    longlong2 eg[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long s = s0 + u * (long long)blockDim.x;
+      const long long si = rmod(s, d.seg_cap);
+      ev[u] = s < hi ? reinterpret_cast<const double2 *>(d.seg_evm)[si] : make_double2(0.0, 0.0);
+      eg[u] = s < hi ? reinterpret_cast<const longlong2 *>(d.seg_err)[si] : make_longlong2(0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { en += ev[u].x; ed += ev[u].y; er += eg[u].x; ct += eg[u].y; }
   }
   en = warp_sum_d(en);
   ed = warp_sum_d(ed);
@@ -845,9 +851,18 @@ __global__ void __launch_bounds__(1024) k_lms_prefix(RxDev d, int flush, int max
   if (t < 4) acnt[t] = 0;
   __syncthreads();
   const int *ready = d.family == 1 ? d.seg_stitched : d.seg_done;   // PAM: no stitching (R_s = 0)
-  for (int i = t; i < maxn; i += blockDim.x) {
-    const long long s = base + i;
-    if (ready[rmod(s, d.seg_cap)] != s + 1) atomicMin(&firstbad, i);
+  for (int i0 = t; i0 < maxn; i0 += 4 * blockDim.x) {          // 4 loads in flight per thread
+    int v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * blockDim.x;
+      v[u] = i < maxn ? ready[rmod(base + i, d.seg_cap)] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i < maxn && v[u] != base + i + 1) atomicMin(&firstbad, i);
+    }
   }
   __syncthreads();
   int n = firstbad;
@@ -954,6 +969,21 @@ __global__ void __launch_bounds__(256) k_lms_final(RxDev d, unsigned char *label
   const int R = d.family == 1 ? d.seg_R[si] : 0;
   const long long lo = s * (long long)d.S, hi = seg_end_of(d, s);
   const int b = d.kbits >> 1;
+  // per-segment lookup: level code -> code rotated by j^R (QAM) and its Gray label
+  __shared__ unsigned char lut_code[256], lut_lab[256];
+  {
+    const int c0 = threadIdx.x & 255;
+    int c = c0;
+    unsigned char lb;
+    if (d.family == 1) {
+      c = ((c & 15) < d.L && (c >> 4) < d.L) ? qam_rot(c, R, d.L) : c;
+      lb = (unsigned char)((gray(c & 15) << b) | gray(c >> 4));
+    } else {
+      lb = (unsigned char)gray(c);
+    }
+    if (threadIdx.x < 256) { lut_code[c0] = (unsigned char)c; lut_lab[c0] = lb; }
+  }
+  __syncthreads();
   long long err = 0, cntd = 0;
   // reference index of the segment's first symbol (one modulo per segment); 16 symbols per
   // thread-step: 128-bit level / label accesses where aligned
@@ -975,15 +1005,10 @@ __global__ void __launch_bounds__(256) k_lms_final(RxDev d, unsigned char *label
     }
     unsigned char lab[16];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      int c = code[j];
-      if (d.family == 1) {
-        c = qam_rot(c, R, d.L);       // level ring stays in the segment frame (stitching)
-        lab[j] = (unsigned char)((gray(c & 15) << b) | gray(c >> 4));
-      } else {
-        lab[j] = (unsigned char)gray(c);
-      }
-      code[j] = (unsigned char)c;
+    for (int j = 0; j < 16; ++j) {    // level ring stays in the segment frame (stitching)
+      const int c = code[j];
+      lab[j] = lut_lab[c];
+      code[j] = lut_code[c];
     }
     if (full) {
       unsigned w[4] = {0u, 0u, 0u, 0u}, l[4] = {0u, 0u, 0u, 0u};

@@ -32,11 +32,37 @@ def _torch_cuda():
     return torch
 
 
-def _compare_labels(rec, rx, out, labels):
-    """(1) bit-exact outside the excluded set (near-boundary decisions and what follows them in
-    the same segment); (2) at most 1e-3 of all labels differ; (3) every differing label's
-    oracle soft value lies within 0.05 of a decision boundary. The excluded fraction is a
-    property of the format and SNR (dense for PAM-16), so it is reported, not bounded."""
+def _bps_flip_blocks(R, rx, out, m_end):
+    """Blind phase search is an argmax over P_t test phases: where two phases score within
+    rounding of each other the fp32 kernel and the fp64 oracle may pick neighbours (SURVEY §8(c)
+    'BPS on noisy data: parity unpinned'). Such a block shows up as a common rotation of the
+    GPU's z' against the oracle's by about one test-phase step. Returns the first symbol of every
+    flipped block, and checks that each flip is exactly one step (anything else is a bug)."""
+    if R is None or rx.get("cpr_test_phases", 0) == 0:
+        return np.zeros(0, np.int64)
+    try:
+        zg = R.probe("Y", 0, m_end)
+    except Exception:                       # streaming rings no longer hold the whole record
+        return np.zeros(0, np.int64)
+    zo = out["lms"]["z"][:m_end]
+    step = (np.pi / 2) / rx["cpr_test_phases"]
+    dphi = np.angle(zg * np.conj(zo))
+    B = rx["lms_block"]
+    nb = m_end // B
+    med = np.median(dphi[:nb * B].reshape(nb, B), axis=1)
+    flip = np.abs(med) > 0.3 * step
+    if np.any(flip):
+        ratio = np.abs(med[flip]) / step
+        assert np.all(np.abs(ratio - np.rint(ratio)) < 0.35) and np.all(np.rint(ratio) == 1), ratio
+    return np.nonzero(flip)[0] * B
+
+
+def _compare_labels(rec, rx, out, labels, R=None):
+    """(1) bit-exact outside the excluded set (near-boundary decisions, BPS near-tie blocks, and
+    what follows them in the same segment); (2) at most 1e-3 of all labels differ; (3) every
+    differing label's oracle soft value lies within 0.05 of a decision boundary, or in a BPS
+    near-tie block. The excluded fraction is a property of the format and SNR (dense for PAM-16),
+    so it is reported, not bounded."""
     m_end = out["m_end"]
     lab_o = out["labels"][:m_end].astype(np.int64)
     lab_g = labels[:m_end].astype(np.int64)
@@ -45,16 +71,22 @@ def _compare_labels(rec, rx, out, labels):
     S = rx["lms_segment"]
     seg = np.arange(m_end) // S
     excl = np.zeros(m_end, bool)
-    for s in np.unique(seg[near]):
-        first = np.argmax(near & (seg == s))
+    flips = _bps_flip_blocks(R, rx, out, m_end)
+    start = near.copy()
+    start[flips] = True
+    for s in np.unique(seg[start]):
+        first = np.argmax(start & (seg == s))
         excl[first:(s + 1) * S] = True
     mism = lab_o != lab_g
     bad = mism & ~excl
     assert not np.any(bad), f"{int(bad.sum())} label mismatches away from thresholds, first at {np.argmax(bad)}"
     assert mism.sum() <= 1e-3 * m_end, f"{int(mism.sum())} of {m_end} labels differ"
     loose = near_threshold(soft, rec.fmt, rec.M, 0.05)
-    assert np.all(loose[mism]), f"{int(np.sum(mism & ~loose))} mismatches far from a boundary"
-    print(f"labels: {int(mism.sum())} differ, excluded fraction {excl.mean():.4f}")
+    in_flip = np.zeros(m_end, bool)
+    for f in flips:
+        in_flip[f:(f // S + 1) * S] = True
+    assert np.all((loose | in_flip)[mism]), f"{int(np.sum(mism & ~loose & ~in_flip))} mismatches far from a boundary"
+    print(f"labels: {int(mism.sum())} differ, excluded fraction {excl.mean():.4f}, BPS near-tie blocks {len(flips)}")
     return mism, excl
 
 
@@ -99,7 +131,7 @@ def test_c1_sync_training_labels_counters(c1):
     assert abs(st["sync_gamma"] - out["sync"]["gamma"]) < 1e-4
     w = R.train_taps()
     assert rel_l2(w, out["lms"]["w_train"]) < TOL_FIELD
-    mism, _ = _compare_labels(rec, rx, out, labels)
+    mism, _ = _compare_labels(rec, rx, out, labels, R)
     _compare_counters(rec, out, st, mism)
     assert st["status_flags"] == 0
     assert st["clipped"] == out["clipped"]
@@ -153,7 +185,7 @@ def test_multi_buffer_parity(name, n, extra, batch, call_bufs):
     if rec.fmt == "qam":
         assert st["sync_phase"] == out["sync"]["phase"]
     assert rel_l2(R.train_taps(), out["lms"]["w_train"]) < 1e-3
-    mism, excl = _compare_labels(rec, rx, out, labels)
+    mism, excl = _compare_labels(rec, rx, out, labels, R)
     _compare_counters(rec, out, st, mism)
 
 
@@ -185,7 +217,7 @@ def test_f32_input_matches_u16():
     Rb, lb, sb = run_gpu(rec, rxf, chunk=256 * 512)
     m_end = out["m_end"]
     assert rel_l2(Rb.probe("E", 0, 4096), out["E"][:4096]) < TOL_FIELD
-    mism, excl = _compare_labels(rec, rx, out, lb)
+    mism, excl = _compare_labels(rec, rx, out, lb, Rb)
     _compare_counters(rec, out, sb, mism)
     assert sb["clipped"] == 0
     assert np.mean(la[:m_end] != lb[:m_end]) <= 1e-3
@@ -208,6 +240,53 @@ def test_set_taps_warm_start():
     out = O.receive_pam(rec.codes, p)
     R, labels, st = run_gpu(rec, rx, pre=lambda R: R.set_taps(w0))
     assert rel_l2(R.train_taps(), out["lms"]["w_train"]) < 1e-3
-    mism, excl = _compare_labels(rec, rx, out, labels)
+    mism, excl = _compare_labels(rec, rx, out, labels, R)
     with pytest.raises(RxError):
         R.set_taps(w0)
+
+
+@pytest.mark.parametrize("ch", [0, 1, 2, 3, 4, 5, 6, 7])
+def test_c5_formats_parity(ch):
+    """Every format of the mixed-channel config C5 (PAM-2/4/8/16, QAM-4/16/64) at 2^20 samples
+    with 256-block buffers: labels / counters / EVM against the oracle."""
+    _torch_cuda()
+    rec, rx = make_config(f"C5:{ch}", n_samples=1 << 20)
+    rx["buffer_blocks"] = 256
+    out = run_oracle(rec, rx)
+    R, labels, st = run_gpu(rec, rx, chunk=256 * 512)
+    assert st["sync_offset"] == out["sync"]["offset"]
+    assert rel_l2(R.train_taps(), out["lms"]["w_train"]) < 1e-3
+    mism, excl = _compare_labels(rec, rx, out, labels, R)
+    _compare_counters(rec, out, st, mism)
+
+
+def test_boundary_edge_cases():
+    """Argument and state errors at the C ABI (SURVEY §8(b) 'Errors'): empty calls are no-ops,
+    sizes that are not a multiple of hop / exceed the call limit / misaligned pointers are
+    RX_EINVAL, calls after rx_flush are RX_ESTATE; a flush with no input finishes cleanly."""
+    torch = _torch_cuda()
+    from paper_2011_13695_b200 import RX_PAM, Receiver, RxError
+    from paper_2011_13695_b200.rx import load
+    import ctypes
+    rec, rx = make_config("C1")
+    R = Receiver(RX_PAM, rec.M, rec.static_taps, lms_taps=rx["lms_taps"], train_symbols=rx["train_symbols"])
+    codes = torch.zeros(4096, dtype=torch.int16, device="cuda")
+    labels = torch.zeros(1024, dtype=torch.uint8, device="cuda")
+    R.process(codes[:0], labels)                                   # n = 0
+    with pytest.raises(RxError) as e:
+        R.process(codes[:500], labels)                             # not a multiple of hop
+    assert e.value.status == -1
+    with pytest.raises(RxError):
+        R.process(codes[1:513], labels)                            # misaligned device pointer
+    max_call = (R.cfg.history_buffers - 2) * R.cfg.buffer_blocks * 512
+    big = torch.zeros(max_call + 512, dtype=torch.int16, device="cuda")
+    with pytest.raises(RxError):
+        R.process(big, labels)                                     # above the per-call limit
+    R.flush(labels)
+    st = R.stats()
+    assert st["samples_in"] == 0 and st["bits"] == 0
+    assert st["status_flags"] & ~2 == 0            # only RX_FLAG_SYNC: an empty stream never syncs
+    with pytest.raises(RxError) as e:
+        R.process(codes[:512], labels)
+    assert e.value.status == -8                                    # RX_ESTATE after flush
+    R.close()
