@@ -181,12 +181,28 @@ __device__ __forceinline__ long long warp_incl_max_ll(long long v) {
 // (c) k_pam_tau: tau_b = -(offset + local prefix) / 2 pi, M_b = ceil(256 b - 128 - tau_b).
 #define CLK_TILE 256
 __device__ __forceinline__ double theta_of(const double2 *Ct, int i, int hh) {   // window at tile i
-  double sr = 0.0, si = 0.0;
-  for (int k = 0; k <= 2 * hh; ++k) { const double2 c = Ct[i + k]; sr += c.x; si += c.y; }
-  return (sr == 0.0 && si == 0.0) ? __longlong_as_double(0x7ff8000000000000LL) : atan2(si, sr);
+  // 4 interleaved partial sums (independent add chains), combined in a fixed order
+  double sr[4] = {0.0, 0.0, 0.0, 0.0}, si[4] = {0.0, 0.0, 0.0, 0.0};
+  const int n = 2 * hh + 1;
+  int k = 0;
+  for (; k + 4 <= n; k += 4) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { const double2 c = Ct[i + k + u]; sr[u] += c.x; si[u] += c.y; }
+  }
+  for (; k < n; ++k) { const double2 c = Ct[i + k]; sr[0] += c.x; si[0] += c.y; }
+  const double r = (sr[0] + sr[1]) + (sr[2] + sr[3]), m = (si[0] + si[1]) + (si[2] + si[3]);
+  return (r == 0.0 && m == 0.0) ? __longlong_as_double(0x7ff8000000000000LL) : atan2(m, r);
 }
 
-__global__ void __launch_bounds__(CLK_TILE) k_pam_theta(RxDev d, long long b0, long long b1, long long blast) {
+// FUSED = true: one launch does (a)-(c). Tile t publishes its total (tagged with the launch id),
+// then forms its offset from the call carry plus the totals of tiles 0..t-1 summed in a fixed
+// order (deterministic; every tile waits only for totals, so nothing is chained), and finishes
+// tau / M itself. Needs every tile co-resident (the host falls back to three launches for
+// more than CLK_FUSE_MAX tiles).
+#define CLK_FUSE_MAX 512
+template <bool FUSED>
+__global__ void __launch_bounds__(CLK_TILE) k_pam_theta(RxDev d, long long b0, long long b1, long long blast,
+                                                        long long launch_id) {
   extern __shared__ double2 Ct[];                 // [CLK_TILE + 1 + 2 h]: blocks base-1-h ..
   __shared__ double th_sh[CLK_TILE + 1];
   __shared__ double wsum[CLK_TILE / 32];
@@ -254,14 +270,51 @@ __global__ void __launch_bounds__(CLK_TILE) k_pam_theta(RxDev d, long long b0, l
   __syncthreads();
   double off = 0.0;
   for (int w = 0; w < warp; ++w) off += wsum[w];
-  if (b < b1) d.tau[rmod(b, d.blk_cap)] = off + incl;    // local prefix (finished by k_pam_tau)
+  if (!FUSED && b < b1) d.tau[rmod(b, d.blk_cap)] = off + incl;   // local prefix (finished by k_pam_tau)
   if (t == CLK_TILE - 1) {
     double tot = 0.0;
     for (int w = 0; w < CLK_TILE / 32; ++w) tot += wsum[w];
     d.clk_part[blockIdx.x] = tot;
     d.clk_last[blockIdx.x] = tcur;                       // resolved phase of the tile's last block
+    if (FUSED) {
+      __threadfence();
+      atomicExch((unsigned long long *)&d.clk_flag[blockIdx.x], (unsigned long long)launch_id);
+    }
+  }
+  if constexpr (FUSED) {
+    // tile offset = carry + sum_{t' < tile} tot_t' (lane-strided then fixed tree: deterministic)
+    __shared__ double tile_off;
+    if (warp == 0) {
+      double acc = 0.0;
+      for (int i = lane; i < (int)blockIdx.x; i += 32) {
+        while (((volatile long long *)d.clk_flag)[i] != launch_id) { }
+        __threadfence();
+        acc += ((volatile double *)d.clk_part)[i];
+      }
+      acc = warp_sum_d(acc);
+      if (lane == 0) tile_off = d.st->thetau_prev + acc;
+    }
+    __syncthreads();
+    const double tu = tile_off + off + incl;
+    if (b < b1) {
+      const double tau = -tu * INV_2PI;
+      d.tau[rmod(b, d.blk_cap)] = tau;
+      d.Mb[rmod(b, d.blk_cap)] = (long long)ceil(256.0 * (double)b - 128.0 - tau);
+    }
   }
   (void)INV_2PI;
+}
+
+// carries after a fused clock launch: thetau_prev += sum of all tile totals, theta_prev
+__global__ void k_pam_clock_carry(RxDev d, int ntiles) {
+  const int lane = threadIdx.x;
+  double acc = 0.0;
+  for (int i = lane; i < ntiles; i += 32) acc += d.clk_part[i];
+  acc = warp_sum_d(acc);
+  if (lane == 0) {
+    d.st->thetau_prev += acc;
+    d.st->theta_prev = d.clk_last[ntiles - 1];
+  }
 }
 
 // (b) offsets of the tiles (exclusive scan of the tile totals, plus the carried unwrapped phase)

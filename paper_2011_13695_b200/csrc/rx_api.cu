@@ -61,6 +61,7 @@ struct rx_handle {
   std::vector<void *> allocs;
   // host-known progress (absolute units)
   long long n_in, fe_done, clk_done, be_done, norm_done, s2_done, cfo_done;
+  long long clk_launch;          // fused clock launches so far (tags the tile totals)
   bool flushed;
   long long launches;
   int sps;
@@ -414,6 +415,7 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
     TRY(dalloc(h, &d.clk_part, maxtiles));
     TRY(dalloc(h, &d.clk_off, maxtiles));
     TRY(dalloc(h, &d.clk_last, maxtiles));
+    TRY(dalloc(h, &d.clk_flag, maxtiles));
   } else {
     d.E_cap = next_pow2((long long)HB * c.buffer_blocks * 512);
     d.z_cap = next_pow2((long long)HB * c.buffer_blocks * 256);
@@ -466,7 +468,8 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   // kernels needing > 48 KB dynamic shared memory
   const size_t cfo_smem = (1024 + CFO_GROUPS * FFT_PAD_N) * sizeof(float2);
   const size_t clk_smem = (CLK_TILE + 1 + 2 * c.clock_avg_half) * sizeof(double2);
-  if (cudaFuncSetAttribute(k_pam_theta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)clk_smem) != cudaSuccess ||
+  if (cudaFuncSetAttribute(k_pam_theta<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)clk_smem) != cudaSuccess ||
+      cudaFuncSetAttribute(k_pam_theta<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)clk_smem) != cudaSuccess ||
       cudaFuncSetAttribute(k_cfo_spec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfo_smem) != cudaSuccess ||
       cudaFuncSetAttribute(k_sync_corr<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536) != cudaSuccess ||
       cudaFuncSetAttribute(k_sync_corr<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536) != cudaSuccess) {
@@ -631,9 +634,15 @@ static void run_pam(rx_handle *h, cudaStream_t s, const InView &in, unsigned cha
   if (clk_target > h->clk_done) {
     const size_t smem = (CLK_TILE + 1 + 2 * d.clock_half) * sizeof(double2);
     const unsigned ntiles = gridc(clk_target - h->clk_done, CLK_TILE);
-    KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_pam_theta<<<ntiles, CLK_TILE, smem, s>>>(d, h->clk_done, clk_target, h->fe_done - 1)));
-    KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_pam_carry<<<1, 1024, 0, s>>>(d, (int)ntiles)));
-    KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_pam_tau<<<gridc(clk_target - h->clk_done, 256), 256, 0, s>>>(d, h->clk_done, clk_target)));
+    if (ntiles <= CLK_FUSE_MAX) {   // every tile co-resident: one pass + the carry
+      const long long id = ++h->clk_launch;
+      KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_pam_theta<true><<<ntiles, CLK_TILE, smem, s>>>(d, h->clk_done, clk_target, h->fe_done - 1, id)));
+      KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_pam_clock_carry<<<1, 32, 0, s>>>(d, (int)ntiles)));
+    } else {
+      KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_pam_theta<false><<<ntiles, CLK_TILE, smem, s>>>(d, h->clk_done, clk_target, h->fe_done - 1, 0)));
+      KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_pam_carry<<<1, 1024, 0, s>>>(d, (int)ntiles)));
+      KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_pam_tau<<<gridc(clk_target - h->clk_done, 256), 256, 0, s>>>(d, h->clk_done, clk_target)));
+    }
     h->clk_done = clk_target;
   }
   long long be_target = flush ? h->fe_done - 1 : h->clk_done - 1;
