@@ -54,12 +54,20 @@ __device__ __forceinline__ int load_block_regs(const InView &in, long long b, fl
     for (int r = 0; r < 8; ++r) w[r] = __ldg(src + j + 64 * r);
 #pragma unroll
     for (int r = 0; r < 8; ++r) v[r] = make_float2(fmaf(code_lo(w[r]), scale, off), fmaf(code_hi(w[r]), scale, off));
+    // clipped codes (0 or 4095) per 16-bit half: (c + 1) & 0xFFE is 0 exactly for those, and
+    // adding 0x7FFF sets bit 15 of every other half (no carry between halves: halves < 0x1000)
 #pragma unroll
     for (int r = 4; r < 8; ++r) {
-      clip += __popc(__vcmpeq2(w[r], 0u) | __vcmpeq2(w[r], 0x0FFF0FFFu)) >> 4;
-      const long long p = p0 + 2 * (j + 64 * r);
-      if (p >= in.keep_from)
-        reinterpret_cast<uint32_t *>(in.hist_w)[(p & (in.hist_cap - 1)) >> 1] = w[r];
+      const uint32_t u = (w[r] + 0x00010001u) & 0x0FFE0FFEu;
+      clip += 2 - __popc((u + 0x7FFF7FFFu) & 0x80008000u);
+    }
+    if (p0 + 1024 > in.keep_from) {   // the call's tail: append the owned half to the history ring
+#pragma unroll
+      for (int r = 4; r < 8; ++r) {
+        const long long p = p0 + 2 * (j + 64 * r);
+        if (p >= in.keep_from)
+          reinterpret_cast<uint32_t *>(in.hist_w)[(p & (in.hist_cap - 1)) >> 1] = w[r];
+      }
     }
   } else {
 #pragma unroll
