@@ -212,37 +212,57 @@ def run_mode(torch, dist, R, ring, n_step, steps, warmup, world, dev, units, lab
 
 
 def e2e_run(torch, R, n_step, host_codes, steps, dev):
-    """Same metric end to end through the public API: pinned host input -> H2D -> rx_process
-    calls -> D2H of the step's labels, all inside the timed region (one stream)."""
+    """Same metric end to end through the public API: every step copies its input from pinned
+    host memory to the device, runs the rx_process calls and reads its labels and counters back
+    into pinned host memory, all inside the timed region. Double-buffered on three streams (H2D,
+    processing, D2H) so the copy engines overlap the kernels of the neighbouring steps, as a
+    streaming receiver would run."""
     import ctypes
-    stream = torch.cuda.Stream(device=dev)
-    sp = ctypes.c_void_p(stream.cuda_stream)
+    proc = torch.cuda.Stream(device=dev)
+    h2d = torch.cuda.Stream(device=dev)
+    d2h = torch.cuda.Stream(device=dev)
+    sp = ctypes.c_void_p(proc.cuda_stream)
     pinned_in = torch.from_numpy(host_codes[:n_step].view("int16")).pin_memory()
-    dbuf = torch.empty(n_step, dtype=torch.int16, device=dev)
+    dbuf = [torch.empty(n_step, dtype=torch.int16, device=dev) for _ in range(2)]
     labels = torch.zeros(1 << 24, dtype=torch.uint8, device=dev)
     nlab = n_step // 2
-    pinned_out = torch.empty(nlab, dtype=torch.uint8).pin_memory()
-    cnt = torch.zeros(8, dtype=torch.float64, device=dev)
-    cnt_host = torch.empty(8, dtype=torch.float64).pin_memory()
+    pinned_out = [torch.empty(nlab, dtype=torch.uint8).pin_memory() for _ in range(2)]
+    cnt = [torch.zeros(8, dtype=torch.float64, device=dev) for _ in range(2)]
+    cnt_host = [torch.empty(8, dtype=torch.float64).pin_memory() for _ in range(2)]
+    ev_in = [torch.cuda.Event() for _ in range(2)]      # input of buffer i on the device
+    ev_done = [torch.cuda.Event() for _ in range(2)]    # processing of buffer i finished
+    ev_out = [torch.cuda.Event() for _ in range(2)]     # labels of buffer i on the host
 
-    def one():
-        with torch.cuda.stream(stream):
-            dbuf.copy_(pinned_in, non_blocking=True)
+    def one(k):
+        i = k % 2
+        with torch.cuda.stream(h2d):
+            h2d.wait_event(ev_done[i])                  # dbuf[i] free again
+            dbuf[i].copy_(pinned_in, non_blocking=True)
+            ev_in[i].record(h2d)
+        proc.wait_event(ev_in[i])
         for off in range(0, n_step, CHUNK):
             n = min(CHUNK, n_step - off)
-            R.process_ptr(dbuf.data_ptr() + 2 * off, n, labels.data_ptr(), labels.numel(), sp)
-        R.export_counters(cnt, stream=stream)
-        with torch.cuda.stream(stream):
-            pinned_out.copy_(labels[:nlab], non_blocking=True)
-            cnt_host.copy_(cnt, non_blocking=True)
+            R.process_ptr(dbuf[i].data_ptr() + 2 * off, n, labels.data_ptr(), labels.numel(), sp)
+        R.export_counters(cnt[i], stream=proc)
+        ev_done[i].record(proc)
+        with torch.cuda.stream(d2h):
+            d2h.wait_event(ev_done[i])
+            d2h.wait_event(ev_out[i])                   # host buffer i read back two steps ago
+            pinned_out[i].copy_(labels[i * nlab:(i + 1) * nlab], non_blocking=True)
+            cnt_host[i].copy_(cnt[i], non_blocking=True)
+            ev_out[i].record(d2h)
 
-    one()
+    for k in range(2):
+        one(k)
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(steps):
-        one()
-    e1.record(stream)
+    e0.record(proc)
+    h2d.wait_event(e0)
+    for k in range(steps):
+        one(k)
+    proc.wait_stream(d2h)
+    proc.wait_stream(h2d)
+    e1.record(proc)
     torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1)
     return dict(ms=ms, h2d=2 * n_step, d2h=nlab + 8 * 8)
