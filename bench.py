@@ -268,6 +268,106 @@ def e2e_run(torch, R, n_step, host_codes, steps, dev):
     return dict(ms=ms, h2d=2 * n_step, d2h=nlab + 8 * 8)
 
 
+def _gen_c5(ch):
+    from rxsynth import make_config
+    return make_config(f"C5:{ch}", keep_tx=True) if ch % 8 < 4 else make_config(f"C5:{ch}")
+
+
+def c5_run(torch, dist, rank, world, dev, steps, warmup, ring_gib):
+    """BASELINE.json configs[4]: 8 independent channels per GPU, mixed PAM-2/4/8/16
+    and KK QAM-4/16/64/16 (C2/C4-style impairments), each one librx handle on its own CUDA
+    stream so the channels' kernels overlap; the 8N channels' packed counters are all-reduced
+    over NCCL once per step (SURVEY §8(e) mode 1). One step = one 16,776,704-sample record per
+    channel. Returns the bench sub-object (value = all ranks' samples / max-over-ranks time)."""
+    import concurrent.futures as cf
+    import multiprocessing as mp
+    from paper_2011_13695_b200 import RX_PAM, RX_QAM_KK, Receiver, multi
+    from rxsynth.configs import N_C2
+    from rxsynth.ring import pam_ring, tiled_ring
+    chans = list(range(8 * rank, 8 * rank + 8))
+    t0 = time.time()
+    with cf.ProcessPoolExecutor(max_workers=min(8, os.cpu_count() or 1),
+                                mp_context=mp.get_context("spawn")) as ex:
+        recs = list(ex.map(_gen_c5, chans))
+    t_gen = time.time() - t0
+    # PAM rings continue the record with its clock offset and must not wrap inside the run
+    # (a wrap restarts the PRBS); KK records are exactly periodic and tile seamlessly
+    per_ring = max(warmup + steps + 1, int(ring_gib * (1 << 30) / 8 / 2 // N_C2)) * N_C2
+    chs = []
+    for ch, (rec, rx) in zip(chans, recs):
+        if rec.fmt == "pam":
+            ring = pam_ring(rec, per_ring, dev, seed=7000 + ch)
+            R = Receiver(RX_PAM, rec.M, rec.static_taps, device=dev.index or 0,
+                         history_buffers=CALL_BUFFERS + 2, **rx_fields(rx))
+        else:
+            ring = tiled_ring(rec, per_ring, dev)
+            R = Receiver(RX_QAM_KK, rec.M, rec.static_taps, device=dev.index or 0,
+                         dc_offset=rec.dc_offset, history_buffers=CALL_BUFFERS + 2, **rx_fields(rx))
+        rec.meta.pop("x_tx", None)
+        labels = torch.zeros(1 << 24, dtype=torch.uint8, device=dev)
+        chs.append(Stream1(R, ring, N_C2, labels, torch.cuda.Stream(device=dev)))
+    main = torch.cuda.Stream(device=dev)
+    cnt = torch.zeros(len(chs), 8, dtype=torch.float64, device=dev)
+    fork, joins = torch.cuda.Event(), [torch.cuda.Event() for _ in chs]
+
+    def one_step():
+        fork.record(main)
+        for i, c in enumerate(chs):
+            c.stream.wait_event(fork)
+            c.step()
+            c.R.export_counters(cnt[i], stream=c.stream)
+            joins[i].record(c.stream)
+        for j in joins:
+            main.wait_event(j)
+        if world > 1:
+            with torch.cuda.stream(main):
+                multi.allreduce_counters(cnt)
+
+    for _ in range(warmup):
+        one_step()
+    torch.cuda.synchronize(dev)
+    l0 = sum(c.R.stats(c.stream)["launches"] for c in chs)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(dev.index if dev.index is not None else 0)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(main)
+    for _ in range(steps):
+        one_step()
+    e1.record(main)
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    launches = sum(c.R.stats(c.stream)["launches"] for c in chs) - l0
+    per_fmt = {}
+    c_all = cnt.cpu().tolist()
+    for (rec, _), c in zip(recs, c_all):
+        key = f"{'PAM' if rec.fmt == 'pam' else 'QAM'}-{rec.M}"
+        acc = per_fmt.setdefault(key, [0.0] * 8)
+        for k in range(8):
+            acc[k] += c[k]
+    for c in chs:
+        c.R.close()
+    del chs
+    torch.cuda.empty_cache()
+    return {"workload": "C5: 8 independent channels per GPU (PAM-2/4/8/16 C2-style, KK QAM-4/16/64/16 "
+                        "C4-style), one 16,776,704-sample record per channel per step, one CUDA stream "
+                        "per channel, NCCL all-reduce of the packed counters per step",
+            "value": round(8 * world * N_C2 * steps / (ms / 1e3) / 1e9, 3), "unit": "GSa/s",
+            "channels": 8 * world, "steps": steps, "ms_per_step": round(ms / steps, 4),
+            "gpu_launches": launches, "clocks": clk, "gen_seconds": round(t_gen, 1),
+            "input": f"per-channel device rings {per_ring * 2 / 2**20:.0f} MiB (8 per GPU, "
+                     f"{8 * per_ring * 2 / 2**30:.2f} GiB > L2)",
+            "quality_rank0_by_format": {k: multi_summary(v) for k, v in sorted(per_fmt.items())}}
+
+
 # ------------------------------------------------------------------------ GPU arm
 def gpu_main(args):
     import numpy as np
@@ -399,6 +499,12 @@ def gpu_main(args):
                                   "evm_db": 10 * math.log10(s4["evm_num"] / s4["evm_den"]) if s4["evm_den"] > 0 else None}}
         line["gpu_launches"] += r4["launches"]
         R4.close()
+        del ring4
+        torch.cuda.empty_cache()
+    # ---- C5: 8 mixed channels per GPU, concurrent streams (every N)
+    if not args.no_c5:
+        line["c5"] = c5_run(torch, dist, rank, world, dev, args.c5_steps, 2, args.ring_gib)
+        line["gpu_launches"] += line["c5"]["gpu_launches"]
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -441,6 +547,8 @@ def main():
     ap.add_argument("--no-kk", action="store_true")
     ap.add_argument("--kk-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--c5-steps", type=int, default=4)
     ap.add_argument("--ring-gib", type=float, default=1.0)
     ap.add_argument("--lms-batch", type=int, default=0,
                     help="segments per equaliser launch (rx_config.lms_batch_segments; 0 = library "

@@ -53,7 +53,7 @@ def c5_channel(ch: int, n_samples: int = N_C2):
     rx["cpr_test_phases"] = 0 if M == 4 else 32
     return dict(gen=dict(kind="qam", M=M, n_samples=n_samples, seed=5000 + ch,
                          cspr_db=6.0 if M == 4 else 11.0, osnr_db=30.0, cfo_hz=5e6,
-                         linewidth_hz=10e3, rx_lpf=False, roadm_b3db=1.5e9),
+                         linewidth_hz=10e3, rx_lpf=False, roadm_b3db=1.5e9, periodic=True),
                 rx=rx)
 
 

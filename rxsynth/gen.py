@@ -284,7 +284,8 @@ def pam_record(M: int, n_samples: int, *, seed: int, snr_db: float | None = None
 def kk_record(M: int, n_samples: int, *, seed: int, cspr_db: float, osnr_db: float | None,
               cfo_hz: float = 0.0, linewidth_hz: float = 0.0, rx_lpf: bool = False,
               roadm_b3db: float | None = None, offset: int | None = None,
-              carrier_hz: float = 0.547e9, n_static_taps: int = 203) -> Record:
+              carrier_hz: float = 0.547e9, n_static_taps: int = 203,
+              periodic: bool = False) -> Record:
     """1 GBaud QAM-M at 4 sps with a digital carrier tone 0.547 GHz above the data.
 
     Field in the tone's frame: E = A + s(t) e^{-j 2 pi f_c t}, |A|^2 = CSPR * mean|s|^2;
@@ -292,6 +293,11 @@ def kk_record(M: int, n_samples: int, *, seed: int, cspr_db: float, osnr_db: flo
     super-Gaussian 'ROADM' filtering of the data term; complex AWGN at the given OSNR over
     12.5 GHz of total power; square-law detection; optional 1 GHz receiver LPF; AC coupling
     (the removed mean is returned as dc_offset in x units); 12-bit ADC.
+
+    periodic=True makes the record exactly periodic, so a tiled ring of it is a seamless stream
+    (bench inputs): the tone and CFO frequencies are rounded to whole cycles per record (a shift
+    of at most FS/(2 n), 119 Hz at 2^24 samples) and the phase noise is a Wiener bridge (the
+    walk minus its linear drift, so it ends where it starts).
     """
     rng = np.random.default_rng(seed)
     sps, baud, beta = 4, 1e9, 0.01
@@ -313,8 +319,13 @@ def kk_record(M: int, n_samples: int, *, seed: int, cspr_db: float, osnr_db: flo
     s = np.fft.ifft(F)
     del F, up
     n = np.arange(n_samples, dtype=np.float64)
+    if periodic:
+        cfo_hz = round(cfo_hz * n_samples / FS) * FS / n_samples
+        carrier_hz = round(carrier_hz * n_samples / FS) * FS / n_samples
     if linewidth_hz > 0:
         phi = np.cumsum(rng.normal(0.0, math.sqrt(2 * math.pi * linewidth_hz / FS), n_samples))
+        if periodic:
+            phi -= (n + 1.0) / n_samples * phi[-1]
         s *= np.exp(1j * phi)
     if cfo_hz != 0.0:
         s *= np.exp(2j * math.pi * cfo_hz / FS * n)
