@@ -48,7 +48,7 @@ __device__ __forceinline__ long long seg_end_of(const RxDev &d, long long s) {
 template <bool CPLX>
 __device__ __forceinline__ bool sync_ready(const RxDev &d) {
   const long long need = CPLX ? 2 * (d.m0 + d.W_sync) + 2 : d.m0 + d.W_sync;
-  return d.st->v_front >= need;
+  return d.st->v_lms >= need;
 }
 
 template <bool CPLX>
@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(256) k_sync_corr(RxDev d) {
   extern __shared__ float2 zeta[];   // [nh][W]
   if (d.st->synced || !sync_ready<CPLX>(d)) return;
   const int nh = CPLX ? 2 : 1, W = d.W_sync;
-  const long long vend = d.st->v_front;
+  const long long vend = d.st->v_lms;
   for (int i = threadIdx.x; i < nh * W; i += blockDim.x) {
     const int h = i / W, k = i % W;
     zeta[i] = CPLX ? lms_in<true>(d, 2 * (d.m0 + k) + h, vend) : lms_in<false>(d, d.m0 + k, vend);
@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(1024) k_sync_pick(RxDev d, int flush) {
     return;
   }
   const int nh = CPLX ? 2 : 1, W = d.W_sync;
-  const long long vend = st->v_front;
+  const long long vend = st->v_lms;
   for (int h = 0; h < nh; ++h) {
     double s = 0.0;
     for (int k = threadIdx.x; k < W; k += blockDim.x) {
@@ -599,7 +599,7 @@ __global__ void __launch_bounds__(32) k_lms_train(RxDev d, int flush) {
   if (!st->synced || st->trained) return;
   const int lane = threadIdx.x;
   const int K = d.K, c = K >> 1, stride = CPLX ? 2 : 1;
-  const long long vend = st->v_front;
+  const long long vend = st->v_lms;
   const long long last = (long long)stride * (d.m0 + d.T_train - 1) + (CPLX ? st->sync_phase : 0) + c;
   if (last >= vend && !flush) return;
   float2 wk = make_float2(lane == c ? 1.f : 0.f, 0.f);    // centre spike ...
@@ -710,7 +710,7 @@ __global__ void __launch_bounds__(128) k_lms_seg(RxDev d, int flush, int nseg, u
   if (me >= 0 && lo >= me) return;
   const long long hi = seg_end_of(d, s);
   const int K = d.K, c = K >> 1, stride = CPLX ? 2 : 1;
-  const long long vend = st->v_front;
+  const long long vend = st->v_lms;
   if (me < 0) {   // streaming: all taps of the last symbol must be available
     const long long lastidx = (long long)stride * (hi - 1) + (CPLX ? st->sync_phase : 0) + c;
     if (lastidx >= vend) return;

@@ -39,6 +39,7 @@ __global__ void k_kk_mend(RxDev d, long long q_end) {
     set_flag(d.st, RX_FLAG_SYNC);
   }
 }
+__global__ void k_lms_snapshot(RxDev d) { d.st->v_lms = d.st->v_front; }
 __global__ void k_export_counters(const DevState *st, double *o) {
   o[0] = (double)st->bit_errors; o[1] = (double)st->bits; o[2] = (double)st->symbols_counted;
   o[3] = st->evm_num; o[4] = st->evm_den; o[5] = (double)st->clipped;
@@ -61,6 +62,13 @@ struct rx_handle {
   std::vector<void *> allocs;
   // host-known progress (absolute units)
   long long n_in, fe_done, clk_done, be_done, norm_done, s2_done, cfo_done;
+  // Equaliser side stream: every streaming call forks the equaliser work on the data the
+  // earlier calls normalised (sync, training, block-LMS rounds, stitching, labels, counters)
+  // onto `side`, concurrently with its own front-end / clock / back-end / normalisation, and
+  // joins it back before the call's work on the caller's stream ends.
+  cudaStream_t side;
+  cudaEvent_t ev_fork, ev_join;
+  long long lms_sym_ub;          // symbol upper bound of the data normalised by earlier calls
   long long clk_launch;          // fused clock launches so far (tags the tile totals)
   bool flushed;
   long long launches;
@@ -234,6 +242,9 @@ extern "C" void rx_destroy(rx_handle *h) {
   cudaSetDevice(h->device);
   for (void *p : h->allocs) cudaFree(p);
   if (h->hm_host) cudaFreeHost(h->hm_host);
+  if (h->side) cudaStreamDestroy(h->side);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
   for (auto &e : h->prof_pending) { cudaEventDestroy(e.second.first); cudaEventDestroy(e.second.second); }
   for (auto &e : h->prof_free) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   delete h;
@@ -396,7 +407,9 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   const long long tail_sym = (long long)c.tap_lag_epochs * E_sym;
   const long long bsym = (long long)c.lms_batch_segments * c.lms_segment;
   const long long batch_sym = bsym + (bsym > tail_sym ? tail_sym : bsym);
-  d.sym_cap = next_pow2((long long)HB * c.buffer_blocks * (kk ? 128 : 260) + batch_sym);
+  // (HB + 1 buffers: the equaliser side stream reads the previous calls' symbols while the
+  // current call writes up to one more call of them)
+  d.sym_cap = next_pow2((long long)(HB + HB - 2) * c.buffer_blocks * (kk ? 128 : 260) + batch_sym);
   if (!kk) {
     TRY(dalloc(h, &d.C, d.blk_cap));
     TRY(dalloc(h, &d.theta, d.blk_cap));
@@ -421,7 +434,7 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
     d.z_cap = next_pow2((long long)HB * c.buffer_blocks * 256);
     TRY(dalloc(h, &d.E, d.E_cap));
     TRY(dalloc(h, &d.z, d.z_cap));
-    d.zp_cap = next_pow2((long long)HB * c.buffer_blocks * 256 + 2 * batch_sym);
+    d.zp_cap = next_pow2((long long)(HB + HB - 2) * c.buffer_blocks * 256 + 2 * batch_sym);
     TRY(dalloc(h, &d.zp, d.zp_cap));
     TRY(dalloc(h, &d.cfo, d.buf_cap));
     d.cfo_G = (int)(h->Q / 1024 / CFO_GROUPS + 1);      // spectrum rows per buffer
@@ -475,6 +488,16 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
       cudaFuncSetAttribute(k_sync_corr<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536) != cudaSuccess) {
     rx_destroy(h);
     return RX_ECUDA;
+  }
+  {
+    int lo = 0, hi = 0;   // the equaliser's latency-bound warps get the SM slots first
+    if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, hi) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      rx_destroy(h);
+      return RX_ECUDA;
+    }
   }
   if (cudaDeviceSynchronize() != cudaSuccess) { rx_destroy(h); return RX_ECUDA; }
 #undef TRY
@@ -666,8 +689,12 @@ static void run_pam(rx_handle *h, cudaStream_t s, const InView &in, unsigned cha
     }
   }
   if (flush) KLAUNCH(h, RX_K_MISC, s, (k_pam_mend<<<1, 1, 0, s>>>(d, h->be_done > 0 ? h->be_done : 0)));
-  launch_sync_train<false>(h, s, flush);
-  launch_lms_rounds(h, s, labels, lab_cap, flush, 256 * h->be_done + h->be_done / 4 + 4096);
+  h->lms_sym_ub = 256 * h->be_done + h->be_done / 4 + 4096;
+  if (flush) {
+    KLAUNCH(h, RX_K_MISC, s, (k_lms_snapshot<<<1, 1, 0, s>>>(d)));
+    launch_sync_train<false>(h, s, flush);
+    launch_lms_rounds(h, s, labels, lab_cap, flush, h->lms_sym_ub);
+  }
 }
 
 static void run_kk(rx_handle *h, cudaStream_t s, const InView &in, unsigned char *labels,
@@ -704,9 +731,29 @@ static void run_kk(rx_handle *h, cudaStream_t s, const InView &in, unsigned char
       h->cfo_done += nbuf;
     }
   }
-  launch_sync_train<true>(h, s, flush);
-  if (flush) KLAUNCH(h, RX_K_MISC, s, (k_kk_mend<<<1, 1, 0, s>>>(d, q_front)));
-  launch_lms_rounds(h, s, labels, lab_cap, flush, q_front / 2 + 1);
+  h->lms_sym_ub = q_front / 2 + 1;
+  if (flush) {   // m_end needs the sync phase: sync, then the end marker, then the rounds
+    KLAUNCH(h, RX_K_MISC, s, (k_lms_snapshot<<<1, 1, 0, s>>>(d)));
+    launch_sync_train<true>(h, s, flush);
+    KLAUNCH(h, RX_K_MISC, s, (k_kk_mend<<<1, 1, 0, s>>>(d, q_front)));
+    KLAUNCH(h, RX_K_MISC, s, (k_lms_snapshot<<<1, 1, 0, s>>>(d)));
+    launch_lms_rounds(h, s, labels, lab_cap, flush, h->lms_sym_ub);
+  }
+}
+
+// Streaming call: the equaliser stage (sync, training, LMS rounds and their post-processing)
+// works on what earlier calls normalised (v_lms = v_front at the start of this call), on the
+// side stream, while this call's front-end ... normalisation run on the caller's stream. Results
+// do not depend on it (the equaliser output is independent of how its rounds are batched).
+static void fork_equaliser(rx_handle *h, cudaStream_t s, unsigned char *labels, long long lab_cap) {
+  RxDev &d = h->d;
+  KLAUNCH(h, RX_K_MISC, s, (k_lms_snapshot<<<1, 1, 0, s>>>(d)));
+  cudaEventRecord(h->ev_fork, s);
+  cudaStreamWaitEvent(h->side, h->ev_fork, 0);
+  if (d.family == RX_PAM) launch_sync_train<false>(h, h->side, 0);
+  else launch_sync_train<true>(h, h->side, 0);
+  launch_lms_rounds(h, h->side, labels, lab_cap, 0, h->lms_sym_ub);
+  cudaEventRecord(h->ev_join, h->side);
 }
 
 static InView make_view(const rx_handle *h, const void *samples, long long n) {
@@ -738,8 +785,12 @@ extern "C" rx_status rx_process(rx_handle *h, const void *d_samples, long long n
   cudaStream_t s = (cudaStream_t)stream;
   const InView in = make_view(h, d_samples, n);
   h->n_in += n;
-  if (h->d.family == RX_PAM) run_pam(h, s, in, labels_capacity ? d_labels : nullptr, labels_capacity ? labels_capacity : 1, 0);
-  else run_kk(h, s, in, labels_capacity ? d_labels : nullptr, labels_capacity ? labels_capacity : 1, 0);
+  unsigned char *lab = labels_capacity ? d_labels : nullptr;
+  const long long cap = labels_capacity ? labels_capacity : 1;
+  fork_equaliser(h, s, lab, cap);
+  if (h->d.family == RX_PAM) run_pam(h, s, in, lab, cap, 0);
+  else run_kk(h, s, in, lab, cap, 0);
+  CK(cudaStreamWaitEvent(s, h->ev_join, 0));
   return check_launch();
 }
 

@@ -14,6 +14,8 @@ struct DevState {
   double theta_prev, thetau_prev;
   // ---- normalisation fronts
   long long v_front;        // PAM: uhat valid for m < v_front; KK: z' valid for q < v_front
+  long long v_lms;          // the equaliser's snapshot of v_front, taken on the caller's stream
+                            // before the call forks its equaliser work onto the side stream
   long long m_end;          // final symbol count (set at flush), else -1
   // ---- sync / training
   int synced, trained, sync_offset, sync_phase, sync_polarity, pad0;
