@@ -594,8 +594,14 @@ def lms_segments(v, stride, off, m_end, seeds_fn, slicer: _Slicer, lp: LmsParams
     s_hi = np.array([min((s + 1) * S, m_end) for s in segs], dtype=np.int64)
     nblk = int(np.max(-(-(s_hi - t0) // B))) if ns else 0
     dt = np.float64 if real else np.complex128
-    W = np.stack([seeds_fn(s) for s in segs]).astype(dt)
-    Vw = np.zeros_like(W)
+    # seeds_fn(s) -> w, or (w, v) for the widely-linear equaliser (its v-branch is seeded like w)
+    sd = [seeds_fn(s) for s in segs]
+    if lp.widely_linear:
+        W = np.stack([w for w, _ in sd]).astype(dt)
+        Vw = np.stack([v_ for _, v_ in sd]).astype(dt)
+    else:
+        W = np.stack(sd).astype(dt)
+        Vw = np.zeros_like(W)
     theta = np.zeros(ns)
     diverged = False
     L = slicer.L
@@ -669,11 +675,16 @@ def lms_full(v, stride, off, m_end, ref_idx_fn, ref_val_fn, slicer: _Slicer, lp:
     s0 = m0 // lp.S
     L = slicer.L
 
+    canon_v = np.zeros_like(canon)
+    seeds_v = {}
+
     def seed(s):
         e = (s * lp.S) // lp.E
         w = w_train if e < lp.D else seeds[e]
         if seed_rotation is not None:
             w = w * (1j) ** int(seed_rotation(s))
+        if lp.widely_linear:   # (w, v): the v-branch seeds follow the same rule (DESIGN R-WL)
+            return w, (v_train if e < lp.D else seeds_v[e])
         return w
 
     for wave in range(0, n_epoch, lp.D):
@@ -714,10 +725,15 @@ def lms_full(v, stride, off, m_end, ref_idx_fn, ref_val_fn, slicer: _Slicer, lp:
                 # average, phi_s = arg(sum_k w_k |w_k|); carrier phase noise decorrelates the
                 # absolute frame across an epoch, and CPR + stitching absorb the common phase.
                 w = r["w"]
-                canon[s] = w * np.exp(-1j * np.angle(np.sum(w * np.abs(w))))
+                rot = np.exp(-1j * np.angle(np.sum(w * np.abs(w))))
+                canon[s] = w * rot
+                # widely linear: y = w^H u + v^H conj(u); (c w)^H u + (c v)^H conj(u) = c* y, so
+                # the v-branch takes the same factor (DESIGN R-WL)
+                canon_v[s] = r["v"] * rot
         for e in range(wave, min(n_epoch, wave + lp.D)):
             lo, hi = e * seg_per_epoch, min(n_seg, (e + 1) * seg_per_epoch)
             seeds[e + lp.D] = np.mean(canon[lo:hi], axis=0)
+            seeds_v[e + lp.D] = np.mean(canon_v[lo:hi], axis=0)
     # assemble outputs over m in [0, m_end)
     shape = (m_end,) if real else (m_end, 2)
     idx_out = np.zeros(shape, dtype=np.int64)
@@ -730,8 +746,8 @@ def lms_full(v, stride, off, m_end, ref_idx_fn, ref_val_fn, slicer: _Slicer, lp:
         idx_out[mm] = ii if real else rotate_indices(ii, int(R[s]), L)
         z_out[mm] = r["z"][sel]
         seg_of[mm] = s
-    return dict(idx=idx_out, z=z_out, R=R, r_rel=r_rel, w_train=w_train, canon=canon,
-                diverged=diverged, seg_of=seg_of)
+    return dict(idx=idx_out, z=z_out, R=R, r_rel=r_rel, w_train=w_train, v_train=v_train,
+                canon=canon, canon_v=canon_v, diverged=diverged, seg_of=seg_of)
 
 
 # ============================================================================ c-11

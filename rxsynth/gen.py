@@ -285,7 +285,7 @@ def kk_record(M: int, n_samples: int, *, seed: int, cspr_db: float, osnr_db: flo
               cfo_hz: float = 0.0, linewidth_hz: float = 0.0, rx_lpf: bool = False,
               roadm_b3db: float | None = None, offset: int | None = None,
               carrier_hz: float = 0.547e9, n_static_taps: int = 203,
-              periodic: bool = False) -> Record:
+              periodic: bool = False, iq_imbalance: complex = 0.0) -> Record:
     """1 GBaud QAM-M at 4 sps with a digital carrier tone 0.547 GHz above the data.
 
     Field in the tone's frame: E = A + s(t) e^{-j 2 pi f_c t}, |A|^2 = CSPR * mean|s|^2;
@@ -298,6 +298,8 @@ def kk_record(M: int, n_samples: int, *, seed: int, cspr_db: float, osnr_db: flo
     (bench inputs): the tone and CFO frequencies are rounded to whole cycles per record (a shift
     of at most FS/(2 n), 119 Hz at 2^24 samples) and the phase noise is a Wiener bridge (the
     walk minus its linear drift, so it ends where it starts).
+    iq_imbalance = beta: transmitter IQ imbalance of the shaped data, s <- s + beta conj(s) (the
+    impairment the paper's widely-linear equaliser compensates).
     """
     rng = np.random.default_rng(seed)
     sps, baud, beta = 4, 1e9, 0.01
@@ -318,6 +320,8 @@ def kk_record(M: int, n_samples: int, *, seed: int, cspr_db: float, osnr_db: flo
         F *= super_gaussian(f_hz, roadm_b3db)
     s = np.fft.ifft(F)
     del F, up
+    if iq_imbalance:
+        s = s + complex(iq_imbalance) * np.conj(s)
     n = np.arange(n_samples, dtype=np.float64)
     if periodic:
         cfo_hz = round(cfo_hz * n_samples / FS) * FS / n_samples
@@ -348,6 +352,7 @@ def kk_record(M: int, n_samples: int, *, seed: int, cspr_db: float, osnr_db: flo
                   meta=dict(seed=seed, cspr_db=cspr_db, osnr_db=osnr_db, cfo_hz=cfo_hz,
                             linewidth_hz=linewidth_hz, rx_lpf=rx_lpf, roadm_b3db=roadm_b3db,
                             carrier_hz=carrier_hz, clipped=clipped, full_scale=fs,
+                            iq_imbalance=complex(iq_imbalance),
                             tone_amp=A, data_power=Ps))
 
 

@@ -1,0 +1,125 @@
+"""Pins of the oracle's widely-linear equaliser (CPU only).
+
+The paper's KK equaliser is a "4-tap adaptive widely-linear TD DDLMS" that also compensates
+the transmitter's IQ imbalance. The build runs it as the widely-linear form of the
+segmented block-LMS of SURVEY c-9: y = w^H u + v^H conj(u), v <- v + mu sum conj(u) conj(e)
+(reading R-WL). Closed forms pinned here, none of which calls
+the oracle's arithmetic to produce the expected value:
+
+  * IQ imbalance z = alpha s + beta conj(s) of a proper unit-power QAM stream s has the exact
+    widely-linear inverse s = conj(w_c) z + conj(v_c) conj(z) with
+    w_c = alpha / (|alpha|^2 - |beta|^2),  v_c = -conj(beta) / (|alpha|^2 - |beta|^2);
+    noiseless training converges to it (the Wiener solution with zero error).
+  * The strictly linear MMSE solution is w_c = alpha / (|alpha|^2 + |beta|^2) and leaves the
+    image: error power |beta|^2 / (|alpha|^2 + |beta|^2).
+  * With a static carrier phase phi0 (z = e^{j phi0}(alpha s + beta s*)), every
+    phase-equivalent WL solution has v_c / w_c = -e^{-2j phi0} conj(beta) / alpha; a common
+    rotation of (w, v) (the canonical lag-D seeds, reading R-SEED) keeps that ratio, a
+    mismatched one does not.
+"""
+import math
+
+import numpy as np
+
+from oracle import rx_oracle as O
+
+ALPHA = 1.0 * np.exp(0.05j)
+BETA = 0.15 * np.exp(-0.6j)
+
+
+def _qam16_stream(n, seed, phi0=0.0):
+    """2-sps stream: even samples e^{j phi0}(alpha s + beta s*) of QAM-16 symbols s, odd samples
+    independent (uncorrelated with every s_m, so the Wiener taps on them are 0)."""
+    rng = np.random.default_rng(seed)
+    sl = O._Slicer("qam", 16)
+    idx = rng.integers(0, 4, size=(n, 2))
+    s = sl.value(idx)
+    z = np.empty(2 * n, dtype=np.complex128)
+    z[0::2] = np.exp(1j * phi0) * (ALPHA * s + BETA * np.conj(s))
+    z[1::2] = 0.3 * (rng.normal(size=n) + 1j * rng.normal(size=n))
+    return z, s, idx, sl
+
+
+def _train(z, s, wl, T=24576, mu=1e-3, K=4):
+    lp = O.LmsParams(K=K, B=32, mu=mu, T_train=T, widely_linear=wl)
+    m0 = 64
+    return O.lms_train(z, 2, 0, s[m0:m0 + T], m0, lp, real=False)
+
+
+def test_wl_training_converges_to_the_closed_form_iq_inverse():
+    z, s, _, _ = _qam16_stream(32768, 1)
+    w, v = _train(z, s, wl=True)
+    den = abs(ALPHA) ** 2 - abs(BETA) ** 2
+    w_c, v_c = ALPHA / den, -np.conj(BETA) / den
+    c = 2
+    assert abs(w[c] - w_c) < 2e-3 and abs(v[c] - v_c) < 2e-3
+    others = [k for k in range(4) if k != c]
+    assert np.max(np.abs(w[others])) < 2e-3 and np.max(np.abs(v[others])) < 2e-3
+    # the equalised training data reproduces s (image rejected)
+    m = np.arange(30000, 32000)
+    U = O.tap_matrix(z, m, 2, 0, 4)
+    y = U @ np.conj(w) + np.conj(U) @ np.conj(v)
+    err_db = 10 * math.log10(np.mean(np.abs(y - s[m]) ** 2))
+    assert err_db < -50
+
+
+def test_linear_training_converges_to_linear_mmse_and_keeps_the_image():
+    z, s, _, _ = _qam16_stream(32768, 2)
+    w, v = _train(z, s, wl=False)
+    assert np.all(v == 0)
+    w_c = ALPHA / (abs(ALPHA) ** 2 + abs(BETA) ** 2)
+    assert abs(w[2] - w_c) < 5e-3
+    m = np.arange(30000, 32000)
+    U = O.tap_matrix(z, m, 2, 0, 4)
+    y = U @ np.conj(w)
+    err = np.mean(np.abs(y - s[m]) ** 2)
+    closed = abs(BETA) ** 2 / (abs(ALPHA) ** 2 + abs(BETA) ** 2)
+    assert abs(10 * math.log10(err / closed)) < 0.5       # within 0.5 dB of the closed form
+    # image rejection: WL >= 25 dB better than linear-only (SURVEY §8(f) NEXT-1 pin)
+    w2, v2 = _train(z, s, wl=True)
+    y2 = U @ np.conj(w2) + np.conj(U) @ np.conj(v2)
+    err2 = np.mean(np.abs(y2 - s[m]) ** 2)
+    assert 10 * math.log10(err / err2) > 25
+
+
+def _full(phi0, wl, seed=3, n=8 * 4096):
+    z, s, idx, sl = _qam16_stream(n, seed, phi0)
+    lp = O.LmsParams(K=4, B=32, S=1024, O=64, mu=1e-3, T_train=8192, D=2, E=4096, cpr="bps", P_t=32,
+                     widely_linear=wl)
+    m0 = 256
+    lm = O.lms_full(z, 2, 0, n, lambda m: idx[np.asarray(m)], lambda m: s[np.asarray(m)], sl, lp,
+                    False, m0)
+    return lm, s, idx, sl, lp
+
+
+def _abs_frame(lm):
+    """z' of each segment rotated by its stitched quadrant j^{R_s} (c-9 'Stitching')."""
+    return lm["z"] * (1j) ** lm["R"][lm["seg_of"]]
+
+
+def test_wl_segmented_equaliser_seeds_keep_the_iq_inverse_and_decide_error_free():
+    phi0 = 0.7
+    lm, s, idx, sl, lp = _full(phi0, wl=True)
+    ratio = -np.exp(-2j * phi0) * np.conj(BETA) / ALPHA
+    # training pair and every seeded epoch's canonical pair keep v_c / w_c
+    assert abs(lm["v_train"][2] / lm["w_train"][2] - ratio) < 0.02
+    seg_per_epoch = lp.E // lp.S
+    n_seg = lm["canon"].shape[0]
+    for e in range(n_seg // seg_per_epoch):
+        sl_ = slice(e * seg_per_epoch, (e + 1) * seg_per_epoch)
+        w_bar = np.mean(lm["canon"][sl_], axis=0)
+        v_bar = np.mean(lm["canon_v"][sl_], axis=0)
+        assert abs(v_bar[2] / w_bar[2] - ratio) < 0.02, e
+    # noiseless: every decision after training equals the transmitted symbol
+    lo = 8192 + 256
+    assert np.array_equal(lm["idx"][lo:], idx[lo:])
+    assert 10 * math.log10(np.mean(np.abs(_abs_frame(lm)[lo:] - s[lo:]) ** 2)) < -35
+
+
+def test_linear_segmented_equaliser_is_image_limited():
+    lm, s, idx, sl, lp = _full(0.7, wl=False)
+    lo = 8192 + 256
+    # the error sits near the linear-MMSE image floor (-16.6 dB here), far above the WL one
+    err_db = 10 * math.log10(np.mean(np.abs(_abs_frame(lm)[lo:] - s[lo:]) ** 2))
+    closed = 10 * math.log10(abs(BETA) ** 2 / (abs(ALPHA) ** 2 + abs(BETA) ** 2))
+    assert closed - 2 < err_db < closed + 2
