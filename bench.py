@@ -268,6 +268,45 @@ def e2e_run(torch, R, n_step, host_codes, steps, dev):
     return dict(ms=ms, h2d=2 * n_step, d2h=nlab + 8 * 8)
 
 
+def class_flops(name, n_step, rx, kk):
+    """Algorithmic flops of one kernel class per step, None if the
+    class has no flop model (HBM / latency classes)."""
+    if name in FLOPS_PER_UNIT:
+        return FLOPS_PER_UNIT[name] * (n_step // 512)
+    if name == "LMS":
+        if kk:   # 16K flop per complex T/2 symbol + BPS 17 flop per test phase
+            return (16 * rx["lms_taps"] + 17 * rx["cpr_test_phases"]) * (n_step // 4)
+        return 4 * rx["lms_taps"] * (n_step // 2)
+    return None
+
+
+def isolated_classes(torch, make_rx, ring, n_step, rx, kk, dev, peak, steps=2):
+    """Per-class kernel time with the equaliser stage serialised on the caller's stream
+    (rx_config.serial_equaliser = 1: no overlap between kernel classes), CUDA events per launch:
+    the kernel-quality view of the roofline next to the live (overlapped) one."""
+    R = make_rx(serial_equaliser=1)
+    st = torch.cuda.Stream(device=dev)
+    lab = torch.zeros(1 << 24, dtype=torch.uint8, device=dev)
+    ch = Stream1(R, ring, n_step, lab, st)
+    for _ in range(3):
+        ch.step()
+    torch.cuda.synchronize(dev)
+    R.profile_enable()
+    for _ in range(steps):
+        ch.step()
+    prof = R.profile_read()
+    R.close()
+    out = {}
+    for name, (ms, n) in prof.items():
+        f = class_flops(name, n_step, rx, kk)
+        e = {"ms_per_step": round(ms / steps, 4)}
+        if f and ms > 0:
+            a = f * steps / (ms / 1e3) / 1e12
+            e.update(achieved_tflops=round(a, 3), frac=round(a / peak, 4))
+        out[name] = e
+    return out
+
+
 def _gen_c5(ch):
     from rxsynth import make_config
     return make_config(f"C5:{ch}", keep_tx=True) if ch % 8 < 4 else make_config(f"C5:{ch}")
@@ -284,7 +323,7 @@ def c5_run(torch, dist, rank, world, dev, steps, warmup, ring_gib):
     from paper_2011_13695_b200 import RX_PAM, RX_QAM_KK, Receiver, multi
     from rxsynth.configs import N_C2
     from rxsynth.ring import pam_ring, tiled_ring
-    chans = list(range(8 * rank, 8 * rank + 8))
+    chans = multi.channel_shard(8 * world, world, rank)      # 8 channels per rank
     t0 = time.time()
     with cf.ProcessPoolExecutor(max_workers=min(8, os.cpu_count() or 1),
                                 mp_context=mp.get_context("spawn")) as ex:
@@ -393,8 +432,11 @@ def gpu_main(args):
     n_step = N_C2
     ring_samples = max(1, int(args.ring_gib * (1 << 30) / 2 // n_step)) * n_step
     ring = pam_ring(rec, ring_samples, dev, seed=seed)
-    R = Receiver(RX_PAM, rec.M, rec.static_taps, device=local, history_buffers=CALL_BUFFERS + 2,
-                 **({"lms_batch_segments": args.lms_batch} if args.lms_batch else {}), **rx_fields(rx))
+    def make_pam(**kw):
+        return Receiver(RX_PAM, rec.M, rec.static_taps, device=local, history_buffers=CALL_BUFFERS + 2,
+                        **({"lms_batch_segments": args.lms_batch} if args.lms_batch else {}),
+                        **rx_fields(rx), **kw)
+    R = make_pam()
     res = run_mode(torch, dist, R, ring, n_step, args.steps, args.warmup, world, dev, None)
     value = world * n_step * args.steps / (res["ms"] / 1e3) / 1e9
     ms_step = res["ms"] / args.steps
@@ -423,7 +465,11 @@ def gpu_main(args):
                 "traffic": traffic, "kernel_ms_per_step": dom["ms"] / args.steps,
                 "share_of_step": dom["ms"] / res["ms"],
                 "peak_note": "FP32 CUDA-core peak = 148 SMs x 128 lanes x 2 flop x max SM clock "
-                             "(guide unit counts; the path is FP32/smem bound, SURVEY §8(d))"}
+                             "(guide unit counts; the path is FP32/smem bound, SURVEY §8(d))",
+                "live_note": "live = timed region, where the equaliser stage runs on the library's side "
+                             "stream concurrently with the front-end (kernel times include that overlap); "
+                             "isolated = the same classes with serial_equaliser=1 (untimed pass)"}
+        roof["isolated"] = isolated_classes(torch, make_pam, ring, n_step, rx, False, dev, peak_fp32)
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GSa/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
@@ -470,9 +516,12 @@ def gpu_main(args):
     if world == 1 and not args.no_kk:
         rec4, rx4 = make_config("C4")
         ring4 = tiled_ring(rec4, max(1, int(args.ring_gib * (1 << 30) / 2 // N_C4)) * N_C4, dev)
-        R4 = Receiver(RX_QAM_KK, rec4.M, rec4.static_taps, device=local, dc_offset=rec4.dc_offset,
-                      history_buffers=CALL_BUFFERS + 2,
-                      **({"lms_batch_segments": args.lms_batch} if args.lms_batch else {}), **rx_fields(rx4))
+        def make_kk(**kw):
+            return Receiver(RX_QAM_KK, rec4.M, rec4.static_taps, device=local, dc_offset=rec4.dc_offset,
+                            history_buffers=CALL_BUFFERS + 2,
+                            **({"lms_batch_segments": args.lms_batch} if args.lms_batch else {}),
+                            **rx_fields(rx4), **kw)
+        R4 = make_kk()
         r4 = run_mode(torch, None, R4, ring4, N_C4, args.kk_steps, 2, 1, dev, None)
         s4 = r4["stats"]
         v4 = N_C4 * args.kk_steps / (r4["ms"] / 1e3) / 1e9
@@ -485,6 +534,7 @@ def gpu_main(args):
                 f4 = FLOPS_PER_UNIT[dom4["name"]] * (N_C4 // 512)
             a4 = f4 * args.kk_steps / (dom4["ms"] / 1e3) / 1e12
             kk_roof = {"kernel_class": dom4["name"], "bound": "alu", "achieved": a4, "peak": peak_fp32,
+                       "isolated": isolated_classes(torch, make_kk, ring4, N_C4, rx4, True, dev, peak_fp32, 1),
                        "unit": "TFLOP/s", "frac": a4 / peak_fp32, "share_of_step": dom4["ms"] / r4["ms"]}
         elif dom4:
             kk_roof = {"kernel_class": dom4["name"], "share_of_step": dom4["ms"] / r4["ms"]}

@@ -81,7 +81,12 @@ typedef struct {
   int lms_segment;            /* S symbols per parallel segment: 4096; divides the epoch */
   int lms_overlap;            /* O warm-up symbols per segment (KK 256, PAM 0); multiple of B */
   int tap_lag_epochs;         /* D: seeds of epoch e are the mean canonical taps of e-D (8) */
-  int widely_linear;          /* reserved, must be 0 in this build (paper's WL DDLMS: next) */
+  int widely_linear;          /* KK only: 1 = widely-linear equaliser, y = w^H u + v^H conj(u)
+                                 (the paper's "widely-linear TD DDLMS", compensating Tx
+                                 IQ imbalance), run as the segmented block-LMS of SURVEY c-9: the
+                                 v-branch is trained with w, and every decision-directed segment
+                                 starts its v-branch at 0 (DESIGN reading R-WL); 0 = strictly
+                                 linear. PAM: must be 0 */
   double mu;                  /* block-sum LMS step (1e-3 PAM, 2e-3 KK) */
   int train_symbols;          /* data-aided training symbols after sync (8192); multiple of B */
   int cfo_enable;             /* KK: per-buffer 4th-power CFO estimate + removal (1) */
@@ -99,6 +104,11 @@ typedef struct {
                                  pending (more concurrent segment-warps per launch; results do
                                  not depend on it; adds latency); 0 = every call */
   int input_format;           /* rx_input_format of every rx_process call of this handle */
+  int serial_equaliser;       /* 0 (default): each rx_process call forks the equaliser stage (sync,
+                                 training, LMS rounds, stitching, labels, counters) on the data the
+                                 earlier calls normalised onto an internal stream, concurrent with
+                                 its own front-end; 1: everything in order on cuda_stream (for
+                                 isolated kernel timing). Results are identical either way */
 } rx_config;
 
 /* Sample formats accepted by rx_process:
@@ -164,7 +174,8 @@ rx_status rx_export_counters(rx_handle *h, double *d_out, void *cuda_stream);
 rx_status rx_reset_stats(rx_handle *h, void *cuda_stream);
 
 /* Trained taps W_train (after sync + training): K values (PAM) or 2K interleaved (KK),
- * host_out capacity in doubles. Synchronises the handle's last stream. */
+ * host_out capacity in doubles; a widely-linear handle also writes V_train (2K interleaved)
+ * after W_train when capacity >= 4K. Synchronises the device. */
 rx_status rx_get_taps(rx_handle *h, double *host_out, int capacity);
 
 /* Start taps of the training pass, replacing the centre spike of SURVEY c-9 'Training':

@@ -675,16 +675,16 @@ def lms_full(v, stride, off, m_end, ref_idx_fn, ref_val_fn, slicer: _Slicer, lp:
     s0 = m0 // lp.S
     L = slicer.L
 
-    canon_v = np.zeros_like(canon)
-    seeds_v = {}
-
     def seed(s):
         e = (s * lp.S) // lp.E
         w = w_train if e < lp.D else seeds[e]
         if seed_rotation is not None:
             w = w * (1j) ** int(seed_rotation(s))
-        if lp.widely_linear:   # (w, v): the v-branch seeds follow the same rule (DESIGN R-WL)
-            return w, (v_train if e < lp.D else seeds_v[e])
+        if lp.widely_linear:
+            # (w, v): every decision-directed segment starts its v-branch at 0 (DESIGN R-WL): the
+            # conjugate branch's value depends on the absolute carrier phase during the segment
+            # (v/w = -e^{-2j phi} conj(beta)/alpha), which no earlier frame knows
+            return w, np.zeros_like(w)
         return w
 
     for wave in range(0, n_epoch, lp.D):
@@ -725,15 +725,10 @@ def lms_full(v, stride, off, m_end, ref_idx_fn, ref_val_fn, slicer: _Slicer, lp:
                 # average, phi_s = arg(sum_k w_k |w_k|); carrier phase noise decorrelates the
                 # absolute frame across an epoch, and CPR + stitching absorb the common phase.
                 w = r["w"]
-                rot = np.exp(-1j * np.angle(np.sum(w * np.abs(w))))
-                canon[s] = w * rot
-                # widely linear: y = w^H u + v^H conj(u); (c w)^H u + (c v)^H conj(u) = c* y, so
-                # the v-branch takes the same factor (DESIGN R-WL)
-                canon_v[s] = r["v"] * rot
+                canon[s] = w * np.exp(-1j * np.angle(np.sum(w * np.abs(w))))
         for e in range(wave, min(n_epoch, wave + lp.D)):
             lo, hi = e * seg_per_epoch, min(n_seg, (e + 1) * seg_per_epoch)
             seeds[e + lp.D] = np.mean(canon[lo:hi], axis=0)
-            seeds_v[e + lp.D] = np.mean(canon_v[lo:hi], axis=0)
     # assemble outputs over m in [0, m_end)
     shape = (m_end,) if real else (m_end, 2)
     idx_out = np.zeros(shape, dtype=np.int64)
@@ -747,7 +742,8 @@ def lms_full(v, stride, off, m_end, ref_idx_fn, ref_val_fn, slicer: _Slicer, lp:
         z_out[mm] = r["z"][sel]
         seg_of[mm] = s
     return dict(idx=idx_out, z=z_out, R=R, r_rel=r_rel, w_train=w_train, v_train=v_train,
-                canon=canon, canon_v=canon_v, diverged=diverged, seg_of=seg_of)
+                canon=canon, diverged=diverged, seg_of=seg_of,
+                seg_v=[r["v"] for r in results], seg_w=[r["w"] for r in results])
 
 
 # ============================================================================ c-11

@@ -164,6 +164,7 @@ struct LmsSmemT {
   using T = typename LmsElem<CPLX>::T;
   alignas(16) T ring[2 * LMS_RING];
   alignas(16) T w[32];
+  alignas(16) T v[32];      // widely-linear branch (KK, widely_linear = 1)
   alignas(16) T e[32];
   alignas(16) float2 y[32];
 };
@@ -304,9 +305,12 @@ __device__ __forceinline__ float level_of(int i, float two_s, float off) { retur
 // the block, lane k tap k; the inputs stream through a per-warp mirrored shared-memory ring
 // filled LMS_AHEAD blocks ahead with cp.async, so the serial block recursion never waits on
 // HBM and every window access is an immediate offset.
-template <bool CPLX, int CPR, int MODE, int KP>
+//
+// WLIN (KK): widely-linear form of c-9, y = w^H u + v^H conj(u), v <- v + mu sum conj(u) conj(e)
+// (the paper's "widely-linear TD DDLMS"; DESIGN reading R-WL); lane k also owns v_k.
+template <bool CPLX, int CPR, int MODE, int KP, bool WLIN = false>
 __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, long long t_end,
-                         long long out_lo, float2 &wk, unsigned char *warm, double &evn,
+                         long long out_lo, float2 &wk, float2 &vk, unsigned char *warm, double &evn,
                          double &evd, long long vend, int bps_bar = 0, float2 *bps_part = nullptr) {
   using T = typename LmsElem<CPLX>::T;
   const int lane = threadIdx.x & 31;
@@ -336,6 +340,10 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
   const int tq = lane >> 3, tr = lane & 7;
   const int io = TILED ? 4 * tr + tq : lane;
   if (lane >= K) wk = make_float2(0.f, 0.f);
+  if constexpr (WLIN) {
+    if (lane >= K) vk = make_float2(0.f, 0.f);
+    reinterpret_cast<float2 *>(sm.v)[lane] = vk;
+  }
   if (CPLX) reinterpret_cast<float2 *>(sm.w)[lane] = wk;
   else reinterpret_cast<float *>(sm.w)[lane] = wk.x;
   if (TILED) {
@@ -401,6 +409,19 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
           A.y = fmaf(ww.x, u0.y, fmaf(-ww.y, u0.x, A.y));
           A.x = fmaf(ww.z, u1.x, fmaf(ww.w, u1.y, A.x));
           A.y = fmaf(ww.z, u1.y, fmaf(-ww.w, u1.x, A.y));
+        }
+        if constexpr (WLIN) {   // + sum_k conj(v_k u_k): (vx ux - vy uy) - j (vx uy + vy ux)
+          const float4 *v4 = reinterpret_cast<const float4 *>(sm.v);
+#pragma unroll
+          for (int k = 0; k < KP; k += 2) {
+            const float4 vv = v4[k >> 1];
+            const float2 u0 = as_c(ub[-k]), u1 = as_c(ub[-k - 1]);
+            float2 &A = a[(k >> 1) & 3];
+            A.x = fmaf(vv.x, u0.x, fmaf(-vv.y, u0.y, A.x));
+            A.y = fmaf(-vv.x, u0.y, fmaf(-vv.y, u0.x, A.y));
+            A.x = fmaf(vv.z, u1.x, fmaf(-vv.w, u1.y, A.x));
+            A.y = fmaf(-vv.z, u1.y, fmaf(-vv.w, u1.x, A.y));
+          }
         }
       } else {
         const float4 *w4 = reinterpret_cast<const float4 *>(sm.w);
@@ -535,6 +556,24 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
           G.x = fmaf(u1.x, ee.z, fmaf(u1.y, ee.w, G.x));
           G.y = fmaf(u1.y, ee.z, fmaf(-u1.x, ee.w, G.y));
         }
+        if constexpr (WLIN) {   // h_k = sum_i u_i[k] e_i; v_k <- v_k + mu conj(h_k)
+          float2 hh[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const float4 ee = e4[i >> 1];
+            const float2 u0 = as_c(ug[stride * i]), u1 = as_c(ug[stride * (i + 1)]);
+            float2 &H = hh[(i >> 1) & 1];
+            H.x = fmaf(u0.x, ee.x, fmaf(-u0.y, ee.y, H.x));
+            H.y = fmaf(u0.x, ee.y, fmaf(u0.y, ee.x, H.y));
+            H.x = fmaf(u1.x, ee.z, fmaf(-u1.y, ee.w, H.x));
+            H.y = fmaf(u1.x, ee.w, fmaf(u1.y, ee.z, H.y));
+          }
+          if (lane < K) {
+            vk.x = fmaf(mu, hh[0].x + hh[1].x, vk.x);
+            vk.y = fmaf(-mu, hh[0].y + hh[1].y, vk.y);
+          }
+          reinterpret_cast<float2 *>(sm.v)[lane] = vk;
+        }
       } else {
         const float4 *e4 = reinterpret_cast<const float4 *>(sm.e);
 #pragma unroll
@@ -592,7 +631,7 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
 }
 
 // ------------------------------------------------------------------ training (1 warp)
-template <bool CPLX, int KP>
+template <bool CPLX, int KP, bool WLIN = false>
 __global__ void __launch_bounds__(32) k_lms_train(RxDev d, int flush) {
   __shared__ LmsSmemT<CPLX> sm;
   DevState *st = d.st;
@@ -605,8 +644,10 @@ __global__ void __launch_bounds__(32) k_lms_train(RxDev d, int flush) {
   float2 wk = make_float2(lane == c ? 1.f : 0.f, 0.f);    // centre spike ...
   if (d.has_winit) wk = lane < K ? d.w_init[lane] : make_float2(0.f, 0.f);   // ... or rx_set_taps
   double en = 0.0, ed = 0.0;
-  lms_run<CPLX, 0, 0, KP>(d, sm, d.m0, d.m0 + d.T_train, 0, wk, nullptr, en, ed, vend);
+  float2 vk = make_float2(0.f, 0.f);                      // widely-linear branch starts at 0
+  lms_run<CPLX, 0, 0, KP, WLIN>(d, sm, d.m0, d.m0 + d.T_train, 0, wk, vk, nullptr, en, ed, vend);
   if (lane < K) d.w_train[lane] = wk;
+  if (WLIN && lane < K) d.v_train[lane] = vk;
   __threadfence();
   if (lane == 0) { st->trained = 1; d.hm->trained = 1; }
 }
@@ -690,7 +731,7 @@ __device__ void bps_helper(const RxDev &d, const float2 *ys, long long t_begin, 
 
 // ------------------------------------------------------------------ segments (1 warp each)
 // Segment s outputs [sS, min((s+1)S, m_end)), recursion starts O symbols early (c-9).
-template <bool CPLX, int CPR, int KP>
+template <bool CPLX, int CPR, int KP, bool WLIN = false>
 __global__ void __launch_bounds__(128) k_lms_seg(RxDev d, int flush, int nseg, unsigned char *labels,
                                                  long long lab_cap) {
   // BPS segments run on a warp pair (LMS warp + BPS helper), others on one warp
@@ -717,7 +758,9 @@ __global__ void __launch_bounds__(128) k_lms_seg(RxDev d, int flush, int nseg, u
   }
   // seed: W_train for e < D, else the mean canonical taps of epoch e - D (c-9 'Seed')
   const long long e = lo / d.E_sym;
-  float2 wk = make_float2(0.f, 0.f);
+  // widely linear: the v-branch of every decision-directed segment starts at 0 (reading R-WL:
+  // its value depends on the absolute carrier phase during the segment, v/w = -e^{-2j phi} b*/a)
+  float2 wk = make_float2(0.f, 0.f), vk = make_float2(0.f, 0.f);
   if (e < d.D) {
     if (lane < K) wk = d.w_train[lane];
   } else {
@@ -732,8 +775,8 @@ __global__ void __launch_bounds__(128) k_lms_seg(RxDev d, int flush, int nseg, u
     bps_helper(d, sm[warp].y, t0, hi, 1 + slot, bps_part[slot]);
     return;
   }
-  const float th = lms_run<CPLX, CPR, 1, KP>(d, sm[warp], t0, hi, lo, wk, warm, en, ed, vend,
-                                             PAIR == 2 ? 1 + slot : 0, bps_part[slot]);
+  const float th = lms_run<CPLX, CPR, 1, KP, WLIN>(d, sm[warp], t0, hi, lo, wk, vk, warm, en, ed, vend,
+                                                   PAIR == 2 ? 1 + slot : 0, bps_part[slot]);
   en = warp_sum_d(en);
   ed = warp_sum_d(ed);
   const long long si = rmod(s, d.seg_cap);
@@ -1091,27 +1134,31 @@ __global__ void __launch_bounds__(1024) k_lms_seeds(RxDev d, int flush) {
   long long s_hi = s_lo + spe;
   if (s_hi > hi) s_hi = hi;
   const int t = threadIdx.x, k = t >> 5, lane = t & 31;
-  float sx = 0.f, sy = 0.f;
-  if (k < d.K) {
-    long long s = s_lo + lane;
-    for (; s + 96 < s_hi; s += 128) {          // 4 independent loads in flight, summed in order
-      const float2 w0 = d.seg_w[rmod(s, d.seg_cap) * RX_MAX_K + k];
-      const float2 w1 = d.seg_w[rmod(s + 32, d.seg_cap) * RX_MAX_K + k];
-      const float2 w2 = d.seg_w[rmod(s + 64, d.seg_cap) * RX_MAX_K + k];
-      const float2 w3 = d.seg_w[rmod(s + 96, d.seg_cap) * RX_MAX_K + k];
-      sx += w0.x; sy += w0.y; sx += w1.x; sy += w1.y;
-      sx += w2.x; sy += w2.y; sx += w3.x; sy += w3.y;
+  // mean over the epoch's segments of the canonical taps
+  {
+    const float2 *src = d.seg_w;
+    float sx = 0.f, sy = 0.f;
+    if (k < d.K) {
+      long long s = s_lo + lane;
+      for (; s + 96 < s_hi; s += 128) {          // 4 independent loads in flight, summed in order
+        const float2 w0 = src[rmod(s, d.seg_cap) * RX_MAX_K + k];
+        const float2 w1 = src[rmod(s + 32, d.seg_cap) * RX_MAX_K + k];
+        const float2 w2 = src[rmod(s + 64, d.seg_cap) * RX_MAX_K + k];
+        const float2 w3 = src[rmod(s + 96, d.seg_cap) * RX_MAX_K + k];
+        sx += w0.x; sy += w0.y; sx += w1.x; sy += w1.y;
+        sx += w2.x; sy += w2.y; sx += w3.x; sy += w3.y;
+      }
+      for (; s < s_hi; s += 32) {
+        const float2 w = src[rmod(s, d.seg_cap) * RX_MAX_K + k];
+        sx += w.x; sy += w.y;
+      }
     }
-    for (; s < s_hi; s += 32) {
-      const float2 w = d.seg_w[rmod(s, d.seg_cap) * RX_MAX_K + k];
-      sx += w.x; sy += w.y;
+    sx = warp_sum(sx);
+    sy = warp_sum(sy);
+    if (k < d.K && lane == 0) {
+      const float inv = 1.0f / (float)(s_hi - s_lo);
+      d.seed[rmod(tgt, d.seed_cap) * RX_MAX_K + k] = make_float2(sx * inv, sy * inv);
     }
-  }
-  sx = warp_sum(sx);
-  sy = warp_sum(sy);
-  if (k < d.K && lane == 0) {
-    const float inv = 1.0f / (float)(s_hi - s_lo);
-    d.seed[rmod(tgt, d.seed_cap) * RX_MAX_K + k] = make_float2(sx * inv, sy * inv);
   }
   __syncthreads();
   if (t == 0) { __threadfence(); d.seed_ready[rmod(tgt, d.seed_cap)] = (int)(tgt + 1); }

@@ -202,7 +202,7 @@ static rx_status validate(const rx_config *c) {
   if (c->lms_overlap < 0 || c->lms_overlap % 32 || c->lms_overlap > RX_MAX_O || c->lms_overlap > c->lms_segment) return RX_EINVAL;
   if (c->family == RX_PAM && c->lms_overlap != 0) return RX_EINVAL;
   if (c->tap_lag_epochs < 1 || c->tap_lag_epochs > 32) return RX_EINVAL;
-  if (c->widely_linear != 0) return RX_EINVAL;
+  if (c->widely_linear != 0 && (c->widely_linear != 1 || c->family != RX_QAM_KK)) return RX_EINVAL;
   if (!(c->mu > 0) || c->mu > 1.0) return RX_EINVAL;
   if (c->train_symbols < 32 || c->train_symbols % 32) return RX_EINVAL;
   if (c->cpr_test_phases < 0 || c->cpr_test_phases > RX_MAX_PT) return RX_EINVAL;
@@ -212,6 +212,7 @@ static rx_status validate(const rx_config *c) {
   if (c->clock_avg_half < 0 || c->clock_avg_half > 2048) return RX_EINVAL;
   if (c->history_buffers < 3 || c->history_buffers > 64) return RX_EINVAL;
   if (c->input_format != RX_IN_U12_IN_U16 && c->input_format != RX_IN_F32) return RX_EINVAL;
+  if (c->serial_equaliser != 0 && c->serial_equaliser != 1) return RX_EINVAL;
   if (c->lms_batch_segments < 0 || c->lms_batch_segments > (1 << 16)) return RX_EINVAL;
   if (c->family == RX_QAM_KK && !(c->sideband == 1 || c->sideband == -1)) return RX_EINVAL;
   if (c->family == RX_PAM && c->thresholds) {
@@ -450,6 +451,8 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   TRY(dalloc(h, &d.w_init, RX_MAX_K));
   d.seed_cap = 64;
   TRY(dalloc(h, &d.seed, d.seed_cap * RX_MAX_K));
+  d.wl = c.widely_linear;
+  if (d.wl) TRY(dalloc(h, &d.v_train, RX_MAX_K));
   TRY(dalloc(h, &d.seed_ready, d.seed_cap));
   d.seg_cap = next_pow2(d.sym_cap / c.lms_segment + 8);
   TRY(dalloc(h, &d.seg_w, d.seg_cap * RX_MAX_K));
@@ -536,27 +539,33 @@ static unsigned gridc(long long n, int per) { return (unsigned)((n + per - 1) / 
 typedef void (*lms_seg_fn)(RxDev, int, int, unsigned char *, long long);
 typedef void (*lms_train_fn)(RxDev, int);
 static int kp_of(int K) { return K <= 4 ? 4 : (K <= 8 ? 8 : (K <= 16 ? 16 : 32)); }
-template <bool CPLX, int CPR>
+template <bool CPLX, int CPR, bool WL = false>
 static lms_seg_fn seg_kp(int K) {
   switch (kp_of(K)) {
-    case 4: return k_lms_seg<CPLX, CPR, 4>;
-    case 8: return k_lms_seg<CPLX, CPR, 8>;
-    case 16: return k_lms_seg<CPLX, CPR, 16>;
-    default: return k_lms_seg<CPLX, CPR, 32>;
+    case 4: return k_lms_seg<CPLX, CPR, 4, WL>;
+    case 8: return k_lms_seg<CPLX, CPR, 8, WL>;
+    case 16: return k_lms_seg<CPLX, CPR, 16, WL>;
+    default: return k_lms_seg<CPLX, CPR, 32, WL>;
   }
 }
 static lms_seg_fn lms_seg_kernel(const RxDev &d) {
   if (d.family == RX_PAM) return seg_kp<false, 0>(d.K);
+  if (d.wl) return d.cpr == 1 ? seg_kp<true, 1, true>(d.K) : seg_kp<true, 2, true>(d.K);
   return d.cpr == 1 ? seg_kp<true, 1>(d.K) : seg_kp<true, 2>(d.K);
 }
-template <bool CPLX>
-static lms_train_fn lms_train_kernel(int K) {
+template <bool CPLX, bool WL = false>
+static lms_train_fn lms_train_kp(int K) {
   switch (kp_of(K)) {
-    case 4: return k_lms_train<CPLX, 4>;
-    case 8: return k_lms_train<CPLX, 8>;
-    case 16: return k_lms_train<CPLX, 16>;
-    default: return k_lms_train<CPLX, 32>;
+    case 4: return k_lms_train<CPLX, 4, WL>;
+    case 8: return k_lms_train<CPLX, 8, WL>;
+    case 16: return k_lms_train<CPLX, 16, WL>;
+    default: return k_lms_train<CPLX, 32, WL>;
   }
+}
+template <bool CPLX>
+static lms_train_fn lms_train_kernel(const RxDev &d) {
+  if (CPLX && d.wl) return lms_train_kp<true, true>(d.K);
+  return lms_train_kp<CPLX>(d.K);
 }
 
 template <bool CPLX>
@@ -569,7 +578,7 @@ static void launch_sync_train(rx_handle *h, cudaStream_t s, int flush) {
     KLAUNCH(h, RX_K_SYNC, s, (k_sync_corr<CPLX><<<gridc((long long)nh * RX_PREF, 256), 256, smem, s>>>(d)));
     KLAUNCH(h, RX_K_SYNC, s, (k_sync_pick<CPLX><<<1, 1024, 0, s>>>(d, flush)));
   }
-  KLAUNCH(h, RX_K_SYNC, s, (lms_train_kernel<CPLX>(d.K)<<<1, 32, 0, s>>>(d, flush)));
+  KLAUNCH(h, RX_K_SYNC, s, (lms_train_kernel<CPLX>(d)<<<1, 32, 0, s>>>(d, flush)));
 }
 
 static void launch_lms_round(rx_handle *h, cudaStream_t s, unsigned char *labels, long long lab_cap,
@@ -787,10 +796,18 @@ extern "C" rx_status rx_process(rx_handle *h, const void *d_samples, long long n
   h->n_in += n;
   unsigned char *lab = labels_capacity ? d_labels : nullptr;
   const long long cap = labels_capacity ? labels_capacity : 1;
-  fork_equaliser(h, s, lab, cap);
+  const bool serial = h->cfg.serial_equaliser != 0;
+  if (!serial) fork_equaliser(h, s, lab, cap);
   if (h->d.family == RX_PAM) run_pam(h, s, in, lab, cap, 0);
   else run_kk(h, s, in, lab, cap, 0);
-  CK(cudaStreamWaitEvent(s, h->ev_join, 0));
+  if (serial) {   // same stages, in order on the caller's stream, on everything normalised so far
+    KLAUNCH(h, RX_K_MISC, s, (k_lms_snapshot<<<1, 1, 0, s>>>(h->d)));
+    if (h->d.family == RX_PAM) launch_sync_train<false>(h, s, 0);
+    else launch_sync_train<true>(h, s, 0);
+    launch_lms_rounds(h, s, lab, cap, 0, h->lms_sym_ub);
+  } else {
+    CK(cudaStreamWaitEvent(s, h->ev_join, 0));
+  }
   return check_launch();
 }
 
@@ -853,6 +870,10 @@ extern "C" rx_status rx_get_taps(rx_handle *h, double *out, int capacity) {
   for (int k = 0; k < h->d.K; ++k) {
     if (kk) { out[2 * k] = w[k].x; out[2 * k + 1] = w[k].y; }
     else out[k] = w[k].x;
+  }
+  if (h->d.wl && capacity >= 2 * need) {   // widely linear: V_train follows W_train
+    CK(cudaMemcpy(w, h->d.v_train, sizeof(float2) * h->d.K, cudaMemcpyDeviceToHost));
+    for (int k = 0; k < h->d.K; ++k) { out[need + 2 * k] = w[k].x; out[need + 2 * k + 1] = w[k].y; }
   }
   return RX_OK;
 }

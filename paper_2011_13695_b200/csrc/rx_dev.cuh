@@ -101,6 +101,8 @@ struct RxDev {
   float2 *w_init;                  // [K] start taps of training (rx_set_taps)
   int has_winit;
   float2 *seed; int *seed_ready; long long seed_cap;   // per epoch [K]
+  int wl;                          // widely-linear equaliser (KK)
+  float2 *v_train;                 // [K] trained v-branch (DD segments start theirs at 0)
   float2 *seg_w; float *seg_theta; int *seg_done; int *seg_stitched; int *seg_r; int *seg_R;
   double *seg_evm; long long *seg_err; long long seg_cap;
   unsigned char *seg_warm;         // [seg_cap][O]

@@ -43,6 +43,7 @@ class RxConfig(ctypes.Structure):
         ("warmup_symbols", _c_ll), ("history_buffers", ctypes.c_int),
         ("lms_batch_segments", ctypes.c_int),
         ("input_format", ctypes.c_int),
+        ("serial_equaliser", ctypes.c_int),
     ]
 
 
@@ -200,11 +201,16 @@ class Receiver:
         _check(load().rx_reset_stats(self._h, _stream_ptr(stream)), "rx_reset_stats")
 
     def train_taps(self) -> np.ndarray:
+        """W_train (K real / complex); widely linear: (W_train, V_train)."""
         K = self.cfg.lms_taps
-        n = 2 * K if self.family == RX_QAM_KK else K
+        wl = self.family == RX_QAM_KK and self.cfg.widely_linear
+        n = (4 if wl else 2) * K if self.family == RX_QAM_KK else K
         out = np.zeros(n, dtype=np.float64)
         _check(load().rx_get_taps(self._h, out.ctypes.data_as(_c_dp), n), "rx_get_taps")
-        return out[0::2] + 1j * out[1::2] if self.family == RX_QAM_KK else out
+        if self.family != RX_QAM_KK:
+            return out
+        c = out[0::2] + 1j * out[1::2]
+        return (c[:K], c[K:]) if wl else c
 
     def set_taps(self, w) -> None:
         """Start taps of the training pass (rx_set_taps); K real (PAM) or K complex (KK)."""
