@@ -542,53 +542,65 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
         if (fabsf(wk.x) > 1e3f) set_flag(d.st, RX_FLAG_DIVERGE);
       }
     } else {
-      const T *ug = win + KP - 1 - (lane < KP ? lane : 0);     // lanes >= KP: discarded
-      float2 g[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      // lane = (group, tap kt): tap kt = lane % KP sums the block's symbols i in [i0, i0 + KP),
+      // i0 = KP * group; the 32 / KP group partials are combined by xor shuffles, so no lane
+      // works on a padding tap and every lane ends with its tap's full sum
+      const int kt = lane & (KP - 1), i0 = lane & ~(KP - 1);
+      const T *ug = win + KP - 1 - kt + stride * i0;
+      float2 g[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      float2 hh[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};   // WLIN: sum_i u_i[k] e_i
       if (CPLX) {
-        const float4 *e4 = reinterpret_cast<const float4 *>(sm.e);
+        const float4 *e4 = reinterpret_cast<const float4 *>(sm.e) + (i0 >> 1);
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) {
+        for (int i = 0; i < KP; i += 2) {
           const float4 ee = e4[i >> 1];                         // e_i, e_{i+1} (broadcast)
           const float2 u0 = as_c(ug[stride * i]), u1 = as_c(ug[stride * (i + 1)]);
-          float2 &G = g[(i >> 1) & 3];
+          float2 &G = g[(i >> 1) & 1];
           G.x = fmaf(u0.x, ee.x, fmaf(u0.y, ee.y, G.x));
           G.y = fmaf(u0.y, ee.x, fmaf(-u0.x, ee.y, G.y));
           G.x = fmaf(u1.x, ee.z, fmaf(u1.y, ee.w, G.x));
           G.y = fmaf(u1.y, ee.z, fmaf(-u1.x, ee.w, G.y));
-        }
-        if constexpr (WLIN) {   // h_k = sum_i u_i[k] e_i; v_k <- v_k + mu conj(h_k)
-          float2 hh[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-          for (int i = 0; i < 32; i += 2) {
-            const float4 ee = e4[i >> 1];
-            const float2 u0 = as_c(ug[stride * i]), u1 = as_c(ug[stride * (i + 1)]);
+          if constexpr (WLIN) {
             float2 &H = hh[(i >> 1) & 1];
             H.x = fmaf(u0.x, ee.x, fmaf(-u0.y, ee.y, H.x));
             H.y = fmaf(u0.x, ee.y, fmaf(u0.y, ee.x, H.y));
             H.x = fmaf(u1.x, ee.z, fmaf(-u1.y, ee.w, H.x));
             H.y = fmaf(u1.x, ee.w, fmaf(u1.y, ee.z, H.y));
           }
-          if (lane < K) {
-            vk.x = fmaf(mu, hh[0].x + hh[1].x, vk.x);
-            vk.y = fmaf(-mu, hh[0].y + hh[1].y, vk.y);
-          }
-          reinterpret_cast<float2 *>(sm.v)[lane] = vk;
         }
       } else {
-        const float4 *e4 = reinterpret_cast<const float4 *>(sm.e);
+        const float4 *e4 = reinterpret_cast<const float4 *>(sm.e) + (i0 >> 2);
 #pragma unroll
-        for (int i = 0; i < 32; i += 4) {
+        for (int i = 0; i < KP; i += 4) {
           const float4 ee = e4[i >> 2];
-          float2 &G = g[(i >> 2) & 3];
+          float2 &G = g[(i >> 2) & 1];
           G.x = fmaf(as_c(ug[i]).x, ee.x, G.x);
           G.x = fmaf(as_c(ug[i + 1]).x, ee.y, G.x);
           G.x = fmaf(as_c(ug[i + 2]).x, ee.z, G.x);
           G.x = fmaf(as_c(ug[i + 3]).x, ee.w, G.x);
         }
       }
+      float gx = g[0].x + g[1].x, gy = g[0].y + g[1].y;
+      float hx = hh[0].x + hh[1].x, hy = hh[0].y + hh[1].y;
+#pragma unroll
+      for (int o = KP; o < 32; o <<= 1) {
+        gx += __shfl_xor_sync(0xffffffffu, gx, o);
+        if (CPLX) gy += __shfl_xor_sync(0xffffffffu, gy, o);
+        if (WLIN) {
+          hx += __shfl_xor_sync(0xffffffffu, hx, o);
+          hy += __shfl_xor_sync(0xffffffffu, hy, o);
+        }
+      }
+      if constexpr (WLIN) {   // v_k <- v_k + mu conj(h_k)
+        if (lane < K) {
+          vk.x = fmaf(mu, hx, vk.x);
+          vk.y = fmaf(-mu, hy, vk.y);
+        }
+        reinterpret_cast<float2 *>(sm.v)[lane] = vk;
+      }
       if (lane < K) {
-        wk.x = fmaf(mu, (g[0].x + g[1].x) + (g[2].x + g[3].x), wk.x);
-        if (CPLX) wk.y = fmaf(mu, (g[0].y + g[1].y) + (g[2].y + g[3].y), wk.y);
+        wk.x = fmaf(mu, gx, wk.x);
+        if (CPLX) wk.y = fmaf(mu, gy, wk.y);
         // divergence (reading R-DIV): any single tap beyond 1e3 flags at once,
         // the full norm is checked at the end of the run
         if (cabs2(wk) > 1e6f) set_flag(d.st, RX_FLAG_DIVERGE);
