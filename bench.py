@@ -307,6 +307,63 @@ def isolated_classes(torch, make_rx, ring, n_step, rx, kk, dev, peak, steps=2):
     return out
 
 
+def _gen_c3(cspr):
+    from rxsynth import make_config
+    return make_config("C3", cspr_db=cspr)
+
+
+def c3_sweep(torch, dev, local):
+    """BASELINE.json configs[2]: 1 GBaud KK QAM-4 with a 20 MHz frequency offset at
+    OSNR 10 dB, swept over the carrier-to-signal power ratio (P:246 reports the optimum near
+    6 dB); one 16,776,704-sample record per point through a fresh handle, device-resident input,
+    CUDA events around each record's rx_process calls + flush."""
+    import concurrent.futures as cf
+    import ctypes
+    import multiprocessing as mp
+    from paper_2011_13695_b200 import RX_QAM_KK, Receiver
+    from rxsynth.configs import C3_CSPR_DB
+    t0 = time.time()
+    with cf.ProcessPoolExecutor(max_workers=min(8, os.cpu_count() or 1),
+                                mp_context=mp.get_context("spawn")) as ex:
+        recs = list(ex.map(_gen_c3, C3_CSPR_DB))
+    t_gen = time.time() - t0
+    st = torch.cuda.Stream(device=dev)
+    sp = ctypes.c_void_p(st.cuda_stream)
+    lab = torch.zeros(1 << 24, dtype=torch.uint8, device=dev)
+    pts, ms_tot, n_tot = [], 0.0, 0
+    for cspr, (rec, rx) in zip(C3_CSPR_DB, recs):
+        codes = torch.from_numpy(rec.codes.view("int16")).to(dev)
+        R = Receiver(RX_QAM_KK, rec.M, rec.static_taps, device=local, dc_offset=rec.dc_offset,
+                     history_buffers=CALL_BUFFERS + 2, **rx_fields(rx))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for off in range(0, rec.n, CHUNK):
+            n = min(CHUNK, rec.n - off)
+            R.process_ptr(codes.data_ptr() + 2 * off, n, lab.data_ptr(), lab.numel(), sp)
+        R.flush(lab, stream=st)
+        e1.record(st)
+        s1 = R.stats(st)
+        ms = e0.elapsed_time(e1)
+        ms_tot += ms
+        n_tot += rec.n
+        ber = s1["bit_errors"] / max(s1["bits"], 1)
+        pts.append({"cspr_db": cspr, "ber": ber, "evm_db": round(10 * math.log10(s1["evm_num"] / s1["evm_den"]), 3)
+                    if s1["evm_den"] > 0 else None, "domain_errors": s1["domain_errors"],
+                    "sync_gamma": round(s1["sync_gamma"], 4), "ms": round(ms, 3)})
+        R.close()
+    best = min(pts, key=lambda p: p["ber"])
+    return {"workload": "C3: KK QAM-4 1 GBaud 4 sps, +20 MHz CFO, 100 kHz linewidth, OSNR 10 dB, "
+                        "CSPR sweep, 16,776,704 samples per point (one record, streamed + flushed)",
+            "points": pts, "best_cspr_db": best["cspr_db"], "paper_optimum_cspr_db": 6,
+            "value": round(n_tot / (ms_tot / 1e3) / 1e9, 3), "unit": "GSa/s",
+            "note": "value includes handle start-up (sync, training) and the flush of each record. "
+                    "At OSNR 10 dB and 100 kHz linewidth the non-differential CPR slips a quadrant "
+                    "now and then over 4.2 M symbols; segment stitching (SURVEY c-9) carries a slip "
+                    "into every later segment (no pilots), so BER jumps towards 0.5 from the first "
+                    "slip on. The GPU matches the oracle here (test_c3_cspr_sweep_parity)",
+            "gen_seconds": round(t_gen, 1)}
+
+
 def _gen_c5(ch):
     from rxsynth import make_config
     return make_config(f"C5:{ch}", keep_tx=True) if ch % 8 < 4 else make_config(f"C5:{ch}")
@@ -551,6 +608,9 @@ def gpu_main(args):
         R4.close()
         del ring4
         torch.cuda.empty_cache()
+    # ---- C3: CSPR sweep (N = 1)
+    if world == 1 and not args.no_c3:
+        line["c3_sweep"] = c3_sweep(torch, dev, local)
     # ---- C5: 8 mixed channels per GPU, concurrent streams (every N)
     if not args.no_c5:
         line["c5"] = c5_run(torch, dist, rank, world, dev, args.c5_steps, 2, args.ring_gib)
@@ -598,6 +658,7 @@ def main():
     ap.add_argument("--kk-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--no-c3", action="store_true")
     ap.add_argument("--c5-steps", type=int, default=4)
     ap.add_argument("--ring-gib", type=float, default=1.0)
     ap.add_argument("--lms-batch", type=int, default=0,

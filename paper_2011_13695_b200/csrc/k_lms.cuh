@@ -206,12 +206,15 @@ __device__ __forceinline__ void lms_stage(const RxDev &d, LmsSmemT<CPLX> &sm, lo
 // p + 32). Distances are in units of the level spacing 2s: u = y e^{-j phi_p} / 2s + (L - 1)/2
 // puts the levels on the integers 0..L-1, so |z - slice(z)|^2 = (2s)^2 sum (u - clamp(rint u))^2
 // (the common factor (2s)^2 does not move the argmin). Fixed summation order.
-__device__ __forceinline__ float bps_dist(float2 yi, float2 r, float cst, float Lm1) {
+// acc += |u - clamp(rint(u))|^2 over both axes of y e^{-j phi} / 2s + (L - 1)/2 (two FFMA
+// accumulations, no separate product)
+__device__ __forceinline__ void bps_acc(float2 yi, float2 r, float cst, float Lm1, float &acc) {
   const float ux = fmaf(yi.x, r.x, fmaf(-yi.y, r.y, cst));
   const float uy = fmaf(yi.x, r.y, fmaf(yi.y, r.x, cst));
   const float ex = ux - fminf(fmaxf(rintf(ux), 0.f), Lm1);
   const float ey = uy - fminf(fmaxf(rintf(uy), 0.f), Lm1);
-  return fmaf(ex, ex, ey * ey);
+  acc = fmaf(ex, ex, acc);
+  acc = fmaf(ey, ey, acc);
 }
 __device__ __forceinline__ void bps_partial(const float2 *ys, int i0, int i1, float2 rsA, float2 rsB, int L,
                                             bool two, float &dA, float &dB) {
@@ -222,17 +225,17 @@ __device__ __forceinline__ void bps_partial(const float2 *ys, int i0, int i1, fl
 #pragma unroll 4
   for (int i = 0; i < n2; ++i) {
     const float4 yy = y4[(i0 >> 1) + i];
-    a0 += bps_dist(make_float2(yy.x, yy.y), rsA, cst, Lm1);
-    a1 += bps_dist(make_float2(yy.z, yy.w), rsA, cst, Lm1);
+    bps_acc(make_float2(yy.x, yy.y), rsA, cst, Lm1, a0);
+    bps_acc(make_float2(yy.z, yy.w), rsA, cst, Lm1, a1);
     if (two) {
-      b0 += bps_dist(make_float2(yy.x, yy.y), rsB, cst, Lm1);
-      b1 += bps_dist(make_float2(yy.z, yy.w), rsB, cst, Lm1);
+      bps_acc(make_float2(yy.x, yy.y), rsB, cst, Lm1, b0);
+      bps_acc(make_float2(yy.z, yy.w), rsB, cst, Lm1, b1);
     }
   }
   if ((i1 - i0) & 1) {
     const float2 yi = ys[i1 - 1];
-    a0 += bps_dist(yi, rsA, cst, Lm1);
-    if (two) b0 += bps_dist(yi, rsB, cst, Lm1);
+    bps_acc(yi, rsA, cst, Lm1, a0);
+    if (two) bps_acc(yi, rsB, cst, Lm1, b0);
   }
   dA += a0 + a1;
   dB += b0 + b1;

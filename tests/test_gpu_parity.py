@@ -317,3 +317,22 @@ def test_widely_linear_iq_imbalance_parity(K):
           f"vs {st_lin['bit_errors']}/{st_lin['bits']}")
     assert gain > 2.0
     assert st["bit_errors"] <= st_lin["bit_errors"]
+
+
+@pytest.mark.parametrize("cspr", [2.0, 10.0])
+def test_c3_cspr_sweep_parity(cspr):
+    """BASELINE.json configs[2] sweeps the carrier-to-signal power ratio (the KK optimum
+    for QAM-4 at OSNR 10 dB is about 6 dB): the chain must match the oracle at every point,
+    including the low-CSPR end where the minimum-phase condition fails and the domain guard
+    (I + dc <= 0) fires."""
+    _torch_cuda()
+    rec, rx = make_config("C3", n_samples=1 << 20, cspr_db=cspr)
+    rx["buffer_blocks"] = 256
+    out = run_oracle(rec, rx)
+    R, labels, st = run_gpu(rec, rx, chunk=256 * 512)
+    assert st["domain_errors"] == out["domain"]
+    z = R.probe("Z", 0, out["z"].shape[0])
+    assert rel_l2(z, out["z"]) < TOL_FIELD
+    assert st["sync_offset"] == out["sync"]["offset"]
+    mism, excl = _compare_labels(rec, rx, out, labels, R)
+    _compare_counters(rec, out, st, mism)
