@@ -493,7 +493,8 @@ def gpu_main(args):
         return Receiver(RX_PAM, rec.M, rec.static_taps, device=local, history_buffers=CALL_BUFFERS + 2,
                         **({"lms_batch_segments": args.lms_batch} if args.lms_batch else {}),
                         **rx_fields(rx), **kw)
-    R = make_pam()
+    W21 = round(0.021 * 2e9 / 4096) * 4096     # 21 ms of 2 GBaud symbols, whole segments
+    R = make_pam(q_window_symbols=W21)
     res = run_mode(torch, dist, R, ring, n_step, args.steps, args.warmup, world, dev, None)
     value = world * n_step * args.steps / (res["ms"] / 1e3) / 1e9
     ms_step = res["ms"] / args.steps
@@ -550,6 +551,15 @@ def gpu_main(args):
                     "sync_gamma": st["sync_gamma"], "flags": st["status_flags"]},
         "gen_seconds": round(t_gen, 1),
     }
+    # ---- Q trace: BER in 21 ms sections, windows completed so far on this channel
+    from paper_2011_13695_b200 import multi as _multi
+    nwin = st["symbols_out"] // W21
+    if nwin > 0:
+        qe, qb = R.q_trace(0, int(nwin))
+        line["quality"]["q_trace_21ms"] = {
+            "window_symbols": W21, "windows": int(nwin),
+            "q_db": [round(_multi.q_db_from_ber(int(e) / int(b)), 3) if b else None for e, b in zip(qe, qb)],
+            "note": "the first window includes the warm-up symbols, which are not counted"}
     # ---- e2e through the public API with host buffers
     e2e = e2e_run(torch, R, n_step, rec.codes, max(3, args.steps // 2), dev)
     e_ms = torch.tensor([e2e["ms"]], dtype=torch.float64, device=dev)

@@ -109,6 +109,10 @@ typedef struct {
                                  earlier calls normalised onto an internal stream, concurrent with
                                  its own front-end; 1: everything in order on cuda_stream (for
                                  isolated kernel timing). Results are identical either way */
+  long long q_window_symbols; /* > 0: also count bit errors / bits per window of this many
+                                 symbols (window w = symbols [w W, (w+1) W)), the paper's "Q
+                                 estimated from the BER in sections of 21 ms" (21 ms =
+                                 42 M symbols at 2 GBaud); a multiple of lms_segment; 0 = off */
 } rx_config;
 
 /* Sample formats accepted by rx_process:
@@ -169,6 +173,15 @@ rx_status rx_get_stats(rx_handle *h, rx_stats *host_out, void *cuda_stream);
  * all-reduce them with NCCL on the same stream (one collective per round). */
 #define RX_NCOUNTERS 8
 rx_status rx_export_counters(rx_handle *h, double *d_out, void *cuda_stream);
+
+/* Windowed BER counters (q_window_symbols > 0): synchronise cuda_stream and copy the bit errors
+ * and counted bits of windows [first_window, first_window + n) to host_errors / host_bits
+ * (n long longs each). Held: the window of the newest finalised symbol (still open: partial
+ * counts) and the RX_Q_WINDOWS - 1 windows before it. RX_EINVAL if the trace is off or a
+ * window is not held. rx_reset_stats does not clear the trace. */
+#define RX_Q_WINDOWS 4096
+rx_status rx_get_q_trace(rx_handle *h, long long first_window, int n, long long *host_errors,
+                         long long *host_bits, void *cuda_stream);
 
 /* Zero the BER/EVM/clip/domain counters (enqueued on cuda_stream). */
 rx_status rx_reset_stats(rx_handle *h, void *cuda_stream);

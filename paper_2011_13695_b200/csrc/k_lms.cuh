@@ -873,6 +873,32 @@ __device__ __forceinline__ void lms_add_counters(const RxDev &d, long long lo, l
 #pragma unroll
     for (int u = 0; u < 4; ++u) { en += ev[u].x; ed += ev[u].y; er += eg[u].x; ct += eg[u].y; }
   }
+  if (d.q_segs > 0) {
+    // Q-trace windows. Segments are finalised once each, in increasing order, by this
+    // single CTA: a window's ring slot is cleared in the round that finalises its first segment,
+    // then segments with the same window combine per warp, one atomic each
+    for (long long w = (lo + d.q_segs - 1) / d.q_segs + t; w * d.q_segs < hi; w += blockDim.x) {
+      unsigned long long *q = d.q_win + 2 * (w & (RX_Q_WINDOWS - 1));
+      q[0] = 0ull;
+      q[1] = 0ull;
+    }
+    __syncthreads();
+    for (long long b = lo; b < hi; b += blockDim.x) {
+      const long long s = b + t;
+      const unsigned act = __ballot_sync(0xffffffffu, s < hi);
+      if (s < hi) {
+        const long long w = s / d.q_segs;
+        const longlong2 eg = reinterpret_cast<const longlong2 *>(d.seg_err)[rmod(s, d.seg_cap)];
+        const unsigned m = __match_any_sync(act, w);
+        const unsigned e = __reduce_add_sync(m, (unsigned)eg.x), c = __reduce_add_sync(m, (unsigned)eg.y);
+        if ((t & 31) == __ffs(m) - 1) {
+          unsigned long long *q = d.q_win + 2 * (w & (RX_Q_WINDOWS - 1));
+          atomicAdd(q, (unsigned long long)e);
+          atomicAdd(q + 1, (unsigned long long)c);
+        }
+      }
+    }
+  }
   en = warp_sum_d(en);
   ed = warp_sum_d(ed);
   for (int o = 16; o > 0; o >>= 1) {

@@ -213,6 +213,7 @@ static rx_status validate(const rx_config *c) {
   if (c->history_buffers < 3 || c->history_buffers > 64) return RX_EINVAL;
   if (c->input_format != RX_IN_U12_IN_U16 && c->input_format != RX_IN_F32) return RX_EINVAL;
   if (c->serial_equaliser != 0 && c->serial_equaliser != 1) return RX_EINVAL;
+  if (c->q_window_symbols < 0 || (c->q_window_symbols > 0 && c->q_window_symbols % c->lms_segment)) return RX_EINVAL;
   if (c->lms_batch_segments < 0 || c->lms_batch_segments > (1 << 16)) return RX_EINVAL;
   if (c->family == RX_QAM_KK && !(c->sideband == 1 || c->sideband == -1)) return RX_EINVAL;
   if (c->family == RX_PAM && c->thresholds) {
@@ -453,6 +454,8 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   TRY(dalloc(h, &d.seed, d.seed_cap * RX_MAX_K));
   d.wl = c.widely_linear;
   if (d.wl) TRY(dalloc(h, &d.v_train, RX_MAX_K));
+  d.q_segs = c.q_window_symbols / c.lms_segment;
+  if (d.q_segs > 0) TRY(dalloc(h, &d.q_win, 2 * RX_Q_WINDOWS));
   TRY(dalloc(h, &d.seed_ready, d.seed_cap));
   d.seg_cap = next_pow2(d.sym_cap / c.lms_segment + 8);
   TRY(dalloc(h, &d.seg_w, d.seg_cap * RX_MAX_K));
@@ -992,6 +995,28 @@ extern "C" rx_status rx_profile_read(rx_handle *h, double *ms, long long *counts
     h->prof_free.push_back(e.second);
   }
   h->prof_pending.clear();
+  return RX_OK;
+}
+
+extern "C" rx_status rx_get_q_trace(rx_handle *h, long long first, int n, long long *err, long long *bits,
+                                    void *stream) {
+  if (!h || n < 0 || (n > 0 && (!err || !bits)) || first < 0 || h->d.q_segs <= 0) return RX_EINVAL;
+  if (n > RX_Q_WINDOWS) return RX_EINVAL;
+  CK(cudaSetDevice(h->device));
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  DevState st;
+  CK(cudaMemcpy(&st, h->st_dev, sizeof(st), cudaMemcpyDeviceToHost));
+  // held: the window of the newest finalised segment (possibly still open) and the
+  // RX_Q_WINDOWS - 1 before it (older slots have been reused)
+  const long long newest = st.seg_next > 0 ? (st.seg_next - 1) / h->d.q_segs : -1;
+  if (n > 0 && (first + n - 1 > newest || first < newest - RX_Q_WINDOWS + 1)) return RX_EINVAL;
+  std::vector<unsigned long long> q(2 * (size_t)RX_Q_WINDOWS);
+  CK(cudaMemcpy(q.data(), h->d.q_win, q.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < n; ++i) {
+    const long long w = (first + i) & (RX_Q_WINDOWS - 1);
+    err[i] = (long long)q[2 * w];
+    bits[i] = (long long)q[2 * w + 1] * h->d.kbits;
+  }
   return RX_OK;
 }
 

@@ -103,6 +103,8 @@ struct RxDev {
   float2 *seed; int *seed_ready; long long seed_cap;   // per epoch [K]
   int wl;                          // widely-linear equaliser (KK)
   float2 *v_train;                 // [K] trained v-branch (DD segments start theirs at 0)
+  long long q_segs;                // segments per Q-trace window (0 = off)
+  unsigned long long *q_win;       // [RX_Q_WINDOWS][2]: bit errors, counted symbols
   float2 *seg_w; float *seg_theta; int *seg_done; int *seg_stitched; int *seg_r; int *seg_R;
   double *seg_evm; long long *seg_err; long long seg_cap;
   unsigned char *seg_warm;         // [seg_cap][O]

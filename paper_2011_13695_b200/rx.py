@@ -44,6 +44,7 @@ class RxConfig(ctypes.Structure):
         ("lms_batch_segments", ctypes.c_int),
         ("input_format", ctypes.c_int),
         ("serial_equaliser", ctypes.c_int),
+        ("q_window_symbols", _c_ll),
     ]
 
 
@@ -63,7 +64,7 @@ class RxStats(ctypes.Structure):
 EXPORTS = ("rx_config_default", "rx_create", "rx_process", "rx_flush", "rx_get_stats",
            "rx_reset_stats", "rx_get_taps", "rx_probe_read", "rx_destroy", "rx_strerror",
            "rx_version", "rx_profile_enable", "rx_profile_read", "rx_export_counters",
-           "rx_set_taps")
+           "rx_set_taps", "rx_get_q_trace")
 NCOUNTERS = 8
 COUNTERS = ("bit_errors", "bits", "symbols_counted", "evm_num", "evm_den", "clipped",
             "domain_errors", "symbols_out")
@@ -102,6 +103,8 @@ def load(path: str = SO_PATH):
     lib.rx_export_counters.argtypes = [vp, vp, vp]
     lib.rx_export_counters.restype = ctypes.c_int
     lib.rx_profile_read.argtypes = [vp, _c_dp, ctypes.POINTER(_c_ll), ctypes.c_int]
+    lib.rx_get_q_trace.argtypes = [vp, _c_ll, ctypes.c_int, ctypes.POINTER(_c_ll), ctypes.POINTER(_c_ll), vp]
+    lib.rx_get_q_trace.restype = ctypes.c_int
     for f in ("rx_create", "rx_process", "rx_flush", "rx_get_stats", "rx_reset_stats",
               "rx_get_taps", "rx_set_taps", "rx_probe_read", "rx_profile_enable", "rx_profile_read"):
         getattr(lib, f).restype = ctypes.c_int
@@ -191,6 +194,15 @@ class Receiver:
         st = RxStats()
         _check(load().rx_get_stats(self._h, ctypes.byref(st), _stream_ptr(stream)), "rx_get_stats")
         return {k: getattr(st, k) for k, _ in RxStats._fields_}
+
+    def q_trace(self, first: int, n: int, stream=None):
+        """Windowed (bit_errors, bits) of Q-trace windows [first, first + n) (rx_get_q_trace)."""
+        err = np.zeros(n, dtype=np.int64)
+        bits = np.zeros(n, dtype=np.int64)
+        _check(load().rx_get_q_trace(self._h, first, n, err.ctypes.data_as(ctypes.POINTER(_c_ll)),
+                                     bits.ctypes.data_as(ctypes.POINTER(_c_ll)), _stream_ptr(stream)),
+               "rx_get_q_trace")
+        return err, bits
 
     def export_counters(self, out, stream=None):
         """Enqueue a device copy of the counters into `out` (float64 CUDA tensor, >= 8)."""

@@ -336,3 +336,35 @@ def test_c3_cspr_sweep_parity(cspr):
     assert st["sync_offset"] == out["sync"]["offset"]
     mism, excl = _compare_labels(rec, rx, out, labels, R)
     _compare_counters(rec, out, st, mism)
+
+
+def test_q_trace_windows_match_oracle_counts():
+    """Windowed BER counters (P:336 'Q estimated from the BER in sections of 21 ms', scaled down
+    to 8-segment windows): per-window bit errors and bits equal the oracle's per-symbol error
+    counts binned by window, the windows sum to the totals, and rx_get_q_trace refuses windows
+    that are not held."""
+    _torch_cuda()
+    from paper_2011_13695_b200 import RxError
+    rec, rx = make_config("C2", n_samples=1 << 21)
+    W = 8 * 4096
+    rx.update(buffer_blocks=256, q_window_symbols=W)
+    out = run_oracle(rec, rx)
+    R, labels, st = run_gpu(rec, rx, chunk=256 * 512)
+    m_end = out["m_end"]
+    nwin = -(-m_end // W)
+    err_g, bits_g = R.q_trace(0, nwin)
+    assert int(err_g.sum()) == st["bit_errors"] and int(bits_g.sum()) == st["bits"]
+    labr, _, _ = O.reference(rec.fmt, rec.M)
+    m = np.arange(m_end)
+    ref = labr[(out["sync"]["offset"] + m - rx["sync_start"]) % O.P_REF]
+    e = O.popcount(out["labels"][:m_end].astype(np.int64) ^ ref)
+    counted = m >= rx["warmup_symbols"]
+    err_o = np.bincount(m[counted] // W, weights=e[counted], minlength=nwin).astype(np.int64)
+    bits_o = np.bincount(m[counted] // W, minlength=nwin).astype(np.int64) * int(round(math.log2(rec.M)))
+    assert np.array_equal(bits_g, bits_o)
+    mism = out["labels"][:m_end] != labels[:m_end]
+    k = int(round(math.log2(rec.M)))
+    allow = np.bincount(m[mism & counted] // W, minlength=nwin) * k
+    assert np.all(np.abs(err_g - err_o) <= allow), (err_g, err_o)
+    with pytest.raises(RxError):
+        R.q_trace(nwin, 1)
