@@ -655,6 +655,23 @@ static void launch_lms_rounds(rx_handle *h, cudaStream_t s, unsigned char *label
   }
 }
 
+// H8: normalisation of every buffer whose symbols are complete (all of them at flush)
+static void launch_norm_pam(rx_handle *h, cudaStream_t s, int flush) {
+  RxDev &d = h->d;
+  const long long BB = d.buffer_blocks;
+  long long nbuf = 0;
+  while ((h->norm_done + nbuf + 1) * BB <= h->be_done || (flush && (h->norm_done + nbuf) * BB < h->be_done)) ++nbuf;
+  if (nbuf == 0) return;
+  const long long beta0 = h->norm_done;
+  const long long bend = h->be_done;
+  for (long long b0 = 0; b0 < nbuf; b0 += 16) {
+    const long long nb = nbuf - b0 < 16 ? nbuf - b0 : 16;
+    KLAUNCH(h, RX_K_NORM, s, (k_norm_stats<<<dim3(NORM_G, (unsigned)nb), 1024, 0, s>>>(d, beta0 + b0, bend, flush)));
+    KLAUNCH(h, RX_K_NORM, s, (k_norm_apply<<<dim3(NORM_AG, (unsigned)nb), 256, 0, s>>>(d, beta0 + b0, nb, bend, flush)));
+  }
+  h->norm_done += nbuf;
+}
+
 static void run_pam(rx_handle *h, cudaStream_t s, const InView &in, unsigned char *labels,
                     long long lab_cap, int flush) {
   RxDev &d = h->d;
@@ -686,20 +703,9 @@ static void run_pam(rx_handle *h, cudaStream_t s, const InView &in, unsigned cha
     else KLAUNCH(h, RX_K_PAM_BE, s, (k_pam_be<false><<<gridc(be_target - h->be_done, FE_GROUPS), 256, 0, s>>>(d, h->be_done, be_target)));
     h->be_done = be_target;
   }
-  {
-    long long nbuf = 0;
-    while ((h->norm_done + nbuf + 1) * BB <= h->be_done || (flush && (h->norm_done + nbuf) * BB < h->be_done)) ++nbuf;
-    if (nbuf > 0) {
-      const long long beta0 = h->norm_done;
-      const long long bend = h->be_done;
-      for (long long b0 = 0; b0 < nbuf; b0 += 16) {
-        const long long nb = nbuf - b0 < 16 ? nbuf - b0 : 16;
-        KLAUNCH(h, RX_K_NORM, s, (k_norm_stats<<<dim3(NORM_G, (unsigned)nb), 1024, 0, s>>>(d, beta0 + b0, bend, flush)));
-        KLAUNCH(h, RX_K_NORM, s, (k_norm_apply<<<dim3(NORM_AG, (unsigned)nb), 256, 0, s>>>(d, beta0 + b0, nb, bend, flush)));
-      }
-      h->norm_done += nbuf;
-    }
-  }
+  // streaming: the buffer normalisation runs on the equaliser side stream at the start of the
+  // next call (fork_equaliser), ahead of the equaliser that consumes it
+  if (flush || h->cfg.serial_equaliser) launch_norm_pam(h, s, flush);
   if (flush) KLAUNCH(h, RX_K_MISC, s, (k_pam_mend<<<1, 1, 0, s>>>(d, h->be_done > 0 ? h->be_done : 0)));
   h->lms_sym_ub = 256 * h->be_done + h->be_done / 4 + 4096;
   if (flush) {
@@ -759,11 +765,19 @@ static void run_kk(rx_handle *h, cudaStream_t s, const InView &in, unsigned char
 // do not depend on it (the equaliser output is independent of how its rounds are batched).
 static void fork_equaliser(rx_handle *h, cudaStream_t s, unsigned char *labels, long long lab_cap) {
   RxDev &d = h->d;
-  KLAUNCH(h, RX_K_MISC, s, (k_lms_snapshot<<<1, 1, 0, s>>>(d)));
+  // KK: z' (and v_front) are written by this call's CFO stage on the caller's stream, so the
+  // snapshot is taken there first. PAM: the normalisation of the earlier calls' buffers moves
+  // to the side stream too (it only feeds the equaliser), ahead of the snapshot.
+  if (d.family != RX_PAM) KLAUNCH(h, RX_K_MISC, s, (k_lms_snapshot<<<1, 1, 0, s>>>(d)));
   cudaEventRecord(h->ev_fork, s);
   cudaStreamWaitEvent(h->side, h->ev_fork, 0);
-  if (d.family == RX_PAM) launch_sync_train<false>(h, h->side, 0);
-  else launch_sync_train<true>(h, h->side, 0);
+  if (d.family == RX_PAM) {
+    launch_norm_pam(h, h->side, 0);
+    KLAUNCH(h, RX_K_MISC, h->side, (k_lms_snapshot<<<1, 1, 0, h->side>>>(d)));
+    launch_sync_train<false>(h, h->side, 0);
+  } else {
+    launch_sync_train<true>(h, h->side, 0);
+  }
   launch_lms_rounds(h, h->side, labels, lab_cap, 0, h->lms_sym_ub);
   cudaEventRecord(h->ev_join, h->side);
 }
