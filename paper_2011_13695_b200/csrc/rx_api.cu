@@ -69,6 +69,8 @@ struct rx_handle {
   cudaStream_t side;
   cudaEvent_t ev_fork, ev_join;
   long long lms_sym_ub;          // symbol upper bound of the data normalised by earlier calls
+  struct ZpJob { long long beta0, nb, q_front; };
+  std::vector<ZpJob> zp_pending; // KK: CFO carry + z' groups deferred to the next call's side stream
   long long clk_launch;          // fused clock launches so far (tags the tile totals)
   bool flushed;
   long long launches;
@@ -433,7 +435,8 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
     TRY(dalloc(h, &d.clk_flag, maxtiles));
   } else {
     d.E_cap = next_pow2((long long)HB * c.buffer_blocks * 512);
-    d.z_cap = next_pow2((long long)HB * c.buffer_blocks * 256);
+    // (+ one call: the side stream's z' pass reads the previous call's z while stage 2 writes)
+    d.z_cap = next_pow2((long long)(HB + HB - 2) * c.buffer_blocks * 256);
     TRY(dalloc(h, &d.E, d.E_cap));
     TRY(dalloc(h, &d.z, d.z_cap));
     d.zp_cap = next_pow2((long long)(HB + HB - 2) * c.buffer_blocks * 256 + 2 * batch_sym);
@@ -715,9 +718,20 @@ static void run_pam(rx_handle *h, cudaStream_t s, const InView &in, unsigned cha
   }
 }
 
+// KK: the deferred CFO carry + z' groups, in buffer order (the DDS origin is a chain)
+static void launch_zp_pending(rx_handle *h, cudaStream_t s) {
+  RxDev &d = h->d;
+  for (const auto &j : h->zp_pending) {
+    KLAUNCH(h, RX_K_CFO, s, (k_cfo_carry<<<1, 1, 0, s>>>(d, j.beta0, (int)j.nb)));
+    KLAUNCH(h, RX_K_CFO, s, (k_kk_zprime<<<2048, 256, 0, s>>>(d, j.beta0, (int)j.nb, j.q_front)));
+  }
+  h->zp_pending.clear();
+}
+
 static void run_kk(rx_handle *h, cudaStream_t s, const InView &in, unsigned char *labels,
                    long long lab_cap, int flush) {
   RxDev &d = h->d;
+  if (flush) launch_zp_pending(h, s);
   const long long s1_target = h->n_in / 512;
   if (s1_target > h->fe_done) {
     KLAUNCH(h, RX_K_KK_S1, s, (k_kk_s1<<<gridc(s1_target - h->fe_done, FE_GROUPS), 256, 0, s>>>(d, in, h->fe_done, s1_target)));
@@ -743,8 +757,12 @@ static void run_kk(rx_handle *h, cudaStream_t s, const InView &in, unsigned char
         KLAUNCH(h, RX_K_CFO, s, (k_cfo_spec<<<dim3((unsigned)nrows, (unsigned)nb), 1024, smem, s>>>(d, beta0 + b0, q_front)));
         KLAUNCH(h, RX_K_CFO, s, (k_cfo_final<<<(unsigned)nb, 1024, 0, s>>>(d, beta0 + b0, q_front, nrows)));
         if (d.cfo_enable) KLAUNCH(h, RX_K_CFO, s, (k_cfo_fine<<<dim3((unsigned)fine_ctas, (unsigned)nb), 256, 0, s>>>(d, beta0 + b0, q_front, fine_ctas)));
-        KLAUNCH(h, RX_K_CFO, s, (k_cfo_carry<<<1, 1, 0, s>>>(d, beta0 + b0, (int)nb)));
-        KLAUNCH(h, RX_K_CFO, s, (k_kk_zprime<<<2048, 256, 0, s>>>(d, beta0 + b0, (int)nb, q_front)));
+        if (flush || h->cfg.serial_equaliser) {
+          KLAUNCH(h, RX_K_CFO, s, (k_cfo_carry<<<1, 1, 0, s>>>(d, beta0 + b0, (int)nb)));
+          KLAUNCH(h, RX_K_CFO, s, (k_kk_zprime<<<2048, 256, 0, s>>>(d, beta0 + b0, (int)nb, q_front)));
+        } else {   // the DDS carry and z' only feed the equaliser: next call, side stream
+          h->zp_pending.push_back({beta0 + b0, nb, q_front});
+        }
       }
       h->cfo_done += nbuf;
     }
@@ -765,19 +783,15 @@ static void run_kk(rx_handle *h, cudaStream_t s, const InView &in, unsigned char
 // do not depend on it (the equaliser output is independent of how its rounds are batched).
 static void fork_equaliser(rx_handle *h, cudaStream_t s, unsigned char *labels, long long lab_cap) {
   RxDev &d = h->d;
-  // KK: z' (and v_front) are written by this call's CFO stage on the caller's stream, so the
-  // snapshot is taken there first. PAM: the normalisation of the earlier calls' buffers moves
-  // to the side stream too (it only feeds the equaliser), ahead of the snapshot.
-  if (d.family != RX_PAM) KLAUNCH(h, RX_K_MISC, s, (k_lms_snapshot<<<1, 1, 0, s>>>(d)));
+  // The stages that only feed the equaliser move to the side stream too, ahead of the snapshot:
+  // PAM: the normalisation of the earlier calls' buffers; KK: their CFO carry and z'.
   cudaEventRecord(h->ev_fork, s);
   cudaStreamWaitEvent(h->side, h->ev_fork, 0);
-  if (d.family == RX_PAM) {
-    launch_norm_pam(h, h->side, 0);
-    KLAUNCH(h, RX_K_MISC, h->side, (k_lms_snapshot<<<1, 1, 0, h->side>>>(d)));
-    launch_sync_train<false>(h, h->side, 0);
-  } else {
-    launch_sync_train<true>(h, h->side, 0);
-  }
+  if (d.family == RX_PAM) launch_norm_pam(h, h->side, 0);
+  else launch_zp_pending(h, h->side);
+  KLAUNCH(h, RX_K_MISC, h->side, (k_lms_snapshot<<<1, 1, 0, h->side>>>(d)));
+  if (d.family == RX_PAM) launch_sync_train<false>(h, h->side, 0);
+  else launch_sync_train<true>(h, h->side, 0);
   launch_lms_rounds(h, h->side, labels, lab_cap, 0, h->lms_sym_ub);
   cudaEventRecord(h->ev_join, h->side);
 }
