@@ -356,11 +356,9 @@ def c3_sweep(torch, dev, local):
                         "CSPR sweep, 16,776,704 samples per point (one record, streamed + flushed)",
             "points": pts, "best_cspr_db": best["cspr_db"], "paper_optimum_cspr_db": 6,
             "value": round(n_tot / (ms_tot / 1e3) / 1e9, 3), "unit": "GSa/s",
-            "note": "value includes handle start-up (sync, training) and the flush of each record. "
-                    "At OSNR 10 dB and 100 kHz linewidth the non-differential CPR slips a quadrant "
-                    "now and then over 4.2 M symbols; segment stitching (SURVEY c-9) carries a slip "
-                    "into every later segment (no pilots), so BER jumps towards 0.5 from the first "
-                    "slip on. The GPU matches the oracle here (test_c3_cspr_sweep_parity)",
+            "note": "value includes handle start-up (sync, training) and the flush of each record; "
+                    "at fixed OSNR a high CSPR leaves too little signal power, a low one breaks the "
+                    "minimum-phase condition (domain errors)",
             "gen_seconds": round(t_gen, 1)}
 
 

@@ -91,6 +91,11 @@ typedef struct {
   int train_symbols;          /* data-aided training symbols after sync (8192); multiple of B */
   int cfo_enable;             /* KK: per-buffer 4th-power CFO estimate + removal (1) */
   int cpr_test_phases;        /* KK: 0 = Viterbi-Viterbi (QAM-4), else BPS test phases (<= 64) */
+  int cpr_anchor;             /* KK quadrant of each equaliser segment: 1 (default) = anchored to
+                                 the known PRBS reference over its first 256 symbols (BER-tester
+                                 mode, DESIGN reading R-ANCHOR2: a slip cannot propagate); 0 = the
+                                 SURVEY c-9 stitch chain R_s = R_{s-1} + r_s from the warm-up
+                                 overlap (no reference needed after segment s0) */
   unsigned prbs_order;        /* 15: PRBS x^15+x^14+1 reference (BER tester) */
   unsigned prbs_seed;         /* 0x7FFF */
   long long sync_start;       /* m0: first symbol of the sync window (4096); multiple of

@@ -489,6 +489,7 @@ class LmsParams:
     cpr: str = "none"           # "none" (PAM) | "vv" | "bps"
     P_t: int = 32
     widely_linear: bool = False
+    anchor_each: bool = False   # QAM: every segment's quadrant from the reference (DESIGN R-ANCHOR2)
 
 
 def tap_matrix(v: np.ndarray, m: np.ndarray, stride: int, off: int, K: int) -> np.ndarray:
@@ -693,7 +694,21 @@ def lms_full(v, stride, off, m_end, ref_idx_fn, ref_val_fn, slicer: _Slicer, lp:
         diverged |= dv
         for r in res:
             results[r["s"]] = r
-        if lp.O > 0 and not real:
+        if not real and lp.anchor_each:
+            # DESIGN reading R-ANCHOR2 (BER-tester mode): every segment is anchored to the known
+            # reference like segment s0 (R-ANCHOR), R_s = argmax_r #{m in its first 256 output
+            # symbols (from m0 for s0) : d_m j^r = ref_m}, lowest r on ties; no chain, so a
+            # wrong quadrant decision cannot propagate into later segments
+            for s in segs:
+                cur = results[s]
+                a0 = m0 if s == s0 else s * lp.S
+                sel = (cur["m"] >= a0) & (cur["m"] < a0 + 256) & (cur["m"] >= cur["lo"])
+                ref_i = ref_idx_fn(cur["m"][sel])
+                counts = [int(np.sum(np.all(rotate_indices(cur["idx"][sel], r, L) == ref_i, axis=1)))
+                          for r in range(4)]
+                R[s] = int(np.argmax(counts))
+                r_rel[s] = (R[s] - R[s - 1]) % 4 if s > 0 else 0
+        elif lp.O > 0 and not real:
             # stitching (c-9 'Stitching'): r_s from the warm-up overlap with segment s-1
             for s in segs:
                 if s == 0:
@@ -802,6 +817,7 @@ class RxParams:
     lms_overlap: int = 0
     tap_lag_epochs: int = 8
     widely_linear: bool = False
+    cpr_anchor: int = 1        # QAM: 1 = every segment anchored to the reference, 0 = c-9 chain
     mu: float = 1e-3
     train_symbols: int = 8192
     cpr_test_phases: int = 0
@@ -822,7 +838,8 @@ def _lms_params(p: RxParams) -> LmsParams:
         cpr = "vv" if p.cpr_test_phases == 0 else "bps"
     return LmsParams(K=p.lms_taps, B=p.lms_block, S=p.lms_segment, O=p.lms_overlap, mu=p.mu,
                      T_train=p.train_symbols, D=p.tap_lag_epochs, E=E, cpr=cpr,
-                     P_t=max(p.cpr_test_phases, 1), widely_linear=p.widely_linear)
+                     P_t=max(p.cpr_test_phases, 1), widely_linear=p.widely_linear,
+                     anchor_each=bool(p.cpr_anchor) and p.fmt != "pam")
 
 
 def _finish(p: RxParams, v, stride, off, m_end, sync, out):

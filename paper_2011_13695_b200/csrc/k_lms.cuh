@@ -823,8 +823,39 @@ __global__ void __launch_bounds__(256) k_lms_stitch(RxDev d, int nseg) {
   if (blockIdx.x >= nseg) return;
   const long long si = rmod(s, d.seg_cap);
   if (d.seg_done[si] != s + 1 || d.seg_stitched[si] == s + 1) return;
-  if (s > 0 && d.seg_done[rmod(s - 1, d.seg_cap)] != s) return;
   if (threadIdx.x < 4) cnt[threadIdx.x] = 0;
+  if (d.anchor_each) {
+    // R-ANCHOR2: R_s = argmax_r #{m in the segment's first 256 outputs (from m0 for s0) :
+    // d_m j^r = ref_m}, lowest r on ties; stored as the absolute quadrant (no prefix chain)
+    __syncthreads();
+    const long long a0 = (s == d.m0 / d.S) ? d.m0 : s * (long long)d.S;
+    long long a1 = a0 + 256;
+    const long long hi = seg_end_of(d, s);
+    if (a1 > hi) a1 = hi;
+    int c4[4] = {0, 0, 0, 0};
+    for (long long m = a0 + threadIdx.x; m < a1; m += blockDim.x) {
+      const int cur = d.level[rmod(m, d.sym_cap)];
+      const long long ri = ((d.st->sync_offset + m - d.m0) % RX_PREF + RX_PREF) % RX_PREF;
+      const int ref = d.ref_idx[ri];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) c4[r] += (qam_rot(cur, r, d.L) == ref);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int v = __reduce_add_sync(0xffffffffu, c4[r]);
+      if ((threadIdx.x & 31) == 0) atomicAdd(&cnt[r], v);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int best = 0;
+      for (int r = 1; r < 4; ++r) if (cnt[r] > cnt[best]) best = r;
+      d.seg_r[si] = best;
+      __threadfence();
+      d.seg_stitched[si] = (int)(s + 1);
+    }
+    return;
+  }
+  if (s > 0 && d.seg_done[rmod(s - 1, d.seg_cap)] != s) return;
   __syncthreads();
   const bool doit = (d.family == 1) && d.O > 0 && s > 0;
   if (doit) {
@@ -955,6 +986,10 @@ __global__ void __launch_bounds__(1024) k_lms_prefix(RxDev d, int flush, int max
   __shared__ int A_sh, known_sh;
   if (t == 0) { A_sh = st->anchor_A; known_sh = st->anchor_known; }
   __syncthreads();
+  if (!known_sh && d.anchor_each) {   // R-ANCHOR2: every R_s is absolute (k_lms_stitch)
+    if (t == 0) { A_sh = 0; known_sh = 1; }
+    __syncthreads();
+  }
   if (!known_sh) {
     const long long me = st->m_end;
     const bool s0_exists = !(me >= 0 && s0 * (long long)d.S >= me);
@@ -996,7 +1031,12 @@ __global__ void __launch_bounds__(1024) k_lms_prefix(RxDev d, int flush, int max
   // prefix of r over [base, base + n) in chunks of 1024 (QAM; PAM has R_s = 0): warp shuffle
   // scans + one scan of the 32 warp totals
   int carry = (int)(st->r_prefix & 3);
-  if (d.family == 1) {
+  if (d.family == 1 && d.anchor_each) {
+    for (int i = t; i < n; i += blockDim.x) {
+      const long long si = rmod(base + i, d.seg_cap);
+      d.seg_R[si] = d.seg_r[si];
+    }
+  } else if (d.family == 1) {
     __shared__ int wsum[32];
     const int lane = t & 31, warp = t >> 5;
     for (int c0 = 0; c0 < n; c0 += 1024) {

@@ -156,6 +156,7 @@ extern "C" void rx_config_default(rx_config *c, int family, int order) {
   c->train_symbols = 8192;
   c->cfo_enable = 1;
   c->cpr_test_phases = order == 4 ? 0 : 32;
+  c->cpr_anchor = 1;
   c->prbs_order = 15;
   c->prbs_seed = 0x7FFF;
   c->sync_start = 4096;
@@ -215,6 +216,7 @@ static rx_status validate(const rx_config *c) {
   if (c->history_buffers < 3 || c->history_buffers > 64) return RX_EINVAL;
   if (c->input_format != RX_IN_U12_IN_U16 && c->input_format != RX_IN_F32) return RX_EINVAL;
   if (c->serial_equaliser != 0 && c->serial_equaliser != 1) return RX_EINVAL;
+  if (c->cpr_anchor != 0 && c->cpr_anchor != 1) return RX_EINVAL;
   if (c->q_window_symbols < 0 || (c->q_window_symbols > 0 && c->q_window_symbols % c->lms_segment)) return RX_EINVAL;
   if (c->lms_batch_segments < 0 || c->lms_batch_segments > (1 << 16)) return RX_EINVAL;
   if (c->family == RX_QAM_KK && !(c->sideband == 1 || c->sideband == -1)) return RX_EINVAL;
@@ -288,6 +290,7 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   d.D = c.tap_lag_epochs;
   d.cpr = kk ? (c.cpr_test_phases == 0 ? 1 : 2) : 0;
   d.Pt = c.cpr_test_phases;
+  d.anchor_each = kk && c.cpr_anchor;
   d.mu = (float)c.mu;
   d.T_train = c.train_symbols;
   d.m0 = c.sync_start;

@@ -60,6 +60,7 @@ struct RxDev {
   int buffer_blocks;
   long long E_sym;           // symbols per LMS epoch
   int K, B, S, O, D, cpr, Pt;
+  int anchor_each;           // KK: every segment's quadrant from the reference (R-ANCHOR2)
   float mu;
   int T_train;
   long long m0;

@@ -38,6 +38,7 @@ class RxConfig(ctypes.Structure):
         ("widely_linear", ctypes.c_int),
         ("mu", ctypes.c_double), ("train_symbols", ctypes.c_int),
         ("cfo_enable", ctypes.c_int), ("cpr_test_phases", ctypes.c_int),
+        ("cpr_anchor", ctypes.c_int),
         ("prbs_order", ctypes.c_uint), ("prbs_seed", ctypes.c_uint),
         ("sync_start", _c_ll), ("sync_window", ctypes.c_int), ("sync_min_corr", ctypes.c_double),
         ("warmup_symbols", _c_ll), ("history_buffers", ctypes.c_int),

@@ -210,6 +210,58 @@ def test_stitching_resolves_forced_segment_quadrants():
     assert np.all(good)
 
 
+def _slip_stream(n, m0, o, slip_at):
+    """Noiseless QAM-16 on the T/2 grid, static phase 0.2 rad, plus a quarter-turn carrier slip
+    (phase + pi/2) from symbol slip_at on."""
+    _, idx_ref, vals_ref = O.reference("qam", 16)
+    m = np.arange(n)
+    sym = vals_ref[(o + m - m0) % O.P_REF]
+    ph = np.exp(1j * (0.2 + (m >= slip_at) * math.pi / 2))
+    z = np.zeros(2 * n, dtype=np.complex128)
+    z[0::2] = sym * ph
+    z[1::2] = 0.5 * (sym + np.roll(sym, -1)) * ph
+    return z, idx_ref, vals_ref, m
+
+
+@pytest.mark.parametrize("anchor_each", [False, True])
+def test_quadrant_slip_chain_carries_it_anchoring_confines_it(anchor_each):
+    """A quarter-turn carrier slip inside segment 5 is tracked by the CPR unwrap as a quadrant
+    change (|jump| = pi/2 is ambiguous). The c-9 stitch chain (R_s = R_{s-1} + r_s) carries the
+    rotated frame into every later segment, so every later decision is rotated; per-segment
+    anchoring to the reference (DESIGN R-ANCHOR2) confines the damage to the rest of segment 5:
+    later segments decode error-free."""
+    n, m0, o, S = 40_000, 4096, 321, 4096
+    slip = 5 * S + 1000
+    z, idx_ref, vals_ref, m = _slip_stream(n, m0, o, slip)
+    lp = O.LmsParams(K=4, S=S, O=256, mu=1e-3, T_train=2048, E=1 << 20, cpr="bps", P_t=16,
+                     anchor_each=anchor_each)
+    lm = O.lms_full(z, 2, 0, n, lambda mm: idx_ref[(o + mm - m0) % O.P_REF],
+                    lambda mm: vals_ref[(o + mm - m0) % O.P_REF], O._Slicer("qam", 16), lp, False, m0)
+    good = np.all(lm["idx"] == idx_ref[(o + m - m0) % O.P_REF], axis=1)
+    assert np.all(good[64:slip])                          # before the slip: error free
+    later = good[6 * S:]
+    if anchor_each:
+        assert np.all(later)
+    else:
+        assert not np.any(later)                          # the rotated frame propagates
+
+
+def test_anchoring_resolves_forced_segment_quadrants():
+    """As test_stitching_resolves_forced_segment_quadrants, with every segment anchored to the
+    reference: R_s undoes each segment's forced seed rotation, zero errors."""
+    rng = np.random.default_rng(4)
+    n, m0, o = 40_000, 4096, 123
+    z, idx_ref, vals_ref, m = _slip_stream(n, m0, o, 10 * n)
+    lp = O.LmsParams(K=4, S=4096, O=256, mu=1e-3, T_train=2048, E=1 << 20, cpr="bps", P_t=16,
+                     anchor_each=True)
+    rot = rng.integers(0, 4, size=64)
+    lm = O.lms_full(z, 2, 0, n, lambda mm: idx_ref[(o + mm - m0) % O.P_REF],
+                    lambda mm: vals_ref[(o + mm - m0) % O.P_REF], O._Slicer("qam", 16), lp, False, m0,
+                    seed_rotation=lambda s: rot[s])
+    assert len(set(((lm["R"] - rot[:len(lm["R"])]) % 4).tolist())) == 1
+    assert np.all(np.all(lm["idx"][64:] == idx_ref[(o + m[64:] - m0) % O.P_REF], axis=1))
+
+
 # ---------------------------------------------------------------- CFO
 
 @pytest.mark.parametrize("df", [0.0, 5e6, -20e6, 20e6, 37.3e6])
