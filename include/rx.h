@@ -188,6 +188,18 @@ rx_status rx_export_counters(rx_handle *h, double *d_out, void *cuda_stream);
 rx_status rx_get_q_trace(rx_handle *h, long long first_window, int n, long long *host_errors,
                          long long *host_bits, void *cuda_stream);
 
+/* PAM threshold calibration, the paper's "decision thresholds are optimized offline beforehand
+ * and uploaded", read as in SPEC S:361: on finalised symbols [first_symbol,
+ * first_symbol + count) still held in the device rings (after sync), the mean equaliser output
+ * of the symbols whose PRBS reference level is i gives level i's position; the thresholds are
+ * the midpoints between adjacent level means. Writes M-1 thresholds to host_thresholds and, if
+ * not NULL, the M level means to host_level_means (pass the thresholds to rx_config.thresholds
+ * of a new handle). Synchronises cuda_stream. RX_EINVAL: not PAM, range not finalised / held,
+ * or a level without symbols; RX_ESTATE: not synced. */
+rx_status rx_calibrate_thresholds(rx_handle *h, long long first_symbol, long long count,
+                                  double *host_thresholds, double *host_level_means,
+                                  void *cuda_stream);
+
 /* Zero the BER/EVM/clip/domain counters (enqueued on cuda_stream). */
 rx_status rx_reset_stats(rx_handle *h, void *cuda_stream);
 

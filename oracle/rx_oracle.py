@@ -761,6 +761,19 @@ def lms_full(v, stride, off, m_end, ref_idx_fn, ref_val_fn, slicer: _Slicer, lp:
                 seg_v=[r["v"] for r in results], seg_w=[r["w"] for r in results])
 
 
+# ============================================================================ calibration
+
+def calibrate_thresholds(y: np.ndarray, ref_level: np.ndarray, M: int):
+    """PAM decision thresholds "optimized offline beforehand and uploaded", by SPEC's
+    reading: level positions estimated on a calibration run - here data-aided, the mean
+    equalised value of the symbols whose reference level is i - and thresholds at the midpoints
+    between adjacent level means. Returns (thresholds [M-1], level means [M])."""
+    y = np.real(np.asarray(y, dtype=np.float64))
+    ref_level = np.asarray(ref_level)
+    means = np.array([np.mean(y[ref_level == i]) for i in range(M)])
+    return 0.5 * (means[:-1] + means[1:]), means
+
+
 # ============================================================================ c-11
 
 def count_errors(fmt, M, idx, z, slicer: _Slicer, ref_labels_fn, m_lo, m_hi):

@@ -40,6 +40,38 @@ __global__ void k_kk_mend(RxDev d, long long q_end) {
   }
 }
 __global__ void k_lms_snapshot(RxDev d) { d.st->v_lms = d.st->v_front; }
+
+// PAM threshold calibration: per-CTA, per-reference-level sums and counts of the
+// equaliser output over symbols [m0, m1), each thread in a fixed order, then a fixed-order CTA
+// reduction (deterministic); the host adds the CTA partials in order
+#define CAL_G 148
+__global__ void __launch_bounds__(256) k_calib_levels(RxDev d, long long m0, long long m1) {
+  __shared__ double ss[8][16], sc[8][16];
+  double s[16], c[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) { s[i] = 0.0; c[i] = 0.0; }
+  const long long o = d.st->sync_offset;
+  for (long long m = m0 + (long long)blockIdx.x * blockDim.x + threadIdx.x; m < m1;
+       m += (long long)gridDim.x * blockDim.x) {
+    const int lv = d.ref_idx[((o + m - d.m0) % RX_PREF + RX_PREF) % RX_PREF];
+    const double y = (double)d.yout[rmod(m, d.sym_cap)].x;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) if (i == lv) { s[i] += y; c[i] += 1.0; }
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const double a = warp_sum_d(s[i]), b = warp_sum_d(c[i]);
+    if (lane == 0) { ss[w][i] = a; sc[w][i] = b; }
+  }
+  __syncthreads();
+  if (threadIdx.x < 16) {
+    double a = 0.0, b = 0.0;
+    for (int k = 0; k < 8; ++k) { a += ss[k][threadIdx.x]; b += sc[k][threadIdx.x]; }
+    d.cal_part[(blockIdx.x * 16 + threadIdx.x) * 2] = a;
+    d.cal_part[(blockIdx.x * 16 + threadIdx.x) * 2 + 1] = b;
+  }
+}
 __global__ void k_export_counters(const DevState *st, double *o) {
   o[0] = (double)st->bit_errors; o[1] = (double)st->bits; o[2] = (double)st->symbols_counted;
   o[3] = st->evm_num; o[4] = st->evm_den; o[5] = (double)st->clipped;
@@ -460,6 +492,7 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   TRY(dalloc(h, &d.seed, d.seed_cap * RX_MAX_K));
   d.wl = c.widely_linear;
   if (d.wl) TRY(dalloc(h, &d.v_train, RX_MAX_K));
+  if (!kk) TRY(dalloc(h, &d.cal_part, (long long)CAL_G * 16 * 2));
   d.q_segs = c.q_window_symbols / c.lms_segment;
   if (d.q_segs > 0) TRY(dalloc(h, &d.q_win, 2 * RX_Q_WINDOWS));
   TRY(dalloc(h, &d.seed_ready, d.seed_cap));
@@ -1026,6 +1059,36 @@ extern "C" rx_status rx_profile_read(rx_handle *h, double *ms, long long *counts
     h->prof_free.push_back(e.second);
   }
   h->prof_pending.clear();
+  return RX_OK;
+}
+
+extern "C" rx_status rx_calibrate_thresholds(rx_handle *h, long long first, long long count, double *thr,
+                                             double *means, void *stream) {
+  if (!h || !thr || first < 0 || count <= 0 || h->d.family != RX_PAM) return RX_EINVAL;
+  CK(cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaStreamSynchronize(s));
+  DevState st;
+  CK(cudaMemcpy(&st, h->st_dev, sizeof(st), cudaMemcpyDeviceToHost));
+  if (!st.synced) return RX_ESTATE;
+  // finalised and still held by the symbol rings (with a one-call margin for the writers)
+  const long long held_lo = st.symbols_out - h->d.sym_cap / 2;
+  if (first + count > st.symbols_out || first < held_lo) return RX_EINVAL;
+  KLAUNCH(h, RX_K_MISC, s, (k_calib_levels<<<CAL_G, 256, 0, s>>>(h->d, first, first + count)));
+  if (check_launch() != RX_OK) return RX_ECUDA;
+  std::vector<double> part((size_t)CAL_G * 16 * 2);
+  CK(cudaMemcpyAsync(part.data(), h->d.cal_part, part.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const int M = h->d.M;
+  std::vector<double> mu(M);
+  for (int i = 0; i < M; ++i) {
+    double a = 0.0, b = 0.0;
+    for (int g = 0; g < CAL_G; ++g) { a += part[(g * 16 + i) * 2]; b += part[(g * 16 + i) * 2 + 1]; }
+    if (b <= 0.0) return RX_EINVAL;
+    mu[i] = a / b;
+  }
+  for (int i = 0; i + 1 < M; ++i) thr[i] = 0.5 * (mu[i] + mu[i + 1]);
+  if (means) for (int i = 0; i < M; ++i) means[i] = mu[i];
   return RX_OK;
 }
 

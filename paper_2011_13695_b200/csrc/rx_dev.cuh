@@ -104,6 +104,7 @@ struct RxDev {
   float2 *seed; int *seed_ready; long long seed_cap;   // per epoch [K]
   int wl;                          // widely-linear equaliser (KK)
   float2 *v_train;                 // [K] trained v-branch (DD segments start theirs at 0)
+  double *cal_part;                // PAM threshold calibration partials [CAL_G][16][2]
   long long q_segs;                // segments per Q-trace window (0 = off)
   unsigned long long *q_win;       // [RX_Q_WINDOWS][2]: bit errors, counted symbols
   float2 *seg_w; float *seg_theta; int *seg_done; int *seg_stitched; int *seg_r; int *seg_R;

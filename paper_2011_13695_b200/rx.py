@@ -65,7 +65,7 @@ class RxStats(ctypes.Structure):
 EXPORTS = ("rx_config_default", "rx_create", "rx_process", "rx_flush", "rx_get_stats",
            "rx_reset_stats", "rx_get_taps", "rx_probe_read", "rx_destroy", "rx_strerror",
            "rx_version", "rx_profile_enable", "rx_profile_read", "rx_export_counters",
-           "rx_set_taps", "rx_get_q_trace")
+           "rx_set_taps", "rx_get_q_trace", "rx_calibrate_thresholds")
 NCOUNTERS = 8
 COUNTERS = ("bit_errors", "bits", "symbols_counted", "evm_num", "evm_den", "clipped",
             "domain_errors", "symbols_out")
@@ -106,6 +106,8 @@ def load(path: str = SO_PATH):
     lib.rx_profile_read.argtypes = [vp, _c_dp, ctypes.POINTER(_c_ll), ctypes.c_int]
     lib.rx_get_q_trace.argtypes = [vp, _c_ll, ctypes.c_int, ctypes.POINTER(_c_ll), ctypes.POINTER(_c_ll), vp]
     lib.rx_get_q_trace.restype = ctypes.c_int
+    lib.rx_calibrate_thresholds.argtypes = [vp, _c_ll, _c_ll, _c_dp, _c_dp, vp]
+    lib.rx_calibrate_thresholds.restype = ctypes.c_int
     for f in ("rx_create", "rx_process", "rx_flush", "rx_get_stats", "rx_reset_stats",
               "rx_get_taps", "rx_set_taps", "rx_probe_read", "rx_profile_enable", "rx_profile_read"):
         getattr(lib, f).restype = ctypes.c_int
@@ -195,6 +197,16 @@ class Receiver:
         st = RxStats()
         _check(load().rx_get_stats(self._h, ctypes.byref(st), _stream_ptr(stream)), "rx_get_stats")
         return {k: getattr(st, k) for k, _ in RxStats._fields_}
+
+    def calibrate_thresholds(self, first: int, count: int, stream=None):
+        """PAM decision thresholds from the equaliser output of finalised symbols
+        [first, first + count) (rx_calibrate_thresholds): (thresholds [M-1], level means [M])."""
+        thr = np.zeros(self.order - 1, dtype=np.float64)
+        means = np.zeros(self.order, dtype=np.float64)
+        _check(load().rx_calibrate_thresholds(self._h, first, count, thr.ctypes.data_as(_c_dp),
+                                              means.ctypes.data_as(_c_dp), _stream_ptr(stream)),
+               "rx_calibrate_thresholds")
+        return thr, means
 
     def q_trace(self, first: int, n: int, stream=None):
         """Windowed (bit_errors, bits) of Q-trace windows [first, first + n) (rx_get_q_trace)."""

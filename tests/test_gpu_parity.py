@@ -441,3 +441,39 @@ def test_stitch_chain_mode_parity():
     assert np.array_equal(seg_R, out["lms"]["R"])
     mism, excl = _compare_labels(rec, rx, out, labels, R)
     _compare_counters(rec, out, st, mism)
+
+
+def test_threshold_calibration_matches_oracle():
+    """rx_calibrate_thresholds (P:167 'optimized offline beforehand and uploaded', S:361 reading):
+    per-reference-level means of the GPU equaliser output and their midpoints against the
+    oracle's calibrate_thresholds on the oracle's equaliser output of the same symbols; a handle
+    created with the calibrated thresholds decodes the record as well as the ideal midpoints."""
+    _torch_cuda()
+    from paper_2011_13695_b200 import RxError
+    rec, rx = make_config("C2", n_samples=1 << 21)
+    rx["buffer_blocks"] = 256
+    out = run_oracle(rec, rx)
+    R, labels, st = run_gpu(rec, rx, chunk=256 * 512)
+    lo, hi = rx["warmup_symbols"], out["m_end"]
+    thr, means = R.calibrate_thresholds(lo, hi - lo)
+    _, idx_ref, _ = O.reference("pam", rec.M)
+    m = np.arange(lo, hi)
+    ref_level = idx_ref[(out["sync"]["offset"] + m - rx["sync_start"]) % O.P_REF]
+    thr_o, means_o = O.calibrate_thresholds(out["lms"]["z"][lo:hi], ref_level, rec.M)
+    assert np.max(np.abs(means - means_o)) < 1e-4 and np.max(np.abs(thr - thr_o)) < 1e-4
+    with pytest.raises(RxError):
+        R.calibrate_thresholds(hi - 10, 100)                 # beyond the finalised symbols
+    from paper_2011_13695_b200 import RX_PAM, Receiver
+    fields = {k: v for k, v in rx.items() if k in ("lms_taps", "lms_block", "lms_segment", "lms_overlap",
+                                                   "mu", "train_symbols", "sync_start", "sync_window",
+                                                   "warmup_symbols", "buffer_blocks")}
+    R2 = Receiver(RX_PAM, rec.M, rec.static_taps, thresholds=thr, history_buffers=10, **fields)
+    import torch
+    codes = torch.from_numpy(rec.codes.view(np.int16)).cuda()
+    lab2 = torch.zeros(rec.n, dtype=torch.uint8, device="cuda")
+    for off in range(0, rec.n, 256 * 512):
+        R2.process(codes[off:off + 256 * 512], lab2)
+    R2.flush(lab2)
+    st2 = R2.stats()
+    print(f"calibrated thresholds BER {st2['bit_errors']}/{st2['bits']} vs midpoints {st['bit_errors']}/{st['bits']}")
+    assert st2["bit_errors"] <= 1.1 * st["bit_errors"] + 20

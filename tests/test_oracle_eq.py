@@ -373,3 +373,31 @@ def test_lag_d_seeded_epochs_survive_carrier_phase_noise():
     early = 1 - ok[E:4 * E].mean()                      # W_train-seeded epochs 1..3
     late = 1 - ok[4 * E:(out["m_end"] // E) * E].mean()  # lag-D seeded epochs
     assert early < 0.01 and late < 2 * early + 2e-3, (early, late)
+
+
+# ---------------------------------------------------------------- calibration
+
+def test_threshold_calibration_closed_forms():
+    """Noiseless non-uniform levels (a compressive transfer curve, the reason thresholds are
+    optimised offline) -> thresholds at the exact midpoints of the true levels; with
+    AWGN the midpoints of the per-level means are unbiased (within 4 sigma/sqrt(n)); ideal
+    levels reduce to the midpoints of c-11."""
+    rng = np.random.default_rng(11)
+    M = 8
+    ideal = O.pam_levels(M)
+    true = np.tanh(1.3 * ideal) / np.tanh(1.3)
+    ref = rng.integers(0, M, size=200_000)
+    thr, means = O.calibrate_thresholds(true[ref], ref, M)
+    assert np.allclose(means, true, atol=1e-15)
+    assert np.allclose(thr, 0.5 * (true[1:] + true[:-1]), atol=1e-15)
+    sigma = 0.02
+    thr2, _ = O.calibrate_thresholds(true[ref] + sigma * rng.normal(size=ref.size), ref, M)
+    n_min = np.bincount(ref, minlength=M).min()
+    assert np.all(np.abs(thr2 - thr) < 4 * sigma / math.sqrt(n_min))
+    thr3, _ = O.calibrate_thresholds(ideal[ref], ref, M)
+    assert np.allclose(thr3, O.midpoints(ideal), atol=1e-15)
+    # the calibrated slicer removes the errors the ideal midpoints make on the compressed levels
+    y = true[ref] + 0.01 * rng.normal(size=ref.size)
+    e_ideal = np.mean(O.slice_axis(y, O.midpoints(ideal)) != ref)
+    e_cal = np.mean(O.slice_axis(y, thr) != ref)
+    assert e_cal < 1e-4 < e_ideal
