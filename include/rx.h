@@ -200,6 +200,18 @@ rx_status rx_calibrate_thresholds(rx_handle *h, long long first_symbol, long lon
                                   double *host_thresholds, double *host_level_means,
                                   void *cuda_stream);
 
+/* KK DC-offset calibration. The paper restores the DC of the AC-coupled intensity "using the
+ * method of [Luis:20]" without restating it; built as a grid search that reuses the
+ * whole chain: for each of the n_candidates dc values a temporary handle with cfg (dc_offset
+ * replaced) streams the n_samples of the calibration record at d_samples (device memory,
+ * cfg->input_format) and is flushed; host_evm_db[i] gets its decision-referenced EVM (+inf if
+ * frame sync failed), *best_index the lowest EVM (lowest index on ties). Synchronises
+ * cuda_stream once per candidate. RX_EINVAL: not KK, bad sizes; other errors from rx_create /
+ * rx_process are passed through. */
+rx_status rx_calibrate_dc(const rx_config *cfg, int cuda_device, const void *d_samples,
+                          long long n_samples, const double *candidates, int n_candidates,
+                          double *host_evm_db, int *best_index, void *cuda_stream);
+
 /* Zero the BER/EVM/clip/domain counters (enqueued on cuda_stream). */
 rx_status rx_reset_stats(rx_handle *h, void *cuda_stream);
 

@@ -774,6 +774,20 @@ def calibrate_thresholds(y: np.ndarray, ref_level: np.ndarray, M: int):
     return 0.5 * (means[:-1] + means[1:]), means
 
 
+def calibrate_dc(codes: np.ndarray, p: "RxParams", candidates):
+    """KK DC offset of the AC-coupled receiver (the DC is restored "using the method of
+    [Luis:20]", which the paper does not restate): grid search - run the whole KK chain once per
+    candidate dc and keep the one with the lowest decision-referenced EVM (lowest index on ties).
+    Returns (EVM dB per candidate, best index)."""
+    evm = []
+    for dc in candidates:
+        q = dataclasses.replace(p, dc_offset=float(dc))
+        out = receive_kk(codes, q)
+        evm.append(out["evm_db"] if out["sync"]["gamma"] >= q.sync_min_corr else float("inf"))
+    evm = np.asarray(evm)
+    return evm, int(np.argmin(evm))
+
+
 # ============================================================================ c-11
 
 def count_errors(fmt, M, idx, z, slicer: _Slicer, ref_labels_fn, m_lo, m_hi):

@@ -1092,6 +1092,36 @@ extern "C" rx_status rx_calibrate_thresholds(rx_handle *h, long long first, long
   return RX_OK;
 }
 
+extern "C" rx_status rx_calibrate_dc(const rx_config *cfg, int dev, const void *d_samples, long long n,
+                                     const double *cands, int ncand, double *evm, int *best, void *stream) {
+  if (!cfg || !cands || !evm || !best || ncand <= 0 || n <= 0 || n % 512 || !d_samples) return RX_EINVAL;
+  if (cfg->family != RX_QAM_KK) return RX_EINVAL;
+  const size_t es = cfg->input_format == RX_IN_F32 ? 4 : 2;
+  int bi = -1;
+  for (int i = 0; i < ncand; ++i) {
+    rx_config c = *cfg;
+    c.dc_offset = cands[i];
+    rx_handle *h = nullptr;
+    rx_status st = rx_create(&c, dev, &h);
+    if (st) return st;
+    for (long long off = 0; off < n && st == RX_OK; off += h->max_call) {
+      const long long k = n - off < h->max_call ? n - off : h->max_call;
+      st = rx_process(h, (const char *)d_samples + off * es, k, nullptr, 0, stream);
+    }
+    if (st == RX_OK) st = rx_flush(h, nullptr, 0, stream);
+    rx_stats s;
+    if (st == RX_OK) st = rx_get_stats(h, &s, stream);
+    rx_destroy(h);
+    if (st != RX_OK && st != RX_ESYNC && st != RX_EDOMAIN && st != RX_EDIVERGE) return st;
+    const bool ok = st == RX_OK || st == RX_EDOMAIN || st == RX_EDIVERGE;
+    evm[i] = (ok && s.synced && !(s.status_flags & RX_FLAG_SYNC) && s.evm_den > 0.0)
+                 ? 10.0 * log10(s.evm_num / s.evm_den) : INFINITY;
+    if (bi < 0 || evm[i] < evm[bi]) bi = i;
+  }
+  *best = bi;
+  return RX_OK;
+}
+
 extern "C" rx_status rx_get_q_trace(rx_handle *h, long long first, int n, long long *err, long long *bits,
                                     void *stream) {
   if (!h || n < 0 || (n > 0 && (!err || !bits)) || first < 0 || h->d.q_segs <= 0) return RX_EINVAL;

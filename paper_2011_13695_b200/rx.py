@@ -65,7 +65,7 @@ class RxStats(ctypes.Structure):
 EXPORTS = ("rx_config_default", "rx_create", "rx_process", "rx_flush", "rx_get_stats",
            "rx_reset_stats", "rx_get_taps", "rx_probe_read", "rx_destroy", "rx_strerror",
            "rx_version", "rx_profile_enable", "rx_profile_read", "rx_export_counters",
-           "rx_set_taps", "rx_get_q_trace", "rx_calibrate_thresholds")
+           "rx_set_taps", "rx_get_q_trace", "rx_calibrate_thresholds", "rx_calibrate_dc")
 NCOUNTERS = 8
 COUNTERS = ("bit_errors", "bits", "symbols_counted", "evm_num", "evm_den", "clipped",
             "domain_errors", "symbols_out")
@@ -108,6 +108,9 @@ def load(path: str = SO_PATH):
     lib.rx_get_q_trace.restype = ctypes.c_int
     lib.rx_calibrate_thresholds.argtypes = [vp, _c_ll, _c_ll, _c_dp, _c_dp, vp]
     lib.rx_calibrate_thresholds.restype = ctypes.c_int
+    lib.rx_calibrate_dc.argtypes = [ctypes.POINTER(RxConfig), ctypes.c_int, vp, _c_ll, _c_dp, ctypes.c_int,
+                                    _c_dp, ctypes.POINTER(ctypes.c_int), vp]
+    lib.rx_calibrate_dc.restype = ctypes.c_int
     for f in ("rx_create", "rx_process", "rx_flush", "rx_get_stats", "rx_reset_stats",
               "rx_get_taps", "rx_set_taps", "rx_probe_read", "rx_profile_enable", "rx_profile_read"):
         getattr(lib, f).restype = ctypes.c_int
@@ -287,3 +290,26 @@ class Receiver:
             self.close()
         except Exception:
             pass
+
+
+def calibrate_dc(order: int, static_taps, samples, candidates, device: int = 0, stream=None, **fields):
+    """KK DC-offset grid search through the chain (rx_calibrate_dc): ``samples`` is a
+    device tensor holding the calibration record; returns (EVM dB per candidate, best index)."""
+    lib = load()
+    cfg = default_config(RX_QAM_KK, order)
+    taps = np.asarray(static_taps)
+    buf = np.ascontiguousarray(np.stack([taps.real, taps.imag], axis=-1).reshape(-1), dtype=np.float64)
+    cfg.static_taps = buf.ctypes.data_as(_c_dp)
+    cfg.n_static_taps = buf.shape[0] // 2
+    for k, v in fields.items():
+        if not hasattr(cfg, k):
+            raise TypeError(f"unknown rx_config field {k}")
+        setattr(cfg, k, v)
+    cand = np.ascontiguousarray(candidates, dtype=np.float64)
+    evm = np.zeros(cand.shape[0], dtype=np.float64)
+    best = ctypes.c_int(-1)
+    _check(lib.rx_calibrate_dc(ctypes.byref(cfg), device, ctypes.c_void_p(samples.data_ptr()),
+                               int(samples.numel()), cand.ctypes.data_as(_c_dp), int(cand.shape[0]),
+                               evm.ctypes.data_as(_c_dp), ctypes.byref(best), _stream_ptr(stream)),
+           "rx_calibrate_dc")
+    return evm, best.value

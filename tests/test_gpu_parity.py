@@ -477,3 +477,23 @@ def test_threshold_calibration_matches_oracle():
     st2 = R2.stats()
     print(f"calibrated thresholds BER {st2['bit_errors']}/{st2['bits']} vs midpoints {st['bit_errors']}/{st['bits']}")
     assert st2["bit_errors"] <= 1.1 * st["bit_errors"] + 20
+
+
+def test_kk_dc_calibration_matches_oracle():
+    """rx_calibrate_dc: per-candidate EVM of the chain on a calibration record against
+    the oracle's grid search (0.01 dB), same choice, the generator's DC."""
+    torch = _torch_cuda()
+    from paper_2011_13695_b200 import rx as rxmod
+    from tests.gpu_util import oracle_params
+    rec, rx = make_config("C4", n_samples=1 << 20)
+    rx["buffer_blocks"] = 256
+    cands = np.array([0.8, 0.9, 1.0, 1.1, 1.2]) * rec.dc_offset
+    evm_o, best_o = O.calibrate_dc(rec.codes, oracle_params(rec, rx), cands)
+    codes = torch.from_numpy(rec.codes.view(np.int16)).cuda()
+    fields = {k: v for k, v in rx.items() if k in ("lms_taps", "lms_block", "lms_segment", "lms_overlap", "mu",
+                                                   "train_symbols", "sync_start", "sync_window",
+                                                   "warmup_symbols", "cpr_test_phases", "buffer_blocks")}
+    evm_g, best_g = rxmod.calibrate_dc(rec.M, rec.static_taps, codes, cands, history_buffers=6, **fields)
+    print("dc calibration EVM gpu", np.round(evm_g, 3), "oracle", np.round(evm_o, 3))
+    assert best_g == best_o == 2
+    assert np.all(np.abs(evm_g - evm_o) < 0.01)

@@ -401,3 +401,17 @@ def test_threshold_calibration_closed_forms():
     e_ideal = np.mean(O.slice_axis(y, O.midpoints(ideal)) != ref)
     e_cal = np.mean(O.slice_axis(y, thr) != ref)
     assert e_cal < 1e-4 < e_ideal
+
+
+def test_kk_dc_calibration_finds_the_generators_dc():
+    """P:215 (DC restored for the AC-coupled ADC): the grid search over the whole KK chain picks
+    the DC the generator removed (known by construction) from {0.8, 0.9, 1, 1.1, 1.2} x truth;
+    EVM rises on both sides, with domain errors (I + dc <= 0) below it."""
+    from tests.gpu_util import oracle_params
+    rec, rx = make_config("C4", n_samples=1 << 19)
+    rx["buffer_blocks"] = 256
+    p = oracle_params(rec, rx)
+    f = np.array([0.8, 0.9, 1.0, 1.1, 1.2])
+    evm, best = O.calibrate_dc(rec.codes, p, f * rec.dc_offset)
+    assert best == 2
+    assert evm[0] > evm[1] > evm[2] < evm[3] < evm[4]
