@@ -87,3 +87,36 @@ def test_product_package_never_imports_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, f), errors="ignore").read()
                 assert not pat.search(txt), f
+
+
+def test_new_config_fields_validated_before_touching_the_gpu(lib):
+    """widely_linear (KK only), cpr_anchor, serial_equaliser (0/1), q_window_symbols (a
+    multiple of lms_segment) are checked by rx_create before any CUDA call; calibration entry
+    points reject wrong families / arguments synchronously."""
+    from paper_2011_13695_b200 import rx
+    import numpy as np
+    taps = np.ones(503)
+    h = ctypes.c_void_p()
+
+    def pam():
+        c = rx.default_config(rx.RX_PAM, 4)
+        c.static_taps = taps.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        c.n_static_taps = 503
+        return c
+    for field, bad in (("widely_linear", 1), ("serial_equaliser", 2), ("cpr_anchor", 3),
+                       ("q_window_symbols", 4097), ("q_window_symbols", -4096)):
+        c = pam()
+        setattr(c, field, bad)
+        assert lib.rx_create(ctypes.byref(c), 0, ctypes.byref(h)) == -1, field
+    c = pam()                                                # a PAM config is not a KK calibration
+    cand = np.array([1.0])
+    evm = np.zeros(1)
+    best = ctypes.c_int(-1)
+    dp = ctypes.POINTER(ctypes.c_double)
+    assert lib.rx_calibrate_dc(ctypes.byref(c), 0, ctypes.c_void_p(16), 4096, cand.ctypes.data_as(dp), 1,
+                               evm.ctypes.data_as(dp), ctypes.byref(best), None) == -1
+    thr = np.zeros(3)
+    assert lib.rx_calibrate_thresholds(None, 0, 10, thr.ctypes.data_as(dp), None, None) == -1
+    e = np.zeros(1, dtype=np.int64)
+    lp = ctypes.POINTER(ctypes.c_longlong)
+    assert lib.rx_get_q_trace(None, 0, 1, e.ctypes.data_as(lp), e.ctypes.data_as(lp), None) == -1
