@@ -212,6 +212,17 @@ rx_status rx_calibrate_dc(const rx_config *cfg, int cuda_device, const void *d_s
                           long long n_samples, const double *candidates, int n_candidates,
                           double *host_evm_db, int *best_index, void *cuda_stream);
 
+/* Static-equaliser design (host only, no GPU): the paper's static FIRs are "optimized offline"
+ * (503 taps PAM; 203 taps KK) without a stated method; SPEC's reading:
+ * per-bin regularised MMSE on the 1024-bin grid, H_eq[k] = conj(H_ch[k]) H_t[k] /
+ * (|H_ch[k]|^2 + lambda), inverse DFT (1/N), zero-phase taps centred like rx_config.static_taps,
+ * truncated to n_taps and re-windowed (Kaiser, beta = 6: DESIGN reading R-SEQ).
+ * h_channel, h_target: 1024 complex bins interleaved (re, im), bin k = k/1024 of the sample rate.
+ * real_taps = 1 writes the n_taps real parts (PAM), 0 writes 2 n_taps interleaved (KK).
+ * RX_EINVAL: n_taps even or > 1023, lambda < 0, or a zero denominator. */
+rx_status rx_design_static_eq(const double *h_channel, const double *h_target, double lambda,
+                              int n_taps, int real_taps, double *taps_out);
+
 /* Zero the BER/EVM/clip/domain counters (enqueued on cuda_stream). */
 rx_status rx_reset_stats(rx_handle *h, void *cuda_stream);
 

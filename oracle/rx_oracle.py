@@ -774,6 +774,17 @@ def calibrate_thresholds(y: np.ndarray, ref_level: np.ndarray, M: int):
     return 0.5 * (means[:-1] + means[1:]), means
 
 
+def design_static_eq(h_channel: np.ndarray, h_target: np.ndarray, lam: float, n_taps: int):
+    """Static-EQ design, SPEC's reading of "optimized offline":
+    H_eq = conj(H_ch) H_t / (|H_ch|^2 + lambda) per bin of the 1024 grid, h = IDFT(H_eq),
+    zero-phase taps h[i - c] (c = (n_taps - 1)/2) times a Kaiser(beta = 6) window (DESIGN R-SEQ).
+    Returns complex taps (take .real for a real design)."""
+    H = np.conj(h_channel) * h_target / (np.abs(h_channel) ** 2 + lam)
+    h = np.fft.ifft(H)
+    c = (n_taps - 1) // 2
+    return np.kaiser(n_taps, 6.0) * h[(np.arange(n_taps) - c) % h.shape[0]]
+
+
 def calibrate_dc(codes: np.ndarray, p: "RxParams", candidates):
     """KK DC offset of the AC-coupled receiver (the DC is restored "using the method of
     [Luis:20]", which the paper does not restate): grid search - run the whole KK chain once per

@@ -1122,6 +1122,51 @@ extern "C" rx_status rx_calibrate_dc(const rx_config *cfg, int dev, const void *
   return RX_OK;
 }
 
+// modified Bessel function of the first kind, order 0 (series; Kaiser window)
+static double bessel_i0(double x) {
+  double s = 1.0, t = 1.0;
+  for (int k = 1; k < 64; ++k) {
+    t *= (x / (2.0 * k)) * (x / (2.0 * k));
+    s += t;
+    if (t < 1e-18 * s) break;
+  }
+  return s;
+}
+
+extern "C" rx_status rx_design_static_eq(const double *hc, const double *ht, double lambda, int L, int real_taps,
+                                         double *out) {
+  const int N = 1024;
+  if (!hc || !ht || !out || L < 1 || L % 2 == 0 || L > N - 1 || !(lambda >= 0.0)) return RX_EINVAL;
+  std::vector<double> er(N), ei(N);
+  for (int k = 0; k < N; ++k) {   // per-bin regularised MMSE
+    const double cr = hc[2 * k], ci = hc[2 * k + 1], tr = ht[2 * k], ti = ht[2 * k + 1];
+    const double den = cr * cr + ci * ci + lambda;
+    if (den <= 0.0) {
+      if (tr == 0.0 && ti == 0.0) { er[k] = ei[k] = 0.0; continue; }
+      return RX_EINVAL;
+    }
+    er[k] = (cr * tr + ci * ti) / den;   // conj(H_ch) H_t / den
+    ei[k] = (cr * ti - ci * tr) / den;
+  }
+  const int c = (L - 1) / 2;
+  const double beta = 6.0, i0b = bessel_i0(beta);
+  for (int i = 0; i < L; ++i) {
+    const int n = ((i - c) % N + N) % N;   // zero-phase: tap i is time index i - c
+    double sr = 0.0, si = 0.0;
+    for (int k = 0; k < N; ++k) {          // h[n] = (1/N) sum_k H[k] e^{+j 2 pi k n / N}
+      const int ph = (int)(((long long)k * n) % N);
+      const double a = 2.0 * M_PI * ph / N, ca = cos(a), sa = sin(a);
+      sr += er[k] * ca - ei[k] * sa;
+      si += er[k] * sa + ei[k] * ca;
+    }
+    const double r = L > 1 ? (2.0 * i) / (L - 1) - 1.0 : 0.0;
+    const double w = bessel_i0(beta * sqrt(fmax(0.0, 1.0 - r * r))) / i0b;
+    if (real_taps) out[i] = w * sr / N;
+    else { out[2 * i] = w * sr / N; out[2 * i + 1] = w * si / N; }
+  }
+  return RX_OK;
+}
+
 extern "C" rx_status rx_get_q_trace(rx_handle *h, long long first, int n, long long *err, long long *bits,
                                     void *stream) {
   if (!h || n < 0 || (n > 0 && (!err || !bits)) || first < 0 || h->d.q_segs <= 0) return RX_EINVAL;

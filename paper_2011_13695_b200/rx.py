@@ -65,7 +65,8 @@ class RxStats(ctypes.Structure):
 EXPORTS = ("rx_config_default", "rx_create", "rx_process", "rx_flush", "rx_get_stats",
            "rx_reset_stats", "rx_get_taps", "rx_probe_read", "rx_destroy", "rx_strerror",
            "rx_version", "rx_profile_enable", "rx_profile_read", "rx_export_counters",
-           "rx_set_taps", "rx_get_q_trace", "rx_calibrate_thresholds", "rx_calibrate_dc")
+           "rx_set_taps", "rx_get_q_trace", "rx_calibrate_thresholds", "rx_calibrate_dc",
+           "rx_design_static_eq")
 NCOUNTERS = 8
 COUNTERS = ("bit_errors", "bits", "symbols_counted", "evm_num", "evm_den", "clipped",
             "domain_errors", "symbols_out")
@@ -111,6 +112,8 @@ def load(path: str = SO_PATH):
     lib.rx_calibrate_dc.argtypes = [ctypes.POINTER(RxConfig), ctypes.c_int, vp, _c_ll, _c_dp, ctypes.c_int,
                                     _c_dp, ctypes.POINTER(ctypes.c_int), vp]
     lib.rx_calibrate_dc.restype = ctypes.c_int
+    lib.rx_design_static_eq.argtypes = [_c_dp, _c_dp, ctypes.c_double, ctypes.c_int, ctypes.c_int, _c_dp]
+    lib.rx_design_static_eq.restype = ctypes.c_int
     for f in ("rx_create", "rx_process", "rx_flush", "rx_get_stats", "rx_reset_stats",
               "rx_get_taps", "rx_set_taps", "rx_probe_read", "rx_profile_enable", "rx_profile_read"):
         getattr(lib, f).restype = ctypes.c_int
@@ -313,3 +316,18 @@ def calibrate_dc(order: int, static_taps, samples, candidates, device: int = 0, 
                                evm.ctypes.data_as(_c_dp), ctypes.byref(best), _stream_ptr(stream)),
            "rx_calibrate_dc")
     return evm, best.value
+
+
+def design_static_eq(h_channel, h_target, lam: float, n_taps: int, real_taps: bool):
+    """Static-equaliser design (rx_design_static_eq; host only): 1024-bin complex responses in,
+    n_taps zero-phase taps out (real for PAM, complex for KK)."""
+    lib = load()
+
+    def inter(h):
+        h = np.asarray(h, dtype=np.complex128)
+        return np.ascontiguousarray(np.stack([h.real, h.imag], axis=-1).reshape(-1))
+    a, b = inter(h_channel), inter(h_target)
+    out = np.zeros(n_taps if real_taps else 2 * n_taps, dtype=np.float64)
+    _check(lib.rx_design_static_eq(a.ctypes.data_as(_c_dp), b.ctypes.data_as(_c_dp), float(lam), int(n_taps),
+                                   int(bool(real_taps)), out.ctypes.data_as(_c_dp)), "rx_design_static_eq")
+    return out if real_taps else out[0::2] + 1j * out[1::2]
