@@ -497,3 +497,28 @@ def test_kk_dc_calibration_matches_oracle():
     print("dc calibration EVM gpu", np.round(evm_g, 3), "oracle", np.round(evm_o, 3))
     assert best_g == best_o == 2
     assert np.all(np.abs(evm_g - evm_o) < 0.01)
+
+
+def test_data_dependent_error_flags_match_oracle():
+    """SURVEY §8(b) error cases that depend on the data: frame sync below sync_min_corr on a
+    noise-only record sets RX_FLAG_SYNC and counts nothing; an LMS step far too large
+    diverges (reading R-DIV) and sets RX_FLAG_DIVERGE exactly when the oracle reports
+    divergence."""
+    torch = _torch_cuda()
+    from paper_2011_13695_b200 import RX_PAM, Receiver
+    rng = np.random.default_rng(77)
+    rec, rx = make_config("C1")
+    noise = np.clip(np.rint(2047.5 + 300 * rng.normal(size=rec.n)), 0, 4095).astype(np.uint16)
+    R = Receiver(RX_PAM, rec.M, rec.static_taps, lms_taps=rx["lms_taps"], train_symbols=rx["train_symbols"],
+                 history_buffers=3)
+    lab = torch.zeros(rec.n, dtype=torch.uint8, device="cuda")
+    R.process(torch.from_numpy(noise.view(np.int16)).cuda(), lab)
+    R.flush(lab)
+    st = R.stats()
+    assert st["status_flags"] & 2 and st["bits"] == 0 and st["sync_gamma"] < 0.3
+    R.close()
+    rx2 = dict(rx, mu=0.5)
+    out = run_oracle(rec, rx2)
+    R2, _, st2 = run_gpu(rec, rx2)
+    assert out["lms"]["diverged"]
+    assert st2["status_flags"] & 4
