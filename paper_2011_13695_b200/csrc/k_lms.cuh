@@ -746,11 +746,14 @@ __device__ void bps_helper(const RxDev &d, const float2 *ys, long long t_begin, 
 
 // ------------------------------------------------------------------ segments (1 warp each)
 // Segment s outputs [sS, min((s+1)S, m_end)), recursion starts O symbols early (c-9).
+#ifndef LMS_SPC
+#define LMS_SPC 4           // segments (warps) per CTA of k_lms_seg
+#endif
 template <bool CPLX, int CPR, int KP, bool WLIN = false>
-__global__ void __launch_bounds__(128) k_lms_seg(RxDev d, int flush, int nseg, unsigned char *labels,
+__global__ void __launch_bounds__(32 * LMS_SPC) k_lms_seg(RxDev d, int flush, int nseg, unsigned char *labels,
                                                  long long lab_cap) {
   // BPS segments run on a warp pair (LMS warp + BPS helper), others on one warp
-  constexpr int PAIR = 1, SPC = 4 / PAIR;   // PAIR = 2 runs BPS on an extra helper warp
+  constexpr int PAIR = 1, SPC = LMS_SPC / PAIR;   // PAIR = 2 runs BPS on an extra helper warp
   __shared__ LmsSmemT<CPLX> sm[SPC];
   __shared__ float2 bps_part[SPC][32];
   DevState *st = d.st;

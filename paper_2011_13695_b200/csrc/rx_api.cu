@@ -627,8 +627,8 @@ static void launch_lms_round(rx_handle *h, cudaStream_t s, unsigned char *labels
                              int flush, long long nseg) {
   RxDev &d = h->d;
   const long long S = d.S;
-  const int spc = 4;   // segments per CTA (k_lms_seg PAIR)
-  KLAUNCH(h, RX_K_LMS, s, (lms_seg_kernel(d)<<<gridc(nseg, spc), 128, 0, s>>>(d, flush, (int)nseg, labels, lab_cap)));
+  const int spc = LMS_SPC;   // segments per CTA
+  KLAUNCH(h, RX_K_LMS, s, (lms_seg_kernel(d)<<<gridc(nseg, spc), 32 * LMS_SPC, 0, s>>>(d, flush, (int)nseg, labels, lab_cap)));
   if (d.family == RX_PAM) {
     // PAM segments wrote their labels and error counts; the prefix also adds the counters
     KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_prefix<<<1, 1024, 0, s>>>(d, flush, (int)nseg)));
