@@ -163,7 +163,7 @@ def _polyphase_table(ntaps: int, phases: int = _PHASES, win_beta: float = 8.0) -
 
 
 def _resample_periodic(x: np.ndarray, ppm: float, ntaps: int = 32,
-                       n_out: int | None = None, p0: int = 0) -> np.ndarray:
+                       n_out: int | None = None, p0: int = 0, positions=None) -> np.ndarray:
     """Band-limited resampling of a periodic sequence at positions p/(1+eps), eps = ppm*1e-6,
     p = p0 .. p0+n_out-1 (indices mod len(x): the periodic waveform makes a seamless ring).
 
@@ -180,7 +180,7 @@ def _resample_periodic(x: np.ndarray, ppm: float, ntaps: int = 32,
     chunk = 1 << 18
     for s in range(0, n_out, chunk):
         p = np.arange(p0 + s, p0 + min(n_out, s + chunk), dtype=np.float64)
-        t = p / (1.0 + eps)
+        t = p / (1.0 + eps) if positions is None else positions[s:s + p.shape[0]]
         t0 = np.floor(t)
         ph = np.rint((t - t0) * _PHASES).astype(np.int64)
         idx = (t0.astype(np.int64)[:, None] + j[None, :]) % n
@@ -228,13 +228,17 @@ def _tx_indices(fmt, M, nsym, offset):
 
 def pam_record(M: int, n_samples: int, *, seed: int, snr_db: float | None = None,
                channel: str = "b2b", ppm: float = 0.0, offset: int | None = None,
-               n_static_taps: int = 503, echo=(1.0, 0.2, -0.1), keep_tx: bool = False) -> Record:
+               n_static_taps: int = 503, echo=(1.0, 0.2, -0.1), keep_tx: bool = False,
+               ppm_triangle: float = 0.0) -> Record:
     """2 GBaud PAM-M at 2 sps, optional '91 km-like' ISI, clock offset, AWGN.
 
     channel "b2b": no filtering. "isi91": IM/DD CD response cos(2 pi^2 |b2| L f^2)
     (b2 = -21.5 ps^2/km, L = 91 km) x two 1 GHz Butterworth sections x symbol-spaced
     echo [1, 0.2, -0.1]. snr_db: electrical SNR at the matched-filter
     output relative to the ideal levels (C1: 9 dB -> BER Q(sqrt(7.94)) for PAM-2).
+    ppm_triangle = A: a free-running, time-varying clock offset instead of a static one (the
+    paper's Fig. 5 scenario): eps(p) is one triangle period over the record,
+    0 -> +A -> 0 -> -A -> 0 ppm, and sample p is taken at t_p = sum_{i<p} 1/(1 + eps_i).
     """
     rng = np.random.default_rng(seed)
     sps, baud, beta = 2, 2e9, 0.5
@@ -264,7 +268,13 @@ def pam_record(M: int, n_samples: int, *, seed: int, snr_db: float | None = None
         raise ValueError(channel)
     x = np.fft.ifft(F).real
     x_tx = x if keep_tx else None            # periodic, pre-ADC-clock waveform (bench ring)
-    if ppm != 0.0:
+    if ppm_triangle != 0.0:
+        ph = np.arange(n_samples, dtype=np.float64) / n_samples
+        tri = np.where(ph < 0.25, 4 * ph, np.where(ph < 0.75, 2 - 4 * ph, 4 * ph - 4))
+        step = 1.0 / (1.0 + ppm_triangle * 1e-6 * tri)
+        pos = np.concatenate([[0.0], np.cumsum(step[:-1])])
+        x = _resample_periodic(x, 0.0, positions=pos)
+    elif ppm != 0.0:
         x = _resample_periodic(x, ppm)
     taps = static_taps_pam(n_static_taps, sps, beta)
     noise_var = 0.0
@@ -275,7 +285,7 @@ def pam_record(M: int, n_samples: int, *, seed: int, snr_db: float | None = None
     codes, mean, fs, clipped = _quantise(x)
     return Record(codes=codes, fmt="pam", M=M, baud=baud, sps=sps, offset=offset, ppm=ppm,
                   static_taps=taps, tx_index=idx,
-                  meta=dict(seed=seed, snr_db=snr_db, channel=channel, clipped=clipped,
+                  meta=dict(seed=seed, snr_db=snr_db, channel=channel, clipped=clipped, ppm_triangle=ppm_triangle,
                             full_scale=fs, mean=mean, noise_var=noise_var, x_tx=x_tx))
 
 

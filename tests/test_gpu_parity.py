@@ -525,3 +525,22 @@ def test_data_dependent_error_flags_match_oracle():
     R2, _, st2 = run_gpu(rec, rx2)
     assert out["lms"]["diverged"]
     assert st2["status_flags"] & 4
+
+
+def test_time_varying_clock_offset_parity():
+    """Free-running clock (Fig. 5), +-20 ppm triangle over the record: tau_b, M_b, u and
+    the labels / counters against the oracle."""
+    _torch_cuda()
+    rec, rx = make_config("C2", n_samples=1 << 21, M=4, snr_db=17.0, ppm_triangle=20.0)
+    rx["buffer_blocks"] = 256
+    out = run_oracle(rec, rx)
+    R, labels, st = run_gpu(rec, rx, chunk=256 * 512)
+    nb = rec.n // 512
+    assert np.max(np.abs(R.probe("TAU", 0, nb) - out["clock"]["tau"])) < TOL_TAU
+    x = 256.0 * np.arange(nb) - 128.0 - out["clock"]["tau"][:nb]
+    sure = np.abs(x - np.rint(x)) > 1e-6                      # M_b = ceil(x) is decided in fp64
+    assert np.array_equal(R.probe("MB", 0, nb)[sure], out["clock"]["M"][:nb][sure])
+    m_end = out["u"].shape[0]
+    assert rel_l2(R.probe("U", 0, m_end), out["u"]) < TOL_FIELD
+    mism, excl = _compare_labels(rec, rx, out, labels, R)
+    _compare_counters(rec, out, st, mism)

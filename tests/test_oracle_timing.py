@@ -107,3 +107,21 @@ def test_normalisation_closed_form_and_homogeneity():
     uh, dc, A = O.pam_normalise(u, b, 4)
     assert np.allclose(dc, [0, 1]) and np.allclose(A, [1, 2])
     assert np.allclose(uh[:40], uh[40:])
+
+
+def test_q_flat_across_static_and_time_varying_clock_offsets():
+    """Fig. 4 / Fig. 5 behaviour: the Q factor of the PAM chain does
+    not depend on a static clock offset within +-30 ppm (no 8-bit-counter cliff at 30.5 ppm:
+    symbol indices are closed-form, A16) nor on a free-running clock whose offset swings
+    +-20 ppm during the record; all within 0.5 dB of the 0 ppm Q."""
+    from rxsynth import make_config
+    from tests.gpu_util import run_oracle
+    q = {}
+    for name, kw in (("0", dict(ppm=0.0)), ("+30", dict(ppm=30.0)), ("-30", dict(ppm=-30.0)),
+                     ("tri20", dict(ppm_triangle=20.0))):
+        rec, rx = make_config("C2", n_samples=1 << 21, M=4, snr_db=17.0, **kw)
+        out = run_oracle(rec, rx)
+        assert 1e-3 < out["ber"] < 0.05
+        q[name] = float(O.q_from_ber(out["ber"]))
+    for k in ("+30", "-30", "tri20"):
+        assert abs(q[k] - q["0"]) < 0.5, q
