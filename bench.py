@@ -211,7 +211,7 @@ def run_mode(torch, dist, R, ring, n_step, steps, warmup, world, dev, units, lab
                 launches=st1["launches"] - st0["launches"], stats=st1, counters=cnt.cpu().tolist())
 
 
-def e2e_run(torch, R, n_step, host_codes, steps, dev):
+def e2e_run(torch, R, n_step, host_codes, steps, dev, packed=False):
     """Same metric end to end through the public API: every step copies its input from pinned
     host memory to the device, runs the rx_process calls and reads its labels and counters back
     into pinned host memory, all inside the timed region. Double-buffered on three streams (H2D,
@@ -222,8 +222,13 @@ def e2e_run(torch, R, n_step, host_codes, steps, dev):
     h2d = torch.cuda.Stream(device=dev)
     d2h = torch.cuda.Stream(device=dev)
     sp = ctypes.c_void_p(proc.cuda_stream)
-    pinned_in = torch.from_numpy(host_codes[:n_step].view("int16")).pin_memory()
-    dbuf = [torch.empty(n_step, dtype=torch.int16, device=dev) for _ in range(2)]
+    if packed:        # RX_IN_U12_PACKED: the digitiser's 12-bit stream, 1.5 B per sample
+        from rxsynth.gen import pack_u12
+        pinned_in = torch.from_numpy(pack_u12(host_codes[:n_step])).pin_memory()
+    else:
+        pinned_in = torch.from_numpy(host_codes[:n_step].view("int16")).pin_memory()
+    bps = 3 if packed else 4          # input bytes per 2 samples
+    dbuf = [torch.empty_like(pinned_in, device=dev) for _ in range(2)]
     labels = torch.zeros(1 << 24, dtype=torch.uint8, device=dev)
     nlab = n_step // 2
     pinned_out = [torch.empty(nlab, dtype=torch.uint8).pin_memory() for _ in range(2)]
@@ -242,7 +247,7 @@ def e2e_run(torch, R, n_step, host_codes, steps, dev):
         proc.wait_event(ev_in[i])
         for off in range(0, n_step, CHUNK):
             n = min(CHUNK, n_step - off)
-            R.process_ptr(dbuf[i].data_ptr() + 2 * off, n, labels.data_ptr(), labels.numel(), sp)
+            R.process_ptr(dbuf[i].data_ptr() + bps * off // 2, n, labels.data_ptr(), labels.numel(), sp)
         R.export_counters(cnt[i], stream=proc)
         ev_done[i].record(proc)
         with torch.cuda.stream(d2h):
@@ -265,7 +270,7 @@ def e2e_run(torch, R, n_step, host_codes, steps, dev):
     e1.record(proc)
     torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1)
-    return dict(ms=ms, h2d=2 * n_step, d2h=nlab + 8 * 8)
+    return dict(ms=ms, h2d=pinned_in.numel() * pinned_in.element_size(), d2h=nlab + 8 * 8)
 
 
 def class_flops(name, n_step, rx, kk):
@@ -559,13 +564,21 @@ def gpu_main(args):
             "q_db": [round(_multi.q_db_from_ber(int(e) / int(b)), 3) if b else None for e, b in zip(qe, qb)],
             "note": "the first window includes the warm-up symbols, which are not counted"}
     # ---- e2e through the public API with host buffers
-    e2e = e2e_run(torch, R, n_step, rec.codes, max(3, args.steps // 2), dev)
-    e_ms = torch.tensor([e2e["ms"]], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
-    e_steps = max(3, args.steps // 2)
-    line["e2e"] = {"value": round(world * n_step * e_steps / (float(e_ms.item()) / 1e3) / 1e9, 3),
-                   "unit": "GSa/s", "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"]}
+    # (packed 12-bit input, the ADC's format: 1.5 B per sample over PCIe; u16 reported beside it)
+    e_steps = max(5, args.steps)
+
+    def e2e_value(Rx, packed):
+        r = e2e_run(torch, Rx, n_step, rec.codes, e_steps, dev, packed=packed)
+        e_ms = torch.tensor([r["ms"]], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        return {"value": round(world * n_step * e_steps / (float(e_ms.item()) / 1e3) / 1e9, 3),
+                "unit": "GSa/s", "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"]}
+    Rp = make_pam(input_format=2)
+    line["e2e"] = e2e_value(Rp, True)
+    line["e2e"]["input"] = "pinned host, RX_IN_U12_PACKED (2 codes per 3 bytes)"
+    Rp.close()
+    line["e2e_u16"] = e2e_value(R, False)
     R.close()
     del ring
     torch.cuda.empty_cache()

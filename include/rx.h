@@ -125,7 +125,11 @@ typedef struct {
  *                    x = (code - 2047.5) / 2047.5 * adc_gain, codes 0 / 4095 count as clipped
  *  RX_IN_F32:        x = sample * adc_gain (already in x units; e.g. simulated or
  *                    pre-processed streams); nothing is counted as clipped */
-typedef enum { RX_IN_U12_IN_U16 = 0, RX_IN_F32 = 1 } rx_input_format;
+/*  RX_IN_U12_PACKED: ADC codes packed 2 per 3 bytes, little-endian bit stream (sample k = bits
+ *                    [12k, 12k + 12)), e.g. a digitiser's native 12-bit DMA format: 1.5 B per
+ *                    sample over PCIe instead of 2. The library unpacks each call into an
+ *                    internal u16 staging buffer (one HBM pass), then proceeds as RX_IN_U12_IN_U16 */
+typedef enum { RX_IN_U12_IN_U16 = 0, RX_IN_F32 = 1, RX_IN_U12_PACKED = 2 } rx_input_format;
 
 typedef struct rx_handle rx_handle;
 

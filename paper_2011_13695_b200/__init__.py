@@ -10,6 +10,7 @@ from .rx import (  # noqa: F401
     KCLASSES,
     PROBES,
     RX_IN_F32,
+    RX_IN_U12_PACKED,
     RX_IN_U12_IN_U16,
     RX_PAM,
     RX_QAM_KK,

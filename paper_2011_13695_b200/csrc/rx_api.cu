@@ -41,6 +41,19 @@ __global__ void k_kk_mend(RxDev d, long long q_end) {
 }
 __global__ void k_lms_snapshot(RxDev d) { d.st->v_lms = d.st->v_front; }
 
+// RX_IN_U12_PACKED -> u16 codes: thread t turns bytes [12t, 12t + 12) (8 codes, sample k =
+// bits [12k, 12k + 12) of the little-endian stream) into one 16-byte store
+__global__ void __launch_bounds__(256) k_unpack12(const uint32_t *__restrict__ src, uint4 *__restrict__ dst,
+                                                  long long n8) {
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n8; t += (long long)gridDim.x * blockDim.x) {
+    const uint32_t w0 = __ldg(src + 3 * t), w1 = __ldg(src + 3 * t + 1), w2 = __ldg(src + 3 * t + 2);
+    const uint32_t s0 = w0 & 0xFFFu, s1 = (w0 >> 12) & 0xFFFu, s2 = ((w0 >> 24) | (w1 << 8)) & 0xFFFu;
+    const uint32_t s3 = (w1 >> 4) & 0xFFFu, s4 = (w1 >> 16) & 0xFFFu, s5 = ((w1 >> 28) | (w2 << 4)) & 0xFFFu;
+    const uint32_t s6 = (w2 >> 8) & 0xFFFu, s7 = (w2 >> 20) & 0xFFFu;
+    dst[t] = make_uint4(s0 | (s1 << 16), s2 | (s3 << 16), s4 | (s5 << 16), s6 | (s7 << 16));
+  }
+}
+
 // PAM threshold calibration: per-CTA, per-reference-level sums and counts of the
 // equaliser output over symbols [m0, m1), each thread in a fixed order, then a fixed-order CTA
 // reduction (deterministic); the host adds the CTA partials in order
@@ -101,6 +114,7 @@ struct rx_handle {
   cudaStream_t side;
   cudaEvent_t ev_fork, ev_join;
   long long lms_sym_ub;          // symbol upper bound of the data normalised by earlier calls
+  uint16_t *unpacked;            // RX_IN_U12_PACKED: this call's codes unpacked to u16
   struct ZpJob { long long beta0, nb, q_front; };
   std::vector<ZpJob> zp_pending; // KK: CFO carry + z' groups deferred to the next call's side stream
   long long clk_launch;          // fused clock launches so far (tags the tile totals)
@@ -246,7 +260,8 @@ static rx_status validate(const rx_config *c) {
   if (c->sync_start < 0 || c->sync_window < 64 || c->sync_window > 4096) return RX_EINVAL;
   if (c->clock_avg_half < 0 || c->clock_avg_half > 2048) return RX_EINVAL;
   if (c->history_buffers < 3 || c->history_buffers > 64) return RX_EINVAL;
-  if (c->input_format != RX_IN_U12_IN_U16 && c->input_format != RX_IN_F32) return RX_EINVAL;
+  if (c->input_format != RX_IN_U12_IN_U16 && c->input_format != RX_IN_F32 && c->input_format != RX_IN_U12_PACKED)
+    return RX_EINVAL;
   if (c->serial_equaliser != 0 && c->serial_equaliser != 1) return RX_EINVAL;
   if (c->cpr_anchor != 0 && c->cpr_anchor != 1) return RX_EINVAL;
   if (c->q_window_symbols < 0 || (c->q_window_symbols > 0 && c->q_window_symbols % c->lms_segment)) return RX_EINVAL;
@@ -433,6 +448,7 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   h->max_call = (long long)(HB - 2) * c.buffer_blocks * 512;
   h->hist_cap = next_pow2(h->max_call + (1 << 18));   // > max call + clock lookback + kept tail
   d.hist_cap = h->hist_cap;
+  if (c.input_format == RX_IN_U12_PACKED) TRY(dalloc(h, &h->unpacked, h->max_call));
   if (c.input_format == RX_IN_F32) TRY(dalloc(h, &d.histf, d.hist_cap));
   else TRY(dalloc(h, &d.hist, d.hist_cap));
   d.blk_cap = next_pow2((long long)HB * c.buffer_blocks + 256);
@@ -859,6 +875,11 @@ extern "C" rx_status rx_process(rx_handle *h, const void *d_samples, long long n
   if (h->flushed) return RX_ESTATE;
   CK(cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)stream;
+  if (h->cfg.input_format == RX_IN_U12_PACKED && n > 0) {   // unpack the call into the staging buffer
+    KLAUNCH(h, RX_K_MISC, s, (k_unpack12<<<gridc(n / 8, 256) < 4096 ? gridc(n / 8, 256) : 4096, 256, 0, s>>>(
+                                 (const uint32_t *)d_samples, (uint4 *)h->unpacked, n / 8)));
+    d_samples = h->unpacked;
+  }
   const InView in = make_view(h, d_samples, n);
   h->n_in += n;
   unsigned char *lab = labels_capacity ? d_labels : nullptr;
@@ -1096,7 +1117,7 @@ extern "C" rx_status rx_calibrate_dc(const rx_config *cfg, int dev, const void *
                                      const double *cands, int ncand, double *evm, int *best, void *stream) {
   if (!cfg || !cands || !evm || !best || ncand <= 0 || n <= 0 || n % 512 || !d_samples) return RX_EINVAL;
   if (cfg->family != RX_QAM_KK) return RX_EINVAL;
-  const size_t es = cfg->input_format == RX_IN_F32 ? 4 : 2;
+  const size_t es = cfg->input_format == RX_IN_F32 ? 4 : 2;   // bytes per sample (x 3/4 packed)
   int bi = -1;
   for (int i = 0; i < ncand; ++i) {
     rx_config c = *cfg;
@@ -1106,7 +1127,8 @@ extern "C" rx_status rx_calibrate_dc(const rx_config *cfg, int dev, const void *
     if (st) return st;
     for (long long off = 0; off < n && st == RX_OK; off += h->max_call) {
       const long long k = n - off < h->max_call ? n - off : h->max_call;
-      st = rx_process(h, (const char *)d_samples + off * es, k, nullptr, 0, stream);
+      const long long boff = cfg->input_format == RX_IN_U12_PACKED ? off / 2 * 3 : off * (long long)es;
+      st = rx_process(h, (const char *)d_samples + boff, k, nullptr, 0, stream);
     }
     if (st == RX_OK) st = rx_flush(h, nullptr, 0, stream);
     rx_stats s;

@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.path.join(HERE, "librx.so")
 
 RX_PAM, RX_QAM_KK = 0, 1
-RX_IN_U12_IN_U16, RX_IN_F32 = 0, 1
+RX_IN_U12_IN_U16, RX_IN_F32, RX_IN_U12_PACKED = 0, 1, 2
 PROBES = dict(C=0, TAU=1, MB=2, U=3, UHAT=4, E=5, Z=6, CFO=7, Y=8, LEVEL=9, SEG=10, DEBUG=11)
 FLAGS = dict(DOMAIN=1, SYNC=2, DIVERGE=4, CAPACITY=8)
 
@@ -180,14 +180,17 @@ class Receiver:
 
     # -- streaming
     def process(self, samples, labels=None, stream=None):
-        """samples: torch uint16/int16 CUDA tensor of u12 codes (RX_IN_U12_IN_U16) or float32
-        (RX_IN_F32), per the handle's input_format; labels: uint8 CUDA tensor written at index
+        """samples: torch uint16/int16 CUDA tensor of u12 codes (RX_IN_U12_IN_U16), float32
+        (RX_IN_F32) or uint8 bytes of packed 12-bit codes (RX_IN_U12_PACKED, 3 bytes per 2
+        samples), per the handle's input_format; labels: uint8 CUDA tensor written at index
         m % len(labels)."""
-        want = 4 if self.cfg.input_format == RX_IN_F32 else 2
+        fmt = self.cfg.input_format
+        want = {RX_IN_F32: 4, RX_IN_U12_PACKED: 1}.get(fmt, 2)
         if samples.element_size() != want:
-            raise ValueError(f"input_format {self.cfg.input_format} needs {want}-byte samples")
+            raise ValueError(f"input_format {fmt} needs {want}-byte elements")
+        n = samples.numel() * 2 // 3 if fmt == RX_IN_U12_PACKED else samples.numel()
         lp, lc = (labels.data_ptr(), labels.numel()) if labels is not None else (None, 0)
-        _check(load().rx_process(self._h, ctypes.c_void_p(samples.data_ptr()), samples.numel(),
+        _check(load().rx_process(self._h, ctypes.c_void_p(samples.data_ptr()), n,
                                  ctypes.c_void_p(lp), lc, _stream_ptr(stream)), "rx_process")
 
     def process_ptr(self, ptr: int, n: int, labels_ptr: int = 0, labels_cap: int = 0, stream_ptr=None):

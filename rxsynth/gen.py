@@ -370,3 +370,14 @@ def tile_codes(codes: np.ndarray, n_total: int) -> np.ndarray:
     """Tile a (periodic) record into a longer ring, e.g. the >= 1 GiB bench input."""
     reps = -(-n_total // codes.shape[0])
     return np.tile(codes, reps)[:n_total]
+
+
+def pack_u12(codes: np.ndarray) -> np.ndarray:
+    """12-bit codes -> the packed ADC byte stream (2 codes per 3 bytes, little-endian bit
+    stream: code k = bits [12k, 12k + 12)), the RX_IN_U12_PACKED input format."""
+    c = np.asarray(codes, dtype=np.uint32).reshape(-1, 2)
+    out = np.empty((c.shape[0], 3), dtype=np.uint8)
+    out[:, 0] = c[:, 0] & 0xFF
+    out[:, 1] = ((c[:, 0] >> 8) & 0x0F) | ((c[:, 1] & 0x0F) << 4)
+    out[:, 2] = (c[:, 1] >> 4) & 0xFF
+    return out.reshape(-1)

@@ -40,9 +40,13 @@ def run_gpu(rec, rx, chunk=1 << 22, history_buffers=None, device=0, keep=True, p
     if fam == RX_QAM_KK:
         fields["dc_offset"] = rec.dc_offset
     R = Receiver(fam, rec.M, rec.static_taps, device=device, **fields)
+    packed = fields.get("input_format", 0) == 2
     if fields.get("input_format", 0) == 1:
         x = ((rec.codes.astype(np.float64) - 2047.5) / 2047.5).astype(np.float32)
         codes = torch.from_numpy(x).to(f"cuda:{device}")
+    elif packed:                          # RX_IN_U12_PACKED: 3 bytes per 2 codes
+        from rxsynth.gen import pack_u12
+        codes = torch.from_numpy(pack_u12(rec.codes)).to(f"cuda:{device}")
     else:
         codes = torch.from_numpy(rec.codes.view(np.int16)).to(f"cuda:{device}")
     if pre is not None:
@@ -50,7 +54,10 @@ def run_gpu(rec, rx, chunk=1 << 22, history_buffers=None, device=0, keep=True, p
     nsym_ub = rec.n // (2 if fam == RX_PAM else 4) + 4096
     labels = torch.full((nsym_ub,), 0xFF, dtype=torch.uint8, device=f"cuda:{device}")
     for off in range(0, rec.n, chunk):
-        R.process(codes[off:off + chunk], labels)
+        if packed:
+            R.process(codes[off * 3 // 2:(off + chunk) * 3 // 2], labels)
+        else:
+            R.process(codes[off:off + chunk], labels)
     R.flush(labels)
     st = R.stats()
     return R, labels.cpu().numpy(), st

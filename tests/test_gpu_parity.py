@@ -544,3 +544,17 @@ def test_time_varying_clock_offset_parity():
     assert rel_l2(R.probe("U", 0, m_end), out["u"]) < TOL_FIELD
     mism, excl = _compare_labels(rec, rx, out, labels, R)
     _compare_counters(rec, out, st, mism)
+
+
+@pytest.mark.parametrize("name", ["C1", "C3"])
+def test_packed_u12_input_is_bit_identical(name):
+    """RX_IN_U12_PACKED (2 codes per 3 bytes, the digitiser's 12-bit DMA format): the unpacking
+    is exact, so labels, counters and EVM equal the u16 input's bit for bit."""
+    _torch_cuda()
+    rec, rx = make_config(name, n_samples=(1 << 16) if name == "C1" else (1 << 20))
+    rx["buffer_blocks"] = 256 if name == "C3" else 8192
+    _, la, sa = run_gpu(rec, rx, chunk=256 * 512 * 3)
+    _, lb, sb = run_gpu(rec, dict(rx, input_format=2), chunk=256 * 512 * 3)
+    assert np.array_equal(la, lb)
+    for k in ("bit_errors", "bits", "symbols_counted", "clipped", "domain_errors", "evm_num", "evm_den"):
+        assert sa[k] == sb[k], k
