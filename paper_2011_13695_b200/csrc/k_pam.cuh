@@ -10,9 +10,6 @@
 #include "rx_dev.cuh"
 
 #define FE_GROUPS 4
-#ifndef FE_CTAS_PER_SM
-#define FE_CTAS_PER_SM 8   // grid cap of the grid-stride PAM front / back ends (0 = one CTA per group)
-#endif
 
 __device__ __forceinline__ float code_lo(uint32_t w) {     // exact float of the low 16 bits
   return __uint_as_float((w & 0xFFFFu) | 0x4B000000u) - 8388608.0f;
@@ -106,59 +103,54 @@ __global__ void __launch_bounds__(256) k_pam_fe(RxDev d, InView in, long long b0
   const int g = threadIdx.x >> 6, j = threadIdx.x & 63;
   for (int i = threadIdx.x; i < 1024; i += blockDim.x) tw[i] = d.tw[i];
   __syncthreads();   // twiddles visible to every group (the FFT barriers are per group)
-  // grid-stride over groups of FE_GROUPS blocks: the twiddles are staged once per CTA
-  for (long long base = b0 + (long long)blockIdx.x * FE_GROUPS; base < b1;
-       base += (long long)gridDim.x * FE_GROUPS) {
-    const long long b = base + g;
-    const bool act = b < b1;
-    int clip = 0;
-    float2 v[8];
-    if (act) clip = load_block_regs(in, b, d.scale, j, v);
-    else {
+  const long long b = b0 + (long long)blockIdx.x * FE_GROUPS + g;
+  const bool act = b < b1;
+  int clip = 0;
+  float2 v[8];
+  if (act) clip = load_block_regs(in, b, d.scale, j, v);
+  else {
 #pragma unroll
-      for (int r = 0; r < 8; ++r) v[r] = make_float2(0.f, 0.f);
-    }
-    block_reduce_clip(d.st, clip);
-    fft512_regs<false>(buf[g], j, tw, v);
-    fft512_publish_upper(buf[g], j, v);
-    // C_b = sum_{k<512} Y[k] conj(Y[k+512]) = Y0 conj(Y512) + Y256^2 + 2 sum_{k=1}^{255} Y[k] Y[512-k]
-    // (per-thread fp32 partials of 4-5 terms, fp64 across threads)
-    float cr = 0.f, ci = 0.f;
-    if (act) {
-      const float2 *pm = fft_mirror_base(buf[g], j);
-      float2 *xs = d.Xspec + rmod(b, d.xs_cap) * 512;
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int k = j + 64 * r;
-        float2 Xk, Xn;
-        r2c_pair(v[r], fft_partner(pm, j, r, v), tw[k], Xk, Xn);
-        // X for k_pam_be (slot 0 packs the real X[0], X[512]; slot k < 512 holds X[k])
-        if (k == 0) xs[0] = make_float2(Xk.x, Xn.x);
-        else { xs[k] = Xk; xs[512 - k] = Xn; }
-        float2 Yk, Yn;
-        if (HREAL) { Yk = cscale(Xk, __ldg(d.Hr + k)); Yn = cscale(Xn, __ldg(d.Hr + 512 - k)); }
-        else { Yk = cmul(Xk, __ldg(d.H + k)); Yn = cmul(Xn, __ldg(d.H + 512 - k)); }
-        if (k == 0) { cr = fmaf(Yk.x, Yn.x, fmaf(Yk.y, Yn.y, cr)); ci = fmaf(Yk.y, Yn.x, fmaf(-Yk.x, Yn.y, ci)); }
-        else {
-          cr = fmaf(2.f * Yk.x, Yn.x, fmaf(-2.f * Yk.y, Yn.y, cr));
-          ci = fmaf(2.f * Yk.x, Yn.y, fmaf(2.f * Yk.y, Yn.x, ci));
-        }
-      }
-      if (j == 0) {
-        const float2 Z = v[4];                                   // X[256] = conj Z[256]
-        xs[256] = cconj(Z);
-        const float2 Y = HREAL ? cscale(cconj(Z), __ldg(d.Hr + 256)) : cmul(cconj(Z), __ldg(d.H + 256));
-        cr = fmaf(Y.x, Y.x, fmaf(-Y.y, Y.y, cr));
-        ci = fmaf(2.f * Y.x, Y.y, ci);
-      }
-    }
-    const double dr = warp_sum_d((double)cr), di = warp_sum_d((double)ci);
-    if ((threadIdx.x & 31) == 0) red[g][(threadIdx.x >> 5) & 1] = make_double2(dr, di);
-    __syncthreads();
-    if (act && j == 0)
-      d.C[rmod(b, d.blk_cap)] = make_double2(red[g][0].x + red[g][1].x, red[g][0].y + red[g][1].y);
-    __syncthreads();   // buf / red are reused by the next group of blocks
+    for (int r = 0; r < 8; ++r) v[r] = make_float2(0.f, 0.f);
   }
+  block_reduce_clip(d.st, clip);
+  fft512_regs<false>(buf[g], j, tw, v);
+  fft512_publish_upper(buf[g], j, v);
+  // C_b = sum_{k<512} Y[k] conj(Y[k+512]) = Y0 conj(Y512) + Y256^2 + 2 sum_{k=1}^{255} Y[k] Y[512-k]
+  // (per-thread fp32 partials of 4-5 terms, fp64 across threads)
+  float cr = 0.f, ci = 0.f;
+  if (act) {
+    const float2 *pm = fft_mirror_base(buf[g], j);
+    float2 *xs = d.Xspec + rmod(b, d.xs_cap) * 512;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int k = j + 64 * r;
+      float2 Xk, Xn;
+      r2c_pair(v[r], fft_partner(pm, j, r, v), tw[k], Xk, Xn);
+      // X for k_pam_be (slot 0 packs the real X[0], X[512]; slot k < 512 holds X[k])
+      if (k == 0) xs[0] = make_float2(Xk.x, Xn.x);
+      else { xs[k] = Xk; xs[512 - k] = Xn; }
+      float2 Yk, Yn;
+      if (HREAL) { Yk = cscale(Xk, __ldg(d.Hr + k)); Yn = cscale(Xn, __ldg(d.Hr + 512 - k)); }
+      else { Yk = cmul(Xk, __ldg(d.H + k)); Yn = cmul(Xn, __ldg(d.H + 512 - k)); }
+      if (k == 0) { cr = fmaf(Yk.x, Yn.x, fmaf(Yk.y, Yn.y, cr)); ci = fmaf(Yk.y, Yn.x, fmaf(-Yk.x, Yn.y, ci)); }
+      else {
+        cr = fmaf(2.f * Yk.x, Yn.x, fmaf(-2.f * Yk.y, Yn.y, cr));
+        ci = fmaf(2.f * Yk.x, Yn.y, fmaf(2.f * Yk.y, Yn.x, ci));
+      }
+    }
+    if (j == 0) {
+      const float2 Z = v[4];                                   // X[256] = conj Z[256]
+      xs[256] = cconj(Z);
+      const float2 Y = HREAL ? cscale(cconj(Z), __ldg(d.Hr + 256)) : cmul(cconj(Z), __ldg(d.H + 256));
+      cr = fmaf(Y.x, Y.x, fmaf(-Y.y, Y.y, cr));
+      ci = fmaf(2.f * Y.x, Y.y, ci);
+    }
+  }
+  const double dr = warp_sum_d((double)cr), di = warp_sum_d((double)ci);
+  if ((threadIdx.x & 31) == 0) red[g][(threadIdx.x >> 5) & 1] = make_double2(dr, di);
+  __syncthreads();
+  if (act && j == 0)
+    d.C[rmod(b, d.blk_cap)] = make_double2(red[g][0].x + red[g][1].x, red[g][0].y + red[g][1].y);
 }
 
 // ------------------------------------------------------------------ H4
@@ -384,97 +376,92 @@ __global__ void __launch_bounds__(256) k_pam_be(RxDev d, long long b0, long long
   const int g = threadIdx.x >> 6, j = threadIdx.x & 63;
   for (int i = threadIdx.x; i < 1024; i += blockDim.x) tw[i] = d.tw[i];
   __syncthreads();   // twiddles visible to every group (the FFT barriers are per group)
-  // grid-stride over groups of FE_GROUPS blocks: the twiddles are staged once per CTA
-  for (long long base = b0 + (long long)blockIdx.x * FE_GROUPS; base < b1;
-       base += (long long)gridDim.x * FE_GROUPS) {
-    const long long b = base + g;
-    const bool act = b < b1;
-    // the block's spectrum X stored by k_pam_fe (SURVEY §8(a) 'read back spectra' option):
-    // thread j owns the pairs (k, 512 - k), k = j + 64 r, r < 4, and thread 0 also X[256]
-    float2 Xk_[4], Xn_[4], X256 = make_float2(0.f, 0.f);
-    {
-      const float2 *xs = d.Xspec + rmod(act ? b : b0, d.xs_cap) * 512;
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int k = j + 64 * r;
-        const float2 a = act ? xs[k] : make_float2(0.f, 0.f);
-        const float2 c = act ? xs[(512 - k) & 511] : make_float2(0.f, 0.f);
-        if (k == 0) { Xk_[r] = make_float2(a.x, 0.f); Xn_[r] = make_float2(a.y, 0.f); }
-        else { Xk_[r] = a; Xn_[r] = c; }
-      }
-      if (j == 0 && act) X256 = xs[256];
-    }
-    // clock phase of this block: s = 2 tau, i_b = rint(s), f_b = s - i_b   (c-4)
-    const double tau = act ? d.tau[rmod(b, d.blk_cap)] : 0.0;
-    const double sd = 2.0 * tau;
-    const double ibd = rint(sd);
-    const float f = (float)(sd - ibd);
-    // FD clock correction Y'[k] = Y[k] e^{+j pi kappa(k) f / 512}: rotations for k = j + 64 r from
-    // base e^{j pi j f/512} and step e^{j pi f/8}; the partner 512-k is e^{j pi f} conj(rot(k))
-    float2 rot, step, nyq;
-    sincospif((float)j * f * (1.0f / 512.0f), &rot.y, &rot.x);
-    sincospif(f * 0.125f, &step.y, &step.x);
-    sincospif(f, &nyq.y, &nyq.x);
-    float2 Zk[4], Zn[4], Z256;
+  const long long b = b0 + (long long)blockIdx.x * FE_GROUPS + g;
+  const bool act = b < b1;
+  // the block's spectrum X stored by k_pam_fe (SURVEY §8(a) 'read back spectra' option):
+  // thread j owns the pairs (k, 512 - k), k = j + 64 r, r < 4, and thread 0 also X[256]
+  float2 Xk_[4], Xn_[4], X256 = make_float2(0.f, 0.f);
+  {
+    const float2 *xs = d.Xspec + rmod(act ? b : b0, d.xs_cap) * 512;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int k = j + 64 * r;
-      const float2 Xk = Xk_[r], Xn = Xn_[r];
-      float2 Yk, Yn;
-      if (HREAL) { Yk = cscale(Xk, __ldg(d.Hr + k)); Yn = cscale(Xn, __ldg(d.Hr + 512 - k)); }
-      else { Yk = cmul(Xk, __ldg(d.H + k)); Yn = cmul(Xn, __ldg(d.H + 512 - k)); }
-      Yk = cmul(Yk, rot);
-      if (k == 0) Yn = make_float2(Yn.x * nyq.x + Yn.y * nyq.y, 0.0f);   // Nyquist: Re(Y e^{-j pi f})
-      else Yn = cmul(Yn, cmulc(nyq, rot));
-      c2r_pair(Yk, Yn, tw[k], Zk[r], Zn[r]);
-      rot = cmul(rot, step);
+      const float2 a = act ? xs[k] : make_float2(0.f, 0.f);
+      const float2 c = act ? xs[(512 - k) & 511] : make_float2(0.f, 0.f);
+      if (k == 0) { Xk_[r] = make_float2(a.x, 0.f); Xn_[r] = make_float2(a.y, 0.f); }
+      else { Xk_[r] = a; Xn_[r] = c; }
     }
-    {
-      float2 Y = HREAL ? cscale(X256, __ldg(d.Hr + 256)) : cmul(X256, __ldg(d.H + 256));
-      float2 r256;
-      sincospif(0.5f * f, &r256.y, &r256.x);
-      Z256 = cconj(cmul(Y, r256));
-    }
-    {
-      float2 *paw = buf[g] + j + (j >> 4);
-      float2 *pmw = buf[g] + (512 - j) + ((512 - j) >> 4);
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        paw[68 * r] = Zk[r];
-        if (!(j == 0 && r == 0)) pmw[-68 * r] = Zn[r];
-      }
-      if (j == 0) buf[g][256 + (256 >> 4)] = Z256;
-    }
-    __syncthreads();
-    float2 v[8];
-    fft512<true>(buf[g], j, tw, v);
-    fft512_store(buf[g], j, v);
-    // variable-rate extraction (c-4): u_m = y[2m + i_b - 512b + 512], m in [max(M_b,0), M_{b+1})
-    double part = 0.0;
-    if (act) {
-      const long long Mb = d.Mb[rmod(b, d.blk_cap)], Mb1 = d.Mb[rmod(b + 1, d.blk_cap)];
-      const long long lo = Mb > 0 ? Mb : 0;
-      const int base2 = (int)(2 * lo + (long long)ibd - 512 * b + 512);   // local index of m = lo
-      const int cnt = (int)(Mb1 - lo);
-      float ps = 0.f;
-      for (int t = j; t < cnt; t += 64) {
-        const long long m = lo + t;
-        int loc = base2 + 2 * t;                                        // 2m + i_b - 512b + 512
-        if (loc < 0 || loc >= 1024) { set_flag(d.st, 8); loc = loc < 0 ? 0 : 1023; }
-        const int n = loc >> 1;
-        const float2 zz = buf[g][n + (n >> 4)];
-        const float y = ((loc & 1) ? zz.y : zz.x) * (1.0f / 512.0f);
-        d.u[rmod(m, d.sym_cap)] = y;
-        ps += y;
-      }
-      part = (double)ps;
-    }
-    part = warp_sum_d(part);
-    if ((threadIdx.x & 31) == 0) red[g][(threadIdx.x >> 5) & 1] = part;
-    __syncthreads();
-    if (act && j == 0) d.blk_sum[rmod(b, d.blk_cap)] = red[g][0] + red[g][1];
-    __syncthreads();   // buf / red are reused by the next group of blocks
+    if (j == 0 && act) X256 = xs[256];
   }
+  // clock phase of this block: s = 2 tau, i_b = rint(s), f_b = s - i_b   (c-4)
+  const double tau = act ? d.tau[rmod(b, d.blk_cap)] : 0.0;
+  const double sd = 2.0 * tau;
+  const double ibd = rint(sd);
+  const float f = (float)(sd - ibd);
+  // FD clock correction Y'[k] = Y[k] e^{+j pi kappa(k) f / 512}: rotations for k = j + 64 r from
+  // base e^{j pi j f/512} and step e^{j pi f/8}; the partner 512-k is e^{j pi f} conj(rot(k))
+  float2 rot, step, nyq;
+  sincospif((float)j * f * (1.0f / 512.0f), &rot.y, &rot.x);
+  sincospif(f * 0.125f, &step.y, &step.x);
+  sincospif(f, &nyq.y, &nyq.x);
+  float2 Zk[4], Zn[4], Z256;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int k = j + 64 * r;
+    const float2 Xk = Xk_[r], Xn = Xn_[r];
+    float2 Yk, Yn;
+    if (HREAL) { Yk = cscale(Xk, __ldg(d.Hr + k)); Yn = cscale(Xn, __ldg(d.Hr + 512 - k)); }
+    else { Yk = cmul(Xk, __ldg(d.H + k)); Yn = cmul(Xn, __ldg(d.H + 512 - k)); }
+    Yk = cmul(Yk, rot);
+    if (k == 0) Yn = make_float2(Yn.x * nyq.x + Yn.y * nyq.y, 0.0f);   // Nyquist: Re(Y e^{-j pi f})
+    else Yn = cmul(Yn, cmulc(nyq, rot));
+    c2r_pair(Yk, Yn, tw[k], Zk[r], Zn[r]);
+    rot = cmul(rot, step);
+  }
+  {
+    float2 Y = HREAL ? cscale(X256, __ldg(d.Hr + 256)) : cmul(X256, __ldg(d.H + 256));
+    float2 r256;
+    sincospif(0.5f * f, &r256.y, &r256.x);
+    Z256 = cconj(cmul(Y, r256));
+  }
+  {
+    float2 *paw = buf[g] + j + (j >> 4);
+    float2 *pmw = buf[g] + (512 - j) + ((512 - j) >> 4);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      paw[68 * r] = Zk[r];
+      if (!(j == 0 && r == 0)) pmw[-68 * r] = Zn[r];
+    }
+    if (j == 0) buf[g][256 + (256 >> 4)] = Z256;
+  }
+  __syncthreads();
+  float2 v[8];
+  fft512<true>(buf[g], j, tw, v);
+  fft512_store(buf[g], j, v);
+  // variable-rate extraction (c-4): u_m = y[2m + i_b - 512b + 512], m in [max(M_b,0), M_{b+1})
+  double part = 0.0;
+  if (act) {
+    const long long Mb = d.Mb[rmod(b, d.blk_cap)], Mb1 = d.Mb[rmod(b + 1, d.blk_cap)];
+    const long long lo = Mb > 0 ? Mb : 0;
+    const int base2 = (int)(2 * lo + (long long)ibd - 512 * b + 512);   // local index of m = lo
+    const int cnt = (int)(Mb1 - lo);
+    float ps = 0.f;
+    for (int t = j; t < cnt; t += 64) {
+      const long long m = lo + t;
+      int loc = base2 + 2 * t;                                        // 2m + i_b - 512b + 512
+      if (loc < 0 || loc >= 1024) { set_flag(d.st, 8); loc = loc < 0 ? 0 : 1023; }
+      const int n = loc >> 1;
+      const float2 zz = buf[g][n + (n >> 4)];
+      const float y = ((loc & 1) ? zz.y : zz.x) * (1.0f / 512.0f);
+      d.u[rmod(m, d.sym_cap)] = y;
+      ps += y;
+    }
+    part = (double)ps;
+  }
+  part = warp_sum_d(part);
+  if ((threadIdx.x & 31) == 0) red[g][(threadIdx.x >> 5) & 1] = part;
+  __syncthreads();
+  if (act && j == 0) d.blk_sum[rmod(b, d.blk_cap)] = red[g][0] + red[g][1];
 }
 
 // Buffer-wise normalisation (P:167 'three kernels: initialization, estimation of the DC-offset,

@@ -592,13 +592,6 @@ static rx_status check_launch() {
 }
 
 static unsigned gridc(long long n, int per) { return (unsigned)((n + per - 1) / per); }
-// grid of the grid-stride PAM front / back ends: one CTA per FE_GROUPS blocks, capped at
-// FE_CTAS_PER_SM resident CTAs per SM
-static unsigned fe_grid(const rx_handle *h, long long nblocks) {
-  const unsigned g = gridc(nblocks, FE_GROUPS);
-  const unsigned cap = FE_CTAS_PER_SM > 0 ? (unsigned)(FE_CTAS_PER_SM * h->n_sm) : g;
-  return g < cap ? g : cap;
-}
 
 // tap padding KP in {4, 8, 16, 32} (compile-time) and the CPR flavour select the instance
 typedef void (*lms_seg_fn)(RxDev, int, int, unsigned char *, long long);
@@ -737,10 +730,11 @@ static void launch_norm_pam(rx_handle *h, cudaStream_t s, int flush) {
 static void run_pam(rx_handle *h, cudaStream_t s, const InView &in, unsigned char *labels,
                     long long lab_cap, int flush) {
   RxDev &d = h->d;
+  const long long BB = d.buffer_blocks;
   const long long fe_target = h->n_in / 512;
   if (fe_target > h->fe_done) {
-    if (d.H_real) KLAUNCH(h, RX_K_PAM_FE, s, (k_pam_fe<true><<<fe_grid(h, fe_target - h->fe_done), 256, 0, s>>>(d, in, h->fe_done, fe_target)));
-    else KLAUNCH(h, RX_K_PAM_FE, s, (k_pam_fe<false><<<fe_grid(h, fe_target - h->fe_done), 256, 0, s>>>(d, in, h->fe_done, fe_target)));
+    if (d.H_real) KLAUNCH(h, RX_K_PAM_FE, s, (k_pam_fe<true><<<gridc(fe_target - h->fe_done, FE_GROUPS), 256, 0, s>>>(d, in, h->fe_done, fe_target)));
+    else KLAUNCH(h, RX_K_PAM_FE, s, (k_pam_fe<false><<<gridc(fe_target - h->fe_done, FE_GROUPS), 256, 0, s>>>(d, in, h->fe_done, fe_target)));
     h->fe_done = fe_target;
   }
   long long clk_target = flush ? h->fe_done : h->fe_done - d.clock_half;
@@ -760,8 +754,8 @@ static void run_pam(rx_handle *h, cudaStream_t s, const InView &in, unsigned cha
   }
   long long be_target = flush ? h->fe_done - 1 : h->clk_done - 1;
   if (be_target > h->be_done) {
-    if (d.H_real) KLAUNCH(h, RX_K_PAM_BE, s, (k_pam_be<true><<<fe_grid(h, be_target - h->be_done), 256, 0, s>>>(d, h->be_done, be_target)));
-    else KLAUNCH(h, RX_K_PAM_BE, s, (k_pam_be<false><<<fe_grid(h, be_target - h->be_done), 256, 0, s>>>(d, h->be_done, be_target)));
+    if (d.H_real) KLAUNCH(h, RX_K_PAM_BE, s, (k_pam_be<true><<<gridc(be_target - h->be_done, FE_GROUPS), 256, 0, s>>>(d, h->be_done, be_target)));
+    else KLAUNCH(h, RX_K_PAM_BE, s, (k_pam_be<false><<<gridc(be_target - h->be_done, FE_GROUPS), 256, 0, s>>>(d, h->be_done, be_target)));
     h->be_done = be_target;
   }
   // streaming: the buffer normalisation runs on the equaliser side stream at the start of the
