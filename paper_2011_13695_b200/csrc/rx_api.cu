@@ -581,6 +581,9 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
     }                                    \
   } while (0)
 static int g_rx_debug = getenv("RX_DEBUG_SYNC") ? 1 : 0;
+// RX_CLK_FUSE_MAX (tests only): largest call, in clock tiles, that runs the fused one-pass clock
+// kernel; larger calls take the three-launch path (default CLK_FUSE_MAX)
+static long long g_clk_fuse_max = getenv("RX_CLK_FUSE_MAX") ? atoll(getenv("RX_CLK_FUSE_MAX")) : CLK_FUSE_MAX;
 
 static rx_status check_launch() {
   cudaError_t e = cudaGetLastError();
@@ -741,7 +744,7 @@ static void run_pam(rx_handle *h, cudaStream_t s, const InView &in, unsigned cha
   if (clk_target > h->clk_done) {
     const size_t smem = (CLK_TILE + 1 + 2 * d.clock_half) * sizeof(double2);
     const unsigned ntiles = gridc(clk_target - h->clk_done, CLK_TILE);
-    if (ntiles <= CLK_FUSE_MAX) {   // every tile co-resident: one pass + the carry
+    if (ntiles <= g_clk_fuse_max && ntiles <= CLK_FUSE_MAX) {   // every tile co-resident: one pass + carry
       const long long id = ++h->clk_launch;
       KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_pam_theta<true><<<ntiles, CLK_TILE, smem, s>>>(d, h->clk_done, clk_target, h->fe_done - 1, id)));
       KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_pam_clock_carry<<<1, 32, 0, s>>>(d, (int)ntiles)));

@@ -558,3 +558,39 @@ def test_packed_u12_input_is_bit_identical(name):
     assert np.array_equal(la, lb)
     for k in ("bit_errors", "bits", "symbols_counted", "clipped", "domain_errors", "evm_num", "evm_den"):
         assert sa[k] == sb[k], k
+
+
+def test_unfused_clock_path_matches():
+    """Calls longer than CLK_FUSE_MAX clock tiles take the three-launch clock path (tile sums,
+    one-CTA carry scan, tau / M_b): forced here (RX_CLK_FUSE_MAX=0, read at library load, so in a
+    subprocess) on the C2 structure, tau against the oracle and labels / counters equal."""
+    _torch_cuda()
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, json\n"
+        "from rxsynth import make_config\n"
+        "from tests.gpu_util import run_gpu\n"
+        "rec, rx = make_config('C2', n_samples=1 << 21)\n"
+        "rx['buffer_blocks'] = 256\n"
+        "R, lab, st = run_gpu(rec, rx, chunk=256 * 512 * 2)\n"
+        "np.save('/tmp/rx_unfused_tau.npy', R.probe('TAU', 0, rec.n // 512))\n"
+        "np.save('/tmp/rx_unfused_lab.npy', lab)\n"
+        "print(json.dumps({k: st[k] for k in ('bit_errors', 'bits', 'symbols_counted')}))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, RX_CLK_FUSE_MAX="0", PYTHONPATH=root)
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    import json
+    st_u = json.loads(out.stdout.strip().splitlines()[-1])
+    rec, rx = make_config("C2", n_samples=1 << 21)
+    rx["buffer_blocks"] = 256
+    ref = run_oracle(rec, rx)
+    R, lab, st = run_gpu(rec, rx, chunk=256 * 512 * 2)
+    tau_u = np.load("/tmp/rx_unfused_tau.npy")
+    assert np.max(np.abs(tau_u - ref["clock"]["tau"])) < TOL_TAU
+    lab_u = np.load("/tmp/rx_unfused_lab.npy")
+    assert np.mean(lab_u != lab) <= 1e-4
+    assert st_u["bits"] == st["bits"] and st_u["symbols_counted"] == st["symbols_counted"]
