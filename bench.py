@@ -577,6 +577,7 @@ def gpu_main(args):
     Rp = make_pam(input_format=2)
     line["e2e"] = e2e_value(Rp, True)
     line["e2e"]["input"] = "pinned host, RX_IN_U12_PACKED (2 codes per 3 bytes)"
+    line["e2e"]["x_paper_realtime"] = round(line["e2e"]["value"] / world / PAPER_REALTIME_GSA, 2)
     Rp.close()
     line["e2e_u16"] = e2e_value(R, False)
     R.close()
