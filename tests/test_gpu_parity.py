@@ -594,3 +594,24 @@ def test_unfused_clock_path_matches():
     lab_u = np.load("/tmp/rx_unfused_lab.npy")
     assert np.mean(lab_u != lab) <= 1e-4
     assert st_u["bits"] == st["bits"] and st_u["symbols_counted"] == st["symbols_counted"]
+
+
+@pytest.mark.parametrize("name,over", [
+    ("C1", dict(lms_taps=1, lms_segment=64, train_symbols=256)),                    # 1 tap, tiny segments
+    ("C3", dict(lms_taps=1, lms_segment=64, lms_overlap=32, train_symbols=256)),    # KK, VV, 1 tap
+    ("C3", dict(lms_taps=32, lms_segment=8192, lms_overlap=512)),                   # widest taps / overlap
+])
+def test_degenerate_equaliser_configs(name, over):
+    """Degenerate but valid equaliser shapes (SURVEY §8(b) limits: K = 1 and K = 32 taps,
+    64-symbol segments, minimal / maximal overlap, short training) against the oracle."""
+    _torch_cuda()
+    rec, rx = make_config(name, n_samples=(1 << 16) if name == "C1" else (1 << 19))
+    rx.update(over)
+    if name == "C3":
+        rx["buffer_blocks"] = 256
+    out = run_oracle(rec, rx)
+    R, labels, st = run_gpu(rec, rx, chunk=256 * 512)
+    assert st["sync_offset"] == out["sync"]["offset"]
+    assert rel_l2(R.train_taps(), out["lms"]["w_train"]) < 1e-3
+    mism, excl = _compare_labels(rec, rx, out, labels, R)
+    _compare_counters(rec, out, st, mism)
