@@ -293,6 +293,7 @@ static int gray_dec(int g) {
 extern "C" void rx_destroy(rx_handle *h) {
   if (!h) return;
   cudaSetDevice(h->device);
+  if (h->side) cudaStreamSynchronize(h->side);   // equaliser work still reading the rings
   for (void *p : h->allocs) cudaFree(p);
   if (h->hm_host) cudaFreeHost(h->hm_host);
   if (h->side) cudaStreamDestroy(h->side);
