@@ -987,13 +987,15 @@ __global__ void __launch_bounds__(1024) k_lms_prefix(RxDev d, int flush, int max
   // anchor
   const long long s0 = d.m0 / d.S;
   __shared__ int A_sh, known_sh;
-  if (t == 0) { A_sh = st->anchor_A; known_sh = st->anchor_known; }
-  __syncthreads();
-  if (!known_sh && d.anchor_each) {   // R-ANCHOR2: every R_s is absolute (k_lms_stitch)
-    if (t == 0) { A_sh = 0; known_sh = 1; }
-    __syncthreads();
+  if (t == 0) {
+    A_sh = st->anchor_A;
+    known_sh = st->anchor_known;
+    if (!known_sh && d.anchor_each) { A_sh = 0; known_sh = 1; }   // R-ANCHOR2: every R_s is absolute
   }
-  if (!known_sh) {
+  __syncthreads();
+  const int known0 = known_sh;        // block-uniform copy: thread 0 may update known_sh below
+  __syncthreads();
+  if (!known0) {
     const long long me = st->m_end;
     const bool s0_exists = !(me >= 0 && s0 * (long long)d.S >= me);
     if (d.family == 0) {
