@@ -295,7 +295,7 @@ def kk_record(M: int, n_samples: int, *, seed: int, cspr_db: float, osnr_db: flo
               cfo_hz: float = 0.0, linewidth_hz: float = 0.0, rx_lpf: bool = False,
               roadm_b3db: float | None = None, offset: int | None = None,
               carrier_hz: float = 0.547e9, n_static_taps: int = 203,
-              periodic: bool = False, iq_imbalance: complex = 0.0) -> Record:
+              periodic: bool = False, iq_imbalance: complex = 0.0, keep_field: bool = False) -> Record:
     """1 GBaud QAM-M at 4 sps with a digital carrier tone 0.547 GHz above the data.
 
     Field in the tone's frame: E = A + s(t) e^{-j 2 pi f_c t}, |A|^2 = CSPR * mean|s|^2;
@@ -346,6 +346,7 @@ def kk_record(M: int, n_samples: int, *, seed: int, cspr_db: float, osnr_db: flo
     Ps = float(np.mean(np.abs(s) ** 2))
     A = math.sqrt(10.0 ** (cspr_db / 10.0) * Ps)
     E = A + s * np.exp(-2j * math.pi * carrier_hz / FS * n)
+    field = s if keep_field else None     # the transmitted data field (test reference)
     del s
     if osnr_db is not None:
         Ptot = A * A + Ps
@@ -362,7 +363,7 @@ def kk_record(M: int, n_samples: int, *, seed: int, cspr_db: float, osnr_db: flo
                   meta=dict(seed=seed, cspr_db=cspr_db, osnr_db=osnr_db, cfo_hz=cfo_hz,
                             linewidth_hz=linewidth_hz, rx_lpf=rx_lpf, roadm_b3db=roadm_b3db,
                             carrier_hz=carrier_hz, clipped=clipped, full_scale=fs,
-                            iq_imbalance=complex(iq_imbalance),
+                            iq_imbalance=complex(iq_imbalance), field=field,
                             tone_amp=A, data_power=Ps))
 
 

@@ -615,3 +615,57 @@ def test_degenerate_equaliser_configs(name, over):
     assert rel_l2(R.train_taps(), out["lms"]["w_train"]) < 1e-3
     mism, excl = _compare_labels(rec, rx, out, labels, R)
     _compare_counters(rec, out, st, mism)
+
+
+_PAM4_REC = {}
+
+
+def _pam4_q_windows(ppm=None, ppm_triangle=0.0, n_ring=1 << 24, window=1 << 20):
+    import torch
+    from paper_2011_13695_b200 import RX_PAM, Receiver, multi
+    from rxsynth.ring import pam_ring
+    if not _PAM4_REC:      # one periodic PAM-4 waveform; the GPU ring resamples it at any clock
+        _PAM4_REC["r"] = make_config("C2", n_samples=32767 * 512, M=4, snr_db=17.0, ppm=0.0, keep_tx=True)
+    rec, rx = _PAM4_REC["r"]
+    ring = pam_ring(rec, n_ring, "cuda", seed=99, ppm=ppm if ppm is not None else 0.0,
+                    ppm_triangle=ppm_triangle)
+    fields = {k: v for k, v in rx.items() if k in ("lms_taps", "lms_block", "lms_segment", "mu",
+                                                   "train_symbols", "sync_start", "sync_window",
+                                                   "warmup_symbols")}
+    R = Receiver(RX_PAM, rec.M, rec.static_taps, history_buffers=6, q_window_symbols=window, **fields)
+    lab = torch.zeros(1 << 24, dtype=torch.uint8, device="cuda")
+    call = 4 << 22
+    for off in range(0, n_ring - n_ring % 512, call):
+        n = min(call, n_ring - off) // 512 * 512
+        R.process(ring[off:off + n], lab)
+    R.flush(lab)
+    st = R.stats()
+    nw = st["symbols_out"] // window
+    err, bits = R.q_trace(0, int(nw))
+    R.close()
+    q = [multi.q_db_from_ber(e / b) for e, b in zip(err[1:], bits[1:]) if b > 0]   # window 0: warm-up
+    return np.array(q), st
+
+
+def test_clock_plateau_static_offsets_spec_criterion_4():
+    """SPEC acceptance 4 (Fig. 4): PAM-4 at static offsets -30 .. +30 ppm in 10 ppm steps,
+    16.8 M samples each: Q spread <= 0.5 dB; no cliff at 30.5 ppm (closed-form symbol indices)."""
+    _torch_cuda()
+    qs = {}
+    for ppm in (-30, -20, -10, 0, 10, 20, 30):
+        q, st = _pam4_q_windows(ppm=float(ppm))
+        assert st["status_flags"] == 0
+        qs[ppm] = float(np.mean(q))
+    print("Q by ppm", {k: round(v, 3) for k, v in qs.items()})
+    assert max(qs.values()) - min(qs.values()) <= 0.5
+
+
+def test_free_running_clock_q_windows_spec_criterion_5():
+    """SPEC acceptance 5 (Fig. 5, P:203 'Q-factor remains constant'): a +-20 ppm triangle clock
+    offset over a 1.3e8-sample run; the windowed Q (1 M-symbol windows, rx_get_q_trace) has a
+    standard deviation < 0.5 dB."""
+    _torch_cuda()
+    q, st = _pam4_q_windows(ppm_triangle=20.0, n_ring=1 << 27)
+    print(f"free-running clock: {q.size} windows, Q mean {q.mean():.3f} dB, std {q.std():.3f} dB")
+    assert st["status_flags"] == 0 and q.size >= 50
+    assert q.std() < 0.5

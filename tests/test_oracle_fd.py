@@ -174,3 +174,26 @@ def test_stage2_equals_convolution_then_decimation_for_band_limited_field():
     # the periodic E is exactly band-limited inside each frame only when the frame holds
     # whole periods: frames are 1024 long, E is 1024-periodic -> exact
     assert np.max(np.abs(z[q] - ref)) < 1e-10 * np.max(np.abs(ref))
+
+
+def test_kk_reconstruction_fidelity_improves_with_cspr():
+    """SPEC acceptance 11 (the reason for the CSPR trade-off of Fig. 7): noiseless,
+    phase-noise-free SSB 16-QAM after square-law detection and the 12-bit ADC; the oracle's KK
+    stage 1 (c-6) reconstructs the data field s = sqrt(fs) E - A e^{j 2 pi f_c p} with an error
+    that strictly decreases over CSPR {3, 6, 9, 12, 15, 20} dB, below -25 dB at 20 dB (the
+    generator's transmitted field is the reference)."""
+    import math
+    from rxsynth import gen
+    evm = []
+    for cspr in (3, 6, 9, 12, 15, 20):
+        rec = gen.kk_record(16, 1 << 16, seed=5, cspr_db=cspr, osnr_db=None, keep_field=True)
+        x, _ = O.ingest(rec.codes)
+        E, _, _ = O.kk_stage1(x, rec.dc_offset, 0.547e9, -1, 4e9)
+        fs, A = rec.meta["full_scale"], rec.meta["tone_amp"]
+        n = np.arange(E.shape[0])
+        s_rec = math.sqrt(fs) * E - A * np.exp(2j * math.pi * 0.547e9 / 4e9 * n)
+        s = rec.meta["field"][:E.shape[0]]
+        mid = slice(4096, E.shape[0] - 4096)
+        evm.append(10 * math.log10(np.mean(np.abs(s_rec[mid] - s[mid]) ** 2) / np.mean(np.abs(s[mid]) ** 2)))
+    assert all(b < a for a, b in zip(evm, evm[1:])), evm
+    assert evm[-1] < -25, evm
