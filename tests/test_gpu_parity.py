@@ -669,3 +669,54 @@ def test_free_running_clock_q_windows_spec_criterion_5():
     print(f"free-running clock: {q.size} windows, Q mean {q.mean():.3f} dB, std {q.std():.3f} dB")
     assert st["status_flags"] == 0 and q.size >= 50
     assert q.std() < 0.5
+
+
+def _q_db(st):
+    from paper_2011_13695_b200 import multi
+    return multi.q_db_from_ber(st["bit_errors"] / st["bits"]) if st["bit_errors"] > 0 else float("inf")
+
+
+def test_cspr_optimum_spec_criterion_6():
+    """SPEC acceptance 6 (Fig. 7: 6 dB for QAM-4, 11 dB for QAM-16/64): Q against CSPR for
+    QAM-4 at OSNR 10 dB and QAM-16 at OSNR 20 dB (no phase noise, no CFO; 2^21 samples per point)
+    is single-peaked; the QAM-4 peak lies in 6 +- 2 dB. The synthetic link (AWGN at an OSNR over
+    the total power, 12-bit ADC, no receiver electrical noise) puts the QAM-16 peak at 7 dB, not
+    the paper's 11 dB, which SPEC does not claim in absolute terms ('shape, ordering'): the test
+    requires it above QAM-4's reconstruction-limited side (>= 5 dB) and reports it."""
+    _torch_cuda()
+    peaks = {}
+    for M, osnr, grid, lo, hi in ((4, 10.0, (2, 4, 6, 8, 10, 12, 14), 4, 8),
+                                  (16, 20.0, (5, 7, 9, 11, 13, 15, 17), 5, 13)):
+        qs = []
+        for cspr in grid:
+            rec, rx = make_config("C5:4" if M == 4 else "C5:5", n_samples=1 << 21, cspr_db=float(cspr),
+                                  osnr_db=osnr, cfo_hz=0.0, linewidth_hz=0.0, roadm_b3db=None)
+            rx.update(buffer_blocks=256, lms_taps=8)
+            _, _, st = run_gpu(rec, rx, chunk=256 * 512 * 2)
+            qs.append(_q_db(st))
+        print(f"QAM-{M} OSNR {osnr}: Q by CSPR", dict(zip(grid, [round(q, 2) for q in qs])))
+        k = int(np.argmax(qs))
+        assert lo <= grid[k] <= hi, (M, qs)
+        # single peak: rises to the maximum and falls after it (0.2 dB noise allowance)
+        assert all(qs[i + 1] >= qs[i] - 0.2 for i in range(k)) and all(qs[i + 1] <= qs[i] + 0.2 for i in range(k, len(qs) - 1)), qs
+
+
+def test_format_ordering_spec_criterion_7():
+    """SPEC acceptance 7 (Figs. 6, 9): at a common operating point, Q(PAM-2) > Q(PAM-4) > Q(PAM-8) >
+    Q(PAM-16) (same electrical SNR, C2 channel) and Q(QAM-4) > Q(QAM-16) > Q(QAM-64) (same OSNR)."""
+    _torch_cuda()
+    qp = []
+    for M in (2, 4, 8, 16):
+        rec, rx = make_config("C2", n_samples=1 << 21, M=M, snr_db=14.0)
+        rx["buffer_blocks"] = 256
+        _, _, st = run_gpu(rec, rx, chunk=256 * 512 * 2)
+        qp.append(_q_db(st))
+    qq = []
+    for ch, M in ((4, 4), (5, 16), (6, 64)):
+        rec, rx = make_config(f"C5:{ch}", n_samples=1 << 21, osnr_db=22.0, cspr_db=11.0)
+        rx["buffer_blocks"] = 256
+        _, _, st = run_gpu(rec, rx, chunk=256 * 512 * 2)
+        qq.append(_q_db(st))
+    print("Q PAM-2/4/8/16", [round(q, 2) for q in qp], "QAM-4/16/64", [round(q, 2) for q in qq])
+    assert qp[0] > qp[1] > qp[2] > qp[3]
+    assert qq[0] > qq[1] > qq[2]
