@@ -720,3 +720,44 @@ def test_format_ordering_spec_criterion_7():
     print("Q PAM-2/4/8/16", [round(q, 2) for q in qp], "QAM-4/16/64", [round(q, 2) for q in qq])
     assert qp[0] > qp[1] > qp[2] > qp[3]
     assert qq[0] > qq[1] > qq[2]
+
+
+@pytest.mark.parametrize("name", ["C2", "C4"])
+def test_randomised_scheduling_spec_criterion_10(name):
+    """SPEC acceptance 10 (determinism under parallelism), scaled to 8 buffers: 20 runs with random
+    call sizes (multiples of 512 up to the call limit), random equaliser batch sizes and the side
+    stream on or off give byte-identical labels and identical integer counters."""
+    torch = _torch_cuda()
+    from paper_2011_13695_b200 import RX_PAM, RX_QAM_KK, Receiver
+    rec, rx = make_config(name, n_samples=8 * 256 * 512)
+    fam = RX_PAM if rec.fmt == "pam" else RX_QAM_KK
+    fields = {k: v for k, v in rx.items() if k in ("lms_taps", "lms_block", "lms_segment", "lms_overlap", "mu",
+                                                   "train_symbols", "sync_start", "sync_window",
+                                                   "warmup_symbols", "cpr_test_phases")}
+    if fam == RX_QAM_KK:
+        fields["dc_offset"] = rec.dc_offset
+    codes = torch.from_numpy(rec.codes.view(np.int16)).cuda()
+    rng = np.random.default_rng(10)
+    ref = None
+    for run in range(20):
+        hb = int(rng.integers(3, 7))
+        R = Receiver(fam, rec.M, rec.static_taps, buffer_blocks=256, history_buffers=hb,
+                     lms_batch_segments=int(rng.choice([0, 1, 7, 64, 300])),
+                     serial_equaliser=int(rng.integers(0, 2)), **fields)
+        lab = torch.zeros(rec.n, dtype=torch.uint8, device="cuda")
+        max_blocks = (hb - 2) * 256
+        off = 0
+        while off < rec.n:
+            n = min(512 * int(rng.integers(1, max_blocks + 1)), rec.n - off)
+            R.process(codes[off:off + n], lab)
+            off += n
+        R.flush(lab)
+        st = R.stats()
+        R.close()
+        got = (lab.cpu().numpy(), {k: st[k] for k in ("bit_errors", "bits", "symbols_counted", "clipped",
+                                                       "domain_errors", "symbols_out", "sync_offset")})
+        if ref is None:
+            ref = got
+        else:
+            assert np.array_equal(got[0], ref[0]), run
+            assert got[1] == ref[1], (run, got[1], ref[1])
