@@ -761,3 +761,25 @@ def test_randomised_scheduling_spec_criterion_10(name):
         else:
             assert np.array_equal(got[0], ref[0]), run
             assert got[1] == ref[1], (run, got[1], ref[1])
+
+
+@pytest.mark.parametrize("fmt,M", [("pam", 2), ("pam", 4), ("pam", 8), ("pam", 16),
+                                   ("qam", 4), ("qam", 16), ("qam", 64)])
+def test_noiseless_error_free_spec_criterion_3(fmt, M):
+    """SPEC acceptance 3 through the GPU chain: noiseless, offset-free records of every
+    format decode with zero bit errors over >= 10^6 counted bits."""
+    _torch_cuda()
+    from rxsynth import gen
+    if fmt == "pam":
+        rec = gen.pam_record(M, 1 << 21, seed=30 + M, snr_db=None, channel="b2b")
+        rx = dict(lms_taps=15, lms_block=32, lms_segment=4096, lms_overlap=0, mu=1e-3, train_symbols=4096,
+                  sync_start=4096, sync_window=2048, warmup_symbols=8192, buffer_blocks=256)
+    else:
+        rec = gen.kk_record(M, 1 << 22, seed=40 + M, cspr_db=14.0, osnr_db=None)
+        rx = dict(lms_taps=8 if M < 64 else 16, lms_block=32, lms_segment=4096, lms_overlap=256, mu=2e-3,
+                  train_symbols=8192, sync_start=4096, sync_window=2048, warmup_symbols=16384,
+                  cpr_test_phases=0 if M == 4 else 32, buffer_blocks=256)
+    R, labels, st = run_gpu(rec, rx, chunk=256 * 512 * 4)
+    print(f"{fmt}-{M}: {st['bit_errors']} errors in {st['bits']} bits")
+    assert st["sync_offset"] == (rec.offset + 4096) % O.P_REF
+    assert st["bit_errors"] == 0 and st["bits"] >= 1_000_000
