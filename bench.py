@@ -490,7 +490,9 @@ def gpu_main(args):
     rec, rx = make_config("C2", seed=seed, keep_tx=True)
     t_gen = time.time() - t0
     n_step = N_C2
-    ring_samples = max(1, int(args.ring_gib * (1 << 30) / 2 // n_step)) * n_step
+    # >= 1 GiB (> L2) and long enough that the timed steps never wrap (a wrap restarts the
+    # clock-offset waveform and the PRBS): warm-up + 2 profiled + K timed + 3 isolated steps
+    ring_samples = max(int(args.ring_gib * (1 << 30) / 2 // n_step), args.warmup + args.steps + 6) * n_step
     ring = pam_ring(rec, ring_samples, dev, seed=seed)
     def make_pam(**kw):
         return Receiver(RX_PAM, rec.M, rec.static_taps, device=local, history_buffers=CALL_BUFFERS + 2,
