@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(256) k_kk_s2(RxDev d, long long b0, long long 
 // buffers that complete in one call (blockIdx.y = buffer of the call):
 //  k_cfo_spec   16 chunks of 1024 per CTA (one per 64-thread group): |DFT_1024(z^4)|^2 summed
 //               over the CTA's chunks in fixed group order -> one partial row; power partials
-//  k_cfo_final  one CTA per buffer: rows -> S[k] (fixed order), P, k* (lowest on ties), delta,
+//  (final)      the last k_cfo_spec CTA of each buffer: rows -> S[k] (fixed order), P, k* (lowest on ties), delta,
 //               coarse df and its DDS increment
 //  k_cfo_fine   one warp per chunk: a_i = sum (z e^{-j psi_c})^4; the last CTA of a buffer forms
 //               rho = sum a_{i+1} conj(a_i) in index order -> fine df
@@ -177,6 +177,75 @@ __device__ __forceinline__ void buf_range(const RxDev &d, long long beta, long l
   const long long Q = (long long)d.buffer_blocks * 256;
   qlo = beta * Q;
   qhi = qlo + Q < qfront ? qlo + Q : qfront;
+}
+
+// Per-buffer periodogram argmax + log-parabolic interpolation + power (c-8): the CTA that finishes
+// a buffer's spectrum rows (last-CTA ticket in k_cfo_spec) reduces them in fixed row order
+__device__ __forceinline__ void cfo_final_block(const RxDev &d, long long beta, long long qfront, long long rb, int nrows) {
+  __shared__ double Sd[1024];
+  __shared__ double wv[32];
+  __shared__ int wi[32];
+  __shared__ double pws[32];
+  const int t = threadIdx.x;
+  long long qlo, qhi;
+  buf_range(d, beta, qfront, qlo, qhi);
+  double s = 0.0;
+  {
+    int r = 0;
+    for (; r + 32 <= nrows; r += 32) {        // 32 independent loads in flight, summed in order
+      float v[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = __ldcg(d.cfo_part + (rb + r + i) * 1024 + t);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) s += (double)v[i];
+    }
+    for (; r < nrows; ++r) s += (double)__ldcg(d.cfo_part + (rb + r) * 1024 + t);
+  }
+  Sd[t] = s;
+  double pw = 0.0;
+  for (int r = t; r < nrows; r += blockDim.x) pw += __ldcg(d.cfo_pow + rb + r);
+  pw = warp_sum_d(pw);
+  if ((t & 31) == 0) pws[t >> 5] = pw;
+  double bv = s;
+  int bi = t;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+  }
+  if ((t & 31) == 0) { wv[t >> 5] = bv; wi[t >> 5] = bi; }
+  __syncthreads();
+  if (t == 0) {
+    double P = 0.0;
+    for (int w = 0; w < 32; ++w) P += pws[w];
+    const long long n = qhi - qlo;
+    P = n > 0 ? P / (double)n : 1.0;
+    if (!(P > 0.0)) P = 1.0;
+    double best = wv[0];
+    int k = wi[0];
+    for (int w = 1; w < 32; ++w)
+      if (wv[w] > best || (wv[w] == best && wi[w] < k)) { best = wv[w]; k = wi[w]; }
+    const long long nch = n / 1024;
+    double df = 0.0;
+    const bool have = nch > 0;
+    if (have) {
+      const double lm = log(Sd[(k + 1023) & 1023]), l0 = log(Sd[k]), lp = log(Sd[(k + 1) & 1023]);
+      const double delta = 0.5 * (lm - lp) / (lm - 2.0 * l0 + lp);
+      const double kap = (double)(k < 512 ? k : k - 1024);
+      df = (kap + delta) * d.fs2 / (4.0 * 1024.0);
+    } else {
+      k = -1;
+    }
+    CfoParam cp;
+    cp.P = P;
+    cp.inv_sqrtP = (float)(1.0 / sqrt(P));
+    cp.kstar = k;
+    cp.df = df;                      // coarse (refined by k_cfo_fine; kstar < 0: reuse previous)
+    cp.inc = (unsigned long long)llrint(ldexp(df / d.fs2, 64));
+    cp.origin = 0ull;
+    d.cfo[rmod(beta, d.buf_cap)] = cp;
+  }
 }
 
 __global__ void __launch_bounds__(1024) k_cfo_spec(RxDev d, long long beta0, long long qfront) {
@@ -246,76 +315,18 @@ __global__ void __launch_bounds__(1024) k_cfo_spec(RxDev d, long long beta0, lon
     for (int i = 0; i < 32; ++i) t += red[i];
     d.cfo_pow[row] = t;
   }
+  // the last CTA of this buffer reduces its rows (formerly the separate k_cfo_final launch)
+  __shared__ int ticket;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) ticket = atomicAdd(&d.cfo_tick_spec[blockIdx.y], 1);
+  __syncthreads();
+  if (ticket != (int)gridDim.x - 1) return;
+  __threadfence();
+  cfo_final_block(d, beta0 + blockIdx.y, qfront, (long long)blockIdx.y * gridDim.x, (int)gridDim.x);
+  if (threadIdx.x == 0) d.cfo_tick_spec[blockIdx.y] = 0;
 }
 
-__global__ void __launch_bounds__(1024) k_cfo_final(RxDev d, long long beta0, long long qfront, int nrows) {
-  __shared__ double Sd[1024];
-  __shared__ double wv[32];
-  __shared__ int wi[32];
-  __shared__ double pws[32];
-  const int t = threadIdx.x;
-  const long long beta = beta0 + blockIdx.x;
-  long long qlo, qhi;
-  buf_range(d, beta, qfront, qlo, qhi);
-  const long long rb = (long long)blockIdx.x * nrows;
-  double s = 0.0;
-  {
-    int r = 0;
-    for (; r + 32 <= nrows; r += 32) {        // 32 independent loads in flight, summed in order
-      float v[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = d.cfo_part[(rb + r + i) * 1024 + t];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) s += (double)v[i];
-    }
-    for (; r < nrows; ++r) s += (double)d.cfo_part[(rb + r) * 1024 + t];
-  }
-  Sd[t] = s;
-  double pw = 0.0;
-  for (int r = t; r < nrows; r += blockDim.x) pw += d.cfo_pow[rb + r];
-  pw = warp_sum_d(pw);
-  if ((t & 31) == 0) pws[t >> 5] = pw;
-  double bv = s;
-  int bi = t;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-    if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-  }
-  if ((t & 31) == 0) { wv[t >> 5] = bv; wi[t >> 5] = bi; }
-  __syncthreads();
-  if (t == 0) {
-    double P = 0.0;
-    for (int w = 0; w < 32; ++w) P += pws[w];
-    const long long n = qhi - qlo;
-    P = n > 0 ? P / (double)n : 1.0;
-    if (!(P > 0.0)) P = 1.0;
-    double best = wv[0];
-    int k = wi[0];
-    for (int w = 1; w < 32; ++w)
-      if (wv[w] > best || (wv[w] == best && wi[w] < k)) { best = wv[w]; k = wi[w]; }
-    const long long nch = n / 1024;
-    double df = 0.0;
-    const bool have = nch > 0;
-    if (have) {
-      const double lm = log(Sd[(k + 1023) & 1023]), l0 = log(Sd[k]), lp = log(Sd[(k + 1) & 1023]);
-      const double delta = 0.5 * (lm - lp) / (lm - 2.0 * l0 + lp);
-      const double kap = (double)(k < 512 ? k : k - 1024);
-      df = (kap + delta) * d.fs2 / (4.0 * 1024.0);
-    } else {
-      k = -1;
-    }
-    CfoParam cp;
-    cp.P = P;
-    cp.inv_sqrtP = (float)(1.0 / sqrt(P));
-    cp.kstar = k;
-    cp.df = df;                      // coarse (refined by k_cfo_fine; kstar < 0: reuse previous)
-    cp.inc = (unsigned long long)llrint(ldexp(df / d.fs2, 64));
-    cp.origin = 0ull;
-    d.cfo[rmod(beta, d.buf_cap)] = cp;
-  }
-}
 
 __global__ void __launch_bounds__(256) k_cfo_fine(RxDev d, long long beta0, long long qfront, int cta_per_buf) {
   __shared__ int ticket;

@@ -499,6 +499,7 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
     TRY(dalloc(h, &d.cfo_part, maxbuf * d.cfo_G * 1024));
     TRY(dalloc(h, &d.cfo_pow, maxbuf * d.cfo_G));
     TRY(dalloc(h, &d.cfo_tick, maxbuf));
+    TRY(dalloc(h, &d.cfo_tick_spec, maxbuf));
     TRY(dalloc(h, &d.cfo_a, maxbuf * (h->Q / 1024 + 1)));
   }
   TRY(dalloc(h, &d.sync_g, 2 * RX_PREF));
@@ -811,7 +812,6 @@ static void run_kk(rx_handle *h, cudaStream_t s, const InView &in, unsigned char
       for (long long b0 = 0; b0 < nbuf; b0 += h->cfg.history_buffers) {
         const long long nb = nbuf - b0 < h->cfg.history_buffers ? nbuf - b0 : h->cfg.history_buffers;
         KLAUNCH(h, RX_K_CFO, s, (k_cfo_spec<<<dim3((unsigned)nrows, (unsigned)nb), 1024, smem, s>>>(d, beta0 + b0, q_front)));
-        KLAUNCH(h, RX_K_CFO, s, (k_cfo_final<<<(unsigned)nb, 1024, 0, s>>>(d, beta0 + b0, q_front, nrows)));
         if (d.cfo_enable) KLAUNCH(h, RX_K_CFO, s, (k_cfo_fine<<<dim3((unsigned)fine_ctas, (unsigned)nb), 256, 0, s>>>(d, beta0 + b0, q_front, fine_ctas)));
         if (flush || h->cfg.serial_equaliser) {
           KLAUNCH(h, RX_K_CFO, s, (k_cfo_carry<<<1, 1, 0, s>>>(d, beta0 + b0, (int)nb)));

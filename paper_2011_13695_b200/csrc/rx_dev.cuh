@@ -94,7 +94,7 @@ struct RxDev {
   float2 *E; long long E_cap;
   float2 *z; long long z_cap;
   float2 *zp; long long zp_cap;     // z' = normalised, CFO-removed 2-sps field
-  CfoParam *cfo; float *cfo_part; double *cfo_pow; double2 *cfo_a; int *cfo_tick; int cfo_G;
+  CfoParam *cfo; float *cfo_part; double *cfo_pow; double2 *cfo_a; int *cfo_tick; int *cfo_tick_spec; int cfo_G;
   // ---- sync scratch
   float *sync_g; float2 *sync_c;
   // ---- LMS
