@@ -309,20 +309,29 @@ __global__ void __launch_bounds__(CLK_TILE) k_pam_theta(RxDev d, long long b0, l
       d.tau[rmod(b, d.blk_cap)] = tau;
       d.Mb[rmod(b, d.blk_cap)] = (long long)ceil(256.0 * (double)b - 128.0 - tau);
     }
+    // the last tile to finish (every tile has read the call's carry by then) advances the carry:
+    // thetau_prev += sum of the tile totals (lane-strided + warp tree, the former
+    // k_pam_clock_carry's order: a separate launch before), theta_prev = the call's last resolved phase
+    __shared__ int last_tile;
+    __syncthreads();
+    if (t == 0) {
+      __threadfence();
+      last_tile = atomicAdd(d.clk_ticket, 1) == (int)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last_tile && warp == 0) {
+      __threadfence();
+      double acc = 0.0;
+      for (int i = lane; i < (int)gridDim.x; i += 32) acc += ((volatile double *)d.clk_part)[i];
+      acc = warp_sum_d(acc);
+      if (lane == 0) {
+        d.st->thetau_prev += acc;
+        d.st->theta_prev = ((volatile double *)d.clk_last)[gridDim.x - 1];
+        *d.clk_ticket = 0;
+      }
+    }
   }
   (void)INV_2PI;
-}
-
-// carries after a fused clock launch: thetau_prev += sum of all tile totals, theta_prev
-__global__ void k_pam_clock_carry(RxDev d, int ntiles) {
-  const int lane = threadIdx.x;
-  double acc = 0.0;
-  for (int i = lane; i < ntiles; i += 32) acc += d.clk_part[i];
-  acc = warp_sum_d(acc);
-  if (lane == 0) {
-    d.st->thetau_prev += acc;
-    d.st->theta_prev = d.clk_last[ntiles - 1];
-  }
 }
 
 // (b) offsets of the tiles (exclusive scan of the tile totals, plus the carried unwrapped phase)

@@ -485,6 +485,7 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
     TRY(dalloc(h, &d.clk_off, maxtiles));
     TRY(dalloc(h, &d.clk_last, maxtiles));
     TRY(dalloc(h, &d.clk_flag, maxtiles));
+    TRY(dalloc(h, &d.clk_ticket, 1));
   } else {
     d.E_cap = next_pow2((long long)HB * c.buffer_blocks * 512);
     // (+ one call: the side stream's z' pass reads the previous call's z while stage 2 writes)
@@ -749,7 +750,6 @@ static void run_pam(rx_handle *h, cudaStream_t s, const InView &in, unsigned cha
     if (ntiles <= g_clk_fuse_max && ntiles <= CLK_FUSE_MAX) {   // every tile co-resident: one pass + carry
       const long long id = ++h->clk_launch;
       KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_pam_theta<true><<<ntiles, CLK_TILE, smem, s>>>(d, h->clk_done, clk_target, h->fe_done - 1, id)));
-      KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_pam_clock_carry<<<1, 32, 0, s>>>(d, (int)ntiles)));
     } else {
       KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_pam_theta<false><<<ntiles, CLK_TILE, smem, s>>>(d, h->clk_done, clk_target, h->fe_done - 1, 0)));
       KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_pam_carry<<<1, 1024, 0, s>>>(d, (int)ntiles)));

@@ -91,6 +91,7 @@ struct RxDev {
   double *norm_part; int *norm_tick;   // normalisation partials [16][NORM_G], tickets [16]
   double *clk_part, *clk_off, *clk_last; // unwrap tile totals / offsets / last phases
   long long *clk_flag;                   // fused clock: launch id that published each tile total
+  int *clk_ticket;                       // fused clock: tiles finished (the last one carries)
   float2 *E; long long E_cap;
   float2 *z; long long z_cap;
   float2 *zp; long long zp_cap;     // z' = normalised, CFO-removed 2-sps field
