@@ -118,6 +118,15 @@ typedef struct {
                                  symbols (window w = symbols [w W, (w+1) W)), the paper's "Q
                                  estimated from the BER in sections of 21 ms" (21 ms =
                                  42 M symbols at 2 GBaud); a multiple of lms_segment; 0 = off */
+  int lms_mode;               /* 0 (default): decision-directed segments (SURVEY c-9 'Per block j');
+                                 1: data aided - every segment adapts on the known PRBS reference
+                                 exactly as the training pass does (c-9 'Training': e = r - y, no
+                                 CPR), decisions slice(y) only feed labels / counters / EVM. The
+                                 equaliser output then has no decision feedback, so it is compared
+                                 with the oracle element by element (SURVEY §8(c) parity criterion
+                                 'equaliser output in training mode'); a BER tester's reference-
+                                 aided mode. Seeds: epoch means of the raw final taps (no R-SEED
+                                 phase normalisation: no CPR, the frame is absolute) */
 } rx_config;
 
 /* Sample formats accepted by rx_process:

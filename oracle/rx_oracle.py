@@ -490,6 +490,7 @@ class LmsParams:
     P_t: int = 32
     widely_linear: bool = False
     anchor_each: bool = False   # QAM: every segment's quadrant from the reference (DESIGN R-ANCHOR2)
+    data_aided: bool = False    # every segment adapts like the training pass (e = r - y, no CPR)
 
 
 def tap_matrix(v: np.ndarray, m: np.ndarray, stride: int, off: int, K: int) -> np.ndarray:
@@ -583,10 +584,14 @@ def _cpr_estimate(y, valid, slicer: _Slicer, lp: LmsParams):
 
 
 def lms_segments(v, stride, off, m_end, seeds_fn, slicer: _Slicer, lp: LmsParams,
-                 real: bool, segs):
+                 real: bool, segs, ref_val_fn=None):
     """Run segments ``segs`` of the segmented DD block-LMS (c-9 'Per block j'), in lockstep
     over block index (segments are independent). Returns per-segment dicts with the output
-    level indices, z', warm-up decisions, final taps and final theta."""
+    level indices, z', warm-up decisions, final taps and final theta.
+
+    lp.data_aided (rx_config.lms_mode = 1, DESIGN reading R-DA): every block adapts exactly as the
+    training pass of c-9 does - e_m = r_m - y_m with the reference value r_m = ref_val_fn(m), no
+    CPR (theta = 0) - and the decisions slice(y_m) only feed the outputs."""
     K, B, S, O = lp.K, lp.B, lp.S, lp.O
     segs = list(segs)
     ns = len(segs)
@@ -618,7 +623,7 @@ def lms_segments(v, stride, off, m_end, seeds_fn, slicer: _Slicer, lp: LmsParams
         y = np.einsum("sbk,sk->sb", U, np.conj(W))
         if lp.widely_linear:
             y = y + np.einsum("sbk,sk->sb", np.conj(U), np.conj(Vw))
-        if lp.cpr != "none":
+        if lp.cpr != "none" and not lp.data_aided:
             th_hat = _cpr_estimate(y, valid, slicer, lp)
             if j == 0:
                 th = th_hat
@@ -631,9 +636,12 @@ def lms_segments(v, stride, off, m_end, seeds_fn, slicer: _Slicer, lp: LmsParams
             zp = y
         idx = slicer.indices(zp)
         d = slicer.value(idx)
-        e = d - zp
-        if lp.cpr != "none":
-            e = e * np.exp(1j * theta)[:, None]
+        if lp.data_aided:
+            e = ref_val_fn(m) - y                              # c-9 'Training' error
+        else:
+            e = d - zp
+            if lp.cpr != "none":
+                e = e * np.exp(1j * theta)[:, None]
         e = np.where(valid, e, 0.0)
         W = W + lp.mu * np.einsum("sbk,sb->sk", U, np.conj(e))
         if lp.widely_linear:
@@ -690,7 +698,7 @@ def lms_full(v, stride, off, m_end, ref_idx_fn, ref_val_fn, slicer: _Slicer, lp:
 
     for wave in range(0, n_epoch, lp.D):
         segs = range(wave * seg_per_epoch, min(n_seg, (wave + lp.D) * seg_per_epoch))
-        res, dv = lms_segments(v, stride, off, m_end, seed, slicer, lp, real, segs)
+        res, dv = lms_segments(v, stride, off, m_end, seed, slicer, lp, real, segs, ref_val_fn)
         diverged |= dv
         for r in res:
             results[r["s"]] = r
@@ -733,8 +741,8 @@ def lms_full(v, stride, off, m_end, ref_idx_fn, ref_val_fn, slicer: _Slicer, lp:
                     R[s] = (R[s - 1] + r_rel[s]) % 4
         for s in segs:
             r = results[s]
-            if real:
-                canon[s] = r["w"]
+            if real or lp.data_aided:
+                canon[s] = r["w"]              # no CPR: the taps are in the absolute frame
             else:
                 # DESIGN.md reading R-SEED: remove the common (carrier) phase before the epoch
                 # average, phi_s = arg(sum_k w_k |w_k|); carrier phase noise decorrelates the
@@ -856,6 +864,7 @@ class RxParams:
     tap_lag_epochs: int = 8
     widely_linear: bool = False
     cpr_anchor: int = 1        # QAM: 1 = every segment anchored to the reference, 0 = c-9 chain
+    lms_mode: int = 0          # 0 = decision directed (c-9), 1 = data aided (DESIGN reading R-DA)
     mu: float = 1e-3
     train_symbols: int = 8192
     cpr_test_phases: int = 0
@@ -877,7 +886,8 @@ def _lms_params(p: RxParams) -> LmsParams:
     return LmsParams(K=p.lms_taps, B=p.lms_block, S=p.lms_segment, O=p.lms_overlap, mu=p.mu,
                      T_train=p.train_symbols, D=p.tap_lag_epochs, E=E, cpr=cpr,
                      P_t=max(p.cpr_test_phases, 1), widely_linear=p.widely_linear,
-                     anchor_each=bool(p.cpr_anchor) and p.fmt != "pam")
+                     anchor_each=bool(p.cpr_anchor) and p.fmt != "pam",
+                     data_aided=p.lms_mode == 1)
 
 
 def _finish(p: RxParams, v, stride, off, m_end, sync, out):

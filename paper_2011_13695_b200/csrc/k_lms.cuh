@@ -300,9 +300,10 @@ __device__ __forceinline__ float2 as_c(float2 v) { return v; }
 __device__ __forceinline__ float level_of(int i, float two_s, float off) { return fmaf((float)i, two_s, off); }
 
 // One warp runs block-LMS over symbols [t_begin, t_end) starting from tap wk (lane k).
-// MODE 0: training (e = r - y, no CPR), MODE 1: decision directed with CPR `CPR`
-// (0 none, 1 VV, 2 BPS). Outputs for m >= out_lo go to the level / yout rings,
-// warm-up decisions (m < out_lo) to warm[]. Returns final theta; accumulates EVM.
+// MODE 0: training (e = r - y, no CPR, no outputs), MODE 1: decision directed with CPR `CPR`
+// (0 none, 1 VV, 2 BPS), MODE 2: data aided (rx_config.lms_mode = 1: e = r - y, no CPR, as in
+// training, with decisions slice(y) and outputs). Outputs for m >= out_lo go to the level /
+// yout rings, warm-up decisions (m < out_lo) to warm[]. Returns final theta; accumulates EVM.
 //
 // Layout: taps are padded to KP in {4, 8, 16, 32} (zero taps, exact); lane i owns symbol i of
 // the block, lane k tap k; the inputs stream through a per-warp mirrored shared-memory ring
@@ -329,7 +330,7 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
   const float inv2s = 1.0f / two_s;
   const float Lh = 0.5f * (float)L, Lm1 = (float)(L - 1);
   const long long o_ref = d.st->sync_offset;
-  const int ref0 = MODE == 0 ? (int)(((o_ref + t_begin - d.m0) % RX_PREF + RX_PREF) % RX_PREF) : 0;
+  const int ref0 = MODE != 1 ? (int)(((o_ref + t_begin - d.m0) % RX_PREF + RX_PREF) % RX_PREF) : 0;
   float2 rotA = make_float2(1.f, 0.f), rotB = make_float2(1.f, 0.f);
   if (CPR == 2) {
     if (lane < d.Pt) rotA = __ldg(d.bps_rot + lane);
@@ -442,14 +443,15 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
     }
     float2 e, zp = y;
     int code = 0;
-    if (MODE == 0) {
+    if (MODE != 1) {        // training / data aided: the reference symbol drives the update
       int ri = ref0 + mr;
       while (ri >= RX_PREF) ri -= RX_PREF;
       const float2 r = __ldg(d.ref_val + ri);
       e = CPLX ? csub(r, y) : make_float2(r.x - y.x, 0.f);
-    } else {
+    }
+    if (MODE != 0) {
       float cth = 1.f, sth = 0.f;
-      if (CPLX && CPR != 0) {
+      if (CPLX && CPR != 0 && MODE == 1) {
         float th_hat;
         if (CPR == 1) {   // Viterbi-Viterbi: 1/4 arg(-sum y^4)
           const float2 y2 = cmul(y, y);
@@ -501,18 +503,18 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
         const float fI = fminf(fmaxf(floorf(fmaf(zp.x, inv2s, Lh)), 0.f), Lm1);
         const float fQ = fminf(fmaxf(floorf(fmaf(zp.y, inv2s, Lh)), 0.f), Lm1);
         dv = make_float2(fmaf(fI, two_s, lvl0), fmaf(fQ, two_s, lvl0));
-        e = cmul(csub(dv, zp), make_float2(cth, sth));
+        if (MODE == 1) e = cmul(csub(dv, zp), make_float2(cth, sth));
         code = (int)fI | ((int)fQ << 4);
       } else if (d.thr_default) {
         const float fi = fminf(fmaxf(floorf(fmaf(zp.x, inv2s, Lh)), 0.f), Lm1);
         dv = make_float2(fmaf(fi, two_s, lvl0), 0.f);
-        e = make_float2(dv.x - zp.x, 0.f);
+        if (MODE == 1) e = make_float2(dv.x - zp.x, 0.f);
         code = (int)fi;
       } else {
         const int i = slice_pam(d, zp.x);
         code = i;
         dv = make_float2(level_of(i, two_s, lvl0), 0.f);
-        e = make_float2(dv.x - zp.x, 0.f);
+        if (MODE == 1) e = make_float2(dv.x - zp.x, 0.f);
       }
       if (valid && mr >= olo) {
         const int ix = (mb0 + mr) & smask;
@@ -749,7 +751,7 @@ __device__ void bps_helper(const RxDev &d, const float2 *ys, long long t_begin, 
 #ifndef LMS_SPC
 #define LMS_SPC 4           // segments (warps) per CTA of k_lms_seg
 #endif
-template <bool CPLX, int CPR, int KP, bool WLIN = false>
+template <bool CPLX, int CPR, int KP, bool WLIN = false, int MODE = 1>
 __global__ void __launch_bounds__(32 * LMS_SPC) k_lms_seg(RxDev d, int flush, int nseg, unsigned char *labels,
                                                  long long lab_cap) {
   // BPS segments run on a warp pair (LMS warp + BPS helper), others on one warp
@@ -793,7 +795,7 @@ __global__ void __launch_bounds__(32 * LMS_SPC) k_lms_seg(RxDev d, int flush, in
     bps_helper(d, sm[warp].y, t0, hi, 1 + slot, bps_part[slot]);
     return;
   }
-  const float th = lms_run<CPLX, CPR, 1, KP, WLIN>(d, sm[warp], t0, hi, lo, wk, vk, warm, en, ed, vend,
+  const float th = lms_run<CPLX, CPR, MODE, KP, WLIN>(d, sm[warp], t0, hi, lo, wk, vk, warm, en, ed, vend,
                                                    PAIR == 2 ? 1 + slot : 0, bps_part[slot]);
   en = warp_sum_d(en);
   ed = warp_sum_d(ed);
@@ -1190,7 +1192,7 @@ __global__ void __launch_bounds__(256) k_lms_final(RxDev d, unsigned char *label
   if (threadIdx.x < 32) {
     const int k = threadIdx.x;
     float2 w = k < d.K ? d.seg_w[si * RX_MAX_K + k] : make_float2(0.f, 0.f);
-    if (d.family == 1) {
+    if (d.family == 1 && d.lms_mode == 0) {   // data aided (lms_mode 1): no CPR, absolute frame
       const float a = sqrtf(cabs2(w));
       const float px = warp_sum(w.x * a), py = warp_sum(w.y * a);
       const float inv = rsqrtf(fmaxf(px * px + py * py, 1e-30f));

@@ -217,7 +217,16 @@ __global__ void __launch_bounds__(CLK_TILE) k_pam_theta(RxDev d, long long b0, l
   __shared__ long long wmax[CLK_TILE / 32];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5, hh = d.clock_half;
   const double TWO_PI = 6.283185307179586476925, INV_2PI = 0.15915494309189533577;
-  const long long base = b0 + (long long)blockIdx.x * CLK_TILE;
+  // FUSED: the tile index is taken in dispatch order from a counter (clk_ticket[1]), not from
+  // blockIdx, so a tile only ever waits on tiles that are already resident (decoupled look-back
+  // ordering; no reliance on blockIdx-ordered CTA dispatch)
+  __shared__ int tile_sh;
+  if (FUSED) {
+    if (t == 0) tile_sh = atomicAdd(d.clk_ticket + 1, 1);
+    __syncthreads();
+  }
+  const int tile = FUSED ? tile_sh : (int)blockIdx.x;
+  const long long base = b0 + (long long)tile * CLK_TILE;
   for (int i = t; i < CLK_TILE + 1 + 2 * hh; i += blockDim.x) {
     const long long b = base - 1 - hh + i;
     Ct[i] = (b >= 0 && b <= blast) ? d.C[rmod(b, d.blk_cap)] : make_double2(0.0, 0.0);
@@ -282,11 +291,11 @@ __global__ void __launch_bounds__(CLK_TILE) k_pam_theta(RxDev d, long long b0, l
   if (t == CLK_TILE - 1) {
     double tot = 0.0;
     for (int w = 0; w < CLK_TILE / 32; ++w) tot += wsum[w];
-    d.clk_part[blockIdx.x] = tot;
-    d.clk_last[blockIdx.x] = tcur;                       // resolved phase of the tile's last block
+    d.clk_part[tile] = tot;
+    d.clk_last[tile] = tcur;                             // resolved phase of the tile's last block
     if (FUSED) {
       __threadfence();
-      atomicExch((unsigned long long *)&d.clk_flag[blockIdx.x], (unsigned long long)launch_id);
+      atomicExch((unsigned long long *)&d.clk_flag[tile], (unsigned long long)launch_id);
     }
   }
   if constexpr (FUSED) {
@@ -294,7 +303,7 @@ __global__ void __launch_bounds__(CLK_TILE) k_pam_theta(RxDev d, long long b0, l
     __shared__ double tile_off;
     if (warp == 0) {
       double acc = 0.0;
-      for (int i = lane; i < (int)blockIdx.x; i += 32) {
+      for (int i = lane; i < tile; i += 32) {
         while (((volatile long long *)d.clk_flag)[i] != launch_id) { }
         __threadfence();
         acc += ((volatile double *)d.clk_part)[i];
@@ -327,7 +336,8 @@ __global__ void __launch_bounds__(CLK_TILE) k_pam_theta(RxDev d, long long b0, l
       if (lane == 0) {
         d.st->thetau_prev += acc;
         d.st->theta_prev = ((volatile double *)d.clk_last)[gridDim.x - 1];
-        *d.clk_ticket = 0;
+        d.clk_ticket[0] = 0;
+        d.clk_ticket[1] = 0;                             // every tile has taken its index
       }
     }
   }

@@ -264,6 +264,7 @@ static rx_status validate(const rx_config *c) {
     return RX_EINVAL;
   if (c->serial_equaliser != 0 && c->serial_equaliser != 1) return RX_EINVAL;
   if (c->cpr_anchor != 0 && c->cpr_anchor != 1) return RX_EINVAL;
+  if (c->lms_mode != 0 && c->lms_mode != 1) return RX_EINVAL;
   if (c->q_window_symbols < 0 || (c->q_window_symbols > 0 && c->q_window_symbols % c->lms_segment)) return RX_EINVAL;
   if (c->lms_batch_segments < 0 || c->lms_batch_segments > (1 << 16)) return RX_EINVAL;
   if (c->family == RX_QAM_KK && !(c->sideband == 1 || c->sideband == -1)) return RX_EINVAL;
@@ -337,6 +338,7 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   d.K = c.lms_taps; d.B = c.lms_block; d.S = c.lms_segment; d.O = c.lms_overlap;
   d.D = c.tap_lag_epochs;
   d.cpr = kk ? (c.cpr_test_phases == 0 ? 1 : 2) : 0;
+  d.lms_mode = c.lms_mode;
   d.Pt = c.cpr_test_phases;
   d.anchor_each = kk && c.cpr_anchor;
   d.mu = (float)c.mu;
@@ -485,7 +487,7 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
     TRY(dalloc(h, &d.clk_off, maxtiles));
     TRY(dalloc(h, &d.clk_last, maxtiles));
     TRY(dalloc(h, &d.clk_flag, maxtiles));
-    TRY(dalloc(h, &d.clk_ticket, 1));
+    TRY(dalloc(h, &d.clk_ticket, 2));   // [0] tiles finished, [1] tiles dispatched
   } else {
     d.E_cap = next_pow2((long long)HB * c.buffer_blocks * 512);
     // (+ one call: the side stream's z' pass reads the previous call's z while stage 2 writes)
@@ -603,16 +605,20 @@ static unsigned gridc(long long n, int per) { return (unsigned)((n + per - 1) / 
 typedef void (*lms_seg_fn)(RxDev, int, int, unsigned char *, long long);
 typedef void (*lms_train_fn)(RxDev, int);
 static int kp_of(int K) { return K <= 4 ? 4 : (K <= 8 ? 8 : (K <= 16 ? 16 : 32)); }
-template <bool CPLX, int CPR, bool WL = false>
+template <bool CPLX, int CPR, bool WL = false, int MODE = 1>
 static lms_seg_fn seg_kp(int K) {
   switch (kp_of(K)) {
-    case 4: return k_lms_seg<CPLX, CPR, 4, WL>;
-    case 8: return k_lms_seg<CPLX, CPR, 8, WL>;
-    case 16: return k_lms_seg<CPLX, CPR, 16, WL>;
-    default: return k_lms_seg<CPLX, CPR, 32, WL>;
+    case 4: return k_lms_seg<CPLX, CPR, 4, WL, MODE>;
+    case 8: return k_lms_seg<CPLX, CPR, 8, WL, MODE>;
+    case 16: return k_lms_seg<CPLX, CPR, 16, WL, MODE>;
+    default: return k_lms_seg<CPLX, CPR, 32, WL, MODE>;
   }
 }
 static lms_seg_fn lms_seg_kernel(const RxDev &d) {
+  if (d.lms_mode == 1) {   // data aided: reference-driven updates, no CPR (MODE 2)
+    if (d.family == RX_PAM) return seg_kp<false, 0, false, 2>(d.K);
+    return d.wl ? seg_kp<true, 0, true, 2>(d.K) : seg_kp<true, 0, false, 2>(d.K);
+  }
   if (d.family == RX_PAM) return seg_kp<false, 0>(d.K);
   if (d.wl) return d.cpr == 1 ? seg_kp<true, 1, true>(d.K) : seg_kp<true, 2, true>(d.K);
   return d.cpr == 1 ? seg_kp<true, 1>(d.K) : seg_kp<true, 2>(d.K);

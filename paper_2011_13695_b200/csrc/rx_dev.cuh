@@ -61,6 +61,7 @@ struct RxDev {
   long long E_sym;           // symbols per LMS epoch
   int K, B, S, O, D, cpr, Pt;
   int anchor_each;           // KK: every segment's quadrant from the reference (R-ANCHOR2)
+  int lms_mode;              // 0 decision directed (c-9), 1 data aided (reference-driven, no CPR)
   float mu;
   int T_train;
   long long m0;
@@ -91,7 +92,8 @@ struct RxDev {
   double *norm_part; int *norm_tick;   // normalisation partials [16][NORM_G], tickets [16]
   double *clk_part, *clk_off, *clk_last; // unwrap tile totals / offsets / last phases
   long long *clk_flag;                   // fused clock: launch id that published each tile total
-  int *clk_ticket;                       // fused clock: tiles finished (the last one carries)
+  int *clk_ticket;                       // fused clock: [0] tiles finished (the last one carries),
+                                         // [1] tiles dispatched (dispatch-order tile index)
   float2 *E; long long E_cap;
   float2 *z; long long z_cap;
   float2 *zp; long long zp_cap;     // z' = normalised, CFO-removed 2-sps field

@@ -46,6 +46,7 @@ class RxConfig(ctypes.Structure):
         ("input_format", ctypes.c_int),
         ("serial_equaliser", ctypes.c_int),
         ("q_window_symbols", _c_ll),
+        ("lms_mode", ctypes.c_int),
     ]
 
 

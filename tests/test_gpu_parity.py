@@ -58,21 +58,54 @@ def _bps_flip_blocks(R, rx, out, m_end):
     # of the argmax, or - at full record sizes - a lag-D seed that inherited such a divergence
     # from an earlier epoch); several steps would be a bug. The segment's later blocks follow
     # another trajectory and are excluded with it
+    # CPR unwrap ties (BPS): the unwrap step rounds (theta_{j-1} - theta^_j)/(pi/2); on the test-phase
+    # grid that quotient is exactly n + 1/2 when the estimate jumps by P_t/2 steps (pi/4), and fp32 /
+    # fp64 rounding of the exact tie picks either quadrant: the rest of the segment then sits a
+    # quarter turn apart (the labels differ there; R_s anchors only at the segment start)
+    raw = np.median(np.angle(zg[:nb * B] * np.conj(zo[:nb * B])).reshape(nb, B), axis=1)
+    quarter = np.abs(np.abs(raw) - np.pi / 2) < 0.3 * step
+    flip |= quarter
     seg = (np.arange(nb) * B) // rx["lms_segment"]
     blocks = np.nonzero(flip)[0]
     first = blocks[np.r_[True, seg[blocks][1:] != seg[blocks][:-1]]] if blocks.size else blocks
     if first.size:
-        ratio = np.abs(med[first]) / step
+        ratio = np.where(quarter[first], 0.0, np.abs(med[first]) / step)
         assert np.all(ratio < 1.35), ratio
+        if np.any(quarter[first]):
+            print(f"CPR unwrap ties (quarter turn from this block on): {int(np.sum(quarter[first]))}")
     return first * B
 
 
-def _compare_labels(rec, rx, out, labels, R=None, strict=True):
-    """(1) bit-exact outside the excluded set (near-boundary decisions, BPS near-tie blocks, and
-    what follows them in the same segment); (2) at most 1e-3 of all labels differ; (3) every
-    differing label's oracle soft value lies within 0.05 of a decision boundary, or in a BPS
-    near-tie block. The excluded fraction is a property of the format and SNR (dense for PAM-16),
-    so it is reported, not bounded."""
+def _contaminated_epochs(start, m_end, rx):
+    """Epochs whose lag-D seeds descend from a segment where the GPU and oracle trajectories
+    parted (a flipped decision changes that segment's final taps, hence the mean canonical taps
+    that seed epoch e + D, e + 2D, ...): the equaliser output there differs at the seed level, so
+    it is not compared element-wise (labels still are)."""
+    E = rx.get("buffer_blocks", 8192) * (256 if rx.get("_fmt") == "pam" else 128)
+    D = rx.get("tap_lag_epochs", 8)
+    ne = -(-m_end // E)
+    hit = np.zeros(ne, bool)
+    if np.any(start):
+        hit[np.unique(np.nonzero(start)[0] // E)] = True
+    cont = np.zeros(ne, bool)
+    for e in range(D, ne):
+        cont[e] = hit[e - D] or cont[e - D]
+    return cont, E
+
+
+def _compare_labels(rec, rx, out, labels, R=None, strict=True, max_excl=0.02):
+    """GPU vs oracle decisions and equaliser output (SURVEY §8(c) 'GPU-vs-oracle parity').
+
+    A GPU and an oracle trajectory can part only where a decision actually differs: at a symbol
+    whose oracle soft value lies within DELTA = 1e-3 of a decision boundary AND whose labels
+    differ, or in a BPS near-tie block. From such a point to the end of its segment the symbols
+    are excluded (segments restart from common seeds). Asserted:
+      (1) every other label is bit-exact;
+      (2) at most 1e-3 of all labels differ;
+      (3) the excluded fraction is <= max_excl (reported);
+      (4) the equaliser output z' (probe Y) equals the oracle's z element-wise, relative L2
+          <= 1e-4, on every non-excluded symbol of the epochs whose seeds are not descended
+          from an excluded segment (when the rings still hold the record)."""
     m_end = out["m_end"]
     lab_o = out["labels"][:m_end].astype(np.int64)
     lab_g = labels[:m_end].astype(np.int64)
@@ -80,27 +113,37 @@ def _compare_labels(rec, rx, out, labels, R=None, strict=True):
     near = near_threshold(soft, rec.fmt, rec.M, DELTA)
     S = rx["lms_segment"]
     seg = np.arange(m_end) // S
-    excl = np.zeros(m_end, bool)
+    mism = lab_o != lab_g
     flips = _bps_flip_blocks(R, rx, out, m_end)
-    start = near.copy()
+    start = near & mism
     start[flips] = True
+    excl = np.zeros(m_end, bool)
     for s in np.unique(seg[start]):
         first = np.argmax(start & (seg == s))
         excl[first:(s + 1) * S] = True
-    mism = lab_o != lab_g
     bad = mism & ~excl
-    assert not np.any(bad), f"{int(bad.sum())} label mismatches away from thresholds, first at {np.argmax(bad)}"
+    assert not np.any(bad), f"{int(bad.sum())} label mismatches not preceded in their segment by a " \
+                            f"near-boundary flip, first at {np.argmax(bad)}"
     assert mism.sum() <= 1e-3 * m_end, f"{int(mism.sum())} of {m_end} labels differ"
-    loose = near_threshold(soft, rec.fmt, rec.M, 0.05)
-    in_flip = np.zeros(m_end, bool)
-    for f in flips:
-        in_flip[f:(f // S + 1) * S] = True
+    frac = float(excl.mean())
+    print(f"labels: {int(mism.sum())} differ, {int(np.sum(near & mism))} near-boundary flips, "
+          f"BPS near-tie blocks {len(flips)}, excluded fraction {frac:.5f}")
     if strict:
-        assert np.all((loose | in_flip)[mism]), f"{int(np.sum(mism & ~loose & ~in_flip))} mismatches far from a boundary"
-    # full record sizes (strict=False): after a near-tie the fp32 and fp64 trajectories of a
-    # segment, and through the lag-D seeds those of later epochs, may drift apart (DD-mode
-    # trajectories are parity unpinned); (1) and (2) still hold
-    print(f"labels: {int(mism.sum())} differ, excluded fraction {excl.mean():.4f}, BPS near-tie blocks {len(flips)}")
+        assert frac <= max_excl, f"excluded fraction {frac:.4f} > {max_excl}"
+    y_err = None
+    if R is not None:
+        try:
+            Y = R.probe("Y", 0, m_end)
+        except Exception:                       # streaming rings no longer hold the record
+            Y = None
+        if Y is not None:
+            cont, E = _contaminated_epochs(start, m_end, dict(rx, _fmt=rec.fmt))
+            ok = ~excl & ~cont[np.arange(m_end) // E]
+            yg = Y if rec.fmt == "qam" else Y.real
+            y_err = rel_l2(yg[ok], soft[ok])
+            print(f"equaliser output: rel-L2 {y_err:.2e} over {ok.mean():.4f} of the symbols")
+            assert ok.mean() >= 0.5
+            assert y_err <= TOL_FIELD, y_err
     return mism, excl
 
 
@@ -198,9 +241,41 @@ def test_multi_buffer_parity(name, n, extra, batch, call_bufs):
     assert st["sync_offset"] == out["sync"]["offset"]
     if rec.fmt == "qam":
         assert st["sync_phase"] == out["sync"]["phase"]
-    assert rel_l2(R.train_taps(), out["lms"]["w_train"]) < 1e-3
+    assert rel_l2(R.train_taps(), out["lms"]["w_train"]) < TOL_FIELD
     mism, excl = _compare_labels(rec, rx, out, labels, R)
     _compare_counters(rec, out, st, mism)
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4"])
+def test_data_aided_equaliser_output_parity(name):
+    """SURVEY §8(c) parity criterion 'equaliser output in training mode (no decision feedback):
+    relative L2 over the record <= 1e-4' (rx_config.lms_mode = 1, DESIGN reading R-DA): every
+    segment adapts on the reference like the training pass, so no GPU decision feeds back and the
+    GPU equaliser output z' must equal the oracle's element by element over the whole record
+    (all segments, all epochs, the lag-D seeds included); labels are bit-exact except the
+    near-boundary symbols themselves (no contamination without feedback)."""
+    _torch_cuda()
+    rec, rx = make_config(name, n_samples=1 << 21)
+    rx.update(buffer_blocks=256, lms_mode=1)
+    out = run_oracle(rec, rx)
+    R, labels, st = run_gpu(rec, rx, chunk=256 * 512)
+    assert st["sync_offset"] == out["sync"]["offset"]
+    assert rel_l2(R.train_taps(), out["lms"]["w_train"]) < TOL_FIELD
+    m_end = out["m_end"]
+    Y = R.probe("Y", 0, m_end)
+    z = out["lms"]["z"][:m_end]
+    err = rel_l2(Y if rec.fmt == "qam" else Y.real, z)
+    near = near_threshold(z, rec.fmt, rec.M, DELTA)
+    mism = out["labels"][:m_end] != labels[:m_end]
+    print(f"{name} data aided: z' rel-L2 {err:.2e} over {m_end} symbols; {int(mism.sum())} labels differ "
+          f"({int(near.sum())} near a boundary); BER {st['bit_errors']}/{st['bits']}")
+    assert err <= TOL_FIELD
+    assert not np.any(mism & ~near)
+    _compare_counters(rec, out, st, mism)
+    # per-segment relative L2 as well: no segment may hide behind the record average
+    S = rx["lms_segment"]
+    for s0 in range(0, m_end - S, S):
+        assert rel_l2((Y if rec.fmt == "qam" else Y.real)[s0:s0 + S], z[s0:s0 + S]) <= TOL_FIELD, s0
 
 
 def test_chunking_invariance():
@@ -253,7 +328,7 @@ def test_set_taps_warm_start():
                       "dc_offset": rec.dc_offset, "w_init": w0})
     out = O.receive_pam(rec.codes, p)
     R, labels, st = run_gpu(rec, rx, pre=lambda R: R.set_taps(w0))
-    assert rel_l2(R.train_taps(), out["lms"]["w_train"]) < 1e-3
+    assert rel_l2(R.train_taps(), out["lms"]["w_train"]) < TOL_FIELD
     mism, excl = _compare_labels(rec, rx, out, labels, R)
     with pytest.raises(RxError):
         R.set_taps(w0)
@@ -269,7 +344,7 @@ def test_c5_formats_parity(ch):
     out = run_oracle(rec, rx)
     R, labels, st = run_gpu(rec, rx, chunk=256 * 512)
     assert st["sync_offset"] == out["sync"]["offset"]
-    assert rel_l2(R.train_taps(), out["lms"]["w_train"]) < 1e-3
+    assert rel_l2(R.train_taps(), out["lms"]["w_train"]) < TOL_FIELD
     mism, excl = _compare_labels(rec, rx, out, labels, R)
     _compare_counters(rec, out, st, mism)
 
@@ -319,8 +394,8 @@ def test_widely_linear_iq_imbalance_parity(K):
     R, labels, st = run_gpu(rec, rx, chunk=256 * 512)
     assert st["sync_offset"] == out["sync"]["offset"]
     w, v = R.train_taps()
-    assert rel_l2(w, out["lms"]["w_train"]) < 1e-3
-    assert rel_l2(v, out["lms"]["v_train"]) < 1e-3
+    assert rel_l2(w, out["lms"]["w_train"]) < TOL_FIELD
+    assert rel_l2(v, out["lms"]["v_train"]) < TOL_FIELD
     assert np.linalg.norm(v) > 0.05                          # the image branch is in use
     mism, excl = _compare_labels(rec, rx, out, labels, R)
     _compare_counters(rec, out, st, mism)
@@ -398,7 +473,7 @@ def test_full_size_c2_in_bench_launch_configuration():
     out = run_oracle(rec, rx)
     R, labels, st = run_gpu(rec, rx, chunk=BENCH_CHUNK, history_buffers=6)
     assert st["sync_offset"] == out["sync"]["offset"]
-    assert rel_l2(R.train_taps(), out["lms"]["w_train"]) < 1e-3
+    assert rel_l2(R.train_taps(), out["lms"]["w_train"]) < TOL_FIELD
     m_end = out["u"].shape[0]
     lo = m_end - (1 << 20)
     assert rel_l2(R.probe("U", lo, m_end - lo), out["u"][lo:]) < TOL_FIELD
@@ -612,7 +687,7 @@ def test_degenerate_equaliser_configs(name, over):
     out = run_oracle(rec, rx)
     R, labels, st = run_gpu(rec, rx, chunk=256 * 512)
     assert st["sync_offset"] == out["sync"]["offset"]
-    assert rel_l2(R.train_taps(), out["lms"]["w_train"]) < 1e-3
+    assert rel_l2(R.train_taps(), out["lms"]["w_train"]) < TOL_FIELD
     mism, excl = _compare_labels(rec, rx, out, labels, R)
     _compare_counters(rec, out, st, mism)
 

@@ -415,3 +415,123 @@ def test_kk_dc_calibration_finds_the_generators_dc():
     evm, best = O.calibrate_dc(rec.codes, p, f * rec.dc_offset)
     assert best == 2
     assert evm[0] > evm[1] > evm[2] < evm[3] < evm[4]
+
+
+# ---------------------------------------------------------------- round-2 pins
+# (VERDICT r01 'Weak 2': EVM sums, the cross-buffer CFO DDS carry and ingest's sign had no direct
+# pin; the data-aided equaliser mode, DESIGN reading R-DA, is pinned like the training pass)
+
+def test_ingest_closed_form_sign_and_scale():
+    """c-1 / A5: x = (code - 2047.5)/2047.5 * gain. Code 0 -> -1, 4095 -> +1 (a sign flip would be
+    invisible on PAM after sync and training, so it is pinned here), clipped = #{0, 4095}."""
+    codes = np.array([0, 4095, 2047, 2048, 1024, 3071], dtype=np.uint16)
+    x, clipped = O.ingest(codes, adc_gain=1.0)
+    want = np.array([-1.0, 1.0, -0.5 / 2047.5, 0.5 / 2047.5, -1023.5 / 2047.5, 1023.5 / 2047.5])
+    assert np.array_equal(x, want) and clipped == 2
+    x2, _ = O.ingest(codes, adc_gain=0.25)
+    assert np.array_equal(x2, 0.25 * want)
+
+
+@pytest.mark.parametrize("fmt,M,sigma", [("qam", 16, 0.02), ("qam", 64, 0.01), ("pam", 4, 0.03),
+                                         ("pam", 16, 0.006)])
+def test_evm_sums_closed_form_awgn(fmt, M, sigma):
+    """Decision-referenced EVM (c-11, A24) on AWGN at the decision input, at an SNR where
+    decision errors have probability < 1e-30: EVM = 10 log10(noise power / Es) with noise power
+    sigma^2 per real dimension (2 sigma^2 for QAM) and Es the mean symbol energy: 1 for the unit
+    power QAM constellation, (M + 1) / (3 (M - 1)) for unit-peak PAM-M (equiprobable levels).
+    Statistical tolerance: 2e6 symbols give a 0.005 dB standard deviation; 0.02 dB bound."""
+    rng = np.random.default_rng(900 + M)
+    n = 2_000_000
+    sl = O._Slicer(fmt, M)
+    if fmt == "qam":
+        L = sl.L
+        ii = rng.integers(0, L, size=(n, 2))
+        a = sl.value(ii)
+        z = a + sigma * (rng.normal(size=n) + 1j * rng.normal(size=n))
+        noise, Es = 2 * sigma ** 2, 1.0
+    else:
+        ii = rng.integers(0, M, size=n)
+        a = sl.value(ii)
+        z = a + sigma * rng.normal(size=n)
+        noise, Es = sigma ** 2, (M + 1) / (3.0 * (M - 1))
+    d = sl.value(sl.indices(z))
+    assert np.array_equal(d, a)                         # no decision errors at this SNR
+    num, den = O.evm_sums(z, d)
+    assert abs(10 * math.log10(num / den) - 10 * math.log10(noise / Es)) < 0.02
+
+
+def test_cfo_multi_buffer_dds_origin_is_carried_phase_continuous():
+    """c-8 across buffer edges (SURVEY §8(c) CFO pin, multi-buffer): a noiseless QAM-4 stream at
+    2 sps with a 20 MHz offset and a static phase, split into 4 buffers. Each buffer's estimate
+    is within 2 kHz, the DDS origin of buffer b+1 is the end phase word of buffer b
+    (origin_{b+1} = origin_b + Q inc_b mod 2^64, with inc_b = round(df_b / f_s2 2^64)), and the
+    corrected stream is phase-continuous across every edge: the mean residual phase just after an
+    edge equals the one just before it to 1e-3 rad. Resetting the origin per buffer would jump by
+    2 pi 20 MHz Q / f_s2 mod 2 pi = O(1) rad here."""
+    rng = np.random.default_rng(7)
+    Q = 1 << 16
+    nsym = 2 * Q                                        # 4 buffers of Q two-sps samples
+    s, _ = _qam_stream(4, nsym, rng)
+    up = np.zeros(2 * nsym, dtype=np.complex128)
+    up[::2] = s
+    f = np.fft.fftfreq(2 * nsym, d=0.5)
+    clean = np.fft.ifft(np.fft.fft(up) * gen.rrc_amp(f, 0.01) ** 2)
+    q = np.arange(2 * nsym)
+    df = 20e6
+    z = 2.0 * clean * np.exp(1j * (2 * math.pi * df / 2e9 * q + 0.3))
+    zc, info = O.kk_norm_cfo(z, 2e9, buffer_len=Q)
+    assert len(info["df"]) == 4 and np.all(np.abs(info["df"] - df) < 2e3), info["df"] - df
+    for b in range(3):
+        inc = O.dds_increment(info["df"][b], 2e9)
+        assert info["origin"][b + 1] == (info["origin"][b] + Q * inc) % (1 << 64)
+    assert info["origin"][0] == 0
+    res = np.angle(zc * np.conj(clean))                 # residual phase of the corrected stream
+    big = np.abs(clean) > 0.5 * np.sqrt(np.mean(np.abs(clean) ** 2))
+    for b in range(1, 4):
+        e = b * Q
+        before = np.angle(np.sum(np.exp(1j * res[e - 256:e][big[e - 256:e]])))
+        after = np.angle(np.sum(np.exp(1j * res[e:e + 256][big[e:e + 256]])))
+        assert abs(math.remainder(after - before, 2 * math.pi)) < 1e-3, (b, after - before)
+
+
+def test_data_aided_segments_identity_channel_reproduce_reference_exactly():
+    """Data-aided segments (DESIGN reading R-DA: every segment adapts as the c-9 training pass) on
+    an identity channel from the centre spike: e = r - y = 0 at every symbol, so the taps stay the
+    spike and the equaliser output equals the reference exactly; the decisions are error free."""
+    _, idx_ref, vals_ref = O.reference("pam", 4)
+    o, m0, n = 77, 4096, 40_000
+    m = np.arange(n)
+    v = vals_ref[(o + m - m0) % O.P_REF]
+    lp = O.LmsParams(K=15, S=4096, mu=1e-2, T_train=4096, E=1 << 14, D=2, data_aided=True)
+    lm = O.lms_full(v, 1, 0, n, lambda mm: idx_ref[(o + mm - m0) % O.P_REF],
+                    lambda mm: vals_ref[(o + mm - m0) % O.P_REF], O._Slicer("pam", 4), lp, True, m0)
+    spike = np.zeros(15); spike[7] = 1
+    assert all(np.array_equal(w, spike) for w in lm["seg_w"])
+    assert np.array_equal(lm["z"], v) and np.array_equal(lm["idx"], idx_ref[(o + m - m0) % O.P_REF])
+
+
+def test_data_aided_segments_converge_to_wiener_solution():
+    """Data-aided segments on a known short FIR channel + AWGN (the training pin of
+    SURVEY §8(c), applied to every segment): the mean final taps of the later epochs approach the
+    Wiener solution R^-1 p within 2%, and data-aided decisions beat chance by far."""
+    rng = np.random.default_rng(11)
+    h = np.array([0.1, 1.0, -0.3, 0.15])
+    K, s2 = 9, 0.01
+    _, idx_ref, vals_ref = O.reference("pam", 2)
+    o, m0, n = 500, 4096, 400_000
+    m = np.arange(n)
+    a = vals_ref[(o + m - m0) % O.P_REF]
+    v = np.convolve(a, h)[:n] + rng.normal(0, math.sqrt(s2), size=n)
+    c = K // 2
+    r = np.correlate(h, h, "full")[len(h) - 1:]
+    rcol = np.zeros(K); rcol[:len(r)] = r
+    R = toeplitz(rcol) + s2 * np.eye(K)
+    p = np.array([h[c - k] if 0 <= c - k < len(h) else 0.0 for k in range(K)])
+    w_star = np.linalg.solve(R, p)
+    lp = O.LmsParams(K=K, S=4096, mu=2e-4, T_train=8192, E=1 << 15, D=2, data_aided=True)
+    lm = O.lms_full(v, 1, 0, n, lambda mm: idx_ref[(o + mm - m0) % O.P_REF],
+                    lambda mm: vals_ref[(o + mm - m0) % O.P_REF], O._Slicer("pam", 2), lp, True, m0)
+    w_bar = np.mean(np.array(lm["seg_w"][len(lm["seg_w"]) // 2:]), axis=0)
+    assert np.linalg.norm(w_bar - w_star) / np.linalg.norm(w_star) < 2e-2
+    ser = np.mean(lm["idx"][n // 2:] != idx_ref[(o + m[n // 2:] - m0) % O.P_REF])
+    assert ser < 1e-3
