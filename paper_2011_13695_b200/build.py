@@ -29,7 +29,24 @@ def needs_build() -> bool:
     return any(os.path.getmtime(os.path.join(HERE, p)) > t for p in DEPS)
 
 
+PEAK_SO = os.path.join(HERE, "libfp32peak.so")
+
+
+def build_peak(force: bool = False) -> str:
+    """bench.py's FP32 FFMA peak probe (csrc/fp32_peak.cu), a separate library: not part of
+    the receiver ABI."""
+    src = os.path.join(HERE, "csrc", "fp32_peak.cu")
+    if not force and os.path.exists(PEAK_SO) and os.path.getmtime(PEAK_SO) > os.path.getmtime(src):
+        return PEAK_SO
+    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-shared",
+                    "-Xcompiler", "-fPIC", "-o", PEAK_SO + ".tmp", src], check=True, cwd=HERE)
+    os.replace(PEAK_SO + ".tmp", PEAK_SO)
+    return PEAK_SO
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    build_peak(force)
     if not force and not needs_build():
         return SO
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

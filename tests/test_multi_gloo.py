@@ -81,3 +81,34 @@ def test_summary_q_from_ber():
     assert abs(s["q_db"] - 8.4) < 2e-3          # HD-FEC threshold
     assert abs(s["evm_db"] + 20.0) < 1e-12
     assert math.isinf(multi.q_db_from_ber(0.0))
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_gloo_on_one_gpu():
+    """`python bench.py --gpus 2 --backend gloo` launches two ranks itself (torch.distributed.run,
+    127.0.0.1), both on the one visible GPU: gpu_main and c5_run run with world = 2, the counters
+    are all-reduced every step and the line reports n_gpus = 2 with 16 C5 channels and the
+    max-over-ranks timing (VERDICT r01 'Next 2'). Records are shrunk 4x (--record-scale) so the
+    run takes about a minute; 4 buffers per step let the equaliser rounds finalise symbols
+    inside the timed region."""
+    import json
+    import subprocess
+    import sys
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--backend", "gloo",
+                          "--steps", "3", "--warmup", "3", "--c5-steps", "2", "--ring-gib", "0.25",
+                          "--record-scale", "4", "--no-cpu"], cwd=root, env=env, capture_output=True, text=True,
+                         timeout=1200)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0
+    assert line["c5"]["channels"] == 16
+    q = line["quality_all_ranks"]
+    assert q["bits"] > 0 and q["ber"] < 0.01
+    # both ranks ran the same record in lockstep: the all-reduced bit count is 2 x one channel's
+    assert q["bits"] % 2 == 0
+    assert all(v["bits"] > 0 for v in line["c5"]["quality_all_ranks_by_format"].values())
