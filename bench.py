@@ -753,14 +753,20 @@ def gpu_main(args):
     R4.close()
     if n1:
         # the paper's hand-off granularity: one 2^22 buffer per rx_process call
-        R1 = make_kk(history_buffers=3)
-        r1 = run_mode(torch, None, R1, ring4, n4, max(3, args.steps // 2), 3, 1, dev, chunk=BUFFER, with_profile=False)
-        R1.close()
-        v1 = n4 * max(3, args.steps // 2) / (r1["ms"] / 1e3) / 1e9
-        line["per_buffer_call"] = {"value": round(v1, 3), "unit": "GSa/s", "call_samples": BUFFER,
-                                   "ms_per_buffer": round(r1["ms"] / max(3, args.steps // 2) / (n4 // BUFFER), 4),
-                                   "realtime_ratio": round(v1 / PAPER_REALTIME_GSA, 2),
-                                   "host_enqueue_ms_per_buffer": round(r1["host_ms"] / (n4 // BUFFER), 4)}
+        # (equaliser_lag = 1: a call's equaliser rounds overlap the next call's front-end, the
+        # paper's cross-buffer stream overlap; lag 0 = every call joins its own rounds)
+        pb = {}
+        for lag in (1, 0):
+            R1 = make_kk(history_buffers=3, equaliser_lag=lag)
+            ks = max(3, args.steps // 2)
+            r1 = run_mode(torch, None, R1, ring4, n4, ks, 3, 1, dev, chunk=BUFFER, with_profile=False)
+            R1.close()
+            v1 = n4 * ks / (r1["ms"] / 1e3) / 1e9
+            pb[lag] = {"value": round(v1, 3), "ms_per_buffer": round(r1["ms"] / ks / (n4 // BUFFER), 4),
+                       "host_enqueue_ms_per_buffer": round(r1["host_ms"] / (n4 // BUFFER), 4)}
+        line["per_buffer_call"] = dict(pb[1], unit="GSa/s", call_samples=BUFFER, equaliser_lag=1,
+                                       realtime_ratio=round(pb[1]["value"] / PAPER_REALTIME_GSA, 2),
+                                       equaliser_lag_0=pb[0])
         # quadrant modes on one flushed record: anchored (default) and the c-9 stitch chain
         qa = record_quality(torch, make_kk, rec4, dev)
         qc = record_quality(torch, lambda **kw: make_kk(cpr_anchor=0, **kw), rec4, dev)

@@ -127,6 +127,20 @@ typedef struct {
                                  'equaliser output in training mode'); a BER tester's reference-
                                  aided mode. Seeds: epoch means of the raw final taps (no R-SEED
                                  phase normalisation: no CPR, the frame is absolute) */
+  int equaliser_lag;          /* side-stream equaliser (serial_equaliser = 0) only. 0 (default): the
+                                 work an rx_process call enqueues on cuda_stream ends with its own
+                                 equaliser stage; 1: with the PREVIOUS call's, so a call's equaliser
+                                 rounds overlap the next call's front-end (the paper overlaps buffers
+                                 across its five streams) - for small (one-buffer)
+                                 calls. Labels of a call may then be written after its stream work
+                                 completes: d_labels must stay valid until the next rx_process,
+                                 rx_flush, rx_get_stats or rx_export_counters call on the handle has
+                                 been ordered behind it (those calls wait for every forked stage) */
+  int shard_count;            /* time sharding of ONE stream (SURVEY §8(e) mode 2; KK chain): 0 or 1
+                                 = off (rx_process); N > 1 = this handle is shard shard_index of N,
+                                 fed with rx_shard_process (see below). Requires family KK,
+                                 cpr_anchor = 1 and N <= tap_lag_epochs */
+  int shard_index;
 } rx_config;
 
 /* Sample formats accepted by rx_process:
@@ -294,6 +308,36 @@ typedef enum {
 } rx_kernel_class;
 rx_status rx_profile_enable(rx_handle *h, int mask);
 rx_status rx_profile_read(rx_handle *h, double *host_ms, long long *host_counts, int n);
+
+/* ---- Time-block sharding of one stream over GPUs (SURVEY §8(e) mode 2, KK chain) -------------
+ * The paper chains its buffers with ordered carries (the overlap kernel; the clock phase of
+ * the previous buffer). In the KK chain the quantities that cross a buffer boundary are
+ * the overlap-save halos (recomputed from input halos), the CFO DDS phase origin (a prefix over all
+ * earlier buffers' estimates, c-8), the frame-sync result and trained taps from the stream start,
+ * the lag-D seeds (c-9) and z' of the neighbour buffers for the LMS windows at the edges. Paper
+ * buffer b = input samples [b B4, (b+1) B4), B4 = 512 buffer_blocks; with shard_count = N, shard g
+ * owns the buffers b = g mod N. Round r (buffers r N .. r N + N - 1):
+ *  1. rx_shard_process(h, b = r N + g, ...): input samples [max(0, b B4 - RX_SHARD_PRE),
+ *     (b+1) B4 + RX_SHARD_POST) (shorter only on the call holding the stream end, last = 1),
+ *     device u16 codes; KK stage 1 / 2 over the blocks whose frames lie inside, CFO estimate of b.
+ *     d_labels: where the labels of b's symbols go (absolute symbol m at m % labels_capacity).
+ *  2. rx_export_carry(h, d_rec): this round's record (rx_carry_size bytes, 16-byte aligned device
+ *     memory); the caller all-gathers the N records in rank order into one device buffer (NCCL
+ *     all-gather; no host staging).
+ *  3. rx_import_carry(h, d_all, N, g): rebuild the DDS origin chain, take sync / trained taps /
+ *     seeds, then the equaliser, decisions, labels and counters of the shard's buffer of round
+ *     r - 1 (its last segment needs z' of the next buffer, whose CFO estimate arrives now).
+ * After the round holding the stream end, one more export / gather / import without
+ * rx_shard_process finishes every pending buffer. Labels are bit-identical and integer counters
+ * (summed over shards) equal to one handle's on the same stream. All calls are stream-ordered and
+ * asynchronous; errors: RX_EINVAL (arguments, not a shard handle), RX_ESTATE (call order). */
+#define RX_SHARD_PRE 4096
+#define RX_SHARD_POST 4096
+rx_status rx_shard_process(rx_handle *h, long long buffer, const void *d_samples, long long n_samples,
+                           int last, unsigned char *d_labels, long long labels_capacity, void *cuda_stream);
+rx_status rx_carry_size(const rx_handle *h, int *bytes);
+rx_status rx_export_carry(rx_handle *h, void *d_buf, void *cuda_stream);
+rx_status rx_import_carry(rx_handle *h, const void *d_gathered, int n_ranks, int my_rank, void *cuda_stream);
 
 void rx_destroy(rx_handle *h);
 const char *rx_strerror(int status);

@@ -53,6 +53,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
            "-shared", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include"),
            f"-DRX_GIT=\"{_git_rev()}\"", "-o", SO + ".tmp"] + [os.path.join(HERE, s) for s in SOURCES]
+    cmd[1:1] = os.environ.get("RX_NVCC_FLAGS", "").split()     # experiments (e.g. -DLMS_SPC=2)
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)

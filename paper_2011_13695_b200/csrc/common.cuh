@@ -62,6 +62,9 @@ struct InView {
   long long keep_from;      // samples p >= keep_from of this call are kept in the history ring
   int f32;                  // input format RX_IN_F32
   float gain;               // adc_gain (f32 input)
+  long long cnt_lo, cnt_hi; // blocks whose owned samples are counted (clipped / domain); a
+                            // time shard counts only its own buffer's blocks (its halos belong
+                            // to its neighbours)
 };
 __device__ __forceinline__ int in_code(const InView &v, long long p, bool &pad) {
   pad = p < 0;

@@ -50,6 +50,11 @@ __global__ void __launch_bounds__(256) k_kk_s1(RxDev d, InView in, long long b0,
 #pragma unroll
     for (int r = 0; r < 4; ++r) amp[r][0] = amp[r][1] = 0.f;
   }
+  if (b < in.cnt_lo || b >= in.cnt_hi) {   // a time shard's halo block: counted by its owner
+    clip = 0;
+    dom = 0;
+    first_dom = 0x7fffffffffffffffLL;
+  }
   block_reduce_clip(d.st, clip);
   dom = __reduce_add_sync(0xffffffffu, dom);
   if ((threadIdx.x & 31) == 0 && dom) atomicAdd((unsigned long long *)&d.st->domain_errors, (unsigned long long)dom);
@@ -163,15 +168,15 @@ __global__ void __launch_bounds__(256) k_kk_s2(RxDev d, long long b0, long long 
 // ------------------------------------------------------------------ H19-H20
 // Per-buffer power normalisation and coarse + fine CFO (c-8, reading R-CFO), batched over the
 // buffers that complete in one call (blockIdx.y = buffer of the call):
-//  k_cfo_spec   16 chunks of 1024 per CTA (one per 64-thread group): |DFT_1024(z^4)|^2 summed
-//               over the CTA's chunks in fixed group order -> one partial row; power partials
+//  k_cfo_spec   CFO_ROWS CTAs per buffer, 4 chunks of 1024 per CTA step (one per 64-thread
+//               group): |DFT_1024(z^4)|^2 summed over the CTA's chunks in a fixed order -> one
+//               partial row; power partials
 //  (final)      the last k_cfo_spec CTA of each buffer: rows -> S[k] (fixed order), P, k* (lowest on ties), delta,
 //               coarse df and its DDS increment
 //  k_cfo_fine   one warp per chunk: a_i = sum (z e^{-j psi_c})^4; the last CTA of a buffer forms
 //               rho = sum a_{i+1} conj(a_i) in index order -> fine df
 //  k_cfo_carry  one thread: DDS increments and phase origins carried across buffers
-//  k_kk_zprime  z' = z / sqrt(P) e^{-j psi'} over the call's buffers
-#define CFO_GROUPS 16
+//  zp_value     z' = z / sqrt(P) e^{-j psi'}, evaluated where the equaliser stages read it
 __device__ __forceinline__ void buf_range(const RxDev &d, long long beta, long long qfront,
                                           long long &qlo, long long &qhi) {
   const long long Q = (long long)d.buffer_blocks * 256;
@@ -181,33 +186,40 @@ __device__ __forceinline__ void buf_range(const RxDev &d, long long beta, long l
 
 // Per-buffer periodogram argmax + log-parabolic interpolation + power (c-8): the CTA that finishes
 // a buffer's spectrum rows (last-CTA ticket in k_cfo_spec) reduces them in fixed row order
+// (CFO_SPEC_T threads, each owning the bins k = t + CFO_SPEC_T i)
+#define CFO_SPEC_T 256
+#define CFO_ROWS 128           // spectrum rows (CTAs) per buffer
+#define CFO_KPT (1024 / CFO_SPEC_T)
 __device__ __forceinline__ void cfo_final_block(const RxDev &d, long long beta, long long qfront, long long rb, int nrows) {
   __shared__ double Sd[1024];
-  __shared__ double wv[32];
-  __shared__ int wi[32];
-  __shared__ double pws[32];
+  __shared__ double wv[CFO_SPEC_T / 32];
+  __shared__ int wi[CFO_SPEC_T / 32];
+  __shared__ double pws[CFO_SPEC_T / 32];
   const int t = threadIdx.x;
   long long qlo, qhi;
   buf_range(d, beta, qfront, qlo, qhi);
-  double s = 0.0;
-  {
+  double bv = -1.0;
+  int bi = 0x7fffffff;
+#pragma unroll
+  for (int i = 0; i < CFO_KPT; ++i) {
+    const int k = t + CFO_SPEC_T * i;
+    double sk = 0.0;
     int r = 0;
-    for (; r + 32 <= nrows; r += 32) {        // 32 independent loads in flight, summed in order
-      float v[32];
+    for (; r + 16 <= nrows; r += 16) {        // 16 independent loads in flight, summed in row order
+      float v[16];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = __ldcg(d.cfo_part + (rb + r + i) * 1024 + t);
+      for (int u = 0; u < 16; ++u) v[u] = __ldcg(d.cfo_part + (rb + r + u) * 1024 + k);
 #pragma unroll
-      for (int i = 0; i < 32; ++i) s += (double)v[i];
+      for (int u = 0; u < 16; ++u) sk += (double)v[u];
     }
-    for (; r < nrows; ++r) s += (double)__ldcg(d.cfo_part + (rb + r) * 1024 + t);
+    for (; r < nrows; ++r) sk += (double)__ldcg(d.cfo_part + (rb + r) * 1024 + k);
+    Sd[k] = sk;
+    if (sk > bv) { bv = sk; bi = k; }         // k increasing: strict > keeps the lowest on ties
   }
-  Sd[t] = s;
   double pw = 0.0;
   for (int r = t; r < nrows; r += blockDim.x) pw += __ldcg(d.cfo_pow + rb + r);
   pw = warp_sum_d(pw);
   if ((t & 31) == 0) pws[t >> 5] = pw;
-  double bv = s;
-  int bi = t;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
@@ -218,13 +230,13 @@ __device__ __forceinline__ void cfo_final_block(const RxDev &d, long long beta, 
   __syncthreads();
   if (t == 0) {
     double P = 0.0;
-    for (int w = 0; w < 32; ++w) P += pws[w];
+    for (int w = 0; w < CFO_SPEC_T / 32; ++w) P += pws[w];
     const long long n = qhi - qlo;
     P = n > 0 ? P / (double)n : 1.0;
     if (!(P > 0.0)) P = 1.0;
     double best = wv[0];
     int k = wi[0];
-    for (int w = 1; w < 32; ++w)
+    for (int w = 1; w < CFO_SPEC_T / 32; ++w)
       if (wv[w] > best || (wv[w] == best && wi[w] < k)) { best = wv[w]; k = wi[w]; }
     const long long nch = n / 1024;
     double df = 0.0;
@@ -248,63 +260,70 @@ __device__ __forceinline__ void cfo_final_block(const RxDev &d, long long beta, 
   }
 }
 
-__global__ void __launch_bounds__(1024) k_cfo_spec(RxDev d, long long beta0, long long qfront) {
-  extern __shared__ float2 sm[];
-  float2 *tw = sm;
-  float2 *bufs = sm + 1024;                    // [CFO_GROUPS][FFT_PAD_N]; later acc[CFO_GROUPS][1024]
-  __shared__ double red[32];
+// |DFT_1024(z^4)|^2 periodogram rows + power partials. Grid (CFO_ROWS, buffers of the call),
+// CFO_SPEC_T threads = 4 groups of 64, one FFT-1024 (2 x FFT-512 + radix-2) per group at a time:
+// CTA x takes chunks c = 4 (x + CFO_ROWS it) + g, it = 0, 1, ... (4 consecutive chunks per CTA
+// step, every CTA resident in one wave), accumulates |X[k]|^2 of its chunks per thread in
+// registers (chunk order), then sums the 4 groups in fixed order into row x. The power partial
+// sums the same samples (plus, in CTA 0, the tail beyond the last complete chunk).
+__global__ void __launch_bounds__(CFO_SPEC_T, 4) k_cfo_spec(RxDev d, long long beta0, long long qfront) {
+  __shared__ float2 tw[1024];
+  __shared__ float2 bufs[CFO_SPEC_T / 64][FFT_PAD_N];   // FFT scratch; later acc[4][1024] floats
+  __shared__ double red[CFO_SPEC_T / 32];
   const int g = threadIdx.x >> 6, j = threadIdx.x & 63;
   long long qlo, qhi;
   buf_range(d, beta0 + blockIdx.y, qfront, qlo, qhi);
   for (int i = threadIdx.x; i < 1024; i += blockDim.x) tw[i] = d.tw[i];
-  __syncthreads();   // twiddles visible to every group (the FFT barriers are per group)
+  __syncthreads();
   const long long nch = (qhi - qlo) / 1024;
-  const long long c = (long long)blockIdx.x * CFO_GROUPS + g;
-  const bool act = c < nch;
-  float2 *bg = bufs + g * FFT_PAD_N;
-  float2 ve[8], vo[8];
-  float4 zz[8];
+  constexpr int NG = CFO_SPEC_T / 64;
+  float acc[16];
 #pragma unroll
-  for (int r = 0; r < 8; ++r) {
-    zz[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (act) zz[r] = *reinterpret_cast<const float4 *>(d.z + rmod(qlo + 1024 * c + 2 * (j + 64 * r), d.z_cap));
-  }
-  // power partial: the chunk samples this thread loaded, plus (last CTA) the tail < one chunk
+  for (int i = 0; i < 16; ++i) acc[i] = 0.f;
   double pw = 0.0;
-  {
+  const long long steps = (nch + (long long)NG * gridDim.x - 1) / ((long long)NG * gridDim.x);
+  for (long long it = 0; it < steps; ++it) {   // uniform trip count (the FFT barriers are CTA-wide)
+    const long long c = (long long)NG * (blockIdx.x + (long long)gridDim.x * it) + g;
+    const bool act = c < nch;
+    float2 ve[8], vo[8];
     float p0 = 0.f;
 #pragma unroll
-    for (int r = 0; r < 8; ++r) p0 += zz[r].x * zz[r].x + zz[r].y * zz[r].y + zz[r].z * zz[r].z + zz[r].w * zz[r].w;
-    pw = (double)p0;
-    if (blockIdx.x == gridDim.x - 1)
-      for (long long q = qlo + 1024 * nch + threadIdx.x; q < qhi; q += blockDim.x) pw += (double)cabs2(d.z[rmod(q, d.z_cap)]);
+    for (int r = 0; r < 8; ++r) {
+      float4 zz = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (act) zz = *reinterpret_cast<const float4 *>(d.z + rmod(qlo + 1024 * c + 2 * (j + 64 * r), d.z_cap));
+      p0 += zz.x * zz.x + zz.y * zz.y + zz.z * zz.z + zz.w * zz.w;
+      const float2 a = make_float2(zz.x, zz.y), bq = make_float2(zz.z, zz.w);
+      const float2 a2 = cmul(a, a), b2 = cmul(bq, bq);
+      ve[r] = cmul(a2, a2);
+      vo[r] = cmul(b2, b2);
+    }
+    pw += (double)p0;
+    fft512_regs<false, 0>(bufs[g], j, tw, ve);
+    fft512_regs<false, 0>(bufs[g], j, tw, vo);   // same buffer: fft512_regs syncs before its first store
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const float2 od = cmul(vo[r], tw[j + 64 * r]);
+      acc[r] += act ? cabs2(cadd(ve[r], od)) : 0.f;        // X[k],       k = j + 64 r
+      acc[8 + r] += act ? cabs2(csub(ve[r], od)) : 0.f;    // X[k + 512]
+    }
   }
+  if (blockIdx.x == 0)                          // power of the tail beyond the complete chunks
+    for (long long q = qlo + 1024 * nch + threadIdx.x; q < qhi; q += blockDim.x) pw += (double)cabs2(d.z[rmod(q, d.z_cap)]);
+  __syncthreads();                              // every group done with its FFT buffer
+  float *accs = reinterpret_cast<float *>(&bufs[0][0]);
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
-    const float2 a = make_float2(zz[r].x, zz[r].y), bq = make_float2(zz[r].z, zz[r].w);
-    const float2 a2 = cmul(a, a), b2 = cmul(bq, bq);
-    ve[r] = cmul(a2, a2);
-    vo[r] = cmul(b2, b2);
-  }
-  fft512_regs<false, 0>(bg, j, tw, ve);
-  fft512_regs<false, 0>(bg, j, tw, vo);   // same buffer: fft512_regs syncs before its first store
-  __syncthreads();                        // every group done with its FFT buffer
-  float *acc = reinterpret_cast<float *>(bufs);
-#pragma unroll
-  for (int r = 0; r < 8; ++r) {
-    const int k = j + 64 * r;
-    const float2 od = cmul(vo[r], tw[k]);
-    acc[g * 1024 + k] = act ? cabs2(cadd(ve[r], od)) : 0.f;         // X[k]
-    acc[g * 1024 + k + 512] = act ? cabs2(csub(ve[r], od)) : 0.f;   // X[k + 512]
+    accs[g * 1024 + j + 64 * r] = acc[r];
+    accs[g * 1024 + j + 64 * r + 512] = acc[8 + r];
   }
   __syncthreads();
-  // S[k] = sum over the CTA's chunks in fixed group order
   const long long row = (long long)blockIdx.y * gridDim.x + blockIdx.x;
-  {
-    const int k = threadIdx.x;
+#pragma unroll
+  for (int i = 0; i < CFO_KPT; ++i) {
+    const int k = threadIdx.x + CFO_SPEC_T * i;
     float sk = 0.f;
 #pragma unroll
-    for (int gg = 0; gg < CFO_GROUPS; ++gg) sk += acc[gg * 1024 + k];
+    for (int gg = 0; gg < NG; ++gg) sk += accs[gg * 1024 + k];
     d.cfo_part[row * 1024 + k] = sk;
   }
   pw = warp_sum_d(pw);
@@ -312,7 +331,7 @@ __global__ void __launch_bounds__(1024) k_cfo_spec(RxDev d, long long beta0, lon
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
-    for (int i = 0; i < 32; ++i) t += red[i];
+    for (int i = 0; i < CFO_SPEC_T / 32; ++i) t += red[i];
     d.cfo_pow[row] = t;
   }
   // the last CTA of this buffer reduces its rows (formerly the separate k_cfo_final launch)
@@ -387,8 +406,9 @@ __global__ void __launch_bounds__(256) k_cfo_fine(RxDev d, long long beta0, long
   }
 }
 
-// DDS increments and phase origins, carried across buffers (sequential, tiny)
-__global__ void k_cfo_carry(RxDev d, long long beta0, int nbuf) {
+// DDS increments and phase origins, carried across buffers (sequential, tiny); then z' is valid
+// (computed on the fly by zp_value) for q < min((beta0 + nbuf) Q, qfront)
+__global__ void k_cfo_carry(RxDev d, long long beta0, int nbuf, long long qfront) {
   for (int i = 0; i < nbuf; ++i) {
     CfoParam cp = d.cfo[rmod(beta0 + i, d.buf_cap)];
     double df = cp.kstar >= 0 ? cp.df : d.st->cfo_df_prev;   // no complete chunk: reuse
@@ -403,47 +423,168 @@ __global__ void k_cfo_carry(RxDev d, long long beta0, int nbuf) {
     }
     d.cfo[rmod(beta0 + i, d.buf_cap)] = cp;
   }
+  const long long q1 = (beta0 + nbuf) * (long long)d.buffer_blocks * 256;
+  d.st->v_front = q1 < qfront ? q1 : qfront;   // consumed by later launches (stream order)
 }
 
-// z'_q = z_q / sqrt(P_beta) e^{-j psi'_q}, psi' the carried per-buffer CFO DDS (c-8),
-// materialised once into the z' ring that the sync / LMS stages read.
-__global__ void __launch_bounds__(256) k_kk_zprime(RxDev d, long long beta0, int nbuf, long long qfront) {
-  const long long Q = (long long)d.buffer_blocks * 256;
-  const long long q0 = beta0 * Q;
-  long long q1 = (beta0 + nbuf) * Q;
-  if (q1 > qfront) q1 = qfront;
-  if (blockIdx.x == 0 && threadIdx.x == 0) d.st->v_front = q1;   // consumed by later launches
-  // 8 consecutive samples per thread-step (Q is a multiple of 8: one buffer per step): one exact
-  // DDS phase word, then 1-sample step rotations
-  for (long long q = q0 + 8 * ((long long)blockIdx.x * blockDim.x + threadIdx.x); q < q1;
-       q += 8 * (long long)gridDim.x * blockDim.x) {
-    const long long beta = q / Q;
+// z'_q = z_q / sqrt(P_beta) e^{-j psi'_q} (c-8), psi' the carried per-buffer CFO DDS: evaluated
+// where it is consumed (the equaliser's shared-memory staging, frame sync, training) instead of
+// being materialised as a ring (the former k_kk_zprime pass: one HBM read + write of the 2-sps
+// field saved). The phase word is exact (64-bit, absolute index); the rotation takes the MUFU
+// sin/cos of the top 32 bits as an angle in [-pi, pi) (|error| ~ 1e-6 rad).
+struct ZpCache {
+  long long beta;
+  unsigned long long origin, inc;
+  float s;
+};
+__device__ __forceinline__ float2 dds_rot_neg_fast(unsigned long long u) {
+  const float x = (float)(int)(u >> 32) * 1.4629180792671596e-9f;   // pi 2^-31
+  float sn, cs;
+  __sincosf(x, &sn, &cs);
+  return make_float2(cs, -sn);
+}
+__device__ __forceinline__ float2 zp_rotate(const RxDev &d, float2 v, long long q, ZpCache &c) {
+  const long long beta = q >> d.q_shift;
+  if (beta != c.beta) {
     const CfoParam &cp = d.cfo[rmod(beta, d.buf_cap)];
-    const float s = cp.inv_sqrtP;
-    float2 rot = make_float2(1.f, 0.f), st1 = make_float2(1.f, 0.f);
-    if (d.cfo_enable) {
-      rot = dds_rot_neg(cp.origin + (unsigned long long)(q - beta * Q) * cp.inc);
-      st1 = dds_rot_neg(cp.inc);
-    }
-    if (q + 8 <= q1) {
-      const float4 *src = reinterpret_cast<const float4 *>(d.z + rmod(q, d.z_cap));
-      float4 *dst = reinterpret_cast<float4 *>(d.zp + rmod(q, d.zp_cap));
-      float4 zz[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) zz[u] = src[u];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float2 a = cmul(cscale(make_float2(zz[u].x, zz[u].y), s), rot);
-        rot = cmul(rot, st1);
-        const float2 b = cmul(cscale(make_float2(zz[u].z, zz[u].w), s), rot);
-        rot = cmul(rot, st1);
-        dst[u] = make_float4(a.x, a.y, b.x, b.y);
-      }
-    } else {
-      for (long long e = q; e < q1; ++e) {
-        d.zp[rmod(e, d.zp_cap)] = cmul(cscale(d.z[rmod(e, d.z_cap)], s), rot);
-        rot = cmul(rot, st1);
-      }
+    c.beta = beta;
+    c.origin = cp.origin;
+    c.inc = cp.inc;
+    c.s = cp.inv_sqrtP;
+  }
+  v = cscale(v, c.s);
+  if (d.cfo_enable) v = cmul(v, dds_rot_neg_fast(c.origin + (unsigned long long)(q - (beta << d.q_shift)) * c.inc));
+  return v;
+}
+__device__ __forceinline__ float2 zp_value(const RxDev &d, long long q, long long vend, ZpCache &c) {
+  if (q < 0 || q >= vend) return make_float2(0.f, 0.f);
+  return zp_rotate(d, d.z[rmod(q, d.z_cap)], q, c);
+}
+
+
+// ------------------------------------------------------------------ time sharding
+// One shard's per-round carry record (packed; rx_export_carry writes it to device memory, the
+// caller all-gathers the records of every shard (NCCL) and passes them to rx_import_carry).
+// It carries exactly the quantities that cross buffer boundaries in the KK chain:
+//  - the CFO estimate (P, df, k*) of the buffer this shard estimated this round: every shard
+//    rebuilds the DDS origin chain origin_{b+1} = origin_b + Q inc_b (c-8) from all of them;
+//  - the frame-sync result and the trained taps W_train (V_train) from the shard holding the
+//    stream start (c-10, c-9 'Training');
+//  - the lag-D seeds (epoch mean canonical taps, c-9 'Seed') this shard finalised since its last
+//    record, for the shard owning epoch e + D.
+#define RX_CARRY_SEEDS 2
+struct RxCarry {
+  long long beta;                       // buffer estimated this round (-1: none)
+  double P, df;
+  int kstar, flags;                     // flags bit 0: sync + training valid
+  int sync_offset, sync_phase, sync_polarity, pad;
+  double sync_gamma, sync_phi0;
+  float2 w_train[RX_MAX_K], v_train[RX_MAX_K];
+  long long seed_epoch[RX_CARRY_SEEDS]; // -1: slot unused
+  float2 seed[RX_CARRY_SEEDS][RX_MAX_K];
+};
+
+// one thread: the shard's record of this round
+__global__ void k_carry_export(RxDev d, RxCarry *out, long long beta, long long seed_e0, int nseed) {
+  RxCarry c;
+  memset(&c, 0, sizeof(c));
+  c.beta = beta;
+  if (beta >= 0) {
+    const CfoParam cp = d.cfo[rmod(beta, d.buf_cap)];
+    c.P = cp.P;
+    c.df = cp.df;
+    c.kstar = cp.kstar;
+  }
+  const DevState *st = d.st;
+  if (st->synced && st->trained) {
+    c.flags = 1;
+    c.sync_offset = st->sync_offset;
+    c.sync_phase = st->sync_phase;
+    c.sync_polarity = st->sync_polarity;
+    c.sync_gamma = st->sync_gamma;
+    c.sync_phi0 = st->sync_phi0;
+    for (int k = 0; k < RX_MAX_K; ++k) {
+      c.w_train[k] = d.w_train[k];
+      c.v_train[k] = d.wl ? d.v_train[k] : make_float2(0.f, 0.f);
     }
   }
+  for (int i = 0; i < RX_CARRY_SEEDS; ++i) {
+    const long long e = seed_e0 + i;
+    const bool ok = i < nseed && e >= 0 && d.seed_ready[rmod(e, d.seed_cap)] == e + 1;
+    c.seed_epoch[i] = ok ? e : -1;
+    for (int k = 0; k < RX_MAX_K; ++k) c.seed[i][k] = ok ? d.seed[rmod(e, d.seed_cap) * RX_MAX_K + k] : make_float2(0.f, 0.f);
+  }
+  *out = c;
+}
+
+// one thread: every shard's record of the round, in rank order (= buffer order). CFO parameters
+// go to the per-buffer table exactly as cfo_final_block / k_cfo_fine leave them (the origin
+// chain is then advanced by k_cfo_carry over the round's buffers, as in the single stream);
+// sync / training and seeds are taken from whichever record carries them.
+__global__ void k_carry_import(RxDev d, const RxCarry *g, int n) {
+  DevState *st = d.st;
+  for (int i = 0; i < n; ++i) {
+    const RxCarry &c = g[i];
+    if (c.beta >= 0) {
+      CfoParam cp;
+      cp.P = c.P;
+      cp.df = c.df;
+      cp.kstar = c.kstar;
+      cp.inv_sqrtP = (float)(1.0 / sqrt(c.P));
+      cp.inc = (unsigned long long)llrint(ldexp(c.df / d.fs2, 64));
+      cp.origin = 0ull;
+      d.cfo[rmod(c.beta, d.buf_cap)] = cp;
+    }
+    if ((c.flags & 1) && !st->trained) {
+      st->sync_offset = c.sync_offset;
+      st->sync_phase = c.sync_phase;
+      st->sync_polarity = c.sync_polarity;
+      st->sync_gamma = c.sync_gamma;
+      st->sync_phi0 = c.sync_phi0;
+      for (int k = 0; k < RX_MAX_K; ++k) {
+        d.w_train[k] = c.w_train[k];
+        if (d.wl) d.v_train[k] = c.v_train[k];
+      }
+      if (c.sync_gamma < d.sync_min) set_flag(st, RX_FLAG_SYNC_DEV);
+      __threadfence();
+      st->synced = 1;
+      st->trained = 1;
+      d.hm->synced = 1;
+      d.hm->trained = 1;
+    }
+    for (int j = 0; j < RX_CARRY_SEEDS; ++j) {
+      const long long e = c.seed_epoch[j];
+      if (e < 0 || d.seed_ready[rmod(e, d.seed_cap)] == e + 1) continue;
+      for (int k = 0; k < RX_MAX_K; ++k) d.seed[rmod(e, d.seed_cap) * RX_MAX_K + k] = c.seed[j][k];
+      __threadfence();
+      d.seed_ready[rmod(e, d.seed_cap)] = (int)(e + 1);
+    }
+  }
+}
+
+// the DDS origin chain over the round's buffers in buffer order (k_cfo_carry's arithmetic)
+__global__ void k_carry_chain(RxDev d, const RxCarry *g, int n) {
+  for (int i = 0; i < n; ++i) {
+    const long long b = g[i].beta;
+    if (b < 0) continue;
+    CfoParam cp = d.cfo[rmod(b, d.buf_cap)];
+    const double df = cp.kstar >= 0 ? cp.df : d.st->cfo_df_prev;
+    if (d.cfo_enable) {
+      cp.df = df;
+      cp.inc = (unsigned long long)llrint(ldexp(df / d.fs2, 64));
+      cp.origin = d.st->cfo_origin_next;
+      d.st->cfo_origin_next = cp.origin + (unsigned long long)((long long)d.buffer_blocks * 256) * cp.inc;
+      d.st->cfo_df_prev = df;
+    } else {
+      cp.df = 0.0; cp.inc = 0ull; cp.origin = 0ull;
+    }
+    d.cfo[rmod(b, d.buf_cap)] = cp;
+  }
+}
+
+// stage B of a time shard: z' valid below q_valid, finalisation front at the epoch's first segment
+__global__ void k_shard_seek(RxDev d, long long q_valid, long long seg0) {
+  d.st->v_front = q_valid;
+  d.st->seg_next = seg0;
+  d.hm->seg_next = seg0;
 }

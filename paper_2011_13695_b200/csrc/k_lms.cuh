@@ -13,7 +13,11 @@
 template <bool CPLX>
 __device__ __forceinline__ float2 lms_in(const RxDev &d, long long i, long long vend) {
   if (i < 0 || i >= vend) return make_float2(0.f, 0.f);
-  if (CPLX) return d.zp[rmod(i, d.zp_cap)];
+  if (CPLX) {
+    ZpCache c;
+    c.beta = -1;
+    return zp_value(d, i, vend, c);            // z' on the fly (c-8)
+  }
   return make_float2(d.uhat[rmod(i, d.sym_cap)], 0.f);
 }
 
@@ -182,18 +186,19 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // stage input samples [i0, i1) (absolute index of u^ (PAM) or z' (KK)) into the mirrored ring;
-// zero outside [0, vend) (cp.async zero-fill)
+// zero outside [0, vend). PAM: cp.async (zero-fill); KK: z' is formed from z on the way in
+// (zp_value: normalisation + CFO rotation, c-8) and stored by the warp
 template <bool CPLX>
 __device__ __forceinline__ void lms_stage(const RxDev &d, LmsSmemT<CPLX> &sm, long long i0, long long i1,
-                                          long long vend, long long base) {
+                                          long long vend, long long base, ZpCache *zc = nullptr) {
   const int lane = threadIdx.x & 31;
   for (long long i = i0 + lane; i < i1; i += 32) {
     const bool ok = i >= 0 && i < vend;
     const int slot = (int)((i - base) & (LMS_RING - 1));   // block windows start 128 B aligned
     if constexpr (CPLX) {
-      const float2 *src = ok ? d.zp + rmod(i, d.zp_cap) : d.zp;
-      cp_async_elem(&sm.ring[slot], src, ok);
-      cp_async_elem(&sm.ring[slot + LMS_RING], src, ok);
+      const float2 v = zp_value(d, i, vend, *zc);
+      sm.ring[slot] = v;
+      sm.ring[slot + LMS_RING] = v;
     } else {
       const float *src = ok ? d.uhat + rmod(i, d.sym_cap) : d.uhat;
       cp_async_elem(&sm.ring[slot], src, ok);
@@ -286,11 +291,11 @@ __device__ __forceinline__ void lms_stage_vec(const RxDev &d, LmsSmemT<false> &s
 }
 template <bool CPLX>
 __device__ __forceinline__ void lms_stage_any(const RxDev &d, LmsSmemT<CPLX> &sm, long long i0, long long i1,
-                                              long long vend, long long base, bool vec) {
+                                              long long vend, long long base, bool vec, ZpCache *zc = nullptr) {
   if constexpr (!CPLX) {
     if (vec) { lms_stage_vec(d, sm, i0, i1, vend, base); return; }
   }
-  lms_stage<CPLX>(d, sm, i0, i1, vend, base);
+  lms_stage<CPLX>(d, sm, i0, i1, vend, base, zc);
 }
 
 __device__ __forceinline__ float2 as_c(float v) { return make_float2(v, 0.f); }
@@ -362,11 +367,13 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
   // 32-bit ring arithmetic, the mirror copy only for the slots a window can wrap onto (< 64)
   const bool fast = vec && wb0 >= 0 && wb0 + WLa + DS * nblk <= vend;
   const int gbase = (int)(wb0 & (d.sym_cap - 1)), gmask = (int)(d.sym_cap - 1);
-  lms_stage_any<CPLX>(d, sm, wb0, wb0 + WLa, vend, wb0, vec);
+  ZpCache zc;                               // KK: CFO parameters of the buffer last staged
+  zc.beta = -1;
+  lms_stage_any<CPLX>(d, sm, wb0, wb0 + WLa, vend, wb0, vec, &zc);
   cp_async_commit();
 #pragma unroll 1
   for (int g = 1; g < LMS_AHEAD; ++g) {
-    if (g < nblk) lms_stage_any<CPLX>(d, sm, wb0 + WLa + (long long)(g - 1) * DS, wb0 + WLa + (long long)g * DS, vend, wb0, vec);
+    if (g < nblk) lms_stage_any<CPLX>(d, sm, wb0 + WLa + (long long)(g - 1) * DS, wb0 + WLa + (long long)g * DS, vend, wb0, vec, &zc);
     cp_async_commit();
   }
   bool first = true;
@@ -383,6 +390,18 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
 #pragma unroll 1
   for (int jb = 0; jb < nblk32; ++jb) {
     const int rb = 32 * jb;                  // block start relative to t_begin
+    // KK: the z samples of block jb + AHEAD are loaded now and turned into z' at the end of this
+    // block (the load latency hides behind the block's recursion; DS = 64 = 2 per lane)
+    float2 zr[2];
+    long long zq[2];
+    if constexpr (CPLX) {
+      const int jn = jb + LMS_AHEAD;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        zq[u] = wb0 + WLa + (long long)(jn - 1) * DS + lane + 32 * u;
+        zr[u] = (jn < nblk && zq[u] >= 0 && zq[u] < vend) ? d.z[rmod(zq[u], d.z_cap)] : make_float2(0.f, 0.f);
+      }
+    }
     cp_async_wait<LMS_AHEAD - 1>();
     __syncwarp();
     const int nvalid = nsym - rb < 32 ? nsym - rb : 32;
@@ -478,15 +497,16 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
             __syncwarp();
             bps_partial(sm.y, 0, nvalid, rsA, rsB, L, d.Pt > 32, dA, dB);
           }
+          // argmin over the test phases, lowest p on ties (c-9 step 2): the distances are sums of
+          // squares (>= +0), so their IEEE bit patterns order like the values and one warp-wide
+          // integer min (redux.sync) finds the minimum; the lowest lane holding it (ballot) is p
           float bd = lane < d.Pt ? dA : 3.4e38f;
           int bp = lane;
           if (lane + 32 < d.Pt && dB < bd) { bd = dB; bp = lane + 32; }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const float ob = __shfl_xor_sync(0xffffffffu, bd, o);
-            const int op = __shfl_xor_sync(0xffffffffu, bp, o);
-            if (ob < bd || (ob == bd && op < bp)) { bd = ob; bp = op; }
-          }
+          const unsigned bits = __float_as_uint(bd);
+          const unsigned mn = __reduce_min_sync(0xffffffffu, bits);
+          const unsigned lo = __ballot_sync(0xffffffffu, bits == mn && bp < 32);
+          bp = lo ? __ffs(lo) - 1 : __ffs(__ballot_sync(0xffffffffu, bits == mn)) - 1 + 32;
           th_hat = -0.78539816339744831f + ((float)bp + 0.5f) * (1.5707963267948966f / (float)d.Pt);
         }
         if (first) theta = th_hat;
@@ -633,7 +653,13 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
         lms_stage_any<CPLX>(d, sm, wb0 + WLa + (long long)(jn - 1) * DS, wb0 + WLa + (long long)jn * DS, vend, wb0, vec);
       }
     } else if (jn < nblk) {
-      lms_stage_any<CPLX>(d, sm, wb0 + WLa + (long long)(jn - 1) * DS, wb0 + WLa + (long long)jn * DS, vend, wb0, vec);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const float2 v = (zq[u] >= 0 && zq[u] < vend) ? zp_rotate(d, zr[u], zq[u], zc) : make_float2(0.f, 0.f);
+        const int slot = (int)((zq[u] - wb0) & (LMS_RING - 1));
+        sm.ring[slot] = v;
+        sm.ring[slot + LMS_RING] = v;
+      }
     }
     cp_async_commit();
     first = false;
@@ -749,13 +775,16 @@ __device__ void bps_helper(const RxDev &d, const float2 *ys, long long t_begin, 
 // ------------------------------------------------------------------ segments (1 warp each)
 // Segment s outputs [sS, min((s+1)S, m_end)), recursion starts O symbols early (c-9).
 #ifndef LMS_SPC
-#define LMS_SPC 4           // segments (warps) per CTA of k_lms_seg
+#define LMS_SPC 1           // warps per CTA of k_lms_seg (1: finest CTA balance over the SMs; measured 4 -> 1: KK equaliser 0.89 -> 0.72 ms per C4 step)
+#endif
+#ifndef LMS_PAIR
+#define LMS_PAIR 1          // BPS segments: 2 = a helper warp scores half of each block's symbols
 #endif
 template <bool CPLX, int CPR, int KP, bool WLIN = false, int MODE = 1>
 __global__ void __launch_bounds__(32 * LMS_SPC) k_lms_seg(RxDev d, int flush, int nseg, unsigned char *labels,
                                                  long long lab_cap) {
   // BPS segments run on a warp pair (LMS warp + BPS helper), others on one warp
-  constexpr int PAIR = 1, SPC = LMS_SPC / PAIR;   // PAIR = 2 runs BPS on an extra helper warp
+  constexpr int PAIR = (CPR == 2) ? LMS_PAIR : 1, SPC = LMS_SPC / PAIR;   // PAIR = 2: BPS helper warp
   __shared__ LmsSmemT<CPLX> sm[SPC];
   __shared__ float2 bps_part[SPC][32];
   DevState *st = d.st;

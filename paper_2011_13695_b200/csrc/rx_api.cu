@@ -112,13 +112,19 @@ struct rx_handle {
   // onto `side`, concurrently with its own front-end / clock / back-end / normalisation, and
   // joins it back before the call's work on the caller's stream ends.
   cudaStream_t side;
-  cudaEvent_t ev_fork, ev_join;
+  cudaEvent_t ev_fork, ev_join[2];  // join of call k recorded in ev_join[k & 1]
+  long long ncall;                   // streaming rx_process calls so far
   long long lms_sym_ub;          // symbol upper bound of the data normalised by earlier calls
   uint16_t *unpacked;            // RX_IN_U12_PACKED: this call's codes unpacked to u16
   struct ZpJob { long long beta0, nb, q_front; };
   std::vector<ZpJob> zp_pending; // KK: CFO carry + z' groups deferred to the next call's side stream
   long long clk_launch;          // fused clock launches so far (tags the tile totals)
   bool flushed;
+  // time sharding (shard_count > 1): the buffer whose stage A ran last (awaiting export / stage B)
+  struct ShardBuf { long long beta, qfront; int last, valid, exported; unsigned char *labels; long long cap; };
+  ShardBuf sh_cur, sh_pend;     // this round's stage A; the previous round's (stage B at import)
+  long long sh_seed_e;          // lag-D seed epoch produced by the last stage B (-1 none)
+  RxCarry *sh_rec;              // device scratch for the export record
   long long launches;
   int sps;
   long long Q;   // 2-sps samples per buffer (KK)
@@ -265,6 +271,12 @@ static rx_status validate(const rx_config *c) {
   if (c->serial_equaliser != 0 && c->serial_equaliser != 1) return RX_EINVAL;
   if (c->cpr_anchor != 0 && c->cpr_anchor != 1) return RX_EINVAL;
   if (c->lms_mode != 0 && c->lms_mode != 1) return RX_EINVAL;
+  if (c->equaliser_lag != 0 && c->equaliser_lag != 1) return RX_EINVAL;
+  if (c->shard_count < 0 || c->shard_count > 64) return RX_EINVAL;
+  if (c->shard_count > 1) {        // time sharding (SURVEY §8(e) mode 2): the KK chain
+    if (c->family != RX_QAM_KK || c->cpr_anchor != 1 || c->shard_count > c->tap_lag_epochs) return RX_EINVAL;
+    if (c->shard_index < 0 || c->shard_index >= c->shard_count) return RX_EINVAL;
+  }
   if (c->q_window_symbols < 0 || (c->q_window_symbols > 0 && c->q_window_symbols % c->lms_segment)) return RX_EINVAL;
   if (c->lms_batch_segments < 0 || c->lms_batch_segments > (1 << 16)) return RX_EINVAL;
   if (c->family == RX_QAM_KK && !(c->sideband == 1 || c->sideband == -1)) return RX_EINVAL;
@@ -299,7 +311,7 @@ extern "C" void rx_destroy(rx_handle *h) {
   if (h->hm_host) cudaFreeHost(h->hm_host);
   if (h->side) cudaStreamDestroy(h->side);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
-  if (h->ev_join) cudaEventDestroy(h->ev_join);
+  for (int i = 0; i < 2; ++i) if (h->ev_join[i]) cudaEventDestroy(h->ev_join[i]);
   for (auto &e : h->prof_pending) { cudaEventDestroy(e.second.first); cudaEventDestroy(e.second.second); }
   for (auto &e : h->prof_free) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   delete h;
@@ -339,6 +351,8 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   d.D = c.tap_lag_epochs;
   d.cpr = kk ? (c.cpr_test_phases == 0 ? 1 : 2) : 0;
   d.lms_mode = c.lms_mode;
+  d.shard_n = c.shard_count > 1 ? c.shard_count : 1;
+  d.shard_g = c.shard_count > 1 ? c.shard_index : 0;
   d.Pt = c.cpr_test_phases;
   d.anchor_each = kk && c.cpr_anchor;
   d.mu = (float)c.mu;
@@ -467,7 +481,9 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   const long long batch_sym = bsym + (bsym > tail_sym ? tail_sym : bsym);
   // (HB + 1 buffers: the equaliser side stream reads the previous calls' symbols while the
   // current call writes up to one more call of them)
-  d.sym_cap = next_pow2((long long)(HB + HB - 2) * c.buffer_blocks * (kk ? 128 : 260) + batch_sym);
+  // (equaliser_lag = 1: the side stream may still read one more call of them)
+  const long long lag_calls = 1 + c.equaliser_lag;
+  d.sym_cap = next_pow2((long long)(HB + lag_calls * (HB - 2)) * c.buffer_blocks * (kk ? 128 : 260) + batch_sym);
   if (!kk) {
     TRY(dalloc(h, &d.C, d.blk_cap));
     TRY(dalloc(h, &d.theta, d.blk_cap));
@@ -490,14 +506,17 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
     TRY(dalloc(h, &d.clk_ticket, 2));   // [0] tiles finished, [1] tiles dispatched
   } else {
     d.E_cap = next_pow2((long long)HB * c.buffer_blocks * 512);
-    // (+ one call: the side stream's z' pass reads the previous call's z while stage 2 writes)
-    d.z_cap = next_pow2((long long)(HB + HB - 2) * c.buffer_blocks * 256);
+    // z is read by the equaliser (z' on the fly, zp_value) up to one batch + D epochs after stage 2
+    // wrote it, on the side stream while the current call writes one more call of it
+    d.z_cap = next_pow2((long long)(HB + lag_calls * (HB - 2)) * c.buffer_blocks * 256 + 2 * batch_sym);
+    if (c.shard_count > 1)   // a shard's buffers b and b + N (plus halos) are held together
+      d.z_cap = next_pow2((long long)(c.shard_count + 2) * c.buffer_blocks * 256 + 2 * RX_SHARD_POST);
     TRY(dalloc(h, &d.E, d.E_cap));
     TRY(dalloc(h, &d.z, d.z_cap));
-    d.zp_cap = next_pow2((long long)(HB + HB - 2) * c.buffer_blocks * 256 + 2 * batch_sym);
-    TRY(dalloc(h, &d.zp, d.zp_cap));
+    d.q_shift = 0;
+    while ((1LL << d.q_shift) < (long long)c.buffer_blocks * 256) ++d.q_shift;
     TRY(dalloc(h, &d.cfo, d.buf_cap));
-    d.cfo_G = (int)(h->Q / 1024 / CFO_GROUPS + 1);      // spectrum rows per buffer
+    d.cfo_G = CFO_ROWS;                                  // spectrum rows per buffer
     const long long maxbuf = HB;                           // buffers completing in one call
     TRY(dalloc(h, &d.cfo_part, maxbuf * d.cfo_G * 1024));
     TRY(dalloc(h, &d.cfo_pow, maxbuf * d.cfo_G));
@@ -511,6 +530,12 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   TRY(dalloc(h, &d.w_init, RX_MAX_K));
   d.seed_cap = 64;
   TRY(dalloc(h, &d.seed, d.seed_cap * RX_MAX_K));
+  if (c.shard_count > 1) {
+    TRY(dalloc(h, &h->sh_rec, 1));
+    h->cfg.serial_equaliser = 1;   // a shard orders everything on the caller's stream
+  }
+  h->sh_cur.valid = h->sh_pend.valid = 0;
+  h->sh_seed_e = -1;
   d.wl = c.widely_linear;
   if (d.wl) TRY(dalloc(h, &d.v_train, RX_MAX_K));
   if (!kk) TRY(dalloc(h, &d.cal_part, (long long)CAL_G * 16 * 2));
@@ -545,11 +570,9 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   memset((void *)h->hm_host, 0, sizeof(HostMirror));
   if (cudaHostGetDevicePointer((void **)&d.hm, (void *)h->hm_host, 0) != cudaSuccess) { rx_destroy(h); return RX_ECUDA; }
   // kernels needing > 48 KB dynamic shared memory
-  const size_t cfo_smem = (1024 + CFO_GROUPS * FFT_PAD_N) * sizeof(float2);
   const size_t clk_smem = (CLK_TILE + 1 + 2 * c.clock_avg_half) * sizeof(double2);
   if (cudaFuncSetAttribute(k_pam_theta<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)clk_smem) != cudaSuccess ||
       cudaFuncSetAttribute(k_pam_theta<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)clk_smem) != cudaSuccess ||
-      cudaFuncSetAttribute(k_cfo_spec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfo_smem) != cudaSuccess ||
       cudaFuncSetAttribute(k_sync_corr<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536) != cudaSuccess ||
       cudaFuncSetAttribute(k_sync_corr<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536) != cudaSuccess) {
     rx_destroy(h);
@@ -560,7 +583,8 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
     if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, hi) != cudaSuccess ||
         cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&h->ev_join[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_join[1], cudaEventDisableTiming) != cudaSuccess) {
       rx_destroy(h);
       return RX_ECUDA;
     }
@@ -655,7 +679,8 @@ static void launch_lms_round(rx_handle *h, cudaStream_t s, unsigned char *labels
                              int flush, long long nseg) {
   RxDev &d = h->d;
   const long long S = d.S;
-  const int spc = LMS_SPC;   // segments per CTA
+  // segments per CTA: LMS_SPC warps, BPS segments on LMS_PAIR warps each (k_lms_seg)
+  const int spc = (d.cpr == 2 && d.lms_mode == 0) ? LMS_SPC / LMS_PAIR : LMS_SPC;
   KLAUNCH(h, RX_K_LMS, s, (lms_seg_kernel(d)<<<gridc(nseg, spc), 32 * LMS_SPC, 0, s>>>(d, flush, (int)nseg, labels, lab_cap)));
   if (d.family == RX_PAM) {
     // PAM segments wrote their labels and error counts; the prefix also adds the counters
@@ -742,7 +767,6 @@ static void launch_norm_pam(rx_handle *h, cudaStream_t s, int flush) {
 static void run_pam(rx_handle *h, cudaStream_t s, const InView &in, unsigned char *labels,
                     long long lab_cap, int flush) {
   RxDev &d = h->d;
-  const long long BB = d.buffer_blocks;
   const long long fe_target = h->n_in / 512;
   if (fe_target > h->fe_done) {
     if (d.H_real) KLAUNCH(h, RX_K_PAM_FE, s, (k_pam_fe<true><<<gridc(fe_target - h->fe_done, FE_GROUPS), 256, 0, s>>>(d, in, h->fe_done, fe_target)));
@@ -781,12 +805,11 @@ static void run_pam(rx_handle *h, cudaStream_t s, const InView &in, unsigned cha
   }
 }
 
-// KK: the deferred CFO carry + z' groups, in buffer order (the DDS origin is a chain)
+// KK: the deferred CFO carries, in buffer order (the DDS origin is a chain)
 static void launch_zp_pending(rx_handle *h, cudaStream_t s) {
   RxDev &d = h->d;
   for (const auto &j : h->zp_pending) {
-    KLAUNCH(h, RX_K_CFO, s, (k_cfo_carry<<<1, 1, 0, s>>>(d, j.beta0, (int)j.nb)));
-    KLAUNCH(h, RX_K_CFO, s, (k_kk_zprime<<<2048, 256, 0, s>>>(d, j.beta0, (int)j.nb, j.q_front)));
+    KLAUNCH(h, RX_K_CFO, s, (k_cfo_carry<<<1, 1, 0, s>>>(d, j.beta0, (int)j.nb, j.q_front)));
   }
   h->zp_pending.clear();
 }
@@ -812,17 +835,15 @@ static void run_kk(rx_handle *h, cudaStream_t s, const InView &in, unsigned char
     while ((h->cfo_done + nbuf + 1) * Q <= q_front || (flush && (h->cfo_done + nbuf) * Q < q_front)) ++nbuf;
     if (nbuf > 0) {
       const long long beta0 = h->cfo_done;
-      const size_t smem = (1024 + CFO_GROUPS * FFT_PAD_N) * sizeof(float2);
       const int nrows = d.cfo_G;
       const int fine_ctas = (int)((Q / 1024 + 7) / 8);
       for (long long b0 = 0; b0 < nbuf; b0 += h->cfg.history_buffers) {
         const long long nb = nbuf - b0 < h->cfg.history_buffers ? nbuf - b0 : h->cfg.history_buffers;
-        KLAUNCH(h, RX_K_CFO, s, (k_cfo_spec<<<dim3((unsigned)nrows, (unsigned)nb), 1024, smem, s>>>(d, beta0 + b0, q_front)));
+        KLAUNCH(h, RX_K_CFO, s, (k_cfo_spec<<<dim3((unsigned)nrows, (unsigned)nb), CFO_SPEC_T, 0, s>>>(d, beta0 + b0, q_front)));
         if (d.cfo_enable) KLAUNCH(h, RX_K_CFO, s, (k_cfo_fine<<<dim3((unsigned)fine_ctas, (unsigned)nb), 256, 0, s>>>(d, beta0 + b0, q_front, fine_ctas)));
         if (flush || h->cfg.serial_equaliser) {
-          KLAUNCH(h, RX_K_CFO, s, (k_cfo_carry<<<1, 1, 0, s>>>(d, beta0 + b0, (int)nb)));
-          KLAUNCH(h, RX_K_CFO, s, (k_kk_zprime<<<2048, 256, 0, s>>>(d, beta0 + b0, (int)nb, q_front)));
-        } else {   // the DDS carry and z' only feed the equaliser: next call, side stream
+          KLAUNCH(h, RX_K_CFO, s, (k_cfo_carry<<<1, 1, 0, s>>>(d, beta0 + b0, (int)nb, q_front)));
+        } else {   // the DDS carry (z' validity) only feeds the equaliser: next call, side stream
           h->zp_pending.push_back({beta0 + b0, nb, q_front});
         }
       }
@@ -855,7 +876,12 @@ static void fork_equaliser(rx_handle *h, cudaStream_t s, unsigned char *labels, 
   if (d.family == RX_PAM) launch_sync_train<false>(h, h->side, 0);
   else launch_sync_train<true>(h, h->side, 0);
   launch_lms_rounds(h, h->side, labels, lab_cap, 0, h->lms_sym_ub);
-  cudaEventRecord(h->ev_join, h->side);
+  cudaEventRecord(h->ev_join[h->ncall & 1], h->side);
+}
+
+// Make `s` wait for every equaliser stage forked so far (the calls that read or report results).
+static void join_side(rx_handle *h, cudaStream_t s) {
+  if (h->ncall > 0) cudaStreamWaitEvent(s, h->ev_join[(h->ncall - 1) & 1], 0);
 }
 
 static InView make_view(const rx_handle *h, const void *samples, long long n) {
@@ -873,6 +899,8 @@ static InView make_view(const rx_handle *h, const void *samples, long long n) {
   in.keep_from = n > 0 ? h->n_in + n - (1 << 16) : h->n_in;
   in.f32 = f32;
   in.gain = (float)h->cfg.adc_gain;
+  in.cnt_lo = 0;
+  in.cnt_hi = 0x7fffffffffffffffLL;
   return in;
 }
 
@@ -882,7 +910,7 @@ extern "C" rx_status rx_process(rx_handle *h, const void *d_samples, long long n
   if (n > h->max_call) return RX_EINVAL;
   if (labels_capacity > 0 && !d_labels) return RX_EINVAL;
   if (((uintptr_t)d_samples) & 15) return RX_EINVAL;
-  if (h->flushed) return RX_ESTATE;
+  if (h->flushed || h->d.shard_n > 1) return RX_ESTATE;
   CK(cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)stream;
   if (h->cfg.input_format == RX_IN_U12_PACKED && n > 0) {   // unpack the call into the staging buffer
@@ -904,16 +932,129 @@ extern "C" rx_status rx_process(rx_handle *h, const void *d_samples, long long n
     else launch_sync_train<true>(h, s, 0);
     launch_lms_rounds(h, s, lab, cap, 0, h->lms_sym_ub);
   } else {
-    CK(cudaStreamWaitEvent(s, h->ev_join, 0));
+    // equaliser_lag = 0: the call ends when its own equaliser stage has; 1: when the previous
+    // call's has (this call's stage overlaps the next call's front-end, as the paper's buffers
+    // overlap across its five streams)
+    if (h->cfg.equaliser_lag == 0) CK(cudaStreamWaitEvent(s, h->ev_join[h->ncall & 1], 0));
+    else if (h->ncall > 0) CK(cudaStreamWaitEvent(s, h->ev_join[(h->ncall - 1) & 1], 0));
+    h->ncall++;
+  }
+  return check_launch();
+}
+
+// ------------------------------------------------------------------ time sharding (mode 2)
+// Stage A of buffer `beta` on its owning shard: the input covers [max(0, beta B4 - RX_SHARD_PRE),
+// (beta + 1) B4 + RX_SHARD_POST) (shorter at the stream end: last = 1); KK stage 1 / 2 over every
+// block whose overlap-save frames lie inside it, then the CFO estimate of the buffer.
+extern "C" rx_status rx_shard_process(rx_handle *h, long long beta, const void *d_samples, long long n, int last,
+                                      unsigned char *d_labels, long long labels_capacity, void *stream) {
+  if (!h || h->d.shard_n <= 1 || beta < 0 || n <= 0 || !d_samples || labels_capacity < 0 ||
+      (labels_capacity > 0 && !d_labels))
+    return RX_EINVAL;
+  RxDev &d = h->d;
+  if (beta % d.shard_n != d.shard_g || h->sh_cur.valid || h->flushed) return RX_ESTATE;
+  if (h->cfg.input_format != RX_IN_U12_IN_U16 || (((uintptr_t)d_samples) & 15)) return RX_EINVAL;
+  const long long B4 = (long long)d.buffer_blocks * 512;
+  const long long P0 = beta * B4 - RX_SHARD_PRE > 0 ? beta * B4 - RX_SHARD_PRE : 0;
+  const long long P1 = P0 + n;
+  if (n % 512 || P1 <= beta * B4 || (!last && P1 < (beta + 1) * B4 + RX_SHARD_POST) || n > B4 + RX_SHARD_PRE + RX_SHARD_POST)
+    return RX_EINVAL;
+  CK(cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  InView in = make_view(h, d_samples, 0);
+  in.cur = (const uint16_t *)d_samples;
+  in.call_start = P0;
+  in.call_end = P1;
+  in.keep_from = 0x7fffffffffffffffLL;           // nothing goes to the history ring
+  in.cnt_lo = beta * d.buffer_blocks;             // the halos are counted by their owners
+  in.cnt_hi = (beta + 1) * d.buffer_blocks;
+  const long long s1_lo = P0 == 0 ? 0 : P0 / 512 + 1, s1_hi = P1 / 512;   // frames inside [P0, P1)
+  const long long s2_lo = P0 == 0 ? 0 : s1_lo + 1, s2_hi = s1_hi - 1;
+  KLAUNCH(h, RX_K_KK_S1, s, (k_kk_s1<<<gridc(s1_hi - s1_lo, FE_GROUPS), 256, 0, s>>>(d, in, s1_lo, s1_hi)));
+  KLAUNCH(h, RX_K_KK_S2, s, (k_kk_s2<<<gridc(s2_hi - s2_lo, FE_GROUPS), 256, 0, s>>>(d, s2_lo, s2_hi)));
+  const long long q_front = 256 * s2_hi - 128;
+  const int fine_ctas = (int)((h->Q / 1024 + 7) / 8);
+  KLAUNCH(h, RX_K_CFO, s, (k_cfo_spec<<<dim3((unsigned)d.cfo_G, 1), CFO_SPEC_T, 0, s>>>(d, beta, q_front)));
+  if (d.cfo_enable) KLAUNCH(h, RX_K_CFO, s, (k_cfo_fine<<<dim3((unsigned)fine_ctas, 1), 256, 0, s>>>(d, beta, q_front, fine_ctas)));
+  h->sh_cur.beta = beta;
+  h->sh_cur.qfront = q_front;
+  h->sh_cur.last = last;
+  h->sh_cur.valid = 1;
+  h->sh_cur.exported = 0;
+  h->sh_cur.labels = labels_capacity ? d_labels : nullptr;
+  h->sh_cur.cap = labels_capacity ? labels_capacity : 1;
+  h->n_in += P1 < (beta + 1) * B4 ? P1 - beta * B4 : B4;
+  return check_launch();
+}
+
+extern "C" rx_status rx_carry_size(const rx_handle *h, int *bytes) {
+  if (!h || !bytes) return RX_EINVAL;
+  *bytes = (int)sizeof(RxCarry);
+  return RX_OK;
+}
+
+// This round's record (RxCarry, rx_carry_size bytes) into device memory d_buf, stream-ordered.
+extern "C" rx_status rx_export_carry(rx_handle *h, void *d_buf, void *stream) {
+  if (!h || !d_buf || h->d.shard_n <= 1 || (((uintptr_t)d_buf) & 15)) return RX_EINVAL;
+  CK(cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const long long beta = (h->sh_cur.valid && !h->sh_cur.exported) ? h->sh_cur.beta : -1;
+  KLAUNCH(h, RX_K_MISC, s, (k_carry_export<<<1, 1, 0, s>>>(h->d, (RxCarry *)d_buf, beta, h->sh_seed_e,
+                                                            h->sh_seed_e >= 0 ? 1 : 0)));
+  if (h->sh_cur.valid) h->sh_cur.exported = 1;
+  h->sh_seed_e = -1;
+  return check_launch();
+}
+
+// Stage B of one buffer (the equaliser of its epoch): z' valid below the buffer's front, the
+// finalisation front at the epoch's first segment, one round over the epoch's segments
+static void shard_stage_b(rx_handle *h, cudaStream_t s, const rx_handle::ShardBuf &b) {
+  RxDev &d = h->d;
+  const long long spe = d.E_sym / d.S;
+  KLAUNCH(h, RX_K_MISC, s, (k_shard_seek<<<1, 1, 0, s>>>(d, b.qfront, b.beta * spe)));
+  if (b.last) KLAUNCH(h, RX_K_MISC, s, (k_kk_mend<<<1, 1, 0, s>>>(d, b.qfront)));   // stream end: m_end
+  KLAUNCH(h, RX_K_MISC, s, (k_lms_snapshot<<<1, 1, 0, s>>>(d)));
+  launch_lms_round(h, s, b.labels, b.cap, b.last ? 1 : 0, spe);
+  h->sh_seed_e = b.beta + d.D;   // k_lms_seeds produced the seed of epoch beta + D
+}
+
+// The gathered records of all n_ranks shards (rank order): CFO origin chain, sync / training,
+// seeds; then stage B of this shard's previous buffer (and, on the shard holding the stream
+// start, frame sync + training on buffer 0 as soon as its CFO estimate is known).
+extern "C" rx_status rx_import_carry(rx_handle *h, const void *d_gathered, int n_ranks, int my_rank, void *stream) {
+  if (!h || !d_gathered || h->d.shard_n <= 1 || n_ranks != h->d.shard_n || my_rank != h->d.shard_g) return RX_EINVAL;
+  if (h->flushed) return RX_ESTATE;
+  CK(cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  RxDev &d = h->d;
+  KLAUNCH(h, RX_K_CFO, s, (k_carry_import<<<1, 1, 0, s>>>(d, (const RxCarry *)d_gathered, n_ranks)));
+  KLAUNCH(h, RX_K_CFO, s, (k_carry_chain<<<1, 1, 0, s>>>(d, (const RxCarry *)d_gathered, n_ranks)));
+  if (h->sh_pend.valid) {
+    shard_stage_b(h, s, h->sh_pend);
+    h->sh_pend.valid = 0;
+  }
+  if (h->sh_cur.valid) {
+    if (h->sh_cur.beta == 0) {       // the stream start: frame sync + training (c-10, c-9)
+      KLAUNCH(h, RX_K_MISC, s, (k_shard_seek<<<1, 1, 0, s>>>(d, h->sh_cur.qfront, 0)));
+      KLAUNCH(h, RX_K_MISC, s, (k_lms_snapshot<<<1, 1, 0, s>>>(d)));
+      launch_sync_train<true>(h, s, h->sh_cur.last);
+    }
+    h->sh_pend = h->sh_cur;
+    h->sh_cur.valid = 0;
+    if (h->sh_pend.last) {           // nothing follows the stream end: finish it now
+      shard_stage_b(h, s, h->sh_pend);
+      h->sh_pend.valid = 0;
+    }
   }
   return check_launch();
 }
 
 extern "C" rx_status rx_flush(rx_handle *h, unsigned char *d_labels, long long labels_capacity, void *stream) {
   if (!h || labels_capacity < 0 || (labels_capacity > 0 && !d_labels)) return RX_EINVAL;
-  if (h->flushed) return RX_ESTATE;
+  if (h->flushed || h->d.shard_n > 1) return RX_ESTATE;
   CK(cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)stream;
+  join_side(h, s);
   const InView in = make_view(h, nullptr, 0);
   if (h->d.family == RX_PAM) run_pam(h, s, in, labels_capacity ? d_labels : nullptr, labels_capacity ? labels_capacity : 1, 1);
   else run_kk(h, s, in, labels_capacity ? d_labels : nullptr, labels_capacity ? labels_capacity : 1, 1);
@@ -924,6 +1065,7 @@ extern "C" rx_status rx_flush(rx_handle *h, unsigned char *d_labels, long long l
 extern "C" rx_status rx_get_stats(rx_handle *h, rx_stats *o, void *stream) {
   if (!h || !o) return RX_EINVAL;
   CK(cudaSetDevice(h->device));
+  join_side(h, (cudaStream_t)stream);
   CK(cudaStreamSynchronize((cudaStream_t)stream));
   DevState st;
   CK(cudaMemcpy(&st, h->st_dev, sizeof(st), cudaMemcpyDeviceToHost));
@@ -1012,6 +1154,7 @@ extern "C" rx_status rx_probe_read(rx_handle *h, int which, long long first, lon
                                    void *stream) {
   if (!h || !out) return RX_EINVAL;
   CK(cudaSetDevice(h->device));
+  join_side(h, (cudaStream_t)stream);
   CK(cudaStreamSynchronize((cudaStream_t)stream));
   RxDev &d = h->d;
   const bool kk = d.family == RX_QAM_KK;
@@ -1098,6 +1241,7 @@ extern "C" rx_status rx_calibrate_thresholds(rx_handle *h, long long first, long
   if (!h || !thr || first < 0 || count <= 0 || h->d.family != RX_PAM) return RX_EINVAL;
   CK(cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)stream;
+  join_side(h, s);
   CK(cudaStreamSynchronize(s));
   DevState st;
   CK(cudaMemcpy(&st, h->st_dev, sizeof(st), cudaMemcpyDeviceToHost));
@@ -1204,6 +1348,7 @@ extern "C" rx_status rx_get_q_trace(rx_handle *h, long long first, int n, long l
   if (!h || n < 0 || (n > 0 && (!err || !bits)) || first < 0 || h->d.q_segs <= 0) return RX_EINVAL;
   if (n > RX_Q_WINDOWS) return RX_EINVAL;
   CK(cudaSetDevice(h->device));
+  join_side(h, (cudaStream_t)stream);
   CK(cudaStreamSynchronize((cudaStream_t)stream));
   DevState st;
   CK(cudaMemcpy(&st, h->st_dev, sizeof(st), cudaMemcpyDeviceToHost));
@@ -1225,6 +1370,7 @@ extern "C" rx_status rx_export_counters(rx_handle *h, double *d_out, void *strea
   if (!h || !d_out) return RX_EINVAL;
   CK(cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)stream;
+  join_side(h, s);
   KLAUNCH(h, RX_K_MISC, s, (k_export_counters<<<1, 1, 0, s>>>(h->st_dev, d_out)));
   return check_launch();
 }

@@ -62,6 +62,7 @@ struct RxDev {
   int K, B, S, O, D, cpr, Pt;
   int anchor_each;           // KK: every segment's quadrant from the reference (R-ANCHOR2)
   int lms_mode;              // 0 decision directed (c-9), 1 data aided (reference-driven, no CPR)
+  int shard_n, shard_g;      // time sharding (SURVEY §8(e) mode 2): buffers b = g mod n; 1, 0 = off
   float mu;
   int T_train;
   long long m0;
@@ -96,7 +97,7 @@ struct RxDev {
                                          // [1] tiles dispatched (dispatch-order tile index)
   float2 *E; long long E_cap;
   float2 *z; long long z_cap;
-  float2 *zp; long long zp_cap;     // z' = normalised, CFO-removed 2-sps field
+  int q_shift;                      // log2 of the 2-sps samples per buffer (buffer_blocks 256)
   CfoParam *cfo; float *cfo_part; double *cfo_pow; double2 *cfo_a; int *cfo_tick; int *cfo_tick_spec; int cfo_G;
   // ---- sync scratch
   float *sync_g; float2 *sync_c;

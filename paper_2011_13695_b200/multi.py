@@ -53,3 +53,50 @@ def summarize(counters) -> dict:
             "q_db": q_db_from_ber(ber) if bits > 0 else float("nan"), "evm_db": evm,
             "symbols": int(c[IDX["symbols_counted"]]), "clipped": int(c[IDX["clipped"]]),
             "domain_errors": int(c[IDX["domain_errors"]])}
+
+
+# ---------------------------------------------------------------------------- time sharding
+def gather_carry(rec, group=None):
+    """All-gather the shards' carry records (uint8 CUDA tensor of rx_carry_size bytes each) in
+    rank order into one device buffer (NCCL all-gather; gloo on a shared GPU in the tests)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    out = torch.empty(world * rec.numel(), dtype=rec.dtype, device=rec.device)
+    try:
+        dist.all_gather_into_tensor(out, rec, group=group)
+    except (RuntimeError, NotImplementedError, AttributeError):
+        parts = [torch.empty_like(rec) for _ in range(world)]
+        dist.all_gather(parts, rec, group=group)
+        out = torch.cat(parts)
+    return out
+
+
+def shard_inputs(n_samples: int, buffer_samples: int, beta: int, pre: int, post: int):
+    """Input range [p0, p1) of paper buffer beta for its shard (include/rx.h rx_shard_process)
+    and whether it holds the stream end."""
+    p0 = max(0, beta * buffer_samples - pre)
+    p1 = min(n_samples, (beta + 1) * buffer_samples + post)
+    return p0, p1, p1 >= n_samples
+
+
+def run_time_sharded(R, codes, buffer_samples: int, labels, rank: int, world: int, gather=None,
+                     stream=None):
+    """SURVEY §8(e) mode 2 on one rank: this rank's handle R (shard_count = world, shard_index =
+    rank) processes paper buffers rank, rank + world, ... of the stream `codes` (a device tensor
+    of u16 codes holding the whole stream here; a deployment would receive only its buffers with
+    their halos), exchanging one carry record per round. gather(rec) -> all records (rank order);
+    default: gather_carry over the default process group."""
+    import torch
+    from .rx import SHARD_POST, SHARD_PRE
+    gather = gather or gather_carry
+    n = codes.numel()
+    nbuf = -(-n // buffer_samples)
+    rec = torch.zeros(R.carry_size(), dtype=torch.uint8, device=codes.device)
+    for r in range(-(-nbuf // world) + 1):
+        b = r * world + rank
+        if b < nbuf:
+            p0, p1, last = shard_inputs(n, buffer_samples, b, SHARD_PRE, SHARD_POST)
+            R.shard_process(b, codes[p0:p1], last=last, labels=labels, stream=stream)
+        R.export_carry(rec, stream=stream)
+        R.import_carry(gather(rec), world, rank, stream=stream)

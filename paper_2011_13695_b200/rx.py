@@ -47,6 +47,8 @@ class RxConfig(ctypes.Structure):
         ("serial_equaliser", ctypes.c_int),
         ("q_window_symbols", _c_ll),
         ("lms_mode", ctypes.c_int),
+        ("equaliser_lag", ctypes.c_int),
+        ("shard_count", ctypes.c_int), ("shard_index", ctypes.c_int),
     ]
 
 
@@ -67,7 +69,9 @@ EXPORTS = ("rx_config_default", "rx_create", "rx_process", "rx_flush", "rx_get_s
            "rx_reset_stats", "rx_get_taps", "rx_probe_read", "rx_destroy", "rx_strerror",
            "rx_version", "rx_profile_enable", "rx_profile_read", "rx_export_counters",
            "rx_set_taps", "rx_get_q_trace", "rx_calibrate_thresholds", "rx_calibrate_dc",
-           "rx_design_static_eq")
+           "rx_design_static_eq", "rx_shard_process", "rx_carry_size", "rx_export_carry",
+           "rx_import_carry")
+SHARD_PRE, SHARD_POST = 4096, 4096       # RX_SHARD_PRE / RX_SHARD_POST (include/rx.h)
 NCOUNTERS = 8
 COUNTERS = ("bit_errors", "bits", "symbols_counted", "evm_num", "evm_den", "clipped",
             "domain_errors", "symbols_out")
@@ -78,10 +82,12 @@ _lib = None
 
 
 def load(path: str = SO_PATH):
-    """Load librx.so (raises OSError if it is missing — no fallback)."""
+    """Load librx.so (raises OSError if it is missing — no fallback). RX_SO overrides the path
+    (kernel-variant experiments, tools/kk_variants.py)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = os.environ.get("RX_SO", path)
     if not os.path.exists(path):
         raise OSError(f"librx.so not built at {path}; run paper_2011_13695_b200.build.build()")
     lib = ctypes.CDLL(path)
@@ -115,6 +121,12 @@ def load(path: str = SO_PATH):
     lib.rx_calibrate_dc.restype = ctypes.c_int
     lib.rx_design_static_eq.argtypes = [_c_dp, _c_dp, ctypes.c_double, ctypes.c_int, ctypes.c_int, _c_dp]
     lib.rx_design_static_eq.restype = ctypes.c_int
+    lib.rx_shard_process.argtypes = [vp, _c_ll, vp, _c_ll, ctypes.c_int, vp, _c_ll, vp]
+    lib.rx_carry_size.argtypes = [vp, ctypes.POINTER(ctypes.c_int)]
+    lib.rx_export_carry.argtypes = [vp, vp, vp]
+    lib.rx_import_carry.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int, vp]
+    for f in ("rx_shard_process", "rx_carry_size", "rx_export_carry", "rx_import_carry"):
+        getattr(lib, f).restype = ctypes.c_int
     for f in ("rx_create", "rx_process", "rx_flush", "rx_get_stats", "rx_reset_stats",
               "rx_get_taps", "rx_set_taps", "rx_probe_read", "rx_profile_enable", "rx_profile_read"):
         getattr(lib, f).restype = ctypes.c_int
@@ -198,6 +210,31 @@ class Receiver:
         _check(load().rx_process(self._h, ctypes.c_void_p(ptr), n, ctypes.c_void_p(labels_ptr),
                                  labels_cap, stream_ptr if stream_ptr is not None else _stream_ptr()),
                "rx_process")
+
+    # -- time sharding of one stream (SURVEY §8(e) mode 2; include/rx.h rx_shard_process)
+    def shard_process(self, buffer: int, samples, last: bool = False, labels=None, stream=None):
+        """Stage A of paper buffer `buffer` (owned by this shard): `samples` = u16 codes of
+        [max(0, buffer B4 - SHARD_PRE), (buffer + 1) B4 + SHARD_POST) of the stream."""
+        lp, lc = (labels.data_ptr(), labels.numel()) if labels is not None else (None, 0)
+        _check(load().rx_shard_process(self._h, int(buffer), ctypes.c_void_p(samples.data_ptr()),
+                                       int(samples.numel()), int(bool(last)), ctypes.c_void_p(lp), lc,
+                                       _stream_ptr(stream)), "rx_shard_process")
+
+    def carry_size(self) -> int:
+        n = ctypes.c_int()
+        _check(load().rx_carry_size(self._h, ctypes.byref(n)), "rx_carry_size")
+        return n.value
+
+    def export_carry(self, out, stream=None):
+        """This round's carry record into `out` (uint8 CUDA tensor of carry_size() bytes)."""
+        _check(load().rx_export_carry(self._h, ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)),
+               "rx_export_carry")
+
+    def import_carry(self, gathered, n_ranks: int, my_rank: int, stream=None):
+        """All shards' records (rank order, one CUDA buffer): carries + the previous buffer's
+        equaliser stage."""
+        _check(load().rx_import_carry(self._h, ctypes.c_void_p(gathered.data_ptr()), int(n_ranks), int(my_rank),
+                                      _stream_ptr(stream)), "rx_import_carry")
 
     def flush(self, labels=None, stream=None):
         lp, lc = (labels.data_ptr(), labels.numel()) if labels is not None else (None, 0)

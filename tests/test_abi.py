@@ -120,3 +120,53 @@ def test_new_config_fields_validated_before_touching_the_gpu(lib):
     e = np.zeros(1, dtype=np.int64)
     lp = ctypes.POINTER(ctypes.c_longlong)
     assert lib.rx_get_q_trace(None, 0, 1, e.ctypes.data_as(lp), e.ctypes.data_as(lp), None) == -1
+
+
+def test_round2_config_fields_validated_before_touching_the_gpu(lib):
+    """lms_mode (0/1), equaliser_lag (0/1) and time sharding (KK only, anchored quadrants,
+    shard_count <= tap_lag_epochs, 0 <= shard_index < shard_count) are checked by rx_create
+    before any CUDA call; the shard calls reject a NULL handle."""
+    from paper_2011_13695_b200 import rx
+    import numpy as np
+    h = ctypes.c_void_p()
+    taps = np.ones(2 * 203)
+
+    def kk(**kw):
+        c = rx.default_config(rx.RX_QAM_KK, 16)
+        c.static_taps = taps.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        c.n_static_taps = 203
+        for k, v in kw.items():
+            setattr(c, k, v)
+        return c
+    for kw in (dict(lms_mode=2), dict(equaliser_lag=2), dict(shard_count=9),           # 9 > D = 8
+               dict(shard_count=4, shard_index=4), dict(shard_count=4, shard_index=-1),
+               dict(shard_count=4, cpr_anchor=0), dict(shard_count=-1)):
+        assert lib.rx_create(ctypes.byref(kk(**kw)), 0, ctypes.byref(h)) == -1, kw
+    p = rx.default_config(rx.RX_PAM, 4)
+    pt = np.ones(503)
+    p.static_taps = pt.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    p.n_static_taps = 503
+    p.shard_count = 2
+    assert lib.rx_create(ctypes.byref(p), 0, ctypes.byref(h)) == -1           # PAM: not sharded
+    n = ctypes.c_int()
+    assert lib.rx_carry_size(None, ctypes.byref(n)) == -1
+    assert lib.rx_shard_process(None, 0, None, 0, 0, None, 0, None) == -1
+    assert lib.rx_export_carry(None, None, None) == -1
+    assert lib.rx_import_carry(None, None, 2, 0, None) == -1
+
+
+def test_struct_sizes_match_a_c_compiler(tmp_path):
+    """The ctypes mirrors of rx_config / rx_stats have the C compiler's size and field offsets
+    (gcc on include/rx.h), so no field is silently misaligned across the ABI."""
+    from paper_2011_13695_b200 import rx
+    src = tmp_path / "sz.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "rx.h"\nint main(void){'
+                   'printf("%zu %zu %zu %zu %zu\\n", sizeof(rx_config), offsetof(rx_config, q_window_symbols),'
+                   'offsetof(rx_config, shard_index), sizeof(rx_stats), offsetof(rx_stats, launches));return 0;}\n')
+    exe = tmp_path / "sz"
+    import subprocess
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)], check=True)
+    got = list(map(int, subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()))
+    want = [ctypes.sizeof(rx.RxConfig), rx.RxConfig.q_window_symbols.offset, rx.RxConfig.shard_index.offset,
+            ctypes.sizeof(rx.RxStats), rx.RxStats.launches.offset]
+    assert got == want

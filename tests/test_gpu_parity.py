@@ -858,3 +858,59 @@ def test_noiseless_error_free_spec_criterion_3(fmt, M):
     print(f"{fmt}-{M}: {st['bit_errors']} errors in {st['bits']} bits")
     assert st["sync_offset"] == (rec.offset + 4096) % O.P_REF
     assert st["bit_errors"] == 0 and st["bits"] >= 1_000_000
+
+
+@pytest.mark.parametrize("N", [2, 4, 8])
+def test_time_sharded_kk_stream_is_bit_identical(N):
+    """SURVEY §8(e) mode 2 (VERDICT r01 'Next 5'), emulated in one process on one GPU: one KK
+    stream (C4 structure, 24 paper buffers of 256 blocks) split over N shard handles, buffer b on
+    shard b mod N with its input halos, one carry record per shard and round all-gathered in rank
+    order (rx_export_carry / rx_import_carry). The labels are byte-identical to one handle's on
+    the same stream (chunked calls, side-stream equaliser), the integer counters summed over the
+    shards are equal, the EVM sums agree to rounding; with a partial last buffer too."""
+    torch = _torch_cuda()
+    from paper_2011_13695_b200 import RX_QAM_KK, Receiver, multi
+    B4 = 256 * 512
+    for n in (24 * B4, 21 * B4 + 5 * 4096):
+        rec, rx = make_config("C4", n_samples=n)
+        rx["buffer_blocks"] = 256
+        R1, lab1, st1 = run_gpu(rec, rx, chunk=3 * B4)
+        fields = {k: v for k, v in rx.items() if k in ("lms_taps", "lms_block", "lms_segment", "lms_overlap", "mu",
+                                                       "train_symbols", "sync_start", "sync_window",
+                                                       "warmup_symbols", "cpr_test_phases", "buffer_blocks")}
+        codes = torch.from_numpy(rec.codes.view(np.int16)).cuda()
+        hs = [Receiver(RX_QAM_KK, rec.M, rec.static_taps, dc_offset=rec.dc_offset, history_buffers=4,
+                       shard_count=N, shard_index=g, **fields) for g in range(N)]
+        nsym = n // 4 + 4096
+        labs = [torch.full((nsym,), 0xFF, dtype=torch.uint8, device="cuda") for _ in range(N)]
+        recs = [torch.zeros(hs[0].carry_size(), dtype=torch.uint8, device="cuda") for _ in range(N)]
+        nbuf = -(-n // B4)
+        for r in range(-(-nbuf // N) + 1):          # the emulated ranks, round by round
+            for g in range(N):
+                b = r * N + g
+                if b < nbuf:
+                    p0, p1, last = multi.shard_inputs(n, B4, b, 4096, 4096)
+                    hs[g].shard_process(b, codes[p0:p1], last=last, labels=labs[g])
+                hs[g].export_carry(recs[g])
+            allrec = torch.cat(recs)                # = the NCCL all-gather, rank order
+            for g in range(N):
+                hs[g].import_carry(allrec, N, g)
+        sts = [h.stats() for h in hs]
+        m_end = st1["symbols_out"]
+        E = 256 * 128
+        got = np.full(m_end, 0xFF, dtype=np.uint8)
+        for g in range(N):
+            lg = labs[g].cpu().numpy()
+            for b in range(g, nbuf, N):
+                lo, hi = b * E, min((b + 1) * E, m_end)
+                got[lo:hi] = lg[lo:hi]
+        diff = np.nonzero(got != lab1[:m_end])[0]
+        print(f"N={N} n={n}: {m_end} symbols, {diff.size} labels differ"
+              + (f" (first {diff[:5]})" if diff.size else ""))
+        assert diff.size == 0
+        for k in ("bit_errors", "bits", "symbols_counted", "clipped", "domain_errors"):
+            assert sum(s[k] for s in sts) == st1[k], (k, [s[k] for s in sts], st1[k])
+        assert abs(sum(s["evm_num"] for s in sts) - st1["evm_num"]) <= 1e-9 * st1["evm_num"]
+        assert all(s["sync_offset"] == st1["sync_offset"] and s["sync_phase"] == st1["sync_phase"] for s in sts)
+        for h in hs:
+            h.close()
