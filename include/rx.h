@@ -77,7 +77,7 @@ typedef struct {
   int sideband;               /* KK: -1 = signal below the carrier (paper set-up) */
   double dc_offset;           /* KK: static DC restoring the AC-coupled intensity, x units */
   int lms_taps;               /* K: PAM T-spaced real taps (15/31), KK T/2-spaced complex (4..32) */
-  int lms_block;              /* B symbols per tap update: 32 (only 32 is built) */
+  int lms_block;              /* B symbols per tap update: 32; 1 with lms_mode = 2 */
   int lms_segment;            /* S symbols per parallel segment: 4096; divides the epoch */
   int lms_overlap;            /* O warm-up symbols per segment (KK 256, PAM 0); multiple of B */
   int tap_lag_epochs;         /* D: seeds of epoch e are the mean canonical taps of e-D (8) */
@@ -126,7 +126,12 @@ typedef struct {
                                  with the oracle element by element (SURVEY §8(c) parity criterion
                                  'equaliser output in training mode'); a BER tester's reference-
                                  aided mode. Seeds: epoch means of the raw final taps (no R-SEED
-                                 phase normalisation: no CPR, the frame is absolute) */
+                                 phase normalisation: no CPR, the frame is absolute);
+                                 2: the paper's equaliser (KK only): a per-symbol
+                                 (lms_block = 1, lms_taps <= 8) decision-directed LMS, widely linear
+                                 per widely_linear, with NO separate CPR - the taps track the
+                                 carrier ("symbol-phase recovery" by the equaliser); one serial
+                                 recursion per segment (DESIGN reading R-DDLMS; raw-tap seeds) */
   int equaliser_lag;          /* side-stream equaliser (serial_equaliser = 0) only. 0 (default): the
                                  work an rx_process call enqueues on cuda_stream ends with its own
                                  equaliser stage; 1: with the PREVIOUS call's, so a call's equaliser

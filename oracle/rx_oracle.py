@@ -583,6 +583,9 @@ def _cpr_estimate(y, valid, slicer: _Slicer, lp: LmsParams):
     return phis[arg]
 
 
+SYM_INIT = 64              # symbols of the per-symbol DDLMS's seed rotation (DESIGN reading R-DDLMS)
+
+
 def lms_segments(v, stride, off, m_end, seeds_fn, slicer: _Slicer, lp: LmsParams,
                  real: bool, segs, ref_val_fn=None):
     """Run segments ``segs`` of the segmented DD block-LMS (c-9 'Per block j'), in lockstep
@@ -611,6 +614,19 @@ def lms_segments(v, stride, off, m_end, seeds_fn, slicer: _Slicer, lp: LmsParams
     theta = np.zeros(ns)
     diverged = False
     L = slicer.L
+    # per-symbol DDLMS without CPR (lms_mode 2, DESIGN reading R-DDLMS): its taps carry the carrier
+    # phase, which a seed from D epochs back does not know, so each segment adapts on the known
+    # reference during its O warm-up symbols (e = r - y, as the training pass and the quadrant
+    # anchoring of R-ANCHOR2 use it) and decision-directed on its own output symbols
+    ref_warm = lp.cpr == "none" and not real and not lp.data_aided and lp.B == 1
+    if ref_warm:
+        # ... and starts from its seed rotated onto the reference: theta_0 = arg sum_m y_m conj(r_m)
+        # over its first SYM_INIT symbols (y from the seed taps), w <- w e^{j theta_0}
+        m = t0[:, None] + np.arange(SYM_INIT)[None, :]
+        ok = m < s_hi[:, None]
+        y0 = np.einsum("sbk,sk->sb", tap_matrix(v, m, stride, off, K), np.conj(W))
+        c0 = np.sum(np.where(ok, y0 * np.conj(ref_val_fn(np.minimum(m, m_end - 1))), 0.0), axis=1)
+        W = W * np.exp(1j * np.angle(c0))[:, None]
     out_idx = [[] for _ in range(ns)]
     out_z = [[] for _ in range(ns)]
     out_m = [[] for _ in range(ns)]
@@ -638,6 +654,8 @@ def lms_segments(v, stride, off, m_end, seeds_fn, slicer: _Slicer, lp: LmsParams
         d = slicer.value(idx)
         if lp.data_aided:
             e = ref_val_fn(m) - y                              # c-9 'Training' error
+        elif ref_warm:
+            e = np.where(m < s_lo[:, None], ref_val_fn(np.minimum(m, m_end - 1)) - y, d - zp)
         else:
             e = d - zp
             if lp.cpr != "none":
@@ -864,7 +882,8 @@ class RxParams:
     tap_lag_epochs: int = 8
     widely_linear: bool = False
     cpr_anchor: int = 1        # QAM: 1 = every segment anchored to the reference, 0 = c-9 chain
-    lms_mode: int = 0          # 0 = decision directed (c-9), 1 = data aided (DESIGN reading R-DA)
+    lms_mode: int = 0          # 0 = decision directed (c-9), 1 = data aided (DESIGN reading R-DA),
+                               # 2 = per-symbol DDLMS without CPR (lms_block = 1; DESIGN R-DDLMS)
     mu: float = 1e-3
     train_symbols: int = 8192
     cpr_test_phases: int = 0
@@ -883,6 +902,11 @@ def _lms_params(p: RxParams) -> LmsParams:
     else:
         E = p.buffer_blocks * 128
         cpr = "vv" if p.cpr_test_phases == 0 else "bps"
+    if p.lms_mode == 2:
+        # the paper's equaliser (DESIGN reading R-DDLMS): per-symbol
+        # (B = 1) decision-directed LMS, widely linear per rx_config, with no separate CPR - the
+        # taps track the carrier phase ("symbol-phase recovery ... performed by the equalizer")
+        cpr = "none"
     return LmsParams(K=p.lms_taps, B=p.lms_block, S=p.lms_segment, O=p.lms_overlap, mu=p.mu,
                      T_train=p.train_symbols, D=p.tap_lag_epochs, E=E, cpr=cpr,
                      P_t=max(p.cpr_test_phases, 1), widely_linear=p.widely_linear,

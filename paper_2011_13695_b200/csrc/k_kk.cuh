@@ -189,6 +189,7 @@ __device__ __forceinline__ void buf_range(const RxDev &d, long long beta, long l
 // (CFO_SPEC_T threads, each owning the bins k = t + CFO_SPEC_T i)
 #define CFO_SPEC_T 256
 #define CFO_ROWS 128           // spectrum rows (CTAs) per buffer
+#define CFO_GRP 8              // rows summed per group in the two-level row reduction
 #define CFO_KPT (1024 / CFO_SPEC_T)
 __device__ __forceinline__ void cfo_final_block(const RxDev &d, long long beta, long long qfront, long long rb, int nrows) {
   __shared__ double Sd[1024];
@@ -317,7 +318,7 @@ __global__ void __launch_bounds__(CFO_SPEC_T, 4) k_cfo_spec(RxDev d, long long b
     accs[g * 1024 + j + 64 * r + 512] = acc[8 + r];
   }
   __syncthreads();
-  const long long row = (long long)blockIdx.y * gridDim.x + blockIdx.x;
+  const long long row = (long long)blockIdx.y * d.cfo_G + blockIdx.x;   // CFO_ROWS rows + group rows per buffer
 #pragma unroll
   for (int i = 0; i < CFO_KPT; ++i) {
     const int k = threadIdx.x + CFO_SPEC_T * i;
@@ -334,16 +335,44 @@ __global__ void __launch_bounds__(CFO_SPEC_T, 4) k_cfo_spec(RxDev d, long long b
     for (int i = 0; i < CFO_SPEC_T / 32; ++i) t += red[i];
     d.cfo_pow[row] = t;
   }
-  // the last CTA of this buffer reduces its rows (formerly the separate k_cfo_final launch)
+  // two-level fixed-order reduction of the rows: the last CTA of each group of CFO_GRP rows sums
+  // them (row order) into a group row, the last group finisher reduces the group rows (group
+  // order) and takes the argmax / interpolation / power (cfo_final_block)
   __shared__ int ticket;
+  const int ngrp = CFO_ROWS / CFO_GRP, grp = blockIdx.x / CFO_GRP;
+  int *tick = d.cfo_tick_spec + blockIdx.y * (ngrp + 1);
+  const long long rb = (long long)blockIdx.y * d.cfo_G;        // this buffer's rows
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) ticket = atomicAdd(&d.cfo_tick_spec[blockIdx.y], 1);
+  if (threadIdx.x == 0) ticket = atomicAdd(tick + grp, 1);
   __syncthreads();
-  if (ticket != (int)gridDim.x - 1) return;
+  if (ticket != CFO_GRP - 1) return;
   __threadfence();
-  cfo_final_block(d, beta0 + blockIdx.y, qfront, (long long)blockIdx.y * gridDim.x, (int)gridDim.x);
-  if (threadIdx.x == 0) d.cfo_tick_spec[blockIdx.y] = 0;
+#pragma unroll
+  for (int i = 0; i < CFO_KPT; ++i) {
+    const int k = threadIdx.x + CFO_SPEC_T * i;
+    float v[CFO_GRP];
+#pragma unroll
+    for (int r = 0; r < CFO_GRP; ++r) v[r] = __ldcg(d.cfo_part + (rb + grp * CFO_GRP + r) * 1024 + k);
+    float sk = 0.f;
+#pragma unroll
+    for (int r = 0; r < CFO_GRP; ++r) sk += v[r];
+    d.cfo_part[(rb + CFO_ROWS + grp) * 1024 + k] = sk;
+  }
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int r = 0; r < CFO_GRP; ++r) t += __ldcg(d.cfo_pow + rb + grp * CFO_GRP + r);
+    d.cfo_pow[rb + CFO_ROWS + grp] = t;
+    tick[grp] = 0;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) ticket = atomicAdd(tick + ngrp, 1);
+  __syncthreads();
+  if (ticket != ngrp - 1) return;
+  __threadfence();
+  cfo_final_block(d, beta0 + blockIdx.y, qfront, rb + CFO_ROWS, ngrp);
+  if (threadIdx.x == 0) tick[ngrp] = 0;
 }
 
 
@@ -455,6 +484,40 @@ __device__ __forceinline__ float2 zp_rotate(const RxDev &d, float2 v, long long 
   v = cscale(v, c.s);
   if (d.cfo_enable) v = cmul(v, dds_rot_neg_fast(c.origin + (unsigned long long)(q - (beta << d.q_shift)) * c.inc));
   return v;
+}
+// Equaliser staging: a lane stages the samples q, q + 64, q + 128, ... (one per block); its z'
+// rotation advances by the exact-phase-word step e^{-j psi'(64 inc)} (one complex multiply) and is
+// re-anchored on the exact 64-bit phase word every ZP_REANCHOR samples and at every buffer change
+// (fp32 drift <= ZP_REANCHOR x ~1e-7 rad)
+#define ZP_REANCHOR 32
+struct ZpStep {
+  long long beta;
+  float2 rot, step;                // includes 1 / sqrt(P_beta)
+  int age;
+};
+__device__ __forceinline__ float2 zp_step(const RxDev &d, float2 v, long long q, ZpStep &z) {
+  const long long beta = q >> d.q_shift;
+  if (beta != z.beta || z.age >= ZP_REANCHOR) {
+    const CfoParam &cp = d.cfo[rmod(beta, d.buf_cap)];
+    const float s = cp.inv_sqrtP;
+    if (d.cfo_enable) {
+      z.rot = cscale(dds_rot_neg_fast(cp.origin + (unsigned long long)(q - (beta << d.q_shift)) * cp.inc), s);
+      z.step = dds_rot_neg_fast(64ULL * cp.inc);
+    } else {
+      z.rot = make_float2(s, 0.f);
+      z.step = make_float2(1.f, 0.f);
+    }
+    z.beta = beta;
+    z.age = 0;
+  }
+  const float2 out = cmul(v, z.rot);
+  z.rot = cmul(z.rot, z.step);
+  ++z.age;
+  return out;
+}
+__device__ __forceinline__ float2 zp_rotate_or_zero(const RxDev &d, float2 v, long long q, long long vend, ZpCache &c) {
+  if (q < 0 || q >= vend) return make_float2(0.f, 0.f);
+  return zp_rotate(d, v, q, c);
 }
 __device__ __forceinline__ float2 zp_value(const RxDev &d, long long q, long long vend, ZpCache &c) {
   if (q < 0 || q >= vend) return make_float2(0.f, 0.f);

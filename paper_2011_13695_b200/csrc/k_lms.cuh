@@ -221,29 +221,49 @@ __device__ __forceinline__ void bps_acc(float2 yi, float2 r, float cst, float Lm
   acc = fmaf(ex, ex, acc);
   acc = fmaf(ey, ey, acc);
 }
-__device__ __forceinline__ void bps_partial(const float2 *ys, int i0, int i1, float2 rsA, float2 rsB, int L,
-                                            bool two, float &dA, float &dB) {
+template <bool TWO>
+__device__ __forceinline__ void bps_partial_t(const float2 *ys, int i0, int i1, float2 rsA, float2 rsB, int L,
+                                              float &dA, float &dB) {
   const float cst = 0.5f * (float)(L - 1), Lm1 = (float)(L - 1);
   float a0 = 0.f, a1 = 0.f, b0 = 0.f, b1 = 0.f;
   const float4 *y4 = reinterpret_cast<const float4 *>(ys);
-  const int n2 = (i1 - i0) >> 1;     // i0 even
-#pragma unroll 4
-  for (int i = 0; i < n2; ++i) {
-    const float4 yy = y4[(i0 >> 1) + i];
-    bps_acc(make_float2(yy.x, yy.y), rsA, cst, Lm1, a0);
-    bps_acc(make_float2(yy.z, yy.w), rsA, cst, Lm1, a1);
-    if (two) {
-      bps_acc(make_float2(yy.x, yy.y), rsB, cst, Lm1, b0);
-      bps_acc(make_float2(yy.z, yy.w), rsB, cst, Lm1, b1);
+  if (i0 == 0 && i1 == 32) {         // a full block (the common case): straight-line code
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float4 yy = y4[i];
+      bps_acc(make_float2(yy.x, yy.y), rsA, cst, Lm1, a0);
+      bps_acc(make_float2(yy.z, yy.w), rsA, cst, Lm1, a1);
+      if (TWO) {
+        bps_acc(make_float2(yy.x, yy.y), rsB, cst, Lm1, b0);
+        bps_acc(make_float2(yy.z, yy.w), rsB, cst, Lm1, b1);
+      }
     }
-  }
-  if ((i1 - i0) & 1) {
-    const float2 yi = ys[i1 - 1];
-    bps_acc(yi, rsA, cst, Lm1, a0);
-    if (two) bps_acc(yi, rsB, cst, Lm1, b0);
+  } else {
+    const int n2 = (i1 - i0) >> 1;   // i0 even
+#pragma unroll 4
+    for (int i = 0; i < n2; ++i) {
+      const float4 yy = y4[(i0 >> 1) + i];
+      bps_acc(make_float2(yy.x, yy.y), rsA, cst, Lm1, a0);
+      bps_acc(make_float2(yy.z, yy.w), rsA, cst, Lm1, a1);
+      if (TWO) {
+        bps_acc(make_float2(yy.x, yy.y), rsB, cst, Lm1, b0);
+        bps_acc(make_float2(yy.z, yy.w), rsB, cst, Lm1, b1);
+      }
+    }
+    if ((i1 - i0) & 1) {
+      const float2 yi = ys[i1 - 1];
+      bps_acc(yi, rsA, cst, Lm1, a0);
+      if (TWO) bps_acc(yi, rsB, cst, Lm1, b0);
+    }
   }
   dA += a0 + a1;
   dB += b0 + b1;
+}
+// (the summation order is the same on both paths: even / odd symbol chains, then their sum)
+__device__ __forceinline__ void bps_partial(const float2 *ys, int i0, int i1, float2 rsA, float2 rsB, int L,
+                                            bool two, float &dA, float &dB) {
+  if (two) bps_partial_t<true>(ys, i0, i1, rsA, rsB, L, dA, dB);
+  else bps_partial_t<false>(ys, i0, i1, rsA, rsB, L, dA, dB);
 }
 __device__ __forceinline__ void named_bar(int id) {   // the 64 threads of a segment's warp pair
   asm volatile("bar.sync %0, 64;\n" ::"r"(id) : "memory");
@@ -369,6 +389,8 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
   const int gbase = (int)(wb0 & (d.sym_cap - 1)), gmask = (int)(d.sym_cap - 1);
   ZpCache zc;                               // KK: CFO parameters of the buffer last staged
   zc.beta = -1;
+  ZpStep zs[2];                             // KK: per-lane z' phasors of the two staged samples
+  zs[0].beta = zs[1].beta = -1;
   lms_stage_any<CPLX>(d, sm, wb0, wb0 + WLa, vend, wb0, vec, &zc);
   cp_async_commit();
 #pragma unroll 1
@@ -655,7 +677,7 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
     } else if (jn < nblk) {
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
-        const float2 v = (zq[u] >= 0 && zq[u] < vend) ? zp_rotate(d, zr[u], zq[u], zc) : make_float2(0.f, 0.f);
+        const float2 v = (zq[u] >= 0 && zq[u] < vend) ? zp_step(d, zr[u], zq[u], zs[u]) : make_float2(0.f, 0.f);
         const int slot = (int)((zq[u] - wb0) & (LMS_RING - 1));
         sm.ring[slot] = v;
         sm.ring[slot + LMS_RING] = v;
@@ -847,6 +869,224 @@ __global__ void __launch_bounds__(32 * LMS_SPC) k_lms_seg(RxDev d, int flush, in
     __threadfence();
     d.seg_done[si] = (int)(s + 1);
   }
+}
+
+// ------------------------------------------------------------------ per-symbol WL DDLMS (NEXT-1)
+// The paper's KK equaliser proper: a K-tap (4 in the paper) widely-linear TD DDLMS
+// updated after EVERY symbol (B = 1), which also does the symbol-phase recovery (no separate
+// CPR; rx_config.lms_mode = 2, DESIGN reading R-DDLMS). The recursion is serial per symbol, so
+// each thread runs one segment's recursion with its taps, window and error in registers (the
+// paper's "serial in nature" kernel: few processing units, long time); the segment-parallel
+// structure of c-9 (seeds, warm-up, anchored quadrants) supplies the parallelism.
+//   y_m = sum_k conj(w_k) u_m[k] (+ conj(v_k) conj(u_m[k])),  u_m[k] = z'[2m + h* + c - k]
+//   MODE 1: d_m = slice(y_m), e_m = d_m - y_m (reference r_m - y_m on the warm-up symbols, the
+//           seed first rotated onto the reference: DESIGN reading R-DDLMS);
+//   MODE 0 (training): e_m = r_m - y_m
+//   w_k += mu u_m[k] conj(e_m);  v_k += mu conj(u_m[k]) conj(e_m)
+#define SYM_PF 8            // symbols of z prefetched ahead of the recursion (registers)
+#define SYM_INIT 64         // symbols of a DDLMS segment's seed rotation onto the reference (R-DDLMS)
+template <int KP, bool WLIN, int MODE>
+__device__ void lms_sym_run(const RxDev &d, long long t_begin, long long t_end, long long out_lo, float2 (&w)[KP],
+                            float2 (&v)[KP], unsigned char *warm, double &evn, double &evd, long long vend) {
+  const int K = d.K, c = K >> 1, h = d.st->sync_phase;
+  const float mu = d.mu;
+  const int L = d.L;
+  const float two_s = 2.0f * d.qam_sc, lvl0 = -(float)(L - 1) * d.qam_sc, inv2s = 1.0f / two_s;
+  const float Lh = 0.5f * (float)L, Lm1 = (float)(L - 1);
+  // reference index of t_begin: training (MODE 0) adapts on it throughout; DD segments (MODE 1)
+  // on their warm-up symbols m < out_lo (R-DDLMS)
+  int ri = (int)(((d.st->sync_offset + t_begin - d.m0) % RX_PREF + RX_PREF) % RX_PREF);
+  ZpCache zc;
+  zc.beta = -1;
+  // window u_{t_begin}[k] = z'[2 t_begin + h + c - k]
+  float2 U[KP];
+  const long long qb = 2 * t_begin + h + c;
+#pragma unroll
+  for (int k = 0; k < KP; ++k) U[k] = zp_value(d, qb - k, vend, zc);
+  if (MODE == 1) {
+    // the seed rotated onto the reference: c0 = sum_m y_m conj(r_m) over the first SYM_INIT
+    // symbols (y from the seed taps, v = 0), w <- w c0 / |c0| (R-DDLMS)
+    float2 c0 = make_float2(0.f, 0.f);
+    int rj = ri;
+    for (long long m = t_begin; m < t_begin + SYM_INIT && m < t_end; ++m) {
+      const long long q = 2 * m + h + c;
+      float2 y = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+        const float2 u = zp_value(d, q - k, vend, zc);
+        y.x = fmaf(w[k].x, u.x, fmaf(w[k].y, u.y, y.x));
+        y.y = fmaf(w[k].x, u.y, fmaf(-w[k].y, u.x, y.y));
+      }
+      c0 = cadd(c0, cmulc(y, __ldg(d.ref_val + rj)));
+      if (++rj == RX_PREF) rj = 0;
+    }
+    const float a = sqrtf(cabs2(c0));
+    if (a > 0.f) {
+      const float2 rot = make_float2(c0.x / a, c0.y / a);
+#pragma unroll
+      for (int k = 0; k < KP; ++k) w[k] = cmul(w[k], rot);
+    }
+  }
+  // raw z of the two samples entering at symbol m + 1 + i (i < SYM_PF), loaded SYM_PF ahead
+  float2 pf[SYM_PF][2];
+#pragma unroll
+  for (int i = 0; i < SYM_PF; ++i) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const long long q = qb + 2 * (i + 1) - 1 + e;
+      pf[i][e] = (q >= 0 && q < vend) ? d.z[rmod(q, d.z_cap)] : make_float2(0.f, 0.f);
+    }
+  }
+  float evn_f = 0.f, evd_f = 0.f;
+  const long long n = t_end - t_begin;
+  for (long long m0 = 0; m0 < n; m0 += SYM_PF) {
+#pragma unroll
+    for (int i = 0; i < SYM_PF; ++i) {
+      const long long rel = m0 + i;
+      if (rel < n) {
+        const long long m = t_begin + rel;
+        float2 y = make_float2(0.f, 0.f), y2 = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < KP; ++k) {
+          float2 &A = (k & 1) ? y2 : y;
+          A.x = fmaf(w[k].x, U[k].x, fmaf(w[k].y, U[k].y, A.x));
+          A.y = fmaf(w[k].x, U[k].y, fmaf(-w[k].y, U[k].x, A.y));
+          if (WLIN) {
+            A.x = fmaf(v[k].x, U[k].x, fmaf(-v[k].y, U[k].y, A.x));
+            A.y = fmaf(-v[k].x, U[k].y, fmaf(-v[k].y, U[k].x, A.y));
+          }
+        }
+        y = cadd(y, y2);
+        const float fI = fminf(fmaxf(floorf(fmaf(y.x, inv2s, Lh)), 0.f), Lm1);
+        const float fQ = fminf(fmaxf(floorf(fmaf(y.y, inv2s, Lh)), 0.f), Lm1);
+        const float2 dv = make_float2(fmaf(fI, two_s, lvl0), fmaf(fQ, two_s, lvl0));
+        float2 e;
+        const float2 rv = __ldg(d.ref_val + ri);
+        if (++ri == RX_PREF) ri = 0;
+        if (MODE == 0) {
+          e = csub(rv, y);
+        } else {
+          e = m < out_lo ? csub(rv, y) : csub(dv, y);       // reference-aided warm-up (R-DDLMS)
+          const int code = (int)fI | ((int)fQ << 4);
+          if (m >= out_lo) {
+            const long long ix = rmod(m, d.sym_cap);
+            d.level[ix] = (unsigned char)code;
+            d.yout[ix] = y;
+            if (m >= d.warmup) {                            // decision-referenced: e = d - y here
+              evn_f = fmaf(e.x, e.x, fmaf(e.y, e.y, evn_f));
+              evd_f = fmaf(dv.x, dv.x, fmaf(dv.y, dv.y, evd_f));
+            }
+          } else if (warm) {
+            warm[m - (out_lo - d.O)] = (unsigned char)code;
+          }
+        }
+        // w_k += mu u_k conj(e); v_k += mu conj(u_k) conj(e)
+        const float ex = mu * e.x, ey = mu * e.y;
+        float nrm = 0.f;
+#pragma unroll
+        for (int k = 0; k < KP; ++k) {
+          if (k < K) {
+            w[k].x = fmaf(U[k].x, ex, fmaf(U[k].y, ey, w[k].x));
+            w[k].y = fmaf(U[k].y, ex, fmaf(-U[k].x, ey, w[k].y));
+            if (WLIN) {
+              v[k].x = fmaf(U[k].x, ex, fmaf(-U[k].y, ey, v[k].x));
+              v[k].y = fmaf(-U[k].y, ex, fmaf(-U[k].x, ey, v[k].y));
+            }
+            nrm = fmaxf(nrm, cabs2(w[k]));
+          }
+        }
+        if (nrm > 1e6f) set_flag(d.st, RX_FLAG_DIVERGE);   // R-DIV: any tap beyond 1e3
+        // slide the window by one symbol (two T/2 samples enter) and refill the prefetch slot
+#pragma unroll
+        for (int k = KP - 1; k >= 2; --k) U[k] = U[k - 2];
+        const long long qn = qb + 2 * (rel + 1);
+        U[1] = zp_rotate_or_zero(d, pf[i][0], qn - 1, vend, zc);
+        if (KP > 0) U[0] = zp_rotate_or_zero(d, pf[i][1], qn, vend, zc);
+#pragma unroll
+        for (int e2 = 0; e2 < 2; ++e2) {
+          const long long q = qn + 2 * SYM_PF - 1 + e2;
+          pf[i][e2] = (q >= 0 && q < vend) ? d.z[rmod(q, d.z_cap)] : make_float2(0.f, 0.f);
+        }
+      }
+    }
+  }
+  evn += (double)evn_f;
+  evd += (double)evd_f;
+}
+
+template <int KP, bool WLIN>
+__global__ void __launch_bounds__(32) k_lms_train_sym(RxDev d, int flush) {
+  DevState *st = d.st;
+  if (!st->synced || st->trained || threadIdx.x != 0) return;
+  const int K = d.K, c = K >> 1;
+  const long long vend = st->v_lms;
+  const long long last = 2 * (d.m0 + d.T_train - 1) + st->sync_phase + c;
+  if (last >= vend && !flush) return;
+  float2 w[KP], v[KP];
+#pragma unroll
+  for (int k = 0; k < KP; ++k) {
+    w[k] = make_float2(k == c ? 1.f : 0.f, 0.f);                       // centre spike ...
+    if (d.has_winit) w[k] = k < K ? d.w_init[k] : make_float2(0.f, 0.f); // ... or rx_set_taps
+    v[k] = make_float2(0.f, 0.f);
+  }
+  double en = 0.0, ed = 0.0;
+  lms_sym_run<KP, WLIN, 0>(d, d.m0, d.m0 + d.T_train, 0, w, v, nullptr, en, ed, vend);
+#pragma unroll
+  for (int k = 0; k < KP; ++k) {
+    if (k < K) {
+      d.w_train[k] = w[k];
+      if (WLIN) d.v_train[k] = v[k];
+    }
+  }
+  __threadfence();
+  st->trained = 1;
+  d.hm->trained = 1;
+}
+
+// one thread per segment (32 per CTA); outputs, counters and taps as k_lms_seg's
+template <int KP, bool WLIN>
+__global__ void __launch_bounds__(32) k_lms_sym(RxDev d, int flush, int nseg, unsigned char *labels, long long lab_cap) {
+  DevState *st = d.st;
+  if (!st->trained) return;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nseg) return;
+  const long long s = st->seg_next + t;
+  const long long si = rmod(s, d.seg_cap);
+  if (d.seg_done[si] == s + 1) return;
+  const long long lo = s * (long long)d.S;
+  const long long me = st->m_end;
+  if (me >= 0 && lo >= me) return;
+  const long long hi = seg_end_of(d, s);
+  const int K = d.K, c = K >> 1;
+  const long long vend = st->v_lms;
+  if (me < 0 && 2 * (hi - 1) + st->sync_phase + c >= vend) return;   // streaming: data not there yet
+  const long long e = lo / d.E_sym;
+  float2 w[KP], v[KP];
+  if (e >= d.D && d.seed_ready[rmod(e, d.seed_cap)] != e + 1) return;
+#pragma unroll
+  for (int k = 0; k < KP; ++k) {
+    w[k] = k < K ? (e < d.D ? d.w_train[k] : d.seed[rmod(e, d.seed_cap) * RX_MAX_K + k]) : make_float2(0.f, 0.f);
+    v[k] = make_float2(0.f, 0.f);                  // R-WL: every DD segment's v-branch from 0
+  }
+  long long t0 = lo - d.O;
+  if (t0 < 0) t0 = 0;
+  double en = 0.0, ed = 0.0;
+  unsigned char *warm = d.O > 0 ? d.seg_warm + si * d.O : nullptr;
+  lms_sym_run<KP, WLIN, 1>(d, t0, hi, lo, w, v, warm, en, ed, vend);
+  float nrm = 0.f;
+#pragma unroll
+  for (int k = 0; k < KP; ++k) {
+    if (k < K) {
+      d.seg_w[si * RX_MAX_K + k] = w[k];
+      nrm += cabs2(w[k]);
+    }
+  }
+  if (nrm > 1e6f) set_flag(st, RX_FLAG_DIVERGE);
+  d.seg_theta[si] = 0.f;
+  d.seg_evm[2 * si] = en;
+  d.seg_evm[2 * si + 1] = ed;
+  __threadfence();
+  d.seg_done[si] = (int)(s + 1);
 }
 
 // ------------------------------------------------------------------ H22 stitching
@@ -1221,7 +1461,7 @@ __global__ void __launch_bounds__(256) k_lms_final(RxDev d, unsigned char *label
   if (threadIdx.x < 32) {
     const int k = threadIdx.x;
     float2 w = k < d.K ? d.seg_w[si * RX_MAX_K + k] : make_float2(0.f, 0.f);
-    if (d.family == 1 && d.lms_mode == 0) {   // data aided (lms_mode 1): no CPR, absolute frame
+    if (d.family == 1 && d.lms_mode != 1) {   // data aided (lms_mode 1): no CPR, absolute frame
       const float a = sqrtf(cabs2(w));
       const float px = warp_sum(w.x * a), py = warp_sum(w.y * a);
       const float inv = rsqrtf(fmaxf(px * px + py * py, 1e-30f));

@@ -250,7 +250,9 @@ static rx_status validate(const rx_config *c) {
   if (!c->static_taps || c->n_static_taps < 1 || c->n_static_taps % 2 == 0 || c->n_static_taps > c->hop + 1)
     return RX_EINVAL;
   if (c->lms_taps < 1 || c->lms_taps > RX_MAX_K) return RX_EINVAL;
-  if (c->lms_block != 32) return RX_EINVAL;
+  // block LMS: B = 32; lms_mode 2 (per-symbol WL DDLMS, KK, K <= 8): B = 1
+  if (c->lms_mode == 2 ? (c->lms_block != 1 || c->family != RX_QAM_KK || c->lms_taps > 8) : c->lms_block != 32)
+    return RX_EINVAL;
   if (c->lms_segment < 64 || c->lms_segment % 32 || !is_pow2(c->lms_segment)) return RX_EINVAL;
   const long long E = (long long)c->buffer_blocks * (c->family == RX_PAM ? 256 : 128);
   if (E % c->lms_segment) return RX_EINVAL;
@@ -270,7 +272,7 @@ static rx_status validate(const rx_config *c) {
     return RX_EINVAL;
   if (c->serial_equaliser != 0 && c->serial_equaliser != 1) return RX_EINVAL;
   if (c->cpr_anchor != 0 && c->cpr_anchor != 1) return RX_EINVAL;
-  if (c->lms_mode != 0 && c->lms_mode != 1) return RX_EINVAL;
+  if (c->lms_mode < 0 || c->lms_mode > 2) return RX_EINVAL;
   if (c->equaliser_lag != 0 && c->equaliser_lag != 1) return RX_EINVAL;
   if (c->shard_count < 0 || c->shard_count > 64) return RX_EINVAL;
   if (c->shard_count > 1) {        // time sharding (SURVEY §8(e) mode 2): the KK chain
@@ -516,12 +518,12 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
     d.q_shift = 0;
     while ((1LL << d.q_shift) < (long long)c.buffer_blocks * 256) ++d.q_shift;
     TRY(dalloc(h, &d.cfo, d.buf_cap));
-    d.cfo_G = CFO_ROWS;                                  // spectrum rows per buffer
+    d.cfo_G = CFO_ROWS + CFO_ROWS / CFO_GRP;             // spectrum rows per buffer (+ group rows)
     const long long maxbuf = HB;                           // buffers completing in one call
     TRY(dalloc(h, &d.cfo_part, maxbuf * d.cfo_G * 1024));
     TRY(dalloc(h, &d.cfo_pow, maxbuf * d.cfo_G));
     TRY(dalloc(h, &d.cfo_tick, maxbuf));
-    TRY(dalloc(h, &d.cfo_tick_spec, maxbuf));
+    TRY(dalloc(h, &d.cfo_tick_spec, maxbuf * (CFO_ROWS / CFO_GRP + 1)));
     TRY(dalloc(h, &d.cfo_a, maxbuf * (h->Q / 1024 + 1)));
   }
   TRY(dalloc(h, &d.sync_g, 2 * RX_PREF));
@@ -658,8 +660,16 @@ static lms_train_fn lms_train_kp(int K) {
 }
 template <bool CPLX>
 static lms_train_fn lms_train_kernel(const RxDev &d) {
+  if (CPLX && d.lms_mode == 2) {   // per-symbol DDLMS: B = 1 training pass
+    if (d.wl) return d.K <= 4 ? k_lms_train_sym<4, true> : k_lms_train_sym<8, true>;
+    return d.K <= 4 ? k_lms_train_sym<4, false> : k_lms_train_sym<8, false>;
+  }
   if (CPLX && d.wl) return lms_train_kp<true, true>(d.K);
   return lms_train_kp<CPLX>(d.K);
+}
+static lms_seg_fn lms_sym_kernel(const RxDev &d) {
+  if (d.wl) return d.K <= 4 ? k_lms_sym<4, true> : k_lms_sym<8, true>;
+  return d.K <= 4 ? k_lms_sym<4, false> : k_lms_sym<8, false>;
 }
 
 template <bool CPLX>
@@ -679,9 +689,13 @@ static void launch_lms_round(rx_handle *h, cudaStream_t s, unsigned char *labels
                              int flush, long long nseg) {
   RxDev &d = h->d;
   const long long S = d.S;
-  // segments per CTA: LMS_SPC warps, BPS segments on LMS_PAIR warps each (k_lms_seg)
+  // segments per CTA: LMS_SPC warps, BPS segments on LMS_PAIR warps each (k_lms_seg); the
+  // per-symbol DDLMS (lms_mode 2) runs one segment per thread (k_lms_sym)
   const int spc = (d.cpr == 2 && d.lms_mode == 0) ? LMS_SPC / LMS_PAIR : LMS_SPC;
-  KLAUNCH(h, RX_K_LMS, s, (lms_seg_kernel(d)<<<gridc(nseg, spc), 32 * LMS_SPC, 0, s>>>(d, flush, (int)nseg, labels, lab_cap)));
+  if (d.lms_mode == 2)
+    KLAUNCH(h, RX_K_LMS, s, (lms_sym_kernel(d)<<<gridc(nseg, 32), 32, 0, s>>>(d, flush, (int)nseg, labels, lab_cap)));
+  else
+    KLAUNCH(h, RX_K_LMS, s, (lms_seg_kernel(d)<<<gridc(nseg, spc), 32 * LMS_SPC, 0, s>>>(d, flush, (int)nseg, labels, lab_cap)));
   if (d.family == RX_PAM) {
     // PAM segments wrote their labels and error counts; the prefix also adds the counters
     KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_prefix<<<1, 1024, 0, s>>>(d, flush, (int)nseg)));
@@ -835,11 +849,10 @@ static void run_kk(rx_handle *h, cudaStream_t s, const InView &in, unsigned char
     while ((h->cfo_done + nbuf + 1) * Q <= q_front || (flush && (h->cfo_done + nbuf) * Q < q_front)) ++nbuf;
     if (nbuf > 0) {
       const long long beta0 = h->cfo_done;
-      const int nrows = d.cfo_G;
       const int fine_ctas = (int)((Q / 1024 + 7) / 8);
       for (long long b0 = 0; b0 < nbuf; b0 += h->cfg.history_buffers) {
         const long long nb = nbuf - b0 < h->cfg.history_buffers ? nbuf - b0 : h->cfg.history_buffers;
-        KLAUNCH(h, RX_K_CFO, s, (k_cfo_spec<<<dim3((unsigned)nrows, (unsigned)nb), CFO_SPEC_T, 0, s>>>(d, beta0 + b0, q_front)));
+        KLAUNCH(h, RX_K_CFO, s, (k_cfo_spec<<<dim3(CFO_ROWS, (unsigned)nb), CFO_SPEC_T, 0, s>>>(d, beta0 + b0, q_front)));
         if (d.cfo_enable) KLAUNCH(h, RX_K_CFO, s, (k_cfo_fine<<<dim3((unsigned)fine_ctas, (unsigned)nb), 256, 0, s>>>(d, beta0 + b0, q_front, fine_ctas)));
         if (flush || h->cfg.serial_equaliser) {
           KLAUNCH(h, RX_K_CFO, s, (k_cfo_carry<<<1, 1, 0, s>>>(d, beta0 + b0, (int)nb, q_front)));
@@ -974,7 +987,7 @@ extern "C" rx_status rx_shard_process(rx_handle *h, long long beta, const void *
   KLAUNCH(h, RX_K_KK_S2, s, (k_kk_s2<<<gridc(s2_hi - s2_lo, FE_GROUPS), 256, 0, s>>>(d, s2_lo, s2_hi)));
   const long long q_front = 256 * s2_hi - 128;
   const int fine_ctas = (int)((h->Q / 1024 + 7) / 8);
-  KLAUNCH(h, RX_K_CFO, s, (k_cfo_spec<<<dim3((unsigned)d.cfo_G, 1), CFO_SPEC_T, 0, s>>>(d, beta, q_front)));
+  KLAUNCH(h, RX_K_CFO, s, (k_cfo_spec<<<dim3(CFO_ROWS, 1), CFO_SPEC_T, 0, s>>>(d, beta, q_front)));
   if (d.cfo_enable) KLAUNCH(h, RX_K_CFO, s, (k_cfo_fine<<<dim3((unsigned)fine_ctas, 1), 256, 0, s>>>(d, beta, q_front, fine_ctas)));
   h->sh_cur.beta = beta;
   h->sh_cur.qfront = q_front;

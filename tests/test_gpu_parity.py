@@ -914,3 +914,29 @@ def test_time_sharded_kk_stream_is_bit_identical(N):
         assert all(s["sync_offset"] == st1["sync_offset"] and s["sync_phase"] == st1["sync_phase"] for s in sts)
         for h in hs:
             h.close()
+
+
+@pytest.mark.parametrize("name,extra", [
+    # the paper's field trial shared a 10 MHz reference between Tx and Rx (only small phase
+    # fluctuations for the DDLMS to track): 1 kHz linewidth here
+    ("C3", dict(widely_linear=1, linewidth_hz=1e3)),                      # QAM-4, 4 WL taps (the paper's)
+    ("C5:5", dict(widely_linear=1, iq_imbalance=0.12 * np.exp(-0.6j), linewidth_hz=1e3)),   # QAM-16 + IQ
+])
+def test_per_symbol_wl_ddlms_parity(name, extra):
+    """NEXT-1: the paper's own equaliser - a 4-tap widely-linear DDLMS updated every
+    symbol (lms_block = 1, lms_mode = 2) that also recovers the carrier phase (no separate CPR) -
+    against the oracle's B = 1 recursion: training taps, equaliser output element-wise, labels
+    and counters (same criteria as the block-LMS parity)."""
+    _torch_cuda()
+    gen_kw = {k: extra.pop(k) for k in ("iq_imbalance", "linewidth_hz") if k in extra}
+    rec, rx = make_config(name, n_samples=1 << 21, **gen_kw)
+    rx.update(buffer_blocks=256, lms_taps=4, lms_block=1, lms_mode=2, **extra)
+    out = run_oracle(rec, rx)
+    R, labels, st = run_gpu(rec, rx, chunk=256 * 512)
+    assert st["sync_offset"] == out["sync"]["offset"] and st["sync_phase"] == out["sync"]["phase"]
+    w, v = R.train_taps()
+    assert rel_l2(w, out["lms"]["w_train"]) < TOL_FIELD and rel_l2(v, out["lms"]["v_train"]) < TOL_FIELD
+    mism, excl = _compare_labels(rec, dict(rx, cpr_test_phases=0), out, labels, R)
+    _compare_counters(rec, out, st, mism)
+    print(f"{name} per-symbol WL DDLMS: BER {st['bit_errors']}/{st['bits']}, "
+          f"EVM {evm_db(st['evm_num'], st['evm_den']):.2f} dB")

@@ -133,3 +133,62 @@ def test_linear_segmented_equaliser_is_image_limited():
     err_db = 10 * math.log10(np.mean(np.abs(_abs_frame(lm)[lo:] - s[lo:]) ** 2))
     closed = 10 * math.log10(abs(BETA) ** 2 / (abs(ALPHA) ** 2 + abs(BETA) ** 2))
     assert closed - 2 < err_db < closed + 2
+
+
+# ------------------------------------------------------------------ per-symbol DDLMS (NEXT-1)
+# The paper's equaliser proper: a 4-tap widely-linear DDLMS updated every symbol
+# (B = 1) that also does the symbol-phase recovery (no separate CPR; rx_config.lms_mode = 2,
+# DESIGN reading R-DDLMS). Pinned by the same closed forms, now with a static carrier phase phi
+# that only the taps can absorb: w_c = e^{j phi} alpha / den, v_c = -e^{-j phi} conj(beta) / den.
+
+PHI = 0.3
+
+
+def _ddlms_full(z, s, idx, sl, wl, n):
+    lp = O.LmsParams(K=4, B=1, S=4096, O=256, mu=1e-3, T_train=8192, E=1 << 14, D=2, cpr="none",
+                     widely_linear=wl, anchor_each=True)
+    m0 = 64
+
+    def ref_i(m):
+        return idx[np.asarray(m)]
+
+    def ref_v(m):
+        return s[np.asarray(m)]
+    return O.lms_full(z, 2, 0, n, ref_i, ref_v, sl, lp, False, m0)
+
+
+def test_per_symbol_wl_ddlms_training_reaches_the_rotated_closed_form_inverse():
+    """B = 1 training (e = r - y every symbol) on the IQ-imbalanced stream with carrier phase
+    PHI converges to w_c = e^{j PHI} alpha / (|alpha|^2 - |beta|^2), v_c = -e^{-j PHI} conj(beta) /
+    (|alpha|^2 - |beta|^2); the other taps vanish."""
+    z, s, idx, sl = _qam16_stream(16384, 3, phi0=PHI)
+    lp = O.LmsParams(K=4, B=1, mu=5e-4, T_train=16000, widely_linear=True)
+    w, v = O.lms_train(z, 2, 0, s[64:64 + 16000], 64, lp, real=False)
+    den = abs(ALPHA) ** 2 - abs(BETA) ** 2
+    w_c, v_c = np.exp(1j * PHI) * ALPHA / den, -np.exp(-1j * PHI) * np.conj(BETA) / den
+    assert abs(w[2] - w_c) < 2e-3 and abs(v[2] - v_c) < 2e-3
+    assert np.max(np.abs(np.delete(w, 2))) < 2e-3 and np.max(np.abs(np.delete(v, 2))) < 2e-3
+
+
+def test_per_symbol_wl_ddlms_tracks_phase_and_rejects_the_image():
+    """Decision-directed B = 1 segments with no CPR: every segment ends at its phase-rotated
+    closed-form ratio v/w = -e^{-2j PHI} conj(beta)/alpha, decodes error free, and the widely-linear
+    equaliser's decision-referenced EVM beats the strictly linear one by >= 20 dB (the linear
+    one sits at the closed-form image floor |beta|^2 / (|alpha|^2 + |beta|^2))."""
+    n = 40000
+    z, s, idx, sl = _qam16_stream(n, 4, phi0=PHI)
+    out = _ddlms_full(z, s, idx, sl, True, n)
+    assert np.all(out["idx"][64:] == idx[64:])
+    ratio = -np.exp(-2j * PHI) * np.conj(BETA) / ALPHA
+    for w, v in zip(out["seg_w"][1:], out["seg_v"][1:]):
+        assert abs(v[2] / w[2] - ratio) < 1e-2          # v restarts at 0 per segment (R-WL)
+    def evm(o):                          # second half of every segment (v has converged from 0)
+        m = np.arange(8192, n)
+        zz = o["z"][m[(m % 4096) >= 2048]]
+        d = sl.value(sl.indices(zz))
+        num, den = O.evm_sums(zz, d)
+        return 10 * math.log10(num / den)
+    lin = _ddlms_full(z, s, idx, sl, False, n)
+    floor = 10 * math.log10(abs(BETA) ** 2 / (abs(ALPHA) ** 2 + abs(BETA) ** 2))
+    assert abs(evm(lin) - floor) < 1.0
+    assert evm(out) < evm(lin) - 20.0
