@@ -515,20 +515,60 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
             const float2 pb = bps_part[lane];
             dA += pb.x;
             dB += pb.y;
+          } else if (d.Pt == 32 && nvalid == 32) {
+            // 32 test phases over a full block: the grid is symmetric (phi_{31-q} = -phi_q), so
+            // lane l scores the pair (q, 31 - q), q = l & 15, on symbols 16 (l >> 4) .. + 15 with
+            // shared products (3 instead of 4 rotation FMAs per evaluation), the two halves are
+            // added by one shuffle, and lane l < 16 then holds phase l, lane l >= 16 phase 47 - l
+            __syncwarp();
+            const int q = lane & 15, hh = lane >> 4;
+            const float2 rq = __ldg(d.bps_rot + q);                  // e^{-j phi_q} = (cos, -sin)
+            const float cq = rq.x * inv2s, sq = -rq.y * inv2s, cst = 0.5f * (float)(L - 1);
+            const float4 *y4 = reinterpret_cast<const float4 *>(sm.y) + 8 * hh;
+            float p0 = 0.f, p1 = 0.f, m0 = 0.f, m1 = 0.f;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float4 yy = y4[i];
+#pragma unroll
+              for (int hsym = 0; hsym < 2; ++hsym) {
+                const float yx = hsym ? yy.z : yy.x, yq = hsym ? yy.w : yy.y;
+                const float A = fmaf(yx, cq, cst), C = fmaf(yq, cq, cst);
+                const float uxp = fmaf(yq, sq, A), uxm = fmaf(-yq, sq, A);    // phase q / 31 - q
+                const float uyp = fmaf(-yx, sq, C), uym = fmaf(yx, sq, C);
+                const float exp_ = uxp - fminf(fmaxf(rintf(uxp), 0.f), Lm1);
+                const float eyp = uyp - fminf(fmaxf(rintf(uyp), 0.f), Lm1);
+                const float exm = uxm - fminf(fmaxf(rintf(uxm), 0.f), Lm1);
+                const float eym = uym - fminf(fmaxf(rintf(uym), 0.f), Lm1);
+                float &P = hsym ? p1 : p0, &Mm = hsym ? m1 : m0;
+                P = fmaf(exp_, exp_, P);
+                P = fmaf(eyp, eyp, P);
+                Mm = fmaf(exm, exm, Mm);
+                Mm = fmaf(eym, eym, Mm);
+              }
+            }
+            float dp = p0 + p1, dm = m0 + m1;
+            dp += __shfl_xor_sync(0xffffffffu, dp, 16);
+            dm += __shfl_xor_sync(0xffffffffu, dm, 16);
+            dA = hh ? dm : dp;
           } else {
             __syncwarp();
             bps_partial(sm.y, 0, nvalid, rsA, rsB, L, d.Pt > 32, dA, dB);
           }
           // argmin over the test phases, lowest p on ties (c-9 step 2): the distances are sums of
           // squares (>= +0), so their IEEE bit patterns order like the values and one warp-wide
-          // integer min (redux.sync) finds the minimum; the lowest lane holding it (ballot) is p
+          // integer min (redux.sync) finds the minimum; the lowest phase holding it is p
           float bd = lane < d.Pt ? dA : 3.4e38f;
           int bp = lane;
           if (lane + 32 < d.Pt && dB < bd) { bd = dB; bp = lane + 32; }
           const unsigned bits = __float_as_uint(bd);
           const unsigned mn = __reduce_min_sync(0xffffffffu, bits);
-          const unsigned lo = __ballot_sync(0xffffffffu, bits == mn && bp < 32);
-          bp = lo ? __ffs(lo) - 1 : __ffs(__ballot_sync(0xffffffffu, bits == mn)) - 1 + 32;
+          if (d.Pt == 32 && nvalid == 32 && !bps_bar) {   // lanes hold phases 0..15, then 31..16
+            const unsigned m = __ballot_sync(0xffffffffu, bits == mn);
+            bp = (m & 0xFFFFu) ? __ffs(m & 0xFFFFu) - 1 : 47 - (31 - __clz(m));
+          } else {
+            const unsigned lo = __ballot_sync(0xffffffffu, bits == mn && bp < 32);
+            bp = lo ? __ffs(lo) - 1 : __ffs(__ballot_sync(0xffffffffu, bits == mn)) - 1 + 32;
+          }
           th_hat = -0.78539816339744831f + ((float)bp + 0.5f) * (1.5707963267948966f / (float)d.Pt);
         }
         if (first) theta = th_hat;

@@ -21,6 +21,10 @@
 #define RX_GIT "dev"
 #endif
 
+// RX_SIDE_PRIO_LOW (experiments): the equaliser side stream at the lowest instead of the highest
+// stream priority
+static int g_side_low = getenv("RX_SIDE_PRIO_LOW") ? 1 : 0;
+
 // ------------------------------------------------------------------ small kernels
 __global__ void k_pam_mend(RxDev d, long long be_done) {
   long long f = d.Mb[rmod(be_done, d.blk_cap)];
@@ -583,7 +587,7 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   {
     int lo = 0, hi = 0;   // the equaliser's latency-bound warps get the SM slots first
     if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess ||
-        cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, g_side_low ? lo : hi) != cudaSuccess ||
         cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&h->ev_join[0], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&h->ev_join[1], cudaEventDisableTiming) != cudaSuccess) {
