@@ -665,7 +665,7 @@ def gpu_main(args):
                          dev, seed=2001)
 
         def make_pam(**kw):
-            f = dict(rx_fields(rx2), history_buffers=CALL_BUFFERS + 2)
+            f = dict(rx_fields(rx2), history_buffers=CALL_BUFFERS + 2, equaliser_lag=1)
             f.update(kw)
             return Receiver(RX_PAM, rec2.M, rec2.static_taps, device=dev.index, **f)
         W21 = round(0.021 * 2e9 / 4096) * 4096     # 21 ms of 2 GBaud symbols, whole segments
@@ -712,7 +712,10 @@ def gpu_main(args):
     ring4 = tiled_ring(rec4, max(args.warmup + args.steps + 6, int(args.ring_gib * (1 << 30) / 2 // n4)) * n4, dev)
 
     def make_kk(**kw):
-        f = dict(rx_fields(rx4), history_buffers=CALL_BUFFERS + 2)
+        # equaliser_lag = 1: a call's equaliser rounds (side stream) overlap the next call's
+        # front-end - the paper overlaps consecutive buffers across its streams; labels
+        # and counters are identical to lag 0 (rx.h)
+        f = dict(rx_fields(rx4), history_buffers=CALL_BUFFERS + 2, equaliser_lag=1)
         if args.lms_batch:
             f["lms_batch_segments"] = args.lms_batch
         f.update(kw)
@@ -738,7 +741,8 @@ def gpu_main(args):
                    "samples_per_step_per_gpu": n4, "record_scale": sc, "call_size": CHUNK,
                    "input": f"device ring {ring4.numel() * 2 / 2**30:.2f} GiB > L2 (fresh samples every step)",
                    "parallelism": f"{world} independent channel(s), 1 per GPU; all-reduce ({args.backend if world > 1 else 'none'}) "
-                                  f"of the packed counters per step"},
+                                  f"of the packed counters per step",
+                   "equaliser_lag": 1},
         "roofline": roof,
         "gpu_launches": res["launches"],
         "clocks": res["clocks"],

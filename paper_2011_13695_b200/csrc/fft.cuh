@@ -18,6 +18,22 @@ __device__ __forceinline__ int P8(int i) { return i + (i >> 4); }
 //   tw[960 + 8 (r-1) + k]      = W512^(8 r k),       r = 1..7, k < 8    (pass 2)
 #define TW_P3 512
 #define TW_P2 960
+// Every FFT CTA stages the 8 KiB twiddle table into shared memory. The copy is issued with
+// cp.async (16-byte LDGSTS, no register round trip) BEFORE the CTA loads its own blocks, and
+// waited for (tw_wait: wait_all + CTA barrier) just before the first FFT pass, so the table's L2
+// latency hides behind the block loads instead of stalling the CTA at its start.
+__device__ __forceinline__ void tw_stage_async(float2 *tw, const float2 *src) {
+  for (int i = threadIdx.x; i < 512; i += blockDim.x) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(tw + 2 * i);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src + 2 * i));
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
+}
+__device__ __forceinline__ void tw_wait() {
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+}
+
 template <bool INV>
 __device__ __forceinline__ float2 twv(const float2 *tw, int idx) {
   const float2 w = tw[idx];

@@ -16,8 +16,7 @@ __global__ void __launch_bounds__(256) k_kk_s1(RxDev d, InView in, long long b0,
   __shared__ float2 tw[1024];
   __shared__ float2 buf[FE_GROUPS][FFT_PAD_N];
   const int g = threadIdx.x >> 6, j = threadIdx.x & 63;
-  for (int i = threadIdx.x; i < 1024; i += blockDim.x) tw[i] = d.tw[i];
-  __syncthreads();   // twiddles visible to every group (the FFT barriers are per group)
+  tw_stage_async(tw, d.tw);   // waited for (tw_wait) before the first FFT pass
   const long long b = b0 + (long long)blockIdx.x * FE_GROUPS + g;
   const bool act = b < b1;
   int clip = 0, dom = 0;
@@ -59,6 +58,7 @@ __global__ void __launch_bounds__(256) k_kk_s1(RxDev d, InView in, long long b0,
   dom = __reduce_add_sync(0xffffffffu, dom);
   if ((threadIdx.x & 31) == 0 && dom) atomicAdd((unsigned long long *)&d.st->domain_errors, (unsigned long long)dom);
   if (first_dom != 0x7fffffffffffffffLL) atomicMin(&d.st->first_domain, first_dom);
+  tw_wait();
   fft512_regs<false>(buf[g], j, tw, v);
   fft512_publish_upper(buf[g], j, v);
   // FD Hilbert (c-6, A8): Phi = -j sgn(kappa) H, Phi[0] = Phi[512] = 0
@@ -130,8 +130,7 @@ __global__ void __launch_bounds__(256) k_kk_s2(RxDev d, long long b0, long long 
   __shared__ float2 tw[1024];
   __shared__ float2 buf[FE_GROUPS][FFT_PAD_N];
   const int g = threadIdx.x >> 6, j = threadIdx.x & 63;
-  for (int i = threadIdx.x; i < 1024; i += blockDim.x) tw[i] = d.tw[i];
-  __syncthreads();   // twiddles visible to every group (the FFT barriers are per group)
+  tw_stage_async(tw, d.tw);   // waited for (tw_wait) before the first FFT pass
   const long long b = b0 + (long long)blockIdx.x * FE_GROUPS + g;
   const bool act = b < b1;
   float2 ve[8], vo[8];
@@ -146,6 +145,7 @@ __global__ void __launch_bounds__(256) k_kk_s2(RxDev d, long long b0, long long 
 #pragma unroll
     for (int r = 0; r < 8; ++r) { ve[r] = make_float2(e[r].x, e[r].y); vo[r] = make_float2(e[r].z, e[r].w); }
   }
+  tw_wait();
   fft512_regs<false>(buf[g], j, tw, ve);
   fft512_regs<false>(buf[g], j, tw, vo);
 #pragma unroll
@@ -182,6 +182,15 @@ __device__ __forceinline__ void buf_range(const RxDev &d, long long beta, long l
   const long long Q = (long long)d.buffer_blocks * 256;
   qlo = beta * Q;
   qhi = qlo + Q < qfront ? qlo + Q : qfront;
+}
+
+// e^{-j 2 pi u / 2^64} of a 64-bit phase word from its top 32 bits as an angle in [-pi, pi),
+// MUFU sin / cos (|error| ~ 1e-6 rad); the exact-libm variant is dds_rot_neg (common.cuh)
+__device__ __forceinline__ float2 dds_rot_neg_fast(unsigned long long u) {
+  const float x = (float)(int)(u >> 32) * 1.4629180792671596e-9f;   // pi 2^-31
+  float sn, cs;
+  __sincosf(x, &sn, &cs);
+  return make_float2(cs, -sn);
 }
 
 // Per-buffer periodogram argmax + log-parabolic interpolation + power (c-8): the CTA that finishes
@@ -274,8 +283,7 @@ __global__ void __launch_bounds__(CFO_SPEC_T, 4) k_cfo_spec(RxDev d, long long b
   const int g = threadIdx.x >> 6, j = threadIdx.x & 63;
   long long qlo, qhi;
   buf_range(d, beta0 + blockIdx.y, qfront, qlo, qhi);
-  for (int i = threadIdx.x; i < 1024; i += blockDim.x) tw[i] = d.tw[i];
-  __syncthreads();
+  tw_stage_async(tw, d.tw);   // waited for before the first FFT (tw_wait, iteration 0)
   const long long nch = (qhi - qlo) / 1024;
   constexpr int NG = CFO_SPEC_T / 64;
   float acc[16];
@@ -299,6 +307,7 @@ __global__ void __launch_bounds__(CFO_SPEC_T, 4) k_cfo_spec(RxDev d, long long b
       vo[r] = cmul(b2, b2);
     }
     pw += (double)p0;
+    if (it == 0) tw_wait();                     // uniform over the CTA
     fft512_regs<false, 0>(bufs[g], j, tw, ve);
     fft512_regs<false, 0>(bufs[g], j, tw, vo);   // same buffer: fft512_regs syncs before its first store
 #pragma unroll
@@ -392,14 +401,14 @@ __global__ void __launch_bounds__(256) k_cfo_fine(RxDev d, long long beta0, long
 #pragma unroll
     for (int u = 0; u < 32; ++u) zz[u] = d.z[rmod(qlo + 1024 * i + lane + 32 * u, d.z_cap)];
     float ax = 0.f, ay = 0.f;
-    // DDS rotation: exact phase word every 8th sample of the lane, 32-sample step rotations
-    // in between (|error| < 1e-6 rad)
-    const float2 st32 = dds_rot_neg(32ULL * inc);
+    // DDS rotation: exact phase word every 8th sample of the lane (MUFU sin/cos of the top 32
+    // bits), 32-sample step rotations in between (|error| ~ 1e-6 rad)
+    const float2 st32 = dds_rot_neg_fast(32ULL * inc);
     float2 rot = make_float2(1.f, 0.f);
 #pragma unroll
     for (int u = 0; u < 32; ++u) {
       const long long n = 1024 * i + lane + 32 * u;
-      rot = (u & 7) == 0 ? dds_rot_neg((unsigned long long)n * inc) : cmul(rot, st32);
+      rot = (u & 7) == 0 ? dds_rot_neg_fast((unsigned long long)n * inc) : cmul(rot, st32);
       const float2 w = cmul(zz[u], rot);
       const float2 w2 = cmul(w, w), w4 = cmul(w2, w2);
       ax += w4.x;
@@ -466,12 +475,6 @@ struct ZpCache {
   unsigned long long origin, inc;
   float s;
 };
-__device__ __forceinline__ float2 dds_rot_neg_fast(unsigned long long u) {
-  const float x = (float)(int)(u >> 32) * 1.4629180792671596e-9f;   // pi 2^-31
-  float sn, cs;
-  __sincosf(x, &sn, &cs);
-  return make_float2(cs, -sn);
-}
 __device__ __forceinline__ float2 zp_rotate(const RxDev &d, float2 v, long long q, ZpCache &c) {
   const long long beta = q >> d.q_shift;
   if (beta != c.beta) {

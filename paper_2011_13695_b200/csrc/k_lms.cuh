@@ -836,17 +836,25 @@ __device__ void bps_helper(const RxDev &d, const float2 *ys, long long t_begin, 
 
 // ------------------------------------------------------------------ segments (1 warp each)
 // Segment s outputs [sS, min((s+1)S, m_end)), recursion starts O symbols early (c-9).
-#ifndef LMS_SPC
-#define LMS_SPC 1           // warps per CTA of k_lms_seg (1: finest CTA balance over the SMs; measured 4 -> 1: KK equaliser 0.89 -> 0.72 ms per C4 step)
+// warps per CTA of k_lms_seg: KK 1 (finest CTA balance over the SMs for its 2048-segment rounds:
+// measured 4 -> 1 warps, C4 equaliser 0.89 -> 0.72 ms per step), PAM 4 (its shorter rounds of
+// 4096 segments: 4 -> 1 measured 0.081 -> 0.090 ms per C2 step)
+#ifndef LMS_SPC_KK
+#define LMS_SPC_KK 1
 #endif
+#ifndef LMS_SPC_PAM
+#define LMS_SPC_PAM 4
+#endif
+#define LMS_SPC_OF(CPLX) ((CPLX) ? LMS_SPC_KK : LMS_SPC_PAM)
 #ifndef LMS_PAIR
 #define LMS_PAIR 1          // BPS segments: 2 = a helper warp scores half of each block's symbols
 #endif
 template <bool CPLX, int CPR, int KP, bool WLIN = false, int MODE = 1>
-__global__ void __launch_bounds__(32 * LMS_SPC) k_lms_seg(RxDev d, int flush, int nseg, unsigned char *labels,
+__global__ void __launch_bounds__(32 * LMS_SPC_OF(CPLX)) k_lms_seg(RxDev d, int flush, int nseg, unsigned char *labels,
                                                  long long lab_cap) {
   // BPS segments run on a warp pair (LMS warp + BPS helper), others on one warp
-  constexpr int PAIR = (CPR == 2) ? LMS_PAIR : 1, SPC = LMS_SPC / PAIR;   // PAIR = 2: BPS helper warp
+  constexpr int PAIR = (CPR == 2) ? LMS_PAIR : 1, SPC = LMS_SPC_OF(CPLX) / PAIR;   // PAIR = 2: BPS helper warp
+  static_assert(SPC >= 1 && SPC * PAIR == LMS_SPC_OF(CPLX), "LMS_SPC_* must be a multiple of LMS_PAIR");
   __shared__ LmsSmemT<CPLX> sm[SPC];
   __shared__ float2 bps_part[SPC][32];
   DevState *st = d.st;
@@ -1279,7 +1287,8 @@ __global__ void __launch_bounds__(1024) k_lms_prefix(RxDev d, int flush, int max
   if (t == 0) firstbad = maxn;
   if (t < 4) acnt[t] = 0;
   __syncthreads();
-  const int *ready = d.family == 1 ? d.seg_stitched : d.seg_done;   // PAM: no stitching (R_s = 0)
+  // PAM: no stitching (R_s = 0); anchored QAM: R_s is taken by k_lms_final itself (R-ANCHOR2)
+  const int *ready = (d.family == 1 && !d.anchor_each) ? d.seg_stitched : d.seg_done;
   for (int i0 = t; i0 < maxn; i0 += 4 * blockDim.x) {          // 4 loads in flight per thread
     int v[4];
 #pragma unroll
@@ -1348,10 +1357,7 @@ __global__ void __launch_bounds__(1024) k_lms_prefix(RxDev d, int flush, int max
   // scans + one scan of the 32 warp totals
   int carry = (int)(st->r_prefix & 3);
   if (d.family == 1 && d.anchor_each) {
-    for (int i = t; i < n; i += blockDim.x) {
-      const long long si = rmod(base + i, d.seg_cap);
-      d.seg_R[si] = d.seg_r[si];
-    }
+    // (R_s = r_s, both written by k_lms_final)
   } else if (d.family == 1) {
     __shared__ int wsum[32];
     const int lane = t & 31, warp = t >> 5;
@@ -1406,8 +1412,40 @@ __global__ void __launch_bounds__(256) k_lms_final(RxDev d, unsigned char *label
   const long long s = st->fin_lo + blockIdx.x;
   if (blockIdx.x >= nseg || s >= st->fin_hi) return;
   const long long si = rmod(s, d.seg_cap);
-  const int R = d.family == 1 ? d.seg_R[si] : 0;
   const long long lo = s * (long long)d.S, hi = seg_end_of(d, s);
+  int R = 0;
+  if (d.family == 1 && d.anchor_each) {
+    // R-ANCHOR2 (formerly the separate k_lms_stitch launch): R_s = argmax_r #{m in the segment's
+    // first 256 outputs (from m0 for s0) : d_m j^r = ref_m}, lowest r on ties
+    __shared__ int cnt[4];
+    if (threadIdx.x < 4) cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const long long a0 = (s == d.m0 / d.S) ? d.m0 : lo;
+    long long a1 = a0 + 256;
+    if (a1 > hi) a1 = hi;
+    int c4[4] = {0, 0, 0, 0};
+    for (long long m = a0 + threadIdx.x; m < a1; m += blockDim.x) {
+      const int cur = d.level[rmod(m, d.sym_cap)];
+      const long long ri = ((st->sync_offset + m - d.m0) % RX_PREF + RX_PREF) % RX_PREF;
+      const int ref = d.ref_idx[ri];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) c4[r] += (qam_rot(cur, r, d.L) == ref);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int v = __reduce_add_sync(0xffffffffu, c4[r]);
+      if ((threadIdx.x & 31) == 0) atomicAdd(&cnt[r], v);
+    }
+    __syncthreads();
+    for (int r = 1; r < 4; ++r) if (cnt[r] > cnt[R]) R = r;
+    if (threadIdx.x == 0) {
+      d.seg_r[si] = R;
+      d.seg_R[si] = R;
+      d.seg_stitched[si] = (int)(s + 1);
+    }
+  } else if (d.family == 1) {
+    R = d.seg_R[si];
+  }
   const int b = d.kbits >> 1;
   // per-segment lookup: level code -> code rotated by j^R (QAM) and its Gray label
   __shared__ unsigned char lut_code[256], lut_lab[256];

@@ -101,8 +101,7 @@ __global__ void __launch_bounds__(256) k_pam_fe(RxDev d, InView in, long long b0
   __shared__ float2 buf[FE_GROUPS][FFT_PAD_N];
   __shared__ double2 red[FE_GROUPS][2];
   const int g = threadIdx.x >> 6, j = threadIdx.x & 63;
-  for (int i = threadIdx.x; i < 1024; i += blockDim.x) tw[i] = d.tw[i];
-  __syncthreads();   // twiddles visible to every group (the FFT barriers are per group)
+  tw_stage_async(tw, d.tw);   // waited for (tw_wait) before the first FFT pass
   const long long b = b0 + (long long)blockIdx.x * FE_GROUPS + g;
   const bool act = b < b1;
   int clip = 0;
@@ -113,6 +112,7 @@ __global__ void __launch_bounds__(256) k_pam_fe(RxDev d, InView in, long long b0
     for (int r = 0; r < 8; ++r) v[r] = make_float2(0.f, 0.f);
   }
   block_reduce_clip(d.st, clip);
+  tw_wait();
   fft512_regs<false>(buf[g], j, tw, v);
   fft512_publish_upper(buf[g], j, v);
   // C_b = sum_{k<512} Y[k] conj(Y[k+512]) = Y0 conj(Y512) + Y256^2 + 2 sum_{k=1}^{255} Y[k] Y[512-k]
@@ -393,8 +393,7 @@ __global__ void __launch_bounds__(256) k_pam_be(RxDev d, long long b0, long long
   __shared__ float2 buf[FE_GROUPS][FFT_PAD_N];
   __shared__ double red[FE_GROUPS][2];
   const int g = threadIdx.x >> 6, j = threadIdx.x & 63;
-  for (int i = threadIdx.x; i < 1024; i += blockDim.x) tw[i] = d.tw[i];
-  __syncthreads();   // twiddles visible to every group (the FFT barriers are per group)
+  tw_stage_async(tw, d.tw);   // waited for (tw_wait) before the first FFT pass
   const long long b = b0 + (long long)blockIdx.x * FE_GROUPS + g;
   const bool act = b < b1;
   // the block's spectrum X stored by k_pam_fe (SURVEY §8(a) 'read back spectra' option):
@@ -424,6 +423,7 @@ __global__ void __launch_bounds__(256) k_pam_be(RxDev d, long long b0, long long
   sincospif(f * 0.125f, &step.y, &step.x);
   sincospif(f, &nyq.y, &nyq.x);
   float2 Zk[4], Zn[4], Z256;
+  tw_wait();
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     const int k = j + 64 * r;

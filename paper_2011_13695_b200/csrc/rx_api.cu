@@ -693,18 +693,20 @@ static void launch_lms_round(rx_handle *h, cudaStream_t s, unsigned char *labels
                              int flush, long long nseg) {
   RxDev &d = h->d;
   const long long S = d.S;
-  // segments per CTA: LMS_SPC warps, BPS segments on LMS_PAIR warps each (k_lms_seg); the
+  // segments per CTA: wpc warps, BPS segments on LMS_PAIR warps each (k_lms_seg); the
   // per-symbol DDLMS (lms_mode 2) runs one segment per thread (k_lms_sym)
-  const int spc = (d.cpr == 2 && d.lms_mode == 0) ? LMS_SPC / LMS_PAIR : LMS_SPC;
+  const int wpc = d.family == RX_PAM ? LMS_SPC_PAM : LMS_SPC_KK;   // warps per CTA
+  const int spc = (d.cpr == 2 && d.lms_mode == 0) ? wpc / LMS_PAIR : wpc;
   if (d.lms_mode == 2)
     KLAUNCH(h, RX_K_LMS, s, (lms_sym_kernel(d)<<<gridc(nseg, 32), 32, 0, s>>>(d, flush, (int)nseg, labels, lab_cap)));
   else
-    KLAUNCH(h, RX_K_LMS, s, (lms_seg_kernel(d)<<<gridc(nseg, spc), 32 * LMS_SPC, 0, s>>>(d, flush, (int)nseg, labels, lab_cap)));
+    KLAUNCH(h, RX_K_LMS, s, (lms_seg_kernel(d)<<<gridc(nseg, spc), 32 * wpc, 0, s>>>(d, flush, (int)nseg, labels, lab_cap)));
   if (d.family == RX_PAM) {
     // PAM segments wrote their labels and error counts; the prefix also adds the counters
     KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_prefix<<<1, 1024, 0, s>>>(d, flush, (int)nseg)));
   } else {
-    KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_stitch<<<(unsigned)nseg, 256, 0, s>>>(d, (int)nseg)));
+    // anchored quadrants (R-ANCHOR2): k_lms_final takes each R_s itself; the c-9 chain stitches first
+    if (!d.anchor_each) KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_stitch<<<(unsigned)nseg, 256, 0, s>>>(d, (int)nseg)));
     KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_prefix<<<1, 1024, 0, s>>>(d, flush, (int)nseg)));
     KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_final<<<(unsigned)nseg, 256, 0, s>>>(d, labels, lab_cap, (int)nseg)));
     KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_counters<<<1, 1024, 0, s>>>(d)));
