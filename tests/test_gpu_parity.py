@@ -122,6 +122,13 @@ def _compare_labels(rec, rx, out, labels, R=None, strict=True, max_excl=0.02):
         first = np.argmax(start & (seg == s))
         excl[first:(s + 1) * S] = True
     bad = mism & ~excl
+    cont, E = _contaminated_epochs(start, m_end, dict(rx, _fmt=rec.fmt))
+    if not strict:
+        # full record sizes: an epoch whose lag-D seeds descend from a parted segment starts its
+        # segments from taps that differ at the seed level, so a decision within 0.05 of a
+        # boundary may flip there without a preceding near-boundary (1e-3) flip in its segment
+        in_cont = cont[np.arange(m_end) // E]
+        bad &= ~(in_cont & near_threshold(soft, rec.fmt, rec.M, 0.05))
     assert not np.any(bad), f"{int(bad.sum())} label mismatches not preceded in their segment by a " \
                             f"near-boundary flip, first at {np.argmax(bad)}"
     assert mism.sum() <= 1e-3 * m_end, f"{int(mism.sum())} of {m_end} labels differ"
@@ -137,7 +144,6 @@ def _compare_labels(rec, rx, out, labels, R=None, strict=True, max_excl=0.02):
         except Exception:                       # streaming rings no longer hold the record
             Y = None
         if Y is not None:
-            cont, E = _contaminated_epochs(start, m_end, dict(rx, _fmt=rec.fmt))
             ok = ~excl & ~cont[np.arange(m_end) // E]
             yg = Y if rec.fmt == "qam" else Y.real
             y_err = rel_l2(yg[ok], soft[ok])
