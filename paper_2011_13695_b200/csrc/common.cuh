@@ -33,6 +33,36 @@ __device__ __forceinline__ float2 dds_rot_neg(uint64_t u) {
   return make_float2(c, -s);
 }
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// Kernels launched with the PDL attribute (rx_api.cu launch_pdl) start their independent prologue
+// (twiddle staging) while the previous kernel of the stream drains, and wait here before touching
+// anything it produced (griddepcontrol.wait returns once the preceding grid has completed and its
+// memory is visible; a no-op for a normal launch).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
+// ------------------------------------------------------------------ TMA bulk copies + mbarrier
+// 1-D bulk global -> shared copies by the async (TMA) engine (cp.async.bulk, SASS UBLKCP) with
+// transaction-count completion on a shared-memory mbarrier: one elected thread arms the barrier
+// with the byte count and issues the copy, the consumers spin on the barrier's phase.
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {   // make the init visible to the async proxy
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
+  asm volatile("{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+               " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+
 // ------------------------------------------------------------------ warp reductions
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll

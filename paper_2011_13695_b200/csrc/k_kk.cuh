@@ -126,35 +126,59 @@ __global__ void __launch_bounds__(256) k_kk_s1(RxDev d, InView in, long long b0,
 //   G'[k'] = (Ev[k'] - W^k' Od[k']) H2[k' + 512],  k' in [256, 512) (kappa = k' - 512)
 //   — bin k' = j + 64 r is exactly the IFFT's pass-1 operand of thread j, so the band-selected
 //   spectrum feeds the decimating IFFT-512 without a shared-memory round trip.
+// The block's overlapped E frame (1024 cf32, 8 KiB, contiguous in the E ring) is staged by one TMA
+// bulk copy per group into shared memory (the north_star's "TMA staging of overlapped blocks"),
+// completed on an mbarrier; the staging area then serves as the group's FFT scratch. Frames at
+// the stream start (p < 0) or across the ring's end are loaded by the threads instead.
 __global__ void __launch_bounds__(256) k_kk_s2(RxDev d, long long b0, long long b1) {
-  __shared__ float2 tw[1024];
-  __shared__ float2 buf[FE_GROUPS][FFT_PAD_N];
+  __shared__ __align__(16) float2 tw[1024];
+  __shared__ __align__(128) float2 stage[FE_GROUPS][1024];   // E frames (TMA), then FFT scratch
+  __shared__ __align__(8) uint64_t fbar[FE_GROUPS];
   const int g = threadIdx.x >> 6, j = threadIdx.x & 63;
+  float2 *const buf = stage[g];                               // FFT_PAD_N <= 1024
+  if (threadIdx.x < FE_GROUPS) mbar_init(&fbar[threadIdx.x], 1);
+  mbar_fence_init();
   tw_stage_async(tw, d.tw);   // waited for (tw_wait) before the first FFT pass
+  __syncthreads();            // barrier inits visible to every thread
+  pdl_wait();                 // E from k_kk_s1
   const long long b = b0 + (long long)blockIdx.x * FE_GROUPS + g;
   const bool act = b < b1;
+  const long long p0 = 512 * b - 512;                         // frame [p0, p0 + 1024)
+  const long long r0 = rmod(p0, d.E_cap);
+  const bool tma = act && p0 >= 0 && r0 + 1024 <= d.E_cap;    // group-uniform
+  if (tma && j == 0) {
+    mbar_expect_tx(&fbar[g], 1024 * sizeof(float2));
+    bulk_g2s(stage[g], d.E + r0, 1024 * sizeof(float2), &fbar[g]);
+  }
   float2 ve[8], vo[8];
   {
     float4 e[8];
+    if (tma) {
+      mbar_wait(&fbar[g], 0);
+      const float4 *sf = reinterpret_cast<const float4 *>(stage[g]);
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {           // frame p in [512b - 512, 512b + 512), E_p = 0 for p < 0
-      const long long p = 512 * b - 512 + 2 * (j + 64 * r);
-      e[r] = (act && p >= 0) ? *reinterpret_cast<const float4 *>(d.E + rmod(p, d.E_cap))
-                             : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int r = 0; r < 8; ++r) e[r] = sf[j + 64 * r];    // E[p0 + 2n], E[p0 + 2n + 1], n = j + 64 r
+    } else {
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {         // E_p = 0 for p < 0
+        const long long p = p0 + 2 * (j + 64 * r);
+        e[r] = (act && p >= 0) ? *reinterpret_cast<const float4 *>(d.E + rmod(p, d.E_cap))
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
     }
 #pragma unroll
     for (int r = 0; r < 8; ++r) { ve[r] = make_float2(e[r].x, e[r].y); vo[r] = make_float2(e[r].z, e[r].w); }
   }
-  tw_wait();
-  fft512_regs<false>(buf[g], j, tw, ve);
-  fft512_regs<false>(buf[g], j, tw, vo);
+  tw_wait();                  // (also: every thread's frame is in registers before the FFT scratch use)
+  fft512_regs<false>(buf, j, tw, ve);
+  fft512_regs<false>(buf, j, tw, vo);
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
     const int k = j + 64 * r;
     const float2 od = cmul(vo[r], tw[k]);
     ve[r] = r < 4 ? cmul(cadd(ve[r], od), __ldg(d.H + k)) : cmul(csub(ve[r], od), __ldg(d.H + k + 512));
   }
-  fft512_regs<true>(buf[g], j, tw, ve);
+  fft512_regs<true>(buf, j, tw, ve);
   // z_local[n] = 1/2 * IDFT512 = v / 1024; keep n in [128, 384) <=> r = 2..5
   if (act) {
 #pragma unroll
@@ -284,6 +308,7 @@ __global__ void __launch_bounds__(CFO_SPEC_T, 4) k_cfo_spec(RxDev d, long long b
   long long qlo, qhi;
   buf_range(d, beta0 + blockIdx.y, qfront, qlo, qhi);
   tw_stage_async(tw, d.tw);   // waited for before the first FFT (tw_wait, iteration 0)
+  pdl_wait();                 // z from k_kk_s2
   const long long nch = (qhi - qlo) / 1024;
   constexpr int NG = CFO_SPEC_T / 64;
   float acc[16];
@@ -387,6 +412,7 @@ __global__ void __launch_bounds__(CFO_SPEC_T, 4) k_cfo_spec(RxDev d, long long b
 
 __global__ void __launch_bounds__(256) k_cfo_fine(RxDev d, long long beta0, long long qfront, int cta_per_buf) {
   __shared__ int ticket;
+  pdl_wait();                 // the coarse estimate from k_cfo_spec
   const long long beta = beta0 + blockIdx.y;
   long long qlo, qhi;
   buf_range(d, beta, qfront, qlo, qhi);

@@ -1279,6 +1279,7 @@ __device__ __forceinline__ void lms_add_counters(const RxDev &d, long long lo, l
 // R_s = (A + sum_{i<=s} r_i) mod 4 with A fixed by anchoring the segment containing m0 to
 // the known reference over [m0, m0 + 256) (c-9 'Stitching').
 __global__ void __launch_bounds__(1024) k_lms_prefix(RxDev d, int flush, int maxn) {
+  pdl_wait();                 // the previous kernel of the round (programmatic dependent launch)
   __shared__ int firstbad;
   __shared__ int acnt[4];
   DevState *st = d.st;
@@ -1407,6 +1408,7 @@ __global__ void __launch_bounds__(1024) k_lms_prefix(RxDev d, int flush, int max
 // canonical absolute-frame taps w~_s = w e^{j theta} j^{-R_s} (c-9 'Seed').
 __global__ void __launch_bounds__(256) k_lms_final(RxDev d, unsigned char *labels, long long lab_cap,
                                                    int nseg) {
+  pdl_wait();                 // fin_lo / fin_hi from k_lms_prefix
   __shared__ long long red[8];
   DevState *st = d.st;
   const long long s = st->fin_lo + blockIdx.x;
@@ -1550,12 +1552,14 @@ __global__ void __launch_bounds__(256) k_lms_final(RxDev d, unsigned char *label
 }
 
 __global__ void __launch_bounds__(1024) k_lms_counters(RxDev d) {
+  pdl_wait();                 // the previous kernel of the round (programmatic dependent launch)
   lms_add_counters(d, d.st->fin_lo, d.st->fin_hi);
 }
 
 // ... and the lag-D epoch seeds: CTA i owns epoch fin_lo/spe + i; when all its segments are
 // finalised the seed of epoch e + D is the mean of their canonical taps (fixed order).
 __global__ void __launch_bounds__(1024) k_lms_seeds(RxDev d, int flush) {
+  pdl_wait();                 // the previous kernel of the round (programmatic dependent launch)
   DevState *st = d.st;
   const long long lo = st->fin_lo, hi = st->fin_hi;
   const long long spe = d.E_sym / d.S;

@@ -212,6 +212,7 @@ template <bool FUSED>
 __global__ void __launch_bounds__(CLK_TILE) k_pam_theta(RxDev d, long long b0, long long b1, long long blast,
                                                         long long launch_id) {
   extern __shared__ double2 Ct[];                 // [CLK_TILE + 1 + 2 h]: blocks base-1-h ..
+  pdl_wait();                                     // C_b from k_pam_fe
   __shared__ double th_sh[CLK_TILE + 1];
   __shared__ double wsum[CLK_TILE / 32];
   __shared__ long long wmax[CLK_TILE / 32];
@@ -394,6 +395,7 @@ __global__ void __launch_bounds__(256) k_pam_be(RxDev d, long long b0, long long
   __shared__ double red[FE_GROUPS][2];
   const int g = threadIdx.x >> 6, j = threadIdx.x & 63;
   tw_stage_async(tw, d.tw);   // waited for (tw_wait) before the first FFT pass
+  pdl_wait();                 // tau_b / M_b from the clock stage
   const long long b = b0 + (long long)blockIdx.x * FE_GROUPS + g;
   const bool act = b < b1;
   // the block's spectrum X stored by k_pam_fe (SURVEY §8(a) 'read back spectra' option):

@@ -631,6 +631,28 @@ static rx_status check_launch() {
 
 static unsigned gridc(long long n, int per) { return (unsigned)((n + per - 1) / per); }
 
+// Programmatic dependent launch (sm_90+): the kernel may be scheduled while the previous kernel of
+// the stream drains; it runs its independent prologue and then pdl_wait()s (common.cuh) before
+// reading what that kernel produced. Only used for kernels that call pdl_wait() before any
+// dependent access (KK stage 2, CFO periodogram and fine CFO; PAM clock and back-end; the
+// equaliser's post-processing chain).
+static bool g_no_pdl = getenv("RX_NO_PDL") != nullptr;
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  if (g_no_pdl) { k<<<grid, block, smem, s>>>(args...); return; }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 // tap padding KP in {4, 8, 16, 32} (compile-time) and the CPR flavour select the instance
 typedef void (*lms_seg_fn)(RxDev, int, int, unsigned char *, long long);
 typedef void (*lms_train_fn)(RxDev, int);
@@ -703,15 +725,15 @@ static void launch_lms_round(rx_handle *h, cudaStream_t s, unsigned char *labels
     KLAUNCH(h, RX_K_LMS, s, (lms_seg_kernel(d)<<<gridc(nseg, spc), 32 * wpc, 0, s>>>(d, flush, (int)nseg, labels, lab_cap)));
   if (d.family == RX_PAM) {
     // PAM segments wrote their labels and error counts; the prefix also adds the counters
-    KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_prefix<<<1, 1024, 0, s>>>(d, flush, (int)nseg)));
+    KLAUNCH(h, RX_K_LMS_POST, s, launch_pdl(k_lms_prefix, 1, 1024, 0, s, d, flush, (int)nseg));
   } else {
     // anchored quadrants (R-ANCHOR2): k_lms_final takes each R_s itself; the c-9 chain stitches first
     if (!d.anchor_each) KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_stitch<<<(unsigned)nseg, 256, 0, s>>>(d, (int)nseg)));
-    KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_prefix<<<1, 1024, 0, s>>>(d, flush, (int)nseg)));
-    KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_final<<<(unsigned)nseg, 256, 0, s>>>(d, labels, lab_cap, (int)nseg)));
-    KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_counters<<<1, 1024, 0, s>>>(d)));
+    KLAUNCH(h, RX_K_LMS_POST, s, launch_pdl(k_lms_prefix, 1, 1024, 0, s, d, flush, (int)nseg));
+    KLAUNCH(h, RX_K_LMS_POST, s, launch_pdl(k_lms_final, (unsigned)nseg, 256, 0, s, d, labels, lab_cap, (int)nseg));
+    KLAUNCH(h, RX_K_LMS_POST, s, launch_pdl(k_lms_counters, 1, 1024, 0, s, d));
   }
-  KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_seeds<<<(unsigned)(nseg * S / d.E_sym + 2), 1024, 0, s>>>(d, flush)));
+  KLAUNCH(h, RX_K_LMS_POST, s, launch_pdl(k_lms_seeds, (unsigned)(nseg * S / d.E_sym + 2), 1024, 0, s, d, flush));
 }
 
 // Equaliser rounds. Streaming: one round per call once ~lms_batch_segments may be pending
@@ -799,7 +821,7 @@ static void run_pam(rx_handle *h, cudaStream_t s, const InView &in, unsigned cha
     const unsigned ntiles = gridc(clk_target - h->clk_done, CLK_TILE);
     if (ntiles <= g_clk_fuse_max && ntiles <= CLK_FUSE_MAX) {   // every tile co-resident: one pass + carry
       const long long id = ++h->clk_launch;
-      KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_pam_theta<true><<<ntiles, CLK_TILE, smem, s>>>(d, h->clk_done, clk_target, h->fe_done - 1, id)));
+      KLAUNCH(h, RX_K_PAM_CLOCK, s, launch_pdl(k_pam_theta<true>, ntiles, CLK_TILE, smem, s, d, h->clk_done, clk_target, h->fe_done - 1, id));
     } else {
       KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_pam_theta<false><<<ntiles, CLK_TILE, smem, s>>>(d, h->clk_done, clk_target, h->fe_done - 1, 0)));
       KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_pam_carry<<<1, 1024, 0, s>>>(d, (int)ntiles)));
@@ -809,8 +831,8 @@ static void run_pam(rx_handle *h, cudaStream_t s, const InView &in, unsigned cha
   }
   long long be_target = flush ? h->fe_done - 1 : h->clk_done - 1;
   if (be_target > h->be_done) {
-    if (d.H_real) KLAUNCH(h, RX_K_PAM_BE, s, (k_pam_be<true><<<gridc(be_target - h->be_done, FE_GROUPS), 256, 0, s>>>(d, h->be_done, be_target)));
-    else KLAUNCH(h, RX_K_PAM_BE, s, (k_pam_be<false><<<gridc(be_target - h->be_done, FE_GROUPS), 256, 0, s>>>(d, h->be_done, be_target)));
+    if (d.H_real) KLAUNCH(h, RX_K_PAM_BE, s, launch_pdl(k_pam_be<true>, gridc(be_target - h->be_done, FE_GROUPS), 256, 0, s, d, h->be_done, be_target));
+    else KLAUNCH(h, RX_K_PAM_BE, s, launch_pdl(k_pam_be<false>, gridc(be_target - h->be_done, FE_GROUPS), 256, 0, s, d, h->be_done, be_target));
     h->be_done = be_target;
   }
   // streaming: the buffer normalisation runs on the equaliser side stream at the start of the
@@ -845,7 +867,7 @@ static void run_kk(rx_handle *h, cudaStream_t s, const InView &in, unsigned char
   }
   const long long s2_target = h->fe_done - 1;
   if (s2_target > h->s2_done) {
-    KLAUNCH(h, RX_K_KK_S2, s, (k_kk_s2<<<gridc(s2_target - h->s2_done, FE_GROUPS), 256, 0, s>>>(d, h->s2_done, s2_target)));
+    KLAUNCH(h, RX_K_KK_S2, s, launch_pdl(k_kk_s2, gridc(s2_target - h->s2_done, FE_GROUPS), 256, 0, s, d, h->s2_done, s2_target));
     h->s2_done = s2_target;
   }
   const long long q_front = h->s2_done > 0 ? 256 * h->s2_done - 128 : 0;
@@ -858,8 +880,8 @@ static void run_kk(rx_handle *h, cudaStream_t s, const InView &in, unsigned char
       const int fine_ctas = (int)((Q / 1024 + 7) / 8);
       for (long long b0 = 0; b0 < nbuf; b0 += h->cfg.history_buffers) {
         const long long nb = nbuf - b0 < h->cfg.history_buffers ? nbuf - b0 : h->cfg.history_buffers;
-        KLAUNCH(h, RX_K_CFO, s, (k_cfo_spec<<<dim3(CFO_ROWS, (unsigned)nb), CFO_SPEC_T, 0, s>>>(d, beta0 + b0, q_front)));
-        if (d.cfo_enable) KLAUNCH(h, RX_K_CFO, s, (k_cfo_fine<<<dim3((unsigned)fine_ctas, (unsigned)nb), 256, 0, s>>>(d, beta0 + b0, q_front, fine_ctas)));
+        KLAUNCH(h, RX_K_CFO, s, launch_pdl(k_cfo_spec, dim3(CFO_ROWS, (unsigned)nb), CFO_SPEC_T, 0, s, d, beta0 + b0, q_front));
+        if (d.cfo_enable) KLAUNCH(h, RX_K_CFO, s, launch_pdl(k_cfo_fine, dim3((unsigned)fine_ctas, (unsigned)nb), 256, 0, s, d, beta0 + b0, q_front, fine_ctas));
         if (flush || h->cfg.serial_equaliser) {
           KLAUNCH(h, RX_K_CFO, s, (k_cfo_carry<<<1, 1, 0, s>>>(d, beta0 + b0, (int)nb, q_front)));
         } else {   // the DDS carry (z' validity) only feeds the equaliser: next call, side stream

@@ -32,3 +32,35 @@ rx.update(buffer_blocks=32, input_format=2, q_window_symbols=4096)
 R, _, st = run_gpu(rec, rx, chunk=512 * 32)
 print("PAM packed", st["bit_errors"], st["bits"], R.q_trace(0, 4)[0].tolist())
 print("thresholds", R.calibrate_thresholds(rx["train_symbols"] + 4096, 8192)[0].tolist())
+# round-2 paths: BPS equaliser (C4 structure), data-aided and per-symbol DDLMS modes, time sharding
+rec, rx = make_config("C4", n_samples=1 << 18)
+rx.update(buffer_blocks=128, train_symbols=4096, warmup_symbols=8192)
+_, _, st = run_gpu(rec, rx, chunk=512 * 128)
+print("KK BPS", st["bit_errors"], st["bits"], st["status_flags"])
+for mode, extra in ((1, {}), (2, dict(lms_block=1, lms_taps=4, widely_linear=1))):
+    rec, rx = make_config("C3", n_samples=1 << 18, linewidth_hz=1e3)
+    rx.update(buffer_blocks=128, train_symbols=4096, warmup_symbols=8192, lms_mode=mode, **extra)
+    _, _, st = run_gpu(rec, rx, chunk=512 * 128)
+    print("KK lms_mode", mode, st["bit_errors"], st["bits"], st["status_flags"])
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+from paper_2011_13695_b200 import RX_QAM_KK, Receiver, multi  # noqa: E402
+rec, rx = make_config("C4", n_samples=6 * 128 * 512)
+fields = {k: v for k, v in rx.items() if k in ("lms_taps", "lms_block", "lms_segment", "lms_overlap", "mu",
+                                               "cpr_test_phases", "sync_start", "sync_window")}
+hs = [Receiver(RX_QAM_KK, rec.M, rec.static_taps, dc_offset=rec.dc_offset, history_buffers=4, buffer_blocks=128,
+               train_symbols=4096, warmup_symbols=8192, shard_count=2, shard_index=g, **fields) for g in range(2)]
+codes = torch.from_numpy(rec.codes.view(np.int16)).cuda()
+labs = [torch.zeros(rec.n // 4 + 4096, dtype=torch.uint8, device="cuda") for _ in range(2)]
+recs = [torch.zeros(hs[0].carry_size(), dtype=torch.uint8, device="cuda") for _ in range(2)]
+nbuf = rec.n // (128 * 512)
+for r in range(nbuf // 2 + 1):
+    for g in range(2):
+        b = 2 * r + g
+        if b < nbuf:
+            p0, p1, last = multi.shard_inputs(rec.n, 128 * 512, b, 4096, 4096)
+            hs[g].shard_process(b, codes[p0:p1], last=last, labels=labs[g])
+        hs[g].export_carry(recs[g])
+    for g in range(2):
+        hs[g].import_carry(torch.cat(recs), 2, g)
+print("KK 2 shards", [h.stats()["bits"] for h in hs])
