@@ -18,6 +18,8 @@ from .rx import (  # noqa: F401
     RxConfig,
     RxError,
     RxStats,
+    Transmitter,
+    TxConfig,
     default_config,
     load,
 )

@@ -52,6 +52,21 @@ class RxConfig(ctypes.Structure):
     ]
 
 
+class TxConfig(ctypes.Structure):
+    """include/tx.h tx_config (GPU transmitter + channel simulator)."""
+    _fields_ = [
+        ("family", ctypes.c_int), ("order", ctypes.c_int),
+        ("baud", ctypes.c_double), ("sample_rate", ctypes.c_double),
+        ("prbs_seed", ctypes.c_uint), ("symbol_offset", _c_ll),
+        ("shaping_taps", _c_dp), ("n_shaping_taps", ctypes.c_int),
+        ("clock_ppm", ctypes.c_double), ("tone_amp", ctypes.c_double), ("carrier_hz", ctypes.c_double),
+        ("cfo_hz", ctypes.c_double), ("linewidth_hz", ctypes.c_double),
+        ("iq_re", ctypes.c_double), ("iq_im", ctypes.c_double), ("noise_sigma", ctypes.c_double),
+        ("adc_mean", ctypes.c_double), ("adc_full_scale", ctypes.c_double),
+        ("noise_seed", ctypes.c_ulonglong),
+    ]
+
+
 class RxStats(ctypes.Structure):
     _fields_ = [
         ("samples_in", _c_ll), ("symbols_out", _c_ll),
@@ -70,7 +85,7 @@ EXPORTS = ("rx_config_default", "rx_create", "rx_process", "rx_flush", "rx_get_s
            "rx_version", "rx_profile_enable", "rx_profile_read", "rx_export_counters",
            "rx_set_taps", "rx_get_q_trace", "rx_calibrate_thresholds", "rx_calibrate_dc",
            "rx_design_static_eq", "rx_shard_process", "rx_carry_size", "rx_export_carry",
-           "rx_import_carry")
+           "rx_import_carry", "tx_create", "tx_generate", "tx_destroy")
 SHARD_PRE, SHARD_POST = 4096, 4096       # RX_SHARD_PRE / RX_SHARD_POST (include/rx.h)
 NCOUNTERS = 8
 COUNTERS = ("bit_errors", "bits", "symbols_counted", "evm_num", "evm_den", "clipped",
@@ -127,6 +142,12 @@ def load(path: str = SO_PATH):
     lib.rx_import_carry.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int, vp]
     for f in ("rx_shard_process", "rx_carry_size", "rx_export_carry", "rx_import_carry"):
         getattr(lib, f).restype = ctypes.c_int
+    lib.tx_create.argtypes = [ctypes.POINTER(TxConfig), ctypes.c_int, ctypes.POINTER(vp)]
+    lib.tx_create.restype = ctypes.c_int
+    lib.tx_generate.argtypes = [vp, vp, _c_ll, vp]
+    lib.tx_generate.restype = ctypes.c_int
+    lib.tx_destroy.argtypes = [vp]
+    lib.tx_destroy.restype = None
     for f in ("rx_create", "rx_process", "rx_flush", "rx_get_stats", "rx_reset_stats",
               "rx_get_taps", "rx_set_taps", "rx_probe_read", "rx_profile_enable", "rx_profile_read"):
         getattr(lib, f).restype = ctypes.c_int
@@ -372,3 +393,53 @@ def design_static_eq(h_channel, h_target, lam: float, n_taps: int, real_taps: bo
     _check(lib.rx_design_static_eq(a.ctypes.data_as(_c_dp), b.ctypes.data_as(_c_dp), float(lam), int(n_taps),
                                    int(bool(real_taps)), out.ctypes.data_as(_c_dp)), "rx_design_static_eq")
     return out if real_taps else out[0::2] + 1j * out[1::2]
+
+
+class Transmitter:
+    """GPU transmitter + channel simulator (include/tx.h): generates the 12-bit
+    ADC stream of the paper's PAM / KK-QAM set-ups on the device.
+
+    Transmitter(family, order, shaping_taps, device=0, **tx_config fields)"""
+
+    def __init__(self, family: int, order: int, shaping_taps, device: int = 0, **fields):
+        lib = load()
+        cfg = TxConfig()
+        cfg.family, cfg.order = family, order
+        cfg.baud = 2e9 if family == RX_PAM else 1e9
+        cfg.sample_rate = 4e9
+        cfg.prbs_seed = 0x7FFF
+        cfg.carrier_hz = 0.547e9
+        cfg.adc_full_scale = 1.0
+        taps = np.asarray(shaping_taps)
+        if family == RX_QAM_KK:
+            buf = np.ascontiguousarray(np.stack([taps.real, taps.imag], axis=-1).reshape(-1), dtype=np.float64)
+            cfg.n_shaping_taps = buf.shape[0] // 2
+        else:
+            buf = np.ascontiguousarray(taps.real, dtype=np.float64)
+            cfg.n_shaping_taps = buf.shape[0]
+        self._taps = buf
+        cfg.shaping_taps = buf.ctypes.data_as(_c_dp)
+        for k, v in fields.items():
+            if not hasattr(cfg, k):
+                raise TypeError(f"unknown tx_config field {k}")
+            setattr(cfg, k, v)
+        self.cfg = cfg
+        h = ctypes.c_void_p()
+        _check(lib.tx_create(ctypes.byref(cfg), device, ctypes.byref(h)), "tx_create")
+        self._h = h
+
+    def generate(self, out, stream=None):
+        """Fill `out` (uint16 / int16 CUDA tensor, length a multiple of 512) with the next codes."""
+        _check(load().tx_generate(self._h, ctypes.c_void_p(out.data_ptr()), int(out.numel()), _stream_ptr(stream)),
+               "tx_generate")
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load().tx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -17,9 +17,12 @@ def lib():
 
 
 def _declared_functions():
-    src = open(os.path.join(ROOT, "include", "rx.h")).read()
-    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(rx_[a-z_]+)\s*\(", src)))
+    out = set()
+    for hdr in ("rx.h", "tx.h"):
+        src = open(os.path.join(ROOT, "include", hdr)).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        out |= set(re.findall(r"\b((?:rx|tx)_[a-z_]+)\s*\(", src))
+    return sorted(out)
 
 
 def test_header_declares_the_north_star_calls():
@@ -170,3 +173,32 @@ def test_struct_sizes_match_a_c_compiler(tmp_path):
     want = [ctypes.sizeof(rx.RxConfig), rx.RxConfig.q_window_symbols.offset, rx.RxConfig.shard_index.offset,
             ctypes.sizeof(rx.RxStats), rx.RxStats.launches.offset]
     assert got == want
+
+
+def test_tx_struct_layout_and_validation(tmp_path, lib):
+    """tx_config (include/tx.h) mirrors the C layout (gcc), and tx_create rejects bad configs
+    before touching the GPU (odd / too long shaping FIR, wrong sps, KK with a clock offset)."""
+    import subprocess
+    import numpy as np
+    from paper_2011_13695_b200 import rx
+    src = tmp_path / "tx.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "tx.h"\nint main(void){'
+                   'printf("%zu %zu %zu\\n", sizeof(tx_config), offsetof(tx_config, noise_sigma),'
+                   'offsetof(tx_config, noise_seed));return 0;}\n')
+    exe = tmp_path / "tx"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)], check=True)
+    got = list(map(int, subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()))
+    assert got == [ctypes.sizeof(rx.TxConfig), rx.TxConfig.noise_sigma.offset, rx.TxConfig.noise_seed.offset]
+    taps = np.ones(31)
+    h = ctypes.c_void_p()
+    for kw in (dict(n_shaping_taps=30), dict(n_shaping_taps=515), dict(baud=1e9), dict(order=3),
+               dict(adc_full_scale=0.0), dict(family=1, order=16, clock_ppm=5.0)):
+        c = rx.TxConfig()
+        c.family, c.order, c.baud, c.sample_rate, c.prbs_seed = 0, 4, 2e9, 4e9, 0x7FFF
+        c.shaping_taps = taps.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        c.n_shaping_taps, c.adc_full_scale = 31, 1.0
+        for k, v in kw.items():
+            setattr(c, k, v)
+        if c.family == 1:
+            c.baud = 1e9
+        assert lib.tx_create(ctypes.byref(c), 0, ctypes.byref(h)) == -1, kw
