@@ -236,7 +236,8 @@ class Stream1:
         self.k += 1
 
 
-def run_mode(torch, dist, R, ring, n_step, steps, warmup, world, dev, chunk=CHUNK, with_profile=True):
+def run_mode(torch, dist, R, ring, n_step, steps, warmup, world, dev, chunk=CHUNK, with_profile=True,
+             monitor=False):
     """Warm up, profile the kernel classes (untimed), then time `steps` steps."""
     from paper_2011_13695_b200 import multi
     stream = torch.cuda.Stream(device=dev)
@@ -270,6 +271,8 @@ def run_mode(torch, dist, R, ring, n_step, steps, warmup, world, dev, chunk=CHUN
     torch.cuda.synchronize(dev)
     clocks = ClockSampler(dev.index if dev.index is not None else 0)
     clocks.start()
+    if monitor:
+        R.rt_enable(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     th0 = time.perf_counter()
@@ -279,6 +282,10 @@ def run_mode(torch, dist, R, ring, n_step, steps, warmup, world, dev, chunk=CHUN
     e1.record(stream)
     torch.cuda.synchronize(dev)
     clk = clocks.stop()
+    rt = None
+    if monitor:
+        rt = R.rt_stats()
+        R.rt_enable(False)
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
@@ -294,7 +301,7 @@ def run_mode(torch, dist, R, ring, n_step, steps, warmup, world, dev, chunk=CHUN
         if dominant in prof:
             dom = dict(name=dominant, ms=prof[dominant][0], launches=prof[dominant][1])
     return dict(ms=ms_max, clocks=clk, breakdown=breakdown, dominant=dom, host_ms=host_ms,
-                launches=st1["launches"] - st0["launches"], stats=st1, counters=cnt.cpu().tolist())
+                launches=st1["launches"] - st0["launches"], stats=st1, counters=cnt.cpu().tolist(), rt=rt)
 
 
 def e2e_run(torch, R, n_step, host_codes, steps, dev, packed=False, world=1, dist=None):
@@ -763,11 +770,15 @@ def gpu_main(args):
         for lag in (1, 0):
             R1 = make_kk(history_buffers=3, equaliser_lag=lag)
             ks = max(3, args.steps // 2)
-            r1 = run_mode(torch, None, R1, ring4, n4, ks, 3, 1, dev, chunk=BUFFER, with_profile=False)
+            r1 = run_mode(torch, None, R1, ring4, n4, ks, 3, 1, dev, chunk=BUFFER, with_profile=False, monitor=True)
             R1.close()
             v1 = n4 * ks / (r1["ms"] / 1e3) / 1e9
+            rt = r1["rt"] or {}
             pb[lag] = {"value": round(v1, 3), "ms_per_buffer": round(r1["ms"] / ks / (n4 // BUFFER), 4),
-                       "host_enqueue_ms_per_buffer": round(r1["host_ms"] / (n4 // BUFFER), 4)}
+                       "host_enqueue_ms_per_buffer": round(r1["host_ms"] / (n4 // BUFFER), 4),
+                       "rt_monitor": {"calls": rt.get("calls"), "realtime_ratio": round(rt.get("realtime_ratio", 0), 3),
+                                      "max_call_ms": round(rt.get("max_call_ms", 0), 4),
+                                      "max_load": round(rt.get("max_load", 0), 4), "overruns": rt.get("overruns")}}
         line["per_buffer_call"] = dict(pb[1], unit="GSa/s", call_samples=BUFFER, equaliser_lag=1,
                                        realtime_ratio=round(pb[1]["value"] / PAPER_REALTIME_GSA, 2),
                                        equaliser_lag_0=pb[0])

@@ -344,6 +344,21 @@ rx_status rx_carry_size(const rx_handle *h, int *bytes);
 rx_status rx_export_carry(rx_handle *h, void *d_buf, void *cuda_stream);
 rx_status rx_import_carry(rx_handle *h, const void *d_gathered, int n_ranks, int my_rank, void *cuda_stream);
 
+/* ---- Real-time monitor (the paper's real-time budget: one 2^22-sample
+ * buffer per 1.049 ms at 4 GSa/s) -------------------------------------------------------
+ * rx_rt_enable(h, 1) brackets every later rx_process call with CUDA events on its stream;
+ * rx_get_rt_stats synchronises them and reports, over the calls since the last read: the count,
+ * samples, summed span busy_ms, the longest call, max_load = max_k span_k / budget_k (budget =
+ * n_k / sample_rate), overruns (calls slower than their budget) and realtime_ratio = (total
+ * budget) / busy_ms (> 1: faster than real time). A call's span is its time on the caller's
+ * stream (front end, the CFO / clock stages and the joined equaliser stage, per equaliser_lag). */
+typedef struct {
+  long long calls, samples, overruns;
+  double busy_ms, max_call_ms, max_load, realtime_ratio;
+} rx_rt_stats;
+rx_status rx_rt_enable(rx_handle *h, int on);
+rx_status rx_get_rt_stats(rx_handle *h, rx_rt_stats *host_out);
+
 void rx_destroy(rx_handle *h);
 const char *rx_strerror(int status);
 

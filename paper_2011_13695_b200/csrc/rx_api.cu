@@ -141,6 +141,12 @@ struct rx_handle {
   int prof_mask;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_pending;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_free;
+  // real-time monitor (rx_rt_enable): per streaming call, events at its first and last operation
+  // on the caller's stream and the call's sample count
+  int rt_on;
+  struct RtCall { cudaEvent_t a, b; long long n; };
+  std::vector<RtCall> rt_pending;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> rt_free;
 };
 
 static void prof_begin(rx_handle *h, int cls, cudaStream_t s, cudaEvent_t *stop) {
@@ -320,6 +326,8 @@ extern "C" void rx_destroy(rx_handle *h) {
   for (int i = 0; i < 2; ++i) if (h->ev_join[i]) cudaEventDestroy(h->ev_join[i]);
   for (auto &e : h->prof_pending) { cudaEventDestroy(e.second.first); cudaEventDestroy(e.second.second); }
   for (auto &e : h->prof_free) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+  for (auto &e : h->rt_pending) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
+  for (auto &e : h->rt_free) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   delete h;
 }
 
@@ -954,6 +962,12 @@ extern "C" rx_status rx_process(rx_handle *h, const void *d_samples, long long n
   if (h->flushed || h->d.shard_n > 1) return RX_ESTATE;
   CK(cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)stream;
+  std::pair<cudaEvent_t, cudaEvent_t> rt_ev(nullptr, nullptr);
+  if (h->rt_on) {   // real-time monitor: the call's span on the caller's stream
+    if (!h->rt_free.empty()) { rt_ev = h->rt_free.back(); h->rt_free.pop_back(); }
+    else { CK(cudaEventCreate(&rt_ev.first)); CK(cudaEventCreate(&rt_ev.second)); }
+    CK(cudaEventRecord(rt_ev.first, s));
+  }
   if (h->cfg.input_format == RX_IN_U12_PACKED && n > 0) {   // unpack the call into the staging buffer
     KLAUNCH(h, RX_K_MISC, s, (k_unpack12<<<gridc(n / 8, 256) < 4096 ? gridc(n / 8, 256) : 4096, 256, 0, s>>>(
                                  (const uint32_t *)d_samples, (uint4 *)h->unpacked, n / 8)));
@@ -979,6 +993,10 @@ extern "C" rx_status rx_process(rx_handle *h, const void *d_samples, long long n
     if (h->cfg.equaliser_lag == 0) CK(cudaStreamWaitEvent(s, h->ev_join[h->ncall & 1], 0));
     else if (h->ncall > 0) CK(cudaStreamWaitEvent(s, h->ev_join[(h->ncall - 1) & 1], 0));
     h->ncall++;
+  }
+  if (rt_ev.first) {
+    CK(cudaEventRecord(rt_ev.second, s));
+    h->rt_pending.push_back({rt_ev.first, rt_ev.second, n});
   }
   return check_launch();
 }
@@ -1414,4 +1432,38 @@ extern "C" rx_status rx_export_counters(rx_handle *h, double *d_out, void *strea
   join_side(h, s);
   KLAUNCH(h, RX_K_MISC, s, (k_export_counters<<<1, 1, 0, s>>>(h->st_dev, d_out)));
   return check_launch();
+}
+
+// ------------------------------------------------------------------ real-time monitor (NEXT-2)
+extern "C" rx_status rx_rt_enable(rx_handle *h, int on) {
+  if (!h || (on != 0 && on != 1)) return RX_EINVAL;
+  h->rt_on = on;
+  return RX_OK;
+}
+
+// Per streaming call k: span d_k (ms) between its first and last operation on the caller's stream
+// (CUDA events) against its real-time budget n_k / sample_rate; overrun when d_k exceeds it.
+extern "C" rx_status rx_get_rt_stats(rx_handle *h, rx_rt_stats *o) {
+  if (!h || !o) return RX_EINVAL;
+  CK(cudaSetDevice(h->device));
+  memset(o, 0, sizeof(*o));
+  double busy = 0.0, budget = 0.0;
+  for (auto &c : h->rt_pending) {
+    CK(cudaEventSynchronize(c.b));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c.a, c.b));
+    const double bud = (double)c.n / h->cfg.sample_rate * 1e3;
+    o->calls += 1;
+    o->samples += c.n;
+    busy += ms;
+    budget += bud;
+    if (ms > o->max_call_ms) o->max_call_ms = ms;
+    if (bud > 0.0 && ms / bud > o->max_load) o->max_load = ms / bud;
+    if (ms > bud) o->overruns += 1;
+    h->rt_free.push_back({c.a, c.b});
+  }
+  h->rt_pending.clear();
+  o->busy_ms = busy;
+  o->realtime_ratio = busy > 0.0 ? budget / busy : 0.0;
+  return RX_OK;
 }

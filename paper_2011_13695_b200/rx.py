@@ -52,6 +52,11 @@ class RxConfig(ctypes.Structure):
     ]
 
 
+class RtStats(ctypes.Structure):
+    _fields_ = [("calls", _c_ll), ("samples", _c_ll), ("overruns", _c_ll), ("busy_ms", ctypes.c_double),
+                ("max_call_ms", ctypes.c_double), ("max_load", ctypes.c_double), ("realtime_ratio", ctypes.c_double)]
+
+
 class TxConfig(ctypes.Structure):
     """include/tx.h tx_config (GPU transmitter + channel simulator)."""
     _fields_ = [
@@ -85,7 +90,7 @@ EXPORTS = ("rx_config_default", "rx_create", "rx_process", "rx_flush", "rx_get_s
            "rx_version", "rx_profile_enable", "rx_profile_read", "rx_export_counters",
            "rx_set_taps", "rx_get_q_trace", "rx_calibrate_thresholds", "rx_calibrate_dc",
            "rx_design_static_eq", "rx_shard_process", "rx_carry_size", "rx_export_carry",
-           "rx_import_carry", "tx_create", "tx_generate", "tx_destroy")
+           "rx_import_carry", "rx_rt_enable", "rx_get_rt_stats", "tx_create", "tx_generate", "tx_destroy")
 SHARD_PRE, SHARD_POST = 4096, 4096       # RX_SHARD_PRE / RX_SHARD_POST (include/rx.h)
 NCOUNTERS = 8
 COUNTERS = ("bit_errors", "bits", "symbols_counted", "evm_num", "evm_den", "clipped",
@@ -142,6 +147,10 @@ def load(path: str = SO_PATH):
     lib.rx_import_carry.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int, vp]
     for f in ("rx_shard_process", "rx_carry_size", "rx_export_carry", "rx_import_carry"):
         getattr(lib, f).restype = ctypes.c_int
+    lib.rx_rt_enable.argtypes = [vp, ctypes.c_int]
+    lib.rx_rt_enable.restype = ctypes.c_int
+    lib.rx_get_rt_stats.argtypes = [vp, ctypes.POINTER(RtStats)]
+    lib.rx_get_rt_stats.restype = ctypes.c_int
     lib.tx_create.argtypes = [ctypes.POINTER(TxConfig), ctypes.c_int, ctypes.POINTER(vp)]
     lib.tx_create.restype = ctypes.c_int
     lib.tx_generate.argtypes = [vp, vp, _c_ll, vp]
@@ -331,6 +340,17 @@ class Receiver:
         if per > 1:
             return out.reshape(count, per)
         return out
+
+    def rt_enable(self, on: bool = True):
+        """Real-time monitor (rx_rt_enable): time every later rx_process call on its stream."""
+        _check(load().rx_rt_enable(self._h, int(bool(on))), "rx_rt_enable")
+
+    def rt_stats(self) -> dict:
+        """rx_get_rt_stats: calls, samples, busy_ms, max_call_ms, max_load, overruns,
+        realtime_ratio since the last read."""
+        st = RtStats()
+        _check(load().rx_get_rt_stats(self._h, ctypes.byref(st)), "rx_get_rt_stats")
+        return {k: getattr(st, k) for k, _ in RtStats._fields_}
 
     def profile_enable(self, classes=KCLASSES):
         mask = 0

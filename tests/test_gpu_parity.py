@@ -946,3 +946,39 @@ def test_per_symbol_wl_ddlms_parity(name, extra):
     _compare_counters(rec, out, st, mism)
     print(f"{name} per-symbol WL DDLMS: BER {st['bit_errors']}/{st['bits']}, "
           f"EVM {evm_db(st['evm_num'], st['evm_den']):.2f} dB")
+
+
+def test_realtime_monitor_reports_every_call():
+    """rx_rt_enable / rx_get_rt_stats (NEXT-2, the paper's real-time budget P:116): one paper
+    buffer per call of a C3-structure stream; the monitor reports every call and sample, spans
+    that add up to the stream time the CUDA events around the calls measure, and a real-time
+    ratio = (samples / 4 GSa/s) / busy time consistent with them."""
+    torch = _torch_cuda()
+    from paper_2011_13695_b200 import RX_QAM_KK, Receiver
+    rec, rx = make_config("C3", n_samples=8 * 256 * 512)
+    fields = {k: v for k, v in rx.items() if k in ("lms_taps", "lms_block", "lms_segment", "lms_overlap", "mu",
+                                                   "train_symbols", "sync_start", "sync_window",
+                                                   "warmup_symbols", "cpr_test_phases")}
+    R = Receiver(RX_QAM_KK, rec.M, rec.static_taps, dc_offset=rec.dc_offset, buffer_blocks=256,
+                 history_buffers=3, **fields)
+    codes = torch.from_numpy(rec.codes.view(np.int16)).cuda()
+    lab = torch.zeros(rec.n, dtype=torch.uint8, device="cuda")
+    R.process(codes[:256 * 512], lab)                        # start-up call, not monitored
+    torch.cuda.synchronize()
+    R.rt_enable(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for off in range(256 * 512, rec.n, 256 * 512):
+        R.process(codes[off:off + 256 * 512], lab)
+    e1.record()
+    torch.cuda.synchronize()
+    rt = R.rt_stats()
+    total_ms = e0.elapsed_time(e1)
+    print(rt, f"stream {total_ms:.3f} ms")
+    assert rt["calls"] == 7 and rt["samples"] == 7 * 256 * 512
+    assert rt["busy_ms"] <= total_ms * 1.01 and rt["busy_ms"] >= 0.5 * total_ms
+    budget = 7 * 256 * 512 / 4e9 * 1e3
+    assert abs(rt["realtime_ratio"] - budget / rt["busy_ms"]) < 1e-6 * rt["realtime_ratio"]
+    assert rt["max_call_ms"] * 7 >= rt["busy_ms"] - 1e-6
+    assert R.rt_stats()["calls"] == 0                         # read resets
+    R.close()
