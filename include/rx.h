@@ -146,6 +146,10 @@ typedef struct {
                                  fed with rx_shard_process (see below). Requires family KK,
                                  cpr_anchor = 1 and N <= tap_lag_epochs */
   int shard_index;
+  int cuda_graphs;            /* 1 (default): a streaming equaliser round (segment recursion +
+                                 stitching / labels / counters / seeds) is captured once as a CUDA
+                                 graph and replayed per round (its kernels read every per-round
+                                 quantity from device state); 0: launched kernel by kernel */
 } rx_config;
 
 /* Sample formats accepted by rx_process:

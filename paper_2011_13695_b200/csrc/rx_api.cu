@@ -141,6 +141,13 @@ struct rx_handle {
   int prof_mask;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_pending;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_free;
+  // CUDA graph of one streaming equaliser round (cuda_graphs = 1): its kernels read every
+  // per-round quantity from the device state, so one capture (fixed grid, the labels buffer
+  // as captured) replays for every round
+  cudaGraphExec_t lms_graph;
+  unsigned char *lms_graph_labels;
+  long long lms_graph_cap, lms_graph_nseg;
+  int lms_graph_kernels;
   // real-time monitor (rx_rt_enable): per streaming call, events at its first and last operation
   // on the caller's stream and the call's sample count
   int rt_on;
@@ -226,6 +233,7 @@ extern "C" void rx_config_default(rx_config *c, int family, int order) {
   c->sync_min_corr = 0.3;
   c->history_buffers = 3;
   c->lms_batch_segments = family == RX_PAM ? 4096 : 2048;   // D epochs (one round each)
+  c->cuda_graphs = 1;
 }
 
 extern "C" const char *rx_strerror(int s) {
@@ -284,6 +292,7 @@ static rx_status validate(const rx_config *c) {
   if (c->cpr_anchor != 0 && c->cpr_anchor != 1) return RX_EINVAL;
   if (c->lms_mode < 0 || c->lms_mode > 2) return RX_EINVAL;
   if (c->equaliser_lag != 0 && c->equaliser_lag != 1) return RX_EINVAL;
+  if (c->cuda_graphs != 0 && c->cuda_graphs != 1) return RX_EINVAL;
   if (c->shard_count < 0 || c->shard_count > 64) return RX_EINVAL;
   if (c->shard_count > 1) {        // time sharding (SURVEY §8(e) mode 2): the KK chain
     if (c->family != RX_QAM_KK || c->cpr_anchor != 1 || c->shard_count > c->tap_lag_epochs) return RX_EINVAL;
@@ -326,6 +335,7 @@ extern "C" void rx_destroy(rx_handle *h) {
   for (int i = 0; i < 2; ++i) if (h->ev_join[i]) cudaEventDestroy(h->ev_join[i]);
   for (auto &e : h->prof_pending) { cudaEventDestroy(e.second.first); cudaEventDestroy(e.second.second); }
   for (auto &e : h->prof_free) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+  if (h->lms_graph) cudaGraphExecDestroy(h->lms_graph);
   for (auto &e : h->rt_pending) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
   for (auto &e : h->rt_free) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   delete h;
@@ -744,6 +754,38 @@ static void launch_lms_round(rx_handle *h, cudaStream_t s, unsigned char *labels
   KLAUNCH(h, RX_K_LMS_POST, s, launch_pdl(k_lms_seeds, (unsigned)(nseg * S / d.E_sym + 2), 1024, 0, s, d, flush));
 }
 
+// A streaming equaliser round as a CUDA graph (NEXT-2): captured once with a fixed grid that covers
+// any streaming round's segments (the kernels take seg_next / fin_lo / fin_hi from the device
+// state and skip what is not ready), then replayed with one cudaGraphLaunch per round. Not used
+// while tracing (rx_profile_enable) or with RX_DEBUG_SYNC; re-captured if the labels buffer moves.
+static bool lms_graph_round(rx_handle *h, cudaStream_t s, unsigned char *labels, long long lab_cap, long long nseg) {
+  if (!h->cfg.cuda_graphs || h->prof_mask || g_rx_debug) return false;
+  RxDev &d = h->d;
+  if (!h->lms_graph || labels != h->lms_graph_labels || lab_cap != h->lms_graph_cap || nseg > h->lms_graph_nseg) {
+    if (h->lms_graph) { cudaGraphExecDestroy(h->lms_graph); h->lms_graph = nullptr; }
+    long long ng = nseg + (long long)d.E_sym / d.S;    // headroom over this round's grid
+    if (ng > d.seg_cap / 2) ng = d.seg_cap / 2;
+    if (ng < nseg) return false;
+    cudaGraph_t g = nullptr;
+    if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) { cudaGetLastError(); return false; }
+    const long long l0 = h->launches;
+    launch_lms_round(h, s, labels, lab_cap, 0, ng);
+    const int nk = (int)(h->launches - l0);
+    h->launches = l0;
+    if (cudaStreamEndCapture(s, &g) != cudaSuccess || !g) { cudaGetLastError(); return false; }
+    const cudaError_t e = cudaGraphInstantiate(&h->lms_graph, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) { cudaGetLastError(); h->lms_graph = nullptr; return false; }
+    h->lms_graph_labels = labels;
+    h->lms_graph_cap = lab_cap;
+    h->lms_graph_nseg = ng;
+    h->lms_graph_kernels = nk;
+  }
+  if (cudaGraphLaunch(h->lms_graph, s) != cudaSuccess) return false;
+  h->launches += h->lms_graph_kernels;
+  return true;
+}
+
 // Equaliser rounds. Streaming: one round per call once ~lms_batch_segments may be pending
 // (a batch spans fewer than D epochs, so every lag-D seed it needs was finalised by an earlier
 // round). Flush: rounds until every segment is final (each round can unlock the next D epochs;
@@ -778,7 +820,8 @@ static void launch_lms_rounds(rx_handle *h, cudaStream_t s, unsigned char *label
     const long long backlog = seg_ub - h->lms_fin_est;
     long long rounds = (backlog + per_round / 2) / per_round;
     if (rounds < 1) rounds = 1;
-    for (long long r = 0; r < rounds; ++r) launch_lms_round(h, s, labels, lab_cap, flush, nseg);
+    for (long long r = 0; r < rounds; ++r)
+      if (!lms_graph_round(h, s, labels, lab_cap, nseg)) launch_lms_round(h, s, labels, lab_cap, flush, nseg);
     h->lms_fin_est += rounds * per_round;
     if (h->lms_fin_est > seg_ub) h->lms_fin_est = seg_ub;
     return;

@@ -49,6 +49,7 @@ class RxConfig(ctypes.Structure):
         ("lms_mode", ctypes.c_int),
         ("equaliser_lag", ctypes.c_int),
         ("shard_count", ctypes.c_int), ("shard_index", ctypes.c_int),
+        ("cuda_graphs", ctypes.c_int),
     ]
 
 

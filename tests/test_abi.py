@@ -141,7 +141,7 @@ def test_round2_config_fields_validated_before_touching_the_gpu(lib):
         for k, v in kw.items():
             setattr(c, k, v)
         return c
-    for kw in (dict(lms_mode=2), dict(equaliser_lag=2), dict(shard_count=9),           # 9 > D = 8
+    for kw in (dict(lms_mode=3), dict(equaliser_lag=2), dict(cuda_graphs=2), dict(shard_count=9),   # 9 > D = 8
                dict(shard_count=4, shard_index=4), dict(shard_count=4, shard_index=-1),
                dict(shard_count=4, cpr_anchor=0), dict(shard_count=-1)):
         assert lib.rx_create(ctypes.byref(kk(**kw)), 0, ctypes.byref(h)) == -1, kw

@@ -806,8 +806,9 @@ def test_format_ordering_spec_criterion_7():
 @pytest.mark.parametrize("name", ["C2", "C4"])
 def test_randomised_scheduling_spec_criterion_10(name):
     """SPEC acceptance 10 (determinism under parallelism), scaled to 8 buffers: 20 runs with random
-    call sizes (multiples of 512 up to the call limit), random equaliser batch sizes and the side
-    stream on or off give byte-identical labels and identical integer counters."""
+    call sizes (multiples of 512 up to the call limit), random equaliser batch sizes, the side
+    stream on or off, equaliser_lag 0 / 1 and CUDA-graph rounds on or off give byte-identical
+    labels and identical integer counters."""
     torch = _torch_cuda()
     from paper_2011_13695_b200 import RX_PAM, RX_QAM_KK, Receiver
     rec, rx = make_config(name, n_samples=8 * 256 * 512)
@@ -824,7 +825,8 @@ def test_randomised_scheduling_spec_criterion_10(name):
         hb = int(rng.integers(3, 7))
         R = Receiver(fam, rec.M, rec.static_taps, buffer_blocks=256, history_buffers=hb,
                      lms_batch_segments=int(rng.choice([0, 1, 7, 64, 300])),
-                     serial_equaliser=int(rng.integers(0, 2)), **fields)
+                     serial_equaliser=int(rng.integers(0, 2)), equaliser_lag=int(rng.integers(0, 2)),
+                     cuda_graphs=int(rng.integers(0, 2)), **fields)
         lab = torch.zeros(rec.n, dtype=torch.uint8, device="cuda")
         max_blocks = (hb - 2) * 256
         off = 0
