@@ -28,15 +28,21 @@ for r in reps:
                   + run([os.path.join(tools, "ncu_opmix.py"), r]))
 open(os.path.join(d, "ncu_full_summary.jsonl"), "w").write("".join(summ))
 open(os.path.join(d, "ncu_stalls_opmix.txt"), "w").write("\n".join(stalls))
-CLASS = {"k_lms_seg<0": "LMS", "k_pam_be": "PAM_BE", "k_pam_fe": "PAM_FE", "k_norm_stats": "NORM",
-         "k_kk_s1": "KK_S1", "k_kk_s2": "KK_S2", "k_cfo_spec": "CFO", "k_lms_seg<1": "KK_LMS",
-         "k_lms_prefix": "LMS_POST"}
+# ncu kernel -> the bench.py kernel class whose roofline "traffic" it supplies (bench looks up
+# <family>_<class>: prof_kk_* reports come from the C4 KK run, the others from the C2 PAM run)
+CLASS = {"k_lms_seg<0": "LMS", "k_lms_seg<1": "LMS", "k_pam_be": "PAM_BE", "k_pam_fe": "PAM_FE",
+         "k_pam_theta": "PAM_CLOCK", "k_norm_stats": "NORM", "k_kk_s1": "KK_S1", "k_kk_s2": "KK_S2",
+         "k_cfo_spec": "CFO", "k_lms_prefix": "LMS_POST", "k_lms_final": "LMS_POST"}
 traffic = {}
 for line in "".join(summ).splitlines():
     j = json.loads(line)
     name = j.get("Kernel Name", "")
-    cls = next((v for k, v in CLASS.items() if k in name.replace("void ", "")), None)
-    if not cls or cls in traffic:
+    norm = name.replace("void ", "").replace("(bool)", "").replace("false", "0").replace("true", "1")
+    cls = next((v for k, v in CLASS.items() if norm.startswith(k)), None)
+    if not cls:
+        continue
+    cls = ("KK_" if "prof_kk_" in j.get("report", "") else "PAM_") + cls
+    if cls in traffic:
         continue
 
     def val(key):
