@@ -16,7 +16,7 @@ for k in k_pam_be k_pam_fe k_pam_theta k_norm_stats k_lms_prefix; do
     -o $O/prof_$k $B > $O/ncu_full_$k.log 2>&1
 done
 timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-  -k "regex:k_lms_seg<.bool.0" -s 3 -c 1 -o $O/prof_k_lms_seg $B > $O/ncu_full_k_lms_seg.log 2>&1
+  -k "regex:k_lms_seg<.bool.0" -s 1 -c 1 -o $O/prof_k_lms_seg $B > $O/ncu_full_k_lms_seg.log 2>&1
 BK="python bench.py --timed-only --no-pam --steps 2 --warmup 3 --ring-gib 0.25"
 for k in k_kk_s1 k_kk_s2 k_cfo_spec k_cfo_fine k_lms_final; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:^$k -s 6 -c 1 \
