@@ -318,30 +318,45 @@ typedef enum {
 rx_status rx_profile_enable(rx_handle *h, int mask);
 rx_status rx_profile_read(rx_handle *h, double *host_ms, long long *host_counts, int n);
 
-/* ---- Time-block sharding of one stream over GPUs (SURVEY §8(e) mode 2, KK chain) -------------
+/* ---- Time-block sharding of one stream over GPUs (SURVEY §8(e) mode 2) -------------------------
  * The paper chains its buffers with ordered carries (the overlap kernel; the clock phase of
- * the previous buffer). In the KK chain the quantities that cross a buffer boundary are
- * the overlap-save halos (recomputed from input halos), the CFO DDS phase origin (a prefix over all
- * earlier buffers' estimates, c-8), the frame-sync result and trained taps from the stream start,
- * the lag-D seeds (c-9) and z' of the neighbour buffers for the LMS windows at the edges. Paper
- * buffer b = input samples [b B4, (b+1) B4), B4 = 512 buffer_blocks; with shard_count = N, shard g
- * owns the buffers b = g mod N. Round r (buffers r N .. r N + N - 1):
- *  1. rx_shard_process(h, b = r N + g, ...): input samples [max(0, b B4 - RX_SHARD_PRE),
- *     (b+1) B4 + RX_SHARD_POST) (shorter only on the call holding the stream end, last = 1),
- *     device u16 codes; KK stage 1 / 2 over the blocks whose frames lie inside, CFO estimate of b.
- *     d_labels: where the labels of b's symbols go (absolute symbol m at m % labels_capacity).
+ * the previous buffer). Paper buffer b = input samples [b B4, (b+1) B4), B4 = 512
+ * buffer_blocks; with shard_count = N, shard g owns the buffers b = g mod N and reads its input
+ * halos itself: rx_shard_halo(h, &pre, &post) gives them (KK: RX_SHARD_PRE / RX_SHARD_POST; PAM:
+ * the back-end look-back of the buffer's first segment plus the clock windows, 512 (PB + 2 + h) and
+ * 512 (2 + h) with h = clock_avg_half, PB = (S + O + 2 floor(K/2) + 255) / 256 + 2).
+ * What crosses a buffer boundary travels in one record per shard and round:
+ *  KK: the CFO estimate (DDS phase origin = a prefix over all earlier buffers' estimates, c-8);
+ *  PAM: the clock-phase wrap count of the buffer's own blocks (the unwrapped phase is theta_b -
+ *    2 pi N_b, N_b an integer prefix over all earlier blocks; exact) and the buffer's
+ *    normalisation scalars (dc, A; its neighbours normalise their look-back symbols with them);
+ *  both: the frame-sync result and trained taps from the stream start, and the lag-D seed partial
+ *    sums (c-9: 2^-32 fixed point, so an epoch split between shards gets the same seed).
+ * Round r (buffers r N .. r N + N - 1):
+ *  1. rx_shard_process(h, b = r N + g, ...): input samples [max(0, b B4 - pre), (b+1) B4 + post)
+ *     (shorter only on the call holding the stream end, last = 1), device u16 codes. KK: stage 1 / 2
+ *     over the blocks whose frames lie inside, CFO estimate of b. PAM: front-end and clock phases
+ *     of b's blocks and their halo blocks. d_labels: where the labels of b's segments go (absolute
+ *     symbol m at m % labels_capacity).
  *  2. rx_export_carry(h, d_rec): this round's record (rx_carry_size bytes, 16-byte aligned device
  *     memory); the caller all-gathers the N records in rank order into one device buffer (NCCL
  *     all-gather; no host staging).
- *  3. rx_import_carry(h, d_all, N, g): rebuild the DDS origin chain, take sync / trained taps /
+ *  3. rx_import_carry(h, d_all, N, g): take the records. KK: DDS origin chain, sync / trained taps,
  *     seeds, then the equaliser, decisions, labels and counters of the shard's buffer of round
  *     r - 1 (its last segment needs z' of the next buffer, whose CFO estimate arrives now).
+ *     PAM: the wrap base of b, scalars, sync / trained taps, seeds; the equaliser round of the
+ *     shard's buffer of round r - 1 (segments s with (s + 1) S - 1 + floor(K/2) in its symbols,
+ *     after normalising its look-back symbols with the previous buffer's scalars, which arrive
+ *     now), then clock tau_b / M_b, back-end and normalisation of b (sync + training on b = 0).
  * After the round holding the stream end, one more export / gather / import without
  * rx_shard_process finishes every pending buffer. Labels are bit-identical and integer counters
- * (summed over shards) equal to one handle's on the same stream. All calls are stream-ordered and
- * asynchronous; errors: RX_EINVAL (arguments, not a shard handle), RX_ESTATE (call order). */
+ * (summed over shards) equal to one handle's on the same stream. Limits: KK needs cpr_anchor = 1
+ * and N <= tap_lag_epochs; PAM N <= tap_lag_epochs - 2 (epochs drift against buffers with the
+ * sampling clock; an epoch's seed can need the next round's partial). All calls are stream-ordered
+ * and asynchronous; errors: RX_EINVAL (arguments, not a shard handle), RX_ESTATE (call order). */
 #define RX_SHARD_PRE 4096
 #define RX_SHARD_POST 4096
+rx_status rx_shard_halo(const rx_handle *h, long long *pre, long long *post);
 rx_status rx_shard_process(rx_handle *h, long long buffer, const void *d_samples, long long n_samples,
                            int last, unsigned char *d_labels, long long labels_capacity, void *cuda_stream);
 rx_status rx_carry_size(const rx_handle *h, int *bytes);

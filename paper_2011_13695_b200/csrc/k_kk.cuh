@@ -552,131 +552,3 @@ __device__ __forceinline__ float2 zp_value(const RxDev &d, long long q, long lon
   if (q < 0 || q >= vend) return make_float2(0.f, 0.f);
   return zp_rotate(d, d.z[rmod(q, d.z_cap)], q, c);
 }
-
-
-// ------------------------------------------------------------------ time sharding
-// One shard's per-round carry record (packed; rx_export_carry writes it to device memory, the
-// caller all-gathers the records of every shard (NCCL) and passes them to rx_import_carry).
-// It carries exactly the quantities that cross buffer boundaries in the KK chain:
-//  - the CFO estimate (P, df, k*) of the buffer this shard estimated this round: every shard
-//    rebuilds the DDS origin chain origin_{b+1} = origin_b + Q inc_b (c-8) from all of them;
-//  - the frame-sync result and the trained taps W_train (V_train) from the shard holding the
-//    stream start (c-10, c-9 'Training');
-//  - the lag-D seeds (epoch mean canonical taps, c-9 'Seed') this shard finalised since its last
-//    record, for the shard owning epoch e + D.
-#define RX_CARRY_SEEDS 2
-struct RxCarry {
-  long long beta;                       // buffer estimated this round (-1: none)
-  double P, df;
-  int kstar, flags;                     // flags bit 0: sync + training valid
-  int sync_offset, sync_phase, sync_polarity, pad;
-  double sync_gamma, sync_phi0;
-  float2 w_train[RX_MAX_K], v_train[RX_MAX_K];
-  long long seed_epoch[RX_CARRY_SEEDS]; // -1: slot unused
-  float2 seed[RX_CARRY_SEEDS][RX_MAX_K];
-};
-
-// one thread: the shard's record of this round
-__global__ void k_carry_export(RxDev d, RxCarry *out, long long beta, long long seed_e0, int nseed) {
-  RxCarry c;
-  memset(&c, 0, sizeof(c));
-  c.beta = beta;
-  if (beta >= 0) {
-    const CfoParam cp = d.cfo[rmod(beta, d.buf_cap)];
-    c.P = cp.P;
-    c.df = cp.df;
-    c.kstar = cp.kstar;
-  }
-  const DevState *st = d.st;
-  if (st->synced && st->trained) {
-    c.flags = 1;
-    c.sync_offset = st->sync_offset;
-    c.sync_phase = st->sync_phase;
-    c.sync_polarity = st->sync_polarity;
-    c.sync_gamma = st->sync_gamma;
-    c.sync_phi0 = st->sync_phi0;
-    for (int k = 0; k < RX_MAX_K; ++k) {
-      c.w_train[k] = d.w_train[k];
-      c.v_train[k] = d.wl ? d.v_train[k] : make_float2(0.f, 0.f);
-    }
-  }
-  for (int i = 0; i < RX_CARRY_SEEDS; ++i) {
-    const long long e = seed_e0 + i;
-    const bool ok = i < nseed && e >= 0 && d.seed_ready[rmod(e, d.seed_cap)] == e + 1;
-    c.seed_epoch[i] = ok ? e : -1;
-    for (int k = 0; k < RX_MAX_K; ++k) c.seed[i][k] = ok ? d.seed[rmod(e, d.seed_cap) * RX_MAX_K + k] : make_float2(0.f, 0.f);
-  }
-  *out = c;
-}
-
-// one thread: every shard's record of the round, in rank order (= buffer order). CFO parameters
-// go to the per-buffer table exactly as cfo_final_block / k_cfo_fine leave them (the origin
-// chain is then advanced by k_cfo_carry over the round's buffers, as in the single stream);
-// sync / training and seeds are taken from whichever record carries them.
-__global__ void k_carry_import(RxDev d, const RxCarry *g, int n) {
-  DevState *st = d.st;
-  for (int i = 0; i < n; ++i) {
-    const RxCarry &c = g[i];
-    if (c.beta >= 0) {
-      CfoParam cp;
-      cp.P = c.P;
-      cp.df = c.df;
-      cp.kstar = c.kstar;
-      cp.inv_sqrtP = (float)(1.0 / sqrt(c.P));
-      cp.inc = (unsigned long long)llrint(ldexp(c.df / d.fs2, 64));
-      cp.origin = 0ull;
-      d.cfo[rmod(c.beta, d.buf_cap)] = cp;
-    }
-    if ((c.flags & 1) && !st->trained) {
-      st->sync_offset = c.sync_offset;
-      st->sync_phase = c.sync_phase;
-      st->sync_polarity = c.sync_polarity;
-      st->sync_gamma = c.sync_gamma;
-      st->sync_phi0 = c.sync_phi0;
-      for (int k = 0; k < RX_MAX_K; ++k) {
-        d.w_train[k] = c.w_train[k];
-        if (d.wl) d.v_train[k] = c.v_train[k];
-      }
-      if (c.sync_gamma < d.sync_min) set_flag(st, RX_FLAG_SYNC_DEV);
-      __threadfence();
-      st->synced = 1;
-      st->trained = 1;
-      d.hm->synced = 1;
-      d.hm->trained = 1;
-    }
-    for (int j = 0; j < RX_CARRY_SEEDS; ++j) {
-      const long long e = c.seed_epoch[j];
-      if (e < 0 || d.seed_ready[rmod(e, d.seed_cap)] == e + 1) continue;
-      for (int k = 0; k < RX_MAX_K; ++k) d.seed[rmod(e, d.seed_cap) * RX_MAX_K + k] = c.seed[j][k];
-      __threadfence();
-      d.seed_ready[rmod(e, d.seed_cap)] = (int)(e + 1);
-    }
-  }
-}
-
-// the DDS origin chain over the round's buffers in buffer order (k_cfo_carry's arithmetic)
-__global__ void k_carry_chain(RxDev d, const RxCarry *g, int n) {
-  for (int i = 0; i < n; ++i) {
-    const long long b = g[i].beta;
-    if (b < 0) continue;
-    CfoParam cp = d.cfo[rmod(b, d.buf_cap)];
-    const double df = cp.kstar >= 0 ? cp.df : d.st->cfo_df_prev;
-    if (d.cfo_enable) {
-      cp.df = df;
-      cp.inc = (unsigned long long)llrint(ldexp(df / d.fs2, 64));
-      cp.origin = d.st->cfo_origin_next;
-      d.st->cfo_origin_next = cp.origin + (unsigned long long)((long long)d.buffer_blocks * 256) * cp.inc;
-      d.st->cfo_df_prev = df;
-    } else {
-      cp.df = 0.0; cp.inc = 0ull; cp.origin = 0ull;
-    }
-    d.cfo[rmod(b, d.buf_cap)] = cp;
-  }
-}
-
-// stage B of a time shard: z' valid below q_valid, finalisation front at the epoch's first segment
-__global__ void k_shard_seek(RxDev d, long long q_valid, long long seg0) {
-  d.st->v_front = q_valid;
-  d.st->seg_next = seg0;
-  d.hm->seg_next = seg0;
-}

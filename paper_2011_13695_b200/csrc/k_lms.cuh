@@ -1556,49 +1556,113 @@ __global__ void __launch_bounds__(1024) k_lms_counters(RxDev d) {
   lms_add_counters(d, d.st->fin_lo, d.st->fin_hi);
 }
 
-// ... and the lag-D epoch seeds: CTA i owns epoch fin_lo/spe + i; when all its segments are
-// finalised the seed of epoch e + D is the mean of their canonical taps (fixed order).
+// ... and the lag-D epoch seeds (c-9 'Seed': the seed of epoch e + D is the mean of the canonical
+// taps of epoch e's segments). The mean is accumulated per epoch in 2^-32 fixed point (int64:
+// exact, so independent of the order and grouping of the additions): every round adds the
+// segments it finalised, and the epoch's seed is formed once its count is complete. A time shard
+// (SURVEY §8(e) mode 2) can therefore add the partial sums of an epoch split between shards
+// (rx_import_carry) and still form the single stream's seed bit for bit.
+#define SEED_FX 4294967296.0f
+#define SEED_FX_INV 2.3283064365386963e-10
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+// segments in epoch e (spe; fewer for the last epoch once the stream end m_end is known)
+__device__ __forceinline__ long long epoch_segs(const RxDev &d, long long e) {
+  const long long spe = d.E_sym / d.S;
+  const long long me = d.st->m_end;
+  if (me >= 0) {
+    const long long left = (me + d.S - 1) / d.S - e * spe;
+    if (left < spe) return left > 0 ? left : 0;
+  }
+  return spe;
+}
+// add a partial sum (n segments, sums [K][2]) to epoch e's accumulator; tap k by lane k of one
+// warp (every lane calls). Forms the seed of e + D when the epoch is complete.
+__device__ void seed_acc_add(const RxDev &d, long long e, int n, long long sx, long long sy) {
+  const int lane = threadIdx.x & 31;
+  const long long slot = rmod(e, d.seed_cap);
+  const long long tgt = e + d.D;
+  const bool fresh = d.seed_tag[slot] != e + 1;
+  long long *acc = d.seed_acc + slot * RX_MAX_K * 2;
+  long long ax = 0, ay = 0;
+  if (lane < d.K) {
+    ax = (fresh ? 0 : acc[2 * lane]) + sx;
+    ay = (fresh ? 0 : acc[2 * lane + 1]) + sy;
+    acc[2 * lane] = ax;
+    acc[2 * lane + 1] = ay;
+  }
+  const int cnt = (fresh ? 0 : d.seed_cnt[slot]) + n;
+  __syncwarp();
+  if (lane == 0) {
+    d.seed_cnt[slot] = cnt;
+    d.seed_tag[slot] = e + 1;
+  }
+  if (cnt > 0 && cnt >= epoch_segs(d, e) && d.seed_ready[rmod(tgt, d.seed_cap)] != tgt + 1) {
+    if (lane < d.K) {
+      const double inv = SEED_FX_INV / (double)cnt;
+      d.seed[rmod(tgt, d.seed_cap) * RX_MAX_K + lane] = make_float2((float)((double)ax * inv), (float)((double)ay * inv));
+    }
+    __syncwarp();
+    if (lane == 0) { __threadfence(); d.seed_ready[rmod(tgt, d.seed_cap)] = (int)(tgt + 1); }
+  }
+}
+
+// CTA i: epoch fin_lo/spe + i, the segments of it this round finalised ([fin_lo, fin_hi)):
+// warp k sums tap k over them (lane-strided), warp 0 adds the partial to the accumulator. CTAs
+// 0..RX_CARRY_SEEDS-1 also stage their partial for the shard record (epoch -1: none).
 __global__ void __launch_bounds__(1024) k_lms_seeds(RxDev d, int flush) {
   pdl_wait();                 // the previous kernel of the round (programmatic dependent launch)
+  __shared__ long long part[RX_MAX_K][2];
   DevState *st = d.st;
   const long long lo = st->fin_lo, hi = st->fin_hi;
   const long long spe = d.E_sym / d.S;
   const long long e = lo / spe + blockIdx.x;
-  long long e_hi = hi / spe;                      // epochs [., e_hi) complete
-  if (flush && st->m_end >= 0 && hi * (long long)d.S >= st->m_end) e_hi = (hi + spe - 1) / spe;
-  if (e >= e_hi || hi <= lo) return;
-  const long long tgt = e + d.D;
-  if (d.seed_ready[rmod(tgt, d.seed_cap)] == tgt + 1) return;
-  const long long s_lo = e * spe;
-  long long s_hi = s_lo + spe;
-  if (s_hi > hi) s_hi = hi;
   const int t = threadIdx.x, k = t >> 5, lane = t & 31;
-  // mean over the epoch's segments of the canonical taps
-  {
+  const bool has = hi > lo && e <= (hi - 1) / spe;
+  if (!has) {
+    if (blockIdx.x < RX_CARRY_SEEDS && t == 0) d.seed_xp[blockIdx.x].epoch = -1;
+    return;
+  }
+  long long s_lo = e * spe, s_hi = s_lo + spe;
+  if (s_lo < lo) s_lo = lo;
+  if (s_hi > hi) s_hi = hi;
+  long long sx = 0, sy = 0;
+  if (k < d.K) {
     const float2 *src = d.seg_w;
-    float sx = 0.f, sy = 0.f;
-    if (k < d.K) {
-      long long s = s_lo + lane;
-      for (; s + 96 < s_hi; s += 128) {          // 4 independent loads in flight, summed in order
-        const float2 w0 = src[rmod(s, d.seg_cap) * RX_MAX_K + k];
-        const float2 w1 = src[rmod(s + 32, d.seg_cap) * RX_MAX_K + k];
-        const float2 w2 = src[rmod(s + 64, d.seg_cap) * RX_MAX_K + k];
-        const float2 w3 = src[rmod(s + 96, d.seg_cap) * RX_MAX_K + k];
-        sx += w0.x; sy += w0.y; sx += w1.x; sy += w1.y;
-        sx += w2.x; sy += w2.y; sx += w3.x; sy += w3.y;
-      }
-      for (; s < s_hi; s += 32) {
-        const float2 w = src[rmod(s, d.seg_cap) * RX_MAX_K + k];
-        sx += w.x; sy += w.y;
-      }
+    long long s = s_lo + lane;
+    for (; s + 96 < s_hi; s += 128) {            // 4 independent loads in flight
+      const float2 w0 = src[rmod(s, d.seg_cap) * RX_MAX_K + k];
+      const float2 w1 = src[rmod(s + 32, d.seg_cap) * RX_MAX_K + k];
+      const float2 w2 = src[rmod(s + 64, d.seg_cap) * RX_MAX_K + k];
+      const float2 w3 = src[rmod(s + 96, d.seg_cap) * RX_MAX_K + k];
+      sx += __float2ll_rn(w0.x * SEED_FX) + __float2ll_rn(w1.x * SEED_FX) + __float2ll_rn(w2.x * SEED_FX) +
+            __float2ll_rn(w3.x * SEED_FX);
+      sy += __float2ll_rn(w0.y * SEED_FX) + __float2ll_rn(w1.y * SEED_FX) + __float2ll_rn(w2.y * SEED_FX) +
+            __float2ll_rn(w3.y * SEED_FX);
     }
-    sx = warp_sum(sx);
-    sy = warp_sum(sy);
-    if (k < d.K && lane == 0) {
-      const float inv = 1.0f / (float)(s_hi - s_lo);
-      d.seed[rmod(tgt, d.seed_cap) * RX_MAX_K + k] = make_float2(sx * inv, sy * inv);
+    for (; s < s_hi; s += 32) {
+      const float2 w = src[rmod(s, d.seg_cap) * RX_MAX_K + k];
+      sx += __float2ll_rn(w.x * SEED_FX);
+      sy += __float2ll_rn(w.y * SEED_FX);
     }
+    sx = warp_sum_ll(sx);
+    sy = warp_sum_ll(sy);
+    if (lane == 0) { part[k][0] = sx; part[k][1] = sy; }
   }
   __syncthreads();
-  if (t == 0) { __threadfence(); d.seed_ready[rmod(tgt, d.seed_cap)] = (int)(tgt + 1); }
+  if (k == 0) {
+    const long long px = lane < d.K ? part[lane][0] : 0, py = lane < d.K ? part[lane][1] : 0;
+    const int n = (int)(s_hi - s_lo);
+    if (blockIdx.x < RX_CARRY_SEEDS) {
+      SeedPart *xp = d.seed_xp + blockIdx.x;
+      xp->sum[lane][0] = px;
+      xp->sum[lane][1] = py;
+      if (lane == 0) { xp->epoch = e; xp->n = n; }
+    }
+    seed_acc_add(d, e, n, px, py);
+  }
+  (void)flush;
 }

@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(256) k_pam_fe(RxDev d, InView in, long long b0
 #pragma unroll
     for (int r = 0; r < 8; ++r) v[r] = make_float2(0.f, 0.f);
   }
+  if (b < in.cnt_lo || b >= in.cnt_hi) clip = 0;   // a time shard's halo block: counted by its owner
   block_reduce_clip(d.st, clip);
   tw_wait();
   fft512_regs<false>(buf[g], j, tw, v);
@@ -159,8 +160,10 @@ __global__ void __launch_bounds__(256) k_pam_fe(RxDev d, InView in, long long b0
 //            shared-memory tile of C, each thread sliding its window over 8 blocks)
 //   theta_b = atan2(Cbar_b) ; |Cbar| = 0 inherits the previous phase
 //   theta^u_b = theta^u_{b-1} + w(theta_b - theta_{b-1}), w(x) = x - 2 pi rint(x / 2 pi):
-//            the paper's serial single-warp unwrap as a warp-shuffle block scan
-//   tau_b = -theta^u_b / 2 pi ; M_b = ceil(256 b - 128 - tau_b)
+//            the paper's serial single-warp unwrap, telescoped: theta^u_b = theta_b -
+//            2 pi N_b, N_b = sum_{i<=b} rint((theta_i - theta_{i-1}) / 2 pi), an integer scan
+//            (exact in any order: call and shard boundaries cannot change it, DESIGN R-UNWRAP)
+//   tau_b = -theta^u_b / 2 pi = N_b - theta_b / 2 pi ; M_b = ceil(256 b - 128 - tau_b)
 #define CLK_CHUNK 8192
 __device__ __forceinline__ double warp_incl_scan_d(double v) {
   const int lane = threadIdx.x & 31;
@@ -183,11 +186,19 @@ __device__ __forceinline__ long long warp_incl_max_ll(long long v) {
 
 // Three launches, all but (b) fully parallel:
 // (a) k_pam_theta: one CTA per 256 blocks. Cbar_b from a shared-memory C tile (+2h halo),
-//     theta_b = atan2(Cbar_b) (|Cbar| = 0 inherits the previous phase), the wrapped
-//     differences w(theta_b - theta_{b-1}) and their CTA-local inclusive prefix (double).
+//     theta_b = atan2(Cbar_b) (|Cbar| = 0 inherits the previous phase), the wrap counts
+//     n_b = rint((theta_b - theta_{b-1}) / 2 pi) and their CTA-local inclusive prefix.
 // (b) k_pam_carry: one CTA scans the CTA totals -> per-CTA offsets (+ the call's carry).
-// (c) k_pam_tau: tau_b = -(offset + local prefix) / 2 pi, M_b = ceil(256 b - 128 - tau_b).
+// (c) k_pam_tau: N_b = offset + local prefix, tau_b = N_b - theta_b / 2 pi, M_b.
 #define CLK_TILE 256
+// tau_b and M_b from the integer wrap count N_b and the resolved phase theta_b: one expression
+// for every path (fused, three-launch, time shard), so all of them give identical bits
+__device__ __forceinline__ double clk_tau(double N, double th) {
+  return __fma_rn(-th, 0.15915494309189533577, N);
+}
+__device__ __forceinline__ long long clk_mb(long long b, double tau) {
+  return (long long)ceil(__dsub_rn(__dsub_rn(256.0 * (double)b, 128.0), tau));
+}
 __device__ __forceinline__ double theta_of(const double2 *Ct, int i, int hh) {   // window at tile i
   // 4 interleaved partial sums (independent add chains), combined in a fixed order
   double sr[4] = {0.0, 0.0, 0.0, 0.0}, si[4] = {0.0, 0.0, 0.0, 0.0};
@@ -217,7 +228,7 @@ __global__ void __launch_bounds__(CLK_TILE) k_pam_theta(RxDev d, long long b0, l
   __shared__ double wsum[CLK_TILE / 32];
   __shared__ long long wmax[CLK_TILE / 32];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5, hh = d.clock_half;
-  const double TWO_PI = 6.283185307179586476925, INV_2PI = 0.15915494309189533577;
+  const double INV_2PI = 0.15915494309189533577;
   // FUSED: the tile index is taken in dispatch order from a counter (clk_ticket[1]), not from
   // blockIdx, so a tile only ever waits on tiles that are already resident (decoupled look-back
   // ordering; no reliance on blockIdx-ordered CTA dispatch)
@@ -271,13 +282,13 @@ __global__ void __launch_bounds__(CLK_TILE) k_pam_theta(RxDev d, long long b0, l
   };
   const double tprev = src_prev >= 1 ? th_sh[src_prev] : resolve_before();
   const double tcur = src_cur >= 1 ? th_sh[src_cur] : resolve_before();
-  double diff = 0.0;
+  double diff = 0.0;                                     // n_b (an integer, held in a double)
   if (b < b1) {
     const double dd = tcur - tprev;
-    diff = dd - TWO_PI * rint(dd * INV_2PI);
-    if (b == 0) diff = tcur;                             // theta^u_0 = theta_0 (theta_{-1} = 0)
+    diff = rint(dd * INV_2PI);
+    if (b == 0) diff = 0.0;                              // theta^u_0 = theta_0: N_0 = 0
   }
-  // CTA-local inclusive prefix of the wrapped differences
+  // CTA-local inclusive prefix of the wrap counts (integer sums: exact)
   double incl = diff;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -288,7 +299,10 @@ __global__ void __launch_bounds__(CLK_TILE) k_pam_theta(RxDev d, long long b0, l
   __syncthreads();
   double off = 0.0;
   for (int w = 0; w < warp; ++w) off += wsum[w];
-  if (!FUSED && b < b1) d.tau[rmod(b, d.blk_cap)] = off + incl;   // local prefix (finished by k_pam_tau)
+  if (!FUSED && b < b1) {                                // local prefix (finished by k_pam_tau)
+    d.tau[rmod(b, d.blk_cap)] = off + incl;
+    d.theta[rmod(b, d.blk_cap)] = tcur;
+  }
   if (t == CLK_TILE - 1) {
     double tot = 0.0;
     for (int w = 0; w < CLK_TILE / 32; ++w) tot += wsum[w];
@@ -310,18 +324,17 @@ __global__ void __launch_bounds__(CLK_TILE) k_pam_theta(RxDev d, long long b0, l
         acc += ((volatile double *)d.clk_part)[i];
       }
       acc = warp_sum_d(acc);
-      if (lane == 0) tile_off = d.st->thetau_prev + acc;
+      if (lane == 0) tile_off = d.st->wraps_prev + acc;
     }
     __syncthreads();
-    const double tu = tile_off + off + incl;
+    const double Nb = tile_off + off + incl;
     if (b < b1) {
-      const double tau = -tu * INV_2PI;
+      const double tau = clk_tau(Nb, tcur);
       d.tau[rmod(b, d.blk_cap)] = tau;
-      d.Mb[rmod(b, d.blk_cap)] = (long long)ceil(256.0 * (double)b - 128.0 - tau);
+      d.Mb[rmod(b, d.blk_cap)] = clk_mb(b, tau);
     }
     // the last tile to finish (every tile has read the call's carry by then) advances the carry:
-    // thetau_prev += sum of the tile totals (lane-strided + warp tree, the former
-    // k_pam_clock_carry's order: a separate launch before), theta_prev = the call's last resolved phase
+    // wraps_prev += sum of the tile totals, theta_prev = the call's last resolved phase
     __shared__ int last_tile;
     __syncthreads();
     if (t == 0) {
@@ -335,7 +348,7 @@ __global__ void __launch_bounds__(CLK_TILE) k_pam_theta(RxDev d, long long b0, l
       for (int i = lane; i < (int)gridDim.x; i += 32) acc += ((volatile double *)d.clk_part)[i];
       acc = warp_sum_d(acc);
       if (lane == 0) {
-        d.st->thetau_prev += acc;
+        d.st->wraps_prev += acc;
         d.st->theta_prev = ((volatile double *)d.clk_last)[gridDim.x - 1];
         d.clk_ticket[0] = 0;
         d.clk_ticket[1] = 0;                             // every tile has taken its index
@@ -349,7 +362,7 @@ __global__ void __launch_bounds__(CLK_TILE) k_pam_theta(RxDev d, long long b0, l
 __global__ void __launch_bounds__(1024) k_pam_carry(RxDev d, int ntiles) {
   __shared__ double ws[32];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  double carry = d.st->thetau_prev;
+  double carry = d.st->wraps_prev;
   for (int c0 = 0; c0 < ntiles; c0 += 1024) {
     const int i = c0 + t;
     const double v = i < ntiles ? d.clk_part[i] : 0.0;
@@ -370,7 +383,7 @@ __global__ void __launch_bounds__(1024) k_pam_carry(RxDev d, int ntiles) {
     carry += tot;
   }
   if (t == 0) {
-    d.st->thetau_prev = carry;
+    d.st->wraps_prev = carry;
     d.st->theta_prev = d.clk_last[ntiles - 1];
   }
 }
@@ -379,12 +392,11 @@ __global__ void __launch_bounds__(1024) k_pam_carry(RxDev d, int ntiles) {
 __global__ void __launch_bounds__(256) k_pam_tau(RxDev d, long long b0, long long b1) {
   const long long b = b0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= b1) return;
-  const double INV_2PI = 0.15915494309189533577;
   const int tile = (int)((b - b0) / CLK_TILE);
-  const double tu = d.clk_off[tile] + d.tau[rmod(b, d.blk_cap)];
-  const double tau = -tu * INV_2PI;
+  const double Nb = d.clk_off[tile] + d.tau[rmod(b, d.blk_cap)];
+  const double tau = clk_tau(Nb, d.theta[rmod(b, d.blk_cap)]);
   d.tau[rmod(b, d.blk_cap)] = tau;
-  d.Mb[rmod(b, d.blk_cap)] = (long long)ceil(256.0 * (double)b - 128.0 - tau);
+  d.Mb[rmod(b, d.blk_cap)] = clk_mb(b, tau);
 }
 
 // ------------------------------------------------------------------ H1, H2, H5-H7

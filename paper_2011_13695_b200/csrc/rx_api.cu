@@ -16,6 +16,7 @@
 #include "k_pam.cuh"
 #include "k_kk.cuh"
 #include "k_lms.cuh"
+#include "k_shard.cuh"
 
 #ifndef RX_GIT
 #define RX_GIT "dev"
@@ -125,10 +126,13 @@ struct rx_handle {
   long long clk_launch;          // fused clock launches so far (tags the tile totals)
   bool flushed;
   // time sharding (shard_count > 1): the buffer whose stage A ran last (awaiting export / stage B)
-  struct ShardBuf { long long beta, qfront; int last, valid, exported; unsigned char *labels; long long cap; };
+  // (PAM: c_lo / c_hi clock blocks, be_lo / be_hi back-end blocks of the buffer and its halo)
+  struct ShardBuf { long long beta, qfront; int last, valid, exported; unsigned char *labels; long long cap;
+                    long long c_lo, c_hi, be_lo, be_hi; };
   ShardBuf sh_cur, sh_pend;     // this round's stage A; the previous round's (stage B at import)
-  long long sh_seed_e;          // lag-D seed epoch produced by the last stage B (-1 none)
-  RxCarry *sh_rec;              // device scratch for the export record
+  long long sh_norm_beta;       // PAM: buffer normalised at the last import, for the next record
+  long long sh_pre, sh_post;    // input halos (rx_shard_halo)
+  long long sh_pb;              // PAM: back-end blocks before the buffer (equaliser look-back)
   long long launches;
   int sps;
   long long Q;   // 2-sps samples per buffer (KK)
@@ -294,8 +298,12 @@ static rx_status validate(const rx_config *c) {
   if (c->equaliser_lag != 0 && c->equaliser_lag != 1) return RX_EINVAL;
   if (c->cuda_graphs != 0 && c->cuda_graphs != 1) return RX_EINVAL;
   if (c->shard_count < 0 || c->shard_count > 64) return RX_EINVAL;
-  if (c->shard_count > 1) {        // time sharding (SURVEY §8(e) mode 2): the KK chain
-    if (c->family != RX_QAM_KK || c->cpr_anchor != 1 || c->shard_count > c->tap_lag_epochs) return RX_EINVAL;
+  if (c->shard_count > 1) {        // time sharding (SURVEY §8(e) mode 2)
+    // KK: stage B of buffer b one round after its stage A, epochs = buffers: N <= D.
+    // PAM: epochs drift against buffers with the clock, an epoch's last segments may finish a
+    // round later on the next shard: N <= D - 2 keeps every lag-D seed ahead of its use.
+    if (c->family == RX_QAM_KK && (c->cpr_anchor != 1 || c->shard_count > c->tap_lag_epochs)) return RX_EINVAL;
+    if (c->family == RX_PAM && c->shard_count > c->tap_lag_epochs - 2) return RX_EINVAL;
     if (c->shard_index < 0 || c->shard_index >= c->shard_count) return RX_EINVAL;
   }
   if (c->q_window_symbols < 0 || (c->q_window_symbols > 0 && c->q_window_symbols % c->lms_segment)) return RX_EINVAL;
@@ -492,9 +500,20 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   if (c.input_format == RX_IN_U12_PACKED) TRY(dalloc(h, &h->unpacked, h->max_call));
   if (c.input_format == RX_IN_F32) TRY(dalloc(h, &d.histf, d.hist_cap));
   else TRY(dalloc(h, &d.hist, d.hist_cap));
+  // PAM time shard: back-end blocks before the buffer so its first segment (whose last tap may sit
+  // S - 1 symbols into the buffer) has its look-back O and taps; input halos for those blocks'
+  // clock windows and overlap-save frames
+  h->sh_pb = ((long long)c.lms_segment + c.lms_overlap + 2 * (c.lms_taps / 2) + 255) / 256 + 2;
+  if (kk) { h->sh_pre = RX_SHARD_PRE; h->sh_post = RX_SHARD_POST; }
+  else {
+    h->sh_pre = 512 * (h->sh_pb + 2 + c.clock_avg_half);
+    h->sh_post = 512 * (2 + (long long)c.clock_avg_half);
+  }
   d.blk_cap = next_pow2((long long)HB * c.buffer_blocks + 256);
   if (!kk) {   // spectra from k_pam_fe to k_pam_be: one call + the clock look-ahead
     d.xs_cap = next_pow2((long long)(HB - 2) * c.buffer_blocks + 2 * c.clock_avg_half + 64);
+    if (c.shard_count > 1 && d.xs_cap < next_pow2(c.buffer_blocks + h->sh_pb + 2 * c.clock_avg_half + 8))
+      d.xs_cap = next_pow2(c.buffer_blocks + h->sh_pb + 2 * c.clock_avg_half + 8);
     TRY(dalloc(h, &d.Xspec, d.xs_cap * 512));
   }
   d.buf_cap = 64;
@@ -508,6 +527,12 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   // (equaliser_lag = 1: the side stream may still read one more call of them)
   const long long lag_calls = 1 + c.equaliser_lag;
   d.sym_cap = next_pow2((long long)(HB + lag_calls * (HB - 2)) * c.buffer_blocks * (kk ? 128 : 260) + batch_sym);
+  if (!kk && c.shard_count > 1) {   // buffers b and b + N (and halos) are held together
+    const long long need = (long long)(c.shard_count + 2) * c.buffer_blocks * 260;
+    if (d.sym_cap < next_pow2(need)) d.sym_cap = next_pow2(need);
+    const long long nb = c.buffer_blocks + h->sh_pb + 2 * c.clock_avg_half + 8;
+    if (d.blk_cap < next_pow2(nb)) d.blk_cap = next_pow2(nb);
+  }
   if (!kk) {
     TRY(dalloc(h, &d.C, d.blk_cap));
     TRY(dalloc(h, &d.theta, d.blk_cap));
@@ -522,7 +547,8 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
     TRY(dalloc(h, &d.norm_cnt, d.buf_cap));
     TRY(dalloc(h, &d.norm_part, 16 * NORM_G));
     TRY(dalloc(h, &d.norm_tick, 16));
-    const long long maxtiles = ((long long)(HB - 2) * c.buffer_blocks + CLK_TILE - 1) / CLK_TILE + 2;
+    long long maxtiles = ((long long)(HB - 2) * c.buffer_blocks + CLK_TILE - 1) / CLK_TILE + 2;
+    if (c.shard_count > 1) maxtiles += (h->sh_pb + 4 + CLK_TILE - 1) / CLK_TILE + 1;
     TRY(dalloc(h, &d.clk_part, maxtiles));
     TRY(dalloc(h, &d.clk_off, maxtiles));
     TRY(dalloc(h, &d.clk_last, maxtiles));
@@ -555,17 +581,22 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   d.seed_cap = 64;
   TRY(dalloc(h, &d.seed, d.seed_cap * RX_MAX_K));
   if (c.shard_count > 1) {
-    TRY(dalloc(h, &h->sh_rec, 1));
     h->cfg.serial_equaliser = 1;   // a shard orders everything on the caller's stream
   }
   h->sh_cur.valid = h->sh_pend.valid = 0;
-  h->sh_seed_e = -1;
+  h->sh_norm_beta = -1;
   d.wl = c.widely_linear;
   if (d.wl) TRY(dalloc(h, &d.v_train, RX_MAX_K));
   if (!kk) TRY(dalloc(h, &d.cal_part, (long long)CAL_G * 16 * 2));
   d.q_segs = c.q_window_symbols / c.lms_segment;
   if (d.q_segs > 0) TRY(dalloc(h, &d.q_win, 2 * RX_Q_WINDOWS));
   TRY(dalloc(h, &d.seed_ready, d.seed_cap));
+  TRY(dalloc(h, &d.seed_acc, d.seed_cap * RX_MAX_K * 2));
+  TRY(dalloc(h, &d.seed_cnt, d.seed_cap));
+  TRY(dalloc(h, &d.seed_tag, d.seed_cap));
+  TRY(dalloc(h, &d.seed_xp, RX_CARRY_SEEDS));
+  TRY(cudaMemset(d.seed_xp, 0xFF, RX_CARRY_SEEDS * sizeof(SeedPart)) == cudaSuccess ? RX_OK : RX_ECUDA);   // epoch -1
+  TRY(dalloc(h, &d.buf_m, d.buf_cap * 4));
   d.seg_cap = next_pow2(d.sym_cap / c.lms_segment + 8);
   TRY(dalloc(h, &d.seg_w, d.seg_cap * RX_MAX_K));
   TRY(dalloc(h, &d.seg_theta, d.seg_cap));
@@ -751,7 +782,8 @@ static void launch_lms_round(rx_handle *h, cudaStream_t s, unsigned char *labels
     KLAUNCH(h, RX_K_LMS_POST, s, launch_pdl(k_lms_final, (unsigned)nseg, 256, 0, s, d, labels, lab_cap, (int)nseg));
     KLAUNCH(h, RX_K_LMS_POST, s, launch_pdl(k_lms_counters, 1, 1024, 0, s, d));
   }
-  KLAUNCH(h, RX_K_LMS_POST, s, launch_pdl(k_lms_seeds, (unsigned)(nseg * S / d.E_sym + 2), 1024, 0, s, d, flush));
+  const unsigned nseed = (unsigned)(nseg * S / d.E_sym + 2);
+  KLAUNCH(h, RX_K_LMS_POST, s, launch_pdl(k_lms_seeds, nseed > RX_CARRY_SEEDS ? nseed : RX_CARRY_SEEDS, 1024, 0, s, d, flush));
 }
 
 // A streaming equaliser round as a CUDA graph (NEXT-2): captured once with a fixed grid that covers
@@ -1045,9 +1077,13 @@ extern "C" rx_status rx_process(rx_handle *h, const void *d_samples, long long n
 }
 
 // ------------------------------------------------------------------ time sharding (mode 2)
-// Stage A of buffer `beta` on its owning shard: the input covers [max(0, beta B4 - RX_SHARD_PRE),
-// (beta + 1) B4 + RX_SHARD_POST) (shorter at the stream end: last = 1); KK stage 1 / 2 over every
-// block whose overlap-save frames lie inside it, then the CFO estimate of the buffer.
+// Stage A of buffer `beta` on its owning shard. The input covers [max(0, beta B - pre),
+// (beta + 1) B + post) (rx_shard_halo; shorter at the stream end: last = 1).
+//  KK: stage 1 / 2 over every block whose overlap-save frames lie inside it, then the CFO
+//      estimate of the buffer.
+//  PAM: front-end (spectra, C_b) of the buffer's blocks, its back-end look-back blocks and their
+//      clock windows; the clock phases theta_b and their wrap counts relative to block beta B - 1
+//      (the global count arrives with the records: rx_import_carry).
 extern "C" rx_status rx_shard_process(rx_handle *h, long long beta, const void *d_samples, long long n, int last,
                                       unsigned char *d_labels, long long labels_capacity, void *stream) {
   if (!h || h->d.shard_n <= 1 || beta < 0 || n <= 0 || !d_samples || labels_capacity < 0 ||
@@ -1056,10 +1092,10 @@ extern "C" rx_status rx_shard_process(rx_handle *h, long long beta, const void *
   RxDev &d = h->d;
   if (beta % d.shard_n != d.shard_g || h->sh_cur.valid || h->flushed) return RX_ESTATE;
   if (h->cfg.input_format != RX_IN_U12_IN_U16 || (((uintptr_t)d_samples) & 15)) return RX_EINVAL;
-  const long long B4 = (long long)d.buffer_blocks * 512;
-  const long long P0 = beta * B4 - RX_SHARD_PRE > 0 ? beta * B4 - RX_SHARD_PRE : 0;
+  const long long BB = d.buffer_blocks, B4 = BB * 512;
+  const long long P0 = beta * B4 - h->sh_pre > 0 ? beta * B4 - h->sh_pre : 0;
   const long long P1 = P0 + n;
-  if (n % 512 || P1 <= beta * B4 || (!last && P1 < (beta + 1) * B4 + RX_SHARD_POST) || n > B4 + RX_SHARD_PRE + RX_SHARD_POST)
+  if (n % 512 || P1 <= beta * B4 || (!last && P1 < (beta + 1) * B4 + h->sh_post) || n > B4 + h->sh_pre + h->sh_post)
     return RX_EINVAL;
   CK(cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)stream;
@@ -1068,25 +1104,56 @@ extern "C" rx_status rx_shard_process(rx_handle *h, long long beta, const void *
   in.call_start = P0;
   in.call_end = P1;
   in.keep_from = 0x7fffffffffffffffLL;           // nothing goes to the history ring
-  in.cnt_lo = beta * d.buffer_blocks;             // the halos are counted by their owners
-  in.cnt_hi = (beta + 1) * d.buffer_blocks;
-  const long long s1_lo = P0 == 0 ? 0 : P0 / 512 + 1, s1_hi = P1 / 512;   // frames inside [P0, P1)
-  const long long s2_lo = P0 == 0 ? 0 : s1_lo + 1, s2_hi = s1_hi - 1;
-  KLAUNCH(h, RX_K_KK_S1, s, (k_kk_s1<<<gridc(s1_hi - s1_lo, FE_GROUPS), 256, 0, s>>>(d, in, s1_lo, s1_hi)));
-  KLAUNCH(h, RX_K_KK_S2, s, (k_kk_s2<<<gridc(s2_hi - s2_lo, FE_GROUPS), 256, 0, s>>>(d, s2_lo, s2_hi)));
-  const long long q_front = 256 * s2_hi - 128;
-  const int fine_ctas = (int)((h->Q / 1024 + 7) / 8);
-  KLAUNCH(h, RX_K_CFO, s, (k_cfo_spec<<<dim3(CFO_ROWS, 1), CFO_SPEC_T, 0, s>>>(d, beta, q_front)));
-  if (d.cfo_enable) KLAUNCH(h, RX_K_CFO, s, (k_cfo_fine<<<dim3((unsigned)fine_ctas, 1), 256, 0, s>>>(d, beta, q_front, fine_ctas)));
-  h->sh_cur.beta = beta;
-  h->sh_cur.qfront = q_front;
-  h->sh_cur.last = last;
-  h->sh_cur.valid = 1;
-  h->sh_cur.exported = 0;
-  h->sh_cur.labels = labels_capacity ? d_labels : nullptr;
-  h->sh_cur.cap = labels_capacity ? labels_capacity : 1;
+  in.cnt_lo = beta * BB;                          // the halos are counted by their owners
+  in.cnt_hi = (beta + 1) * BB;
+  rx_handle::ShardBuf &sb = h->sh_cur;
+  if (d.family == RX_QAM_KK) {
+    const long long s1_lo = P0 == 0 ? 0 : P0 / 512 + 1, s1_hi = P1 / 512;   // frames inside [P0, P1)
+    const long long s2_lo = P0 == 0 ? 0 : s1_lo + 1, s2_hi = s1_hi - 1;
+    KLAUNCH(h, RX_K_KK_S1, s, (k_kk_s1<<<gridc(s1_hi - s1_lo, FE_GROUPS), 256, 0, s>>>(d, in, s1_lo, s1_hi)));
+    KLAUNCH(h, RX_K_KK_S2, s, (k_kk_s2<<<gridc(s2_hi - s2_lo, FE_GROUPS), 256, 0, s>>>(d, s2_lo, s2_hi)));
+    const long long q_front = 256 * s2_hi - 128;
+    const int fine_ctas = (int)((h->Q / 1024 + 7) / 8);
+    KLAUNCH(h, RX_K_CFO, s, (k_cfo_spec<<<dim3(CFO_ROWS, 1), CFO_SPEC_T, 0, s>>>(d, beta, q_front)));
+    if (d.cfo_enable) KLAUNCH(h, RX_K_CFO, s, (k_cfo_fine<<<dim3((unsigned)fine_ctas, 1), 256, 0, s>>>(d, beta, q_front, fine_ctas)));
+    sb.qfront = q_front;
+  } else {
+    // blocks: front-end [f_lo, f_hi) (block b's frame is samples [512 (b - 1), 512 (b + 1))),
+    // clock [c_lo, c_hi) (windows of +-h blocks inside the front-end's), back-end [be_lo, be_hi)
+    const long long hh = d.clock_half, pb = h->sh_pb;
+    const long long f_lo = beta * BB - pb - 1 - hh > 0 ? beta * BB - pb - 1 - hh : 0;
+    const long long f_hi = last ? P1 / 512 : (beta + 1) * BB + 2 + hh;
+    sb.c_lo = beta * BB - pb > 0 ? beta * BB - pb : 0;
+    sb.c_hi = last ? f_hi : (beta + 1) * BB + 1;
+    sb.be_lo = sb.c_lo;
+    sb.be_hi = last ? f_hi - 1 : (beta + 1) * BB;
+    if (d.H_real) KLAUNCH(h, RX_K_PAM_FE, s, (k_pam_fe<true><<<gridc(f_hi - f_lo, FE_GROUPS), 256, 0, s>>>(d, in, f_lo, f_hi)));
+    else KLAUNCH(h, RX_K_PAM_FE, s, (k_pam_fe<false><<<gridc(f_hi - f_lo, FE_GROUPS), 256, 0, s>>>(d, in, f_lo, f_hi)));
+    // clock pass with a zero carry: N_loc (the first block's own count cancels out of every
+    // difference N_loc(b) - N_loc(beta B - 1))
+    const size_t smem = (CLK_TILE + 1 + 2 * d.clock_half) * sizeof(double2);
+    const unsigned ntiles = gridc(sb.c_hi - sb.c_lo, CLK_TILE);
+    KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_shard_clk_reset<<<1, 1, 0, s>>>(d)));
+    KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_pam_theta<false><<<ntiles, CLK_TILE, smem, s>>>(d, sb.c_lo, sb.c_hi, f_hi - 1, 0)));
+    KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_pam_carry<<<1, 1024, 0, s>>>(d, (int)ntiles)));
+    const long long own_hi = (beta + 1) * BB < sb.c_hi ? (beta + 1) * BB : sb.c_hi;
+    KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_shard_wraps<<<1, 1, 0, s>>>(d, beta, sb.c_lo, own_hi)));
+  }
+  sb.beta = beta;
+  sb.last = last;
+  sb.valid = 1;
+  sb.exported = 0;
+  sb.labels = labels_capacity ? d_labels : nullptr;
+  sb.cap = labels_capacity ? labels_capacity : 1;
   h->n_in += P1 < (beta + 1) * B4 ? P1 - beta * B4 : B4;
   return check_launch();
+}
+
+extern "C" rx_status rx_shard_halo(const rx_handle *h, long long *pre, long long *post) {
+  if (!h || !pre || !post) return RX_EINVAL;
+  *pre = h->sh_pre;
+  *post = h->sh_post;
+  return RX_OK;
 }
 
 extern "C" rx_status rx_carry_size(const rx_handle *h, int *bytes) {
@@ -1101,14 +1168,13 @@ extern "C" rx_status rx_export_carry(rx_handle *h, void *d_buf, void *stream) {
   CK(cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)stream;
   const long long beta = (h->sh_cur.valid && !h->sh_cur.exported) ? h->sh_cur.beta : -1;
-  KLAUNCH(h, RX_K_MISC, s, (k_carry_export<<<1, 1, 0, s>>>(h->d, (RxCarry *)d_buf, beta, h->sh_seed_e,
-                                                            h->sh_seed_e >= 0 ? 1 : 0)));
+  KLAUNCH(h, RX_K_MISC, s, (k_carry_export<<<1, 1, 0, s>>>(h->d, (RxCarry *)d_buf, beta, h->sh_norm_beta)));
   if (h->sh_cur.valid) h->sh_cur.exported = 1;
-  h->sh_seed_e = -1;
+  h->sh_norm_beta = -1;
   return check_launch();
 }
 
-// Stage B of one buffer (the equaliser of its epoch): z' valid below the buffer's front, the
+// KK stage B of one buffer (the equaliser of its epoch): z' valid below the buffer's front, the
 // finalisation front at the epoch's first segment, one round over the epoch's segments
 static void shard_stage_b(rx_handle *h, cudaStream_t s, const rx_handle::ShardBuf &b) {
   RxDev &d = h->d;
@@ -1117,20 +1183,64 @@ static void shard_stage_b(rx_handle *h, cudaStream_t s, const rx_handle::ShardBu
   if (b.last) KLAUNCH(h, RX_K_MISC, s, (k_kk_mend<<<1, 1, 0, s>>>(d, b.qfront)));   // stream end: m_end
   KLAUNCH(h, RX_K_MISC, s, (k_lms_snapshot<<<1, 1, 0, s>>>(d)));
   launch_lms_round(h, s, b.labels, b.cap, b.last ? 1 : 0, spe);
-  h->sh_seed_e = b.beta + d.D;   // k_lms_seeds produced the seed of epoch beta + D
 }
 
-// The gathered records of all n_ranks shards (rank order): CFO origin chain, sync / training,
-// seeds; then stage B of this shard's previous buffer (and, on the shard holding the stream
-// start, frame sync + training on buffer 0 as soon as its CFO estimate is known).
+// PAM stage B of one buffer (one round after its stage A2: the previous buffer's normalisation
+// scalars have arrived): its look-back symbols normalised with them, then one equaliser round
+// over the segments whose last tap position lies in the buffer's symbols
+static void shard_stage_b_pam(rx_handle *h, cudaStream_t s, const rx_handle::ShardBuf &b) {
+  RxDev &d = h->d;
+  KLAUNCH(h, RX_K_NORM, s, (k_shard_halo_norm<<<8, 256, 0, s>>>(d, b.beta)));
+  KLAUNCH(h, RX_K_MISC, s, (k_shard_seek_pam<<<1, 1, 0, s>>>(d, b.beta)));
+  KLAUNCH(h, RX_K_MISC, s, (k_lms_snapshot<<<1, 1, 0, s>>>(d)));
+  launch_lms_round(h, s, b.labels, b.cap, b.last ? 1 : 0, d.E_sym / d.S + 4);
+}
+
+// PAM stage A2 of one buffer (after the exchange that gave its global wrap base): tau_b / M_b,
+// the back-end (symbols u), the buffer's normalisation; frame sync + training at the stream start
+static void shard_stage_a2_pam(rx_handle *h, cudaStream_t s, const rx_handle::ShardBuf &b) {
+  RxDev &d = h->d;
+  KLAUNCH(h, RX_K_PAM_CLOCK, s, (k_shard_tau<<<gridc(b.c_hi - b.c_lo, 256), 256, 0, s>>>(d, b.c_lo, b.c_hi)));
+  if (d.H_real) KLAUNCH(h, RX_K_PAM_BE, s, (k_pam_be<true><<<gridc(b.be_hi - b.be_lo, FE_GROUPS), 256, 0, s>>>(d, b.be_lo, b.be_hi)));
+  else KLAUNCH(h, RX_K_PAM_BE, s, (k_pam_be<false><<<gridc(b.be_hi - b.be_lo, FE_GROUPS), 256, 0, s>>>(d, b.be_lo, b.be_hi)));
+  KLAUNCH(h, RX_K_NORM, s, (k_norm_stats<<<dim3(NORM_G, 1), 1024, 0, s>>>(d, b.beta, b.be_hi, b.last)));
+  KLAUNCH(h, RX_K_NORM, s, (k_norm_apply<<<dim3(NORM_AG, 1), 256, 0, s>>>(d, b.beta, 1, b.be_hi, b.last)));
+  KLAUNCH(h, RX_K_MISC, s, (k_shard_bufm<<<1, 1, 0, s>>>(d, b.beta, b.be_lo, b.be_hi)));
+  if (b.beta == 0) {                 // the stream start: frame sync + training (c-10, c-9)
+    KLAUNCH(h, RX_K_MISC, s, (k_lms_snapshot<<<1, 1, 0, s>>>(d)));
+    launch_sync_train<false>(h, s, b.last);
+  }
+  h->sh_norm_beta = b.beta;
+}
+
+// The gathered records of all n_ranks shards (rank order). KK: CFO origin chain, sync /
+// training, seeds; then stage B of this shard's previous buffer (and, on the shard holding the
+// stream start, frame sync + training on buffer 0 as soon as its CFO estimate is known).
+// PAM: wrap base, normalisation scalars, sync / training, seeds; stage B of the previous
+// buffer, then stage A2 of this round's. A call with nothing new (every rank's buffers done)
+// drains the last stage B.
 extern "C" rx_status rx_import_carry(rx_handle *h, const void *d_gathered, int n_ranks, int my_rank, void *stream) {
   if (!h || !d_gathered || h->d.shard_n <= 1 || n_ranks != h->d.shard_n || my_rank != h->d.shard_g) return RX_EINVAL;
   if (h->flushed) return RX_ESTATE;
   CK(cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)stream;
   RxDev &d = h->d;
-  KLAUNCH(h, RX_K_CFO, s, (k_carry_import<<<1, 1, 0, s>>>(d, (const RxCarry *)d_gathered, n_ranks)));
-  KLAUNCH(h, RX_K_CFO, s, (k_carry_chain<<<1, 1, 0, s>>>(d, (const RxCarry *)d_gathered, n_ranks)));
+  const RxCarry *g = (const RxCarry *)d_gathered;
+  const long long my_beta = h->sh_cur.valid ? h->sh_cur.beta : -1;
+  KLAUNCH(h, RX_K_MISC, s, (k_carry_import<<<1, 32, 0, s>>>(d, g, n_ranks, my_rank, my_beta)));
+  if (d.family == RX_PAM) {
+    if (h->sh_pend.valid) {
+      shard_stage_b_pam(h, s, h->sh_pend);
+      h->sh_pend.valid = 0;
+    }
+    if (h->sh_cur.valid) {
+      shard_stage_a2_pam(h, s, h->sh_cur);
+      h->sh_pend = h->sh_cur;
+      h->sh_cur.valid = 0;
+    }
+    return check_launch();
+  }
+  KLAUNCH(h, RX_K_CFO, s, (k_carry_chain<<<1, 1, 0, s>>>(d, g, n_ranks)));
   if (h->sh_pend.valid) {
     shard_stage_b(h, s, h->sh_pend);
     h->sh_pend.valid = 0;

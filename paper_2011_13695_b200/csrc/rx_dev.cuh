@@ -10,8 +10,12 @@
 #define RX_MAX_O 512
 
 struct DevState {
-  // ---- PAM clock recovery carries (unwrap needs the previous buffer's phase)
-  double theta_prev, thetau_prev;
+  // ---- PAM clock recovery carries (unwrap needs the previous buffer's phase).
+  // The unwrapped phase is theta^u_b = theta_b - 2 pi N_b with N_b = sum_{i <= b} rint((theta_i -
+  // theta_{i-1}) / 2 pi) (the telescoped sum of the wrapped differences): wraps_prev = N of the
+  // last block so far, an integer held in a double (exact), so it does not depend on how the
+  // stream is cut into calls or shards.
+  double theta_prev, wraps_prev;
   // ---- normalisation fronts
   long long v_front;        // PAM: uhat valid for m < v_front; KK: z' valid for q < v_front
   long long v_lms;          // the equaliser's snapshot of v_front, taken on the caller's stream
@@ -33,6 +37,10 @@ struct DevState {
   double evm_num, evm_den;
   long long symbols_out;
   int flags, pad1;
+  // ---- PAM time shard (SURVEY §8(e) mode 2): local wrap count of the reference block
+  // beta B - 1, wraps over the buffer's own blocks, the buffer's global base, the running
+  // total over the buffers imported so far
+  double sh_nref, sh_w, sh_nbase, wrap_total;
 };
 
 struct HostMirror {          // pinned, mapped: device writes hints the host reads lazily
@@ -45,6 +53,13 @@ struct CfoParam {            // per KK buffer (H19-H20)
   unsigned long long inc, origin;
   float inv_sqrtP;
   int kstar;
+};
+
+#define RX_CARRY_SEEDS 3
+struct SeedPart {            // one epoch's partial seed sum over the segments a round finalised
+  long long epoch;           // -1: unused
+  int n, pad;
+  long long sum[RX_MAX_K][2];
 };
 
 struct RxDev {
@@ -106,6 +121,11 @@ struct RxDev {
   float2 *w_init;                  // [K] start taps of training (rx_set_taps)
   int has_winit;
   float2 *seed; int *seed_ready; long long seed_cap;   // per epoch [K]
+  // lag-D seed accumulators per epoch (2^-32 fixed point, [seed_cap][RX_MAX_K][2]), segment
+  // counts, tags (e + 1), and the partial sums of the latest round staged for the shard record
+  long long *seed_acc; int *seed_cnt; long long *seed_tag;
+  struct SeedPart *seed_xp;
+  long long *buf_m;                // PAM shard: per buffer [4]: M of the pre-halo start, M_lo, M_hi
   int wl;                          // widely-linear equaliser (KK)
   float2 *v_train;                 // [K] trained v-branch (DD segments start theirs at 0)
   double *cal_part;                // PAM threshold calibration partials [CAL_G][16][2]

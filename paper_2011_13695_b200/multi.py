@@ -85,18 +85,19 @@ def run_time_sharded(R, codes, buffer_samples: int, labels, rank: int, world: in
     """SURVEY §8(e) mode 2 on one rank: this rank's handle R (shard_count = world, shard_index =
     rank) processes paper buffers rank, rank + world, ... of the stream `codes` (a device tensor
     of u16 codes holding the whole stream here; a deployment would receive only its buffers with
-    their halos), exchanging one carry record per round. gather(rec) -> all records (rank order);
-    default: gather_carry over the default process group."""
+    their halos, R.shard_halo()), exchanging one carry record per round, then one more exchange
+    that finishes the pending buffers. gather(rec) -> all records (rank order); default:
+    gather_carry over the default process group."""
     import torch
-    from .rx import SHARD_POST, SHARD_PRE
     gather = gather or gather_carry
+    pre, post = R.shard_halo()
     n = codes.numel()
     nbuf = -(-n // buffer_samples)
     rec = torch.zeros(R.carry_size(), dtype=torch.uint8, device=codes.device)
     for r in range(-(-nbuf // world) + 1):
         b = r * world + rank
         if b < nbuf:
-            p0, p1, last = shard_inputs(n, buffer_samples, b, SHARD_PRE, SHARD_POST)
+            p0, p1, last = shard_inputs(n, buffer_samples, b, pre, post)
             R.shard_process(b, codes[p0:p1], last=last, labels=labels, stream=stream)
         R.export_carry(rec, stream=stream)
         R.import_carry(gather(rec), world, rank, stream=stream)

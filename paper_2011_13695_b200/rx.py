@@ -90,9 +90,9 @@ EXPORTS = ("rx_config_default", "rx_create", "rx_process", "rx_flush", "rx_get_s
            "rx_reset_stats", "rx_get_taps", "rx_probe_read", "rx_destroy", "rx_strerror",
            "rx_version", "rx_profile_enable", "rx_profile_read", "rx_export_counters",
            "rx_set_taps", "rx_get_q_trace", "rx_calibrate_thresholds", "rx_calibrate_dc",
-           "rx_design_static_eq", "rx_shard_process", "rx_carry_size", "rx_export_carry",
+           "rx_design_static_eq", "rx_shard_process", "rx_shard_halo", "rx_carry_size", "rx_export_carry",
            "rx_import_carry", "rx_rt_enable", "rx_get_rt_stats", "tx_create", "tx_generate", "tx_destroy")
-SHARD_PRE, SHARD_POST = 4096, 4096       # RX_SHARD_PRE / RX_SHARD_POST (include/rx.h)
+SHARD_PRE, SHARD_POST = 4096, 4096       # RX_SHARD_PRE / RX_SHARD_POST (include/rx.h; KK halos)
 NCOUNTERS = 8
 COUNTERS = ("bit_errors", "bits", "symbols_counted", "evm_num", "evm_den", "clipped",
             "domain_errors", "symbols_out")
@@ -144,9 +144,10 @@ def load(path: str = SO_PATH):
     lib.rx_design_static_eq.restype = ctypes.c_int
     lib.rx_shard_process.argtypes = [vp, _c_ll, vp, _c_ll, ctypes.c_int, vp, _c_ll, vp]
     lib.rx_carry_size.argtypes = [vp, ctypes.POINTER(ctypes.c_int)]
+    lib.rx_shard_halo.argtypes = [vp, ctypes.POINTER(_c_ll), ctypes.POINTER(_c_ll)]
     lib.rx_export_carry.argtypes = [vp, vp, vp]
     lib.rx_import_carry.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int, vp]
-    for f in ("rx_shard_process", "rx_carry_size", "rx_export_carry", "rx_import_carry"):
+    for f in ("rx_shard_process", "rx_shard_halo", "rx_carry_size", "rx_export_carry", "rx_import_carry"):
         getattr(lib, f).restype = ctypes.c_int
     lib.rx_rt_enable.argtypes = [vp, ctypes.c_int]
     lib.rx_rt_enable.restype = ctypes.c_int
@@ -245,11 +246,18 @@ class Receiver:
     # -- time sharding of one stream (SURVEY §8(e) mode 2; include/rx.h rx_shard_process)
     def shard_process(self, buffer: int, samples, last: bool = False, labels=None, stream=None):
         """Stage A of paper buffer `buffer` (owned by this shard): `samples` = u16 codes of
-        [max(0, buffer B4 - SHARD_PRE), (buffer + 1) B4 + SHARD_POST) of the stream."""
+        [max(0, buffer B4 - pre), (buffer + 1) B4 + post) of the stream, (pre, post) =
+        shard_halo()."""
         lp, lc = (labels.data_ptr(), labels.numel()) if labels is not None else (None, 0)
         _check(load().rx_shard_process(self._h, int(buffer), ctypes.c_void_p(samples.data_ptr()),
                                        int(samples.numel()), int(bool(last)), ctypes.c_void_p(lp), lc,
                                        _stream_ptr(stream)), "rx_shard_process")
+
+    def shard_halo(self) -> tuple[int, int]:
+        """Input halos (samples before / after a buffer) its shard reads (rx_shard_halo)."""
+        a, b = _c_ll(), _c_ll()
+        _check(load().rx_shard_halo(self._h, ctypes.byref(a), ctypes.byref(b)), "rx_shard_halo")
+        return a.value, b.value
 
     def carry_size(self) -> int:
         n = ctypes.c_int()

@@ -149,8 +149,10 @@ def test_round2_config_fields_validated_before_touching_the_gpu(lib):
     pt = np.ones(503)
     p.static_taps = pt.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
     p.n_static_taps = 503
-    p.shard_count = 2
-    assert lib.rx_create(ctypes.byref(p), 0, ctypes.byref(h)) == -1           # PAM: not sharded
+    p.shard_count = 7
+    assert lib.rx_create(ctypes.byref(p), 0, ctypes.byref(h)) == -1           # PAM: N <= D - 2
+    lo, hi = ctypes.c_longlong(), ctypes.c_longlong()
+    assert lib.rx_shard_halo(None, ctypes.byref(lo), ctypes.byref(hi)) == -1
     n = ctypes.c_int()
     assert lib.rx_carry_size(None, ctypes.byref(n)) == -1
     assert lib.rx_shard_process(None, 0, None, 0, 0, None, 0, None) == -1

@@ -924,6 +924,70 @@ def test_time_sharded_kk_stream_is_bit_identical(N):
             h.close()
 
 
+@pytest.mark.parametrize("N,D,clk", [(2, 8, dict(ppm=20.0)), (4, 8, dict(ppm=-30.0)),
+                                     (6, 8, dict(ppm=0.0, ppm_triangle=20.0)), (8, 10, dict(ppm=30.0))])
+def test_time_sharded_pam_stream_is_bit_identical(N, D, clk):
+    """SURVEY §8(e) mode 2 for the PAM chain (P:156-158: the clock phase of the previous buffer;
+    c-5 buffer normalisation; c-9 lag-D seeds), emulated in one process on one GPU: a C2-structure
+    stream (PAM-16, 91 km-like ISI, 24 paper buffers of 256 blocks; static sampling-clock offsets
+    of +20 / -30 / +30 ppm and a +-20 ppm triangle (Fig. 4 / 5): symbol epochs drift against the
+    buffers, and the last segment of every epoch has its last taps in the next buffer, so each
+    epoch's segments land on two shards) split over N shard handles, buffer b on shard b mod N with its input halos
+    (rx_shard_halo), one carry record per shard and round all-gathered in rank order (wrap counts,
+    normalisation scalars, sync / training, seed partials). Each symbol's label is written by
+    exactly one shard and equals one handle's on the same stream (chunked calls, side-stream
+    equaliser); integer counters summed over the shards are equal, EVM sums agree to rounding;
+    with a partial last buffer too."""
+    torch = _torch_cuda()
+    from paper_2011_13695_b200 import RX_PAM, Receiver, multi
+    B4 = 256 * 512
+    for n in (24 * B4, 21 * B4 + 7 * 4096):
+        rec, rx = make_config("C2", n_samples=n, **clk)
+        rx.update(buffer_blocks=256, tap_lag_epochs=D)
+        R1, lab1, st1 = run_gpu(rec, rx, chunk=3 * B4)
+        fields = {k: v for k, v in rx.items() if k in ("lms_taps", "lms_block", "lms_segment", "lms_overlap", "mu",
+                                                       "train_symbols", "sync_start", "sync_window",
+                                                       "warmup_symbols", "buffer_blocks", "tap_lag_epochs")}
+        codes = torch.from_numpy(rec.codes.view(np.int16)).cuda()
+        hs = [Receiver(RX_PAM, rec.M, rec.static_taps, history_buffers=4, shard_count=N, shard_index=g, **fields)
+              for g in range(N)]
+        pre, post = hs[0].shard_halo()
+        nsym = n // 2 + 4096
+        labs = [torch.full((nsym,), 0xFF, dtype=torch.uint8, device="cuda") for _ in range(N)]
+        recs = [torch.zeros(hs[0].carry_size(), dtype=torch.uint8, device="cuda") for _ in range(N)]
+        nbuf = -(-n // B4)
+        for r in range(-(-nbuf // N) + 1):          # the emulated ranks, round by round (+ the drain)
+            for g in range(N):
+                b = r * N + g
+                if b < nbuf:
+                    p0, p1, last = multi.shard_inputs(n, B4, b, pre, post)
+                    hs[g].shard_process(b, codes[p0:p1], last=last, labels=labs[g])
+                hs[g].export_carry(recs[g])
+            allrec = torch.cat(recs)                # = the NCCL all-gather, rank order
+            for g in range(N):
+                hs[g].import_carry(allrec, N, g)
+        sts = [h.stats() for h in hs]
+        m_end = st1["symbols_out"]
+        got = np.full(m_end, 0xFF, dtype=np.uint8)
+        writers = np.zeros(m_end, dtype=np.int32)
+        for g in range(N):
+            lg = labs[g].cpu().numpy()[:m_end]
+            w = lg != 0xFF
+            got[w] = lg[w]
+            writers += w
+        diff = np.nonzero(got != lab1[:m_end])[0]
+        print(f"N={N} D={D} {clk} n={n}: pre/post {pre}/{post}, {m_end} symbols, {diff.size} labels differ"
+              + (f" (first {diff[:5]})" if diff.size else "") + f", writers {writers.min()}..{writers.max()}")
+        assert diff.size == 0 and writers.min() == 1 and writers.max() == 1
+        for k in ("bit_errors", "bits", "symbols_counted", "clipped"):
+            assert sum(s[k] for s in sts) == st1[k], (k, [s[k] for s in sts], st1[k])
+        assert abs(sum(s["evm_num"] for s in sts) - st1["evm_num"]) <= 1e-9 * st1["evm_num"]
+        assert st1["bits"] > 0 and st1["bit_errors"] < 1e-2 * st1["bits"]      # short PAM-16 record
+        assert all(s["sync_offset"] == st1["sync_offset"] for s in sts)
+        for h in hs:
+            h.close()
+
+
 @pytest.mark.parametrize("name,extra", [
     # the paper's field trial shared a 10 MHz reference between Tx and Rx (P:230: only small phase
     # fluctuations for the DDLMS to track): 1 kHz linewidth here
