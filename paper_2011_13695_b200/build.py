@@ -11,7 +11,8 @@ ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "librx.so")
 SOURCES = ["csrc/rx_api.cu", "csrc/tx_api.cu"]
 DEPS = ["csrc/rx_api.cu", "csrc/common.cuh", "csrc/fft.cuh", "csrc/rx_dev.cuh", "csrc/k_pam.cuh",
-        "csrc/k_kk.cuh", "csrc/k_lms.cuh", "../include/rx.h", "csrc/tx_api.cu", "../include/tx.h"]
+        "csrc/k_kk.cuh", "csrc/k_lms.cuh", "csrc/k_shard.cuh", "../include/rx.h", "csrc/tx_api.cu",
+        "../include/tx.h"]
 
 
 def _git_rev() -> str:

@@ -221,8 +221,17 @@ __device__ __forceinline__ float2 dds_rot_neg_fast(unsigned long long u) {
 // a buffer's spectrum rows (last-CTA ticket in k_cfo_spec) reduces them in fixed row order
 // (CFO_SPEC_T threads, each owning the bins k = t + CFO_SPEC_T i)
 #define CFO_SPEC_T 256
-#define CFO_ROWS 128           // spectrum rows (CTAs) per buffer
+// spectrum rows (CTAs) per buffer and the resident CTAs per SM the register allocation must
+// allow: 3 x 148 SMs hold a 4-buffer call's 416 CTAs in one wave with 80 registers (no spills;
+// 4 CTAs per SM capped them at 64 with 48 B of stack)
+#ifndef CFO_ROWS
+#define CFO_ROWS 104
+#endif
+#ifndef CFO_MINB
+#define CFO_MINB 3
+#endif
 #define CFO_GRP 8              // rows summed per group in the two-level row reduction
+static_assert(CFO_ROWS % CFO_GRP == 0, "CFO_ROWS must be a multiple of CFO_GRP");
 #define CFO_KPT (1024 / CFO_SPEC_T)
 __device__ __forceinline__ void cfo_final_block(const RxDev &d, long long beta, long long qfront, long long rb, int nrows) {
   __shared__ double Sd[1024];
@@ -300,7 +309,7 @@ __device__ __forceinline__ void cfo_final_block(const RxDev &d, long long beta, 
 // step, every CTA resident in one wave), accumulates |X[k]|^2 of its chunks per thread in
 // registers (chunk order), then sums the 4 groups in fixed order into row x. The power partial
 // sums the same samples (plus, in CTA 0, the tail beyond the last complete chunk).
-__global__ void __launch_bounds__(CFO_SPEC_T, 4) k_cfo_spec(RxDev d, long long beta0, long long qfront) {
+__global__ void __launch_bounds__(CFO_SPEC_T, CFO_MINB) k_cfo_spec(RxDev d, long long beta0, long long qfront) {
   __shared__ float2 tw[1024];
   __shared__ float2 bufs[CFO_SPEC_T / 64][FFT_PAD_N];   // FFT scratch; later acc[4][1024] floats
   __shared__ double red[CFO_SPEC_T / 32];

@@ -207,6 +207,20 @@ __device__ __forceinline__ void lms_stage(const RxDev &d, LmsSmemT<CPLX> &sm, lo
   }
 }
 
+// BPS rounding: two FADDs with the 1.5 2^23 shift (round to nearest even, exact for |u| < 2^22)
+// instead of FRND (measured: C4 +1-2 %, the FRND pipe is shared with the concurrent front-end).
+// Beyond 2^22 both forms clamp to the same level, so the distances are identical for every input.
+#ifndef BPS_MAGIC
+#define BPS_MAGIC 1
+#endif
+__device__ __forceinline__ float bps_rint(float u) {
+#if BPS_MAGIC
+  return __fadd_rn(__fadd_rn(u, 12582912.f), -12582912.f);
+#else
+  return rintf(u);
+#endif
+}
+
 // Blind phase search partial sums over symbols [i0, i1) of a block (lane p: test phases p and
 // p + 32). Distances are in units of the level spacing 2s: u = y e^{-j phi_p} / 2s + (L - 1)/2
 // puts the levels on the integers 0..L-1, so |z - slice(z)|^2 = (2s)^2 sum (u - clamp(rint u))^2
@@ -216,8 +230,8 @@ __device__ __forceinline__ void lms_stage(const RxDev &d, LmsSmemT<CPLX> &sm, lo
 __device__ __forceinline__ void bps_acc(float2 yi, float2 r, float cst, float Lm1, float &acc) {
   const float ux = fmaf(yi.x, r.x, fmaf(-yi.y, r.y, cst));
   const float uy = fmaf(yi.x, r.y, fmaf(yi.y, r.x, cst));
-  const float ex = ux - fminf(fmaxf(rintf(ux), 0.f), Lm1);
-  const float ey = uy - fminf(fmaxf(rintf(uy), 0.f), Lm1);
+  const float ex = ux - fminf(fmaxf(bps_rint(ux), 0.f), Lm1);
+  const float ey = uy - fminf(fmaxf(bps_rint(uy), 0.f), Lm1);
   acc = fmaf(ex, ex, acc);
   acc = fmaf(ey, ey, acc);
 }
@@ -535,10 +549,10 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
                 const float A = fmaf(yx, cq, cst), C = fmaf(yq, cq, cst);
                 const float uxp = fmaf(yq, sq, A), uxm = fmaf(-yq, sq, A);    // phase q / 31 - q
                 const float uyp = fmaf(-yx, sq, C), uym = fmaf(yx, sq, C);
-                const float exp_ = uxp - fminf(fmaxf(rintf(uxp), 0.f), Lm1);
-                const float eyp = uyp - fminf(fmaxf(rintf(uyp), 0.f), Lm1);
-                const float exm = uxm - fminf(fmaxf(rintf(uxm), 0.f), Lm1);
-                const float eym = uym - fminf(fmaxf(rintf(uym), 0.f), Lm1);
+                const float exp_ = uxp - fminf(fmaxf(bps_rint(uxp), 0.f), Lm1);
+                const float eyp = uyp - fminf(fmaxf(bps_rint(uyp), 0.f), Lm1);
+                const float exm = uxm - fminf(fmaxf(bps_rint(uxm), 0.f), Lm1);
+                const float eym = uym - fminf(fmaxf(bps_rint(uym), 0.f), Lm1);
                 float &P = hsym ? p1 : p0, &Mm = hsym ? m1 : m0;
                 P = fmaf(exp_, exp_, P);
                 P = fmaf(eyp, eyp, P);
@@ -846,11 +860,16 @@ __device__ void bps_helper(const RxDev &d, const float2 *ys, long long t_begin, 
 #define LMS_SPC_PAM 4
 #endif
 #define LMS_SPC_OF(CPLX) ((CPLX) ? LMS_SPC_KK : LMS_SPC_PAM)
+// minimum resident CTAs per SM the register allocation must allow (0: the compiler default)
+#ifndef LMS_MINB_KK
+#define LMS_MINB_KK 0
+#endif
+#define LMS_MINB_OF(CPLX) ((CPLX) ? LMS_MINB_KK : 0)
 #ifndef LMS_PAIR
 #define LMS_PAIR 1          // BPS segments: 2 = a helper warp scores half of each block's symbols
 #endif
 template <bool CPLX, int CPR, int KP, bool WLIN = false, int MODE = 1>
-__global__ void __launch_bounds__(32 * LMS_SPC_OF(CPLX)) k_lms_seg(RxDev d, int flush, int nseg, unsigned char *labels,
+__global__ void __launch_bounds__(32 * LMS_SPC_OF(CPLX), LMS_MINB_OF(CPLX)) k_lms_seg(RxDev d, int flush, int nseg, unsigned char *labels,
                                                  long long lab_cap) {
   // BPS segments run on a warp pair (LMS warp + BPS helper), others on one warp
   constexpr int PAIR = (CPR == 2) ? LMS_PAIR : 1, SPC = LMS_SPC_OF(CPLX) / PAIR;   // PAIR = 2: BPS helper warp
