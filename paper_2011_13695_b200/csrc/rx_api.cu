@@ -516,7 +516,7 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
       d.xs_cap = next_pow2(c.buffer_blocks + h->sh_pb + 2 * c.clock_avg_half + 8);
     TRY(dalloc(h, &d.Xspec, d.xs_cap * 512));
   }
-  d.buf_cap = 64;
+
   // equaliser batch + the seed-blocked tail that may wait for the next batch (<= D epochs)
   const long long E_sym = (long long)c.buffer_blocks * (kk ? 128 : 256);
   const long long tail_sym = (long long)c.tap_lag_epochs * E_sym;
@@ -526,6 +526,13 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   // current call writes up to one more call of them)
   // (equaliser_lag = 1: the side stream may still read one more call of them)
   const long long lag_calls = 1 + c.equaliser_lag;
+  // per-buffer scalars (KK CFO parameters: z' is formed from them where the equaliser reads it;
+  // PAM normalisation): every buffer the equaliser may still read - one batch + the seed-blocked
+  // tail behind the front - plus the calls in flight on both streams
+  {
+    const long long need = batch_sym / E_sym + 2LL * HB + 4;
+    d.buf_cap = next_pow2(need > 64 ? need : 64);
+  }
   d.sym_cap = next_pow2((long long)(HB + lag_calls * (HB - 2)) * c.buffer_blocks * (kk ? 128 : 260) + batch_sym);
   if (!kk && c.shard_count > 1) {   // buffers b and b + N (and halos) are held together
     const long long need = (long long)(c.shard_count + 2) * c.buffer_blocks * 260;

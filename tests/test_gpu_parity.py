@@ -300,6 +300,29 @@ def test_chunking_invariance():
     assert abs(sa["evm_num"] - sb["evm_num"]) <= 1e-9 * sa["evm_num"]
 
 
+@pytest.mark.parametrize("name", ["C3", "C2"])
+def test_large_history_calls_match_small_calls(name):
+    """the per-buffer scalars (KK CFO parameters, from which z' is formed where the
+    equaliser reads it; PAM normalisation) must outlive every buffer the equaliser may still read.
+    With 256-block buffers the default equaliser batch (2048 KK / 4096 PAM segments) spans ~128
+    buffers, so the equaliser runs far behind the front: 123 buffers in 38-buffer calls
+    (history_buffers = 40) and in 2-buffer calls (history_buffers = 4) give the labels and
+    integer counters of a run whose rounds keep up (lms_batch_segments = D epochs of segments)."""
+    _torch_cuda()
+    B4 = 256 * 512
+    rec, rx = make_config(name, n_samples=3 * 38 * B4 + 9 * B4)
+    rx["buffer_blocks"] = 256
+    _, lr, sr = run_gpu(rec, dict(rx, lms_batch_segments=8 * 256 * (128 if name == "C3" else 256) // 4096),
+                        chunk=2 * B4, history_buffers=4)
+    for chunk, hb in ((38 * B4, 40), (2 * B4, 4)):
+        _, la, sa = run_gpu(rec, rx, chunk=chunk, history_buffers=hb)
+        d = np.nonzero(la != lr)[0]
+        assert d.size == 0, (hb, d.size, d[:5])
+        for k in ("bit_errors", "bits", "symbols_counted", "clipped", "domain_errors", "sync_offset"):
+            assert sa[k] == sr[k], (hb, k)
+    assert sr["bits"] > 0
+
+
 def test_f32_input_matches_u16():
     """RX_IN_F32 (x already in x units) reproduces the u16 path: same labels and counters up to
     threshold flips, fields within fp32 rounding (SURVEY §8(b) rx_input_format)."""

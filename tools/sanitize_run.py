@@ -64,3 +64,25 @@ for r in range(nbuf // 2 + 1):
     for g in range(2):
         hs[g].import_carry(torch.cat(recs), 2, g)
 print("KK 2 shards", [h.stats()["bits"] for h in hs])
+# PAM time shards (C2 structure, 2 shards, 8 buffers of 128 blocks, PB look-back + clock halos)
+from paper_2011_13695_b200 import RX_PAM  # noqa: E402
+rec, rx = make_config("C2", n_samples=8 * 128 * 512)
+fields = {k: v for k, v in rx.items() if k in ("lms_taps", "lms_block", "lms_segment", "lms_overlap", "mu",
+                                               "sync_start", "sync_window")}
+hs = [Receiver(RX_PAM, rec.M, rec.static_taps, history_buffers=4, buffer_blocks=128, train_symbols=8192,
+               warmup_symbols=8192, shard_count=2, shard_index=g, **fields) for g in range(2)]
+pre, post = hs[0].shard_halo()
+codes = torch.from_numpy(rec.codes.view(np.int16)).cuda()
+labs = [torch.zeros(rec.n // 2 + 4096, dtype=torch.uint8, device="cuda") for _ in range(2)]
+recs = [torch.zeros(hs[0].carry_size(), dtype=torch.uint8, device="cuda") for _ in range(2)]
+nbuf = rec.n // (128 * 512)
+for r in range(nbuf // 2 + 1):
+    for g in range(2):
+        b = 2 * r + g
+        if b < nbuf:
+            p0, p1, last = multi.shard_inputs(rec.n, 128 * 512, b, pre, post)
+            hs[g].shard_process(b, codes[p0:p1], last=last, labels=labs[g])
+        hs[g].export_carry(recs[g])
+    for g in range(2):
+        hs[g].import_carry(torch.cat(recs), 2, g)
+print("PAM 2 shards", [h.stats()["bits"] for h in hs])
