@@ -121,8 +121,9 @@ struct rx_handle {
   long long ncall;                   // streaming rx_process calls so far
   long long lms_sym_ub;          // symbol upper bound of the data normalised by earlier calls
   uint16_t *unpacked;            // RX_IN_U12_PACKED: this call's codes unpacked to u16
-  struct ZpJob { long long beta0, nb, q_front; };
-  std::vector<ZpJob> zp_pending; // KK: CFO carry + z' groups deferred to the next call's side stream
+  struct ZpJob { long long beta0, nb, q_front; int est; };
+  std::vector<ZpJob> zp_pending; // KK: CFO groups deferred to the next call's side stream (est = 1:
+                                 // estimate + carry, 0: carry only)
   long long clk_launch;          // fused clock launches so far (tags the tile totals)
   bool flushed;
   // time sharding (shard_count > 1): the buffer whose stage A ran last (awaiting export / stage B)
@@ -940,7 +941,12 @@ static void run_pam(rx_handle *h, cudaStream_t s, const InView &in, unsigned cha
 // KK: the deferred CFO carries, in buffer order (the DDS origin is a chain)
 static void launch_zp_pending(rx_handle *h, cudaStream_t s) {
   RxDev &d = h->d;
+  const int fine_ctas = (int)((h->Q / 1024 + 7) / 8);
   for (const auto &j : h->zp_pending) {
+    if (j.est) {   // plain launches: the producer (stage 2) is on the other stream (event order)
+      KLAUNCH(h, RX_K_CFO, s, (k_cfo_spec<<<dim3(CFO_ROWS, (unsigned)j.nb), CFO_SPEC_T, 0, s>>>(d, j.beta0, j.q_front)));
+      if (d.cfo_enable) KLAUNCH(h, RX_K_CFO, s, (k_cfo_fine<<<dim3((unsigned)fine_ctas, (unsigned)j.nb), 256, 0, s>>>(d, j.beta0, j.q_front, fine_ctas)));
+    }
     KLAUNCH(h, RX_K_CFO, s, (k_cfo_carry<<<1, 1, 0, s>>>(d, j.beta0, (int)j.nb, j.q_front)));
   }
   h->zp_pending.clear();
@@ -970,12 +976,15 @@ static void run_kk(rx_handle *h, cudaStream_t s, const InView &in, unsigned char
       const int fine_ctas = (int)((Q / 1024 + 7) / 8);
       for (long long b0 = 0; b0 < nbuf; b0 += h->cfg.history_buffers) {
         const long long nb = nbuf - b0 < h->cfg.history_buffers ? nbuf - b0 : h->cfg.history_buffers;
-        KLAUNCH(h, RX_K_CFO, s, launch_pdl(k_cfo_spec, dim3(CFO_ROWS, (unsigned)nb), CFO_SPEC_T, 0, s, d, beta0 + b0, q_front));
-        if (d.cfo_enable) KLAUNCH(h, RX_K_CFO, s, launch_pdl(k_cfo_fine, dim3((unsigned)fine_ctas, (unsigned)nb), 256, 0, s, d, beta0 + b0, q_front, fine_ctas));
         if (flush || h->cfg.serial_equaliser) {
+          KLAUNCH(h, RX_K_CFO, s, launch_pdl(k_cfo_spec, dim3(CFO_ROWS, (unsigned)nb), CFO_SPEC_T, 0, s, d, beta0 + b0, q_front));
+          if (d.cfo_enable) KLAUNCH(h, RX_K_CFO, s, launch_pdl(k_cfo_fine, dim3((unsigned)fine_ctas, (unsigned)nb), 256, 0, s, d, beta0 + b0, q_front, fine_ctas));
           KLAUNCH(h, RX_K_CFO, s, (k_cfo_carry<<<1, 1, 0, s>>>(d, beta0 + b0, (int)nb, q_front)));
-        } else {   // the DDS carry (z' validity) only feeds the equaliser: next call, side stream
-          h->zp_pending.push_back({beta0 + b0, nb, q_front});
+        } else {
+          // the CFO estimate and the DDS carry only feed the equaliser (z' where it is read):
+          // they run at the next call on the side stream, concurrently with that call's
+          // front-end (the paper overlaps consecutive buffers across streams)
+          h->zp_pending.push_back({beta0 + b0, nb, q_front, 1});
         }
       }
       h->cfo_done += nbuf;
