@@ -59,6 +59,7 @@ FLOPS_PER_BLOCK = {
     "KK_S1": 2 * FFT_R1024 + 512 * 12,                # R2C + C2R + reconstruction   = 57,344
     "KK_S2": 5 * 1024 * 10 + 512 * 6 + 5 * 512 * 9,   # C2C + EQ + IFFT-512           = 77,312
 }
+FLOPS_PER_BLOCK["KK_FE"] = FLOPS_PER_BLOCK["KK_S1"] + FLOPS_PER_BLOCK["KK_S2"]   # fused stages = 134,656
 
 
 def class_flops(name, n_step, rx, kk):

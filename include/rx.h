@@ -150,6 +150,12 @@ typedef struct {
                                  stitching / labels / counters / seeds) is captured once as a CUDA
                                  graph and replayed per round (its kernels read every per-round
                                  quantity from device state); 0: launched kernel by kernel */
+  int fused_front_end;        /* KK: 1 = both overlap-save stages (H11-H18) in one kernel (k_kk_fe),
+                                 the 4-sps field E kept in shared memory (P:213 'to limit GPU memory
+                                 access'; RX_PROBE_E then returns RX_EINVAL); 0 (default) = two
+                                 kernels with E through an HBM ring (measured faster on B200, see
+                                 DESIGN §6). z, labels and counters are bit-identical either way.
+                                 Time shards (rx_shard_process) use the two kernels */
 } rx_config;
 
 /* Sample formats accepted by rx_process:
@@ -313,7 +319,8 @@ typedef enum {
   RX_K_LMS = 8,         /* H9, H21-H23 segment-parallel block-LMS + CPR + decisions */
   RX_K_LMS_POST = 9,    /* H22-H25 stitching, R_s scan, labels, counters, seeds */
   RX_K_MISC = 10,       /* history copy, bookkeeping */
-  RX_KCLASS_COUNT = 11
+  RX_K_KK_FE = 11,      /* H0, H11-H18 fused KK front-end (fused_front_end = 1): both stages, E on chip */
+  RX_KCLASS_COUNT = 12
 } rx_kernel_class;
 rx_status rx_profile_enable(rx_handle *h, int mask);
 rx_status rx_profile_read(rx_handle *h, double *host_ms, long long *host_counts, int n);

@@ -8,16 +8,24 @@
 #define RX_PREF 32767
 
 // ------------------------------------------------------------------ complex helpers
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+// Complex arithmetic on the sm_100 packed FP32x2 pipe (FADD2 / FMUL2 / FFMA2: two IEEE fp32
+// operations per instruction, each rounded exactly like its scalar form; the operand swaps,
+// broadcasts and single-half negations these need are free SASS modifiers). The FP32 throughput is
+// unchanged (a packed op occupies the FMA pipe for two cycles) but the issue slots of the FFT
+// butterflies, twiddle products and BPS distances halve - the chain's kernels are issue-bound.
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+// a b = (fma(a.x, b.x, -a.y b.y), fma(a.x, b.y, a.y b.x)): one FMUL2 + one FFMA2
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+  const float2 t = __fmul2_rn(make_float2(a.y, a.y), make_float2(b.y, b.x));
+  return __ffma2_rn(make_float2(a.x, a.x), b, make_float2(-t.x, t.y));
 }
-__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // a * conj(b)
-  return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // a * conj(b) = (fma(a.x, b.x, a.y b.y), fma(a.y, b.x, -a.x b.y))
+  const float2 t = __fmul2_rn(make_float2(a.y, a.x), make_float2(b.y, b.y));
+  return __ffma2_rn(a, make_float2(b.x, b.x), make_float2(t.x, -t.y));
 }
 __device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
-__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return __fmul2_rn(a, make_float2(s, s)); }
 __device__ __forceinline__ float2 cmul_i(float2 a) { return make_float2(-a.y, a.x); }    // i a
 __device__ __forceinline__ float2 cmul_mi(float2 a) { return make_float2(a.y, -a.x); }   // -i a
 __device__ __forceinline__ float cabs2(float2 a) { return fmaf(a.x, a.x, a.y * a.y); }

@@ -48,14 +48,17 @@ __device__ __forceinline__ void dft8(float2 (&v)[8]) {
   float2 a1 = cadd(v[1], v[5]), a5 = csub(v[1], v[5]);
   float2 a2 = cadd(v[2], v[6]), a6 = csub(v[2], v[6]);
   float2 a3 = cadd(v[3], v[7]), a7 = csub(v[3], v[7]);
+  // (packed: one FADD2 on the swapped / half-negated operand, one FMUL2; same roundings as
+  // the scalar (x +- y) * r)
+  const float2 rr = make_float2(r, r);
   if (!INV) {
-    a5 = make_float2((a5.x + a5.y) * r, (a5.y - a5.x) * r);      // * (1 - i)/sqrt2
-    a6 = cmul_mi(a6);                                            // * -i
-    a7 = make_float2((a7.y - a7.x) * r, -(a7.x + a7.y) * r);     // * (-1 - i)/sqrt2
+    a5 = __fmul2_rn(__fadd2_rn(a5, make_float2(a5.y, -a5.x)), rr);            // * (1 - i)/sqrt2
+    a6 = cmul_mi(a6);                                                       // * -i
+    a7 = __fmul2_rn(__fadd2_rn(make_float2(a7.y, -a7.x), make_float2(-a7.x, -a7.y)), rr);   // * (-1 - i)/sqrt2
   } else {
-    a5 = make_float2((a5.x - a5.y) * r, (a5.y + a5.x) * r);      // * (1 + i)/sqrt2
+    a5 = __fmul2_rn(__fadd2_rn(a5, make_float2(-a5.y, a5.x)), rr);            // * (1 + i)/sqrt2
     a6 = cmul_i(a6);
-    a7 = make_float2(-(a7.x + a7.y) * r, (a7.x - a7.y) * r);     // * (-1 + i)/sqrt2
+    a7 = __fmul2_rn(__fadd2_rn(make_float2(-a7.x, a7.x), make_float2(-a7.y, -a7.y)), rr);   // * (-1 + i)/sqrt2
   }
   // stage 2 (span 2)
   float2 b0 = cadd(a0, a2), b2 = csub(a0, a2);

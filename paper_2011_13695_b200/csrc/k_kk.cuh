@@ -12,13 +12,15 @@
 #include "k_pam.cuh"
 
 // ------------------------------------------------------------------ H0, H11-H15
-__global__ void __launch_bounds__(256) k_kk_s1(RxDev d, InView in, long long b0, long long b1) {
-  __shared__ float2 tw[1024];
-  __shared__ float2 buf[FE_GROUPS][FFT_PAD_N];
-  const int g = threadIdx.x >> 6, j = threadIdx.x & 63;
-  tw_stage_async(tw, d.tw);   // waited for (tw_wait) before the first FFT pass
-  const long long b = b0 + (long long)blockIdx.x * FE_GROUPS + g;
-  const bool act = b < b1;
+// Stage 1 of block b by the 64-thread group j = 0..63 (every thread of the CTA calls it: the FFT
+// barriers are CTA-wide). act = 0: the group idles through the barriers; count: the block's owned
+// samples are counted (clipped / domain errors; the fused front-end recomputes halo blocks
+// uncounted). wait_tw: the twiddle table's cp.async staging is waited for before the first FFT.
+// The reconstructed pairs (E_p, E_{p+1}), p = 512 b - 512 + 2 (j + 64 r), r = 2..5, p >= 0, go to
+// sink(r, p, pair).
+template <class Sink>
+__device__ __forceinline__ void kk_s1_block(const RxDev &d, const InView &in, long long b, bool act, bool count,
+                                            bool wait_tw, int j, const float2 *tw, float2 *buf, Sink sink) {
   int clip = 0, dom = 0;
   long long first_dom = 0x7fffffffffffffffLL;
   float2 v[8];
@@ -49,7 +51,7 @@ __global__ void __launch_bounds__(256) k_kk_s1(RxDev d, InView in, long long b0,
 #pragma unroll
     for (int r = 0; r < 4; ++r) amp[r][0] = amp[r][1] = 0.f;
   }
-  if (b < in.cnt_lo || b >= in.cnt_hi) {   // a time shard's halo block: counted by its owner
+  if (!count || b < in.cnt_lo || b >= in.cnt_hi) {   // a time shard's halo block: counted by its owner
     clip = 0;
     dom = 0;
     first_dom = 0x7fffffffffffffffLL;
@@ -58,12 +60,12 @@ __global__ void __launch_bounds__(256) k_kk_s1(RxDev d, InView in, long long b0,
   dom = __reduce_add_sync(0xffffffffu, dom);
   if ((threadIdx.x & 31) == 0 && dom) atomicAdd((unsigned long long *)&d.st->domain_errors, (unsigned long long)dom);
   if (first_dom != 0x7fffffffffffffffLL) atomicMin(&d.st->first_domain, first_dom);
-  tw_wait();
-  fft512_regs<false>(buf[g], j, tw, v);
-  fft512_publish_upper(buf[g], j, v);
+  if (wait_tw) tw_wait();
+  fft512_regs<false>(buf, j, tw, v);
+  fft512_publish_upper(buf, j, v);
   // FD Hilbert (c-6, A8): Phi = -j sgn(kappa) H, Phi[0] = Phi[512] = 0
   float2 Zk[4], Zn[4];
-  const float2 *pm = fft_mirror_base(buf[g], j);
+  const float2 *pm = fft_mirror_base(buf, j);
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     const int k = j + 64 * r;
@@ -76,17 +78,17 @@ __global__ void __launch_bounds__(256) k_kk_s1(RxDev d, InView in, long long b0,
   const float2 Z256 = cconj(cmul_mi(cconj(v[4])));
   __syncthreads();
   {
-    float2 *paw = buf[g] + j + (j >> 4);
-    float2 *pmw = buf[g] + (512 - j) + ((512 - j) >> 4);
+    float2 *paw = buf + j + (j >> 4);
+    float2 *pmw = buf + (512 - j) + ((512 - j) >> 4);
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       paw[68 * r] = Zk[r];
       if (!(j == 0 && r == 0)) pmw[-68 * r] = Zn[r];
     }
-    if (j == 0) buf[g][256 + (256 >> 4)] = Z256;
+    if (j == 0) buf[256 + (256 >> 4)] = Z256;
   }
   __syncthreads();
-  fft512<true>(buf[g], j, tw, v);
+  fft512<true>(buf, j, tw, v);
   // v[r] = 512 (phi[2n] + i phi[2n+1]), n = j + 64 r; kept local [256, 768) <=> r = 2..5
   if (act) {
     const float sg = (float)d.sideband;
@@ -113,9 +115,22 @@ __global__ void __launch_bounds__(256) k_kk_s1(RxDev d, InView in, long long b0,
       const float a0 = amp[r - 2][0], a1 = amp[r - 2][1];
       const float2 e0 = cmul(make_float2(a0 * c0, a0 * s0), r0);
       const float2 e1 = cmul(make_float2(a1 * c1, a1 * s1), r1);
-      *reinterpret_cast<float4 *>(d.E + rmod(p, d.E_cap)) = make_float4(e0.x, e0.y, e1.x, e1.y);
+      sink(r, p, make_float4(e0.x, e0.y, e1.x, e1.y));
     }
   }
+}
+
+__global__ void __launch_bounds__(256) k_kk_s1(RxDev d, InView in, long long b0, long long b1) {
+  __shared__ float2 tw[1024];
+  __shared__ float2 buf[FE_GROUPS][FFT_PAD_N];
+  const int g = threadIdx.x >> 6, j = threadIdx.x & 63;
+  tw_stage_async(tw, d.tw);   // waited for (tw_wait) before the first FFT pass
+  const long long b = b0 + (long long)blockIdx.x * FE_GROUPS + g;
+  float2 *const E = d.E;
+  const long long Ecap = d.E_cap;
+  kk_s1_block(d, in, b, b < b1, true, true, j, tw, buf[g], [=](int, long long p, float4 e) {
+    *reinterpret_cast<float4 *>(E + rmod(p, Ecap)) = e;
+  });
 }
 
 // ------------------------------------------------------------------ H16-H18
@@ -130,6 +145,29 @@ __global__ void __launch_bounds__(256) k_kk_s1(RxDev d, InView in, long long b0,
 // bulk copy per group into shared memory (the north_star's "TMA staging of overlapped blocks"),
 // completed on an mbarrier; the staging area then serves as the group's FFT scratch. Frames at
 // the stream start (p < 0) or across the ring's end are loaded by the threads instead.
+// Stage 2 of block b from its frame's even / odd samples in registers (ve[r] = E[p0 + 2n],
+// vo[r] = E[p0 + 2n + 1], n = j + 64 r, p0 = 512 b - 512): every thread of the CTA calls it.
+__device__ __forceinline__ void kk_s2_block(const RxDev &d, long long b, bool act, int j, const float2 *tw,
+                                            float2 *buf, float2 (&ve)[8], float2 (&vo)[8]) {
+  fft512_regs<false>(buf, j, tw, ve);
+  fft512_regs<false>(buf, j, tw, vo);
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int k = j + 64 * r;
+    const float2 od = cmul(vo[r], tw[k]);
+    ve[r] = r < 4 ? cmul(cadd(ve[r], od), __ldg(d.H + k)) : cmul(csub(ve[r], od), __ldg(d.H + k + 512));
+  }
+  fft512_regs<true>(buf, j, tw, ve);
+  // z_local[n] = 1/2 * IDFT512 = v / 1024; keep n in [128, 384) <=> r = 2..5
+  if (act) {
+#pragma unroll
+    for (int r = 2; r < 6; ++r) {
+      const long long q = 256 * b - 256 + j + 64 * r;
+      if (q >= 0) d.z[rmod(q, d.z_cap)] = cscale(ve[r], 1.0f / 1024.0f);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) k_kk_s2(RxDev d, long long b0, long long b1) {
   __shared__ __align__(16) float2 tw[1024];
   __shared__ __align__(128) float2 stage[FE_GROUPS][1024];   // E frames (TMA), then FFT scratch
@@ -170,22 +208,65 @@ __global__ void __launch_bounds__(256) k_kk_s2(RxDev d, long long b0, long long 
     for (int r = 0; r < 8; ++r) { ve[r] = make_float2(e[r].x, e[r].y); vo[r] = make_float2(e[r].z, e[r].w); }
   }
   tw_wait();                  // (also: every thread's frame is in registers before the FFT scratch use)
-  fft512_regs<false>(buf, j, tw, ve);
-  fft512_regs<false>(buf, j, tw, vo);
+  kk_s2_block(d, b, act, j, tw, buf, ve, vo);
+}
+
+// ------------------------------------------------------------------ H0, H11-H18 fused
+// k_kk_fe: both overlap-save stages in one kernel, the 4-sps field E never leaving the SM
+// (P:213 'to limit GPU memory access'; only the 2-sps field z touches HBM).
+// CTA c owns the stage-2 blocks [x_c, x_c + per_cta) of [x0, x1) and walks them in steps of
+// FE_GROUPS: iteration k computes stage 1 of the blocks y = x_c - 1 + 4k + g (one per group) into
+// a shared ring of KKFE_SLOTS x 512 E samples (slot y mod KKFE_SLOTS), then, after one CTA barrier,
+// stage 2 of the blocks x = x_c - 2 + 4k + g, whose frames [512x - 512, 512x + 512) are the
+// upper half of slot x - 1, slot x and the lower half of slot x + 1 (all written by now).
+// The CTA recomputes the stage-1 blocks x_c - 1 and x_c + per_cta at its edges (halos, not
+// counted); a stage-1 block is counted by the CTA whose stage-2 range holds it (the last CTA
+// also counts x1), and only if it is new in this call (y >= f0). The arithmetic of both stages
+// is kk_s1_block / kk_s2_block, so z is bit-identical to the k_kk_s1 -> E -> k_kk_s2 path.
+#define KKFE_SLOTS 6
+#define KKFE_SMEM (KKFE_SLOTS * 256 * 16)   // dynamic shared memory of k_kk_fe (static: 25.6 KB)
+__global__ void __launch_bounds__(256, 4) k_kk_fe(RxDev d, InView in, long long f0, long long x0, long long x1,
+                                                  int per_cta) {
+  __shared__ __align__(16) float2 tw[1024];
+  __shared__ __align__(16) float2 buf[FE_GROUPS][FFT_PAD_N];
+  extern __shared__ __align__(16) float4 ring_dyn[];          // [KKFE_SLOTS][256]: 512 E samples per slot
+  float4 (*const ring)[256] = reinterpret_cast<float4 (*)[256]>(ring_dyn);
+  const int g = threadIdx.x >> 6, j = threadIdx.x & 63;
+  const long long xc0 = x0 + (long long)blockIdx.x * per_cta;
+  if (xc0 >= x1) return;                                      // CTA-uniform
+  const long long xc1 = xc0 + per_cta < x1 ? xc0 + per_cta : x1;
+  const bool last = xc1 == x1;
+  tw_stage_async(tw, d.tw);
+  const int niter = (int)((xc1 - xc0 + 2 + FE_GROUPS - 1) / FE_GROUPS);
+  for (int k = 0; k < niter; ++k) {
+    // ---- stage 1 of y into slot y mod KKFE_SLOTS
+    const long long y = xc0 - 1 + (long long)FE_GROUPS * k + g;
+    const bool act1 = y >= 0 && y <= xc1;
+    const bool cnt = y >= f0 && ((y >= xc0 && y < xc1) || (last && y >= xc1));
+    float4 *const slot = ring[(int)(y % KKFE_SLOTS + KKFE_SLOTS) % KKFE_SLOTS];
+    kk_s1_block(d, in, y, act1, cnt, k == 0, j, tw, buf[g], [=](int r, long long, float4 e) {
+      slot[j + 64 * (r - 2)] = e;
+    });
+    __syncthreads();
+    // ---- stage 2 of x from slots x - 1, x, x + 1
+    const long long x = xc0 - 2 + (long long)FE_GROUPS * k + g;
+    const bool act2 = x >= xc0 && x < xc1;
+    float2 ve[8], vo[8];
+    {
+      const int sm = (int)((x - 1) % KKFE_SLOTS + KKFE_SLOTS) % KKFE_SLOTS;
+      const int s0 = sm + 1 == KKFE_SLOTS ? 0 : sm + 1, sp = s0 + 1 == KKFE_SLOTS ? 0 : s0 + 1;
+      const long long p0 = 512 * x - 512;
 #pragma unroll
-  for (int r = 0; r < 8; ++r) {
-    const int k = j + 64 * r;
-    const float2 od = cmul(vo[r], tw[k]);
-    ve[r] = r < 4 ? cmul(cadd(ve[r], od), __ldg(d.H + k)) : cmul(csub(ve[r], od), __ldg(d.H + k + 512));
-  }
-  fft512_regs<true>(buf, j, tw, ve);
-  // z_local[n] = 1/2 * IDFT512 = v / 1024; keep n in [128, 384) <=> r = 2..5
-  if (act) {
-#pragma unroll
-    for (int r = 2; r < 6; ++r) {
-      const long long q = 256 * b - 256 + j + 64 * r;
-      if (q >= 0) d.z[rmod(q, d.z_cap)] = cscale(ve[r], 1.0f / 1024.0f);
+      for (int r = 0; r < 8; ++r) {
+        // frame offset m = 2 (j + 64 r): slot x - 1 + (r + 2) / 4 at pair index j + 64 ((r + 2) % 4)
+        const int sl = r < 2 ? sm : (r < 6 ? s0 : sp);
+        float4 e = ring[sl][j + 64 * ((r + 2) & 3)];
+        if (!act2 || p0 + 2 * (j + 64 * r) < 0) e = make_float4(0.f, 0.f, 0.f, 0.f);   // E_p = 0 for p < 0
+        ve[r] = make_float2(e.x, e.y);
+        vo[r] = make_float2(e.z, e.w);
+      }
     }
+    kk_s2_block(d, x, act2, j, tw, buf[g], ve, vo);
   }
 }
 

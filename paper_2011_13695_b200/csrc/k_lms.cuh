@@ -464,10 +464,10 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
           const float4 ww = w4[k >> 1];                         // taps k, k+1 (broadcast)
           const float2 u0 = as_c(ub[-k]), u1 = as_c(ub[-k - 1]);
           float2 &A = a[(k >> 1) & 3];
-          A.x = fmaf(ww.x, u0.x, fmaf(ww.y, u0.y, A.x));
-          A.y = fmaf(ww.x, u0.y, fmaf(-ww.y, u0.x, A.y));
-          A.x = fmaf(ww.z, u1.x, fmaf(ww.w, u1.y, A.x));
-          A.y = fmaf(ww.z, u1.y, fmaf(-ww.w, u1.x, A.y));
+          // A += conj(w) u as two packed FFMA2 (inner products first, as the scalar form:
+          // A.x = fma(w.x, u.x, fma(w.y, u.y, A.x)), A.y = fma(w.x, u.y, fma(-w.y, u.x, A.y)))
+          A = __ffma2_rn(make_float2(ww.x, ww.x), u0, __ffma2_rn(make_float2(ww.y, -ww.y), make_float2(u0.y, u0.x), A));
+          A = __ffma2_rn(make_float2(ww.z, ww.z), u1, __ffma2_rn(make_float2(ww.w, -ww.w), make_float2(u1.y, u1.x), A));
         }
         if constexpr (WLIN) {   // + sum_k conj(v_k u_k): (vx ux - vy uy) - j (vx uy + vy ux)
           const float4 *v4 = reinterpret_cast<const float4 *>(sm.v);
@@ -539,28 +539,36 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
             const float2 rq = __ldg(d.bps_rot + q);                  // e^{-j phi_q} = (cos, -sin)
             const float cq = rq.x * inv2s, sq = -rq.y * inv2s, cst = 0.5f * (float)(L - 1);
             const float4 *y4 = reinterpret_cast<const float4 *>(sm.y) + 8 * hh;
-            float p0 = 0.f, p1 = 0.f, m0 = 0.f, m1 = 0.f;
+            // packed FP32x2 (FFMA2 / FADD2; the clamps stay scalar FMNMX): the pair (phase q,
+            // phase 31 - q) of one axis shares an instruction, roundings identical to the scalar
+            // form, 19 instead of 30 instructions per symbol and phase pair
+            const float2 cq2 = make_float2(cq, cq), cst2 = make_float2(cst, cst);
+            const float2 sqpm = make_float2(sq, -sq), sqmp = make_float2(-sq, sq);
+            const float2 mg = make_float2(12582912.f, 12582912.f), mgn = make_float2(-12582912.f, -12582912.f);
+            float2 pm0 = make_float2(0.f, 0.f), pm1 = make_float2(0.f, 0.f);   // (P, M) per symbol parity
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               const float4 yy = y4[i];
 #pragma unroll
               for (int hsym = 0; hsym < 2; ++hsym) {
                 const float yx = hsym ? yy.z : yy.x, yq = hsym ? yy.w : yy.y;
-                const float A = fmaf(yx, cq, cst), C = fmaf(yq, cq, cst);
-                const float uxp = fmaf(yq, sq, A), uxm = fmaf(-yq, sq, A);    // phase q / 31 - q
-                const float uyp = fmaf(-yx, sq, C), uym = fmaf(yx, sq, C);
-                const float exp_ = uxp - fminf(fmaxf(bps_rint(uxp), 0.f), Lm1);
-                const float eyp = uyp - fminf(fmaxf(bps_rint(uyp), 0.f), Lm1);
-                const float exm = uxm - fminf(fmaxf(bps_rint(uxm), 0.f), Lm1);
-                const float eym = uym - fminf(fmaxf(bps_rint(uym), 0.f), Lm1);
-                float &P = hsym ? p1 : p0, &Mm = hsym ? m1 : m0;
-                P = fmaf(exp_, exp_, P);
-                P = fmaf(eyp, eyp, P);
-                Mm = fmaf(exm, exm, Mm);
-                Mm = fmaf(eym, eym, Mm);
+                const float2 AC = __ffma2_rn(make_float2(yx, yq), cq2, cst2);               // (A, C)
+                // (sq, -sq) yq + A, (-sq, sq) yx + C: the symbol and A / C enter as broadcast operands
+                const float2 ux = __ffma2_rn(sqpm, make_float2(yq, yq), make_float2(AC.x, AC.x));   // phase q / 31 - q
+                const float2 uy = __ffma2_rn(sqmp, make_float2(yx, yx), make_float2(AC.y, AC.y));
+#if BPS_MAGIC
+                const float2 rx = __fadd2_rn(__fadd2_rn(ux, mg), mgn), ry = __fadd2_rn(__fadd2_rn(uy, mg), mgn);
+#else
+                const float2 rx = make_float2(rintf(ux.x), rintf(ux.y)), ry = make_float2(rintf(uy.x), rintf(uy.y));
+#endif
+                const float2 ex = __fadd2_rn(ux, make_float2(-fminf(fmaxf(rx.x, 0.f), Lm1), -fminf(fmaxf(rx.y, 0.f), Lm1)));
+                const float2 ey = __fadd2_rn(uy, make_float2(-fminf(fmaxf(ry.x, 0.f), Lm1), -fminf(fmaxf(ry.y, 0.f), Lm1)));
+                float2 &PM = hsym ? pm1 : pm0;
+                PM = __ffma2_rn(ex, ex, PM);
+                PM = __ffma2_rn(ey, ey, PM);
               }
             }
-            float dp = p0 + p1, dm = m0 + m1;
+            float dp = pm0.x + pm1.x, dm = pm0.y + pm1.y;
             dp += __shfl_xor_sync(0xffffffffu, dp, 16);
             dm += __shfl_xor_sync(0xffffffffu, dm, 16);
             dA = hh ? dm : dp;
@@ -657,10 +665,9 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
           const float4 ee = e4[i >> 1];                         // e_i, e_{i+1} (broadcast)
           const float2 u0 = as_c(ug[stride * i]), u1 = as_c(ug[stride * (i + 1)]);
           float2 &G = g[(i >> 1) & 1];
-          G.x = fmaf(u0.x, ee.x, fmaf(u0.y, ee.y, G.x));
-          G.y = fmaf(u0.y, ee.x, fmaf(-u0.x, ee.y, G.y));
-          G.x = fmaf(u1.x, ee.z, fmaf(u1.y, ee.w, G.x));
-          G.y = fmaf(u1.y, ee.z, fmaf(-u1.x, ee.w, G.y));
+          // G += u conj(e), packed (G.x = fma(u.x, e.x, fma(u.y, e.y, G.x)), G.y = fma(u.y, e.x, fma(-u.x, e.y, G.y)))
+          G = __ffma2_rn(u0, make_float2(ee.x, ee.x), __ffma2_rn(make_float2(u0.y, -u0.x), make_float2(ee.y, ee.y), G));
+          G = __ffma2_rn(u1, make_float2(ee.z, ee.z), __ffma2_rn(make_float2(u1.y, -u1.x), make_float2(ee.w, ee.w), G));
           if constexpr (WLIN) {
             float2 &H = hh[(i >> 1) & 1];
             H.x = fmaf(u0.x, ee.x, fmaf(-u0.y, ee.y, H.x));

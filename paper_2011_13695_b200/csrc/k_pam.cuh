@@ -43,6 +43,9 @@ __device__ __forceinline__ int load_block_regs(const InView &in, long long b, fl
       for (int r = 0; r < 8; ++r) {
         const long long p = p0 + 2 * (j + 64 * r);
         v[r] = make_float2(in_xf(in, p), in_xf(in, p + 1));
+        if (r >= 4 && p >= in.keep_from && p >= in.call_start)   // (the call's own samples)
+          reinterpret_cast<float2 *>(in.histf_w)[(p & (in.hist_cap - 1)) >> 1] =
+              make_float2(in.curf[p - in.call_start], in.curf[p + 1 - in.call_start]);
       }
     }
     return 0;
@@ -80,6 +83,9 @@ __device__ __forceinline__ int load_block_regs(const InView &in, long long b, fl
         const int c = in_code(in, p, pad);
         x[e] = pad ? 0.f : fmaf((float)c, scale, off);
         if (!pad && r >= 4) clip += (c == 0 || c == 4095);
+        // every owned sample of the call reaches the history ring, also when its block's frame
+        // starts in an earlier call (k_kk_fe recomputes stage-1 blocks up to 1536 samples back)
+        if (r >= 4 && p >= in.keep_from && p >= in.call_start) in.hist_w[p & (in.hist_cap - 1)] = (uint16_t)c;
       }
       v[r] = make_float2(x[0], x[1]);
     }

@@ -141,6 +141,7 @@ struct rx_handle {
   long long lms_launched_upto;   // segment estimate at the last equaliser launch
   long long lms_fin_est;         // host estimate of the finalised segment frontier (streaming)
   int n_sm;                      // SM count (persistent grids)
+  int fe_slots;                  // resident k_kk_fe CTAs per GPU (occupancy x SMs)
   long long max_call;            // samples per rx_process call: (history_buffers - 2) buffers
   // tracing
   int prof_mask;
@@ -239,6 +240,7 @@ extern "C" void rx_config_default(rx_config *c, int family, int order) {
   c->history_buffers = 3;
   c->lms_batch_segments = family == RX_PAM ? 4096 : 2048;   // D epochs (one round each)
   c->cuda_graphs = 1;
+  c->fused_front_end = 0;
 }
 
 extern "C" const char *rx_strerror(int s) {
@@ -298,6 +300,7 @@ static rx_status validate(const rx_config *c) {
   if (c->lms_mode < 0 || c->lms_mode > 2) return RX_EINVAL;
   if (c->equaliser_lag != 0 && c->equaliser_lag != 1) return RX_EINVAL;
   if (c->cuda_graphs != 0 && c->cuda_graphs != 1) return RX_EINVAL;
+  if (c->fused_front_end != 0 && c->fused_front_end != 1) return RX_EINVAL;
   if (c->shard_count < 0 || c->shard_count > 64) return RX_EINVAL;
   if (c->shard_count > 1) {        // time sharding (SURVEY §8(e) mode 2)
     // KK: stage B of buffer b one round after its stage A, epochs = buffers: N <= D.
@@ -569,7 +572,7 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
     d.z_cap = next_pow2((long long)(HB + lag_calls * (HB - 2)) * c.buffer_blocks * 256 + 2 * batch_sym);
     if (c.shard_count > 1)   // a shard's buffers b and b + N (plus halos) are held together
       d.z_cap = next_pow2((long long)(c.shard_count + 2) * c.buffer_blocks * 256 + 2 * RX_SHARD_POST);
-    TRY(dalloc(h, &d.E, d.E_cap));
+    if (!c.fused_front_end || c.shard_count > 1) TRY(dalloc(h, &d.E, d.E_cap));   // fused: E stays on chip
     TRY(dalloc(h, &d.z, d.z_cap));
     d.q_shift = 0;
     while ((1LL << d.q_shift) < (long long)c.buffer_blocks * 256) ++d.q_shift;
@@ -637,9 +640,18 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   if (cudaFuncSetAttribute(k_pam_theta<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)clk_smem) != cudaSuccess ||
       cudaFuncSetAttribute(k_pam_theta<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)clk_smem) != cudaSuccess ||
       cudaFuncSetAttribute(k_sync_corr<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536) != cudaSuccess ||
-      cudaFuncSetAttribute(k_sync_corr<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536) != cudaSuccess) {
+      cudaFuncSetAttribute(k_sync_corr<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536) != cudaSuccess ||
+      cudaFuncSetAttribute(k_kk_fe, cudaFuncAttributeMaxDynamicSharedMemorySize, KKFE_SMEM) != cudaSuccess) {
     rx_destroy(h);
     return RX_ECUDA;
+  }
+  {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_kk_fe, 256, KKFE_SMEM) != cudaSuccess || per_sm < 1) {
+      rx_destroy(h);
+      return RX_ECUDA;
+    }
+    h->fe_slots = per_sm * h->n_sm;
   }
   {
     int lo = 0, hi = 0;   // the equaliser's latency-bound warps get the SM slots first
@@ -694,6 +706,7 @@ static unsigned gridc(long long n, int per) { return (unsigned)((n + per - 1) / 
 // dependent access (KK stage 2, CFO periodogram and fine CFO; PAM clock and back-end; the
 // equaliser's post-processing chain).
 static bool g_no_pdl = getenv("RX_NO_PDL") != nullptr;
+static long long g_fe_per_cta = getenv("RX_FE_PER_CTA") ? atoll(getenv("RX_FE_PER_CTA")) : 0;   // k_kk_fe experiments
 template <typename... KArgs, typename... Args>
 static void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
   if (g_no_pdl) { k<<<grid, block, smem, s>>>(args...); return; }
@@ -957,7 +970,25 @@ static void run_kk(rx_handle *h, cudaStream_t s, const InView &in, unsigned char
   RxDev &d = h->d;
   if (flush) launch_zp_pending(h, s);
   const long long s1_target = h->n_in / 512;
-  if (s1_target > h->fe_done) {
+  if (h->cfg.fused_front_end && s1_target > h->fe_done) {
+    // one kernel for both stages over the stage-2 blocks [s2_done, s1_target - 1) (stage 1 of
+    // [fe_done, s1_target) counted). per_cta = 4 n - 2 stage-2 blocks per CTA (n iterations of
+    // FE_GROUPS stage-1 blocks, 2 of them halos), n from the smallest per-CTA share that keeps the
+    // grid within the resident CTA slots, or g_fe_per_cta (experiments)
+    const long long x0 = h->s2_done, x1 = s1_target - 1;
+    if (x1 > x0) {
+      const long long L = x1 - x0;
+      long long per = g_fe_per_cta;
+      if (per <= 0) {
+        const long long share = (L + h->fe_slots - 1) / h->fe_slots;
+        per = FE_GROUPS * ((share + 2 + FE_GROUPS - 1) / FE_GROUPS) - 2;
+      }
+      KLAUNCH(h, RX_K_KK_FE, s, (k_kk_fe<<<gridc(L, (int)per), 256, KKFE_SMEM, s>>>(d, in, h->fe_done, x0, x1, (int)per)));
+      h->s2_done = x1;
+      h->fe_done = s1_target;   // (else: nothing computed or counted yet)
+    }
+  }
+  if (!h->cfg.fused_front_end && s1_target > h->fe_done) {
     KLAUNCH(h, RX_K_KK_S1, s, (k_kk_s1<<<gridc(s1_target - h->fe_done, FE_GROUPS), 256, 0, s>>>(d, in, h->fe_done, s1_target)));
     h->fe_done = s1_target;
   }
@@ -1392,7 +1423,7 @@ extern "C" rx_status rx_probe_read(rx_handle *h, int which, long long first, lon
     case RX_PROBE_MB: if (kk) return RX_EINVAL; return ring_read(d.Mb, d.blk_cap, sizeof(long long), first, count, out);
     case RX_PROBE_U: if (kk) return RX_EINVAL; return ring_read(d.u, d.sym_cap, sizeof(float), first, count, out);
     case RX_PROBE_UHAT: if (kk) return RX_EINVAL; return ring_read(d.uhat, d.sym_cap, sizeof(float), first, count, out);
-    case RX_PROBE_E: if (!kk) return RX_EINVAL; return ring_read(d.E, d.E_cap, sizeof(float2), first, count, out);
+    case RX_PROBE_E: if (!kk || !d.E) return RX_EINVAL; return ring_read(d.E, d.E_cap, sizeof(float2), first, count, out);
     case RX_PROBE_Z: if (!kk) return RX_EINVAL; return ring_read(d.z, d.z_cap, sizeof(float2), first, count, out);
     case RX_PROBE_CFO: {
       if (!kk) return RX_EINVAL;

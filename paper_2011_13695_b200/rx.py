@@ -50,6 +50,7 @@ class RxConfig(ctypes.Structure):
         ("equaliser_lag", ctypes.c_int),
         ("shard_count", ctypes.c_int), ("shard_index", ctypes.c_int),
         ("cuda_graphs", ctypes.c_int),
+        ("fused_front_end", ctypes.c_int),
     ]
 
 
@@ -97,7 +98,7 @@ NCOUNTERS = 8
 COUNTERS = ("bit_errors", "bits", "symbols_counted", "evm_num", "evm_den", "clipped",
             "domain_errors", "symbols_out")
 KCLASSES = ("PAM_FE", "PAM_CLOCK", "PAM_BE", "NORM", "KK_S1", "KK_S2", "CFO", "SYNC", "LMS",
-            "LMS_POST", "MISC")
+            "LMS_POST", "MISC", "KK_FE")
 
 _lib = None
 

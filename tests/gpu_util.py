@@ -11,7 +11,8 @@ from oracle import rx_oracle as O
 RX_FIELDS = ("lms_taps", "lms_block", "lms_segment", "lms_overlap", "mu", "train_symbols",
              "sync_start", "sync_window", "warmup_symbols", "cpr_test_phases", "tap_lag_epochs",
              "sync_min_corr", "buffer_blocks", "clock_avg_half", "cfo_enable", "lms_batch_segments",
-             "input_format", "widely_linear", "q_window_symbols", "cpr_anchor", "lms_mode")
+             "input_format", "widely_linear", "q_window_symbols", "cpr_anchor", "lms_mode",
+             "fused_front_end")
 
 
 def oracle_params(rec, rx) -> O.RxParams:

@@ -223,6 +223,8 @@ def test_multi_buffer_parity(name, n, extra, batch, call_bufs):
     rx["buffer_blocks"] = 256
     if batch is not None:
         rx["lms_batch_segments"] = batch
+    if rec.fmt != "pam" and batch is None:
+        rx["fused_front_end"] = 0      # E is probed: the two-kernel front-end keeps it in HBM
     out = run_oracle(rec, rx)
     R, labels, st = run_gpu(rec, rx, chunk=256 * 512 * call_bufs,
                             history_buffers=(None if batch is None else call_bufs + 2))
@@ -300,6 +302,39 @@ def test_chunking_invariance():
     assert abs(sa["evm_num"] - sb["evm_num"]) <= 1e-9 * sa["evm_num"]
 
 
+@pytest.mark.parametrize("name,cspr,chunks", [
+    ("C3", 2.0, (256 * 512, 512 * 37, 512 * 3, 3 * 256 * 512)),   # domain errors at the low-CSPR end
+    ("C4", None, (2 * 256 * 512, 512 * 101)),
+])
+def test_fused_front_end_is_bit_identical(name, cspr, chunks):
+    """fused_front_end = 1 (k_kk_fe: both overlap-save stages in one kernel, E in shared memory,
+    halo stage-1 blocks recomputed per CTA) gives the z field of the two-kernel path (E through
+    an HBM ring) bit for bit, for any call chunking, and therefore identical labels and counters;
+    clipped / domain-error counts (each stage-1 block counted exactly once despite the halos) and
+    the first domain-error index equal too."""
+    _torch_cuda()
+    extra = {} if cspr is None else {"cspr_db": cspr}
+    rec, rx = make_config(name, n_samples=1 << 20, **extra)
+    rx["buffer_blocks"] = 256
+    nz = (rec.n // 512 - 2) * 256 - 128
+    R0, l0, s0 = run_gpu(rec, dict(rx, fused_front_end=0), chunk=256 * 512)
+    z0 = R0.probe("Z", 0, nz)
+    keys = ("bit_errors", "bits", "symbols_counted", "clipped", "domain_errors",
+            "first_domain_error_index", "sync_offset", "symbols_out")
+    if cspr is not None:
+        assert s0["domain_errors"] > 0
+    for chunk in chunks:
+        R1, l1, s1 = run_gpu(rec, dict(rx, fused_front_end=1), chunk=chunk)
+        z1 = R1.probe("Z", 0, nz)
+        assert np.array_equal(z0.view(np.uint64), z1.view(np.uint64)), (chunk, np.nonzero(z0 != z1)[0][:5])
+        assert np.array_equal(l0, l1), chunk
+        for k in keys:
+            assert s0[k] == s1[k], (chunk, k, s0[k], s1[k])
+        assert s0["evm_num"] == s1["evm_num"]
+        with pytest.raises(Exception):
+            R1.probe("E", 0, 16)        # not materialised
+
+
 @pytest.mark.parametrize("name", ["C3", "C2"])
 def test_large_history_calls_match_small_calls(name):
     """the per-buffer scalars (KK CFO parameters, from which z' is formed where the
@@ -331,7 +366,7 @@ def test_f32_input_matches_u16():
     rx["buffer_blocks"] = 256
     out = run_oracle(rec, rx)
     Ra, la, sa = run_gpu(rec, rx, chunk=256 * 512)
-    rxf = dict(rx, input_format=1)
+    rxf = dict(rx, input_format=1, fused_front_end=0)   # E is probed
     Rb, lb, sb = run_gpu(rec, rxf, chunk=256 * 512)
     m_end = out["m_end"]
     assert rel_l2(Rb.probe("E", 0, 4096), out["E"][:4096]) < TOL_FIELD
@@ -849,7 +884,8 @@ def test_randomised_scheduling_spec_criterion_10(name):
         R = Receiver(fam, rec.M, rec.static_taps, buffer_blocks=256, history_buffers=hb,
                      lms_batch_segments=int(rng.choice([0, 1, 7, 64, 300])),
                      serial_equaliser=int(rng.integers(0, 2)), equaliser_lag=int(rng.integers(0, 2)),
-                     cuda_graphs=int(rng.integers(0, 2)), **fields)
+                     cuda_graphs=int(rng.integers(0, 2)), **fields,
+                     **({"fused_front_end": int(rng.integers(0, 2))} if fam == RX_QAM_KK else {}))
         lab = torch.zeros(rec.n, dtype=torch.uint8, device="cuda")
         max_blocks = (hb - 2) * 256
         off = 0

@@ -29,6 +29,8 @@ def child(so, steps=10, chunk=None, lms_batch=0):
                  equaliser_lag=int(os.environ.get("LMS_LAG", "0")))
         if lms_batch:
             f["lms_batch_segments"] = lms_batch
+        if os.environ.get("RX_FUSED"):
+            f["fused_front_end"] = int(os.environ["RX_FUSED"])
         if os.environ.get("LMS_D"):
             f["tap_lag_epochs"] = int(os.environ["LMS_D"])
         f.update(kw)
@@ -38,7 +40,8 @@ def child(so, steps=10, chunk=None, lms_batch=0):
     st = res["stats"]
     R.close()
     iso = bench.isolated_classes(torch, make_kk, ring, rec.n, rx, True, dev, 72.2, 2)
-    out = {"so": os.path.basename(so), "lag": os.environ.get("LMS_LAG", "0"), "D": os.environ.get("LMS_D", "8"),
+    out = {"so": os.path.basename(so), "fused": os.environ.get("RX_FUSED", "1"),
+           "fe_per_cta": os.environ.get("RX_FE_PER_CTA", "auto"), "lag": os.environ.get("LMS_LAG", "0"), "D": os.environ.get("LMS_D", "8"),
            "batch": lms_batch, "value": round(rec.n * steps / (res["ms"] / 1e3) / 1e9, 3),
            "ms": round(res["ms"] / steps, 4), "live": res["breakdown"],
            "iso": {k: v["ms_per_step"] for k, v in iso.items()},
