@@ -28,22 +28,27 @@ __device__ __forceinline__ void kk_s1_block(const RxDev &d, const InView &in, lo
   if (act) {
     clip = load_block_regs(in, b, d.scale, j, v);       // x_p = 0 for p < 0 (c-0) -> I = dc
     const long long p0 = 512 * b - 512;
+    const float2 dc2 = make_float2(d.dc, d.dc);
+    const float2 hl = make_float2(0.5f * 0.693147182f, 0.5f * 0.693147182f);   // 1/2 ln 2 (exact halving)
+    unsigned fail = 0;                                  // I + dc <= 0 among the owned samples (r >= 4)
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
-      float hh[2];
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        float I = (e ? v[r].y : v[r].x) + d.dc;         // P:215 static DC offset
-        const long long p = p0 + 2 * (j + 64 * r) + e;
-        if (I <= 0.0f && r >= 4) {                      // owned samples counted once (A7)
-          ++dom;
-          if (p < first_dom) first_dom = p;
-        }
-        I = fmaxf(I, 1e-12f);
-        hh[e] = 0.5f * __logf(I);                       // P:215 logarithm for the phase (MUFU lg2)
-        if (r >= 2 && r < 6) amp[r - 2][e] = I * rsqrtf(I);   // P:215 square root: amplitude
+      float2 I = __fadd2_rn(v[r], dc2);                 // P:215 static DC offset
+      if (r >= 4) fail |= ((unsigned)(I.x <= 0.0f) | ((unsigned)(I.y <= 0.0f) << 1)) << (2 * (r - 4));
+      I = make_float2(fmaxf(I.x, 1e-12f), fmaxf(I.y, 1e-12f));
+      // P:215 logarithm for the phase: 1/2 ln I = log2(I) (ln 2 / 2) (MUFU lg2, one FMUL2)
+      const float2 hh = __fmul2_rn(make_float2(__log2f(I.x), __log2f(I.y)), hl);
+      if (r >= 2 && r < 6) {                            // P:215 square root: amplitude
+        const float2 a = __fmul2_rn(I, make_float2(rsqrtf(I.x), rsqrtf(I.y)));
+        amp[r - 2][0] = a.x;
+        amp[r - 2][1] = a.y;
       }
-      v[r] = make_float2(hh[0], hh[1]);
+      v[r] = hh;
+    }
+    if (fail) {                                         // owned samples counted once (A7)
+      dom = __popc(fail);
+      const int k = __ffs(fail) - 1;                    // the first in index order
+      first_dom = p0 + 2 * (j + 64 * (4 + (k >> 1))) + (k & 1);
     }
   } else {
 #pragma unroll
@@ -97,7 +102,7 @@ __device__ __forceinline__ void kk_s1_block(const RxDev &d, const InView &in, lo
     // (|error| ~ 1e-7 after the 3 steps)
     const long long pa = 512 * b - 512 + 2 * (j + 128);
     float2 rp = dds_rot_neg((unsigned long long)pa * d.carrier_inc);
-    const float2 st1 = dds_rot_neg(d.carrier_inc), st128 = dds_rot_neg(d.carrier_inc * 128ULL);
+    const float2 st1 = d.carrier_st1, st128 = d.carrier_st128;   // (rx_create)
 #pragma unroll
     for (int r = 2; r < 6; ++r) {
       const int n = j + 64 * r;
@@ -105,16 +110,16 @@ __device__ __forceinline__ void kk_s1_block(const RxDev &d, const InView &in, lo
       const float2 r0 = rp, r1 = cmul(rp, st1);
       rp = cmul(rp, st128);
       if (p < 0) continue;
-      // sigma phi in [-pi, pi] first, then the MUFU sin/cos (accurate there)
-      float ph0 = sg * v[r].x * (1.0f / 512.0f), ph1 = sg * v[r].y * (1.0f / 512.0f);
-      ph0 -= 6.283185307179586f * rintf(ph0 * 0.15915494309189535f);
-      ph1 -= 6.283185307179586f * rintf(ph1 * 0.15915494309189535f);
+      // sigma phi in [-pi, pi] first, then the MUFU sin/cos (accurate there); the pair of samples
+      // on the packed pipe (sigma / 512 and the 2 pi multiples exact, as in the scalar form)
+      float2 ph = __fmul2_rn(v[r], make_float2(sg * (1.0f / 512.0f), sg * (1.0f / 512.0f)));
+      const float2 k2 = __fmul2_rn(ph, make_float2(0.15915494309189535f, 0.15915494309189535f));
+      ph = __ffma2_rn(make_float2(rintf(k2.x), rintf(k2.y)), make_float2(-6.283185307179586f, -6.283185307179586f), ph);
       float s0, c0, s1, c1;
-      __sincosf(ph0, &s0, &c0);
-      __sincosf(ph1, &s1, &c1);
-      const float a0 = amp[r - 2][0], a1 = amp[r - 2][1];
-      const float2 e0 = cmul(make_float2(a0 * c0, a0 * s0), r0);
-      const float2 e1 = cmul(make_float2(a1 * c1, a1 * s1), r1);
+      __sincosf(ph.x, &s0, &c0);
+      __sincosf(ph.y, &s1, &c1);
+      const float2 e0 = cmul(__fmul2_rn(make_float2(c0, s0), make_float2(amp[r - 2][0], amp[r - 2][0])), r0);
+      const float2 e1 = cmul(__fmul2_rn(make_float2(c1, s1), make_float2(amp[r - 2][1], amp[r - 2][1])), r1);
       sink(r, p, make_float4(e0.x, e0.y, e1.x, e1.y));
     }
   }

@@ -56,7 +56,12 @@ __device__ __forceinline__ int load_block_regs(const InView &in, long long b, fl
 #pragma unroll
     for (int r = 0; r < 8; ++r) w[r] = __ldg(src + j + 64 * r);
 #pragma unroll
-    for (int r = 0; r < 8; ++r) v[r] = make_float2(fmaf(code_lo(w[r]), scale, off), fmaf(code_hi(w[r]), scale, off));
+    for (int r = 0; r < 8; ++r) {   // (code - 2047.5) scale as one FADD2 (exact codes) + one FFMA2
+      const float2 c = __fadd2_rn(make_float2(__uint_as_float((w[r] & 0xFFFFu) | 0x4B000000u),
+                                              __uint_as_float((w[r] >> 16) | 0x4B000000u)),
+                                  make_float2(-8388608.0f, -8388608.0f));
+      v[r] = __ffma2_rn(c, make_float2(scale, scale), make_float2(off, off));
+    }
     // clipped codes (0 or 4095) per 16-bit half: (c + 1) & 0xFFE is 0 exactly for those, and
     // adding 0x7FFF sets bit 15 of every other half (no carry between halves: halves < 0x1000)
 #pragma unroll

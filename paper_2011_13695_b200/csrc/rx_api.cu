@@ -379,6 +379,14 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   d.dc = (float)c.dc_offset;
   d.sideband = c.sideband;
   d.carrier_inc = (unsigned long long)llrint(ldexp((double)c.sideband * c.carrier_offset_hz / c.sample_rate, 64));
+  {   // the kernels' per-thread DDS step rotations (dds_rot_neg of the top 32 bits, here in fp64)
+    auto rot = [](unsigned long long u) {
+      const double x = (double)(int)(u >> 32) * ldexp(1.0, -31) * 3.141592653589793;
+      return make_float2((float)cos(x), (float)-sin(x));
+    };
+    d.carrier_st1 = rot(d.carrier_inc);
+    d.carrier_st128 = rot(d.carrier_inc * 128ULL);
+  }
   d.fs2 = c.sample_rate / 2.0;
   d.clock_half = c.clock_avg_half;
   d.buffer_blocks = c.buffer_blocks;

@@ -70,6 +70,7 @@ struct RxDev {
   float dc;                  // KK dc offset
   int sideband;
   unsigned long long carrier_inc;    // DDS increment of sigma * f_c (c-0)
+  float2 carrier_st1, carrier_st128; // e^{-j psi} of 1 and 128 increments (host, fp64 -> fp32)
   double fs2;                // KK 2-sps rate
   int clock_half;
   int buffer_blocks;
