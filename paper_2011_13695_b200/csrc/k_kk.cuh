@@ -616,12 +616,16 @@ __device__ __forceinline__ float2 zp_rotate(const RxDev &d, float2 v, long long 
 #define ZP_REANCHOR 32
 struct ZpStep {
   long long beta;
+  long long qlim;                  // the phasor steps hold for q < qlim (same buffer, < ZP_REANCHOR
+                                   // steps since the anchor, q < vend)
   float2 rot, step;                // includes 1 / sqrt(P_beta)
-  int age;
 };
-__device__ __forceinline__ float2 zp_step(const RxDev &d, float2 v, long long q, ZpStep &z) {
-  const long long beta = q >> d.q_shift;
-  if (beta != z.beta || z.age >= ZP_REANCHOR) {
+// z'_q of the staging lane's next sample q (q advances by 64 per call): one complex multiply and
+// one phasor step while q < qlim, else the exact-phase-word re-anchor (or 0 outside [0, vend))
+__device__ __forceinline__ float2 zp_step(const RxDev &d, float2 v, long long q, ZpStep &z, long long vend) {
+  if (!(q >= 0 && q < z.qlim)) {
+    if (q < 0 || q >= vend) return make_float2(0.f, 0.f);
+    const long long beta = q >> d.q_shift;
     const CfoParam &cp = d.cfo[rmod(beta, d.buf_cap)];
     const float s = cp.inv_sqrtP;
     if (d.cfo_enable) {
@@ -632,11 +636,12 @@ __device__ __forceinline__ float2 zp_step(const RxDev &d, float2 v, long long q,
       z.step = make_float2(1.f, 0.f);
     }
     z.beta = beta;
-    z.age = 0;
+    long long lim = (beta + 1) << d.q_shift;
+    if (q + 64LL * ZP_REANCHOR < lim) lim = q + 64LL * ZP_REANCHOR;
+    z.qlim = lim < vend ? lim : vend;
   }
   const float2 out = cmul(v, z.rot);
   z.rot = cmul(z.rot, z.step);
-  ++z.age;
   return out;
 }
 __device__ __forceinline__ float2 zp_rotate_or_zero(const RxDev &d, float2 v, long long q, long long vend, ZpCache &c) {

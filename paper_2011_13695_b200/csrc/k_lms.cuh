@@ -376,6 +376,15 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
     if (lane + 32 < d.Pt) rotB = __ldg(d.bps_rot + lane + 32);
   }
   float theta = 0.f;
+  // BPS over full 32-phase blocks: lane l scores the phase pair (q, 31 - q), q = l & 15; its
+  // rotation e^{-j phi_q} / 2s is loaded once per run, not per block
+  float bq_c = 0.f, bq_s = 0.f;
+  if (CPR == 2 && d.Pt == 32) {
+    const float2 rq = __ldg(d.bps_rot + (lane & 15));         // e^{-j phi_q} = (cos, -sin)
+    bq_c = rq.x * inv2s;
+    bq_s = -rq.y * inv2s;
+  }
+  float wmax = 0.f;   // max |w_k|^2 over the run's blocks (R-DIV: any tap beyond 1e3 at any block)
   // TILED (PAM, KP = 32): lane (q, r) = (lane >> 3, lane & 7) owns output / tap io = 4r + q and
   // computes a 4 x 8 register tile of each contraction from 128-bit shared loads, reduced over q
   // with two shuffle stages; otherwise lane i owns output i and tap i
@@ -404,7 +413,7 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
   ZpCache zc;                               // KK: CFO parameters of the buffer last staged
   zc.beta = -1;
   ZpStep zs[2];                             // KK: per-lane z' phasors of the two staged samples
-  zs[0].beta = zs[1].beta = -1;
+  zs[0].qlim = zs[1].qlim = -1;                 // (re-anchor at the first use)
   lms_stage_any<CPLX>(d, sm, wb0, wb0 + WLa, vend, wb0, vec, &zc);
   cp_async_commit();
 #pragma unroll 1
@@ -535,9 +544,8 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
             // shared products (3 instead of 4 rotation FMAs per evaluation), the two halves are
             // added by one shuffle, and lane l < 16 then holds phase l, lane l >= 16 phase 47 - l
             __syncwarp();
-            const int q = lane & 15, hh = lane >> 4;
-            const float2 rq = __ldg(d.bps_rot + q);                  // e^{-j phi_q} = (cos, -sin)
-            const float cq = rq.x * inv2s, sq = -rq.y * inv2s, cst = 0.5f * (float)(L - 1);
+            const int hh = lane >> 4;
+            const float cq = bq_c, sq = bq_s, cst = 0.5f * (float)(L - 1);
             const float4 *y4 = reinterpret_cast<const float4 *>(sm.y) + 8 * hh;
             // packed FP32x2 (FFMA2 / FADD2; the clamps stay scalar FMNMX): the pair (phase q,
             // phase 31 - q) of one axis shares an instruction, roundings identical to the scalar
@@ -648,7 +656,7 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
       const float g = lms_tile_reduce(acc, tq);
       if (io < K) {
         wk.x = fmaf(mu, g, wk.x);
-        if (fabsf(wk.x) > 1e3f) set_flag(d.st, RX_FLAG_DIVERGE);
+        wmax = fmaxf(wmax, wk.x * wk.x);          // (|w_k| > 1e3 <=> w_k^2 > 1e6; flagged after the loop)
       }
     } else {
       // lane = (group, tap kt): tap kt = lane % KP sums the block's symbols i in [i0, i0 + KP),
@@ -709,9 +717,9 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
       if (lane < K) {
         wk.x = fmaf(mu, gx, wk.x);
         if (CPLX) wk.y = fmaf(mu, gy, wk.y);
-        // divergence (reading R-DIV): any single tap beyond 1e3 flags at once,
-        // the full norm is checked at the end of the run
-        if (cabs2(wk) > 1e6f) set_flag(d.st, RX_FLAG_DIVERGE);
+        // divergence (reading R-DIV): any single tap beyond 1e3 at any block - tracked
+        // as the running max of |w_k|^2 (flagged after the loop), the full norm at the end
+        wmax = fmaxf(wmax, cabs2(wk));
       }
     }
     if (CPLX) reinterpret_cast<float2 *>(sm.w)[lane] = wk;
@@ -738,7 +746,7 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
     } else if (jn < nblk) {
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
-        const float2 v = (zq[u] >= 0 && zq[u] < vend) ? zp_step(d, zr[u], zq[u], zs[u]) : make_float2(0.f, 0.f);
+        const float2 v = zp_step(d, zr[u], zq[u], zs[u], vend);
         const int slot = (int)((zq[u] - wb0) & (LMS_RING - 1));
         sm.ring[slot] = v;
         sm.ring[slot + LMS_RING] = v;
@@ -752,6 +760,7 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
   evd += (double)evd_f;
   if (TILED) wk.x = reinterpret_cast<const float *>(sm.w)[lane];   // back to lane = tap order
   const float nrm = warp_sum(lane < K ? cabs2(wk) : 0.f);
+  if (__any_sync(0xffffffffu, wmax > 1e6f) && lane == 0) set_flag(d.st, RX_FLAG_DIVERGE);
   if (lane == 0 && nrm > 1e6f) set_flag(d.st, RX_FLAG_DIVERGE);
   return theta;
 }
