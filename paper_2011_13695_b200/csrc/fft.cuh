@@ -90,8 +90,22 @@ __device__ __forceinline__ void fft_sync() {
   else __syncthreads();
 }
 
+// The pass-3 twiddles W512^(r j), r = 1..7, of thread j are the same for every transform the thread
+// runs (conjugated for the inverse): kernels that run several FFT-512s per block load them once
+// (fft_t3_load) and pass them in registers, saving 7 shared loads (14 wavefronts per warp) per
+// transform - the FFT kernels are shared-memory-bandwidth bound (ncu: 0.66-0.81 wavefronts per
+// SM cycle).
+struct FftT3 { float2 w[7]; };
+__device__ __forceinline__ FftT3 fft_t3_load(const float2 *tw, int j) {
+  FftT3 t;
+#pragma unroll
+  for (int r = 1; r < 8; ++r) t.w[r - 1] = tw[TW_P3 + j + 64 * (r - 1)];
+  return t;
+}
+
 template <bool INV, int GB = 0>
-__device__ __forceinline__ void fft512_regs(float2 *buf, int j, const float2 *tw, float2 (&v)[8]) {
+__device__ __forceinline__ void fft512_regs(float2 *buf, int j, const float2 *tw, float2 (&v)[8],
+                                            const FftT3 *t3r = nullptr) {
   // pass-1 input already in registers: v[r] = z[j + 64 r]
   float2 *const pa = buf + j + (j >> 4);
   float2 *const pw1 = buf + 8 * j + (j >> 1);
@@ -120,7 +134,12 @@ __device__ __forceinline__ void fft512_regs(float2 *buf, int j, const float2 *tw
 #pragma unroll
   for (int r = 0; r < 8; ++r) v[r] = pa[68 * r];
 #pragma unroll
-  for (int r = 1; r < 8; ++r) v[r] = cmul(v[r], twv<INV>(t3, 64 * (r - 1)));
+  for (int r = 1; r < 8; ++r) {
+    float2 w;
+    if (t3r) w = INV ? cconj(t3r->w[r - 1]) : t3r->w[r - 1];
+    else w = twv<INV>(t3, 64 * (r - 1));
+    v[r] = cmul(v[r], w);
+  }
   dft8<INV>(v);
   // result: v[r] = X[j + 64 r]
 }

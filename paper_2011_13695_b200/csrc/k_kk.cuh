@@ -18,6 +18,9 @@
 // uncounted). wait_tw: the twiddle table's cp.async staging is waited for before the first FFT.
 // The reconstructed pairs (E_p, E_{p+1}), p = 512 b - 512 + 2 (j + 64 r), r = 2..5, p >= 0, go to
 // sink(r, p, pair).
+#ifndef KK_S1_T3
+#define KK_S1_T3 0          // measured: 48 -> 72 registers, KK_S1 0.395 -> 0.438 ms (not kept)
+#endif
 template <class Sink>
 __device__ __forceinline__ void kk_s1_block(const RxDev &d, const InView &in, long long b, bool act, bool count,
                                             bool wait_tw, int j, const float2 *tw, float2 *buf, Sink sink) {
@@ -66,7 +69,13 @@ __device__ __forceinline__ void kk_s1_block(const RxDev &d, const InView &in, lo
   if ((threadIdx.x & 31) == 0 && dom) atomicAdd((unsigned long long *)&d.st->domain_errors, (unsigned long long)dom);
   if (first_dom != 0x7fffffffffffffffLL) atomicMin(&d.st->first_domain, first_dom);
   if (wait_tw) tw_wait();
-  fft512_regs<false>(buf, j, tw, v);
+#if KK_S1_T3
+  const FftT3 t3 = fft_t3_load(tw, j);          // shared by the forward and inverse transforms
+  const FftT3 *t3p = &t3;
+#else
+  const FftT3 *t3p = nullptr;
+#endif
+  fft512_regs<false>(buf, j, tw, v, t3p);
   fft512_publish_upper(buf, j, v);
   // FD Hilbert (c-6, A8): Phi = -j sgn(kappa) H, Phi[0] = Phi[512] = 0
   float2 Zk[4], Zn[4];
@@ -93,7 +102,12 @@ __device__ __forceinline__ void kk_s1_block(const RxDev &d, const InView &in, lo
     if (j == 0) buf[256 + (256 >> 4)] = Z256;
   }
   __syncthreads();
-  fft512<true>(buf, j, tw, v);
+  {
+    const float2 *const pa = buf + j + (j >> 4);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = pa[68 * r];
+  }
+  fft512_regs<true>(buf, j, tw, v, t3p);
   // v[r] = 512 (phi[2n] + i phi[2n+1]), n = j + 64 r; kept local [256, 768) <=> r = 2..5
   if (act) {
     const float sg = (float)d.sideband;
@@ -152,17 +166,35 @@ __global__ void __launch_bounds__(256) k_kk_s1(RxDev d, InView in, long long b0,
 // the stream start (p < 0) or across the ring's end are loaded by the threads instead.
 // Stage 2 of block b from its frame's even / odd samples in registers (ve[r] = E[p0 + 2n],
 // vo[r] = E[p0 + 2n + 1], n = j + 64 r, p0 = 512 b - 512): every thread of the CTA calls it.
+// W16^r = e^{-2 pi i r / 16} (r < 8) as literals
+__device__ __forceinline__ float2 w16c(int r) {
+  switch (r) {
+    case 1: return make_float2(0.92387953251128674f, -0.38268343236508977f);
+    case 2: return make_float2(0.70710678118654752f, -0.70710678118654752f);
+    case 3: return make_float2(0.38268343236508977f, -0.92387953251128674f);
+    case 4: return make_float2(0.0f, -1.0f);
+    case 5: return make_float2(-0.38268343236508977f, -0.92387953251128674f);
+    case 6: return make_float2(-0.70710678118654752f, -0.70710678118654752f);
+    case 7: return make_float2(-0.92387953251128674f, -0.38268343236508977f);
+    default: return make_float2(1.0f, 0.0f);
+  }
+}
 __device__ __forceinline__ void kk_s2_block(const RxDev &d, long long b, bool act, int j, const float2 *tw,
                                             float2 *buf, float2 (&ve)[8], float2 (&vo)[8]) {
-  fft512_regs<false>(buf, j, tw, ve);
-  fft512_regs<false>(buf, j, tw, vo);
+  const FftT3 t3 = fft_t3_load(tw, j);        // shared by the three transforms
+  fft512_regs<false>(buf, j, tw, ve, &t3);
+  fft512_regs<false>(buf, j, tw, vo, &t3);
+  // radix-2 combination, W1024^k for k = j + 64 r: W1024^j W16^r (one shared load, the W16^r
+  // are constants; |error| ~ 1e-7)
+  const float2 w0 = tw[j];
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
     const int k = j + 64 * r;
-    const float2 od = cmul(vo[r], tw[k]);
+    const float2 wk = r == 0 ? w0 : cmul(w0, w16c(r));
+    const float2 od = cmul(vo[r], wk);
     ve[r] = r < 4 ? cmul(cadd(ve[r], od), __ldg(d.H + k)) : cmul(csub(ve[r], od), __ldg(d.H + k + 512));
   }
-  fft512_regs<true>(buf, j, tw, ve);
+  fft512_regs<true>(buf, j, tw, ve, &t3);
   // z_local[n] = 1/2 * IDFT512 = v / 1024; keep n in [128, 384) <=> r = 2..5
   if (act) {
 #pragma unroll
@@ -173,6 +205,9 @@ __device__ __forceinline__ void kk_s2_block(const RxDev &d, long long b, bool ac
   }
 }
 
+#ifndef KK_S2_TMA
+#define KK_S2_TMA 1
+#endif
 __global__ void __launch_bounds__(256) k_kk_s2(RxDev d, long long b0, long long b1) {
   __shared__ __align__(16) float2 tw[1024];
   __shared__ __align__(128) float2 stage[FE_GROUPS][1024];   // E frames (TMA), then FFT scratch
@@ -188,7 +223,7 @@ __global__ void __launch_bounds__(256) k_kk_s2(RxDev d, long long b0, long long 
   const bool act = b < b1;
   const long long p0 = 512 * b - 512;                         // frame [p0, p0 + 1024)
   const long long r0 = rmod(p0, d.E_cap);
-  const bool tma = act && p0 >= 0 && r0 + 1024 <= d.E_cap;    // group-uniform
+  const bool tma = KK_S2_TMA && act && p0 >= 0 && r0 + 1024 <= d.E_cap;    // group-uniform
   if (tma && j == 0) {
     mbar_expect_tx(&fbar[g], 1024 * sizeof(float2));
     bulk_g2s(stage[g], d.E + r0, 1024 * sizeof(float2), &fbar[g]);
@@ -411,6 +446,7 @@ __global__ void __launch_bounds__(CFO_SPEC_T, CFO_MINB) k_cfo_spec(RxDev d, long
   for (int i = 0; i < 16; ++i) acc[i] = 0.f;
   double pw = 0.0;
   const long long steps = (nch + (long long)NG * gridDim.x - 1) / ((long long)NG * gridDim.x);
+  FftT3 t3;
   for (long long it = 0; it < steps; ++it) {   // uniform trip count (the FFT barriers are CTA-wide)
     const long long c = (long long)NG * (blockIdx.x + (long long)gridDim.x * it) + g;
     const bool act = c < nch;
@@ -427,9 +463,12 @@ __global__ void __launch_bounds__(CFO_SPEC_T, CFO_MINB) k_cfo_spec(RxDev d, long
       vo[r] = cmul(b2, b2);
     }
     pw += (double)p0;
-    if (it == 0) tw_wait();                     // uniform over the CTA
-    fft512_regs<false, 0>(bufs[g], j, tw, ve);
-    fft512_regs<false, 0>(bufs[g], j, tw, vo);   // same buffer: fft512_regs syncs before its first store
+    if (it == 0) {                              // uniform over the CTA
+      tw_wait();
+      t3 = fft_t3_load(tw, j);
+    }
+    fft512_regs<false, 0>(bufs[g], j, tw, ve, &t3);
+    fft512_regs<false, 0>(bufs[g], j, tw, vo, &t3);   // same buffer: fft512_regs syncs before its first store
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       const float2 od = cmul(vo[r], tw[j + 64 * r]);
