@@ -430,17 +430,36 @@ __device__ __forceinline__ void cfo_final_block(const RxDev &d, long long beta, 
 // step, every CTA resident in one wave), accumulates |X[k]|^2 of its chunks per thread in
 // registers (chunk order), then sums the 4 groups in fixed order into row x. The power partial
 // sums the same samples (plus, in CTA 0, the tail beyond the last complete chunk).
+// CFO_STAGE: each group's next chunk (1024 z, 8 KiB, contiguous in the ring: chunks start at
+// multiples of 1024 from a buffer start) is fetched by one TMA bulk copy into dynamic shared memory
+// while the group transforms the current one (mbarrier completion, one phase per chunk)
+#ifndef CFO_STAGE
+#define CFO_STAGE 1
+#endif
+#define CFO_STAGE_SMEM (CFO_STAGE ? (CFO_SPEC_T / 64) * 1024 * 8 : 0)
 __global__ void __launch_bounds__(CFO_SPEC_T, CFO_MINB) k_cfo_spec(RxDev d, long long beta0, long long qfront) {
   __shared__ float2 tw[1024];
   __shared__ float2 bufs[CFO_SPEC_T / 64][FFT_PAD_N];   // FFT scratch; later acc[4][1024] floats
   __shared__ double red[CFO_SPEC_T / 32];
+  __shared__ __align__(8) uint64_t fbar[CFO_SPEC_T / 64];
+  extern __shared__ __align__(128) float4 cfo_stage_dyn[];  // [NG][512]: 1024 z per group
   const int g = threadIdx.x >> 6, j = threadIdx.x & 63;
   long long qlo, qhi;
   buf_range(d, beta0 + blockIdx.y, qfront, qlo, qhi);
   tw_stage_async(tw, d.tw);   // waited for before the first FFT (tw_wait, iteration 0)
+  constexpr int NG = CFO_SPEC_T / 64;
+  if (CFO_STAGE && threadIdx.x < NG) mbar_init(&fbar[threadIdx.x], 1);
+  if (CFO_STAGE) mbar_fence_init();
+  __syncthreads();
   pdl_wait();                 // z from k_kk_s2
   const long long nch = (qhi - qlo) / 1024;
-  constexpr int NG = CFO_SPEC_T / 64;
+  float4 *const stage = cfo_stage_dyn + 512 * g;
+  auto chunk_of = [&](long long it) { return (long long)NG * (blockIdx.x + (long long)gridDim.x * it) + g; };
+  auto fetch = [&](long long c) {   // one thread per group
+    mbar_expect_tx(&fbar[g], 1024 * sizeof(float2));
+    bulk_g2s(stage, d.z + rmod(qlo + 1024 * c, d.z_cap), 1024 * sizeof(float2), &fbar[g]);
+  };
+  if (CFO_STAGE && j == 0 && chunk_of(0) < nch) fetch(chunk_of(0));
   float acc[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) acc[i] = 0.f;
@@ -448,14 +467,16 @@ __global__ void __launch_bounds__(CFO_SPEC_T, CFO_MINB) k_cfo_spec(RxDev d, long
   const long long steps = (nch + (long long)NG * gridDim.x - 1) / ((long long)NG * gridDim.x);
   FftT3 t3;
   for (long long it = 0; it < steps; ++it) {   // uniform trip count (the FFT barriers are CTA-wide)
-    const long long c = (long long)NG * (blockIdx.x + (long long)gridDim.x * it) + g;
+    const long long c = chunk_of(it);
     const bool act = c < nch;
     float2 ve[8], vo[8];
     float p0 = 0.f;
+    if (CFO_STAGE && act) mbar_wait(&fbar[g], (unsigned)(it & 1));
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       float4 zz = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (act) zz = *reinterpret_cast<const float4 *>(d.z + rmod(qlo + 1024 * c + 2 * (j + 64 * r), d.z_cap));
+      if (act) zz = CFO_STAGE ? stage[j + 64 * r]
+                              : *reinterpret_cast<const float4 *>(d.z + rmod(qlo + 1024 * c + 2 * (j + 64 * r), d.z_cap));
       p0 += zz.x * zz.x + zz.y * zz.y + zz.z * zz.z + zz.w * zz.w;
       const float2 a = make_float2(zz.x, zz.y), bq = make_float2(zz.z, zz.w);
       const float2 a2 = cmul(a, a), b2 = cmul(bq, bq);
@@ -468,6 +489,12 @@ __global__ void __launch_bounds__(CFO_SPEC_T, CFO_MINB) k_cfo_spec(RxDev d, long
       t3 = fft_t3_load(tw, j);
     }
     fft512_regs<false, 0>(bufs[g], j, tw, ve, &t3);
+    // every thread of the CTA has passed the transform's barriers, so the group's staged chunk
+    // has been read: the next one goes into the same stage (async-proxy write after generic reads)
+    if (CFO_STAGE && j == 0 && chunk_of(it + 1) < nch) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      fetch(chunk_of(it + 1));
+    }
     fft512_regs<false, 0>(bufs[g], j, tw, vo, &t3);   // same buffer: fft512_regs syncs before its first store
 #pragma unroll
     for (int r = 0; r < 8; ++r) {

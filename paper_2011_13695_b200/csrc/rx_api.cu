@@ -649,7 +649,8 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
       cudaFuncSetAttribute(k_pam_theta<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)clk_smem) != cudaSuccess ||
       cudaFuncSetAttribute(k_sync_corr<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536) != cudaSuccess ||
       cudaFuncSetAttribute(k_sync_corr<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536) != cudaSuccess ||
-      cudaFuncSetAttribute(k_kk_fe, cudaFuncAttributeMaxDynamicSharedMemorySize, KKFE_SMEM) != cudaSuccess) {
+      cudaFuncSetAttribute(k_kk_fe, cudaFuncAttributeMaxDynamicSharedMemorySize, KKFE_SMEM) != cudaSuccess ||
+      cudaFuncSetAttribute(k_cfo_spec, cudaFuncAttributeMaxDynamicSharedMemorySize, CFO_STAGE_SMEM) != cudaSuccess) {
     rx_destroy(h);
     return RX_ECUDA;
   }
@@ -965,7 +966,7 @@ static void launch_zp_pending(rx_handle *h, cudaStream_t s) {
   const int fine_ctas = (int)((h->Q / 1024 + 7) / 8);
   for (const auto &j : h->zp_pending) {
     if (j.est) {   // plain launches: the producer (stage 2) is on the other stream (event order)
-      KLAUNCH(h, RX_K_CFO, s, (k_cfo_spec<<<dim3(CFO_ROWS, (unsigned)j.nb), CFO_SPEC_T, 0, s>>>(d, j.beta0, j.q_front)));
+      KLAUNCH(h, RX_K_CFO, s, (k_cfo_spec<<<dim3(CFO_ROWS, (unsigned)j.nb), CFO_SPEC_T, CFO_STAGE_SMEM, s>>>(d, j.beta0, j.q_front)));
       if (d.cfo_enable) KLAUNCH(h, RX_K_CFO, s, (k_cfo_fine<<<dim3((unsigned)fine_ctas, (unsigned)j.nb), 256, 0, s>>>(d, j.beta0, j.q_front, fine_ctas)));
     }
     KLAUNCH(h, RX_K_CFO, s, (k_cfo_carry<<<1, 1, 0, s>>>(d, j.beta0, (int)j.nb, j.q_front)));
@@ -1016,7 +1017,7 @@ static void run_kk(rx_handle *h, cudaStream_t s, const InView &in, unsigned char
       for (long long b0 = 0; b0 < nbuf; b0 += h->cfg.history_buffers) {
         const long long nb = nbuf - b0 < h->cfg.history_buffers ? nbuf - b0 : h->cfg.history_buffers;
         if (flush || h->cfg.serial_equaliser) {
-          KLAUNCH(h, RX_K_CFO, s, launch_pdl(k_cfo_spec, dim3(CFO_ROWS, (unsigned)nb), CFO_SPEC_T, 0, s, d, beta0 + b0, q_front));
+          KLAUNCH(h, RX_K_CFO, s, launch_pdl(k_cfo_spec, dim3(CFO_ROWS, (unsigned)nb), CFO_SPEC_T, CFO_STAGE_SMEM, s, d, beta0 + b0, q_front));
           if (d.cfo_enable) KLAUNCH(h, RX_K_CFO, s, launch_pdl(k_cfo_fine, dim3((unsigned)fine_ctas, (unsigned)nb), 256, 0, s, d, beta0 + b0, q_front, fine_ctas));
           KLAUNCH(h, RX_K_CFO, s, (k_cfo_carry<<<1, 1, 0, s>>>(d, beta0 + b0, (int)nb, q_front)));
         } else {
@@ -1169,7 +1170,7 @@ extern "C" rx_status rx_shard_process(rx_handle *h, long long beta, const void *
     KLAUNCH(h, RX_K_KK_S2, s, (k_kk_s2<<<gridc(s2_hi - s2_lo, FE_GROUPS), 256, 0, s>>>(d, s2_lo, s2_hi)));
     const long long q_front = 256 * s2_hi - 128;
     const int fine_ctas = (int)((h->Q / 1024 + 7) / 8);
-    KLAUNCH(h, RX_K_CFO, s, (k_cfo_spec<<<dim3(CFO_ROWS, 1), CFO_SPEC_T, 0, s>>>(d, beta, q_front)));
+    KLAUNCH(h, RX_K_CFO, s, (k_cfo_spec<<<dim3(CFO_ROWS, 1), CFO_SPEC_T, CFO_STAGE_SMEM, s>>>(d, beta, q_front)));
     if (d.cfo_enable) KLAUNCH(h, RX_K_CFO, s, (k_cfo_fine<<<dim3((unsigned)fine_ctas, 1), 256, 0, s>>>(d, beta, q_front, fine_ctas)));
     sb.qfront = q_front;
   } else {
