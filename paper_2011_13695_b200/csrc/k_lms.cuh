@@ -827,7 +827,7 @@ __device__ __forceinline__ void pam_finalise(const RxDev &d, long long lo, long 
         }
       }
     }
-    int ri = r0 + (int)(v % RX_PREF);
+    int ri = r0 + (int)v % RX_PREF;    // (v < 2^31: 32-bit modulo)
     if (ri >= RX_PREF) ri -= RX_PREF;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
@@ -1461,9 +1461,12 @@ __global__ void __launch_bounds__(256) k_lms_final(RxDev d, unsigned char *label
     long long a1 = a0 + 256;
     if (a1 > hi) a1 = hi;
     int c4[4] = {0, 0, 0, 0};
+    // reference index of a0 (one 64-bit modulo per CTA; the window is < RX_PREF symbols long)
+    const int ra0 = (int)(((st->sync_offset + a0 - d.m0) % RX_PREF + RX_PREF) % RX_PREF);
     for (long long m = a0 + threadIdx.x; m < a1; m += blockDim.x) {
       const int cur = d.level[rmod(m, d.sym_cap)];
-      const long long ri = ((st->sync_offset + m - d.m0) % RX_PREF + RX_PREF) % RX_PREF;
+      int ri = ra0 + (int)(m - a0);
+      if (ri >= RX_PREF) ri -= RX_PREF;
       const int ref = d.ref_idx[ri];
 #pragma unroll
       for (int r = 0; r < 4; ++r) c4[r] += (qam_rot(cur, r, d.L) == ref);
@@ -1543,7 +1546,7 @@ __global__ void __launch_bounds__(256) k_lms_final(RxDev d, unsigned char *label
         if (++li == lab_cap) li = 0;
       }
     }
-    int ri = r0 + (int)(v % RX_PREF);
+    int ri = r0 + (int)v % RX_PREF;    // (v < 2^31: 32-bit modulo)
     if (ri >= RX_PREF) ri -= RX_PREF;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {

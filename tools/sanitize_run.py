@@ -37,6 +37,10 @@ rec, rx = make_config("C4", n_samples=1 << 18)
 rx.update(buffer_blocks=128, train_symbols=4096, warmup_symbols=8192)
 _, _, st = run_gpu(rec, rx, chunk=512 * 128)
 print("KK BPS", st["bit_errors"], st["bits"], st["status_flags"])
+# round-2b: the fused KK front-end (k_kk_fe, E in shared memory) over ragged calls
+rx.update(fused_front_end=1)
+_, _, st = run_gpu(rec, rx, chunk=512 * 37)
+print("KK fused front-end", st["bit_errors"], st["bits"], st["status_flags"])
 for mode, extra in ((1, {}), (2, dict(lms_block=1, lms_taps=4, widely_linear=1))):
     rec, rx = make_config("C3", n_samples=1 << 18, linewidth_hz=1e3)
     rx.update(buffer_blocks=128, train_symbols=4096, warmup_symbols=8192, lms_mode=mode, **extra)
