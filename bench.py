@@ -813,7 +813,7 @@ def gpu_main(args):
     line["summary"] = {"kk_c4_gsa": line["value"], "pam_c2_gsa": line.get("pam", {}).get("value"),
                        "c5_gsa": line.get("c5", {}).get("value"), "e2e_c4_gsa": line.get("e2e", {}).get("value"),
                        "per_buffer_call_gsa": line.get("per_buffer_call", {}).get("value"),
-                       "lms_frac": (roof or {}).get("frac"), "chain_frac": (roof or {}).get("chain", {}).get("frac"),
+                       "dominant_class": (roof or {}).get("kernel_class"), "dominant_frac": (roof or {}).get("frac"), "chain_frac": (roof or {}).get("chain", {}).get("frac"),
                        "fp32_peak_tflops": round(peak, 2), "n_gpus": world}
     if rank == 0:
         print(json.dumps(line), flush=True)
