@@ -6,8 +6,10 @@
 #pragma once
 #include "common.cuh"
 
-#define FFT_PAD_N 544   // 512 float2 + one pad per 16: every FFT access pattern is
-                        // conflict-free (2 wavefronts per 64-bit warp access), see tools/banks
+#define FFT_PAD_N 576   // 512 float2 + padding: P8(i) = i + i/16 between passes 1 and 2 (and for
+                        // the real-FFT packing), Q(i) = i + 2 (i/16) between passes 2 and 3 (max 573):
+                        // every FFT access pattern is conflict-free (2 wavefronts per 64-bit warp
+                        // access; ncu measured the pass-2 stores at 4 with P8 there)
 
 __device__ __forceinline__ int P8(int i) { return i + (i >> 4); }
 
@@ -80,7 +82,7 @@ __device__ __forceinline__ void dft8(float2 (&v)[8]) {
 // Padded addresses are formed from one per-thread base plus compile-time offsets:
 //   P8(j + 64 r)   = (j + j/16) + 68 r
 //   P8(8 j + r)    = (8 j + j/2) + r                     (r < 8)
-//   P8(B + 8 r)    = (B + B/16) + 8 r + r/2,  B = 64 (j/8) + j%8
+//   Q(B + 8 r)     = (72 (j/8) + j%8) + 8 r + 2 (r/2), Q(j + 64 r) = (j + 2 (j/16)) + 72 r  (passes 2 -> 3)
 // Barrier of one transform: GB = 0 -> __syncthreads (default); GB = 1 -> only the 64 threads of
 // the group (named barrier 1 + group; measured 3-5% slower on k_pam_fe / k_pam_be than the CTA
 // barrier, kept for experiments; kernels then need a CTA barrier after staging shared tables).
@@ -109,8 +111,10 @@ __device__ __forceinline__ void fft512_regs(float2 *buf, int j, const float2 *tw
   // pass-1 input already in registers: v[r] = z[j + 64 r]
   float2 *const pa = buf + j + (j >> 4);
   float2 *const pw1 = buf + 8 * j + (j >> 1);
-  const int B = (j >> 3) * 64 + (j & 7);
-  float2 *const pw2 = buf + B + (B >> 4);
+  // pass-2 outputs go to Q(B + 8 r), Q(i) = i + 2 (i >> 4), B = 64 (j / 8) + j % 8:
+  //   Q(B + 8 r) = (72 (j / 8) + j % 8) + 8 r + 2 (r / 2);   pass 3 reads Q(j + 64 r) = (j + 2 (j / 16)) + 72 r
+  float2 *const pw2 = buf + 72 * (j >> 3) + (j & 7);
+  const float2 *const pq = buf + j + 2 * (j >> 4);
   dft8<INV>(v);
   fft_sync<GB>();
 #pragma unroll
@@ -126,13 +130,13 @@ __device__ __forceinline__ void fft512_regs(float2 *buf, int j, const float2 *tw
     dft8<INV>(v);
     fft_sync<GB>();
 #pragma unroll
-    for (int r = 0; r < 8; ++r) pw2[8 * r + (r >> 1)] = v[r];
+    for (int r = 0; r < 8; ++r) pw2[8 * r + 2 * (r >> 1)] = v[r];
     fft_sync<GB>();
   }
   // pass 3: Ns = 64, twiddle W512^(r j)
   const float2 *t3 = tw + TW_P3 + j;
 #pragma unroll
-  for (int r = 0; r < 8; ++r) v[r] = pa[68 * r];
+  for (int r = 0; r < 8; ++r) v[r] = pq[72 * r];
 #pragma unroll
   for (int r = 1; r < 8; ++r) {
     float2 w;
