@@ -667,11 +667,18 @@ __device__ float lms_run(const RxDev &d, LmsSmemT<CPLX> &sm, long long t_begin, 
       float2 g[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       float2 hh[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};   // WLIN: sum_i u_i[k] e_i
       if (CPLX) {
-        const float4 *e4 = reinterpret_cast<const float4 *>(sm.e) + (i0 >> 1);
+        // (KP < 32) the group takes the symbol pairs t = group + (32 / KP) m, m < KP / 2, instead of
+        // a contiguous run: the T/2-spaced window reads of one half-warp then cover distinct banks
+        // (contiguous runs put groups 8 symbols = 16 samples apart, a 2-way conflict in ncu)
+        constexpr int NGR = 32 / KP;
+        const int grp = lane / KP;
+        const T *ugc = win + KP - 1 - kt;
+        const float4 *e4 = reinterpret_cast<const float4 *>(sm.e);
 #pragma unroll
         for (int i = 0; i < KP; i += 2) {
-          const float4 ee = e4[i >> 1];                         // e_i, e_{i+1} (broadcast)
-          const float2 u0 = as_c(ug[stride * i]), u1 = as_c(ug[stride * (i + 1)]);
+          const int t = grp + NGR * (i >> 1);                   // symbols 2t, 2t + 1
+          const float4 ee = e4[t];                              // e_2t, e_2t+1 (group broadcast)
+          const float2 u0 = as_c(ugc[2 * stride * t]), u1 = as_c(ugc[2 * stride * t + stride]);
           float2 &G = g[(i >> 1) & 1];
           // G += u conj(e), packed (G.x = fma(u.x, e.x, fma(u.y, e.y, G.x)), G.y = fma(u.y, e.x, fma(-u.x, e.y, G.y)))
           G = __ffma2_rn(u0, make_float2(ee.x, ee.x), __ffma2_rn(make_float2(u0.y, -u0.x), make_float2(ee.y, ee.y), G));
