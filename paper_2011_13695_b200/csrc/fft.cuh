@@ -6,10 +6,13 @@
 #pragma once
 #include "common.cuh"
 
-#define FFT_PAD_N 576   // 512 float2 + padding: P8(i) = i + i/16 between passes 1 and 2 (and for
-                        // the real-FFT packing), Q(i) = i + 2 (i/16) between passes 2 and 3 (max 573):
-                        // every FFT access pattern is conflict-free (2 wavefronts per 64-bit warp
-                        // access; ncu measured the pass-2 stores at 4 with P8 there)
+#define FFT_PAD_N 576   // 512 float2 + padding. Three layouts, one per exchange: P8(i) = i + i/16
+                        // between passes 1 and 2 (stride-8 stores), Q(i) = i + 2 (i/16) between
+                        // passes 2 and 3 (max 573), and the natural (unpadded) layout for the
+                        // transforms' inputs / outputs and the real-FFT packing (contiguous runs,
+                        // ascending or mirrored): under the half-warp bank model every access is
+                        // conflict-free (tools/banks.py; ncu measured 4 wavefronts per pass-2
+                        // store and per mirror load with P8 there)
 
 __device__ __forceinline__ int P8(int i) { return i + (i >> 4); }
 
@@ -150,9 +153,9 @@ __device__ __forceinline__ void fft512_regs(float2 *buf, int j, const float2 *tw
 
 template <bool INV, int GB = 0>
 __device__ __forceinline__ void fft512(float2 *buf, int j, const float2 *tw, float2 (&v)[8]) {
-  const float2 *const pa = buf + j + (j >> 4);
+  const float2 *const pa = buf + j;            // natural (unpadded) layout, see FFT_PAD_N
 #pragma unroll
-  for (int r = 0; r < 8; ++r) v[r] = pa[68 * r];
+  for (int r = 0; r < 8; ++r) v[r] = pa[64 * r];
   fft512_regs<INV, GB>(buf, j, tw, v);
 }
 
@@ -160,23 +163,23 @@ __device__ __forceinline__ void fft512(float2 *buf, int j, const float2 *tw, flo
 // partner 512 - k is v[7 - r] of thread (64 - j) % 64, so only v[4..7] are published.
 template <int GB = 0>
 __device__ __forceinline__ void fft512_publish_upper(float2 *buf, int j, const float2 (&v)[8]) {
-  float2 *const pa = buf + j + (j >> 4);
+  float2 *const pa = buf + j;
   fft_sync<GB>();
 #pragma unroll
-  for (int q = 4; q < 8; ++q) pa[68 * q] = v[q];
+  for (int q = 4; q < 8; ++q) pa[64 * q] = v[q];
   fft_sync<GB>();
 }
 __device__ __forceinline__ float2 fft_partner(const float2 *pm, int j, int r, const float2 (&v)[8]) {
-  return (j == 0 && r == 0) ? v[0] : pm[-68 * r];
+  return (j == 0 && r == 0) ? v[0] : pm[-64 * r];
 }
 
 // Store the pass-3 result back (natural order) — only needed when other threads read it.
 template <int GB = 0>
 __device__ __forceinline__ void fft512_store(float2 *buf, int j, const float2 (&v)[8]) {
-  float2 *const pa = buf + j + (j >> 4);
+  float2 *const pa = buf + j;
   fft_sync<GB>();
 #pragma unroll
-  for (int r = 0; r < 8; ++r) pa[68 * r] = v[r];
+  for (int r = 0; r < 8; ++r) pa[64 * r] = v[r];
   fft_sync<GB>();
 }
 
@@ -184,11 +187,10 @@ __device__ __forceinline__ void fft512_store(float2 *buf, int j, const float2 (&
 // buf[P8(k)] = pa[68 r] and buf[P8(512 - k)] = pm[-68 r] with pm = P8(512 - j) (j >= 1);
 // j = 0, r = 0 pairs bin 0 with itself (index 0).
 __device__ __forceinline__ const float2 *fft_mirror_base(const float2 *buf, int j) {
-  const int q = 512 - j;
-  return buf + q + (q >> 4);
+  return buf + (512 - j);     // j = 0: buf + 512 (inside FFT_PAD_N; its r = 0 partner is v[0])
 }
 __device__ __forceinline__ float2 fft_mirror(const float2 *buf, const float2 *pm, int j, int r) {
-  return (j == 0 && r == 0) ? buf[0] : pm[-68 * r];
+  return (j == 0 && r == 0) ? buf[0] : pm[-64 * r];
 }
 
 // ---------------------------------------------------------------------------------------

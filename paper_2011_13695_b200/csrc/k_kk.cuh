@@ -92,20 +92,20 @@ __device__ __forceinline__ void kk_s1_block(const RxDev &d, const InView &in, lo
   const float2 Z256 = cconj(cmul_mi(cconj(v[4])));
   __syncthreads();
   {
-    float2 *paw = buf + j + (j >> 4);
-    float2 *pmw = buf + (512 - j) + ((512 - j) >> 4);
+    float2 *paw = buf + j;                      // natural layout
+    float2 *pmw = buf + (512 - j);
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-      paw[68 * r] = Zk[r];
-      if (!(j == 0 && r == 0)) pmw[-68 * r] = Zn[r];
+      paw[64 * r] = Zk[r];
+      if (!(j == 0 && r == 0)) pmw[-64 * r] = Zn[r];
     }
-    if (j == 0) buf[256 + (256 >> 4)] = Z256;
+    if (j == 0) buf[256] = Z256;
   }
   __syncthreads();
   {
-    const float2 *const pa = buf + j + (j >> 4);
+    const float2 *const pa = buf + j;
 #pragma unroll
-    for (int r = 0; r < 8; ++r) v[r] = pa[68 * r];
+    for (int r = 0; r < 8; ++r) v[r] = pa[64 * r];
   }
   fft512_regs<true>(buf, j, tw, v, t3p);
   // v[r] = 512 (phi[2n] + i phi[2n+1]), n = j + 64 r; kept local [256, 768) <=> r = 2..5
@@ -139,7 +139,7 @@ __device__ __forceinline__ void kk_s1_block(const RxDev &d, const InView &in, lo
   }
 }
 
-__global__ void __launch_bounds__(256) k_kk_s1(RxDev d, InView in, long long b0, long long b1) {
+__global__ void __launch_bounds__(256, 5) k_kk_s1(RxDev d, InView in, long long b0, long long b1) {   // 5 CTAs / SM: <= 51 registers
   __shared__ float2 tw[1024];
   __shared__ float2 buf[FE_GROUPS][FFT_PAD_N];
   const int g = threadIdx.x >> 6, j = threadIdx.x & 63;

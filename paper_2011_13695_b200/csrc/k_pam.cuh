@@ -469,14 +469,14 @@ __global__ void __launch_bounds__(256) k_pam_be(RxDev d, long long b0, long long
     Z256 = cconj(cmul(Y, r256));
   }
   {
-    float2 *paw = buf[g] + j + (j >> 4);
-    float2 *pmw = buf[g] + (512 - j) + ((512 - j) >> 4);
+    float2 *paw = buf[g] + j;                   // natural layout
+    float2 *pmw = buf[g] + (512 - j);
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-      paw[68 * r] = Zk[r];
-      if (!(j == 0 && r == 0)) pmw[-68 * r] = Zn[r];
+      paw[64 * r] = Zk[r];
+      if (!(j == 0 && r == 0)) pmw[-64 * r] = Zn[r];
     }
-    if (j == 0) buf[g][256 + (256 >> 4)] = Z256;
+    if (j == 0) buf[g][256] = Z256;
   }
   __syncthreads();
   float2 v[8];
@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(256) k_pam_be(RxDev d, long long b0, long long
       int loc = base2 + 2 * t;                                        // 2m + i_b - 512b + 512
       if (loc < 0 || loc >= 1024) { set_flag(d.st, 8); loc = loc < 0 ? 0 : 1023; }
       const int n = loc >> 1;
-      const float2 zz = buf[g][n + (n >> 4)];
+      const float2 zz = buf[g][n];                 // natural layout
       const float y = ((loc & 1) ? zz.y : zz.x) * (1.0f / 512.0f);
       d.u[rmod(m, d.sym_cap)] = y;
       ps += y;
