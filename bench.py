@@ -727,6 +727,8 @@ def gpu_main(args):
         f = dict(rx_fields(rx4), history_buffers=CALL_BUFFERS + 2, equaliser_lag=1)
         if args.lms_batch:
             f["lms_batch_segments"] = args.lms_batch
+        if args.fused_fe:
+            f["fused_front_end"] = 1
         f.update(kw)
         return Receiver(RX_QAM_KK, rec4.M, rec4.static_taps, device=dev.index, dc_offset=rec4.dc_offset, **f)
 
@@ -882,6 +884,8 @@ def main():
     ap.add_argument("--lms-batch", type=int, default=0,
                     help="segments per equaliser launch (rx_config.lms_batch_segments; 0 = library "
                          "default: D epochs, i.e. 4096 PAM / 2048 KK)")
+    ap.add_argument("--fused-fe", action="store_true",
+                    help="KK: rx_config.fused_front_end = 1 (k_kk_fe, E in shared memory; profiling / comparison)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
