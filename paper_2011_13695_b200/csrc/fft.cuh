@@ -200,9 +200,13 @@ __device__ __forceinline__ float2 fft_mirror(const float2 *buf, const float2 *pm
 //   X[512-k] = conj(Xe - W^k Xo)   (W = e^{-2 pi i/1024}).
 // Thread j of a group owns the bin pairs (k, 512-k) for k = j + 64 r, r = 0..3; thread 0
 // additionally owns k = 256 (X[256] = conj Z[256]); k = 0 pairs with 512.
+// HALF = false: the same pair without the two exact 1/2 scalings (outputs exactly 2x; callers fold
+// the power of two into a later scale - bit-identical results, two FMUL2 fewer per pair)
+template <bool HALF = true>
 __device__ __forceinline__ void r2c_pair(float2 Zk, float2 Zn, float2 w, float2 &Xk, float2 &Xn) {
-  float2 Xe = cscale(cadd(Zk, cconj(Zn)), 0.5f);
-  float2 Xo = cscale(cmul_mi(csub(Zk, cconj(Zn))), 0.5f);
+  float2 Xe = cadd(Zk, cconj(Zn));
+  float2 Xo = cmul_mi(csub(Zk, cconj(Zn)));
+  if (HALF) { Xe = cscale(Xe, 0.5f); Xo = cscale(Xo, 0.5f); }
   float2 t = cmul(w, Xo);
   Xk = cadd(Xe, t);
   Xn = cconj(csub(Xe, t));
@@ -212,9 +216,11 @@ __device__ __forceinline__ void r2c_pair(float2 Zk, float2 Zn, float2 w, float2 
 // satisfies y[2n] + i y[2n+1] = IFFT512(Z)[n] / 512 (unnormalised IFFT512 used).
 //   Xe = (Y[k] + conj Y[512-k])/2, Xo = (Y[k] - conj Y[512-k])/2 * conj(W^k)
 //   Z[k] = Xe + i Xo, Z[512-k] = conj(Xe) + i conj(Xo)
+template <bool HALF = true>
 __device__ __forceinline__ void c2r_pair(float2 Yk, float2 Yn, float2 w, float2 &Zk, float2 &Zn) {
-  float2 Xe = cscale(cadd(Yk, cconj(Yn)), 0.5f);
-  float2 Xo = cscale(cmulc(csub(Yk, cconj(Yn)), w), 0.5f);
+  float2 Xe = cadd(Yk, cconj(Yn));
+  float2 Xo = cmulc(csub(Yk, cconj(Yn)), w);
+  if (HALF) { Xe = cscale(Xe, 0.5f); Xo = cscale(Xo, 0.5f); }
   Zk = cadd(Xe, cmul_i(Xo));
   Zn = cadd(cconj(Xe), cmul_i(cconj(Xo)));
 }

@@ -84,12 +84,13 @@ __device__ __forceinline__ void kk_s1_block(const RxDev &d, const InView &in, lo
   for (int r = 0; r < 4; ++r) {
     const int k = j + 64 * r;
     float2 Xk, Xn;
-    r2c_pair(v[r], fft_partner(pm, j, r, v), tw[k], Xk, Xn);
+    // (both packings without their 1/2 scalings: Z is exactly 4x, folded into the phase scale below)
+    r2c_pair<false>(v[r], fft_partner(pm, j, r, v), tw[k], Xk, Xn);
     float2 Pk = cmul_mi(Xk), Pn = cmul_mi(Xn);
     if (k == 0) { Pk = make_float2(0.f, 0.f); Pn = make_float2(0.f, 0.f); }
-    c2r_pair(Pk, Pn, tw[k], Zk[r], Zn[r]);
+    c2r_pair<false>(Pk, Pn, tw[k], Zk[r], Zn[r]);
   }
-  const float2 Z256 = cconj(cmul_mi(cconj(v[4])));
+  const float2 Z256 = cscale(cconj(cmul_mi(cconj(v[4]))), 4.0f);
   __syncthreads();
   {
     float2 *paw = buf + j;                      // natural layout
@@ -108,7 +109,8 @@ __device__ __forceinline__ void kk_s1_block(const RxDev &d, const InView &in, lo
     for (int r = 0; r < 8; ++r) v[r] = pa[64 * r];
   }
   fft512_regs<true>(buf, j, tw, v, t3p);
-  // v[r] = 512 (phi[2n] + i phi[2n+1]), n = j + 64 r; kept local [256, 768) <=> r = 2..5
+  // v[r] = 2048 (phi[2n] + i phi[2n+1]) (512 of the unnormalised IFFT, 4 of the unscaled
+  // packings), n = j + 64 r; kept local [256, 768) <=> r = 2..5
   if (act) {
     const float sg = (float)d.sideband;
     // downshift to DC: e^{-j psi(p; sigma f_c)}, 64-bit DDS from the absolute index for
@@ -126,7 +128,7 @@ __device__ __forceinline__ void kk_s1_block(const RxDev &d, const InView &in, lo
       if (p < 0) continue;
       // sigma phi in [-pi, pi] first, then the MUFU sin/cos (accurate there); the pair of samples
       // on the packed pipe (sigma / 512 and the 2 pi multiples exact, as in the scalar form)
-      float2 ph = __fmul2_rn(v[r], make_float2(sg * (1.0f / 512.0f), sg * (1.0f / 512.0f)));
+      float2 ph = __fmul2_rn(v[r], make_float2(sg * (1.0f / 2048.0f), sg * (1.0f / 2048.0f)));
       const float2 k2 = __fmul2_rn(ph, make_float2(0.15915494309189535f, 0.15915494309189535f));
       ph = __ffma2_rn(make_float2(rintf(k2.x), rintf(k2.y)), make_float2(-6.283185307179586f, -6.283185307179586f), ph);
       float s0, c0, s1, c1;
