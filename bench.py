@@ -371,14 +371,14 @@ def e2e_run(torch, R, n_step, host_codes, steps, dev, packed=False, world=1, dis
     return dict(ms=float(t.item()), h2d=pinned_in.numel() * pinned_in.element_size(), d2h=nlab + 8 * 8)
 
 
-def isolated_classes(torch, make_rx, ring, n_step, rx, kk, dev, peak, steps=2):
+def isolated_classes(torch, make_rx, ring, n_step, rx, kk, dev, peak, steps=2, chunk=CHUNK):
     """Per-class kernel time with the equaliser stage serialised on the caller's stream
     (rx_config.serial_equaliser = 1: no overlap between kernel classes), CUDA events per launch:
     the kernel-quality view of the roofline next to the live (overlapped) one."""
     R = make_rx(serial_equaliser=1)
     st = torch.cuda.Stream(device=dev)
     lab = torch.zeros(1 << 24, dtype=torch.uint8, device=dev)
-    ch = Stream1(R, ring, n_step, lab, st)
+    ch = Stream1(R, ring, n_step, lab, st, chunk)
     for _ in range(3):
         ch.step()
     torch.cuda.synchronize(dev)
@@ -768,10 +768,11 @@ def gpu_main(args):
     R4.close()
     if n1 and not args.timed_only:
         # the paper's hand-off granularity: one 2^22 buffer per rx_process call
-        # (equaliser_lag = 1: a call's equaliser rounds overlap the next call's front-end, the
-        # paper's cross-buffer stream overlap; lag 0 = every call joins its own rounds)
+        # (equaliser_lag = L: a call's equaliser stage overlaps the next L calls' front-ends, the
+        # paper's cross-buffer stream overlap; a round runs every lms_batch_segments / 256 =
+        # 8 one-buffer calls, so L = 8 hides it; lag 0 = every call joins its own stage)
         pb = {}
-        for lag in (1, 0):
+        for lag in (8, 1, 0):
             R1 = make_kk(history_buffers=3, equaliser_lag=lag)
             ks = max(3, args.steps // 2)
             r1 = run_mode(torch, None, R1, ring4, n4, ks, 3, 1, dev, chunk=BUFFER, with_profile=False, monitor=True)
@@ -783,9 +784,9 @@ def gpu_main(args):
                        "rt_monitor": {"calls": rt.get("calls"), "realtime_ratio": round(rt.get("realtime_ratio", 0), 3),
                                       "max_call_ms": round(rt.get("max_call_ms", 0), 4),
                                       "max_load": round(rt.get("max_load", 0), 4), "overruns": rt.get("overruns")}}
-        line["per_buffer_call"] = dict(pb[1], unit="GSa/s", call_samples=BUFFER, equaliser_lag=1,
-                                       realtime_ratio=round(pb[1]["value"] / PAPER_REALTIME_GSA, 2),
-                                       equaliser_lag_0=pb[0])
+        line["per_buffer_call"] = dict(pb[8], unit="GSa/s", call_samples=BUFFER, equaliser_lag=8,
+                                       realtime_ratio=round(pb[8]["value"] / PAPER_REALTIME_GSA, 2),
+                                       equaliser_lag_1=pb[1], equaliser_lag_0=pb[0])
         # quadrant modes on one flushed record: anchored (default) and the c-9 stitch chain
         qa = record_quality(torch, make_kk, rec4, dev)
         qc = record_quality(torch, lambda **kw: make_kk(cpr_anchor=0, **kw), rec4, dev)

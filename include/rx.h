@@ -132,15 +132,18 @@ typedef struct {
                                  per widely_linear, with NO separate CPR - the taps track the
                                  carrier ("symbol-phase recovery" by the equaliser); one serial
                                  recursion per segment (DESIGN reading R-DDLMS; raw-tap seeds) */
-  int equaliser_lag;          /* side-stream equaliser (serial_equaliser = 0) only. 0 (default): the
-                                 work an rx_process call enqueues on cuda_stream ends with its own
-                                 equaliser stage; 1: with the PREVIOUS call's, so a call's equaliser
-                                 rounds overlap the next call's front-end (the paper overlaps buffers
-                                 across its five streams) - for small (one-buffer)
-                                 calls. Labels of a call may then be written after its stream work
-                                 completes: d_labels must stay valid until the next rx_process,
-                                 rx_flush, rx_get_stats or rx_export_counters call on the handle has
-                                 been ordered behind it (those calls wait for every forked stage) */
+  int equaliser_lag;          /* side-stream equaliser (serial_equaliser = 0) only, 0..16. 0 (default):
+                                 the work an rx_process call enqueues on cuda_stream ends with its own
+                                 equaliser stage; L >= 1: with the stage forked L calls EARLIER, so a
+                                 call's equaliser rounds overlap the next L calls' front-ends (the
+                                 paper overlaps buffers across its five streams) - for small
+                                 (one-buffer) calls, where a round runs only every
+                                 lms_batch_segments / (segments per call) calls, L of about that
+                                 ratio hides it. The rings grow by L calls. Labels of a call may then
+                                 be written after its stream work completes: d_labels must stay
+                                 valid until L more rx_process calls, or an rx_flush, rx_get_stats or
+                                 rx_export_counters call, have been ordered behind it (the latter
+                                 wait for every forked stage) */
   int shard_count;            /* time sharding of ONE stream (SURVEY §8(e) mode 2; KK chain): 0 or 1
                                  = off (rx_process); N > 1 = this handle is shard shard_index of N,
                                  fed with rx_shard_process (see below). Requires family KK,

@@ -25,6 +25,10 @@
 // RX_SIDE_PRIO_LOW (experiments): the equaliser side stream at the lowest instead of the highest
 // stream priority
 static int g_side_low = getenv("RX_SIDE_PRIO_LOW") ? 1 : 0;
+// KK CFO groups deferred on the side stream until this many buffers are pending (zp_due)
+#ifndef CFO_DEFER_BUFS
+#define CFO_DEFER_BUFS 4
+#endif
 
 // ------------------------------------------------------------------ small kernels
 __global__ void k_pam_mend(RxDev d, long long be_done) {
@@ -117,7 +121,7 @@ struct rx_handle {
   // onto `side`, concurrently with its own front-end / clock / back-end / normalisation, and
   // joins it back before the call's work on the caller's stream ends.
   cudaStream_t side;
-  cudaEvent_t ev_fork, ev_join[2];  // join of call k recorded in ev_join[k & 1]
+  cudaEvent_t ev_fork, ev_join[RX_MAX_LAG + 1];  // join of call k recorded in ev_join[k % (RX_MAX_LAG + 1)]
   long long ncall;                   // streaming rx_process calls so far
   long long lms_sym_ub;          // symbol upper bound of the data normalised by earlier calls
   uint16_t *unpacked;            // RX_IN_U12_PACKED: this call's codes unpacked to u16
@@ -142,6 +146,7 @@ struct rx_handle {
   long long lms_fin_est;         // host estimate of the finalised segment frontier (streaming)
   int n_sm;                      // SM count (persistent grids)
   int fe_slots;                  // resident k_kk_fe CTAs per GPU (occupancy x SMs)
+  long long cfo_maxbuf;          // buffers per CFO launch (scratch rows)
   long long max_call;            // samples per rx_process call: (history_buffers - 2) buffers
   // tracing
   int prof_mask;
@@ -298,7 +303,7 @@ static rx_status validate(const rx_config *c) {
   if (c->serial_equaliser != 0 && c->serial_equaliser != 1) return RX_EINVAL;
   if (c->cpr_anchor != 0 && c->cpr_anchor != 1) return RX_EINVAL;
   if (c->lms_mode < 0 || c->lms_mode > 2) return RX_EINVAL;
-  if (c->equaliser_lag != 0 && c->equaliser_lag != 1) return RX_EINVAL;
+  if (c->equaliser_lag < 0 || c->equaliser_lag > RX_MAX_LAG) return RX_EINVAL;
   if (c->cuda_graphs != 0 && c->cuda_graphs != 1) return RX_EINVAL;
   if (c->fused_front_end != 0 && c->fused_front_end != 1) return RX_EINVAL;
   if (c->shard_count < 0 || c->shard_count > 64) return RX_EINVAL;
@@ -344,7 +349,7 @@ extern "C" void rx_destroy(rx_handle *h) {
   if (h->hm_host) cudaFreeHost(h->hm_host);
   if (h->side) cudaStreamDestroy(h->side);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
-  for (int i = 0; i < 2; ++i) if (h->ev_join[i]) cudaEventDestroy(h->ev_join[i]);
+  for (int i = 0; i <= RX_MAX_LAG; ++i) if (h->ev_join[i]) cudaEventDestroy(h->ev_join[i]);
   for (auto &e : h->prof_pending) { cudaEventDestroy(e.second.first); cudaEventDestroy(e.second.second); }
   for (auto &e : h->prof_free) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   if (h->lms_graph) cudaGraphExecDestroy(h->lms_graph);
@@ -536,13 +541,13 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
   const long long batch_sym = bsym + (bsym > tail_sym ? tail_sym : bsym);
   // (HB + 1 buffers: the equaliser side stream reads the previous calls' symbols while the
   // current call writes up to one more call of them)
-  // (equaliser_lag = 1: the side stream may still read one more call of them)
+  // (equaliser_lag = L: the side stream may still read L more calls of them)
   const long long lag_calls = 1 + c.equaliser_lag;
   // per-buffer scalars (KK CFO parameters: z' is formed from them where the equaliser reads it;
   // PAM normalisation): every buffer the equaliser may still read - one batch + the seed-blocked
   // tail behind the front - plus the calls in flight on both streams
   {
-    const long long need = batch_sym / E_sym + 2LL * HB + 4;
+    const long long need = batch_sym / E_sym + 2LL * HB + 4 + (long long)c.equaliser_lag * (HB - 2) + CFO_DEFER_BUFS;
     d.buf_cap = next_pow2(need > 64 ? need : 64);
   }
   d.sym_cap = next_pow2((long long)(HB + lag_calls * (HB - 2)) * c.buffer_blocks * (kk ? 128 : 260) + batch_sym);
@@ -586,7 +591,8 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
     while ((1LL << d.q_shift) < (long long)c.buffer_blocks * 256) ++d.q_shift;
     TRY(dalloc(h, &d.cfo, d.buf_cap));
     d.cfo_G = CFO_ROWS + CFO_ROWS / CFO_GRP;             // spectrum rows per buffer (+ group rows)
-    const long long maxbuf = HB;                           // buffers completing in one call
+    const long long maxbuf = HB > 8 ? HB : 8;              // buffers per CFO launch (a call's, or deferred groups)
+    h->cfo_maxbuf = maxbuf;
     TRY(dalloc(h, &d.cfo_part, maxbuf * d.cfo_G * 1024));
     TRY(dalloc(h, &d.cfo_pow, maxbuf * d.cfo_G));
     TRY(dalloc(h, &d.cfo_tick, maxbuf));
@@ -667,8 +673,11 @@ extern "C" rx_status rx_create(const rx_config *cfg, int cuda_device, rx_handle 
     if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, g_side_low ? lo : hi) != cudaSuccess ||
         cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&h->ev_join[0], cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&h->ev_join[1], cudaEventDisableTiming) != cudaSuccess) {
+        [&] {
+          for (int i = 0; i <= RX_MAX_LAG; ++i)
+            if (cudaEventCreateWithFlags(&h->ev_join[i], cudaEventDisableTiming) != cudaSuccess) return true;
+          return false;
+        }()) {
       rx_destroy(h);
       return RX_ECUDA;
     }
@@ -964,14 +973,42 @@ static void run_pam(rx_handle *h, cudaStream_t s, const InView &in, unsigned cha
 static void launch_zp_pending(rx_handle *h, cudaStream_t s) {
   RxDev &d = h->d;
   const int fine_ctas = (int)((h->Q / 1024 + 7) / 8);
-  for (const auto &j : h->zp_pending) {
+  // contiguous deferred groups run as one launch set (up to cfo_maxbuf buffers): with one-buffer
+  // calls the estimate of several buffers then shares one wave instead of a latency-bound launch
+  // chain per buffer (results do not depend on the grouping: fixed spectrum rows per buffer, the
+  // DDS carry runs over the buffers in order)
+  size_t i = 0;
+  const size_t n = h->zp_pending.size();
+  while (i < n) {
+    rx_handle::ZpJob j = h->zp_pending[i];
+    size_t k = i + 1;
+    while (k < n && h->zp_pending[k].est == j.est && h->zp_pending[k].beta0 == j.beta0 + j.nb &&
+           j.nb + h->zp_pending[k].nb <= h->cfo_maxbuf) {
+      j.nb += h->zp_pending[k].nb;
+      j.q_front = h->zp_pending[k].q_front;
+      ++k;
+    }
     if (j.est) {   // plain launches: the producer (stage 2) is on the other stream (event order)
       KLAUNCH(h, RX_K_CFO, s, (k_cfo_spec<<<dim3(CFO_ROWS, (unsigned)j.nb), CFO_SPEC_T, CFO_STAGE_SMEM, s>>>(d, j.beta0, j.q_front)));
       if (d.cfo_enable) KLAUNCH(h, RX_K_CFO, s, (k_cfo_fine<<<dim3((unsigned)fine_ctas, (unsigned)j.nb), 256, 0, s>>>(d, j.beta0, j.q_front, fine_ctas)));
     }
     KLAUNCH(h, RX_K_CFO, s, (k_cfo_carry<<<1, 1, 0, s>>>(d, j.beta0, (int)j.nb, j.q_front)));
+    i = k;
   }
   h->zp_pending.clear();
+}
+
+// Deferred KK CFO groups wait (streaming, after training) until CFO_DEFER_BUFS buffers are pending
+// or an equaliser round is due - the only consumer of z' then (formed from the CFO parameters)
+static bool zp_due(const rx_handle *h) {
+  if (h->zp_pending.empty()) return false;
+  if (!h->hm_host->trained) return true;       // sync / training read z' of the first buffers
+  long long nb = 0;
+  for (const auto &j : h->zp_pending) nb += j.nb;
+  if (nb >= CFO_DEFER_BUFS) return true;
+  const long long batch = h->cfg.lms_batch_segments;
+  const long long seg_ub = h->lms_sym_ub / h->d.S + 1;
+  return batch <= 0 || seg_ub - h->lms_launched_upto >= batch;   // the test of launch_lms_rounds
 }
 
 static void run_kk(rx_handle *h, cudaStream_t s, const InView &in, unsigned char *labels,
@@ -1051,17 +1088,17 @@ static void fork_equaliser(rx_handle *h, cudaStream_t s, unsigned char *labels, 
   cudaEventRecord(h->ev_fork, s);
   cudaStreamWaitEvent(h->side, h->ev_fork, 0);
   if (d.family == RX_PAM) launch_norm_pam(h, h->side, 0);
-  else launch_zp_pending(h, h->side);
+  else if (zp_due(h)) launch_zp_pending(h, h->side);
   KLAUNCH(h, RX_K_MISC, h->side, (k_lms_snapshot<<<1, 1, 0, h->side>>>(d)));
   if (d.family == RX_PAM) launch_sync_train<false>(h, h->side, 0);
   else launch_sync_train<true>(h, h->side, 0);
   launch_lms_rounds(h, h->side, labels, lab_cap, 0, h->lms_sym_ub);
-  cudaEventRecord(h->ev_join[h->ncall & 1], h->side);
+  cudaEventRecord(h->ev_join[h->ncall % (RX_MAX_LAG + 1)], h->side);
 }
 
 // Make `s` wait for every equaliser stage forked so far (the calls that read or report results).
 static void join_side(rx_handle *h, cudaStream_t s) {
-  if (h->ncall > 0) cudaStreamWaitEvent(s, h->ev_join[(h->ncall - 1) & 1], 0);
+  if (h->ncall > 0) cudaStreamWaitEvent(s, h->ev_join[(h->ncall - 1) % (RX_MAX_LAG + 1)], 0);
 }
 
 static InView make_view(const rx_handle *h, const void *samples, long long n) {
@@ -1118,11 +1155,12 @@ extern "C" rx_status rx_process(rx_handle *h, const void *d_samples, long long n
     else launch_sync_train<true>(h, s, 0);
     launch_lms_rounds(h, s, lab, cap, 0, h->lms_sym_ub);
   } else {
-    // equaliser_lag = 0: the call ends when its own equaliser stage has; 1: when the previous
-    // call's has (this call's stage overlaps the next call's front-end, as the paper's buffers
-    // overlap across its five streams)
-    if (h->cfg.equaliser_lag == 0) CK(cudaStreamWaitEvent(s, h->ev_join[h->ncall & 1], 0));
-    else if (h->ncall > 0) CK(cudaStreamWaitEvent(s, h->ev_join[(h->ncall - 1) & 1], 0));
+    // equaliser_lag = L: the call ends when the equaliser stage forked L calls earlier has (L = 0:
+    // its own; L >= 1: this call's stage overlaps the next L calls' front-ends, as the paper's
+    // buffers overlap across its five streams, P:146 - with small calls a round, which runs once
+    // per lms_batch_segments, needs several calls of front-end to hide behind)
+    const long long L = h->cfg.equaliser_lag;
+    if (h->ncall >= L) CK(cudaStreamWaitEvent(s, h->ev_join[(h->ncall - L) % (RX_MAX_LAG + 1)], 0));
     h->ncall++;
   }
   if (rt_ev.first) {

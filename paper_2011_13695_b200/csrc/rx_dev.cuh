@@ -8,6 +8,7 @@
 #define RX_MAX_K 32
 #define RX_MAX_PT 64
 #define RX_MAX_O 512
+#define RX_MAX_LAG 16        // rx_config.equaliser_lag upper bound
 
 struct DevState {
   // ---- PAM clock recovery carries (unwrap needs the previous buffer's phase).

@@ -910,7 +910,7 @@ def test_randomised_scheduling_spec_criterion_10(name):
         hb = int(rng.integers(3, 7))
         R = Receiver(fam, rec.M, rec.static_taps, buffer_blocks=256, history_buffers=hb,
                      lms_batch_segments=int(rng.choice([0, 1, 7, 64, 300])),
-                     serial_equaliser=int(rng.integers(0, 2)), equaliser_lag=int(rng.integers(0, 2)),
+                     serial_equaliser=int(rng.integers(0, 2)), equaliser_lag=int(rng.choice([0, 1, 3, 8])),
                      cuda_graphs=int(rng.integers(0, 2)), **fields,
                      **({"fused_front_end": int(rng.integers(0, 2))} if fam == RX_QAM_KK else {}))
         lab = torch.zeros(rec.n, dtype=torch.uint8, device="cuda")

@@ -36,12 +36,13 @@ def child(so, steps=10, chunk=None, lms_batch=0):
         f.update(kw)
         return Receiver(RX_QAM_KK, rec.M, rec.static_taps, device=0, dc_offset=rec.dc_offset, **f)
     R = make_kk()
-    res = bench.run_mode(torch, None, R, ring, rec.n, steps, 3, 1, dev)
+    chunk = int(os.environ.get("KV_CHUNK", "0")) or bench.CHUNK     # samples per rx_process call
+    res = bench.run_mode(torch, None, R, ring, rec.n, steps, 3, 1, dev, chunk=chunk)
     st = res["stats"]
     R.close()
-    iso = bench.isolated_classes(torch, make_kk, ring, rec.n, rx, True, dev, 72.2, 2)
+    iso = bench.isolated_classes(torch, make_kk, ring, rec.n, rx, True, dev, 72.2, 2, chunk) if not os.environ.get("KV_NOISO") else {}
     out = {"so": os.path.basename(so), "fused": os.environ.get("RX_FUSED", "1"),
-           "fe_per_cta": os.environ.get("RX_FE_PER_CTA", "auto"), "lag": os.environ.get("LMS_LAG", "0"), "D": os.environ.get("LMS_D", "8"),
+           "fe_per_cta": os.environ.get("RX_FE_PER_CTA", "auto"), "chunk": chunk, "lag": os.environ.get("LMS_LAG", "0"), "D": os.environ.get("LMS_D", "8"),
            "batch": lms_batch, "value": round(rec.n * steps / (res["ms"] / 1e3) / 1e9, 3),
            "ms": round(res["ms"] / steps, 4), "live": res["breakdown"],
            "iso": {k: v["ms_per_step"] for k, v in iso.items()},
