@@ -1448,10 +1448,14 @@ __global__ void __launch_bounds__(1024) k_lms_prefix(RxDev d, int flush, int max
 // ------------------------------------------------------------------ H10/H23/H25 finalise
 // Final labels (rotated by j^{R_s}), reference comparison, per-segment error counts,
 // canonical absolute-frame taps w~_s = w e^{j theta} j^{-R_s} (c-9 'Seed').
-__global__ void __launch_bounds__(256) k_lms_final(RxDev d, unsigned char *labels, long long lab_cap,
+#ifndef LMS_FINAL_T
+#define LMS_FINAL_T 64      // threads per segment CTA of k_lms_final (measured: 256 -> 64, LMS_POST 0.116 -> 0.103 ms)
+#endif
+__global__ void __launch_bounds__(LMS_FINAL_T) k_lms_final(RxDev d, unsigned char *labels, long long lab_cap,
                                                    int nseg) {
   pdl_wait();                 // fin_lo / fin_hi from k_lms_prefix
-  __shared__ long long red[8];
+  constexpr int NW = LMS_FINAL_T / 32;
+  __shared__ long long red[NW];
   DevState *st = d.st;
   const long long s = st->fin_lo + blockIdx.x;
   if (blockIdx.x >= nseg || s >= st->fin_hi) return;
@@ -1497,16 +1501,18 @@ __global__ void __launch_bounds__(256) k_lms_final(RxDev d, unsigned char *label
   // per-segment lookup: level code -> code rotated by j^R (QAM) and its Gray label
   __shared__ unsigned char lut_code[256], lut_lab[256];
   {
-    const int c0 = threadIdx.x & 255;
-    int c = c0;
-    unsigned char lb;
-    if (d.family == 1) {
-      c = ((c & 15) < d.L && (c >> 4) < d.L) ? qam_rot(c, R, d.L) : c;
-      lb = (unsigned char)((gray(c & 15) << b) | gray(c >> 4));
-    } else {
-      lb = (unsigned char)gray(c);
+    for (int c0 = threadIdx.x; c0 < 256; c0 += LMS_FINAL_T) {
+      int c = c0;
+      unsigned char lb;
+      if (d.family == 1) {
+        c = ((c & 15) < d.L && (c >> 4) < d.L) ? qam_rot(c, R, d.L) : c;
+        lb = (unsigned char)((gray(c & 15) << b) | gray(c >> 4));
+      } else {
+        lb = (unsigned char)gray(c);
+      }
+      lut_code[c0] = (unsigned char)c;
+      lut_lab[c0] = lb;
     }
-    if (threadIdx.x < 256) { lut_code[c0] = (unsigned char)c; lut_lab[c0] = lb; }
   }
   __syncthreads();
   long long err = 0, cntd = 0;
@@ -1570,7 +1576,7 @@ __global__ void __launch_bounds__(256) k_lms_final(RxDev d, unsigned char *label
   __syncthreads();
   if (threadIdx.x == 0) {
     long long e2 = 0;
-    for (int w = 0; w < 8; ++w) e2 += red[w];
+    for (int w = 0; w < NW; ++w) e2 += red[w];
     d.seg_err[2 * si] = e2;
   }
   __syncthreads();
@@ -1578,7 +1584,7 @@ __global__ void __launch_bounds__(256) k_lms_final(RxDev d, unsigned char *label
   __syncthreads();
   if (threadIdx.x == 0) {
     long long c2 = 0;
-    for (int w = 0; w < 8; ++w) c2 += red[w];
+    for (int w = 0; w < NW; ++w) c2 += red[w];
     d.seg_err[2 * si + 1] = c2;
   }
   // canonical taps for the lag-D seeds (reading R-SEED): QAM taps are rotated so

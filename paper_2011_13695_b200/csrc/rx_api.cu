@@ -818,7 +818,7 @@ static void launch_lms_round(rx_handle *h, cudaStream_t s, unsigned char *labels
     // anchored quadrants (R-ANCHOR2): k_lms_final takes each R_s itself; the c-9 chain stitches first
     if (!d.anchor_each) KLAUNCH(h, RX_K_LMS_POST, s, (k_lms_stitch<<<(unsigned)nseg, 256, 0, s>>>(d, (int)nseg)));
     KLAUNCH(h, RX_K_LMS_POST, s, launch_pdl(k_lms_prefix, 1, 1024, 0, s, d, flush, (int)nseg));
-    KLAUNCH(h, RX_K_LMS_POST, s, launch_pdl(k_lms_final, (unsigned)nseg, 256, 0, s, d, labels, lab_cap, (int)nseg));
+    KLAUNCH(h, RX_K_LMS_POST, s, launch_pdl(k_lms_final, (unsigned)nseg, LMS_FINAL_T, 0, s, d, labels, lab_cap, (int)nseg));
     KLAUNCH(h, RX_K_LMS_POST, s, launch_pdl(k_lms_counters, 1, 1024, 0, s, d));
   }
   const unsigned nseed = (unsigned)(nseg * S / d.E_sym + 2);
