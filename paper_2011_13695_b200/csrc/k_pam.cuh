@@ -9,7 +9,9 @@
 #include "fft.cuh"
 #include "rx_dev.cuh"
 
+#ifndef FE_GROUPS
 #define FE_GROUPS 4
+#endif
 
 __device__ __forceinline__ float code_lo(uint32_t w) {     // exact float of the low 16 bits
   return __uint_as_float((w & 0xFFFFu) | 0x4B000000u) - 8388608.0f;
