@@ -210,7 +210,7 @@ __device__ __forceinline__ void kk_s2_block(const RxDev &d, long long b, bool ac
 #ifndef KK_S2_TMA
 #define KK_S2_TMA 1
 #endif
-__global__ void __launch_bounds__(256) k_kk_s2(RxDev d, long long b0, long long b1) {
+__global__ void __launch_bounds__(256, 4) k_kk_s2(RxDev d, long long b0, long long b1) {   // 4 CTAs / SM: <= 64 registers
   __shared__ __align__(16) float2 tw[1024];
   __shared__ __align__(128) float2 stage[FE_GROUPS][1024];   // E frames (TMA), then FFT scratch
   __shared__ __align__(8) uint64_t fbar[FE_GROUPS];

@@ -109,7 +109,7 @@ __device__ __forceinline__ void block_reduce_clip(DevState *st, int clip) {
 // HREAL: the static-EQ spectrum is real (zero-phase symmetric real taps, the PAM case) and is
 // applied as a real scale per bin.
 template <bool HREAL>
-__global__ void __launch_bounds__(256) k_pam_fe(RxDev d, InView in, long long b0, long long b1) {
+__global__ void __launch_bounds__(256, 6) k_pam_fe(RxDev d, InView in, long long b0, long long b1) {   // 6 CTAs / SM: <= 40 registers
   __shared__ float2 tw[1024];
   __shared__ float2 buf[FE_GROUPS][FFT_PAD_N];
   __shared__ double2 red[FE_GROUPS][2];
