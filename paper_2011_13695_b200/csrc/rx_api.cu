@@ -1461,6 +1461,9 @@ extern "C" rx_status rx_probe_read(rx_handle *h, int which, long long first, lon
   if (!h || !out) return RX_EINVAL;
   CK(cudaSetDevice(h->device));
   join_side(h, (cudaStream_t)stream);
+  // deferred KK CFO groups (zp_due) run now, in buffer order after every forked stage, so the
+  // CFO / z' probes see every completed buffer
+  if (!h->zp_pending.empty()) launch_zp_pending(h, (cudaStream_t)stream);
   CK(cudaStreamSynchronize((cudaStream_t)stream));
   RxDev &d = h->d;
   const bool kk = d.family == RX_QAM_KK;

@@ -16,7 +16,7 @@ import pytest
 
 from oracle import rx_oracle as O
 from rxsynth import make_config
-from tests.gpu_util import evm_db, near_threshold, rel_l2, run_gpu, run_oracle
+from tests.gpu_util import RX_FIELDS, evm_db, near_threshold, rel_l2, run_gpu, run_oracle
 
 pytestmark = pytest.mark.gpu
 
@@ -360,6 +360,31 @@ def test_fused_front_end_is_bit_identical(name, cspr, chunks):
         assert s0["evm_num"] == s1["evm_num"]
         with pytest.raises(Exception):
             R1.probe("E", 0, 16)        # not materialised
+
+
+def test_deferred_cfo_groups_are_complete_when_probed():
+    """One-buffer calls after training defer the KK CFO estimate of up to 4 buffers on the side
+    stream (zp_due): an rx_probe_read in between runs the deferred groups first, so every buffer
+    the front-end completed has its CFO parameters, equal to the oracle's."""
+    _torch_cuda()
+    import torch
+    from paper_2011_13695_b200 import RX_QAM_KK, Receiver
+    rec, rx = make_config("C3", n_samples=1 << 20)
+    rx["buffer_blocks"] = 256
+    out = run_oracle(rec, rx)
+    fields = {k: v for k, v in rx.items() if k in RX_FIELDS}
+    R = Receiver(RX_QAM_KK, rec.M, rec.static_taps, dc_offset=rec.dc_offset, history_buffers=3, **fields)
+    codes = torch.from_numpy(rec.codes.view(np.int16)).cuda()
+    lab = torch.zeros(rec.n, dtype=torch.uint8, device="cuda")
+    B = 256 * 512
+    nb_stream = rec.n // B - 2
+    for i in range(nb_stream):
+        R.process(codes[i * B:(i + 1) * B], lab)
+    done = nb_stream - 1                        # buffers whose 2-sps field the front-end completed
+    cfo = R.probe("CFO", 0, done)
+    assert np.allclose(cfo[:, 0], out["cfo"]["P"][:done], rtol=1e-4)
+    assert np.all(np.abs(cfo[:, 1] - out["cfo"]["df"][:done]) < 50.0), (cfo[:, 1], out["cfo"]["df"][:done])
+    R.close()
 
 
 @pytest.mark.parametrize("name", ["C3", "C2"])
