@@ -461,14 +461,14 @@ __global__ void __launch_bounds__(256) k_pam_be(RxDev d, long long b0, long long
     Yk = cmul(Yk, rot);
     if (k == 0) Yn = make_float2(Yn.x * nyq.x + Yn.y * nyq.y, 0.0f);   // Nyquist: Re(Y e^{-j pi f})
     else Yn = cmul(Yn, cmulc(nyq, rot));
-    c2r_pair(Yk, Yn, tw[k], Zk[r], Zn[r]);
+    c2r_pair<false>(Yk, Yn, tw[k], Zk[r], Zn[r]);   // without its exact 1/2 (x2 folded into 1/1024 below)
     rot = cmul(rot, step);
   }
   {
     float2 Y = HREAL ? cscale(X256, __ldg(d.Hr + 256)) : cmul(X256, __ldg(d.H + 256));
     float2 r256;
     sincospif(0.5f * f, &r256.y, &r256.x);
-    Z256 = cconj(cmul(Y, r256));
+    Z256 = cscale(cconj(cmul(Y, r256)), 2.0f);      // (the packing's x2)
   }
   {
     float2 *paw = buf[g] + j;                   // natural layout
@@ -498,7 +498,7 @@ __global__ void __launch_bounds__(256) k_pam_be(RxDev d, long long b0, long long
       if (loc < 0 || loc >= 1024) { set_flag(d.st, 8); loc = loc < 0 ? 0 : 1023; }
       const int n = loc >> 1;
       const float2 zz = buf[g][n];                 // natural layout
-      const float y = ((loc & 1) ? zz.y : zz.x) * (1.0f / 512.0f);
+      const float y = ((loc & 1) ? zz.y : zz.x) * (1.0f / 1024.0f);
       d.u[rmod(m, d.sym_cap)] = y;
       ps += y;
     }

@@ -16,12 +16,16 @@ def child():
     from tests.gpu_util import run_gpu
     rec, rx = make_config(os.environ.get("CMP_CFG", "C3"), n_samples=1 << 20)
     rx["buffer_blocks"] = 256
-    rx["fused_front_end"] = 0
-    R, lab, st = run_gpu(rec, rx, chunk=256 * 512)
-    nE = (rec.n // 512 - 1) * 512 - 256
-    E = R.probe("E", 0, nE)
-    z = R.probe("Z", 0, (rec.n // 512 - 2) * 256 - 128)
-    out = {k: hashlib.sha1(v.tobytes()).hexdigest()[:16] for k, v in (("E", E), ("z", z), ("labels", lab))}
+    if rec.fmt == "pam":
+        R, lab, st = run_gpu(rec, rx, chunk=256 * 512)
+        nu = st["symbols_out"]
+        arrs = (("U", R.probe("U", 0, nu)), ("UHAT", R.probe("UHAT", 0, nu)), ("labels", lab))
+    else:
+        rx["fused_front_end"] = 0
+        R, lab, st = run_gpu(rec, rx, chunk=256 * 512)
+        nE = (rec.n // 512 - 1) * 512 - 256
+        arrs = (("E", R.probe("E", 0, nE)), ("z", R.probe("Z", 0, (rec.n // 512 - 2) * 256 - 128)), ("labels", lab))
+    out = {k: hashlib.sha1(v.tobytes()).hexdigest()[:16] for k, v in arrs}
     out["bit_errors"] = st["bit_errors"]
     print("RESULT " + json.dumps(out))
 
