@@ -11,6 +11,16 @@
 #include "rx_dev.cuh"
 #include "k_pam.cuh"
 
+// Twiddle source per kernel: 1 = the 8 KiB table read from global memory (L1 / L2), 0 = staged into
+// shared memory by every CTA (cp.async). Measured (C4, isolated): k_kk_s1 0.387 -> 0.370 ms with the
+// global table (the staging loop was 5 % of its stall samples); k_kk_s2 unchanged and one spill
+#ifndef KK_S1_TW_GLOBAL
+#define KK_S1_TW_GLOBAL 1
+#endif
+#ifndef KK_S2_TW_GLOBAL
+#define KK_S2_TW_GLOBAL 0
+#endif
+
 // ------------------------------------------------------------------ H0, H11-H15
 // Stage 1 of block b by the 64-thread group j = 0..63 (every thread of the CTA calls it: the FFT
 // barriers are CTA-wide). act = 0: the group idles through the barriers; count: the block's owned
@@ -142,14 +152,19 @@ __device__ __forceinline__ void kk_s1_block(const RxDev &d, const InView &in, lo
 }
 
 __global__ void __launch_bounds__(256, 5) k_kk_s1(RxDev d, InView in, long long b0, long long b1) {   // 5 CTAs / SM: <= 51 registers
-  __shared__ float2 tw[1024];
   __shared__ float2 buf[FE_GROUPS][FFT_PAD_N];
   const int g = threadIdx.x >> 6, j = threadIdx.x & 63;
-  tw_stage_async(tw, d.tw);   // waited for (tw_wait) before the first FFT pass
+#if KK_S1_TW_GLOBAL
+  const float2 *const tw = d.tw;   // the 8 KiB table from L1 / L2 (no per-CTA staging)
+#else
+  __shared__ float2 tws[1024];
+  const float2 *const tw = tws;
+  tw_stage_async(tws, d.tw);  // waited for (tw_wait) before the first FFT pass
+#endif
   const long long b = b0 + (long long)blockIdx.x * FE_GROUPS + g;
   float2 *const E = d.E;
   const long long Ecap = d.E_cap;
-  kk_s1_block(d, in, b, b < b1, true, true, j, tw, buf[g], [=](int, long long p, float4 e) {
+  kk_s1_block(d, in, b, b < b1, true, !KK_S1_TW_GLOBAL, j, tw, buf[g], [=](int, long long p, float4 e) {
     *reinterpret_cast<float4 *>(E + rmod(p, Ecap)) = e;
   });
 }
@@ -211,14 +226,21 @@ __device__ __forceinline__ void kk_s2_block(const RxDev &d, long long b, bool ac
 #define KK_S2_TMA 1
 #endif
 __global__ void __launch_bounds__(256, 4) k_kk_s2(RxDev d, long long b0, long long b1) {   // 4 CTAs / SM: <= 64 registers
-  __shared__ __align__(16) float2 tw[1024];
+#if KK_S2_TW_GLOBAL
+  const float2 *const tw = d.tw;   // the 8 KiB table from L1 / L2 (no per-CTA staging)
+#else
+  __shared__ __align__(16) float2 tws[1024];
+  const float2 *const tw = tws;
+#endif
   __shared__ __align__(128) float2 stage[FE_GROUPS][1024];   // E frames (TMA), then FFT scratch
   __shared__ __align__(8) uint64_t fbar[FE_GROUPS];
   const int g = threadIdx.x >> 6, j = threadIdx.x & 63;
   float2 *const buf = stage[g];                               // FFT_PAD_N <= 1024
   if (threadIdx.x < FE_GROUPS) mbar_init(&fbar[threadIdx.x], 1);
   mbar_fence_init();
-  tw_stage_async(tw, d.tw);   // waited for (tw_wait) before the first FFT pass
+#if !KK_S2_TW_GLOBAL
+  tw_stage_async(tws, d.tw);  // waited for (tw_wait) before the first FFT pass
+#endif
   __syncthreads();            // barrier inits visible to every thread
   pdl_wait();                 // E from k_kk_s1
   const long long b = b0 + (long long)blockIdx.x * FE_GROUPS + g;
@@ -249,7 +271,11 @@ __global__ void __launch_bounds__(256, 4) k_kk_s2(RxDev d, long long b0, long lo
 #pragma unroll
     for (int r = 0; r < 8; ++r) { ve[r] = make_float2(e[r].x, e[r].y); vo[r] = make_float2(e[r].z, e[r].w); }
   }
+#if KK_S2_TW_GLOBAL
+  __syncthreads();            // every thread's frame is in registers before the FFT scratch use
+#else
   tw_wait();                  // (also: every thread's frame is in registers before the FFT scratch use)
+#endif
   kk_s2_block(d, b, act, j, tw, buf, ve, vo);
 }
 
