@@ -13,12 +13,16 @@
 
 // Twiddle source per kernel: 1 = the 8 KiB table read from global memory (L1 / L2), 0 = staged into
 // shared memory by every CTA (cp.async). Measured (C4, isolated): k_kk_s1 0.387 -> 0.370 ms with the
-// global table (the staging loop was 5 % of its stall samples); k_kk_s2 unchanged and one spill
+// global table (the staging loop was 5 % of its stall samples); k_kk_s2 0.402 -> 0.395 ms with the
+// global table and without the register copy of the pass-3 twiddles (KK_S2_T3 = 0: no spill)
 #ifndef KK_S1_TW_GLOBAL
 #define KK_S1_TW_GLOBAL 1
 #endif
+#ifndef KK_S2_T3
+#define KK_S2_T3 0          // 1: k_kk_s2 loads the pass-3 twiddles once per block for its three transforms
+#endif
 #ifndef KK_S2_TW_GLOBAL
-#define KK_S2_TW_GLOBAL 0
+#define KK_S2_TW_GLOBAL 1
 #endif
 
 // ------------------------------------------------------------------ H0, H11-H15
@@ -198,9 +202,14 @@ __device__ __forceinline__ float2 w16c(int r) {
 }
 __device__ __forceinline__ void kk_s2_block(const RxDev &d, long long b, bool act, int j, const float2 *tw,
                                             float2 *buf, float2 (&ve)[8], float2 (&vo)[8]) {
+#if KK_S2_T3
   const FftT3 t3 = fft_t3_load(tw, j);        // shared by the three transforms
-  fft512_regs<false>(buf, j, tw, ve, &t3);
-  fft512_regs<false>(buf, j, tw, vo, &t3);
+  const FftT3 *const t3p = &t3;
+#else
+  const FftT3 *const t3p = nullptr;
+#endif
+  fft512_regs<false>(buf, j, tw, ve, t3p);
+  fft512_regs<false>(buf, j, tw, vo, t3p);
   // radix-2 combination, W1024^k for k = j + 64 r: W1024^j W16^r (one shared load, the W16^r
   // are constants; |error| ~ 1e-7)
   const float2 w0 = tw[j];
@@ -211,7 +220,7 @@ __device__ __forceinline__ void kk_s2_block(const RxDev &d, long long b, bool ac
     const float2 od = cmul(vo[r], wk);
     ve[r] = r < 4 ? cmul(cadd(ve[r], od), __ldg(d.H + k)) : cmul(csub(ve[r], od), __ldg(d.H + k + 512));
   }
-  fft512_regs<true>(buf, j, tw, ve, &t3);
+  fft512_regs<true>(buf, j, tw, ve, t3p);
   // z_local[n] = 1/2 * IDFT512 = v / 1024; keep n in [128, 384) <=> r = 2..5
   if (act) {
 #pragma unroll
