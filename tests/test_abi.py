@@ -126,7 +126,7 @@ def test_new_config_fields_validated_before_touching_the_gpu(lib):
 
 
 def test_round2_config_fields_validated_before_touching_the_gpu(lib):
-    """lms_mode (0/1), equaliser_lag (0/1) and time sharding (KK only, anchored quadrants,
+    """lms_mode (0/1), equaliser_lag (0..16) and time sharding (KK only, anchored quadrants,
     shard_count <= tap_lag_epochs, 0 <= shard_index < shard_count) are checked by rx_create
     before any CUDA call; the shard calls reject a NULL handle."""
     from paper_2011_13695_b200 import rx
@@ -141,7 +141,8 @@ def test_round2_config_fields_validated_before_touching_the_gpu(lib):
         for k, v in kw.items():
             setattr(c, k, v)
         return c
-    for kw in (dict(lms_mode=3), dict(equaliser_lag=2), dict(cuda_graphs=2), dict(shard_count=9),   # 9 > D = 8
+    for kw in (dict(lms_mode=3), dict(equaliser_lag=17), dict(equaliser_lag=-1), dict(cuda_graphs=2),
+               dict(fused_front_end=2), dict(shard_count=9),   # 9 > D = 8
                dict(shard_count=4, shard_index=4), dict(shard_count=4, shard_index=-1),
                dict(shard_count=4, cpr_anchor=0), dict(shard_count=-1)):
         assert lib.rx_create(ctypes.byref(kk(**kw)), 0, ctypes.byref(h)) == -1, kw
